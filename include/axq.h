@@ -1,0 +1,170 @@
+/*
+ * axq.h -- C ABI of the B200-native approximate-multiplier LUT layer (AdaPT,
+ * arXiv 2203.04071).  Every multiply of a quantized convolution / linear layer is
+ * replaced by a lookup into an approximate multiplier's 2^b x 2^b product table.
+ *
+ * Citations: "P:n" = PAPER.md line n; "S:n" = SPEC.md line n;
+ * readings "A1".."A23" are listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - extern "C", plain pointers and sizes; no CUDA or torch types.  `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Tensor pointers are DEVICE pointers on the current CUDA device unless the argument
+ *     name says host_.  The caller owns every buffer; hot calls never allocate, never
+ *     synchronize and are asynchronous on `stream`.
+ *   - Arguments are validated on the host before any launch.  Errors are returned as
+ *     axq_status codes (no exceptions, no abort, no printing).  On an error no kernel was
+ *     launched, except AXQ_ERR_CUDA (a launch failed; axq_last_cuda_error() has the code).
+ *   - Integer outputs are exact: int32 accumulation is associative, so results are
+ *     bit-identical for every tiling, split-K factor and GPU count (A23).
+ *   - fp32 steps are pinned (IEEE division, round-half-even, no FMA contraction) so that
+ *     quantized codes match the oracle bit for bit (A1, A3, A14).
+ *   - Reentrant; LUT handles are immutable after creation, one per device, usable from
+ *     any stream.
+ */
+#ifndef AXQ_H
+#define AXQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AXQ_OK = 0,
+    AXQ_ERR_INVALID = 1,     /* null pointer, extent < 0, bad leading dimension, bits not in
+                                [2,8], misaligned pointer where alignment is documented */
+    AXQ_ERR_OVERFLOW = 2,    /* K * max|LUT| >= 2^31: an int32 accumulator could overflow */
+    AXQ_ERR_UNSUPPORTED = 3, /* a documented-but-unimplemented case (e.g. groups > 1) */
+    AXQ_ERR_CUDA = 4         /* a CUDA call failed; see axq_last_cuda_error() */
+} axq_status;
+
+/* Device representation chosen by axq_lut_create. */
+typedef enum {
+    AXQ_LUT_DELTA8 = 0, /* int8 E = LUT - a*w, shared-memory resident (64 KiB), exact part
+                           added with dp4a */
+    AXQ_LUT_I16 = 1,    /* int16 LUT values, shared-memory resident (128 KiB) */
+    AXQ_LUT_I32 = 2     /* int32 values read through L1/L2 (correctness path) */
+} axq_lut_repr;
+
+typedef struct axq_lut* axq_lut_t;
+
+/* Returns the CUDA error code of the last AXQ_ERR_CUDA on this thread (0 if none). */
+int axq_last_cuda_error(void);
+/* Static string for a status code. */
+const char* axq_status_string(axq_status s);
+/* Library version: major*10000 + minor*100 + patch. */
+int axq_version(void);
+
+/* ---------------------------------------------------------------------------------
+ * ACU table.  "the corresponding LUT is produced from AdaPT's Look-up Table (LUT)
+ * generator" (§III.C); any deterministic multiplier is allowed.
+ *
+ * axq_lut_create: host_table is a HOST int32 array of 2^(2*bits) entries, entry
+ *   (ua << bits) | uw = ACU(a, w), ua / uw the b-bit two's-complement patterns of the
+ *   activation a and the weight w (first index = ACTIVATION, A8).  bits in [2,8].
+ *   The library copies the table, picks the device representation (axq_lut_repr),
+ *   uploads it to the current device and synchronizes.  *out receives the handle.
+ * axq_lut_destroy: frees the handle (synchronizes the device first).  NULL is a no-op.
+ * axq_lut_info: bits, representation and the min / max table value (any out-pointer
+ *   may be NULL).
+ * ------------------------------------------------------------------------------- */
+axq_status axq_lut_create(int bits, const int32_t* host_table, axq_lut_t* out);
+axq_status axq_lut_destroy(axq_lut_t lut);
+axq_status axq_lut_info(axq_lut_t lut, int* bits, int* repr, int32_t* tmin, int32_t* tmax);
+
+/* ---------------------------------------------------------------------------------
+ * Quantizer.  "real_value = A x quantized_value + B where A is the scale and B is the
+ * zero point (often set to zero)" (§III.A); per-tensor max calibration (BJ:ns,
+ * overriding P:93-95's histogram, A5/A6).
+ *
+ * axq_amax:   *d_amax = max_i |x_i| over n fp32 values (exact).  n >= 0 (n = 0 -> 0).
+ * axq_scale:  *d_scale = fl32(*d_amax / (2^(bits-1)-1)), or 1.0 if *d_amax == 0 (A4).
+ * axq_quantize: q_i = clamp(rint(fl32(x_i / *d_scale)), -(2^(b-1)-1), 2^(b-1)-1), rint =
+ *   round half to even (A1), symmetric clamp (A2), IEEE division (A3).  q is int8 holding
+ *   the sign-extended b-bit code.  Layout-preserving.
+ * axq_quantize_nchw_to_nhwc: the same map on an fp32 NCHW tensor, writing int8 NHWC (the
+ *   layout axq_lut_conv2d reads).
+ * ------------------------------------------------------------------------------- */
+axq_status axq_amax(const float* x, int64_t n, float* d_amax, void* stream);
+axq_status axq_scale(const float* d_amax, int bits, float* d_scale, void* stream);
+axq_status axq_quantize(const float* x, int64_t n, const float* d_scale, int bits,
+                        int8_t* q, void* stream);
+axq_status axq_quantize_nchw_to_nhwc(const float* x, int64_t N, int64_t C, int64_t H,
+                                     int64_t W, const float* d_scale, int bits, int8_t* q,
+                                     void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * LUT-GEMM.  Linear layer y = x A^T + b (§III.B.3) with "the inner
+ * multiplications between each input and filter values using a LUT" (§IV):
+ *     C[m][n] = sum_{k<K} LUT[A[m][k]][W[n][k]]    (int32; BJ:ns acc[m,n])
+ * A: int8 activations, element (m,k) at A[m*lda + k], lda >= K.
+ * W: int8 weights stored [N][K] (PyTorch Linear layout), element (n,k) at W[n*ldw + k].
+ * C: int32 [M][ldc], ldc >= N, overwritten.
+ * M, N, K >= 0 (any zero extent: C gets zeros for K == 0, nothing otherwise).
+ * Operands must be b-bit codes (sign-extended in int8) of the LUT's bit width; other
+ * values index the table by their low b bits.
+ * Errors: AXQ_ERR_OVERFLOW if K * max|LUT| >= 2^31.
+ * ------------------------------------------------------------------------------- */
+axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
+                        const int8_t* W, int64_t ldw, axq_lut_t lut, int32_t* C, int64_t ldc,
+                        void* stream);
+
+/* Fused dequantize epilogue (P:74 with both operands' scales; "+ b"):
+ *     y = fl(fl((float)acc * fl(*d_scale_a * *d_scale_w)) + bias[n])      (A14)
+ * bias may be NULL.  workspace: NULL, or device int32 scratch of M*N elements that lets
+ * the library split K across CTAs when M*N alone cannot fill the GPU (results identical).
+ */
+typedef struct axq_epilogue {
+    const float* d_scale_a; /* device fp32 scalar: activation scale */
+    const float* d_scale_w; /* device fp32 scalar: weight scale */
+    const float* bias;      /* device fp32 [N] or NULL */
+    float* y;               /* device fp32 output */
+    int64_t ldy;            /* GEMM: row stride of y ([M][ldy], ldy >= N); conv: ignored */
+    int32_t* workspace;     /* device int32 [M*N] or NULL */
+} axq_epilogue;
+
+axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
+                           const int8_t* W, int64_t ldw, axq_lut_t lut,
+                           const axq_epilogue* ep, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * LUT convolution.  X (N, C_in, H_in, W_in) -> Y (N, C_out, H_out, W_out) with kernel
+ * size, padding, stride and groups (§III.B.1), computed as the im2col GEMM of P:119
+ * without materialising the im2col matrix (implicit im2col):
+ *     Y[img][ho][wo][co] = sum_{r,s,c} LUT[x(img, ho*sh-ph+r*dh, wo*sw-pw+s*dw, c)][Wt[co][r][s][c]]
+ * where x(...) = X value inside the image and 0 at a padded tap -- the 0 is still looked
+ * up (A11), exactly as the zero entries of the paper's im2col matrix are multiplied.
+ * X: int8 NHWC [N][H][W][C];  Wt: int8 [C_out][R][S][C] (KRSC);  Y: int32 NHWC
+ * [N][H_out][W_out][C_out].  groups must be 1 (others: AXQ_ERR_UNSUPPORTED).
+ * ------------------------------------------------------------------------------- */
+typedef struct axq_conv_desc {
+    int64_t N, H, W, C;       /* input */
+    int64_t K, R, S;          /* output channels, filter height / width */
+    int64_t stride_h, stride_w, pad_h, pad_w, dil_h, dil_w, groups;
+} axq_conv_desc;
+
+axq_status axq_conv2d_out_hw(const axq_conv_desc* d, int64_t* Ho, int64_t* Wo);
+axq_status axq_lut_conv2d(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
+                          axq_lut_t lut, int32_t* Y, void* stream);
+/* Fused dequant epilogue writing fp32 NCHW y[img][co][ho][wo] (the paper's layout). */
+axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
+                             axq_lut_t lut, const axq_epilogue* ep, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Dequantize (unfused), same pinned formula as the epilogue.
+ * axq_dequantize: acc int32 [M][ldacc] -> y fp32 [M][ldy], bias[n] (nullable).
+ * axq_dequantize_nhwc_to_nchw: acc int32 NHWC [N][HW][C] -> y fp32 NCHW [N][C][HW].
+ * ------------------------------------------------------------------------------- */
+axq_status axq_dequantize(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
+                          const float* d_scale_a, const float* d_scale_w, const float* bias,
+                          float* y, int64_t ldy, void* stream);
+axq_status axq_dequantize_nhwc_to_nchw(int64_t N, int64_t HW, int64_t C, const int32_t* acc,
+                                       const float* d_scale_a, const float* d_scale_w,
+                                       const float* bias, float* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AXQ_H */

@@ -1,0 +1,249 @@
+"""Thin ctypes binding of libaxq.so (include/axq.h).  Argument marshalling only: every step
+of the path runs in the library's CUDA kernels.  Tensors are torch CUDA tensors (PyTorch is
+used for device memory and streams only); each wrapper has the C entry point's name.
+
+There is no fallback: if libaxq.so is missing or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libaxq.so"
+
+AXQ_OK, AXQ_ERR_INVALID, AXQ_ERR_OVERFLOW, AXQ_ERR_UNSUPPORTED, AXQ_ERR_CUDA = range(5)
+REPR_NAMES = {0: "delta8", 1: "int16", 2: "int32"}
+
+EXPORTED = [
+    "axq_last_cuda_error", "axq_status_string", "axq_version",
+    "axq_lut_create", "axq_lut_destroy", "axq_lut_info",
+    "axq_amax", "axq_scale", "axq_quantize", "axq_quantize_nchw_to_nhwc",
+    "axq_lut_gemm", "axq_lut_gemm_dq",
+    "axq_conv2d_out_hw", "axq_lut_conv2d", "axq_lut_conv2d_dq",
+    "axq_dequantize", "axq_dequantize_nhwc_to_nchw",
+]
+
+
+class AxqError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__("%s failed: status %d (%s)" % (fn, status, msg))
+        self.status = status
+
+
+class axq_epilogue(ctypes.Structure):
+    _fields_ = [("d_scale_a", ctypes.c_void_p), ("d_scale_w", ctypes.c_void_p),
+                ("bias", ctypes.c_void_p), ("y", ctypes.c_void_p), ("ldy", ctypes.c_int64),
+                ("workspace", ctypes.c_void_p)]
+
+
+class axq_conv_desc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("N", "H", "W", "C", "K", "R", "S", "stride_h", "stride_w", "pad_h", "pad_w",
+                 "dil_h", "dil_w", "groups")]
+
+
+_lib = None
+
+
+def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load libaxq.so (raises if it has not been built -- there is no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ImportError("libaxq.so not built at %s (run __graft_entry__.build())" % p)
+    L = ctypes.CDLL(str(p))
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    sig = {
+        "axq_last_cuda_error": ([], i32),
+        "axq_status_string": ([i32], ctypes.c_char_p),
+        "axq_version": ([], i32),
+        "axq_lut_create": ([i32, vp, ctypes.POINTER(vp)], i32),
+        "axq_lut_destroy": ([vp], i32),
+        "axq_lut_info": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)], i32),
+        "axq_amax": ([vp, i64, vp, vp], i32),
+        "axq_scale": ([vp, i32, vp, vp], i32),
+        "axq_quantize": ([vp, i64, vp, i32, vp, vp], i32),
+        "axq_quantize_nchw_to_nhwc": ([vp, i64, i64, i64, i64, vp, i32, vp, vp], i32),
+        "axq_lut_gemm": ([i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, vp], i32),
+        "axq_lut_gemm_dq": ([i64, i64, i64, vp, i64, vp, i64, vp,
+                             ctypes.POINTER(axq_epilogue), vp], i32),
+        "axq_conv2d_out_hw": ([ctypes.POINTER(axq_conv_desc), ctypes.POINTER(i64),
+                               ctypes.POINTER(i64)], i32),
+        "axq_lut_conv2d": ([ctypes.POINTER(axq_conv_desc), vp, vp, vp, vp, vp], i32),
+        "axq_lut_conv2d_dq": ([ctypes.POINTER(axq_conv_desc), vp, vp, vp,
+                               ctypes.POINTER(axq_epilogue), vp], i32),
+        "axq_dequantize": ([i64, i64, vp, i64, vp, vp, vp, vp, i64, vp], i32),
+        "axq_dequantize_nhwc_to_nchw": ([i64, i64, i64, vp, vp, vp, vp, vp, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(fn: str, st: int) -> None:
+    if st != AXQ_OK:
+        L = load()
+        msg = L.axq_status_string(st).decode()
+        if st == AXQ_ERR_CUDA:
+            msg += " (cudaError %d)" % L.axq_last_cuda_error()
+        raise AxqError(fn, st, msg)
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---------------------------------------------------------------------------------------
+# ACU table handle
+# ---------------------------------------------------------------------------------------
+class Lut:
+    """Owns an axq_lut_t (device copy of an ACU table in the chosen representation)."""
+
+    def __init__(self, bits: int, host_table: np.ndarray):
+        t = np.ascontiguousarray(host_table, dtype=np.int32)
+        if t.size != 1 << (2 * bits):
+            raise ValueError("table must have 2^(2*bits) entries")
+        h = ctypes.c_void_p()
+        _check("axq_lut_create", load().axq_lut_create(int(bits), t.ctypes.data, ctypes.byref(h)))
+        self.handle = h
+        self.bits = int(bits)
+        b, r, lo, hi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int32(), ctypes.c_int32()
+        _check("axq_lut_info", load().axq_lut_info(h, ctypes.byref(b), ctypes.byref(r),
+                                                   ctypes.byref(lo), ctypes.byref(hi)))
+        self.repr = REPR_NAMES[r.value]
+        self.tmin, self.tmax = lo.value, hi.value
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            load().axq_lut_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def axq_lut_create(bits: int, host_table: np.ndarray) -> Lut:
+    return Lut(bits, host_table)
+
+
+def axq_lut_destroy(lut: Lut) -> None:
+    lut.close()
+
+
+# ---------------------------------------------------------------------------------------
+# Quantizer
+# ---------------------------------------------------------------------------------------
+def axq_amax(x, d_amax, stream=None) -> None:
+    _check("axq_amax", load().axq_amax(_ptr(x), x.numel(), _ptr(d_amax), _stream(stream)))
+
+
+def axq_scale(d_amax, bits: int, d_scale, stream=None) -> None:
+    _check("axq_scale", load().axq_scale(_ptr(d_amax), int(bits), _ptr(d_scale), _stream(stream)))
+
+
+def axq_quantize(x, d_scale, bits: int, q, stream=None) -> None:
+    assert x.is_contiguous() and q.is_contiguous() and q.numel() == x.numel()
+    _check("axq_quantize", load().axq_quantize(_ptr(x), x.numel(), _ptr(d_scale), int(bits),
+                                               _ptr(q), _stream(stream)))
+
+
+def axq_quantize_nchw_to_nhwc(x, d_scale, bits: int, q, stream=None) -> None:
+    assert x.is_contiguous() and q.is_contiguous() and x.dim() == 4
+    N, C, H, W = x.shape
+    _check("axq_quantize_nchw_to_nhwc",
+           load().axq_quantize_nchw_to_nhwc(_ptr(x), N, C, H, W, _ptr(d_scale), int(bits),
+                                            _ptr(q), _stream(stream)))
+
+
+# ---------------------------------------------------------------------------------------
+# LUT GEMM / conv / dequant
+# ---------------------------------------------------------------------------------------
+def axq_lut_gemm(A, W, lut: Lut, C, stream=None) -> None:
+    """A int8 [M][K] (row stride A.stride(0)), W int8 [N][K], C int32 [M][N]."""
+    M, K = A.shape
+    N = W.shape[0]
+    _check("axq_lut_gemm", load().axq_lut_gemm(M, N, K, _ptr(A), A.stride(0), _ptr(W),
+                                               W.stride(0), lut.handle, _ptr(C), C.stride(0),
+                                               _stream(stream)))
+
+
+def _epilogue(d_scale_a, d_scale_w, bias, y, ldy, workspace):
+    return axq_epilogue(_ptr(d_scale_a), _ptr(d_scale_w), _ptr(bias), _ptr(y), int(ldy),
+                        _ptr(workspace))
+
+
+def axq_lut_gemm_dq(A, W, lut: Lut, d_scale_a, d_scale_w, bias, y, workspace=None,
+                    stream=None) -> None:
+    M, K = A.shape
+    N = W.shape[0]
+    ep = _epilogue(d_scale_a, d_scale_w, bias, y, y.stride(0), workspace)
+    _check("axq_lut_gemm_dq", load().axq_lut_gemm_dq(M, N, K, _ptr(A), A.stride(0), _ptr(W),
+                                                     W.stride(0), lut.handle, ctypes.byref(ep),
+                                                     _stream(stream)))
+
+
+def conv_desc(N, H, W, C, K, R, S, stride=(1, 1), pad=(0, 0), dil=(1, 1), groups=1):
+    return axq_conv_desc(N, H, W, C, K, R, S, stride[0], stride[1], pad[0], pad[1], dil[0],
+                         dil[1], groups)
+
+
+def axq_conv2d_out_hw(desc: axq_conv_desc):
+    ho, wo = ctypes.c_int64(), ctypes.c_int64()
+    _check("axq_conv2d_out_hw", load().axq_conv2d_out_hw(ctypes.byref(desc), ctypes.byref(ho),
+                                                         ctypes.byref(wo)))
+    return ho.value, wo.value
+
+
+def axq_lut_conv2d(desc: axq_conv_desc, X_nhwc, W_krsc, lut: Lut, Y_nhwc, stream=None) -> None:
+    _check("axq_lut_conv2d", load().axq_lut_conv2d(ctypes.byref(desc), _ptr(X_nhwc),
+                                                   _ptr(W_krsc), lut.handle, _ptr(Y_nhwc),
+                                                   _stream(stream)))
+
+
+def axq_lut_conv2d_dq(desc: axq_conv_desc, X_nhwc, W_krsc, lut: Lut, d_scale_a, d_scale_w,
+                      bias, y_nchw, workspace=None, stream=None) -> None:
+    ep = _epilogue(d_scale_a, d_scale_w, bias, y_nchw, 0, workspace)
+    _check("axq_lut_conv2d_dq", load().axq_lut_conv2d_dq(ctypes.byref(desc), _ptr(X_nhwc),
+                                                         _ptr(W_krsc), lut.handle,
+                                                         ctypes.byref(ep), _stream(stream)))
+
+
+def axq_dequantize(acc, d_scale_a, d_scale_w, bias, y, stream=None) -> None:
+    M, N = acc.shape
+    _check("axq_dequantize", load().axq_dequantize(M, N, _ptr(acc), acc.stride(0),
+                                                   _ptr(d_scale_a), _ptr(d_scale_w),
+                                                   _ptr(bias), _ptr(y), y.stride(0),
+                                                   _stream(stream)))
+
+
+def axq_dequantize_nhwc_to_nchw(acc_nhwc, d_scale_a, d_scale_w, bias, y_nchw,
+                                stream=None) -> None:
+    N, H, W, C = acc_nhwc.shape
+    _check("axq_dequantize_nhwc_to_nchw",
+           load().axq_dequantize_nhwc_to_nchw(N, H * W, C, _ptr(acc_nhwc), _ptr(d_scale_a),
+                                              _ptr(d_scale_w), _ptr(bias), _ptr(y_nchw),
+                                              _stream(stream)))

@@ -1,0 +1,455 @@
+// axq_api.cu -- the extern "C" boundary (include/axq.h): argument validation, ACU table
+// representation, kernel selection and launch.  Compiled for sm_100a only.
+#include "../../include/axq.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "mm_launch.h"
+#include "quant_kernels.cuh"
+
+struct axq_lut {
+    int bits;
+    int repr;
+    int device;
+    int32_t tmin, tmax, t00;
+    int64_t absmax;
+    void* d_table;
+    int table_bytes;
+};
+
+namespace {
+
+thread_local int g_last_cuda = 0;
+
+inline axq_status cuda_fail(cudaError_t e) {
+    g_last_cuda = (int)e;
+    return AXQ_ERR_CUDA;
+}
+
+inline axq_status check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+    return AXQ_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        cached[dev] = n;
+    }
+    return cached[dev];
+}
+
+int stream_grid(int64_t n_items, int per_block) {
+    int64_t g = (n_items + per_block - 1) / per_block;
+    int64_t cap = (int64_t)sm_count() * 8;
+    return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------------------------
+// LUT-MM launch plumbing (kernels are instantiated in mm_delta8.cu / mm_i16.cu / mm_i32.cu)
+// ---------------------------------------------------------------------------------------
+using axq::Cfg;
+using axq::CFG_BIG;
+using axq::CFG_SMALL;
+
+axq_status launch_mm(int epi, int loader, int repr, const axq::MMArgs& p, const Cfg& c,
+                     dim3 grid, cudaStream_t st) {
+    int rc;
+    switch (repr) {
+        case AXQ_LUT_DELTA8: rc = axq::launch_mm_delta8(epi, loader, p, c, grid, st); break;
+        case AXQ_LUT_I16: rc = axq::launch_mm_i16(epi, loader, p, c, grid, st); break;
+        default: rc = axq::launch_mm_i32(epi, loader, p, c, grid, st); break;
+    }
+    if (rc != 0) return cuda_fail((cudaError_t)rc);
+    return AXQ_OK;
+}
+
+Cfg pick_cfg(int64_t M) { return M <= 2048 ? CFG_SMALL : CFG_BIG; }
+
+// K-splitting so that small M*N problems still fill the SMs (exact: integer atomics).
+int64_t pick_k_split(int64_t M, int64_t N, int64_t K, const Cfg& c, bool allow) {
+    int64_t kr = ((K + axq::KC - 1) / axq::KC) * axq::KC;
+    if (!allow || K <= 0) return std::max<int64_t>(kr, axq::KC);
+    int64_t bm = (int64_t)c.warps * 32 * c.R;
+    int64_t tiles = ((M + bm - 1) / bm) * ((N + c.tn - 1) / c.tn);
+    int64_t want = (int64_t)sm_count() * 2;
+    if (tiles >= want) return kr;
+    int64_t splits = (want + tiles - 1) / tiles;
+    int64_t max_splits = std::max<int64_t>(1, kr / (4 * axq::KC));  // >= 64 k per split
+    splits = std::min(splits, max_splits);
+    int64_t ks = (kr + splits - 1) / splits;
+    ks = ((ks + axq::KC - 1) / axq::KC) * axq::KC;
+    return std::max<int64_t>(ks, axq::KC);
+}
+
+axq_status check_lut(axq_lut_t lut) {
+    if (!lut || !lut->d_table) return AXQ_ERR_INVALID;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != lut->device) return AXQ_ERR_INVALID;
+    return AXQ_OK;
+}
+
+axq_status overflow_guard(axq_lut_t lut, int64_t K) {
+    // int32 accumulation is exact iff every partial sum fits; K * max|T| < 2^31 suffices.
+    if (K > 0 && (double)K * (double)lut->absmax >= 2147483648.0) return AXQ_ERR_OVERFLOW;
+    return AXQ_OK;
+}
+
+void fill_common(axq::MMArgs& p, axq_lut_t lut) {
+    p.table = lut->d_table;
+    p.table_bytes = lut->table_bytes;
+    p.t00 = lut->t00;
+}
+
+}  // namespace
+
+extern "C" {
+
+int axq_last_cuda_error(void) { return g_last_cuda; }
+
+const char* axq_status_string(axq_status s) {
+    switch (s) {
+        case AXQ_OK: return "ok";
+        case AXQ_ERR_INVALID: return "invalid argument";
+        case AXQ_ERR_OVERFLOW: return "int32 accumulator could overflow (K * max|LUT| >= 2^31)";
+        case AXQ_ERR_UNSUPPORTED: return "unsupported case";
+        case AXQ_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+int axq_version(void) { return 100; }
+
+// ---------------------------------------------------------------------------------------
+// ACU table
+// ---------------------------------------------------------------------------------------
+axq_status axq_lut_create(int bits, const int32_t* host_table, axq_lut_t* out) {
+    if (!out || !host_table || bits < 2 || bits > 8) return AXQ_ERR_INVALID;
+    *out = nullptr;
+    const int n = 1 << bits, mask = n - 1;
+    int64_t tmin = INT32_MAX, tmax = INT32_MIN;
+    bool delta_ok = true;
+    for (int ua = 0; ua < n; ++ua) {
+        for (int uw = 0; uw < n; ++uw) {
+            int64_t v = host_table[(ua << bits) | uw];
+            tmin = std::min(tmin, v);
+            tmax = std::max(tmax, v);
+            int a = (ua >= n / 2) ? ua - n : ua, w = (uw >= n / 2) ? uw - n : uw;
+            int64_t e = v - (int64_t)a * w;
+            if (e < -128 || e > 127) delta_ok = false;
+        }
+    }
+    int repr = delta_ok ? AXQ_LUT_DELTA8
+                        : (tmin >= INT16_MIN && tmax <= INT16_MAX) ? AXQ_LUT_I16 : AXQ_LUT_I32;
+    const int esz = repr == AXQ_LUT_DELTA8 ? 1 : repr == AXQ_LUT_I16 ? 2 : 4;
+    // Device layout: 8-bit two's-complement pattern space, TRANSPOSED: entry [uw8][ua8].
+    // Patterns that are not sign-extended b-bit codes are never produced by the quantizer
+    // and hold 0.
+    std::vector<uint8_t> dev_tab((size_t)65536 * esz, 0);
+    for (int uw8 = 0; uw8 < 256; ++uw8) {
+        int w = (int)(int8_t)uw8;
+        if (w < -(n / 2) || w >= n / 2) continue;
+        for (int ua8 = 0; ua8 < 256; ++ua8) {
+            int a = (int)(int8_t)ua8;
+            if (a < -(n / 2) || a >= n / 2) continue;
+            int32_t v = host_table[((a & mask) << bits) | (w & mask)];
+            size_t idx = ((size_t)uw8 << 8) | (size_t)ua8;
+            if (repr == AXQ_LUT_DELTA8) {
+                dev_tab[idx] = (uint8_t)(int8_t)(v - a * w);
+            } else if (repr == AXQ_LUT_I16) {
+                int16_t s = (int16_t)v;
+                std::memcpy(&dev_tab[idx * 2], &s, 2);
+            } else {
+                std::memcpy(&dev_tab[idx * 4], &v, 4);
+            }
+        }
+    }
+    axq_lut* L = new axq_lut();
+    L->bits = bits;
+    L->repr = repr;
+    cudaGetDevice(&L->device);
+    L->tmin = (int32_t)tmin;
+    L->tmax = (int32_t)tmax;
+    L->t00 = host_table[0];
+    L->absmax = std::max<int64_t>(std::llabs(tmin), std::llabs(tmax));
+    L->table_bytes = 65536 * esz;
+    cudaError_t e = cudaMalloc(&L->d_table, L->table_bytes);
+    if (e != cudaSuccess) {
+        delete L;
+        return cuda_fail(e);
+    }
+    e = cudaMemcpy(L->d_table, dev_tab.data(), L->table_bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(L->d_table);
+        delete L;
+        return cuda_fail(e);
+    }
+    *out = L;
+    return AXQ_OK;
+}
+
+axq_status axq_lut_destroy(axq_lut_t lut) {
+    if (!lut) return AXQ_OK;
+    cudaDeviceSynchronize();
+    cudaFree(lut->d_table);
+    delete lut;
+    return AXQ_OK;
+}
+
+axq_status axq_lut_info(axq_lut_t lut, int* bits, int* repr, int32_t* tmin, int32_t* tmax) {
+    if (!lut) return AXQ_ERR_INVALID;
+    if (bits) *bits = lut->bits;
+    if (repr) *repr = lut->repr;
+    if (tmin) *tmin = lut->tmin;
+    if (tmax) *tmax = lut->tmax;
+    return AXQ_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Quantizer
+// ---------------------------------------------------------------------------------------
+axq_status axq_amax(const float* x, int64_t n, float* d_amax, void* stream) {
+    if (n < 0 || !d_amax || (n > 0 && !x)) return AXQ_ERR_INVALID;
+    cudaError_t e = cudaMemsetAsync(d_amax, 0, sizeof(float), S(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (n == 0) return AXQ_OK;
+    axq::amax_kernel<<<stream_grid(n / 4 + 1, 256 * 4), 256, 0, S(stream)>>>(
+        x, n, reinterpret_cast<unsigned int*>(d_amax));
+    return check_launch();
+}
+
+axq_status axq_scale(const float* d_amax, int bits, float* d_scale, void* stream) {
+    if (!d_amax || !d_scale || bits < 2 || bits > 8) return AXQ_ERR_INVALID;
+    axq::scale_kernel<<<1, 1, 0, S(stream)>>>(d_amax, bits, d_scale);
+    return check_launch();
+}
+
+axq_status axq_quantize(const float* x, int64_t n, const float* d_scale, int bits, int8_t* q,
+                        void* stream) {
+    if (n < 0 || !d_scale || bits < 2 || bits > 8 || (n > 0 && (!x || !q))) return AXQ_ERR_INVALID;
+    if (n == 0) return AXQ_OK;
+    axq::quantize_kernel<<<stream_grid(n / 4 + 1, 256 * 4), 256, 0, S(stream)>>>(x, n, d_scale, bits, q);
+    return check_launch();
+}
+
+axq_status axq_quantize_nchw_to_nhwc(const float* x, int64_t N, int64_t C, int64_t H, int64_t W,
+                                     const float* d_scale, int bits, int8_t* q, void* stream) {
+    if (N < 0 || C < 0 || H < 0 || W < 0 || !d_scale || bits < 2 || bits > 8) return AXQ_ERR_INVALID;
+    if (N == 0 || C == 0 || H == 0 || W == 0) return AXQ_OK;
+    if (!x || !q || N > 65535) return AXQ_ERR_INVALID;
+    int64_t HW = H * W;
+    dim3 grid((unsigned)((HW + 31) / 32), (unsigned)((C + 31) / 32), (unsigned)N);
+    axq::quantize_nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, S(stream)>>>(x, C, HW, d_scale, bits, q);
+    return check_launch();
+}
+
+// ---------------------------------------------------------------------------------------
+// LUT-GEMM
+// ---------------------------------------------------------------------------------------
+static axq_status gemm_common(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
+                              const int8_t* W, int64_t ldw, axq_lut_t lut) {
+    if (M < 0 || N < 0 || K < 0) return AXQ_ERR_INVALID;
+    axq_status s = check_lut(lut);
+    if (s != AXQ_OK) return s;
+    if (M > 0 && N > 0 && K > 0) {
+        if (!A || !W || lda < K || ldw < K) return AXQ_ERR_INVALID;
+    }
+    return overflow_guard(lut, K);
+}
+
+axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
+                        const int8_t* W, int64_t ldw, axq_lut_t lut, int32_t* C, int64_t ldc,
+                        void* stream) {
+    axq_status s = gemm_common(M, N, K, A, lda, W, ldw, lut);
+    if (s != AXQ_OK) return s;
+    if (M == 0 || N == 0) return AXQ_OK;
+    if (!C || ldc < N) return AXQ_ERR_INVALID;
+    if (K == 0) {
+        cudaError_t e = cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, S(stream));
+        return e == cudaSuccess ? AXQ_OK : cuda_fail(e);
+    }
+    axq::MMArgs p{};
+    p.A = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = K;
+    fill_common(p, lut);
+    p.C_out = C; p.ldc = ldc;
+    Cfg c = pick_cfg(M);
+    p.k_split = pick_k_split(M, N, K, c, true);
+    int64_t splits = (K + p.k_split - 1) / p.k_split;
+    int64_t bm = (int64_t)c.warps * 32 * c.R;
+    dim3 grid((unsigned)((M + bm - 1) / bm), (unsigned)((N + c.tn - 1) / c.tn), (unsigned)splits);
+    int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
+    int epi = axq::EPI_RAW;
+    if (splits > 1) {
+        cudaError_t e = cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, S(stream));
+        if (e != cudaSuccess) return cuda_fail(e);
+        epi = axq::EPI_RAW_ATOMIC;
+    }
+    return launch_mm(epi, loader, lut->repr, p, c, grid, S(stream));
+}
+
+axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
+                           const int8_t* W, int64_t ldw, axq_lut_t lut, const axq_epilogue* ep,
+                           void* stream) {
+    axq_status s = gemm_common(M, N, K, A, lda, W, ldw, lut);
+    if (s != AXQ_OK) return s;
+    if (!ep || !ep->d_scale_a || !ep->d_scale_w) return AXQ_ERR_INVALID;
+    if (M == 0 || N == 0) return AXQ_OK;
+    if (!ep->y || ep->ldy < N) return AXQ_ERR_INVALID;
+    axq::MMArgs p{};
+    p.A = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = std::max<int64_t>(K, 0);
+    fill_common(p, lut);
+    p.sa = ep->d_scale_a; p.sw_ = ep->d_scale_w; p.bias = ep->bias; p.y = ep->y; p.ldy = ep->ldy;
+    Cfg c = pick_cfg(M);
+    p.k_split = pick_k_split(M, N, K, c, ep->workspace != nullptr);
+    int64_t splits = K > 0 ? (K + p.k_split - 1) / p.k_split : 1;
+    int64_t bm = (int64_t)c.warps * 32 * c.R;
+    dim3 grid((unsigned)((M + bm - 1) / bm), (unsigned)((N + c.tn - 1) / c.tn), (unsigned)splits);
+    int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
+    if (splits > 1) {
+        p.C_out = ep->workspace; p.ldc = N;
+        cudaError_t e = cudaMemsetAsync(ep->workspace, 0, (size_t)M * N * 4, S(stream));
+        if (e != cudaSuccess) return cuda_fail(e);
+        s = launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, S(stream));
+        if (s != AXQ_OK) return s;
+        return axq_dequantize(M, N, ep->workspace, N, ep->d_scale_a, ep->d_scale_w, ep->bias,
+                              ep->y, ep->ldy, stream);
+    }
+    return launch_mm(axq::EPI_DQ_ROWS, loader, lut->repr, p, c, grid, S(stream));
+}
+
+// ---------------------------------------------------------------------------------------
+// LUT convolution (implicit im2col)
+// ---------------------------------------------------------------------------------------
+axq_status axq_conv2d_out_hw(const axq_conv_desc* d, int64_t* Ho, int64_t* Wo) {
+    if (!d || !Ho || !Wo) return AXQ_ERR_INVALID;
+    if (d->stride_h <= 0 || d->stride_w <= 0 || d->dil_h <= 0 || d->dil_w <= 0 || d->pad_h < 0 ||
+        d->pad_w < 0 || d->R <= 0 || d->S <= 0)
+        return AXQ_ERR_INVALID;
+    *Ho = (d->H + 2 * d->pad_h - d->dil_h * (d->R - 1) - 1) / d->stride_h + 1;
+    *Wo = (d->W + 2 * d->pad_w - d->dil_w * (d->S - 1) - 1) / d->stride_w + 1;
+    return AXQ_OK;
+}
+
+static axq_status conv_setup(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
+                             axq_lut_t lut, axq::MMArgs& p, int& loader) {
+    if (!d) return AXQ_ERR_INVALID;
+    if (d->N < 0 || d->H <= 0 || d->W <= 0 || d->C <= 0 || d->K < 0) return AXQ_ERR_INVALID;
+    if (d->groups != 1) return d->groups < 1 ? AXQ_ERR_INVALID : AXQ_ERR_UNSUPPORTED;
+    int64_t Ho, Wo;
+    axq_status s = axq_conv2d_out_hw(d, &Ho, &Wo);
+    if (s != AXQ_OK) return s;
+    if (Ho <= 0 || Wo <= 0) return AXQ_ERR_INVALID;
+    s = check_lut(lut);
+    if (s != AXQ_OK) return s;
+    const int64_t K = d->R * d->S * d->C;
+    s = overflow_guard(lut, K);
+    if (s != AXQ_OK) return s;
+    if (d->N > 0 && d->K > 0 && (!X || !Wt)) return AXQ_ERR_INVALID;
+    if (d->H * d->W * d->C >= (int64_t)1 << 31 || Ho * Wo >= (int64_t)1 << 31) return AXQ_ERR_INVALID;
+    p = axq::MMArgs{};
+    p.A = X; p.lda = 0; p.W = Wt; p.ldw = K;
+    p.M = d->N * Ho * Wo; p.N = d->K; p.K = K;
+    p.H = (int)d->H; p.Wd = (int)d->W; p.C = (int)d->C; p.Ho = (int)Ho; p.Wo = (int)Wo;
+    p.S = (int)d->S; p.sh = (int)d->stride_h; p.sw = (int)d->stride_w;
+    p.ph = (int)d->pad_h; p.pw = (int)d->pad_w; p.dh = (int)d->dil_h; p.dw = (int)d->dil_w;
+    fill_common(p, lut);
+    loader = ((d->C & 15) == 0 && aligned16(X)) ? axq::LOAD_CONV : axq::LOAD_CONV_BYTES;
+    return AXQ_OK;
+}
+
+axq_status axq_lut_conv2d(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
+                          axq_lut_t lut, int32_t* Y, void* stream) {
+    axq::MMArgs p;
+    int loader;
+    axq_status s = conv_setup(d, X, Wt, lut, p, loader);
+    if (s != AXQ_OK) return s;
+    if (p.M == 0 || p.N == 0) return AXQ_OK;
+    if (!Y) return AXQ_ERR_INVALID;
+    p.C_out = Y; p.ldc = p.N;
+    Cfg c = pick_cfg(p.M);
+    p.k_split = pick_k_split(p.M, p.N, p.K, c, true);
+    int64_t splits = (p.K + p.k_split - 1) / p.k_split;
+    int64_t bm = (int64_t)c.warps * 32 * c.R;
+    dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + c.tn - 1) / c.tn), (unsigned)splits);
+    int epi = axq::EPI_RAW;
+    if (splits > 1) {
+        cudaError_t e = cudaMemsetAsync(Y, 0, (size_t)p.M * p.N * 4, S(stream));
+        if (e != cudaSuccess) return cuda_fail(e);
+        epi = axq::EPI_RAW_ATOMIC;
+    }
+    return launch_mm(epi, loader, lut->repr, p, c, grid, S(stream));
+}
+
+axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
+                             axq_lut_t lut, const axq_epilogue* ep, void* stream) {
+    axq::MMArgs p;
+    int loader;
+    axq_status s = conv_setup(d, X, Wt, lut, p, loader);
+    if (s != AXQ_OK) return s;
+    if (!ep || !ep->d_scale_a || !ep->d_scale_w) return AXQ_ERR_INVALID;
+    if (p.M == 0 || p.N == 0) return AXQ_OK;
+    if (!ep->y) return AXQ_ERR_INVALID;
+    p.sa = ep->d_scale_a; p.sw_ = ep->d_scale_w; p.bias = ep->bias; p.y = ep->y;
+    Cfg c = pick_cfg(p.M);
+    p.k_split = pick_k_split(p.M, p.N, p.K, c, ep->workspace != nullptr);
+    int64_t splits = (p.K + p.k_split - 1) / p.k_split;
+    int64_t bm = (int64_t)c.warps * 32 * c.R;
+    dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + c.tn - 1) / c.tn), (unsigned)splits);
+    if (splits > 1) {
+        p.C_out = ep->workspace; p.ldc = p.N;
+        cudaError_t e = cudaMemsetAsync(ep->workspace, 0, (size_t)p.M * p.N * 4, S(stream));
+        if (e != cudaSuccess) return cuda_fail(e);
+        s = launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, S(stream));
+        if (s != AXQ_OK) return s;
+        return axq_dequantize_nhwc_to_nchw(d->N, (int64_t)p.Ho * p.Wo, p.N, ep->workspace,
+                                           ep->d_scale_a, ep->d_scale_w, ep->bias, ep->y, stream);
+    }
+    return launch_mm(axq::EPI_DQ_NCHW, loader, lut->repr, p, c, grid, S(stream));
+}
+
+// ---------------------------------------------------------------------------------------
+// Dequantize
+// ---------------------------------------------------------------------------------------
+axq_status axq_dequantize(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
+                          const float* d_scale_a, const float* d_scale_w, const float* bias,
+                          float* y, int64_t ldy, void* stream) {
+    if (M < 0 || N < 0 || !d_scale_a || !d_scale_w) return AXQ_ERR_INVALID;
+    if (M == 0 || N == 0) return AXQ_OK;
+    if (!acc || !y || ldacc < N || ldy < N) return AXQ_ERR_INVALID;
+    axq::dequant_rows_kernel<<<stream_grid(M * N, 256 * 4), 256, 0, S(stream)>>>(
+        M, N, acc, ldacc, d_scale_a, d_scale_w, bias, y, ldy);
+    return check_launch();
+}
+
+axq_status axq_dequantize_nhwc_to_nchw(int64_t N, int64_t HW, int64_t C, const int32_t* acc,
+                                       const float* d_scale_a, const float* d_scale_w,
+                                       const float* bias, float* y, void* stream) {
+    if (N < 0 || HW < 0 || C < 0 || !d_scale_a || !d_scale_w) return AXQ_ERR_INVALID;
+    if (N == 0 || HW == 0 || C == 0) return AXQ_OK;
+    if (!acc || !y || N > 65535) return AXQ_ERR_INVALID;
+    dim3 grid((unsigned)((HW + 31) / 32), (unsigned)((C + 31) / 32), (unsigned)N);
+    axq::dequant_nhwc_to_nchw_kernel<<<grid, dim3(32, 8), 0, S(stream)>>>(acc, HW, C, d_scale_a,
+                                                                        d_scale_w, bias, y);
+    return check_launch();
+}
+
+}  // extern "C"

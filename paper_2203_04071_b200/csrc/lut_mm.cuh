@@ -1,0 +1,339 @@
+// lut_mm.cuh -- the approximate LUT-GEMM / implicit-im2col LUT-conv core (sm_100a).
+//
+// Computes acc[m][n] = sum_k LUT[a[m][k]][w[n][k]] in int32 (BASELINE.json north_star;
+// PAPER.md:161 "the inner multiplications between each input and filter values using a
+// LUT"), where a[m][k] is a row of A (linear layer) or of the implicit im2col
+// matrix of a convolution.
+//
+// Design:
+//  * The ACU table lives in shared memory for the whole CTA, TRANSPOSED (row = weight
+//    pattern uw, column = activation pattern ua) so that the 32 lanes of one gather share
+//    the weight and differ only in the activation: a row is 256 B (int8) = 2 bank lines,
+//    so a gather costs at most 2 wavefronts and 1 for the usual |a| < 64 codes.
+//  * Representation DELTA8 stores E = LUT - a*w as int8 (64 KiB); the exact part a*w is
+//    added with one dp4a per 4 lookups, so lookups stay 1 byte wide.  I16 stores LUT
+//    values directly (128 KiB); I32 reads a global int32 table (correctness path).
+//  * One lane owns R output rows (m) x TN output columns (n); the 32 lanes of a warp own
+//    32 consecutive rows.  The gather index (uw << 8) | ua is built by ONE byte-permute
+//    (PRMT) from a zero-padded activation word and the packed weight word.
+//  * K is streamed in chunks of KC = 16 bytes: activations go global -> registers
+//    (lane-private rows, 16-byte loads, prefetched one chunk ahead); the CTA's weight
+//    tile [KC/4][TN] (packed 4 k per word) is staged through double-buffered shared
+//    memory and read with broadcast 16-byte loads.
+//  * K-tail storage padding contributes (0,0) lookups; they are removed exactly by
+//    subtracting npad * LUT[0][0] (semantic conv padding is NOT removed: A11).
+//  * Split-K over gridDim.z (int32 atomics; exact because integer addition is
+//    associative).  Epilogues: raw int32, atomic int32, fused dequant to [M][N] fp32 or to
+//    NCHW fp32 (lanes = consecutive pixels -> coalesced stores).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace axq {
+
+constexpr int KC = 16;
+
+enum { REPR_DELTA8 = 0, REPR_I16 = 1, REPR_I32 = 2 };
+enum { EPI_RAW = 0, EPI_RAW_ATOMIC = 1, EPI_DQ_ROWS = 2, EPI_DQ_NCHW = 3 };
+enum { LOAD_GEMM = 0, LOAD_CONV = 1, LOAD_GEMM_BYTES = 2, LOAD_CONV_BYTES = 3 };
+
+struct MMArgs {
+    const int8_t* A;  // GEMM: [M][lda]; conv: NHWC input X
+    int64_t lda;
+    const int8_t* W;  // [N][ldw]  (conv: KRSC flattened, ldw = R*S*C)
+    int64_t ldw;
+    int64_t M, N, K;
+    // conv geometry
+    int H, Wd, C, Ho, Wo, S, sh, sw, ph, pw, dh, dw;
+    const void* table;  // device table (representation-specific layout, [uw][ua])
+    int table_bytes;
+    int32_t t00;        // LUT[0][0] (value of one storage-padding lookup)
+    int64_t k_split;    // K extent per gridDim.z slice, multiple of KC
+    // outputs
+    int32_t* C_out;
+    int64_t ldc;
+    const float* sa;
+    const float* sw_;
+    const float* bias;
+    float* y;
+    int64_t ldy;
+};
+
+template <int REPR>
+__device__ __forceinline__ int lut_fetch(const int8_t* lut_s, const int32_t* lut_g, uint32_t idx) {
+    if constexpr (REPR == REPR_DELTA8) {
+        return (int)lut_s[idx];
+    } else if constexpr (REPR == REPR_I16) {
+        return (int)reinterpret_cast<const int16_t*>(lut_s)[idx];
+    } else {
+        return __ldg(lut_g + idx);
+    }
+}
+
+__device__ __forceinline__ uint4 ldg16(const int8_t* p) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+// Per-row state of the activation loader.
+struct RowInfo {
+    int64_t m;       // global row
+    int64_t base;    // GEMM: m*lda ; conv: img*H*W*C
+    int hb, wb;      // conv: ho*sh - ph, wo*sw - pw
+    bool valid;
+};
+
+template <int LOADER>
+__device__ __forceinline__ RowInfo make_row(const MMArgs& p, int64_t m) {
+    RowInfo ri;
+    ri.m = m;
+    ri.valid = m < p.M;
+    if constexpr (LOADER == LOAD_GEMM || LOADER == LOAD_GEMM_BYTES) {
+        ri.base = m * p.lda;
+        ri.hb = ri.wb = 0;
+    } else {
+        int64_t hw = (int64_t)p.Ho * p.Wo;
+        int64_t mm = ri.valid ? m : 0;
+        int64_t img = mm / hw;
+        int64_t rem = mm - img * hw;
+        int ho = (int)(rem / p.Wo), wo = (int)(rem - (int64_t)ho * p.Wo);
+        ri.base = img * (int64_t)p.H * p.Wd * p.C;
+        ri.hb = ho * p.sh - p.ph;
+        ri.wb = wo * p.sw - p.pw;
+    }
+    return ri;
+}
+
+// Load the 16 activation bytes a[m][k0 .. k0+15] (zeros beyond K or out of range rows;
+// zeros at semantic conv padding taps, which ARE looked up).
+template <int LOADER>
+__device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int64_t k0) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if constexpr (LOADER == LOAD_GEMM) {
+        if (ri.valid && k0 + KC <= p.K) return ldg16(p.A + ri.base + k0);
+        if (ri.valid) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            for (int j = 0; j < KC; ++j)
+                if (k0 + j < p.K)
+                    w[j >> 2] |= (uint32_t)(uint8_t)p.A[ri.base + k0 + j] << (8 * (j & 3));
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return v;
+    } else if constexpr (LOADER == LOAD_GEMM_BYTES) {
+        if (ri.valid) {
+            uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < KC; ++j)
+                if (k0 + j < p.K)
+                    w[j >> 2] |= (uint32_t)(uint8_t)p.A[ri.base + k0 + j] << (8 * (j & 3));
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return v;
+    } else if constexpr (LOADER == LOAD_CONV) {
+        // C % 16 == 0: the chunk lies inside one filter tap (r, s).
+        int rs = (int)(k0 / p.C);
+        int c0 = (int)(k0 - (int64_t)rs * p.C);
+        int r = rs / p.S, s = rs - r * p.S;
+        int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
+        if (ri.valid && k0 < p.K && hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
+            v = ldg16(p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c0);
+        return v;
+    } else {  // LOAD_CONV_BYTES: any C
+        if (ri.valid) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            for (int j = 0; j < KC; ++j) {
+                int64_t k = k0 + j;
+                if (k < p.K) {
+                    int rs = (int)(k / p.C);
+                    int c = (int)(k - (int64_t)rs * p.C);
+                    int r = rs / p.S, s = rs - r * p.S;
+                    int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
+                    if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
+                        w[j >> 2] |= (uint32_t)(uint8_t)p.A[ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c]
+                                     << (8 * (j & 3));
+                }
+            }
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return v;
+    }
+}
+
+__device__ __forceinline__ uint4 load_w(const MMArgs& p, int64_t n, int64_t k0, bool vec) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (n >= p.N) return v;
+    const int8_t* row = p.W + n * p.ldw;
+    if (vec && k0 + KC <= p.K) return ldg16(row + k0);
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (int j = 0; j < KC; ++j)
+        if (k0 + j < p.K) w[j >> 2] |= (uint32_t)(uint8_t)row[k0 + j] << (8 * (j & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16) ? 1 : 3)
+lut_mm_kernel(const MMArgs p) {
+    constexpr int NT = WARPS * 32;
+    constexpr int BM = WARPS * 32 * R;
+    extern __shared__ __align__(16) int8_t smem[];
+    // layout: [table (table_bytes, 0 for I32)] [W tiles: 2 x KC/4 x TN words]
+    int8_t* lut_s = smem;
+    const int tbytes = (REPR == REPR_I32) ? 0 : p.table_bytes;
+    uint32_t* w_s = reinterpret_cast<uint32_t*>(smem + tbytes);
+    const int32_t* lut_g = reinterpret_cast<const int32_t*>(p.table);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m0 = (int64_t)blockIdx.x * BM;
+    const int64_t n0 = (int64_t)blockIdx.y * TN;
+    const int64_t kb = (int64_t)blockIdx.z * p.k_split;
+    const int64_t ke = min(p.K, kb + p.k_split);
+    const int nchunks = (int)((ke - kb + KC - 1) / KC);
+    const bool wvec = ((p.ldw & 15) == 0) && ((reinterpret_cast<uintptr_t>(p.W) & 15) == 0);
+
+    // ---- stage the ACU table in shared memory (once per CTA) ----
+    if constexpr (REPR != REPR_I32) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.table);
+        uint4* dst = reinterpret_cast<uint4*>(lut_s);
+        for (int i = tid; i < tbytes / 16; i += NT) dst[i] = __ldg(src + i);
+    }
+
+    RowInfo rows[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        rows[r] = make_row<LOADER>(p, m0 + (int64_t)(warp * R + r) * 32 + lane);
+
+    int acc[R][TN];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int n = 0; n < TN; ++n) acc[r][n] = 0;
+
+    uint4 a_cur[R], a_nxt[R];
+    uint4 w_nxt = make_uint4(0, 0, 0, 0);
+    if (nchunks > 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) a_cur[r] = load_a<LOADER>(p, rows[r], kb);
+        if (tid < TN) {
+            uint4 wv = load_w(p, n0 + tid, kb, wvec);
+            w_s[0 * TN + tid] = wv.x;
+            w_s[1 * TN + tid] = wv.y;
+            w_s[2 * TN + tid] = wv.z;
+            w_s[3 * TN + tid] = wv.w;
+        }
+    }
+    __syncthreads();
+
+    for (int ci = 0; ci < nchunks; ++ci) {
+        const bool has_next = ci + 1 < nchunks;
+        const int64_t kn = kb + (int64_t)(ci + 1) * KC;
+        if (has_next) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) a_nxt[r] = load_a<LOADER>(p, rows[r], kn);
+            if (tid < TN) w_nxt = load_w(p, n0 + tid, kn, wvec);
+        }
+        const uint32_t* ws = w_s + (ci & 1) * (4 * TN);
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq) {
+            uint32_t a4[R], alo[R], ahi[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                a4[r] = (kq == 0) ? a_cur[r].x : (kq == 1) ? a_cur[r].y : (kq == 2) ? a_cur[r].z : a_cur[r].w;
+                alo[r] = __byte_perm(a4[r], 0u, 0x4140);  // [a0, 0, a1, 0]
+                ahi[r] = __byte_perm(a4[r], 0u, 0x4342);  // [a2, 0, a3, 0]
+            }
+#pragma unroll
+            for (int n4 = 0; n4 < TN / 4; ++n4) {
+                const uint4 wv = *reinterpret_cast<const uint4*>(ws + kq * TN + n4 * 4);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t w4 = (j == 0) ? wv.x : (j == 1) ? wv.y : (j == 2) ? wv.z : wv.w;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        // gather index (uw << 8) | ua for the 4 k of this word
+                        const uint32_t i0 = __byte_perm(alo[r], w4, 0x1140);
+                        const uint32_t i1 = __byte_perm(alo[r], w4, 0x3352);
+                        const uint32_t i2 = __byte_perm(ahi[r], w4, 0x1160);
+                        const uint32_t i3 = __byte_perm(ahi[r], w4, 0x3372);
+                        const int e0 = lut_fetch<REPR>(lut_s, lut_g, i0);
+                        const int e1 = lut_fetch<REPR>(lut_s, lut_g, i1);
+                        const int e2 = lut_fetch<REPR>(lut_s, lut_g, i2);
+                        const int e3 = lut_fetch<REPR>(lut_s, lut_g, i3);
+                        int s = acc[r][n4 * 4 + j];
+                        if constexpr (REPR == REPR_DELTA8) s = __dp4a((int)a4[r], (int)w4, s);
+                        acc[r][n4 * 4 + j] = s + e0 + e1 + e2 + e3;
+                    }
+                }
+            }
+        }
+        if (has_next) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) a_cur[r] = a_nxt[r];
+            if (tid < TN) {
+                uint32_t* wd = w_s + ((ci + 1) & 1) * (4 * TN);
+                wd[0 * TN + tid] = w_nxt.x;
+                wd[1 * TN + tid] = w_nxt.y;
+                wd[2 * TN + tid] = w_nxt.z;
+                wd[3 * TN + tid] = w_nxt.w;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- remove storage-padding lookups of the K tail (exact) ----
+    const int64_t npad = (int64_t)nchunks * KC - (ke - kb);
+    if (npad > 0) {
+        const int corr = (int)(npad * (int64_t)p.t00);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int n = 0; n < TN; ++n) acc[r][n] -= corr;
+    }
+
+    // ---- epilogue ----
+    float sc = 0.f;
+    if constexpr (EPI == EPI_DQ_ROWS || EPI == EPI_DQ_NCHW) sc = __fmul_rn(*p.sa, *p.sw_);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const RowInfo& ri = rows[r];
+        if (!ri.valid) continue;
+        const int64_t m = ri.m;
+        if constexpr (EPI == EPI_RAW) {
+            int32_t* c = p.C_out + m * p.ldc + n0;
+            if (n0 + TN <= p.N && ((p.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.C_out) & 15) == 0)) {
+#pragma unroll
+                for (int n = 0; n < TN; n += 4)
+                    *reinterpret_cast<int4*>(c + n) = make_int4(acc[r][n], acc[r][n + 1], acc[r][n + 2], acc[r][n + 3]);
+            } else {
+#pragma unroll
+                for (int n = 0; n < TN; ++n)
+                    if (n0 + n < p.N) c[n] = acc[r][n];
+            }
+        } else if constexpr (EPI == EPI_RAW_ATOMIC) {
+            int32_t* c = p.C_out + m * p.ldc + n0;
+#pragma unroll
+            for (int n = 0; n < TN; ++n)
+                if (n0 + n < p.N) atomicAdd(c + n, acc[r][n]);
+        } else if constexpr (EPI == EPI_DQ_ROWS) {
+            float* yr = p.y + m * p.ldy + n0;
+#pragma unroll
+            for (int n = 0; n < TN; ++n) {
+                if (n0 + n < p.N) {
+                    float v = __fmul_rn(__int2float_rn(acc[r][n]), sc);
+                    yr[n] = p.bias ? __fadd_rn(v, p.bias[n0 + n]) : v;
+                }
+            }
+        } else {  // EPI_DQ_NCHW: m = (img, ho, wo); y[img][n][ho][wo]
+            const int64_t hw = (int64_t)p.Ho * p.Wo;
+            const int64_t img = m / hw, pix = m - img * hw;
+            float* yb = p.y + img * p.N * hw + pix;
+#pragma unroll
+            for (int n = 0; n < TN; ++n) {
+                if (n0 + n < p.N) {
+                    float v = __fmul_rn(__int2float_rn(acc[r][n]), sc);
+                    __stcs(yb + (n0 + n) * hw, p.bias ? __fadd_rn(v, p.bias[n0 + n]) : v);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace axq

@@ -1,0 +1,55 @@
+// mm_launch.cuh -- template dispatch of lut_mm_kernel instantiations for one table
+// representation (included once per representation .cu so they compile in parallel).
+#pragma once
+#include "mm_launch.h"
+
+namespace axq {
+
+template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI>
+int launch_one(const MMArgs& p, dim3 grid, cudaStream_t st) {
+    auto kern = lut_mm_kernel<REPR, TN, R, WARPS, LOADER, EPI>;
+    int smem = (REPR == REPR_I32 ? 0 : p.table_bytes) + 2 * (KC / 4) * TN * 4;
+    static unsigned configured = 0;  // bit per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(configured & (1u << (dev & 31)))) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        configured |= 1u << (dev & 31);
+    }
+    kern<<<grid, WARPS * 32, smem, st>>>(p);
+    return (int)cudaGetLastError();
+}
+
+// Byte-wise loaders (unaligned / tiny C) and the int32 table use only the SMALL tile.
+template <int REPR, int LOADER, int EPI>
+int launch_cfg(const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st) {
+    constexpr bool big_ok = (REPR != REPR_I32) && (LOADER == LOAD_GEMM || LOADER == LOAD_CONV);
+    if constexpr (big_ok) {
+        if (c.warps == CFG_BIG.warps && c.R == CFG_BIG.R)
+            return launch_one<REPR, CFG_BIG.tn, CFG_BIG.R, CFG_BIG.warps, LOADER, EPI>(p, grid, st);
+    }
+    return launch_one<REPR, CFG_SMALL.tn, CFG_SMALL.R, CFG_SMALL.warps, LOADER, EPI>(p, grid, st);
+}
+
+template <int REPR, int EPI>
+int launch_loader(int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st) {
+    switch (loader) {
+        case LOAD_GEMM: return launch_cfg<REPR, LOAD_GEMM, EPI>(p, c, grid, st);
+        case LOAD_GEMM_BYTES: return launch_cfg<REPR, LOAD_GEMM_BYTES, EPI>(p, c, grid, st);
+        case LOAD_CONV: return launch_cfg<REPR, LOAD_CONV, EPI>(p, c, grid, st);
+        default: return launch_cfg<REPR, LOAD_CONV_BYTES, EPI>(p, c, grid, st);
+    }
+}
+
+template <int REPR>
+int launch_mm_repr(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st) {
+    switch (epi) {
+        case EPI_RAW: return launch_loader<REPR, EPI_RAW>(loader, p, c, grid, st);
+        case EPI_RAW_ATOMIC: return launch_loader<REPR, EPI_RAW_ATOMIC>(loader, p, c, grid, st);
+        case EPI_DQ_ROWS: return launch_loader<REPR, EPI_DQ_ROWS>(loader, p, c, grid, st);
+        default: return launch_loader<REPR, EPI_DQ_NCHW>(loader, p, c, grid, st);
+    }
+}
+
+}  // namespace axq

@@ -1,0 +1,151 @@
+// quant_kernels.cuh -- amax / scale / quantize / dequantize kernels (sm_100a).
+//
+// The quantizer is the paper's affine map "real_value = A x quantized_value + B" with
+// B = 0 (§III.A) and a per-tensor max-calibrated scale (BASELINE.json
+// north_star; A5/A6).  Every fp32 step is pinned with explicit round-to-nearest
+// intrinsics so that the integer codes are bit-identical to the CPU oracle (A1, A3, A14):
+//   scale      s = __fdiv_rn(amax, qmax)                (amax == 0 -> 1, A4)
+//   quantize   q = __float2int_rn(clamp(__fdiv_rn(x, s)))  (half-to-even, A1)
+//   dequant    y = __fadd_rn(__fmul_rn(__int2float_rn(acc), __fmul_rn(sa, sw)), bias)
+// All of these are HBM-bound streaming kernels; grids are sized in multiples of the SM
+// count and use 16-byte vector accesses where the layout allows.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace axq {
+
+__device__ __forceinline__ float qmax_of(int bits) { return (float)((1 << (bits - 1)) - 1); }
+
+__device__ __forceinline__ int8_t quantize_one(float x, float s, float qmax) {
+    float t = __fdiv_rn(x, s);
+    t = fminf(fmaxf(t, -qmax), qmax);
+    return (int8_t)__float2int_rn(t);
+}
+
+__device__ __forceinline__ float dequant_one(int32_t acc, float sc, float b) {
+    return __fadd_rn(__fmul_rn(__int2float_rn(acc), sc), b);
+}
+
+// ---- amax: max |x| (exact).  |x| >= 0 so the IEEE bit pattern orders like an unsigned int,
+// which lets one atomicMax per block combine block maxima. ----
+__global__ void amax_kernel(const float* __restrict__ x, int64_t n, unsigned int* out) {
+    float m = 0.f;
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    int64_t n4 = vec ? n / 4 : 0;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t i = tid; i < n4; i += stride) {
+        float4 v = __ldcs(x4 + i);
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (int64_t i = n4 * 4 + tid; i < n; i += stride) m = fmaxf(m, fabsf(x[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float wm[32];
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wm[wid] = m;
+    __syncthreads();
+    if (wid == 0) {
+        m = lane < (int)(blockDim.x >> 5) ? wm[lane] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) atomicMax(out, __float_as_uint(m));
+    }
+}
+
+__global__ void scale_kernel(const float* d_amax, int bits, float* d_scale) {
+    float a = *d_amax;
+    *d_scale = (a == 0.f) ? 1.0f : __fdiv_rn(a, qmax_of(bits));
+}
+
+// ---- quantize, layout preserving ----
+__global__ void quantize_kernel(const float* __restrict__ x, int64_t n,
+                                const float* __restrict__ d_scale, int bits,
+                                int8_t* __restrict__ q) {
+    const float s = *d_scale, qm = qmax_of(bits);
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+               ((reinterpret_cast<uintptr_t>(q) & 3) == 0);
+    int64_t n4 = vec ? n / 4 : 0;
+    for (int64_t i = tid; i < n4; i += stride) {
+        float4 v = __ldcs(reinterpret_cast<const float4*>(x) + i);
+        uint32_t w = (uint32_t)(uint8_t)quantize_one(v.x, s, qm) |
+                     ((uint32_t)(uint8_t)quantize_one(v.y, s, qm) << 8) |
+                     ((uint32_t)(uint8_t)quantize_one(v.z, s, qm) << 16) |
+                     ((uint32_t)(uint8_t)quantize_one(v.w, s, qm) << 24);
+        reinterpret_cast<uint32_t*>(q)[i] = w;
+    }
+    for (int64_t i = n4 * 4 + tid; i < n; i += stride) q[i] = quantize_one(x[i], s, qm);
+}
+
+// ---- quantize NCHW fp32 -> NHWC int8, tiled transpose through shared memory.
+// Block = (image, 32 consecutive hw positions, 32 consecutive channels): reads are
+// 128-byte rows along hw, writes are 32-byte rows along c. ----
+__global__ void quantize_nchw_to_nhwc_kernel(const float* __restrict__ x, int64_t C,
+                                             int64_t HW, const float* __restrict__ d_scale,
+                                             int bits, int8_t* __restrict__ q) {
+    __shared__ int8_t tile[32][33];
+    const float s = *d_scale, qm = qmax_of(bits);
+    int64_t img = blockIdx.z;
+    int64_t hw0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    const float* xi = x + img * C * HW;
+    for (int cc = ty; cc < 32; cc += 8) {
+        int64_t c = c0 + cc, hw = hw0 + tx;
+        if (c < C && hw < HW) tile[cc][tx] = quantize_one(__ldcs(xi + c * HW + hw), s, qm);
+    }
+    __syncthreads();
+    int8_t* qi = q + img * HW * C;
+    for (int hh = ty; hh < 32; hh += 8) {
+        int64_t hw = hw0 + hh, c = c0 + tx;
+        if (c < C && hw < HW) qi[hw * C + c] = tile[tx][hh];
+    }
+}
+
+// ---- dequantize [M][ldacc] int32 -> [M][ldy] fp32 with bias[n] ----
+__global__ void dequant_rows_kernel(int64_t M, int64_t N, const int32_t* __restrict__ acc,
+                                    int64_t ldacc, const float* __restrict__ sa,
+                                    const float* __restrict__ sw, const float* __restrict__ bias,
+                                    float* __restrict__ y, int64_t ldy) {
+    const float sc = __fmul_rn(*sa, *sw);
+    int64_t total = M * N;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+        int64_t m = i / N, n = i - m * N;
+        float b = bias ? bias[n] : 0.f;
+        float v = __fmul_rn(__int2float_rn(acc[m * ldacc + n]), sc);
+        y[m * ldy + n] = bias ? __fadd_rn(v, b) : v;
+    }
+}
+
+// ---- dequantize NHWC int32 [N][HW][C] -> NCHW fp32 [N][C][HW] (tiled transpose) ----
+__global__ void dequant_nhwc_to_nchw_kernel(const int32_t* __restrict__ acc, int64_t HW,
+                                            int64_t C, const float* __restrict__ sa,
+                                            const float* __restrict__ sw,
+                                            const float* __restrict__ bias,
+                                            float* __restrict__ y) {
+    __shared__ float tile[32][33];
+    const float sc = __fmul_rn(*sa, *sw);
+    int64_t img = blockIdx.z;
+    int64_t hw0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    int tx = threadIdx.x, ty = threadIdx.y;
+    const int32_t* ai = acc + img * HW * C;
+    for (int hh = ty; hh < 32; hh += 8) {
+        int64_t hw = hw0 + hh, c = c0 + tx;
+        if (c < C && hw < HW) {
+            float v = __fmul_rn(__int2float_rn(ai[hw * C + c]), sc);
+            tile[hh][tx] = bias ? __fadd_rn(v, bias[c]) : v;
+        }
+    }
+    __syncthreads();
+    float* yi = y + img * C * HW;
+    for (int cc = ty; cc < 32; cc += 8) {
+        int64_t c = c0 + cc, hw = hw0 + tx;
+        if (c < C && hw < HW) yi[c * HW + hw] = tile[tx][cc];
+    }
+}
+
+}  // namespace axq

@@ -1,0 +1,109 @@
+"""Approximate layers built from the C ABI (the "approximate layer library" of PAPER.md:113-141,
+§III.B, reduced to what the hot path needs).  Each forward runs the §8(a) steps in order --
+amax -> scale -> quantize -> LUT-GEMM/conv -> dequantize(+bias) -- every one of them a
+libaxq kernel on the caller's stream; torch only allocates device memory.
+
+Weight preparation (amax_w, scale_w, quantize, relayout) happens once at construction and is
+not part of a timed step (the paper calibrates offline).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib as ax
+
+
+class ApproxLinear:
+    """y = x W^T + b with every multiply a LUT lookup."""
+
+    def __init__(self, weight: torch.Tensor, bias: torch.Tensor | None, lut: ax.Lut,
+                 device="cuda"):
+        self.lut = lut
+        self.bits = lut.bits
+        w = weight.to(device=device, dtype=torch.float32).contiguous()
+        self.N, self.K = w.shape
+        self.d_amax_w = torch.empty(1, device=device)
+        self.d_scale_w = torch.empty(1, device=device)
+        self.qw = torch.empty(self.N, self.K, dtype=torch.int8, device=device)
+        ax.axq_amax(w, self.d_amax_w)
+        ax.axq_scale(self.d_amax_w, self.bits, self.d_scale_w)
+        ax.axq_quantize(w, self.d_scale_w, self.bits, self.qw)
+        self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
+        self.d_amax_a = torch.empty(1, device=device)
+        self.d_scale_a = torch.empty(1, device=device)
+        self._bufs = {}
+
+    def buffers(self, M: int, device):
+        b = self._bufs.get(M)
+        if b is None:
+            b = dict(qa=torch.empty(M, self.K, dtype=torch.int8, device=device),
+                     ws=torch.empty(M, self.N, dtype=torch.int32, device=device))
+            self._bufs[M] = b
+        return b
+
+    def forward(self, x: torch.Tensor, y: torch.Tensor | None = None, d_scale_a=None):
+        """x fp32 [M][K] -> y fp32 [M][N].  With d_scale_a given (static calibration), the
+        amax/scale steps are skipped."""
+        M = x.shape[0]
+        b = self.buffers(M, x.device)
+        if y is None:
+            y = torch.empty(M, self.N, dtype=torch.float32, device=x.device)
+        if d_scale_a is None:
+            ax.axq_amax(x, self.d_amax_a)
+            ax.axq_scale(self.d_amax_a, self.bits, self.d_scale_a)
+            d_scale_a = self.d_scale_a
+        ax.axq_quantize(x, d_scale_a, self.bits, b["qa"])
+        ax.axq_lut_gemm_dq(b["qa"], self.qw, self.lut, d_scale_a, self.d_scale_w, self.bias, y,
+                           workspace=b["ws"])
+        return y
+
+    __call__ = forward
+
+
+class ApproxConv2d:
+    """Conv2d with every multiply a LUT lookup; NCHW fp32 in/out, implicit im2col."""
+
+    def __init__(self, weight: torch.Tensor, bias: torch.Tensor | None, lut: ax.Lut,
+                 stride=(1, 1), padding=(0, 0), device="cuda"):
+        self.lut = lut
+        self.bits = lut.bits
+        w = weight.to(device=device, dtype=torch.float32).contiguous()   # [K][C][R][S]
+        self.Kout, self.C, self.R, self.S = w.shape
+        self.stride, self.padding = tuple(stride), tuple(padding)
+        self.d_amax_w = torch.empty(1, device=device)
+        self.d_scale_w = torch.empty(1, device=device)
+        q = torch.empty(w.shape, dtype=torch.int8, device=device)
+        ax.axq_amax(w, self.d_amax_w)
+        ax.axq_scale(self.d_amax_w, self.bits, self.d_scale_w)
+        ax.axq_quantize(w, self.d_scale_w, self.bits, q)
+        self.qw_kcrs = q
+        self.qw = q.permute(0, 2, 3, 1).contiguous()                      # KRSC relayout
+        self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
+        self.d_amax_a = torch.empty(1, device=device)
+        self.d_scale_a = torch.empty(1, device=device)
+        self._bufs = {}
+
+    def desc(self, N, H, W):
+        return ax.conv_desc(N, H, W, self.C, self.Kout, self.R, self.S, self.stride, self.padding)
+
+    def forward(self, x: torch.Tensor, y: torch.Tensor | None = None, d_scale_a=None):
+        N, C, H, W = x.shape
+        d = self.desc(N, H, W)
+        Ho, Wo = ax.axq_conv2d_out_hw(d)
+        key = (N, H, W)
+        b = self._bufs.get(key)
+        if b is None:
+            b = dict(qx=torch.empty(N, H, W, C, dtype=torch.int8, device=x.device))
+            self._bufs[key] = b
+        if y is None:
+            y = torch.empty(N, self.Kout, Ho, Wo, dtype=torch.float32, device=x.device)
+        if d_scale_a is None:
+            ax.axq_amax(x, self.d_amax_a)
+            ax.axq_scale(self.d_amax_a, self.bits, self.d_scale_a)
+            d_scale_a = self.d_scale_a
+        ax.axq_quantize_nchw_to_nhwc(x, d_scale_a, self.bits, b["qx"])
+        ax.axq_lut_conv2d_dq(d, b["qx"], self.qw, self.lut, d_scale_a, self.d_scale_w, self.bias, y)
+        return y
+
+    __call__ = forward
