@@ -82,7 +82,12 @@ axq_status launch_mm(int epi, int loader, int repr, const axq::MMArgs& p, const 
     return AXQ_OK;
 }
 
-Cfg pick_cfg(int64_t M) { return M <= 2048 ? CFG_SMALL : CFG_BIG; }
+// Must agree with mm_launch.cuh::launch_cfg: byte-wise loaders and the int32 table only
+// have the SMALL tile instantiated.
+Cfg pick_cfg(int64_t M, int loader, int repr) {
+    const bool big_ok = repr != AXQ_LUT_I32 && (loader == axq::LOAD_GEMM || loader == axq::LOAD_CONV);
+    return (M > 2048 && big_ok) ? CFG_BIG : CFG_SMALL;
+}
 
 // K-splitting so that small M*N problems still fill the SMs (exact: integer atomics).
 int64_t pick_k_split(int64_t M, int64_t N, int64_t K, const Cfg& c, bool allow) {
@@ -291,12 +296,12 @@ axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_
     p.A = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = K;
     fill_common(p, lut);
     p.C_out = C; p.ldc = ldc;
-    Cfg c = pick_cfg(M);
+    int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
+    Cfg c = pick_cfg(M, loader, lut->repr);
     p.k_split = pick_k_split(M, N, K, c, true);
     int64_t splits = (K + p.k_split - 1) / p.k_split;
     int64_t bm = (int64_t)c.warps * 32 * c.R;
     dim3 grid((unsigned)((M + bm - 1) / bm), (unsigned)((N + c.tn - 1) / c.tn), (unsigned)splits);
-    int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
     int epi = axq::EPI_RAW;
     if (splits > 1) {
         cudaError_t e = cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, S(stream));
@@ -318,12 +323,12 @@ axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int
     p.A = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = std::max<int64_t>(K, 0);
     fill_common(p, lut);
     p.sa = ep->d_scale_a; p.sw_ = ep->d_scale_w; p.bias = ep->bias; p.y = ep->y; p.ldy = ep->ldy;
-    Cfg c = pick_cfg(M);
+    int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
+    Cfg c = pick_cfg(M, loader, lut->repr);
     p.k_split = pick_k_split(M, N, K, c, ep->workspace != nullptr);
     int64_t splits = K > 0 ? (K + p.k_split - 1) / p.k_split : 1;
     int64_t bm = (int64_t)c.warps * 32 * c.R;
     dim3 grid((unsigned)((M + bm - 1) / bm), (unsigned)((N + c.tn - 1) / c.tn), (unsigned)splits);
-    int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
     if (splits > 1) {
         p.C_out = ep->workspace; p.ldc = N;
         cudaError_t e = cudaMemsetAsync(ep->workspace, 0, (size_t)M * N * 4, S(stream));
@@ -385,7 +390,7 @@ axq_status axq_lut_conv2d(const axq_conv_desc* d, const int8_t* X, const int8_t*
     if (p.M == 0 || p.N == 0) return AXQ_OK;
     if (!Y) return AXQ_ERR_INVALID;
     p.C_out = Y; p.ldc = p.N;
-    Cfg c = pick_cfg(p.M);
+    Cfg c = pick_cfg(p.M, loader, lut->repr);
     p.k_split = pick_k_split(p.M, p.N, p.K, c, true);
     int64_t splits = (p.K + p.k_split - 1) / p.k_split;
     int64_t bm = (int64_t)c.warps * 32 * c.R;
@@ -409,7 +414,7 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
     if (p.M == 0 || p.N == 0) return AXQ_OK;
     if (!ep->y) return AXQ_ERR_INVALID;
     p.sa = ep->d_scale_a; p.sw_ = ep->d_scale_w; p.bias = ep->bias; p.y = ep->y;
-    Cfg c = pick_cfg(p.M);
+    Cfg c = pick_cfg(p.M, loader, lut->repr);
     p.k_split = pick_k_split(p.M, p.N, p.K, c, ep->workspace != nullptr);
     int64_t splits = (p.K + p.k_split - 1) / p.k_split;
     int64_t bm = (int64_t)c.warps * 32 * c.R;
