@@ -149,3 +149,74 @@ def random_lut(seed: int, bits: int) -> np.ndarray:
     lim = 1 << (2 * bits - 2)
     return np.random.default_rng(seed).integers(-lim, lim, size=1 << (2 * bits), endpoint=True,
                                                 dtype=np.int64).astype(np.int32)
+
+
+# --------------------------------------------------------------------------------------
+# configs[3]: ResNet-50-shaped forward (weights are requested by each side with its own
+# layer enumeration; tensor_index 0 = images, 1.. = weights in forward order, A16)
+# --------------------------------------------------------------------------------------
+
+def config3_images(batch: int = 256, start: int = 0) -> np.ndarray:
+    """x ~ N(0,1) [256,3,224,224] fp32 (rows start..start+batch of the seeded batch)."""
+    x = normal(3, 0, (256, 3, 224, 224))
+    return np.ascontiguousarray(x[start:start + batch])
+
+
+def kaiming_conv(config: int, idx: int, cout: int, cin: int, r: int, s: int) -> np.ndarray:
+    """Kaiming-normal, fan_out mode: std = sqrt(2 / (Cout*R*S)) (A16)."""
+    return normal(config, idx, (cout, cin, r, s), math.sqrt(2.0 / (cout * r * s)))
+
+
+def kaiming_fc(config: int, idx: int, out_f: int, in_f: int) -> np.ndarray:
+    """Kaiming-normal, fan_in mode: std = sqrt(2 / in) (A16)."""
+    return normal(config, idx, (out_f, in_f), math.sqrt(2.0 / in_f))
+
+
+def fc_bias(config: int, idx: int, out_f: int, in_f: int) -> np.ndarray:
+    b = 1.0 / math.sqrt(in_f)
+    return uniform(config, idx, (out_f,), -b, b)
+
+
+# --------------------------------------------------------------------------------------
+# configs[4]: LSTM (input 512, hidden 1024, seq 128, batch 64)
+# --------------------------------------------------------------------------------------
+
+@dataclass
+class LstmCase:
+    x: np.ndarray       # fp32 [T][B][I]
+    W_ih: np.ndarray    # fp32 [4H][I]  gate order i, f, g, o
+    W_hh: np.ndarray    # fp32 [4H][H]
+    b_ih: np.ndarray
+    b_hh: np.ndarray
+    luts: dict          # bits -> int32 table
+
+
+def config4(T: int = 128, B: int = 64, I: int = 512, H: int = 1024) -> LstmCase:
+    s = 1.0 / 32.0
+    x = normal(4, 0, (128, 64, 512))[:T, :B, :I]
+    W_ih = uniform(4, 1, (4096, 512), -s, s)
+    W_hh = uniform(4, 2, (4096, 1024), -s, s)
+    b_ih = uniform(4, 3, (4096,), -s, s)
+    b_hh = uniform(4, 4, (4096,), -s, s)
+    if (I, H) != (512, 1024):   # reduced parity cases: sub-blocks of the same draws
+        rows = np.concatenate([np.arange(g * 1024, g * 1024 + H) for g in range(4)])
+        W_ih, W_hh = W_ih[rows][:, :I], W_hh[rows][:, :H]
+        b_ih, b_hh = b_ih[rows], b_hh[rows]
+    luts = {b: lut_randerr(b, 4, 10 + b) for b in (4, 6, 8)}
+    return LstmCase(x=np.ascontiguousarray(x), W_ih=np.ascontiguousarray(W_ih),
+                    W_hh=np.ascontiguousarray(W_hh), b_ih=np.ascontiguousarray(b_ih),
+                    b_hh=np.ascontiguousarray(b_hh), luts=luts)
+
+
+def network_weights(specs, config: int = 3) -> dict:
+    """Weights for a layer list given as (name, kind, cout, cin, k, ...) tuples in forward
+    order: tensor_index = position + 1; the fc bias takes the index after the fc weight."""
+    W = {}
+    for i, sp in enumerate(specs):
+        name, kind, cout, cin, k = sp[:5]
+        if kind == "conv":
+            W[name] = kaiming_conv(config, i + 1, cout, cin, k, k)
+        else:
+            W[name] = kaiming_fc(config, i + 1, cout, cin)
+            W[name + ".b"] = fc_bias(config, i + 2, cout, cin)
+    return W

@@ -84,16 +84,17 @@ axq_status axq_lut_info(axq_lut_t lut, int* bits, int* repr, int32_t* tmin, int3
  * axq_quantize: q_i = clamp(rint(fl32(x_i / *d_scale)), -(2^(b-1)-1), 2^(b-1)-1), rint =
  *   round half to even (A1), symmetric clamp (A2), IEEE division (A3).  q is int8 holding
  *   the sign-extended b-bit code.  Layout-preserving.
- * axq_quantize_nchw_to_nhwc: the same map on an fp32 NCHW tensor, writing int8 NHWC (the
- *   layout axq_lut_conv2d reads).
+ * axq_quantize_nchw_to_nhwc: the same map on an fp32 NCHW tensor [N][C][H][W], writing int8
+ *   NHWC [N][H][W][Cq] (the layout axq_lut_conv2d reads); Cq >= C, channels C..Cq-1 are
+ *   written as 0 (storage padding, see axq_conv_desc.c_valid).
  * ------------------------------------------------------------------------------- */
 axq_status axq_amax(const float* x, int64_t n, float* d_amax, void* stream);
 axq_status axq_scale(const float* d_amax, int bits, float* d_scale, void* stream);
 axq_status axq_quantize(const float* x, int64_t n, const float* d_scale, int bits,
                         int8_t* q, void* stream);
 axq_status axq_quantize_nchw_to_nhwc(const float* x, int64_t N, int64_t C, int64_t H,
-                                     int64_t W, const float* d_scale, int bits, int8_t* q,
-                                     void* stream);
+                                     int64_t W, int64_t Cq, const float* d_scale, int bits,
+                                     int8_t* q, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * LUT-GEMM.  Linear layer y = x A^T + b (§III.B.3) with "the inner
@@ -111,18 +112,34 @@ axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_
                         const int8_t* W, int64_t ldw, axq_lut_t lut, int32_t* C, int64_t ldc,
                         void* stream);
 
-/* Fused dequantize epilogue (P:74 with both operands' scales; "+ b"):
- *     y = fl(fl((float)acc * fl(*d_scale_a * *d_scale_w)) + bias[n])      (A14)
- * bias may be NULL.  workspace: NULL, or device int32 scratch of M*N elements that lets
- * the library split K across CTAs when M*N alone cannot fill the GPU (results identical).
- */
+/* Fused dequantize epilogue (P:74 with both operands' scales; "+ b"), applied per
+ * output element in this pinned fp32 order (A13/A14/A17):
+ *     v = fl(fl((float)acc) * fl(*d_scale_a * *d_scale_w))
+ *     v = fl(v + bias[n])            if bias
+ *     v = fl(v + residual[m][n])     if residual   (row / NHWC layout, stride ldr)
+ *     v = max(v, 0)                  if relu
+ *     y = v                          if y
+ *     q_out[m][n] = clamp(rint(fl(v / *d_scale_out)))   if q_out  (requantize for the next
+ *                                    layer with bits_out, same rule as axq_quantize)
+ * Zero-initialise the struct and set what is needed.  workspace: NULL, or device int32
+ * scratch of M*N elements that lets the library split K across CTAs when M*N alone cannot
+ * fill the GPU (results identical).  Layout of y: GEMM -> [M][ldy]; conv -> NCHW unless
+ * y_nhwc = 1 ([N*Ho*Wo][ldy]).  q_out is always [M][ldq] (conv: NHWC). */
 typedef struct axq_epilogue {
-    const float* d_scale_a; /* device fp32 scalar: activation scale */
-    const float* d_scale_w; /* device fp32 scalar: weight scale */
-    const float* bias;      /* device fp32 [N] or NULL */
-    float* y;               /* device fp32 output */
-    int64_t ldy;            /* GEMM: row stride of y ([M][ldy], ldy >= N); conv: ignored */
-    int32_t* workspace;     /* device int32 [M*N] or NULL */
+    const float* d_scale_a;   /* device fp32 scalar: activation scale (required) */
+    const float* d_scale_w;   /* device fp32 scalar: weight scale (required) */
+    const float* bias;        /* device fp32 [N] or NULL */
+    float* y;                 /* device fp32 output or NULL */
+    int64_t ldy;              /* row stride of y (GEMM, or conv with y_nhwc) */
+    int32_t* workspace;       /* device int32 [M*N] or NULL */
+    const float* residual;    /* device fp32 [M][ldr] or NULL */
+    int64_t ldr;
+    int32_t relu;             /* nonzero: ReLU after the residual add */
+    int32_t y_nhwc;           /* conv only: 1 -> y is NHWC [M][ldy] */
+    int8_t* q_out;            /* device int8 [M][ldq] requantized output or NULL */
+    int64_t ldq;
+    const float* d_scale_out; /* device fp32 scalar, required with q_out */
+    int32_t bits_out;         /* 2..8, required with q_out */
 } axq_epilogue;
 
 axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
@@ -140,9 +157,12 @@ axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int
  * [N][H_out][W_out][C_out].  groups must be 1 (others: AXQ_ERR_UNSUPPORTED).
  * ------------------------------------------------------------------------------- */
 typedef struct axq_conv_desc {
-    int64_t N, H, W, C;       /* input */
+    int64_t N, H, W, C;       /* input (C = channels as stored, i.e. the NHWC row length) */
     int64_t K, R, S;          /* output channels, filter height / width */
     int64_t stride_h, stride_w, pad_h, pad_w, dil_h, dil_w, groups;
+    int64_t c_valid;          /* 0, or the number of real channels (< C): channels >= c_valid
+                                 are STORAGE padding holding a = 0 and w = 0; their lookups
+                                 are removed exactly (they are not the paper's padding) */
 } axq_conv_desc;
 
 axq_status axq_conv2d_out_hw(const axq_conv_desc* d, int64_t* Ho, int64_t* Wo);
@@ -156,6 +176,8 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
  * Dequantize (unfused), same pinned formula as the epilogue.
  * axq_dequantize: acc int32 [M][ldacc] -> y fp32 [M][ldy], bias[n] (nullable).
  * axq_dequantize_nhwc_to_nchw: acc int32 NHWC [N][HW][C] -> y fp32 NCHW [N][C][HW].
+ * axq_epilogue_apply: the full axq_epilogue on an int32 [M][ldacc] accumulator (y in row
+ *   layout [M][ldy]).
  * ------------------------------------------------------------------------------- */
 axq_status axq_dequantize(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
                           const float* d_scale_a, const float* d_scale_w, const float* bias,
@@ -163,6 +185,38 @@ axq_status axq_dequantize(int64_t M, int64_t N, const int32_t* acc, int64_t ldac
 axq_status axq_dequantize_nhwc_to_nchw(int64_t N, int64_t HW, int64_t C, const int32_t* acc,
                                        const float* d_scale_a, const float* d_scale_w,
                                        const float* bias, float* y, void* stream);
+axq_status axq_epilogue_apply(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
+                              const axq_epilogue* ep, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Model glue for the ResNet-50-shaped forward (BASELINE.json configs[3]; A16/A17).
+ * axq_maxpool2d_nhwc_i8: max pooling on int8 codes NHWC [N][H][W][C] -> [N][Ho][Wo][C],
+ *   window R x S, stride, padding; out-of-image taps are ignored (-inf padding).  Pooling
+ *   codes equals quantizing the pooled fp32 values because quantization is monotone
+ *   (A17).
+ * axq_avgpool_nhwc: global average pool fp32 NHWC [N][HW][C] -> y fp32 [N][C]: a sequential
+ *   fp32 sum over hw = 0..HW-1, then one IEEE division by (float)HW (A17).  If q is given,
+ *   also writes q = quantize(y) with *d_scale / bits (int8 [N][C]).
+ * ------------------------------------------------------------------------------- */
+axq_status axq_maxpool2d_nhwc_i8(const int8_t* x, int64_t N, int64_t H, int64_t W, int64_t C,
+                                 int64_t R, int64_t S, int64_t stride, int64_t pad, int8_t* y,
+                                 void* stream);
+axq_status axq_avgpool_nhwc(const float* x, int64_t N, int64_t HW, int64_t C, float* y,
+                            int8_t* q, const float* d_scale, int bits, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * LSTM cell (BASELINE.json configs[4]; "mathematically equivalent with the vanilla
+ * Pytorch RNN layer", gates i, f, g, o; A18).  For b in [0,B), j in [0,Hd):
+ *   gate_x = fl(gates_ih[b][x*Hd + j] + gates_hh[b][x*Hd + j])   x = i, f, g, o
+ *   i = sigma(gate_i), f = sigma(gate_f), g = tanh(gate_g), o = sigma(gate_o)
+ *   c[b][j] = fl(fl(f*c) + fl(i*g));  h = fl(o * tanh(c))
+ * with the pinned fp32 exp of A18 inside sigma / tanh.  gates_* are fp32 [B][4*Hd] (bias
+ * already added by the GEMM epilogues).  c is updated in place; h is written to h_out
+ * [B][Hd] (fp32) and, if q_h is given, quantized with *d_scale_h / bits into q_h [B][Hd].
+ * ------------------------------------------------------------------------------- */
+axq_status axq_lstm_cell(int64_t B, int64_t Hd, const float* gates_ih, const float* gates_hh,
+                         float* c, float* h_out, int8_t* q_h, const float* d_scale_h, int bits,
+                         void* stream);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,8 @@ EXPORTED = [
     "axq_amax", "axq_scale", "axq_quantize", "axq_quantize_nchw_to_nhwc",
     "axq_lut_gemm", "axq_lut_gemm_dq",
     "axq_conv2d_out_hw", "axq_lut_conv2d", "axq_lut_conv2d_dq",
-    "axq_dequantize", "axq_dequantize_nhwc_to_nchw",
+    "axq_dequantize", "axq_dequantize_nhwc_to_nchw", "axq_epilogue_apply",
+    "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
 ]
 
 
@@ -37,13 +38,16 @@ class AxqError(RuntimeError):
 class axq_epilogue(ctypes.Structure):
     _fields_ = [("d_scale_a", ctypes.c_void_p), ("d_scale_w", ctypes.c_void_p),
                 ("bias", ctypes.c_void_p), ("y", ctypes.c_void_p), ("ldy", ctypes.c_int64),
-                ("workspace", ctypes.c_void_p)]
+                ("workspace", ctypes.c_void_p), ("residual", ctypes.c_void_p),
+                ("ldr", ctypes.c_int64), ("relu", ctypes.c_int32), ("y_nhwc", ctypes.c_int32),
+                ("q_out", ctypes.c_void_p), ("ldq", ctypes.c_int64),
+                ("d_scale_out", ctypes.c_void_p), ("bits_out", ctypes.c_int32)]
 
 
 class axq_conv_desc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("N", "H", "W", "C", "K", "R", "S", "stride_h", "stride_w", "pad_h", "pad_w",
-                 "dil_h", "dil_w", "groups")]
+                 "dil_h", "dil_w", "groups", "c_valid")]
 
 
 _lib = None
@@ -70,7 +74,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_amax": ([vp, i64, vp, vp], i32),
         "axq_scale": ([vp, i32, vp, vp], i32),
         "axq_quantize": ([vp, i64, vp, i32, vp, vp], i32),
-        "axq_quantize_nchw_to_nhwc": ([vp, i64, i64, i64, i64, vp, i32, vp, vp], i32),
+        "axq_quantize_nchw_to_nhwc": ([vp, i64, i64, i64, i64, i64, vp, i32, vp, vp], i32),
         "axq_lut_gemm": ([i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, vp], i32),
         "axq_lut_gemm_dq": ([i64, i64, i64, vp, i64, vp, i64, vp,
                              ctypes.POINTER(axq_epilogue), vp], i32),
@@ -81,6 +85,10 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
                                ctypes.POINTER(axq_epilogue), vp], i32),
         "axq_dequantize": ([i64, i64, vp, i64, vp, vp, vp, vp, i64, vp], i32),
         "axq_dequantize_nhwc_to_nchw": ([i64, i64, i64, vp, vp, vp, vp, vp, vp], i32),
+        "axq_epilogue_apply": ([i64, i64, vp, i64, ctypes.POINTER(axq_epilogue), vp], i32),
+        "axq_maxpool2d_nhwc_i8": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp], i32),
+        "axq_avgpool_nhwc": ([vp, i64, i64, i64, vp, vp, vp, i32, vp], i32),
+        "axq_lstm_cell": ([i64, i64, vp, vp, vp, vp, vp, vp, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -172,11 +180,12 @@ def axq_quantize(x, d_scale, bits: int, q, stream=None) -> None:
 
 
 def axq_quantize_nchw_to_nhwc(x, d_scale, bits: int, q, stream=None) -> None:
+    """x fp32 [N][C][H][W] -> q int8 [N][H][W][Cq] (Cq = q.shape[-1] >= C, pad channels 0)."""
     assert x.is_contiguous() and q.is_contiguous() and x.dim() == 4
     N, C, H, W = x.shape
     _check("axq_quantize_nchw_to_nhwc",
-           load().axq_quantize_nchw_to_nhwc(_ptr(x), N, C, H, W, _ptr(d_scale), int(bits),
-                                            _ptr(q), _stream(stream)))
+           load().axq_quantize_nchw_to_nhwc(_ptr(x), N, C, H, W, q.shape[-1], _ptr(d_scale),
+                                            int(bits), _ptr(q), _stream(stream)))
 
 
 # ---------------------------------------------------------------------------------------
@@ -191,9 +200,17 @@ def axq_lut_gemm(A, W, lut: Lut, C, stream=None) -> None:
                                                _stream(stream)))
 
 
-def _epilogue(d_scale_a, d_scale_w, bias, y, ldy, workspace):
+def make_epilogue(d_scale_a, d_scale_w, bias=None, y=None, ldy=0, workspace=None,
+                  residual=None, ldr=0, relu=False, y_nhwc=False, q_out=None, ldq=0,
+                  d_scale_out=None, bits_out=0) -> axq_epilogue:
     return axq_epilogue(_ptr(d_scale_a), _ptr(d_scale_w), _ptr(bias), _ptr(y), int(ldy),
-                        _ptr(workspace))
+                        _ptr(workspace), _ptr(residual), int(ldr), int(bool(relu)),
+                        int(bool(y_nhwc)), _ptr(q_out), int(ldq), _ptr(d_scale_out),
+                        int(bits_out))
+
+
+def _epilogue(d_scale_a, d_scale_w, bias, y, ldy, workspace):
+    return make_epilogue(d_scale_a, d_scale_w, bias, y, ldy, workspace)
 
 
 def axq_lut_gemm_dq(A, W, lut: Lut, d_scale_a, d_scale_w, bias, y, workspace=None,
@@ -206,9 +223,10 @@ def axq_lut_gemm_dq(A, W, lut: Lut, d_scale_a, d_scale_w, bias, y, workspace=Non
                                                      _stream(stream)))
 
 
-def conv_desc(N, H, W, C, K, R, S, stride=(1, 1), pad=(0, 0), dil=(1, 1), groups=1):
+def conv_desc(N, H, W, C, K, R, S, stride=(1, 1), pad=(0, 0), dil=(1, 1), groups=1,
+              c_valid=0):
     return axq_conv_desc(N, H, W, C, K, R, S, stride[0], stride[1], pad[0], pad[1], dil[0],
-                         dil[1], groups)
+                         dil[1], groups, c_valid)
 
 
 def axq_conv2d_out_hw(desc: axq_conv_desc):
@@ -247,3 +265,47 @@ def axq_dequantize_nhwc_to_nchw(acc_nhwc, d_scale_a, d_scale_w, bias, y_nchw,
            load().axq_dequantize_nhwc_to_nchw(N, H * W, C, _ptr(acc_nhwc), _ptr(d_scale_a),
                                               _ptr(d_scale_w), _ptr(bias), _ptr(y_nchw),
                                               _stream(stream)))
+
+
+def axq_lut_gemm_ep(A, W, lut: Lut, ep: axq_epilogue, stream=None) -> None:
+    """axq_lut_gemm_dq with a caller-built epilogue (make_epilogue)."""
+    M, K = A.shape
+    N = W.shape[0]
+    _check("axq_lut_gemm_dq", load().axq_lut_gemm_dq(M, N, K, _ptr(A), A.stride(0), _ptr(W),
+                                                     W.stride(0), lut.handle, ctypes.byref(ep),
+                                                     _stream(stream)))
+
+
+def axq_lut_conv2d_ep(desc: axq_conv_desc, X_nhwc, W_krsc, lut: Lut, ep: axq_epilogue,
+                      stream=None) -> None:
+    _check("axq_lut_conv2d_dq", load().axq_lut_conv2d_dq(ctypes.byref(desc), _ptr(X_nhwc),
+                                                         _ptr(W_krsc), lut.handle,
+                                                         ctypes.byref(ep), _stream(stream)))
+
+
+def axq_epilogue_apply(acc, ep: axq_epilogue, stream=None) -> None:
+    M, N = acc.shape
+    _check("axq_epilogue_apply", load().axq_epilogue_apply(M, N, _ptr(acc), acc.stride(0),
+                                                           ctypes.byref(ep), _stream(stream)))
+
+
+def axq_maxpool2d_nhwc_i8(x, R, S, stride, pad, y, stream=None) -> None:
+    N, H, W, C = x.shape
+    _check("axq_maxpool2d_nhwc_i8", load().axq_maxpool2d_nhwc_i8(
+        _ptr(x), N, H, W, C, R, S, stride, pad, _ptr(y), _stream(stream)))
+
+
+def axq_avgpool_nhwc(x, y=None, q=None, d_scale=None, bits=8, stream=None) -> None:
+    """x fp32 [N][H][W][C] (or [N][HW][C]) -> y fp32 [N][C] and/or q int8 [N][C]."""
+    N, C = x.shape[0], x.shape[-1]
+    HW = x.numel() // (N * C) if N * C else 0
+    _check("axq_avgpool_nhwc", load().axq_avgpool_nhwc(_ptr(x), N, HW, C, _ptr(y), _ptr(q),
+                                                       _ptr(d_scale), int(bits), _stream(stream)))
+
+
+def axq_lstm_cell(gates_ih, gates_hh, c, h_out, q_h=None, d_scale_h=None, bits=8,
+                  stream=None) -> None:
+    B, H4 = gates_hh.shape
+    _check("axq_lstm_cell", load().axq_lstm_cell(B, H4 // 4, _ptr(gates_ih), _ptr(gates_hh),
+                                                 _ptr(c), _ptr(h_out), _ptr(q_h),
+                                                 _ptr(d_scale_h), int(bits), _stream(stream)))

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "mm_launch.h"
+#include "glue_kernels.cuh"
 #include "quant_kernels.cuh"
 
 struct axq_lut {
@@ -257,13 +258,20 @@ axq_status axq_quantize(const float* x, int64_t n, const float* d_scale, int bit
 }
 
 axq_status axq_quantize_nchw_to_nhwc(const float* x, int64_t N, int64_t C, int64_t H, int64_t W,
-                                     const float* d_scale, int bits, int8_t* q, void* stream) {
-    if (N < 0 || C < 0 || H < 0 || W < 0 || !d_scale || bits < 2 || bits > 8) return AXQ_ERR_INVALID;
-    if (N == 0 || C == 0 || H == 0 || W == 0) return AXQ_OK;
+                                     int64_t Cq, const float* d_scale, int bits, int8_t* q,
+                                     void* stream) {
+    if (N < 0 || C < 0 || H < 0 || W < 0 || Cq < C || !d_scale || bits < 2 || bits > 8)
+        return AXQ_ERR_INVALID;
+    if (N == 0 || Cq == 0 || H == 0 || W == 0) return AXQ_OK;
     if (!x || !q || N > 65535) return AXQ_ERR_INVALID;
-    int64_t HW = H * W;
-    dim3 grid((unsigned)((HW + 31) / 32), (unsigned)((C + 31) / 32), (unsigned)N);
-    axq::quantize_nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, S(stream)>>>(x, C, HW, d_scale, bits, q);
+    const int64_t HW = H * W;
+    if (Cq <= 16) {  // few channels (network input): one pixel per thread
+        axq::quantize_nchw_to_nhwc_small_kernel<<<stream_grid(N * HW, 256), 256, 0, S(stream)>>>(
+            x, N, C, HW, Cq, d_scale, bits, q);
+    } else {
+        dim3 grid((unsigned)((HW + 63) / 64), (unsigned)((Cq + 63) / 64), (unsigned)N);
+        axq::quantize_nchw_to_nhwc_kernel<<<grid, 256, 0, S(stream)>>>(x, C, HW, Cq, d_scale, bits, q);
+    }
     return check_launch();
 }
 
@@ -281,6 +289,73 @@ static axq_status gemm_common(int64_t M, int64_t N, int64_t K, const int8_t* A, 
     return overflow_guard(lut, K);
 }
 
+static axq_status check_epilogue(const axq_epilogue* ep, int64_t N, bool conv) {
+    if (!ep || !ep->d_scale_a || !ep->d_scale_w) return AXQ_ERR_INVALID;
+    const bool rows = !conv || ep->y_nhwc;
+    if (ep->y && rows && ep->ldy < N) return AXQ_ERR_INVALID;
+    if (ep->residual && (ep->ldr < N || (conv && !ep->y_nhwc && ep->y))) return AXQ_ERR_INVALID;
+    if (ep->q_out && (ep->ldq < N || !ep->d_scale_out || ep->bits_out < 2 || ep->bits_out > 8))
+        return AXQ_ERR_INVALID;
+    return AXQ_OK;
+}
+
+static axq::EpiArgs to_epi(const axq_epilogue* ep, bool nchw, int64_t hw) {
+    axq::EpiArgs e{};
+    e.sa = ep->d_scale_a;
+    e.sw = ep->d_scale_w;
+    e.bias = ep->bias;
+    e.residual = ep->residual;
+    e.ldr = ep->ldr;
+    e.relu = ep->relu;
+    e.y = ep->y;
+    e.ldy = ep->ldy;
+    e.y_nchw = nchw ? 1 : 0;
+    e.hw = hw;
+    e.q = ep->q_out;
+    e.ldq = ep->ldq;
+    e.s_out = ep->d_scale_out;
+    e.bits_out = ep->bits_out;
+    return e;
+}
+
+static axq_status launch_epilogue(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
+                                  const axq::EpiArgs& e, cudaStream_t st) {
+    axq::epilogue_kernel<<<stream_grid(M * N, 256 * 4), 256, 0, st>>>(M, N, acc, ldacc, e);
+    return check_launch();
+}
+
+// Common driver: plan split-K, launch the fused or the split (atomic + epilogue) variant.
+static axq_status run_mm(axq::MMArgs& p, int loader, axq_lut_t lut, const axq::EpiArgs* epi,
+                         int32_t* workspace, int32_t* C_raw, int64_t ldc, cudaStream_t st) {
+    Cfg c = pick_cfg(p.M, loader, lut->repr);
+    const bool can_split = epi ? (workspace != nullptr) : true;
+    p.k_split = pick_k_split(p.M, p.N, p.K, c, can_split);
+    const int64_t splits = p.K > 0 ? (p.K + p.k_split - 1) / p.k_split : 1;
+    const int64_t bm = (int64_t)c.warps * 32 * c.R;
+    dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + c.tn - 1) / c.tn), (unsigned)splits);
+    if (!epi) {
+        p.C_out = C_raw;
+        p.ldc = ldc;
+        if (splits > 1) {
+            cudaError_t e = cudaMemset2DAsync(C_raw, ldc * 4, 0, p.N * 4, p.M, st);
+            if (e != cudaSuccess) return cuda_fail(e);
+            return launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, st);
+        }
+        return launch_mm(axq::EPI_RAW, loader, lut->repr, p, c, grid, st);
+    }
+    if (splits > 1) {
+        p.C_out = workspace;
+        p.ldc = p.N;
+        cudaError_t e = cudaMemsetAsync(workspace, 0, (size_t)p.M * p.N * 4, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        axq_status s = launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, st);
+        if (s != AXQ_OK) return s;
+        return launch_epilogue(p.M, p.N, workspace, p.N, *epi, st);
+    }
+    p.ep = *epi;
+    return launch_mm(axq::EPI_FUSED, loader, lut->repr, p, c, grid, st);
+}
+
 axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
                         const int8_t* W, int64_t ldw, axq_lut_t lut, int32_t* C, int64_t ldc,
                         void* stream) {
@@ -295,20 +370,8 @@ axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_
     axq::MMArgs p{};
     p.A = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = K;
     fill_common(p, lut);
-    p.C_out = C; p.ldc = ldc;
     int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
-    Cfg c = pick_cfg(M, loader, lut->repr);
-    p.k_split = pick_k_split(M, N, K, c, true);
-    int64_t splits = (K + p.k_split - 1) / p.k_split;
-    int64_t bm = (int64_t)c.warps * 32 * c.R;
-    dim3 grid((unsigned)((M + bm - 1) / bm), (unsigned)((N + c.tn - 1) / c.tn), (unsigned)splits);
-    int epi = axq::EPI_RAW;
-    if (splits > 1) {
-        cudaError_t e = cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, S(stream));
-        if (e != cudaSuccess) return cuda_fail(e);
-        epi = axq::EPI_RAW_ATOMIC;
-    }
-    return launch_mm(epi, loader, lut->repr, p, c, grid, S(stream));
+    return run_mm(p, loader, lut, nullptr, nullptr, C, ldc, S(stream));
 }
 
 axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
@@ -316,29 +379,15 @@ axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int
                            void* stream) {
     axq_status s = gemm_common(M, N, K, A, lda, W, ldw, lut);
     if (s != AXQ_OK) return s;
-    if (!ep || !ep->d_scale_a || !ep->d_scale_w) return AXQ_ERR_INVALID;
+    s = check_epilogue(ep, N, false);
+    if (s != AXQ_OK) return s;
     if (M == 0 || N == 0) return AXQ_OK;
-    if (!ep->y || ep->ldy < N) return AXQ_ERR_INVALID;
     axq::MMArgs p{};
-    p.A = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = std::max<int64_t>(K, 0);
+    p.A = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = K;
     fill_common(p, lut);
-    p.sa = ep->d_scale_a; p.sw_ = ep->d_scale_w; p.bias = ep->bias; p.y = ep->y; p.ldy = ep->ldy;
+    axq::EpiArgs e = to_epi(ep, false, 0);
     int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
-    Cfg c = pick_cfg(M, loader, lut->repr);
-    p.k_split = pick_k_split(M, N, K, c, ep->workspace != nullptr);
-    int64_t splits = K > 0 ? (K + p.k_split - 1) / p.k_split : 1;
-    int64_t bm = (int64_t)c.warps * 32 * c.R;
-    dim3 grid((unsigned)((M + bm - 1) / bm), (unsigned)((N + c.tn - 1) / c.tn), (unsigned)splits);
-    if (splits > 1) {
-        p.C_out = ep->workspace; p.ldc = N;
-        cudaError_t e = cudaMemsetAsync(ep->workspace, 0, (size_t)M * N * 4, S(stream));
-        if (e != cudaSuccess) return cuda_fail(e);
-        s = launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, S(stream));
-        if (s != AXQ_OK) return s;
-        return axq_dequantize(M, N, ep->workspace, N, ep->d_scale_a, ep->d_scale_w, ep->bias,
-                              ep->y, ep->ldy, stream);
-    }
-    return launch_mm(axq::EPI_DQ_ROWS, loader, lut->repr, p, c, grid, S(stream));
+    return run_mm(p, loader, lut, &e, ep->workspace, nullptr, 0, S(stream));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -358,6 +407,7 @@ static axq_status conv_setup(const axq_conv_desc* d, const int8_t* X, const int8
                              axq_lut_t lut, axq::MMArgs& p, int& loader) {
     if (!d) return AXQ_ERR_INVALID;
     if (d->N < 0 || d->H <= 0 || d->W <= 0 || d->C <= 0 || d->K < 0) return AXQ_ERR_INVALID;
+    if (d->c_valid < 0 || d->c_valid > d->C) return AXQ_ERR_INVALID;
     if (d->groups != 1) return d->groups < 1 ? AXQ_ERR_INVALID : AXQ_ERR_UNSUPPORTED;
     int64_t Ho, Wo;
     axq_status s = axq_conv2d_out_hw(d, &Ho, &Wo);
@@ -366,7 +416,8 @@ static axq_status conv_setup(const axq_conv_desc* d, const int8_t* X, const int8
     s = check_lut(lut);
     if (s != AXQ_OK) return s;
     const int64_t K = d->R * d->S * d->C;
-    s = overflow_guard(lut, K);
+    const int64_t cv = d->c_valid ? d->c_valid : d->C;
+    s = overflow_guard(lut, d->R * d->S * cv);
     if (s != AXQ_OK) return s;
     if (d->N > 0 && d->K > 0 && (!X || !Wt)) return AXQ_ERR_INVALID;
     if (d->H * d->W * d->C >= (int64_t)1 << 31 || Ho * Wo >= (int64_t)1 << 31) return AXQ_ERR_INVALID;
@@ -377,7 +428,13 @@ static axq_status conv_setup(const axq_conv_desc* d, const int8_t* X, const int8
     p.S = (int)d->S; p.sh = (int)d->stride_h; p.sw = (int)d->stride_w;
     p.ph = (int)d->pad_h; p.pw = (int)d->pad_w; p.dh = (int)d->dil_h; p.dw = (int)d->dil_w;
     fill_common(p, lut);
-    loader = ((d->C & 15) == 0 && aligned16(X)) ? axq::LOAD_CONV : axq::LOAD_CONV_BYTES;
+    p.pad_lookups = (int32_t)(d->R * d->S * (d->C - cv));
+    if ((d->C & 15) == 0 && aligned16(X))
+        loader = axq::LOAD_CONV;
+    else if ((d->C & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 3) == 0)
+        loader = axq::LOAD_CONV_C4;
+    else
+        loader = axq::LOAD_CONV_BYTES;
     return AXQ_OK;
 }
 
@@ -389,19 +446,7 @@ axq_status axq_lut_conv2d(const axq_conv_desc* d, const int8_t* X, const int8_t*
     if (s != AXQ_OK) return s;
     if (p.M == 0 || p.N == 0) return AXQ_OK;
     if (!Y) return AXQ_ERR_INVALID;
-    p.C_out = Y; p.ldc = p.N;
-    Cfg c = pick_cfg(p.M, loader, lut->repr);
-    p.k_split = pick_k_split(p.M, p.N, p.K, c, true);
-    int64_t splits = (p.K + p.k_split - 1) / p.k_split;
-    int64_t bm = (int64_t)c.warps * 32 * c.R;
-    dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + c.tn - 1) / c.tn), (unsigned)splits);
-    int epi = axq::EPI_RAW;
-    if (splits > 1) {
-        cudaError_t e = cudaMemsetAsync(Y, 0, (size_t)p.M * p.N * 4, S(stream));
-        if (e != cudaSuccess) return cuda_fail(e);
-        epi = axq::EPI_RAW_ATOMIC;
-    }
-    return launch_mm(epi, loader, lut->repr, p, c, grid, S(stream));
+    return run_mm(p, loader, lut, nullptr, nullptr, Y, p.N, S(stream));
 }
 
 axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
@@ -410,29 +455,16 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
     int loader;
     axq_status s = conv_setup(d, X, Wt, lut, p, loader);
     if (s != AXQ_OK) return s;
-    if (!ep || !ep->d_scale_a || !ep->d_scale_w) return AXQ_ERR_INVALID;
+    s = check_epilogue(ep, d->K, true);
+    if (s != AXQ_OK) return s;
     if (p.M == 0 || p.N == 0) return AXQ_OK;
-    if (!ep->y) return AXQ_ERR_INVALID;
-    p.sa = ep->d_scale_a; p.sw_ = ep->d_scale_w; p.bias = ep->bias; p.y = ep->y;
-    Cfg c = pick_cfg(p.M, loader, lut->repr);
-    p.k_split = pick_k_split(p.M, p.N, p.K, c, ep->workspace != nullptr);
-    int64_t splits = (p.K + p.k_split - 1) / p.k_split;
-    int64_t bm = (int64_t)c.warps * 32 * c.R;
-    dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + c.tn - 1) / c.tn), (unsigned)splits);
-    if (splits > 1) {
-        p.C_out = ep->workspace; p.ldc = p.N;
-        cudaError_t e = cudaMemsetAsync(ep->workspace, 0, (size_t)p.M * p.N * 4, S(stream));
-        if (e != cudaSuccess) return cuda_fail(e);
-        s = launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, S(stream));
-        if (s != AXQ_OK) return s;
-        return axq_dequantize_nhwc_to_nchw(d->N, (int64_t)p.Ho * p.Wo, p.N, ep->workspace,
-                                           ep->d_scale_a, ep->d_scale_w, ep->bias, ep->y, stream);
-    }
-    return launch_mm(axq::EPI_DQ_NCHW, loader, lut->repr, p, c, grid, S(stream));
+    const bool nchw = !ep->y_nhwc;
+    axq::EpiArgs e = to_epi(ep, nchw, (int64_t)p.Ho * p.Wo);
+    return run_mm(p, loader, lut, &e, ep->workspace, nullptr, 0, S(stream));
 }
 
 // ---------------------------------------------------------------------------------------
-// Dequantize
+// Dequantize / epilogue
 // ---------------------------------------------------------------------------------------
 axq_status axq_dequantize(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
                           const float* d_scale_a, const float* d_scale_w, const float* bias,
@@ -454,6 +486,62 @@ axq_status axq_dequantize_nhwc_to_nchw(int64_t N, int64_t HW, int64_t C, const i
     dim3 grid((unsigned)((HW + 31) / 32), (unsigned)((C + 31) / 32), (unsigned)N);
     axq::dequant_nhwc_to_nchw_kernel<<<grid, dim3(32, 8), 0, S(stream)>>>(acc, HW, C, d_scale_a,
                                                                         d_scale_w, bias, y);
+    return check_launch();
+}
+
+axq_status axq_epilogue_apply(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
+                              const axq_epilogue* ep, void* stream) {
+    if (M < 0 || N < 0 || ldacc < N) return AXQ_ERR_INVALID;
+    axq_status s = check_epilogue(ep, N, false);
+    if (s != AXQ_OK) return s;
+    if (M == 0 || N == 0) return AXQ_OK;
+    if (!acc) return AXQ_ERR_INVALID;
+    return launch_epilogue(M, N, acc, ldacc, to_epi(ep, false, 0), S(stream));
+}
+
+// ---------------------------------------------------------------------------------------
+// Model glue
+// ---------------------------------------------------------------------------------------
+axq_status axq_maxpool2d_nhwc_i8(const int8_t* x, int64_t N, int64_t H, int64_t W, int64_t C,
+                                 int64_t R, int64_t Sz, int64_t stride, int64_t pad, int8_t* y,
+                                 void* stream) {
+    if (N < 0 || H <= 0 || W <= 0 || C <= 0 || R <= 0 || Sz <= 0 || stride <= 0 || pad < 0 ||
+        pad >= R || pad >= Sz)
+        return AXQ_ERR_INVALID;
+    const int64_t Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - Sz) / stride + 1;
+    if (Ho <= 0 || Wo <= 0) return AXQ_ERR_INVALID;
+    if (N == 0) return AXQ_OK;
+    if (!x || !y) return AXQ_ERR_INVALID;
+    if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 3) == 0) {
+        axq::maxpool_nhwc_i8_kernel<<<stream_grid(N * Ho * Wo * (C / 4), 256), 256, 0, S(stream)>>>(
+            x, N, (int)H, (int)W, (int)C, (int)R, (int)Sz, (int)stride, (int)pad, (int)Ho, (int)Wo, y);
+    } else {
+        axq::maxpool_nhwc_i8_bytes_kernel<<<stream_grid(N * Ho * Wo * C, 256), 256, 0, S(stream)>>>(
+            x, N, (int)H, (int)W, (int)C, (int)R, (int)Sz, (int)stride, (int)pad, (int)Ho, (int)Wo, y);
+    }
+    return check_launch();
+}
+
+axq_status axq_avgpool_nhwc(const float* x, int64_t N, int64_t HW, int64_t C, float* y,
+                            int8_t* q, const float* d_scale, int bits, void* stream) {
+    if (N < 0 || HW <= 0 || C <= 0) return AXQ_ERR_INVALID;
+    if (q && (!d_scale || bits < 2 || bits > 8)) return AXQ_ERR_INVALID;
+    if (N == 0) return AXQ_OK;
+    if (!x || (!y && !q)) return AXQ_ERR_INVALID;
+    axq::avgpool_nhwc_kernel<<<stream_grid(N * C, 256), 256, 0, S(stream)>>>(x, N, HW, C, y, q,
+                                                                            d_scale, q ? bits : 8);
+    return check_launch();
+}
+
+axq_status axq_lstm_cell(int64_t B, int64_t Hd, const float* gates_ih, const float* gates_hh,
+                         float* c, float* h_out, int8_t* q_h, const float* d_scale_h, int bits,
+                         void* stream) {
+    if (B < 0 || Hd < 0) return AXQ_ERR_INVALID;
+    if (q_h && (!d_scale_h || bits < 2 || bits > 8)) return AXQ_ERR_INVALID;
+    if (B == 0 || Hd == 0) return AXQ_OK;
+    if (!gates_ih || !gates_hh || !c || !h_out) return AXQ_ERR_INVALID;
+    axq::lstm_cell_kernel<<<stream_grid(B * Hd, 256), 256, 0, S(stream)>>>(
+        B, Hd, gates_ih, gates_hh, c, h_out, q_h, d_scale_h, q_h ? bits : 8);
     return check_launch();
 }
 

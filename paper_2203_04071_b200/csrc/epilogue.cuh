@@ -1,0 +1,72 @@
+// epilogue.cuh -- the dequantize epilogue shared by the LUT kernels and the stand-alone
+// epilogue kernel (split-K path).  Pinned fp32 order (A13/A14, A17):
+//   v = fl(fl((float)acc) * fl(s_a * s_w));  v = fl(v + bias[n]);  v = fl(v + residual[m][n]);
+//   v = relu ? max(v, 0) : v;   y = v;   q = clamp(rint(fl(v / s_out)))
+// "real_value = A x quantized_value" with both operands' scales, "+ b"; the
+// residual add / ReLU / requantize serve the ResNet-50 driver (BJ configs[3], A16/A17).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace axq {
+
+struct EpiArgs {
+    const float* sa;        // device scalar
+    const float* sw;        // device scalar
+    const float* bias;      // [N] or null
+    const float* residual;  // [M][ldr] fp32 or null (row layout only)
+    int64_t ldr;
+    int relu;
+    float* y;               // fp32 output or null
+    int64_t ldy;            // row layout stride
+    int y_nchw;             // 1: y[img][n][pix] with pix in [0, hw)
+    int64_t hw;
+    int8_t* q;              // requantized codes [M][ldq] or null
+    int64_t ldq;
+    const float* s_out;     // device scalar
+    int bits_out;
+};
+
+__device__ __forceinline__ float epi_value(int32_t acc, int64_t m, int64_t n, float sc,
+                                           const EpiArgs& e) {
+    float v = __fmul_rn(__int2float_rn(acc), sc);
+    if (e.bias) v = __fadd_rn(v, e.bias[n]);
+    if (e.residual) v = __fadd_rn(v, e.residual[m * e.ldr + n]);
+    if (e.relu) v = v > 0.f ? v : 0.f;
+    return v;
+}
+
+__device__ __forceinline__ int8_t epi_quant(float v, float s, float qm) {
+    float t = __fdiv_rn(v, s);
+    t = fminf(fmaxf(t, -qm), qm);
+    return (int8_t)__float2int_rn(t);
+}
+
+__device__ __forceinline__ void epi_store(float v, int64_t m, int64_t n, int64_t N,
+                                          const EpiArgs& e, float s_out, float qm) {
+    if (e.y) {
+        if (e.y_nchw) {
+            const int64_t img = m / e.hw, pix = m - img * e.hw;
+            __stcs(e.y + (img * N + n) * e.hw + pix, v);
+        } else {
+            e.y[m * e.ldy + n] = v;
+        }
+    }
+    if (e.q) e.q[m * e.ldq + n] = epi_quant(v, s_out, qm);
+}
+
+// Stand-alone epilogue over an int32 [M][N] accumulator (split-K path).
+static __global__ void epilogue_kernel(int64_t M, int64_t N, const int32_t* __restrict__ acc,
+                                int64_t ldacc, const EpiArgs e) {
+    const float sc = __fmul_rn(*e.sa, *e.sw);
+    const float s_out = e.q ? *e.s_out : 1.f;
+    const float qm = (float)((1 << (e.bits_out > 0 ? e.bits_out - 1 : 7)) - 1);
+    const int64_t total = M * N;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t m = i / N, n = i - m * N;
+        epi_store(epi_value(acc[m * ldacc + n], m, n, sc, e), m, n, N, e, s_out, qm);
+    }
+}
+
+}  // namespace axq

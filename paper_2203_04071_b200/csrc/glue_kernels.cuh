@@ -1,0 +1,144 @@
+// glue_kernels.cuh -- model glue around the LUT layers (sm_100a): int8 max pooling, global
+// average pooling (+ fused quantize) for the ResNet-50-shaped forward (BASELINE.json
+// configs[3], A16/A17) and the LSTM cell with the pinned fp32 exp of DESIGN.md A18
+// (BASELINE.json configs[4]).  All HBM-bound element-wise kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "epilogue.cuh"
+
+namespace axq {
+
+// ---- max pooling over int8 codes, NHWC, 4 channels per thread via byte-SIMD max ----
+__global__ void maxpool_nhwc_i8_kernel(const int8_t* __restrict__ x, int64_t N, int H, int W,
+                                       int C, int R, int S, int stride, int pad, int Ho, int Wo,
+                                       int8_t* __restrict__ y) {
+    const int C4 = C / 4;
+    const int64_t total = N * Ho * Wo * (int64_t)C4;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int c4 = (int)(i % C4);
+        int64_t t = i / C4;
+        const int wo = (int)(t % Wo);
+        t /= Wo;
+        const int ho = (int)(t % Ho);
+        const int64_t n = t / Ho;
+        unsigned int m = 0x80808080u;  // -128 in every byte
+        for (int r = 0; r < R; ++r) {
+            const int hi = ho * stride - pad + r;
+            if (hi < 0 || hi >= H) continue;
+            for (int s = 0; s < S; ++s) {
+                const int wi = wo * stride - pad + s;
+                if (wi < 0 || wi >= W) continue;
+                const unsigned int v = __ldg(reinterpret_cast<const unsigned int*>(
+                    x + ((n * H + hi) * W + wi) * C) + c4);
+                m = __vmaxs4(m, v);
+            }
+        }
+        reinterpret_cast<unsigned int*>(y + ((n * Ho + ho) * Wo + wo) * C)[c4] = m;
+    }
+}
+
+__global__ void maxpool_nhwc_i8_bytes_kernel(const int8_t* __restrict__ x, int64_t N, int H, int W,
+                                             int C, int R, int S, int stride, int pad, int Ho,
+                                             int Wo, int8_t* __restrict__ y) {
+    const int64_t total = N * Ho * Wo * (int64_t)C;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int c = (int)(i % C);
+        int64_t t = i / C;
+        const int wo = (int)(t % Wo);
+        t /= Wo;
+        const int ho = (int)(t % Ho);
+        const int64_t n = t / Ho;
+        int m = -128;
+        for (int r = 0; r < R; ++r) {
+            const int hi = ho * stride - pad + r;
+            if (hi < 0 || hi >= H) continue;
+            for (int s = 0; s < S; ++s) {
+                const int wi = wo * stride - pad + s;
+                if (wi < 0 || wi >= W) continue;
+                m = max(m, (int)x[((n * H + hi) * W + wi) * C + c]);
+            }
+        }
+        y[((n * Ho + ho) * Wo + wo) * C + c] = (int8_t)m;
+    }
+}
+
+// ---- global average pool: sequential fp32 sum over hw, one IEEE division (A17) ----
+__global__ void avgpool_nhwc_kernel(const float* __restrict__ x, int64_t N, int64_t HW,
+                                    int64_t C, float* __restrict__ y, int8_t* __restrict__ q,
+                                    const float* __restrict__ d_scale, int bits) {
+    const float s = q ? *d_scale : 1.f;
+    const float qm = (float)((1 << (bits - 1)) - 1);
+    const float inv_n = (float)HW;
+    const int64_t total = N * C;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int64_t n = i / C, c = i - n * C;
+        const float* xp = x + n * HW * C + c;
+        float acc = 0.f;
+        for (int64_t p = 0; p < HW; ++p) acc = __fadd_rn(acc, xp[p * C]);
+        const float v = __fdiv_rn(acc, inv_n);
+        if (y) y[i] = v;
+        if (q) q[i] = epi_quant(v, s, qm);
+    }
+}
+
+// ---- LSTM cell with the pinned fp32 exp (A18) ----
+// E(x): clamp to [-80, 80]; n = rint(x*log2e); r = (x - n*355/512) - n*fl32(ln2 - 355/512);
+// p = degree-7 Taylor polynomial of e^r (Horner, fp32 coefficients 1/k!); E = p * 2^n.
+__device__ __forceinline__ float pinned_exp(float x) {
+    x = fminf(fmaxf(x, -80.f), 80.f);
+    const float n = rintf(__fmul_rn(x, 1.4426950216293335f));
+    const float r = __fsub_rn(__fsub_rn(x, __fmul_rn(n, 0.693359375f)),
+                              __fmul_rn(n, -0.00021219444170128554f));
+    float p = 0.00019841270113829523f;               // 1/7!
+    p = __fadd_rn(__fmul_rn(p, r), 0.0013888889225199819f);  // 1/6!
+    p = __fadd_rn(__fmul_rn(p, r), 0.008333333767950535f);     // 1/5!
+    p = __fadd_rn(__fmul_rn(p, r), 0.0416666679084301f);       // 1/4!
+    p = __fadd_rn(__fmul_rn(p, r), 0.1666666716337204f);         // 1/3!
+    p = __fadd_rn(__fmul_rn(p, r), 0.5f);                                  // 1/2!
+    p = __fadd_rn(__fmul_rn(p, r), 1.0f);                                  // 1/1!
+    p = __fadd_rn(__fmul_rn(p, r), 1.0f);                                  // 1/0!
+    const float two_n = __int_as_float(((int)n + 127) << 23);              // exact 2^n, n in [-116, 116]
+    return __fmul_rn(p, two_n);
+}
+
+__device__ __forceinline__ float pinned_sigmoid(float x) {
+    return __fdiv_rn(1.0f, __fadd_rn(1.0f, pinned_exp(-x)));
+}
+
+__device__ __forceinline__ float pinned_tanh(float x) {
+    const float e = pinned_exp(__fmul_rn(-2.0f, fabsf(x)));
+    const float t = __fdiv_rn(__fsub_rn(1.0f, e), __fadd_rn(1.0f, e));
+    return copysignf(t, x);
+}
+
+__global__ void lstm_cell_kernel(int64_t B, int64_t Hd, const float* __restrict__ gih,
+                                 const float* __restrict__ ghh, float* __restrict__ c,
+                                 float* __restrict__ h, int8_t* __restrict__ qh,
+                                 const float* __restrict__ d_scale_h, int bits) {
+    const float s = qh ? *d_scale_h : 1.f;
+    const float qm = (float)((1 << (bits - 1)) - 1);
+    const int64_t total = B * Hd;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int64_t b = i / Hd, j = i - b * Hd;
+        const int64_t base = b * 4 * Hd + j;
+        const float gi = __fadd_rn(gih[base], ghh[base]);
+        const float gf = __fadd_rn(gih[base + Hd], ghh[base + Hd]);
+        const float gg = __fadd_rn(gih[base + 2 * Hd], ghh[base + 2 * Hd]);
+        const float go = __fadd_rn(gih[base + 3 * Hd], ghh[base + 3 * Hd]);
+        const float ig = pinned_sigmoid(gi), fg = pinned_sigmoid(gf);
+        const float g = pinned_tanh(gg), og = pinned_sigmoid(go);
+        const float cn = __fadd_rn(__fmul_rn(fg, c[i]), __fmul_rn(ig, g));
+        const float hn = __fmul_rn(og, pinned_tanh(cn));
+        c[i] = cn;
+        h[i] = hn;
+        if (qh) qh[i] = epi_quant(hn, s, qm);
+    }
+}
+
+}  // namespace axq

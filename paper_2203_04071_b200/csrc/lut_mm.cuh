@@ -29,13 +29,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "epilogue.cuh"
+
 namespace axq {
 
 constexpr int KC = 16;
 
 enum { REPR_DELTA8 = 0, REPR_I16 = 1, REPR_I32 = 2 };
-enum { EPI_RAW = 0, EPI_RAW_ATOMIC = 1, EPI_DQ_ROWS = 2, EPI_DQ_NCHW = 3 };
-enum { LOAD_GEMM = 0, LOAD_CONV = 1, LOAD_GEMM_BYTES = 2, LOAD_CONV_BYTES = 3 };
+enum { EPI_RAW = 0, EPI_RAW_ATOMIC = 1, EPI_FUSED = 2 };
+enum { LOAD_GEMM = 0, LOAD_CONV = 1, LOAD_GEMM_BYTES = 2, LOAD_CONV_BYTES = 3, LOAD_CONV_C4 = 4 };
 
 struct MMArgs {
     const int8_t* A;  // GEMM: [M][lda]; conv: NHWC input X
@@ -48,15 +50,12 @@ struct MMArgs {
     const void* table;  // device table (representation-specific layout, [uw][ua])
     int table_bytes;
     int32_t t00;        // LUT[0][0] (value of one storage-padding lookup)
+    int32_t pad_lookups;  // storage-padding lookups per output inside K (padded channels)
     int64_t k_split;    // K extent per gridDim.z slice, multiple of KC
     // outputs
-    int32_t* C_out;
+    int32_t* C_out;     // raw / atomic epilogues
     int64_t ldc;
-    const float* sa;
-    const float* sw_;
-    const float* bias;
-    float* y;
-    int64_t ldy;
+    EpiArgs ep;         // fused epilogue
 };
 
 template <int REPR>
@@ -136,6 +135,26 @@ __device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int6
         int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
         if (ri.valid && k0 < p.K && hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
             v = ldg16(p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c0);
+        return v;
+    } else if constexpr (LOADER == LOAD_CONV_C4) {
+        // C % 4 == 0: each 4-byte group of the chunk lies inside one filter tap.
+        if (ri.valid) {
+            uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t k = k0 + 4 * j;
+                if (k < p.K) {
+                    int rs = (int)(k / p.C);
+                    int c = (int)(k - (int64_t)rs * p.C);
+                    int r = rs / p.S, s = rs - r * p.S;
+                    int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
+                    if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
+                        w[j] = __ldg(reinterpret_cast<const uint32_t*>(
+                            p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c));
+                }
+            }
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
         return v;
     } else {  // LOAD_CONV_BYTES: any C
         if (ri.valid) {
@@ -278,9 +297,10 @@ lut_mm_kernel(const MMArgs p) {
         __syncthreads();
     }
 
-    // ---- remove storage-padding lookups of the K tail (exact) ----
-    const int64_t npad = (int64_t)nchunks * KC - (ke - kb);
-    if (npad > 0) {
+    // ---- remove storage-padding lookups (K tail of this split; padded channels) ----
+    int64_t npad = (int64_t)nchunks * KC - (ke - kb);
+    if (ke == p.K) npad += p.pad_lookups;   // counted once, by the split holding the K end
+    if (npad != 0) {
         const int corr = (int)(npad * (int64_t)p.t00);
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -289,8 +309,14 @@ lut_mm_kernel(const MMArgs p) {
     }
 
     // ---- epilogue ----
-    float sc = 0.f;
-    if constexpr (EPI == EPI_DQ_ROWS || EPI == EPI_DQ_NCHW) sc = __fmul_rn(*p.sa, *p.sw_);
+    float sc = 0.f, s_out = 1.f, qm = 127.f;
+    if constexpr (EPI == EPI_FUSED) {
+        sc = __fmul_rn(*p.ep.sa, *p.ep.sw);
+        if (p.ep.q) {
+            s_out = *p.ep.s_out;
+            qm = (float)((1 << (p.ep.bits_out - 1)) - 1);
+        }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const RowInfo& ri = rows[r];
@@ -312,25 +338,11 @@ lut_mm_kernel(const MMArgs p) {
 #pragma unroll
             for (int n = 0; n < TN; ++n)
                 if (n0 + n < p.N) atomicAdd(c + n, acc[r][n]);
-        } else if constexpr (EPI == EPI_DQ_ROWS) {
-            float* yr = p.y + m * p.ldy + n0;
+        } else {
 #pragma unroll
             for (int n = 0; n < TN; ++n) {
-                if (n0 + n < p.N) {
-                    float v = __fmul_rn(__int2float_rn(acc[r][n]), sc);
-                    yr[n] = p.bias ? __fadd_rn(v, p.bias[n0 + n]) : v;
-                }
-            }
-        } else {  // EPI_DQ_NCHW: m = (img, ho, wo); y[img][n][ho][wo]
-            const int64_t hw = (int64_t)p.Ho * p.Wo;
-            const int64_t img = m / hw, pix = m - img * hw;
-            float* yb = p.y + img * p.N * hw + pix;
-#pragma unroll
-            for (int n = 0; n < TN; ++n) {
-                if (n0 + n < p.N) {
-                    float v = __fmul_rn(__int2float_rn(acc[r][n]), sc);
-                    __stcs(yb + (n0 + n) * hw, p.bias ? __fadd_rn(v, p.bias[n0 + n]) : v);
-                }
+                const int64_t nn = n0 + n;
+                if (nn < p.N) epi_store(epi_value(acc[r][n], m, nn, sc, p.ep), m, nn, p.N, p.ep, s_out, qm);
             }
         }
     }

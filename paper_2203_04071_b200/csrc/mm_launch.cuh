@@ -24,7 +24,7 @@ int launch_one(const MMArgs& p, dim3 grid, cudaStream_t st) {
 // Byte-wise loaders (unaligned / tiny C) and the int32 table use only the SMALL tile.
 template <int REPR, int LOADER, int EPI>
 int launch_cfg(const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st) {
-    constexpr bool big_ok = (REPR != REPR_I32) && (LOADER == LOAD_GEMM || LOADER == LOAD_CONV);
+    constexpr bool big_ok = (REPR != REPR_I32) && (LOADER == LOAD_GEMM || LOADER == LOAD_CONV || LOADER == LOAD_CONV_C4);
     if constexpr (big_ok) {
         if (c.warps == CFG_BIG.warps && c.R == CFG_BIG.R)
             return launch_one<REPR, CFG_BIG.tn, CFG_BIG.R, CFG_BIG.warps, LOADER, EPI>(p, grid, st);
@@ -38,6 +38,7 @@ int launch_loader(int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStre
         case LOAD_GEMM: return launch_cfg<REPR, LOAD_GEMM, EPI>(p, c, grid, st);
         case LOAD_GEMM_BYTES: return launch_cfg<REPR, LOAD_GEMM_BYTES, EPI>(p, c, grid, st);
         case LOAD_CONV: return launch_cfg<REPR, LOAD_CONV, EPI>(p, c, grid, st);
+        case LOAD_CONV_C4: return launch_cfg<REPR, LOAD_CONV_C4, EPI>(p, c, grid, st);
         default: return launch_cfg<REPR, LOAD_CONV_BYTES, EPI>(p, c, grid, st);
     }
 }
@@ -47,8 +48,7 @@ int launch_mm_repr(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid
     switch (epi) {
         case EPI_RAW: return launch_loader<REPR, EPI_RAW>(loader, p, c, grid, st);
         case EPI_RAW_ATOMIC: return launch_loader<REPR, EPI_RAW_ATOMIC>(loader, p, c, grid, st);
-        case EPI_DQ_ROWS: return launch_loader<REPR, EPI_DQ_ROWS>(loader, p, c, grid, st);
-        default: return launch_loader<REPR, EPI_DQ_NCHW>(loader, p, c, grid, st);
+        default: return launch_loader<REPR, EPI_FUSED>(loader, p, c, grid, st);
     }
 }
 

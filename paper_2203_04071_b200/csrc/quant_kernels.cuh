@@ -81,27 +81,79 @@ __global__ void quantize_kernel(const float* __restrict__ x, int64_t n,
     for (int64_t i = n4 * 4 + tid; i < n; i += stride) q[i] = quantize_one(x[i], s, qm);
 }
 
-// ---- quantize NCHW fp32 -> NHWC int8, tiled transpose through shared memory.
-// Block = (image, 32 consecutive hw positions, 32 consecutive channels): reads are
-// 128-byte rows along hw, writes are 32-byte rows along c. ----
-__global__ void quantize_nchw_to_nhwc_kernel(const float* __restrict__ x, int64_t C,
-                                             int64_t HW, const float* __restrict__ d_scale,
-                                             int bits, int8_t* __restrict__ q) {
-    __shared__ int8_t tile[32][33];
+// ---- quantize NCHW fp32 -> NHWC int8 [N][HW][Cq] (channels >= C written as 0).
+// Tiled transpose: a 256-thread block owns (image, 64 hw positions, 64 channels); reads are
+// float4 rows along hw, the int8 tile is transposed in shared memory and written as 32-bit
+// words along c. ----
+__global__ void __launch_bounds__(256)
+quantize_nchw_to_nhwc_kernel(const float* __restrict__ x, int64_t C, int64_t HW, int64_t Cq,
+                             const float* __restrict__ d_scale, int bits, int8_t* __restrict__ q) {
+    __shared__ __align__(16) uint8_t tile[64][68];
     const float s = *d_scale, qm = qmax_of(bits);
-    int64_t img = blockIdx.z;
-    int64_t hw0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
-    int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    const int64_t img = blockIdx.z;
+    const int64_t hw0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
+    const int tid = threadIdx.x;
     const float* xi = x + img * C * HW;
-    for (int cc = ty; cc < 32; cc += 8) {
-        int64_t c = c0 + cc, hw = hw0 + tx;
-        if (c < C && hw < HW) tile[cc][tx] = quantize_one(__ldcs(xi + c * HW + hw), s, qm);
+    const bool vec = ((HW & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int idx = tid + 256 * it;
+        const int cl = idx >> 4, h4 = (idx & 15) * 4;
+        const int64_t c = c0 + cl, hw = hw0 + h4;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (c < C) {
+            if (vec && hw + 3 < HW) {
+                float4 t = __ldcs(reinterpret_cast<const float4*>(xi + c * HW + hw));
+                v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+            } else {
+                for (int j = 0; j < 4; ++j)
+                    if (hw + j < HW) v[j] = xi[c * HW + hw + j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            tile[h4 + j][cl] = (uint8_t)((c < C) ? quantize_one(v[j], s, qm) : 0);
     }
     __syncthreads();
-    int8_t* qi = q + img * HW * C;
-    for (int hh = ty; hh < 32; hh += 8) {
-        int64_t hw = hw0 + hh, c = c0 + tx;
-        if (c < C && hw < HW) qi[hw * C + c] = tile[tx][hh];
+    int8_t* qi = q + img * HW * Cq;
+    const bool wvec = ((Cq & 3) == 0) && ((reinterpret_cast<uintptr_t>(q) & 3) == 0);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int idx = tid + 256 * it;
+        const int hl = idx >> 4, cw = (idx & 15) * 4;
+        const int64_t hw = hw0 + hl, c = c0 + cw;
+        if (hw >= HW || c >= Cq) continue;
+        const uint32_t word = *reinterpret_cast<const uint32_t*>(&tile[hl][cw]);
+        if (wvec && c + 3 < Cq) {
+            *reinterpret_cast<uint32_t*>(qi + hw * Cq + c) = word;
+        } else {
+            for (int j = 0; j < 4; ++j)
+                if (c + j < Cq) qi[hw * Cq + c + j] = (int8_t)((word >> (8 * j)) & 0xff);
+        }
+    }
+}
+
+// Few channels (the network input, C = 3 padded to Cq = 4): one pixel per thread.
+__global__ void quantize_nchw_to_nhwc_small_kernel(const float* __restrict__ x, int64_t N,
+                                                   int64_t C, int64_t HW, int64_t Cq,
+                                                   const float* __restrict__ d_scale, int bits,
+                                                   int8_t* __restrict__ q) {
+    const float s = *d_scale, qm = qmax_of(bits);
+    const int64_t total = N * HW;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int64_t img = i / HW, hw = i - img * HW;
+        const float* xp = x + img * C * HW + hw;
+        int8_t* qp = q + i * Cq;
+        if (Cq == 4 && (reinterpret_cast<uintptr_t>(q) & 3) == 0) {
+            uint32_t w = 0;
+            for (int c = 0; c < C && c < 4; ++c)
+                w |= (uint32_t)(uint8_t)quantize_one(__ldcs(xp + c * HW), s, qm) << (8 * c);
+            *reinterpret_cast<uint32_t*>(qp) = w;
+        } else {
+            for (int64_t c = 0; c < Cq; ++c)
+                qp[c] = c < C ? quantize_one(__ldcs(xp + c * HW), s, qm) : (int8_t)0;
+        }
     }
 }
 

@@ -1,0 +1,279 @@
+"""ResNet-50-shaped approximate forward on the C ABI (BASELINE.json configs[3]).
+
+Every conv and the fc are approximate LUT layers (§III.B; "per-layer max
+calibration", BJ configs[3]); the glue follows DESIGN.md A16/A17:
+  stem 7x7/2 p3 + ReLU -> maxpool 3x3/2 p1 -> bottleneck stages (3,64) (4,128) (6,256) (3,512),
+  expansion 4, stride on the 3x3 conv, projection shortcut on each stage's first block,
+  out = ReLU(main + shortcut) -> global avgpool -> fc 2048 -> 1000 + bias.  No BatchNorm.
+
+Activations live in NHWC on the device: int8 codes for every conv input (written directly by
+the producing conv's epilogue with the consumer's static scale) and fp32 only where the
+network needs real values (block outputs = residuals, projection outputs, the avgpool input).
+Max pooling runs on int8 codes (equal to quantizing the pooled fp32 values: quantization is
+monotone, A17).  The network input (C = 3) is stored with C = 4 (a zero channel with zero
+weights, removed exactly by the conv's `c_valid`).
+
+calibrate(x): the approximate forward with dynamic per-tensor max scales (every conv writes
+fp32, then amax -> scale -> quantize); records each layer's input scale (reading A7').
+forward(x): the static-scale forward with fused requantizing epilogues (the timed path).
+Layer parameters are given by the caller (weights[name] fp32, PyTorch layouts).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as ax
+
+
+def layer_specs(widths=(64, 128, 256, 512), blocks=(3, 4, 6, 3), in_ch=3, stem_ch=64,
+                num_classes=1000, expansion=4):
+    """(name, kind, cout, cin, k, stride, pad) in forward order; weight tensor index = position
+    + 1 (the fc bias follows the fc weight)."""
+    specs = [("stem", "conv", stem_ch, in_ch, 7, 2, 3)]
+    cin = stem_ch
+    for si in range(len(widths)):
+        w = widths[si]
+        for bi in range(blocks[si]):
+            stride = (2 if si > 0 else 1) if bi == 0 else 1
+            p = "s%db%d" % (si, bi)
+            specs.append((p + ".c1", "conv", w, cin, 1, 1, 0))
+            specs.append((p + ".c2", "conv", w, w, 3, stride, 1))
+            specs.append((p + ".c3", "conv", w * expansion, w, 1, 1, 0))
+            if bi == 0:
+                specs.append((p + ".down", "conv", w * expansion, cin, 1, stride, 0))
+            cin = w * expansion
+    specs.append(("fc", "fc", num_classes, cin, 1, 1, 0))
+    return specs
+
+
+def _out(h, k, s, p):
+    return (h + 2 * p - k) // s + 1
+
+
+class ApproxResNet:
+    def __init__(self, weights: dict, lut: ax.Lut, device="cuda", **topo):
+        self.dev = torch.device(device)
+        self.lut, self.bits = lut, lut.bits
+        self.specs = layer_specs(**topo)
+        self.spec = {s[0]: s for s in self.specs}
+        self.blocks = []
+        for s in self.specs:
+            blk = s[0].rsplit(".", 1)[0]
+            if s[0].endswith(".c1"):
+                self.blocks.append(blk)
+        self.slot = {s[0]: i for i, s in enumerate(self.specs)}
+        n = len(self.specs)
+        self.d_amax = torch.zeros(n, device=self.dev)
+        self.s_act = torch.ones(n, device=self.dev)      # per-layer input scales
+        self.s_w = torch.ones(n, device=self.dev)        # per-layer weight scales
+        self.qw = {}
+        for name, kind, cout, cin, k, stride, pad in self.specs:
+            w = torch.as_tensor(weights[name]).to(self.dev, torch.float32).contiguous()
+            i = self.slot[name]
+            q = torch.empty(w.shape, dtype=torch.int8, device=self.dev)
+            ax.axq_amax(w, self.d_amax[i:i + 1])
+            ax.axq_scale(self.d_amax[i:i + 1], self.bits, self.s_w[i:i + 1])
+            ax.axq_quantize(w, self.s_w[i:i + 1], self.bits, q)
+            if kind == "conv":
+                q = q.permute(0, 2, 3, 1).contiguous()                    # KRSC
+                if name == "stem" and cin % 4:
+                    cpad = (cin + 3) // 4 * 4
+                    qp = torch.zeros(cout, k, k, cpad, dtype=torch.int8, device=self.dev)
+                    qp[..., :cin] = q
+                    q = qp
+            self.qw[name] = q
+        self.fc_bias = torch.as_tensor(weights["fc.b"]).to(self.dev, torch.float32).contiguous()
+        self._bufs = {}
+        self.calibrated = False
+
+    # ---------------------------------------------------------------------------------
+    def _s(self, name):
+        i = self.slot[name]
+        return self.s_act[i:i + 1]
+
+    def _sw(self, name):
+        i = self.slot[name]
+        return self.s_w[i:i + 1]
+
+    def _buffers(self, N, H, W):
+        key = (N, H, W)
+        if key in self._bufs:
+            return self._bufs[key]
+        dev, i8, f32 = self.dev, torch.int8, torch.float32
+        b = {}
+        cin = self.spec["stem"][3]
+        cq = (cin + 3) // 4 * 4
+        b["qx"] = torch.empty(N, H, W, cq, dtype=i8, device=dev)
+        h, w = _out(H, 7, 2, 3), _out(W, 7, 2, 3)
+        C = self.spec["stem"][2]
+        b["stem_q"] = torch.empty(N, h, w, C, dtype=i8, device=dev)
+        b["stem_f"] = torch.empty(N, h, w, C, dtype=f32, device=dev)       # calibration only
+        h, w = _out(h, 3, 2, 1), _out(w, 3, 2, 1)
+        b["pool_q"] = torch.empty(N, h, w, C, dtype=i8, device=dev)
+        shapes = {}
+        ws_elems = 0
+        for blk in self.blocks:
+            _, _, wd, cin, _, _, _ = self.spec[blk + ".c1"]
+            stride = self.spec[blk + ".c2"][5]
+            cout = self.spec[blk + ".c3"][2]
+            ho, wo = _out(h, 3, stride, 1), _out(w, 3, stride, 1)
+            shapes[blk] = (h, w, ho, wo)
+            b[blk + ".q1"] = torch.empty(N, h, w, wd, dtype=i8, device=dev)
+            b[blk + ".q2"] = torch.empty(N, ho, wo, wd, dtype=i8, device=dev)
+            b[blk + ".f1"] = torch.empty(N, h, w, wd, dtype=f32, device=dev)     # calibration
+            b[blk + ".f2"] = torch.empty(N, ho, wo, wd, dtype=f32, device=dev)   # calibration
+            b[blk + ".out"] = torch.empty(N, ho, wo, cout, dtype=f32, device=dev)
+            b[blk + ".qout"] = torch.empty(N, ho, wo, cout, dtype=i8, device=dev)
+            if blk + ".down" in self.spec:
+                b[blk + ".res"] = torch.empty(N, ho, wo, cout, dtype=f32, device=dev)
+            ws_elems = max(ws_elems, N * h * w * wd, N * ho * wo * max(wd, cout))
+            h, w = ho, wo
+        cfin = self.spec["fc"][3]
+        b["pool_f"] = torch.empty(N, cfin, dtype=f32, device=dev)
+        b["fc_q"] = torch.empty(N, cfin, dtype=i8, device=dev)
+        b["logits"] = torch.empty(N, self.spec["fc"][2], dtype=f32, device=dev)
+        ws_elems = max(ws_elems, N * self.spec["fc"][2], b["stem_q"].numel())
+        b["ws"] = torch.empty(ws_elems, dtype=torch.int32, device=dev)
+        b["shapes"] = shapes
+        self._bufs[key] = b
+        return b
+
+    def _conv(self, name, xq, N, H, W, stream, **ep_kw):
+        _, _, cout, cin, k, stride, pad = self.spec[name]
+        C = xq.shape[-1]
+        d = ax.conv_desc(N, H, W, C, cout, k, k, (stride, stride), (pad, pad),
+                         c_valid=cin if C != cin else 0)
+        ep = ax.make_epilogue(self._s(name), self._sw(name), y_nhwc=True, **ep_kw)
+        ax.axq_lut_conv2d_ep(d, xq, self.qw[name], self.lut, ep, stream)
+
+    def _calib_scale(self, name, t, stream):
+        i = self.slot[name]
+        ax.axq_amax(t, self.d_amax[i:i + 1], stream)
+        ax.axq_scale(self.d_amax[i:i + 1], self.bits, self.s_act[i:i + 1], stream)
+
+    # ---------------------------------------------------------------------------------
+    def run(self, x: torch.Tensor, calibrate: bool, stream=None) -> torch.Tensor:
+        """x fp32 NCHW [N][3][H][W] on the device -> logits fp32 [N][classes]."""
+        if stream is None:
+            stream = torch.cuda.current_stream(self.dev)
+        N, _, H, W = x.shape
+        b = self._buffers(N, H, W)
+        bits = self.bits
+        ws = b["ws"]
+        # ---- stem ----
+        if calibrate:
+            self._calib_scale("stem", x, stream)
+        ax.axq_quantize_nchw_to_nhwc(x, self._s("stem"), bits, b["qx"], stream)
+        first = self.blocks[0] + ".c1"
+        if calibrate:
+            f = b["stem_f"]
+            self._conv("stem", b["qx"], N, H, W, stream, y=f, ldy=f.shape[-1], relu=True,
+                       workspace=ws)
+            # amax(maxpool(v)) == amax(v): every stem output lies in some pooling window
+            self._calib_scale(first, f, stream)
+            ax.axq_quantize(f, self._s(first), bits, b["stem_q"], stream)
+        else:
+            q = b["stem_q"]
+            self._conv("stem", b["qx"], N, H, W, stream, relu=True, q_out=q, ldq=q.shape[-1],
+                       d_scale_out=self._s(first), bits_out=bits, workspace=ws)
+        h, w = b["stem_q"].shape[1:3]
+        ax.axq_maxpool2d_nhwc_i8(b["stem_q"], 3, 3, 2, 1, b["pool_q"], stream)
+        q_in = b["pool_q"]
+        f_in = None
+        # ---- bottleneck blocks ----
+        for bi, blk in enumerate(self.blocks):
+            h, w, ho, wo = b["shapes"][blk]
+            s_in = self._s(blk + ".c1")
+            has_down = blk + ".down" in self.spec
+            if has_down:
+                if calibrate:                                             # shared input scale
+                    i_d, i_c = self.slot[blk + ".down"], self.slot[blk + ".c1"]
+                    with torch.cuda.stream(stream):
+                        self.s_act[i_d:i_d + 1].copy_(self.s_act[i_c:i_c + 1])
+                r = b[blk + ".res"]
+                self._conv(blk + ".down", q_in, N, h, w, stream, y=r, ldy=r.shape[-1],
+                           workspace=ws)
+            else:
+                r = f_in
+            q1, q2 = b[blk + ".q1"], b[blk + ".q2"]
+            if calibrate:
+                f1, f2 = b[blk + ".f1"], b[blk + ".f2"]
+                self._conv(blk + ".c1", q_in, N, h, w, stream, y=f1, ldy=f1.shape[-1], relu=True,
+                           workspace=ws)
+                self._calib_scale(blk + ".c2", f1, stream)
+                ax.axq_quantize(f1, self._s(blk + ".c2"), bits, q1, stream)
+                self._conv(blk + ".c2", q1, N, h, w, stream, y=f2, ldy=f2.shape[-1], relu=True,
+                           workspace=ws)
+                self._calib_scale(blk + ".c3", f2, stream)
+                ax.axq_quantize(f2, self._s(blk + ".c3"), bits, q2, stream)
+            else:
+                self._conv(blk + ".c1", q_in, N, h, w, stream, relu=True, q_out=q1,
+                           ldq=q1.shape[-1], d_scale_out=self._s(blk + ".c2"), bits_out=bits,
+                           workspace=ws)
+                self._conv(blk + ".c2", q1, N, h, w, stream, relu=True, q_out=q2,
+                           ldq=q2.shape[-1], d_scale_out=self._s(blk + ".c3"), bits_out=bits,
+                           workspace=ws)
+            out, qout = b[blk + ".out"], b[blk + ".qout"]
+            last = bi == len(self.blocks) - 1
+            nxt = "fc" if last else self.blocks[bi + 1] + ".c1"
+            if calibrate or last:
+                self._conv(blk + ".c3", q2, N, ho, wo, stream, y=out, ldy=out.shape[-1],
+                           residual=r, ldr=r.shape[-1], relu=True, workspace=ws)
+                if not last:
+                    self._calib_scale(nxt, out, stream)
+                    ax.axq_quantize(out, self._s(nxt), bits, qout, stream)
+            else:
+                self._conv(blk + ".c3", q2, N, ho, wo, stream, y=out, ldy=out.shape[-1],
+                           residual=r, ldr=r.shape[-1], relu=True, q_out=qout,
+                           ldq=qout.shape[-1], d_scale_out=self._s(nxt), bits_out=bits,
+                           workspace=ws)
+            q_in, f_in = qout, out
+        # ---- head ----
+        if calibrate:
+            ax.axq_avgpool_nhwc(f_in, y=b["pool_f"], stream=stream)
+            self._calib_scale("fc", b["pool_f"], stream)
+            ax.axq_quantize(b["pool_f"], self._s("fc"), bits, b["fc_q"], stream)
+        else:
+            ax.axq_avgpool_nhwc(f_in, q=b["fc_q"], d_scale=self._s("fc"), bits=bits, stream=stream)
+        lg = b["logits"]
+        ep = ax.make_epilogue(self._s("fc"), self._sw("fc"), bias=self.fc_bias, y=lg,
+                              ldy=lg.shape[-1], workspace=ws)
+        ax.axq_lut_gemm_ep(b["fc_q"], self.qw["fc"], self.lut, ep, stream)
+        if calibrate:
+            self.calibrated = True
+        return lg
+
+    def calibrate(self, x, stream=None):
+        return self.run(x, True, stream)
+
+    def forward(self, x, stream=None):
+        assert self.calibrated, "calibrate() first (static per-layer scales)"
+        return self.run(x, False, stream)
+
+    __call__ = forward
+
+    def lookups_per_image(self, H=224, W=224) -> int:
+        tot = 0
+        h, w = H, W
+        for name, kind, cout, cin, k, stride, pad in self.specs:
+            if kind == "fc":
+                tot += cout * cin
+                continue
+            if name == "stem":
+                ho, wo = _out(h, k, stride, pad), _out(w, k, stride, pad)
+                tot += ho * wo * cout * cin * k * k
+                h, w = _out(ho, 3, 2, 1), _out(wo, 3, 2, 1)
+                blk_in = (h, w)
+                continue
+            if name.endswith(".c1"):
+                blk_in = (h, w)
+                hi, wi = blk_in
+            elif name.endswith(".down"):
+                hi, wi = blk_in
+            else:
+                hi, wi = h, w
+            ho, wo = _out(hi, k, stride, pad), _out(wi, k, stride, pad)
+            tot += ho * wo * cout * cin * k * k
+            if not name.endswith(".down"):
+                h, w = ho, wo
+        return tot

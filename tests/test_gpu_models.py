@@ -1,0 +1,98 @@
+"""GPU parity for the model drivers (a7 rows): ResNet-50-shaped forward (BJ configs[3]) and the
+LSTM (BJ configs[4]) on the C ABI against the oracle models.  Everything the GPU computes is
+pinned fp32 glue around exact integer LUT sums, so logits / hidden states are compared bit for
+bit (the 1e-6 relative bound is asserted first)."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+from oracle import models
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+REDUCED = dict(widths=(16, 32, 16, 32), blocks=(1, 2, 1, 1), stem_ch=16, num_classes=24)
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float((np.abs(a - b) / np.maximum(np.abs(b), 1e-30)).max())
+
+
+def _gpu_resnet(lut_np, bits, config, **topo):
+    from paper_2203_04071_b200 import Lut
+    from paper_2203_04071_b200.resnet import ApproxResNet, layer_specs
+    W = datagen.network_weights(layer_specs(**topo), config)
+    return ApproxResNet(W, Lut(bits, lut_np), DEV, **topo)
+
+
+@pytest.mark.parametrize("bits", [8, 6])
+def test_resnet_reduced_bit_exact(bits):
+    lut = datagen.lut_randerr(bits, 3, 50 + bits)
+    x = datagen.normal(33, bits, (3, 3, 40, 36))
+    net = _gpu_resnet(lut, bits, 33, **REDUCED)
+    orc = models.ResNetOracle(lut, bits, config=33, **REDUCED)
+    xd = torch.from_numpy(x).to(DEV)
+    net.calibrate(xd[:2])
+    scales = orc.calibrate(x[:2])
+    for name, s in scales.items():
+        assert net.s_act[net.slot[name]].item() == s, name
+    y = net.forward(xd).cpu().numpy()
+    ref = orc.forward(x, scales)
+    assert _rel(y, ref) <= 1e-6
+    np.testing.assert_array_equal(y, ref)
+
+
+def test_resnet50_config3_full_batch_sampled():
+    """BJ configs[3] at full size: calibrate on images 0-7, forward all 256 images on one GPU
+    (the bench launch configuration); the oracle recomputes images 0 and 255."""
+    lut = datagen.lut_randerr(8, 0, 2)                       # A15: c0's table
+    net = _gpu_resnet(lut, 8, 3)
+    orc = models.ResNetOracle(lut, 8, config=3)
+    x = datagen.config3_images(256)
+    xd = torch.from_numpy(x).to(DEV)
+    net.calibrate(xd[:8])
+    scales = orc.calibrate(x[:8])
+    for name, s in scales.items():
+        assert net.s_act[net.slot[name]].item() == s, name
+    y = net.forward(xd).cpu().numpy()
+    for i in (0, 255):
+        ref = orc.forward(x[i:i + 1], scales)
+        assert _rel(y[i:i + 1], ref) <= 1e-6
+        np.testing.assert_array_equal(y[i:i + 1], ref)
+
+
+@pytest.mark.parametrize("bits", [4, 6, 8])
+def test_lstm_reduced_bit_exact(bits):
+    from paper_2203_04071_b200 import Lut
+    from paper_2203_04071_b200.lstm import ApproxLSTM
+    c = datagen.config4(T=7, B=5, I=48, H=40)
+    net = ApproxLSTM(c.W_ih, c.W_hh, c.b_ih, c.b_hh, Lut(bits, c.luts[bits]), DEV)
+    orc = models.LstmOracle(c, bits)
+    xd = torch.from_numpy(c.x).to(DEV)
+    net.calibrate(xd)
+    s_x, s_h = orc.calibrate()
+    assert net.s_x.item() == s_x and net.s_h.item() == s_h
+    hs, cT = net.forward(xd)
+    hs_ref, c_ref = orc.forward((s_x, s_h))
+    np.testing.assert_array_equal(hs.cpu().numpy(), hs_ref)
+    np.testing.assert_array_equal(cT.cpu().numpy(), c_ref)
+
+
+@pytest.mark.parametrize("bits", [4, 6, 8])
+def test_lstm_config4_full(bits):
+    """BJ configs[4] at full size (input 512, hidden 1024, seq 128, batch 64)."""
+    from paper_2203_04071_b200 import Lut
+    from paper_2203_04071_b200.lstm import ApproxLSTM
+    c = datagen.config4()
+    net = ApproxLSTM(c.W_ih, c.W_hh, c.b_ih, c.b_hh, Lut(bits, c.luts[bits]), DEV)
+    orc = models.LstmOracle(c, bits)
+    xd = torch.from_numpy(c.x).to(DEV)
+    net.calibrate(xd)
+    s_x, s_h = orc.calibrate()
+    assert net.s_x.item() == s_x and net.s_h.item() == s_h
+    hs, cT = net.forward(xd)
+    hs_ref, c_ref = orc.forward((s_x, s_h))
+    np.testing.assert_array_equal(hs.cpu().numpy(), hs_ref)
+    np.testing.assert_array_equal(cT.cpu().numpy(), c_ref)

@@ -291,3 +291,99 @@ def test_config2_conv_sampled_images(ax):
         got = y[img:img + 1].cpu().numpy()
         assert _fp_close(got, ref, sa, sw) <= REL_TOL
         np.testing.assert_array_equal(got, ref)
+
+
+# ----------------------------------------------------------------------------------------
+# fused epilogue variants and model glue kernels
+# ----------------------------------------------------------------------------------------
+
+def test_conv_fused_residual_relu_requantize(ax):
+    Nb, C, H, Wd, K = 2, 32, 9, 7, 48
+    X = datagen.random_int8(120, (Nb, C, H, Wd))
+    Wt = datagen.random_int8(121, (K, C, 3, 3))
+    T = datagen.lut_randerr(8, 0, 2)
+    acc = oracle.lut_conv2d(X, Wt, T, 8, (1, 1), (1, 1)).transpose(0, 2, 3, 1)   # NHWC
+    sa, sw, so = np.float32(0.013), np.float32(0.0041), np.float32(0.05)
+    res = datagen.normal(122, 0, acc.shape, 2.0)
+    v = (acc.astype(np.float32) * np.float32(sa * sw)).astype(np.float32)
+    v = (v + res).astype(np.float32)
+    v = np.where(v > 0, v, np.float32(0)).astype(np.float32)
+    q_ref = oracle.quantize(v, so, 8)
+    lut = ax.Lut(8, T)
+    d = ax.conv_desc(Nb, H, Wd, C, K, 3, 3, (1, 1), (1, 1))
+    y = torch.empty(acc.shape, device=DEV)
+    q = torch.empty(acc.shape, dtype=torch.int8, device=DEV)
+    for ws in (None, torch.empty(acc.size, dtype=torch.int32, device=DEV)):
+        ep = ax.make_epilogue(_t(np.array([sa])), _t(np.array([sw])), y=y, ldy=K, workspace=ws,
+                              residual=_t(res), ldr=K, relu=True, y_nhwc=True, q_out=q, ldq=K,
+                              d_scale_out=_t(np.array([so])), bits_out=8)
+        ax.axq_lut_conv2d_ep(d, _t(X.transpose(0, 2, 3, 1)), _t(Wt.transpose(0, 2, 3, 1)), lut, ep)
+        np.testing.assert_array_equal(y.cpu().numpy(), v)
+        np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
+    lut.close()
+
+
+def test_conv_padded_channels_c_valid(ax):
+    """C = 3 stored as C = 4 with a zero channel: c_valid removes the padding lookups."""
+    X = datagen.random_int8(130, (2, 3, 20, 18))
+    Wt = datagen.random_int8(131, (16, 3, 7, 7))
+    T = datagen.lut_randerr(8, 0, 2)
+    ref = oracle.lut_conv2d(X, Wt, T, 8, (2, 2), (3, 3))
+    Xp = np.zeros((2, 20, 18, 4), np.int8)
+    Xp[..., :3] = X.transpose(0, 2, 3, 1)
+    Wp = np.zeros((16, 7, 7, 4), np.int8)
+    Wp[..., :3] = Wt.transpose(0, 2, 3, 1)
+    lut = ax.Lut(8, T)
+    d = ax.conv_desc(2, 20, 18, 4, 16, 7, 7, (2, 2), (3, 3), c_valid=3)
+    Ho, Wo = ax.axq_conv2d_out_hw(d)
+    Y = torch.empty(2, Ho, Wo, 16, dtype=torch.int32, device=DEV)
+    ax.axq_lut_conv2d(d, _t(Xp), _t(Wp), lut, Y)
+    np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
+    lut.close()
+
+
+def test_maxpool_int8(ax):
+    from oracle.models import _maxpool
+    x = datagen.random_int8(140, (2, 13, 11, 12))          # NHWC codes
+    y = torch.empty(2, 7, 6, 12, dtype=torch.int8, device=DEV)
+    ax.axq_maxpool2d_nhwc_i8(_t(x), 3, 3, 2, 1, y)
+    ref = _maxpool(x.transpose(0, 3, 1, 2).astype(np.float32)).transpose(0, 2, 3, 1)
+    np.testing.assert_array_equal(y.cpu().numpy(), ref.astype(np.int8))
+    x3 = datagen.random_int8(141, (1, 9, 9, 6))            # C % 4 != 0: byte kernel
+    y3 = torch.empty(1, 5, 5, 6, dtype=torch.int8, device=DEV)
+    ax.axq_maxpool2d_nhwc_i8(_t(x3), 3, 3, 2, 1, y3)
+    ref3 = _maxpool(x3.transpose(0, 3, 1, 2).astype(np.float32)).transpose(0, 2, 3, 1)
+    np.testing.assert_array_equal(y3.cpu().numpy(), ref3.astype(np.int8))
+
+
+def test_avgpool_and_quantize(ax):
+    from oracle.models import _avgpool
+    x = np.abs(datagen.normal(150, 0, (3, 7, 7, 40), 3.0))  # NHWC
+    s = np.float32(0.021)
+    y = torch.empty(3, 40, device=DEV)
+    q = torch.empty(3, 40, dtype=torch.int8, device=DEV)
+    ax.axq_avgpool_nhwc(_t(x), y=y, q=q, d_scale=_t(np.array([s])), bits=8)
+    ref = _avgpool(x.transpose(0, 3, 1, 2))
+    np.testing.assert_array_equal(y.cpu().numpy(), ref)
+    np.testing.assert_array_equal(q.cpu().numpy(), oracle.quantize(ref, s, 8))
+
+
+def test_lstm_cell(ax):
+    from oracle.models import pinned_sigmoid, pinned_tanh
+    B, H = 5, 33
+    gih = datagen.normal(160, 0, (B, 4 * H), 3.0)
+    ghh = datagen.normal(160, 1, (B, 4 * H), 3.0)
+    c0 = datagen.normal(160, 2, (B, H))
+    g = (gih + ghh).astype(np.float32)
+    i_, f_ = pinned_sigmoid(g[:, :H]), pinned_sigmoid(g[:, H:2 * H])
+    g_, o_ = pinned_tanh(g[:, 2 * H:3 * H]), pinned_sigmoid(g[:, 3 * H:])
+    c_ref = ((f_ * c0).astype(np.float32) + (i_ * g_).astype(np.float32)).astype(np.float32)
+    h_ref = (o_ * pinned_tanh(c_ref)).astype(np.float32)
+    s = np.float32(1.0 / 127)
+    c = _t(c0)
+    h = torch.empty(B, H, device=DEV)
+    q = torch.empty(B, H, dtype=torch.int8, device=DEV)
+    ax.axq_lstm_cell(_t(gih), _t(ghh), c, h, q_h=q, d_scale_h=_t(np.array([s])), bits=8)
+    np.testing.assert_array_equal(c.cpu().numpy(), c_ref)
+    np.testing.assert_array_equal(h.cpu().numpy(), h_ref)
+    np.testing.assert_array_equal(q.cpu().numpy(), oracle.quantize(h_ref, s, 8))
