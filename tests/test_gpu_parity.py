@@ -313,11 +313,13 @@ def test_conv_fused_residual_relu_requantize(ax):
     d = ax.conv_desc(Nb, H, Wd, C, K, 3, 3, (1, 1), (1, 1))
     y = torch.empty(acc.shape, device=DEV)
     q = torch.empty(acc.shape, dtype=torch.int8, device=DEV)
+    # the epilogue struct holds raw pointers: keep every tensor alive until the launch
+    dsa, dsw, dso, dres = _t(np.array([sa])), _t(np.array([sw])), _t(np.array([so])), _t(res)
+    dX, dW = _t(X.transpose(0, 2, 3, 1)), _t(Wt.transpose(0, 2, 3, 1))
     for ws in (None, torch.empty(acc.size, dtype=torch.int32, device=DEV)):
-        ep = ax.make_epilogue(_t(np.array([sa])), _t(np.array([sw])), y=y, ldy=K, workspace=ws,
-                              residual=_t(res), ldr=K, relu=True, y_nhwc=True, q_out=q, ldq=K,
-                              d_scale_out=_t(np.array([so])), bits_out=8)
-        ax.axq_lut_conv2d_ep(d, _t(X.transpose(0, 2, 3, 1)), _t(Wt.transpose(0, 2, 3, 1)), lut, ep)
+        ep = ax.make_epilogue(dsa, dsw, y=y, ldy=K, workspace=ws, residual=dres, ldr=K,
+                              relu=True, y_nhwc=True, q_out=q, ldq=K, d_scale_out=dso, bits_out=8)
+        ax.axq_lut_conv2d_ep(d, dX, dW, lut, ep)
         np.testing.assert_array_equal(y.cpu().numpy(), v)
         np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
     lut.close()
