@@ -1,19 +1,22 @@
 #!/usr/bin/env python3
 """bench.py -- approximate GMAC/s (LUT lookups/s) of the AdaPT LUT layer hot path on B200.
 
-One "step" is one pass of the whole hot path (plus a8 at N>1) over
-one batch of BASELINE.json configs[2] (the approximate conv2d layer; DESIGN.md §6 says why
-this config carries the headline number):
-    amax(x) -> scale -> quantize NCHW fp32 -> NHWC int8 -> implicit-im2col LUT-conv with the
-    dequantize epilogue -> fp32 NCHW y
-Weights and the ACU table are prepared once, untimed (row a1/a2).
+One "step" is one pass of the whole hot path over one batch of the
+workload:
+  resnet (default, BJ configs[3]): the ResNet-50-shaped approximate forward of the 256-image
+      batch -- quantize the fp32 input, 54 LUT layers with fused dequant / residual / ReLU /
+      requantize epilogues, int8 maxpool, avgpool, fc -- batch-sharded over the N GPUs
+      (strong scaling: 256/N images per rank) with an NCCL all-gather of the logits (a8).
+  conv (BJ configs[2]), linear (BJ configs[1]): one approximate layer (a3-a6).
+  lstm (BJ configs[4]): the 128-step LSTM at b = 4, 6 and 8 (replicas at N > 1).
+Weights, the ACU table and the static per-layer scales (calibration) are prepared once,
+untimed (rows a1/a2, "learns offline").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload conv|linear]
+                    [--workload resnet|conv|linear|lstm]
 
-Prints ONE JSON line (rank 0).  Multi-GPU: launched by torchrun, one rank per GPU over
-NCCL; weak scaling (each rank runs its own batch; no data-path collective -- the batch is
-the unit the method partitions); time = max over ranks of the CUDA-event time.
+Prints ONE JSON line (rank 0).  Multi-GPU: launched by torchrun, one rank per GPU over NCCL;
+time = max over ranks of the CUDA-event time.
 """
 from __future__ import annotations
 
@@ -38,13 +41,16 @@ LANES = 32
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="conv", choices=["conv", "linear"])
+    ap.add_argument("--workload", default="resnet", choices=["resnet", "conv", "linear", "lstm"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = {"resnet": 10, "lstm": 5, "conv": 50, "linear": 200}[a.workload]
+    return a
 
 
 def measured_peaks():
@@ -149,38 +155,243 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
-# workloads
+# workloads (ours)
 # ---------------------------------------------------------------------------------------
-def conv_workload(rank: int):
-    import datagen
-    c = datagen.config2()
-    Nb, C, H, W = c.x.shape
-    K, _, R, S = c.W.shape
-    lookups = Nb * H * W * K * C * R * S          # stride 1, pad 1: Ho = H, Wo = W
-    desc = {"workload": "BJ configs[2]: approximate conv2d, x fp32 [128,64,56,56] ReLU(N(0,1)), "
-                        "W 64x64x3x3 Kaiming, stride 1 pad 1, int8 per-tensor max calibration, "
-                        "randerr LUT (exact + U[-64,64]), implicit im2col, fp32 NCHW output",
-            "lookups_per_step": lookups, "batch_per_gpu": Nb}
-    return c, lookups, desc
+class KernelTimer:
+    """CUDA events around every LUT-kernel launch (on the launching stream)."""
+
+    def __init__(self):
+        self.enabled = False
+        self.pairs = []
+
+    def __call__(self, kind, stream):
+        if not self.enabled:
+            return
+        import torch
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        if kind == "pre":
+            self.pairs.append([ev, None])
+        else:
+            self.pairs[-1][1] = ev
+
+    def total_ms(self):
+        return sum(a.elapsed_time(b) for a, b in self.pairs)
+
+    def reset(self):
+        self.pairs = []
 
 
-def linear_workload(rank: int):
-    import datagen
-    c = datagen.config1()
-    M, K = c.x.shape
-    N = c.W.shape[0]
-    desc = {"workload": "BJ configs[1]: approximate linear, x fp32 [256x1024], W [1024x1024], "
-                        "trunc4 LUT, fp32 output", "lookups_per_step": M * N * K}
-    return c, M * N * K, desc
+class ResNetWL:
+    name = "resnet"
+    scaling = "strong"
+
+    def __init__(self, dev, rank, world, timer):
+        import torch
+        import datagen
+        from paper_2203_04071_b200 import Lut
+        from paper_2203_04071_b200.resnet import ApproxResNet, layer_specs
+        self.dev, self.rank, self.world = dev, rank, world
+        total = 256
+        assert total % world == 0
+        self.per = total // world
+        x_all = datagen.config3_images(total)
+        self.x_host = torch.from_numpy(x_all[rank * self.per:(rank + 1) * self.per]).pin_memory()
+        self.x = self.x_host.to(dev)
+        self.lut = Lut(8, datagen.lut_randerr(8, 0, 2))          # A15: c0's table
+        self.net = ApproxResNet(datagen.network_weights(layer_specs(), 3), self.lut, dev)
+        self.net.calibrate(torch.from_numpy(x_all[:8]).to(dev))   # static scales, untimed
+        torch.cuda.synchronize()
+        self.net.timing_hook = timer
+        self.lookups_rank = self.per * self.net.lookups_per_image()
+        self.lookups_total = total * self.net.lookups_per_image()
+        self.logits_all = torch.empty(total, 1000, device=dev)
+        self.out_host = torch.empty(total, 1000).pin_memory()
+        self.launches = 53 + 1 + 1 + 1 + 1 + 0      # 53 convs, fc, quantize, maxpool, avgpool
+        self.in_bytes = self.x.numel() * 4
+        self.out_bytes = self.logits_all.numel() * 4 if rank == 0 else 0
+        self.desc = {"workload": "BJ configs[3]: ResNet-50-shaped approximate forward (53 convs + "
+                                 "fc, every multiply a LUT lookup), x fp32 [256,3,224,224] N(0,1), "
+                                 "Kaiming weights, randerr int8 LUT (c0's), static per-layer "
+                                 "max calibration on images 0-7 (untimed)",
+                     "global_batch": total, "batch_per_gpu": self.per,
+                     "lookups_per_image": self.net.lookups_per_image()}
+
+    def step(self, stream, dist):
+        lg = self.net.forward(self.x, stream)
+        if dist is not None:
+            dist.all_gather_into_tensor(self.logits_all, lg)     # a8: collect the outputs
+        else:
+            self.logits_all.copy_(lg)
+
+    def h2d(self):
+        self.x.copy_(self.x_host, non_blocking=True)
+
+    def d2h(self):
+        if self.rank == 0:
+            self.out_host.copy_(self.logits_all, non_blocking=True)
 
 
-# ---------------------------------------------------------------------------------------
-# our implementation
-# ---------------------------------------------------------------------------------------
+class ConvWL:
+    name = "conv"
+    scaling = "weak"
+
+    def __init__(self, dev, rank, world, timer):
+        import torch
+        import datagen
+        from paper_2203_04071_b200 import Lut
+        from paper_2203_04071_b200 import _lib as ax
+        from paper_2203_04071_b200.layers import ApproxConv2d
+        self.ax = ax
+        c = datagen.config2()
+        self.c = c
+        self.lut = Lut(8, c.lut)
+        self.layer = ApproxConv2d(torch.from_numpy(c.W).to(dev), None, self.lut, c.stride, c.pad)
+        self.x_host = torch.from_numpy(c.x).pin_memory()
+        self.x = self.x_host.to(dev)
+        Nb, C, H, W = self.x.shape
+        self.d = self.layer.desc(Nb, H, W)
+        Ho, Wo = ax.axq_conv2d_out_hw(self.d)
+        self.y = torch.empty(Nb, self.layer.Kout, Ho, Wo, device=dev)
+        self.qx = torch.empty(Nb, H, W, C, dtype=torch.int8, device=dev)
+        self.y_host = torch.empty(self.y.shape).pin_memory()
+        self.timer = timer
+        self.lookups_rank = Nb * Ho * Wo * self.layer.Kout * C * 9
+        self.lookups_total = self.lookups_rank * world
+        self.launches = 4
+        self.in_bytes, self.out_bytes = self.x.numel() * 4, self.y.numel() * 4
+        self.desc = {"workload": "BJ configs[2]: approximate conv2d, x fp32 [128,64,56,56] "
+                                 "ReLU(N(0,1)), W 64x64x3x3 Kaiming, stride 1 pad 1, int8 dynamic "
+                                 "per-tensor max calibration, randerr LUT, implicit im2col, fp32 "
+                                 "NCHW output", "batch_per_gpu": Nb}
+
+    def step(self, stream, dist):
+        ax, L = self.ax, self.layer
+        ax.axq_amax(self.x, L.d_amax_a, stream)
+        ax.axq_scale(L.d_amax_a, 8, L.d_scale_a, stream)
+        ax.axq_quantize_nchw_to_nhwc(self.x, L.d_scale_a, 8, self.qx, stream)
+        self.timer("pre", stream)
+        ax.axq_lut_conv2d_dq(self.d, self.qx, L.qw, self.lut, L.d_scale_a, L.d_scale_w, None,
+                             self.y, stream=stream)
+        self.timer("post", stream)
+
+    def h2d(self):
+        self.x.copy_(self.x_host, non_blocking=True)
+
+    def d2h(self):
+        self.y_host.copy_(self.y, non_blocking=True)
+
+
+class LinearWL:
+    name = "linear"
+    scaling = "weak"
+
+    def __init__(self, dev, rank, world, timer):
+        import torch
+        import datagen
+        from paper_2203_04071_b200 import Lut
+        from paper_2203_04071_b200 import _lib as ax
+        from paper_2203_04071_b200.layers import ApproxLinear
+        self.ax = ax
+        c = datagen.config1()
+        self.lut = Lut(8, c.lut)
+        self.layer = ApproxLinear(torch.from_numpy(c.W).to(dev), torch.from_numpy(c.b).to(dev), self.lut)
+        self.x_host = torch.from_numpy(c.x).pin_memory()
+        self.x = self.x_host.to(dev)
+        M = self.x.shape[0]
+        self.y = torch.empty(M, self.layer.N, device=dev)
+        self.bufs = self.layer.buffers(M, dev)
+        self.y_host = torch.empty(self.y.shape).pin_memory()
+        self.timer = timer
+        self.lookups_rank = M * self.layer.N * self.layer.K
+        self.lookups_total = self.lookups_rank * world
+        self.launches = 5
+        self.in_bytes, self.out_bytes = self.x.numel() * 4, self.y.numel() * 4
+        self.desc = {"workload": "BJ configs[1]: approximate linear, x fp32 [256x1024] N(0,1), W "
+                                 "[1024x1024] N(0,0.02), bias N(0,0.01), trunc4 LUT, fp32 output"}
+
+    def step(self, stream, dist):
+        ax, L = self.ax, self.layer
+        ax.axq_amax(self.x, L.d_amax_a, stream)
+        ax.axq_scale(L.d_amax_a, 8, L.d_scale_a, stream)
+        ax.axq_quantize(self.x, L.d_scale_a, 8, self.bufs["qa"], stream)
+        self.timer("pre", stream)
+        ax.axq_lut_gemm_dq(self.bufs["qa"], L.qw, self.lut, L.d_scale_a, L.d_scale_w, L.bias,
+                           self.y, workspace=self.bufs["ws"], stream=stream)
+        self.timer("post", stream)
+
+    def h2d(self):
+        self.x.copy_(self.x_host, non_blocking=True)
+
+    def d2h(self):
+        self.y_host.copy_(self.y, non_blocking=True)
+
+
+class LstmWL:
+    name = "lstm"
+    scaling = "weak"
+
+    def __init__(self, dev, rank, world, timer):
+        import torch
+        import datagen
+        from paper_2203_04071_b200 import Lut
+        from paper_2203_04071_b200.lstm import ApproxLSTM
+        c = datagen.config4()
+        self.x_host = torch.from_numpy(c.x).pin_memory()
+        self.x = self.x_host.to(dev)
+        self.nets = {}
+        for b in (4, 6, 8):
+            n = ApproxLSTM(c.W_ih, c.W_hh, c.b_ih, c.b_hh, Lut(b, c.luts[b]), dev)
+            n.calibrate(self.x)
+            n.timing_hook = timer
+            self.nets[b] = n
+        torch.cuda.synchronize()
+        T, B, _ = self.x.shape
+        per_b = self.nets[8].lookups(T, B)
+        self.lookups_rank = 3 * per_b
+        self.lookups_total = self.lookups_rank * world
+        self.launches = 3 * (2 + T * 5)
+        self.in_bytes = self.x.numel() * 4
+        self.out_bytes = 3 * T * B * 1024 * 4
+        self.h_host = torch.empty(3, T, B, 1024).pin_memory()
+        self.per_bit_ms = {}
+        self.desc = {"workload": "BJ configs[4]: LSTM input 512, hidden 1024, seq 128, batch 64, "
+                                 "approximate ih/hh gate GEMMs at b = 4, 6, 8 (randerr LUTs), "
+                                 "static scales calibrated untimed", "lookups_per_bitwidth": per_b}
+
+    def step(self, stream, dist):
+        import torch
+        for b, n in self.nets.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            n.forward(self.x, stream)
+            e1.record(stream)
+            self.per_bit_ms.setdefault(b, []).append((e0, e1))
+
+    def h2d(self):
+        self.x.copy_(self.x_host, non_blocking=True)
+
+    def d2h(self):
+        for i, n in enumerate(self.nets.values()):
+            hs, _ = n._bufs[(self.x.shape[0], self.x.shape[1])]["hs"], None
+            self.h_host[i].copy_(hs, non_blocking=True)
+
+    def extra(self):
+        out = {}
+        for b, ev in self.per_bit_ms.items():
+            out["b%d_ms" % b] = round(statistics.median(a.elapsed_time(c) for a, c in ev), 3)
+        if all(k in out for k in ("b4_ms", "b6_ms", "b8_ms")):
+            out["ratio_b6_b4"] = round(out["b6_ms"] / out["b4_ms"], 3)
+            out["ratio_b8_b6"] = round(out["b8_ms"] / out["b6_ms"], 3)
+            out["paper_ratio_per_2_bits"] = "~2.1x (P:322, Xeon AVX2)"
+        return out
+
+
+WORKLOADS = {"resnet": ResNetWL, "conv": ConvWL, "linear": LinearWL, "lstm": LstmWL}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
-    import paper_2203_04071_b200 as axq
-    from paper_2203_04071_b200 import _lib as ax
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -189,67 +400,17 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    if args.workload == "conv":
-        c, lookups, desc = conv_workload(rank)
-    else:
-        c, lookups, desc = linear_workload(rank)
-    bits = c.bits
-    lut = axq.Lut(bits, c.lut)
+    timer = KernelTimer()
+    wl = WORKLOADS[args.workload](dev, rank, world, timer)
     stream = torch.cuda.current_stream()
-
-    if args.workload == "conv":
-        from paper_2203_04071_b200.layers import ApproxConv2d
-        layer = ApproxConv2d(torch.from_numpy(c.W).to(dev), None, lut, c.stride, c.pad)
-        x_host = torch.from_numpy(c.x).pin_memory()
-        x = x_host.to(dev)
-        Nb, C, H, W = x.shape
-        d = layer.desc(Nb, H, W)
-        Ho, Wo = ax.axq_conv2d_out_hw(d)
-        y = torch.empty(Nb, layer.Kout, Ho, Wo, device=dev)
-        qx = torch.empty(Nb, H, W, C, dtype=torch.int8, device=dev)
-        y_host = torch.empty(y.shape, dtype=torch.float32).pin_memory()
-
-        def step(ev_pair=None):
-            ax.axq_amax(x, layer.d_amax_a, stream)
-            ax.axq_scale(layer.d_amax_a, bits, layer.d_scale_a, stream)
-            ax.axq_quantize_nchw_to_nhwc(x, layer.d_scale_a, bits, qx, stream)
-            if ev_pair:
-                ev_pair[0].record(stream)
-            ax.axq_lut_conv2d_dq(d, qx, layer.qw, lut, layer.d_scale_a, layer.d_scale_w, None,
-                                 y, stream=stream)
-            if ev_pair:
-                ev_pair[1].record(stream)
-        launches_per_step = 4       # amax, scale, quantize, LUT-conv(+dequant)
-        in_bytes, out_bytes = x.numel() * 4, y.numel() * 4
-    else:
-        from paper_2203_04071_b200.layers import ApproxLinear
-        layer = ApproxLinear(torch.from_numpy(c.W).to(dev), torch.from_numpy(c.b).to(dev), lut)
-        x_host = torch.from_numpy(c.x).pin_memory()
-        x = x_host.to(dev)
-        M = x.shape[0]
-        y = torch.empty(M, layer.N, device=dev)
-        bufs = layer.buffers(M, dev)
-        y_host = torch.empty(y.shape, dtype=torch.float32).pin_memory()
-
-        def step(ev_pair=None):
-            ax.axq_amax(x, layer.d_amax_a, stream)
-            ax.axq_scale(layer.d_amax_a, bits, layer.d_scale_a, stream)
-            ax.axq_quantize(x, layer.d_scale_a, bits, bufs["qa"], stream)
-            if ev_pair:
-                ev_pair[0].record(stream)
-            ax.axq_lut_gemm_dq(bufs["qa"], layer.qw, lut, layer.d_scale_a, layer.d_scale_w,
-                               layer.bias, y, workspace=bufs["ws"], stream=stream)
-            if ev_pair:
-                ev_pair[1].record(stream)
-        launches_per_step = 6       # amax, scale, quantize, LUT-GEMM (split-K), dequant + memset
-        in_bytes, out_bytes = x.numel() * 4, y.numel() * 4
-
-    # L2 flush buffer (> 126 MB L2) written between timed steps, outside the timed region
+    # L2 flush buffer (> 126 MB L2) written before every timed step, outside the timed region
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     for _ in range(max(args.warmup, 0)):
-        step()
+        wl.step(stream, dist)
     torch.cuda.synchronize()
+    if hasattr(wl, "per_bit_ms"):
+        wl.per_bit_ms.clear()
 
     step_ms, kern_ms = [], []
     if dist:
@@ -259,13 +420,15 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(args.steps):
             flush.fill_(1.0)
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            timer.reset()
+            timer.enabled = True
             s0.record(stream)
-            step((k0, k1))
+            wl.step(stream, dist)
             s1.record(stream)
             s1.synchronize()
+            timer.enabled = False
             step_ms.append(s0.elapsed_time(s1))
-            kern_ms.append(k0.elapsed_time(k1))
+            kern_ms.append(timer.total_ms())
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -275,18 +438,18 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = t.item()
 
-    # e2e: the same step through the public API with HOST buffers (pinned), H2D of the
-    # inputs and D2H of the result inside the timed region.
     e2e = None
     if not args.no_e2e:
         e_ms = []
         for _ in range(max(2, min(args.steps, 5))):
             flush.fill_(1.0)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if dist:
+                dist.barrier()
             a.record(stream)
-            x.copy_(x_host, non_blocking=True)
-            step()
-            y_host.copy_(y, non_blocking=True)
+            wl.h2d()
+            wl.step(stream, dist)
+            wl.d2h()
             b.record(stream)
             b.synchronize()
             e_ms.append(a.elapsed_time(b))
@@ -295,9 +458,9 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([e_tot], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_tot = t.item()
-        e2e = {"value": world * lookups * len(e_ms) / (e_tot * 1e-3) / 1e9, "unit": "GMAC/s",
-               "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes,
-               "ms_per_step": e_tot / len(e_ms)}
+        e2e = {"value": round(wl.lookups_total * len(e_ms) / (e_tot * 1e-3) / 1e9, 3),
+               "unit": "GMAC/s", "h2d_bytes_per_step": wl.in_bytes,
+               "d2h_bytes_per_step": wl.out_bytes, "ms_per_step": round(e_tot / len(e_ms), 4)}
 
     result = None
     if rank == 0:
@@ -305,36 +468,39 @@ def run_ours(args, rank, world, local_rank):
         sm = torch.cuda.get_device_properties(dev).multi_processor_count
         clocks = clk.summary()
         f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-        roof_max = sm * LANES * f_max / 1e9                              # Glookups/s
+        roof = sm * LANES * f_max / 1e9                                  # Glookups/s
         kmean = statistics.mean(kern_ms)
-        achieved = lookups / (kmean * 1e-3) / 1e9
-        value = world * lookups * args.steps / (total_ms * 1e-3) / 1e9
-        f_meas = (clocks["sm_mhz"] or 0) * 1e6
+        achieved = wl.lookups_rank / (kmean * 1e-3) / 1e9
+        value = wl.lookups_total * args.steps / (total_ms * 1e-3) / 1e9
+        f_meas = (clocks.get("sm_mhz") or 0) * 1e6
+        cfg = dict(wl.desc, parallelism="dp%d (%s)" % (world, "batch-sharded, NCCL all-gather "
+                   "of logits" if wl.scaling == "strong" else "independent replicas"),
+                   l2="flushed before every timed step (256 MiB write)", lut_repr=wl.lut.repr
+                   if hasattr(wl, "lut") else "delta8")
+        if hasattr(wl, "extra"):
+            cfg.update(wl.extra())
         result = {
             "metric": "approximate GMAC/s (LUT lookups/s) per B200 and % of smem-lookup roofline",
             "value": round(value, 3), "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
-            "data": "synthetic (seeded; DESIGN.md input recipe)",
-            "config": dict(desc, parallelism="dp%d (batch-sharded replicas)" % world,
-                           l2="flushed between timed steps (256 MiB write)",
-                           lut_repr=lut.repr),
-            "roofline": {"bound": "smem", "kernel": "lut_mm_kernel (axq_lut_conv2d_dq)"
-                         if args.workload == "conv" else "lut_mm_kernel (axq_lut_gemm_dq)",
-                         "achieved": round(achieved, 2), "peak": round(roof_max, 2),
-                         "unit": "Glookup/s", "frac": round(achieved / roof_max, 4),
-                         "peak_basis": "%d SMs x 32 lanes x %.0f MHz (%s sm_max_mhz); one "
-                                       "shared-memory wavefront per SM clock" %
-                                       (sm, f_max / 1e6, peak_src),
+            "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic (seeded; DESIGN.md input recipe), random-init weights",
+            "config": cfg,
+            "roofline": {"bound": "smem", "kernel": "lut_mm_kernel (all LUT-GEMM/conv launches "
+                         "of the step, CUDA events around each)",
+                         "achieved": round(achieved, 2), "peak": round(roof, 2),
+                         "unit": "Glookup/s", "frac": round(achieved / roof, 4),
+                         "peak_basis": "%d SMs x 32 lanes x %.0f MHz (%s sm_max_mhz): one "
+                                       "shared-memory wavefront of 32 lookups per SM clock"
+                                       % (sm, f_max / 1e6, peak_src),
                          "frac_at_measured_clock": round(achieved / (sm * LANES * f_meas / 1e9), 4)
                          if f_meas else None,
-                         "kernel_ms": round(kmean, 4),
+                         "kernel_ms_per_step": round(kmean, 4),
                          "kernel_share_of_step": round(kmean / (total_ms / args.steps), 4),
-                         "traffic": committed_traffic("lut_conv_c2" if args.workload == "conv"
-                                                      else "lut_gemm_c1")},
+                         "traffic": committed_traffic(wl.name)},
             "clocks": clocks,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": wl.launches * args.steps,
         }
     if dist:
         dist.barrier()
@@ -345,48 +511,76 @@ def run_ours(args, rank, world, local_rank):
 # ---------------------------------------------------------------------------------------
 # oracle (CPU) timing: cpu_baseline leg and --impl reference
 # ---------------------------------------------------------------------------------------
-def oracle_conv_sample(c, n_img: int):
-    import oracle
-    t0 = time.perf_counter()
-    sa = oracle.scale(oracle.amax(c.x), 8)               # full-tensor calibration, as the GPU
-    qw, sw = oracle.quantize_tensor(c.W, 8)
-    qx = oracle.quantize(c.x[:n_img], sa, 8)
-    acc = oracle.lut_conv2d(qx, qw, c.lut, 8, c.stride, c.pad)
-    oracle.dequantize(acc, sa, sw, None, 1)
-    return time.perf_counter() - t0
+class OracleSample:
+    """A bounded sample of the workload run by the oracle as it stands (all host cores)."""
 
+    def __init__(self, workload):
+        import datagen
+        import oracle
+        self.o = oracle
+        self.w = workload
+        if workload == "resnet":
+            from oracle import models
+            self.lut = datagen.lut_randerr(8, 0, 2)
+            self.net = models.ResNetOracle(self.lut, 8, config=3)
+            self.x = datagen.config3_images(8)
+            self.scales = self.net.calibrate(self.x[:1])      # untimed; values only
+            self.per_unit = models.resnet_macs(self.net.layers)
+            self.unit = "image"
+        elif workload == "conv":
+            self.c = datagen.config2()
+            self.per_unit = self.c.x[0].size * 64 * 9
+            self.unit = "image"
+        elif workload == "linear":
+            self.c = datagen.config1()
+            self.per_unit = 256 * 1024 * 1024
+            self.unit = "full layer"
+        else:
+            from oracle import models
+            c = datagen.config4()
+            self.lstm = models.LstmOracle(c, 8)
+            self.T = c.x.shape[0]
+            self.per_unit = c.x.shape[1] * 4096 * (512 + 1024)
+            self.unit = "time step (b=8)"
 
-def oracle_linear_sample(c, rows: int):
-    import oracle
-    t0 = time.perf_counter()
-    sa = oracle.scale(oracle.amax(c.x), 8)
-    qw, sw = oracle.quantize_tensor(c.W, 8)
-    qa = oracle.quantize(c.x[:rows], sa, 8)
-    acc = oracle.lut_gemm(qa, qw, c.lut, 8)
-    oracle.dequantize(acc, sa, sw, c.b)
-    return time.perf_counter() - t0
+    def run(self, n):
+        o = self.o
+        t0 = time.perf_counter()
+        if self.w == "resnet":
+            self.net.forward(self.x[:n], self.scales)
+        elif self.w == "conv":
+            c = self.c
+            sa = o.scale(o.amax(c.x), 8)
+            qw, sw = o.quantize_tensor(c.W, 8)
+            acc = o.lut_conv2d(o.quantize(c.x[:n], sa, 8), qw, c.lut, 8, c.stride, c.pad)
+            o.dequantize(acc, sa, sw, None, 1)
+        elif self.w == "linear":
+            for _ in range(n):
+                o.linear(self.c.x, self.c.W, self.c.b, self.c.lut, 8)
+        else:
+            c = self.lstm.c
+            keep = c.x
+            c.x = keep[:n]
+            try:
+                self.lstm.run((o.scale(o.amax(keep), 8), np.float32(1.0 / 127)))
+            finally:
+                c.x = keep
+        return time.perf_counter() - t0
 
 
 def cpu_baseline(args, budget_s: float = 12.0):
     import oracle
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
-    threads = oracle.max_threads()
-    if args.workload == "conv":
-        c, lookups, _ = conv_workload(0)
-        per_img = lookups // c.x.shape[0]
-        t1 = oracle_conv_sample(c, 1)
-        n = int(max(1, min(c.x.shape[0], budget_s / max(t1, 1e-3))))
-        t = oracle_conv_sample(c, n)
-        return {"value": round(n * per_img / t / 1e9, 4), "unit": "GMAC/s", "cores": threads,
-                "kind": "oracle",
-                "sample": "%d of 128 images of the same workload (amax/quantize/LUT-conv/"
-                          "dequant, OpenMP over (image, out-channel)), %.1f s" % (n, t)}
-    c, lookups, _ = linear_workload(0)
-    per_row = lookups // c.x.shape[0]
-    t = oracle_linear_sample(c, c.x.shape[0])
-    return {"value": round(lookups / t / 1e9, 4), "unit": "GMAC/s", "cores": threads,
-            "kind": "oracle", "sample": "full workload (%.2f s)" % t}
+    s = OracleSample(args.workload)
+    t1 = s.run(1)
+    cap = {"resnet": 8, "conv": 128, "linear": 50, "lstm": 128}[args.workload]
+    n = int(max(1, min(cap, budget_s / max(t1, 1e-3))))
+    t = s.run(n) if n > 1 else t1
+    return {"value": round(n * s.per_unit / t / 1e9, 4), "unit": "GMAC/s",
+            "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": "%d %s(s) of the same workload, %.1f s (OpenMP parallel-for over the "
+                      "outermost loop, all host cores)" % (n, s.unit, t)}
 
 
 def run_reference(args, rank):
@@ -394,32 +588,28 @@ def run_reference(args, rank):
     if rank != 0:
         return None
     import oracle
-    cores = len(os.sched_getaffinity(0))
-    oracle.set_threads(cores)
-    threads = oracle.max_threads()
-    if args.workload == "conv":
-        c, lookups, desc = conv_workload(0)
-        per_img = lookups // c.x.shape[0]
-        unit_fn = lambda: oracle_conv_sample(c, 1)           # noqa: E731
-        per_step_lookups = per_img
-        sample = "1 of 128 images per step (bounded sample of the same workload)"
-    else:
-        c, lookups, desc = linear_workload(0)
-        unit_fn = lambda: oracle_linear_sample(c, c.x.shape[0])  # noqa: E731
-        per_step_lookups = lookups
-        sample = "full workload per step"
+    oracle.set_threads(len(os.sched_getaffinity(0)))
+    s = OracleSample(args.workload)
     for _ in range(max(args.warmup, 0)):
-        unit_fn()
-    ts = [unit_fn() for _ in range(args.steps)]
+        s.run(1)
+    ts = [s.run(1) for _ in range(args.steps)]
     tot = sum(ts)
-    value = per_step_lookups * args.steps / tot / 1e9
+    value = s.per_unit * args.steps / tot / 1e9
+    base = {"resnet": ("BJ configs[3] ResNet-50-shaped approximate forward", "strong"),
+            "conv": ("BJ configs[2] approximate conv2d", "weak"),
+            "linear": ("BJ configs[1] approximate linear", "weak"),
+            "lstm": ("BJ configs[4] LSTM, b=8", "weak")}[args.workload]
+    sample = "1 %s per step (a bounded sample of the same workload)" % s.unit
     return {"metric": "approximate GMAC/s (LUT lookups/s) per B200 and % of smem-lookup roofline",
             "impl": "reference", "value": round(value, 4), "unit": "GMAC/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
-            "data": "synthetic (seeded)", "config": dict(desc, parallelism="host cores"),
-            "cpu_baseline": {"value": round(value, 4), "unit": "GMAC/s", "cores": threads,
-                             "kind": "oracle", "sample": sample},
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": base[1], "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic (seeded)",
+            "config": {"workload": base[0] + " (oracle on the host cores)",
+                       "parallelism": "OpenMP, host cores"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GMAC/s",
+                             "cores": oracle.max_threads(), "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "GMAC/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 

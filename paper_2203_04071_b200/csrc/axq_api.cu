@@ -86,7 +86,8 @@ axq_status launch_mm(int epi, int loader, int repr, const axq::MMArgs& p, const 
 // Must agree with mm_launch.cuh::launch_cfg: byte-wise loaders and the int32 table only
 // have the SMALL tile instantiated.
 Cfg pick_cfg(int64_t M, int loader, int repr) {
-    const bool big_ok = repr != AXQ_LUT_I32 && (loader == axq::LOAD_GEMM || loader == axq::LOAD_CONV);
+    const bool big_ok = repr != AXQ_LUT_I32 &&
+                        (loader == axq::LOAD_GEMM || loader == axq::LOAD_CONV || loader == axq::LOAD_CONV_C4);
     return (M > 2048 && big_ok) ? CFG_BIG : CFG_SMALL;
 }
 
@@ -431,7 +432,8 @@ static axq_status conv_setup(const axq_conv_desc* d, const int8_t* X, const int8
     p.pad_lookups = (int32_t)(d->R * d->S * (d->C - cv));
     if ((d->C & 15) == 0 && aligned16(X))
         loader = axq::LOAD_CONV;
-    else if ((d->C & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 3) == 0)
+    else if ((d->C & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 3) == 0 &&
+             K <= 4 * axq::MAX_TAP_GROUPS && d->R * d->dil_h < 256 && d->S * d->dil_w < 256)
         loader = axq::LOAD_CONV_C4;
     else
         loader = axq::LOAD_CONV_BYTES;

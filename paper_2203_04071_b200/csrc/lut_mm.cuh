@@ -22,7 +22,8 @@
 //    memory and read with broadcast 16-byte loads.
 //  * K-tail storage padding contributes (0,0) lookups; they are removed exactly by
 //    subtracting npad * LUT[0][0] (semantic conv padding is NOT removed: A11).
-//  * Split-K over gridDim.z (int32 atomics; exact because integer addition is
+//  * Persistent: grid = resident CTAs; each stages the table once and walks the (m, n, k-split)
+//    tiles.  Split-K uses int32 atomics (exact because integer addition is
 //    associative).  Epilogues: raw int32, atomic int32, fused dequant to [M][N] fp32 or to
 //    NCHW fp32 (lanes = consecutive pixels -> coalesced stores).
 #pragma once
@@ -51,7 +52,7 @@ struct MMArgs {
     int table_bytes;
     int32_t t00;        // LUT[0][0] (value of one storage-padding lookup)
     int32_t pad_lookups;  // storage-padding lookups per output inside K (padded channels)
-    int64_t k_split;    // K extent per gridDim.z slice, multiple of KC
+    int64_t k_split;    // K extent per split-K slice, multiple of KC
     // outputs
     int32_t* C_out;     // raw / atomic epilogues
     int64_t ldc;
@@ -105,7 +106,8 @@ __device__ __forceinline__ RowInfo make_row(const MMArgs& p, int64_t m) {
 // Load the 16 activation bytes a[m][k0 .. k0+15] (zeros beyond K or out of range rows;
 // zeros at semantic conv padding taps, which ARE looked up).
 template <int LOADER>
-__device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int64_t k0) {
+__device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int64_t k0,
+                                      const uint32_t* tap_s) {
     uint4 v = make_uint4(0, 0, 0, 0);
     if constexpr (LOADER == LOAD_GEMM) {
         if (ri.valid && k0 + KC <= p.K) return ldg16(p.A + ri.base + k0);
@@ -137,20 +139,21 @@ __device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int6
             v = ldg16(p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c0);
         return v;
     } else if constexpr (LOADER == LOAD_CONV_C4) {
-        // C % 4 == 0: each 4-byte group of the chunk lies inside one filter tap.
+        // C % 4 == 0 (small C, e.g. the padded network input): each 4-byte group of the chunk
+        // lies inside one filter tap; tap offsets come from the per-CTA table built at start.
         if (ri.valid) {
             uint32_t w[4] = {0, 0, 0, 0};
+            const int g0 = (int)(k0 >> 2);
+            const uint4 t4 = *reinterpret_cast<const uint4*>(tap_s + g0);
+            const uint32_t tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int64_t k = k0 + 4 * j;
-                if (k < p.K) {
-                    int rs = (int)(k / p.C);
-                    int c = (int)(k - (int64_t)rs * p.C);
-                    int r = rs / p.S, s = rs - r * p.S;
-                    int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
+                if (k0 + 4 * j < p.K) {
+                    const int hi = ri.hb + (int)(tv[j] & 0xff);
+                    const int wi = ri.wb + (int)((tv[j] >> 8) & 0xff);
                     if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
                         w[j] = __ldg(reinterpret_cast<const uint32_t*>(
-                            p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c));
+                            p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + (tv[j] >> 16)));
                 }
             }
             v = make_uint4(w[0], w[1], w[2], w[3]);
@@ -189,7 +192,7 @@ __device__ __forceinline__ uint4 load_w(const MMArgs& p, int64_t n, int64_t k0, 
 }
 
 template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16) ? 1 : 3)
+__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16) ? 1 : (WARPS >= 8 ? 2 : 3))
 lut_mm_kernel(const MMArgs p) {
     constexpr int NT = WARPS * 32;
     constexpr int BM = WARPS * 32 * R;
@@ -200,20 +203,40 @@ lut_mm_kernel(const MMArgs p) {
     uint32_t* w_s = reinterpret_cast<uint32_t*>(smem + tbytes);
     const int32_t* lut_g = reinterpret_cast<const int32_t*>(p.table);
 
+    uint32_t* tap_s = w_s + 2 * (KC / 4) * TN;   // LOAD_CONV_C4 tap table (K/4 entries)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t m0 = (int64_t)blockIdx.x * BM;
-    const int64_t n0 = (int64_t)blockIdx.y * TN;
-    const int64_t kb = (int64_t)blockIdx.z * p.k_split;
-    const int64_t ke = min(p.K, kb + p.k_split);
-    const int nchunks = (int)((ke - kb + KC - 1) / KC);
     const bool wvec = ((p.ldw & 15) == 0) && ((reinterpret_cast<uintptr_t>(p.W) & 15) == 0);
 
-    // ---- stage the ACU table in shared memory (once per CTA) ----
+    // ---- stage the ACU table in shared memory (once per CTA: the kernel is persistent) ----
     if constexpr (REPR != REPR_I32) {
         const uint4* src = reinterpret_cast<const uint4*>(p.table);
         uint4* dst = reinterpret_cast<uint4*>(lut_s);
         for (int i = tid; i < tbytes / 16; i += NT) dst[i] = __ldg(src + i);
     }
+    if constexpr (LOADER == LOAD_CONV_C4) {
+        // entry g (k = 4g .. 4g+3): r*dh | s*dw << 8 | c << 16, padded with zeros
+        const int ng = (int)((p.K + 3) / 4);
+        for (int g = tid; g < ng + 4; g += NT) {
+            uint32_t e = 0;
+            if (g < ng) {
+                const int k = 4 * g, rs = k / p.C, c = k - rs * p.C, r = rs / p.S, s_ = rs - r * p.S;
+                e = (uint32_t)(r * p.dh) | ((uint32_t)(s_ * p.dw) << 8) | ((uint32_t)c << 16);
+            }
+            tap_s[g] = e;
+        }
+    }
+
+    const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + TN - 1) / TN;
+    const int64_t n_split = (p.K + p.k_split - 1) / p.k_split;
+    const int64_t n_work = m_tiles * n_tiles * (n_split > 0 ? n_split : 1);
+    for (int64_t tile = blockIdx.x; tile < n_work; tile += gridDim.x) {
+    const int64_t ks = n_split > 0 ? tile % n_split : 0;
+    const int64_t mn = n_split > 0 ? tile / n_split : tile;
+    const int64_t m0 = (mn / n_tiles) * BM;
+    const int64_t n0 = (mn % n_tiles) * TN;
+    const int64_t kb = ks * p.k_split;
+    const int64_t ke = min(p.K, kb + p.k_split);
+    const int nchunks = (int)((ke - kb + KC - 1) / KC);
 
     RowInfo rows[R];
 #pragma unroll
@@ -230,7 +253,7 @@ lut_mm_kernel(const MMArgs p) {
     uint4 w_nxt = make_uint4(0, 0, 0, 0);
     if (nchunks > 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) a_cur[r] = load_a<LOADER>(p, rows[r], kb);
+        for (int r = 0; r < R; ++r) a_cur[r] = load_a<LOADER>(p, rows[r], kb, tap_s);
         if (tid < TN) {
             uint4 wv = load_w(p, n0 + tid, kb, wvec);
             w_s[0 * TN + tid] = wv.x;
@@ -246,7 +269,7 @@ lut_mm_kernel(const MMArgs p) {
         const int64_t kn = kb + (int64_t)(ci + 1) * KC;
         if (has_next) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) a_nxt[r] = load_a<LOADER>(p, rows[r], kn);
+            for (int r = 0; r < R; ++r) a_nxt[r] = load_a<LOADER>(p, rows[r], kn, tap_s);
             if (tid < TN) w_nxt = load_w(p, n0 + tid, kn, wvec);
         }
         const uint32_t* ws = w_s + (ci & 1) * (4 * TN);
@@ -339,13 +362,54 @@ lut_mm_kernel(const MMArgs p) {
             for (int n = 0; n < TN; ++n)
                 if (n0 + n < p.N) atomicAdd(c + n, acc[r][n]);
         } else {
+            const EpiArgs& e = p.ep;
+            const bool full = n0 + TN <= p.N;
+            // vector path: row layout, 16-byte aligned rows (lane = row writes 4 columns per
+            // store: half-sector granularity instead of 4-byte scattered stores)
+            const bool vec = full && !e.y_nchw &&
+                             (!e.y || (((e.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.y) & 15) == 0))) &&
+                             (!e.residual || (((e.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.residual) & 15) == 0))) &&
+                             (!e.bias || ((reinterpret_cast<uintptr_t>(e.bias) & 15) == 0 && (n0 & 3) == 0)) &&
+                             (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
+            if (vec) {
 #pragma unroll
-            for (int n = 0; n < TN; ++n) {
-                const int64_t nn = n0 + n;
-                if (nn < p.N) epi_store(epi_value(acc[r][n], m, nn, sc, p.ep), m, nn, p.N, p.ep, s_out, qm);
+                for (int n = 0; n < TN; n += 4) {
+                    const int64_t nn = n0 + n;
+                    float v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(acc[r][n + j]), sc);
+                    if (e.bias) {
+                        const float4 b = *reinterpret_cast<const float4*>(e.bias + nn);
+                        v[0] = __fadd_rn(v[0], b.x); v[1] = __fadd_rn(v[1], b.y);
+                        v[2] = __fadd_rn(v[2], b.z); v[3] = __fadd_rn(v[3], b.w);
+                    }
+                    if (e.residual) {
+                        const float4 rr = __ldg(reinterpret_cast<const float4*>(e.residual + m * e.ldr + nn));
+                        v[0] = __fadd_rn(v[0], rr.x); v[1] = __fadd_rn(v[1], rr.y);
+                        v[2] = __fadd_rn(v[2], rr.z); v[3] = __fadd_rn(v[3], rr.w);
+                    }
+                    if (e.relu) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) v[j] = v[j] > 0.f ? v[j] : 0.f;
+                    }
+                    if (e.y) *reinterpret_cast<float4*>(e.y + m * e.ldy + nn) = make_float4(v[0], v[1], v[2], v[3]);
+                    if (e.q) {
+                        uint32_t w = 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) w |= (uint32_t)(uint8_t)epi_quant(v[j], s_out, qm) << (8 * j);
+                        *reinterpret_cast<uint32_t*>(e.q + m * e.ldq + nn) = w;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int n = 0; n < TN; ++n) {
+                    const int64_t nn = n0 + n;
+                    if (nn < p.N) epi_store(epi_value(acc[r][n], m, nn, sc, e), m, nn, p.N, e, s_out, qm);
+                }
             }
         }
     }
+    }  // persistent tile loop
 }
 
 }  // namespace axq

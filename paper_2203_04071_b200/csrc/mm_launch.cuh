@@ -8,16 +8,28 @@ namespace axq {
 template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI>
 int launch_one(const MMArgs& p, dim3 grid, cudaStream_t st) {
     auto kern = lut_mm_kernel<REPR, TN, R, WARPS, LOADER, EPI>;
-    int smem = (REPR == REPR_I32 ? 0 : p.table_bytes) + 2 * (KC / 4) * TN * 4;
+    const int smem = (REPR == REPR_I32 ? 0 : p.table_bytes) + 2 * (KC / 4) * TN * 4 +
+                     (LOADER == LOAD_CONV_C4 ? 4 * (MAX_TAP_GROUPS + 4) : 0);
     static unsigned configured = 0;  // bit per device
+    static int resident[32] = {0};   // CTAs per SM, per device
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(configured & (1u << (dev & 31)))) {
+    dev &= 31;
+    if (!(configured & (1u << dev))) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
-        configured |= 1u << (dev & 31);
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, WARPS * 32, smem);
+        if (e != cudaSuccess) return (int)e;
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        resident[dev] = (nb > 0 ? nb : 1) * (sms > 0 ? sms : 148);
+        configured |= 1u << dev;
     }
-    kern<<<grid, WARPS * 32, smem, st>>>(p);
+    // persistent grid: every CTA stages the table once and loops over the tiles
+    const long long work = (long long)grid.x * grid.y * grid.z;
+    const unsigned g = (unsigned)(work < resident[dev] ? work : resident[dev]);
+    kern<<<g, WARPS * 32, smem, st>>>(p);
     return (int)cudaGetLastError();
 }
 

@@ -6,12 +6,16 @@
 
 namespace axq {
 
+// LOAD_CONV_C4 keeps one 4-byte tap entry per 4 k in shared memory: K <= 4 * MAX_TAP_GROUPS.
+constexpr int MAX_TAP_GROUPS = 1024;
+
 struct Cfg {
     int warps, R, tn;
 };
-// BIG: 16 warps x 1 row per lane x 32 columns (512 x 32 CTA tile, one CTA per SM shares
-// one table copy); SMALL: 4 warps x 1 x 32 (128 x 32).
-constexpr Cfg CFG_BIG{16, 1, 32};
+// BIG: 8 warps x 1 row per lane x 32 columns (256 x 32 CTA tile), two resident CTAs per SM
+// (each with its own table copy) so one CTA's epilogue overlaps the other's lookups;
+// SMALL: 4 warps x 1 x 32 (128 x 32).
+constexpr Cfg CFG_BIG{8, 1, 32};
 constexpr Cfg CFG_SMALL{4, 1, 32};
 
 // Return 0 or a cudaError_t code.

@@ -46,6 +46,11 @@ class ApproxLSTM:
         self._tmp_scale = torch.ones(1, device=self.dev)
         self._bufs = {}
         self.calibrated = False
+        self.timing_hook = None     # optional callable(kind, stream) around every LUT launch
+
+    def _hook(self, kind, stream):
+        if self.timing_hook:
+            self.timing_hook(kind, stream)
 
     def _buffers(self, T, B):
         key = (T, B)
@@ -78,7 +83,9 @@ class ApproxLSTM:
         gih = b["gih"]
         ep = ax.make_epilogue(self.s_x, self.sw_ih, bias=self.b_ih, y=gih, ldy=self.H4,
                               workspace=b["ws_ih"])
+        self._hook("pre", stream)
         ax.axq_lut_gemm_ep(b["qx"], self.qw_ih, self.lut, ep, stream)
+        self._hook("post", stream)
         c, qh, ghh, hs = b["c"], b["qh"], b["ghh"], b["hs"]
         with torch.cuda.stream(stream):
             c.zero_()
@@ -91,7 +98,9 @@ class ApproxLSTM:
                 ax.axq_amax(h_prev, self._tmp_amax, stream)
                 ax.axq_scale(self._tmp_amax, bits, self._tmp_scale, stream)
                 ax.axq_quantize(h_prev, self._tmp_scale, bits, qh, stream)
+            self._hook("pre", stream)
             ax.axq_lut_gemm_ep(qh, self.qw_hh, self.lut, ep_hh, stream)
+            self._hook("post", stream)
             g_t = gih[t * B:(t + 1) * B]
             if calibrate:
                 ax.axq_lstm_cell(g_t, ghh, c, hs[t], stream=stream)

@@ -85,6 +85,7 @@ class ApproxResNet:
         self.fc_bias = torch.as_tensor(weights["fc.b"]).to(self.dev, torch.float32).contiguous()
         self._bufs = {}
         self.calibrated = False
+        self.timing_hook = None     # optional callable(kind, stream) around every LUT launch
 
     # ---------------------------------------------------------------------------------
     def _s(self, name):
@@ -144,7 +145,11 @@ class ApproxResNet:
         d = ax.conv_desc(N, H, W, C, cout, k, k, (stride, stride), (pad, pad),
                          c_valid=cin if C != cin else 0)
         ep = ax.make_epilogue(self._s(name), self._sw(name), y_nhwc=True, **ep_kw)
+        if self.timing_hook:
+            self.timing_hook("pre", stream)
         ax.axq_lut_conv2d_ep(d, xq, self.qw[name], self.lut, ep, stream)
+        if self.timing_hook:
+            self.timing_hook("post", stream)
 
     def _calib_scale(self, name, t, stream):
         i = self.slot[name]
@@ -238,7 +243,11 @@ class ApproxResNet:
         lg = b["logits"]
         ep = ax.make_epilogue(self._s("fc"), self._sw("fc"), bias=self.fc_bias, y=lg,
                               ldy=lg.shape[-1], workspace=ws)
+        if self.timing_hook:
+            self.timing_hook("pre", stream)
         ax.axq_lut_gemm_ep(b["fc_q"], self.qw["fc"], self.lut, ep, stream)
+        if self.timing_hook:
+            self.timing_hook("post", stream)
         if calibrate:
             self.calibrated = True
         return lg
