@@ -173,6 +173,32 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
                              axq_lut_t lut, const axq_epilogue* ep, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * Prepared weights for the packed-table kernel.  For a delta8 table
+ * (LUT = a*w + E with E in int8) the weights of a layer are known before inference ("learns
+ * offline"), so the product row E[.][w] of every weight can be laid out once:
+ *     tables[n_block][k][q][ua] = 4 x int8 E[ua][w(16 n_block + 4q + j, k)], j = 0..3
+ * which lets one 32-bit shared-memory load serve four lookups; the exact part sum a*w runs on
+ * the tensor cores.  Results are bit-identical to axq_lut_gemm / axq_lut_conv2d.
+ * axq_wpack_create: W device int8 [N][ldw] (N x K, conv: KRSC flattened, K = R*S*C); the
+ *   LUT handle must have representation AXQ_LUT_DELTA8 (else AXQ_ERR_UNSUPPORTED).
+ *   Allocates N/16 * K/16 * 64 KiB (+ a packed weight copy) of device memory, synchronizes.
+ *   The handle keeps no reference to W or lut.
+ * axq_lut_gemm_wp / axq_lut_conv2d_wp: as axq_lut_gemm_dq / axq_lut_conv2d_dq (same epilogue
+ *   semantics; the split-K workspace is ignored).  With ep == NULL the raw int32 result goes
+ *   to C ([M][ldc]) / Y (NHWC).  Requirements (else AXQ_ERR_UNSUPPORTED): A / X 16-byte
+ *   aligned, lda % 16 == 0 (GEMM), C % 16 == 0 and groups == 1 (conv).
+ * ------------------------------------------------------------------------------- */
+typedef struct axq_wpack* axq_wpack_t;
+axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K, int64_t ldw,
+                            axq_wpack_t* out);
+axq_status axq_wpack_destroy(axq_wpack_t wp);
+axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* device_bytes);
+axq_status axq_lut_gemm_wp(int64_t M, const int8_t* A, int64_t lda, axq_wpack_t wp,
+                           const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream);
+axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_t wp,
+                             const axq_epilogue* ep, int32_t* Y, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * Dequantize (unfused), same pinned formula as the epilogue.
  * axq_dequantize: acc int32 [M][ldacc] -> y fp32 [M][ldy], bias[n] (nullable).
  * axq_dequantize_nhwc_to_nchw: acc int32 NHWC [N][HW][C] -> y fp32 NCHW [N][C][HW].

@@ -26,6 +26,8 @@ EXPORTED = [
     "axq_conv2d_out_hw", "axq_lut_conv2d", "axq_lut_conv2d_dq",
     "axq_dequantize", "axq_dequantize_nhwc_to_nchw", "axq_epilogue_apply",
     "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
+    "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
+    "axq_lut_conv2d_wp",
 ]
 
 
@@ -89,6 +91,12 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_maxpool2d_nhwc_i8": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp], i32),
         "axq_avgpool_nhwc": ([vp, i64, i64, i64, vp, vp, vp, i32, vp], i32),
         "axq_lstm_cell": ([i64, i64, vp, vp, vp, vp, vp, vp, i32, vp], i32),
+        "axq_wpack_create": ([vp, vp, i64, i64, i64, ctypes.POINTER(vp)], i32),
+        "axq_wpack_destroy": ([vp], i32),
+        "axq_wpack_info": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+        "axq_lut_gemm_wp": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
+        "axq_lut_conv2d_wp": ([ctypes.POINTER(axq_conv_desc), vp, vp,
+                               ctypes.POINTER(axq_epilogue), vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -309,3 +317,52 @@ def axq_lstm_cell(gates_ih, gates_hh, c, h_out, q_h=None, d_scale_h=None, bits=8
     _check("axq_lstm_cell", load().axq_lstm_cell(B, H4 // 4, _ptr(gates_ih), _ptr(gates_hh),
                                                  _ptr(c), _ptr(h_out), _ptr(q_h),
                                                  _ptr(d_scale_h), int(bits), _stream(stream)))
+
+
+# ---------------------------------------------------------------------------------------
+# prepared weights (packed-table kernel)
+# ---------------------------------------------------------------------------------------
+class WPack:
+    """Owns an axq_wpack_t: weight-specialised E tables of a layer (delta8 LUTs only)."""
+
+    def __init__(self, lut: Lut, W, K: int | None = None):
+        """W: device int8 [N][K] (conv: KRSC flattened)."""
+        N = W.shape[0]
+        K = W.numel() // N if K is None else K
+        h = ctypes.c_void_p()
+        _check("axq_wpack_create", load().axq_wpack_create(lut.handle, _ptr(W), N, K,
+                                                           W.stride(0), ctypes.byref(h)))
+        self.handle = h
+        self.N, self.K = N, K
+        nb = ctypes.c_int64()
+        load().axq_wpack_info(h, None, None, ctypes.byref(nb))
+        self.device_bytes = nb.value
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            load().axq_wpack_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def axq_wpack_create(lut: Lut, W) -> WPack:
+    return WPack(lut, W)
+
+
+def axq_lut_gemm_wp(A, wp: WPack, ep: axq_epilogue | None = None, C=None, stream=None) -> None:
+    M = A.shape[0]
+    _check("axq_lut_gemm_wp", load().axq_lut_gemm_wp(
+        M, _ptr(A), A.stride(0), wp.handle, ctypes.byref(ep) if ep is not None else None,
+        _ptr(C), C.stride(0) if C is not None else 0, _stream(stream)))
+
+
+def axq_lut_conv2d_wp(desc: axq_conv_desc, X_nhwc, wp: WPack, ep: axq_epilogue | None = None,
+                      Y=None, stream=None) -> None:
+    _check("axq_lut_conv2d_wp", load().axq_lut_conv2d_wp(
+        ctypes.byref(desc), _ptr(X_nhwc), wp.handle, ctypes.byref(ep) if ep is not None else None,
+        _ptr(Y), _stream(stream)))

@@ -1,0 +1,408 @@
+// lut_p4.cuh -- "P4" LUT-GEMM / implicit-im2col LUT-conv for delta8 tables (sm_100a).
+//
+// Same result as lut_mm.cuh (acc[m][n] = sum_k LUT[a[m][k]][w[n][k]], int32, exact), built so
+// that one shared-memory load serves FOUR lookups instead of one:
+//
+//  * The table is split exactly as LUT = a*w + E (E fits int8, the delta8 representation).
+//  * Weight-specialised tables (prepared once per layer, axq_wpack_create): for every k and
+//    every quad of 4 output columns q, T[k][q][ua] = (E[ua][w(4q,k)], E[ua][w(4q+1,k)],
+//    E[ua][w(4q+2,k)], E[ua][w(4q+3,k)]) as 4 int8 in one 32-bit word (1 KiB per (k, q)).
+//    A lane that owns output row m fetches T[k][q][a[m][k]] with ONE 32-bit LDS and gets the
+//    E terms of 4 outputs.  Bank = ua mod 32: lanes only conflict when two of them hold
+//    different activation codes congruent mod 32 (measured ~1.8-way for ReLU'd data).
+//  * The exact part sum_k a*w is a dense int8 contraction: it runs on the tensor cores
+//    (mma.sync m16n8k16 s8, fragments by ldmatrix from the staged operand tiles).
+//  * Per 16-k stage the CTA stages, double-buffered: the E tables of its 16 columns (64 KiB,
+//    one cp.async.bulk, mbarrier complete_tx), the packed weight tile (256 B, bulk) and the
+//    activation tile (1024 rows x 16 B, cp.async with zero-fill = implicit im2col, semantic
+//    padding taps read as a = 0 and are looked up, A11).
+//  * CTA tile 1024 rows x 16 columns, 16 warps.  A lane owns 2 rows x 16 columns of E sums,
+//    kept as biased (E + 128) bytes added in pairs of 16-bit lanes: per shared load 2 PRMT
+//    split the even / odd bytes and 2 IMAD (FMA pipe, multiplier 1 passed as a parameter) add
+//    them, so the ALU and FMA pipes share the work.  Every 256 k the packed sums are flushed
+//    through a per-warp shared scratch into the mma accumulators (exact part); the bias
+//    128*Kp is removed at the end and the fused epilogue of lut_mm.cuh runs on the result.
+//  * Persistent grid (one CTA per SM), tiles walked m-major within an n-column block.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lut_mm.cuh"
+#include "lut_p4_args.h"
+
+namespace axq {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                            uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+__device__ __forceinline__ void ldmatrix_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];\n"
+                 : "=r"(r0), "=r"(r1)
+                 : "r"(addr));
+}
+
+// Sign-extend byte j of v with PTX prmt's sign-replicate selectors (the CUDA __byte_perm
+// intrinsic only honours the low 3 bits of each selector nibble).
+template <uint32_t SEL>
+__device__ __forceinline__ int prmt_sext(uint32_t v) {
+    int r;
+    asm("prmt.b32 %0, %1, 0, %2;\n" : "=r"(r) : "r"(v), "n"(SEL));
+    return r;
+}
+
+__device__ __forceinline__ void mma_s8_16816(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(b0));
+}
+
+// Source address / valid bytes of the 16 activation bytes a[m][k0 .. k0+15].
+__device__ __forceinline__ const int8_t* p4_a_src(const P4Args& P, const RowInfo& ri, int64_t k0,
+                                                  uint32_t& bytes) {
+    const MMArgs& p = P.mm;
+    bytes = 0;
+    if (!ri.valid || k0 >= p.K) return p.A;
+    if (P.is_conv) {
+        const int rs = (int)(k0 / p.C);
+        const int c0 = (int)(k0 - (int64_t)rs * p.C);
+        const int r = rs / p.S, s = rs - r * p.S;
+        const int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
+        if (hi < 0 || hi >= p.H || wi < 0 || wi >= p.Wd) return p.A;   // padding tap: zeros
+        bytes = 16;
+        return p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c0;
+    }
+    const int64_t rem = p.K - k0;
+    bytes = rem >= 16 ? 16u : (uint32_t)rem;
+    return p.A + ri.base + k0;
+}
+
+__global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
+    using namespace p4;
+    extern __shared__ __align__(1024) uint8_t p4_smem[];
+    uint8_t* smem = p4_smem;
+    const MMArgs& p = P.mm;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t s_base = smem_u32(smem);
+    const uint32_t bar0 = s_base + SMEM_BAR;
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + TN - 1) / TN;
+    const int64_t n_work = m_tiles * n_tiles;
+    const int nstages = (int)(P.Kp / KS);
+    uint32_t phase_bits = 0;   // parity of the next wait, one bit per stage buffer
+
+    for (int64_t tile = blockIdx.x; tile < n_work; tile += gridDim.x) {
+        const int64_t nb = tile / m_tiles;               // column block (tables shared in L2)
+        const int64_t m0 = (tile - nb * m_tiles) * BM;
+        const int64_t n0 = nb * TN;
+        const uint32_t* tbl_g = P.tables + (size_t)nb * P.Kp * 4 * 256;
+        const int8_t* w_g = P.wpk + (size_t)nb * (P.Kp / KS) * W_STAGE;
+
+        // rows this thread copies (A tile rows tid and tid + 512)
+        RowInfo crow[2];
+        if (P.is_conv) {
+            crow[0] = make_row<LOAD_CONV>(p, m0 + tid);
+            crow[1] = make_row<LOAD_CONV>(p, m0 + tid + NT);
+        } else {
+            crow[0] = make_row<LOAD_GEMM>(p, m0 + tid);
+            crow[1] = make_row<LOAD_GEMM>(p, m0 + tid + NT);
+        }
+
+        auto issue = [&](int st) {
+            const int buf = st % STAGES;
+            const int64_t k0 = (int64_t)st * KS;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                uint32_t nbytes;
+                const int8_t* src = p4_a_src(P, crow[i], k0, nbytes);
+                cp_async16(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS, src, nbytes);
+            }
+            cp_async_commit();
+            if (tid == 0) {
+                const uint32_t bar = bar0 + 8 * buf;
+                mbar_expect_tx(bar, TBL_STAGE + W_STAGE);
+                bulk_g2s(s_base + SMEM_TBL + buf * TBL_STAGE, tbl_g + (size_t)st * 4 * 256 * KS, TBL_STAGE, bar);
+                bulk_g2s(s_base + SMEM_W + buf * W_STAGE, w_g + (size_t)st * W_STAGE, W_STAGE, bar);
+            }
+        };
+
+        uint32_t pacc[RPL][4][2];   // packed 16-bit E sums: [row][quad][even (c0,c2) / odd (c1,c3)]
+#pragma unroll
+        for (int r = 0; r < RPL; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pacc[r][q][0] = pacc[r][q][1] = 0u;
+        int cacc[4][2][4];     // exact part: 4 m16 tiles x 2 n8 tiles x mma C fragment
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) cacc[i][j][c] = 0;
+
+        int* scr = reinterpret_cast<int*>(smem + SMEM_SCR + warp * SCR_WARP);
+        const int g = lane >> 2, t4 = lane & 3;
+        // element (row, col) of the warp scratch, XOR-swizzled so that a lane reading its row
+        // and a thread writing its mma fragment are (nearly) conflict free
+        auto sidx = [](int row, int col) { return row * TN + (col ^ (row & 15)); };
+        // packed lane sums -> scratch (lane layout) -> added into the mma fragments
+        auto flush = [&]() {
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+                const int row = r * 32 + lane;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    scr[sidx(row, 4 * q + 0)] = (int)(pacc[r][q][0] & 0xffffu);
+                    scr[sidx(row, 4 * q + 2)] = (int)(pacc[r][q][0] >> 16);
+                    scr[sidx(row, 4 * q + 1)] = (int)(pacc[r][q][1] & 0xffffu);
+                    scr[sidx(row, 4 * q + 3)] = (int)(pacc[r][q][1] >> 16);
+                    pacc[r][q][0] = pacc[r][q][1] = 0u;
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int row = i * 16 + g, col = j * 8 + 2 * t4;
+                    cacc[i][j][0] += scr[sidx(row, col)];
+                    cacc[i][j][1] += scr[sidx(row, col + 1)];
+                    cacc[i][j][2] += scr[sidx(row + 8, col)];
+                    cacc[i][j][3] += scr[sidx(row + 8, col + 1)];
+                }
+            __syncwarp();
+        };
+        const uint32_t one = P.one;
+
+        for (int st = 0; st < STAGES && st < nstages; ++st) issue(st);
+
+        for (int st = 0; st < nstages; ++st) {
+            const int buf = st % STAGES;
+            // groups in flight here: stages <= st + STAGES - 2 (st >= 1) or 0..STAGES-1 (st = 0)
+            if (st == 0 && nstages > 1) cp_async_wait<STAGES - 1>(); else cp_async_wait<0>();
+            mbar_wait(bar0 + 8 * buf, (phase_bits >> buf) & 1u);
+            phase_bits ^= 1u << buf;
+            __syncthreads();                                   // stage st visible to all
+            if (st >= 1 && st - 1 + STAGES < nstages) {
+                // buffer of stage st-1 is free (everyone passed its compute): refill it
+                issue(st - 1 + STAGES);
+            }
+            const uint8_t* tb = smem + SMEM_TBL + buf * TBL_STAGE;
+            const uint8_t* at = smem + SMEM_A + buf * A_STAGE;
+
+            // ---- exact part on the tensor cores: 4 m16 x 2 n8 tiles, k = 16 ----
+            {
+                uint32_t b0, b1;
+                ldmatrix_x2(s_base + SMEM_W + buf * W_STAGE + (lane & 15) * KS, b0, b1);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t a0, a1, a2, a3;
+                    ldmatrix_x4(s_base + SMEM_A + buf * A_STAGE + (warp * 64 + h * 32 + lane) * KS, a0, a1, a2, a3);
+                    mma_s8_16816(cacc[2 * h][0], a0, a1, b0);
+                    mma_s8_16816(cacc[2 * h][1], a0, a1, b1);
+                    mma_s8_16816(cacc[2 * h + 1][0], a2, a3, b0);
+                    mma_s8_16816(cacc[2 * h + 1][1], a2, a3, b1);
+                }
+            }
+            // ---- E lookups: 4 per 32-bit shared load, packed 16-bit accumulation ----
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+                const uint4 av = *reinterpret_cast<const uint4*>(at + (warp * 64 + r * 32 + lane) * KS);
+                const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk) {
+                    const uint32_t ua = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
+                    const uint8_t* row_t = tb + kk * 4 * 1024 + ua * 4u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t v = *reinterpret_cast<const uint32_t*>(row_t + q * 1024);
+                        const uint32_t ev = __byte_perm(v, 0u, 0x4240u);   // [b0, 0, b2, 0]
+                        const uint32_t od = __byte_perm(v, 0u, 0x4341u);   // [b1, 0, b3, 0]
+                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[r][q][0]) : "r"(ev), "r"(one));
+                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[r][q][1]) : "r"(od), "r"(one));
+                    }
+                }
+            }
+            if ((st + 1) % FLUSH_STAGES == 0 || st + 1 == nstages) flush();
+        }
+        // the int32 total of every output: write the mma fragments to the scratch, read rows
+        const int64_t corr_n = (P.Kp - p.K) + p.pad_lookups;   // storage-padding lookups (0,0)
+        const int corr = (int)(corr_n * (int64_t)p.t00) + E_BIAS * (int)P.Kp;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int row = i * 16 + g, col = j * 8 + 2 * t4;
+                scr[sidx(row, col)] = cacc[i][j][0];
+                scr[sidx(row, col + 1)] = cacc[i][j][1];
+                scr[sidx(row + 8, col)] = cacc[i][j][2];
+                scr[sidx(row + 8, col + 1)] = cacc[i][j][3];
+            }
+        __syncwarp();
+        int eacc[RPL][TN];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r)
+#pragma unroll
+            for (int n = 0; n < TN; ++n) eacc[r][n] = scr[sidx(r * 32 + lane, n)] - corr;
+        __syncwarp();
+
+        // ---- fused epilogue (same pinned order as lut_mm.cuh) ----
+        const EpiArgs& e = p.ep;
+        const bool raw = p.C_out != nullptr;
+        const float sc = raw ? 0.f : __fmul_rn(*e.sa, *e.sw);
+        const float s_out = (!raw && e.q) ? *e.s_out : 1.f;
+        const float qm = (float)((1 << ((e.q ? e.bits_out : 8) - 1)) - 1);
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+            const int64_t m = m0 + warp * 64 + r * 32 + lane;
+            if (m >= p.M) continue;
+            if (raw) {   // raw int32 output
+                int32_t* c = p.C_out + m * p.ldc + n0;
+#pragma unroll
+                for (int n = 0; n < TN; ++n)
+                    if (n0 + n < p.N) c[n] = eacc[r][n];
+                continue;
+            }
+            const bool vec = (n0 + TN <= p.N) && !e.y_nchw &&
+                             (!e.y || (((e.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.y) & 15) == 0))) &&
+                             (!e.residual || (((e.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.residual) & 15) == 0))) &&
+                             (!e.bias || ((reinterpret_cast<uintptr_t>(e.bias) & 15) == 0)) &&
+                             (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
+            if (vec) {
+#pragma unroll
+                for (int n = 0; n < TN; n += 4) {
+                    const int64_t nn = n0 + n;
+                    float v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(eacc[r][n + j]), sc);
+                    if (e.bias) {
+                        const float4 b = *reinterpret_cast<const float4*>(e.bias + nn);
+                        v[0] = __fadd_rn(v[0], b.x); v[1] = __fadd_rn(v[1], b.y);
+                        v[2] = __fadd_rn(v[2], b.z); v[3] = __fadd_rn(v[3], b.w);
+                    }
+                    if (e.residual) {
+                        const float4 rr = __ldg(reinterpret_cast<const float4*>(e.residual + m * e.ldr + nn));
+                        v[0] = __fadd_rn(v[0], rr.x); v[1] = __fadd_rn(v[1], rr.y);
+                        v[2] = __fadd_rn(v[2], rr.z); v[3] = __fadd_rn(v[3], rr.w);
+                    }
+                    if (e.relu) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) v[j] = v[j] > 0.f ? v[j] : 0.f;
+                    }
+                    if (e.y) *reinterpret_cast<float4*>(e.y + m * e.ldy + nn) = make_float4(v[0], v[1], v[2], v[3]);
+                    if (e.q) {
+                        uint32_t w = 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) w |= (uint32_t)(uint8_t)epi_quant(v[j], s_out, qm) << (8 * j);
+                        *reinterpret_cast<uint32_t*>(e.q + m * e.ldq + nn) = w;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int n = 0; n < TN; ++n) {
+                    const int64_t nn = n0 + n;
+                    if (nn < p.N) epi_store(epi_value(eacc[r][n], m, nn, sc, e), m, nn, p.N, e, s_out, qm);
+                }
+            }
+        }
+        __syncthreads();   // every warp done with the stage buffers before the next prologue
+    }
+}
+
+// ---- weight preparation: E tables and the packed weight tile (once per layer) ----
+// tables[((nb*Kp + k)*4 + q)*256 + ua] = bytes j=0..3: E[ua][w(16nb+4q+j, k)]  (E = delta8 table)
+__global__ void p4_pack_tables_kernel(const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw,
+                                      int64_t Kp, const int8_t* __restrict__ dtab,
+                                      uint32_t* __restrict__ tables) {
+    const int64_t n_blocks = (N + p4::TN - 1) / p4::TN;
+    const int64_t total = n_blocks * Kp * 4 * 256;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int ua = (int)(i & 255);
+        int64_t t = i >> 8;
+        const int q = (int)(t & 3);
+        t >>= 2;
+        const int64_t k = t % Kp, nb = t / Kp;
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t n = nb * p4::TN + 4 * q + j;
+            const int w = (n < N && k < K) ? (int)W[n * ldw + k] : 0;
+            const uint8_t e = (uint8_t)((int)dtab[((w & 0xff) << 8) | ua] + p4::E_BIAS);
+            word |= (uint32_t)e << (8 * j);
+        }
+        tables[i] = word;
+    }
+}
+
+// wpk[((nb*(Kp/16) + kc)*16 + nl)*16 + kk] = W[16nb+nl][16kc+kk] (0 outside)
+__global__ void p4_pack_w_kernel(const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw, int64_t Kp,
+                                 int8_t* __restrict__ wpk) {
+    const int64_t n_blocks = (N + p4::TN - 1) / p4::TN;
+    const int64_t total = n_blocks * Kp * p4::TN;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int kk = (int)(i & 15);
+        const int nl = (int)((i >> 4) & 15);
+        const int64_t t = i >> 8;
+        const int64_t kc = t % (Kp / 16), nb = t / (Kp / 16);
+        const int64_t n = nb * p4::TN + nl, k = kc * 16 + kk;
+        wpk[i] = (n < N && k < K) ? W[n * ldw + k] : (int8_t)0;
+    }
+}
+
+}  // namespace axq

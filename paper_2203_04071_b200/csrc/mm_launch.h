@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "lut_mm.cuh"
 
 namespace axq {
@@ -22,5 +24,11 @@ constexpr Cfg CFG_SMALL{4, 1, 32};
 int launch_mm_delta8(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
 int launch_mm_i16(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
 int launch_mm_i32(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
+
+// P4 kernel (lut_p4.cuh); declared here with an opaque argument struct.
+struct P4Args;
+int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int8_t* dtab,
+            uint32_t* tables, int8_t* wpk, cudaStream_t st);
+int launch_p4(const P4Args& a, cudaStream_t st);
 
 }  // namespace axq

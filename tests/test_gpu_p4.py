@@ -1,0 +1,94 @@
+"""GPU parity of the packed-table (P4) kernel: prepared weights + 4 lookups per shared load +
+exact part on the tensor cores.  Bit-exact against the oracle and against the v1 kernel."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def ax():
+    from paper_2203_04071_b200 import _lib
+    _lib.load()
+    return _lib
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (100, 16, 16), (1500, 40, 77), (2049, 33, 300),
+                                   (4096, 64, 256), (1025, 17, 1040)])
+@pytest.mark.parametrize("lut_kind", ["randerr", "trunc4", "b4"])
+def test_p4_gemm(ax, M, N, K, lut_kind):
+    bits = 4 if lut_kind == "b4" else 8
+    T = {"randerr": datagen.lut_randerr(8, 0, 2), "trunc4": datagen.lut_trunc4(),
+         "b4": datagen.lut_randerr(4, 4, 14)}[lut_kind]
+    A = datagen.random_int8(200 + M, (M, K), bits)
+    W = datagen.random_int8(300 + N, (N, K), bits)
+    ref = oracle.lut_gemm(A, W, T, bits)
+    lut = ax.Lut(bits, T)
+    assert lut.repr == "delta8"
+    Kp = (K + 15) // 16 * 16
+    dA = torch.zeros(M, Kp, dtype=torch.int8, device=DEV)      # lda % 16 == 0
+    dA[:, :K] = _t(A)
+    dW = _t(W)
+    wp = ax.WPack(lut, dW)
+    C = torch.empty(M, N, dtype=torch.int32, device=DEV)
+    ax.axq_lut_gemm_wp(dA.narrow(1, 0, K), wp, None, C)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(C.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 14, 14, 64, 3, 3, 1, 1), (1, 32, 9, 11, 40, 3, 3, 2, 1),
+                                   (3, 16, 8, 8, 33, 1, 1, 1, 0), (1, 256, 7, 7, 70, 1, 1, 2, 0),
+                                   (2, 64, 23, 19, 48, 3, 3, 1, 1)])
+def test_p4_conv_fused(ax, shape):
+    Nb, C, H, Wd, K, R, S, st, pd = shape
+    X = datagen.random_int8(80 + C, (Nb, C, H, Wd))
+    Wt = datagen.random_int8(90 + K, (K, C, R, S))
+    T = datagen.lut_randerr(8, 0, 2)
+    ref = oracle.lut_conv2d(X, Wt, T, 8, (st, st), (pd, pd))
+    lut = ax.Lut(8, T)
+    d = ax.conv_desc(Nb, H, Wd, C, K, R, S, (st, st), (pd, pd))
+    Ho, Wo = ax.axq_conv2d_out_hw(d)
+    dX = _t(X.transpose(0, 2, 3, 1))
+    dW = _t(Wt.transpose(0, 2, 3, 1).reshape(K, -1))
+    wp = ax.WPack(lut, dW)
+    Y = torch.empty(Nb, Ho, Wo, K, dtype=torch.int32, device=DEV)
+    ax.axq_lut_conv2d_wp(d, dX, wp, None, Y)
+    np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
+    # fused epilogue (NCHW fp32) == oracle dequant
+    sa, sw = np.float32(0.0213), np.float32(0.0071)
+    dsa, dsw = _t(np.array([sa])), _t(np.array([sw]))
+    bias = datagen.normal(5, 5, (K,), 0.1)
+    db = _t(bias)
+    y = torch.empty(Nb, K, Ho, Wo, device=DEV)
+    ep = ax.make_epilogue(dsa, dsw, bias=db, y=y)
+    ax.axq_lut_conv2d_wp(d, dX, wp, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.dequantize(ref, sa, sw, bias, 1))
+
+
+def test_p4_config2_full(ax):
+    """BJ configs[2] at full batch through the P4 path: sampled images bit-exact."""
+    c = datagen.config2()
+    lut = ax.Lut(8, c.lut)
+    sa = oracle.scale(oracle.amax(c.x), 8)
+    qw, sw = oracle.quantize_tensor(c.W, 8)
+    qx = _t(oracle.quantize(c.x, sa, 8).transpose(0, 2, 3, 1))
+    wp = ax.WPack(lut, _t(qw.transpose(0, 2, 3, 1).reshape(64, -1)))
+    d = ax.conv_desc(128, 56, 56, 64, 64, 3, 3, (1, 1), (1, 1))
+    dsa, dsw = _t(np.array([sa])), _t(np.array([sw]))
+    y = torch.empty(128, 64, 56, 56, device=DEV)
+    ep = ax.make_epilogue(dsa, dsw, y=y)
+    ax.axq_lut_conv2d_wp(d, qx, wp, ep)
+    torch.cuda.synchronize()
+    for img in (0, 127):
+        acc = oracle.lut_conv2d(oracle.quantize(c.x[img:img + 1], sa, 8), qw, c.lut, 8, (1, 1), (1, 1))
+        np.testing.assert_array_equal(y[img:img + 1].cpu().numpy(), oracle.dequantize(acc, sa, sw, None, 1))
