@@ -350,11 +350,21 @@ class WPack:
             pass
 
 
+P4_BM, P4_TN = 1024, 16
+
+
+def prefer_packed(M: int, N: int, n_sms: int) -> bool:
+    """Packed-table kernel only when its 1024 x 16 tiles fill the GPU (else the per-row-gather
+    kernel, which can split K, is used)."""
+    return ((M + P4_BM - 1) // P4_BM) * ((N + P4_TN - 1) // P4_TN) >= n_sms
+
+
 def axq_wpack_create(lut: Lut, W) -> WPack:
     return WPack(lut, W)
 
 
 def axq_lut_gemm_wp(A, wp: WPack, ep: axq_epilogue | None = None, C=None, stream=None) -> None:
+    """A int8 [M][K] (16-byte aligned rows) with prepared weights; ep or raw int32 C."""
     M = A.shape[0]
     _check("axq_lut_gemm_wp", load().axq_lut_gemm_wp(
         M, _ptr(A), A.stride(0), wp.handle, ctypes.byref(ep) if ep is not None else None,

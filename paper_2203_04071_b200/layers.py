@@ -65,7 +65,7 @@ class ApproxConv2d:
     """Conv2d with every multiply a LUT lookup; NCHW fp32 in/out, implicit im2col."""
 
     def __init__(self, weight: torch.Tensor, bias: torch.Tensor | None, lut: ax.Lut,
-                 stride=(1, 1), padding=(0, 0), device="cuda"):
+                 stride=(1, 1), padding=(0, 0), device="cuda", packed=True):
         self.lut = lut
         self.bits = lut.bits
         w = weight.to(device=device, dtype=torch.float32).contiguous()   # [K][C][R][S]
@@ -80,6 +80,10 @@ class ApproxConv2d:
         self.qw_kcrs = q
         self.qw = q.permute(0, 2, 3, 1).contiguous()                      # KRSC relayout
         self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
+        self.wp = None
+        if packed and lut.repr == "delta8" and self.C % 16 == 0 and self.C * self.R * self.S >= 128:
+            self.wp = ax.WPack(lut, self.qw.reshape(self.Kout, -1))
+        self.n_sms = torch.cuda.get_device_properties(torch.device(device)).multi_processor_count
         self.d_amax_a = torch.empty(1, device=device)
         self.d_scale_a = torch.empty(1, device=device)
         self._bufs = {}
@@ -103,7 +107,18 @@ class ApproxConv2d:
             ax.axq_scale(self.d_amax_a, self.bits, self.d_scale_a)
             d_scale_a = self.d_scale_a
         ax.axq_quantize_nchw_to_nhwc(x, d_scale_a, self.bits, b["qx"])
-        ax.axq_lut_conv2d_dq(d, b["qx"], self.qw, self.lut, d_scale_a, self.d_scale_w, self.bias, y)
+        self.conv_q(d, b["qx"], d_scale_a, y)
         return y
+
+    def conv_q(self, d, qx, d_scale_a, y, stream=None):
+        """LUT conv of int8 NHWC codes with the fused dequant epilogue to fp32 NCHW y (keeps
+        every epilogue tensor referenced until the launch)."""
+        Ho, Wo = ax.axq_conv2d_out_hw(d)
+        if self.wp is not None and ax.prefer_packed(d.N * Ho * Wo, self.Kout, self.n_sms):
+            ep = ax.make_epilogue(d_scale_a, self.d_scale_w, bias=self.bias, y=y)
+            ax.axq_lut_conv2d_wp(d, qx, self.wp, ep, stream=stream)
+        else:
+            ax.axq_lut_conv2d_dq(d, qx, self.qw, self.lut, d_scale_a, self.d_scale_w, self.bias, y,
+                                 stream=stream)
 
     __call__ = forward

@@ -40,6 +40,9 @@ class ApproxLSTM:
         self.b_hh = torch.as_tensor(b_hh).to(self.dev, f32).contiguous()
         self.H4, self.I = self.qw_ih.shape
         self.H = self.H4 // 4
+        # prepared weights for the hoisted input projection (large M) on the packed-table kernel
+        self.wp_ih = ax.WPack(lut, self.qw_ih) if (lut.repr == "delta8" and self.I % 16 == 0) else None
+        self.n_sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.s_x = torch.ones(1, device=self.dev)
         self.s_h = torch.ones(1, device=self.dev)
         self._tmp_amax = torch.zeros(1, device=self.dev)
@@ -84,7 +87,10 @@ class ApproxLSTM:
         ep = ax.make_epilogue(self.s_x, self.sw_ih, bias=self.b_ih, y=gih, ldy=self.H4,
                               workspace=b["ws_ih"])
         self._hook("pre", stream)
-        ax.axq_lut_gemm_ep(b["qx"], self.qw_ih, self.lut, ep, stream)
+        if self.wp_ih is not None and ax.prefer_packed(T * B, self.H4, self.n_sms):
+            ax.axq_lut_gemm_wp(b["qx"], self.wp_ih, ep, stream=stream)
+        else:
+            ax.axq_lut_gemm_ep(b["qx"], self.qw_ih, self.lut, ep, stream)
         self._hook("post", stream)
         c, qh, ghh, hs = b["c"], b["qh"], b["ghh"], b["hs"]
         with torch.cuda.stream(stream):

@@ -51,7 +51,7 @@ def _out(h, k, s, p):
 
 
 class ApproxResNet:
-    def __init__(self, weights: dict, lut: ax.Lut, device="cuda", **topo):
+    def __init__(self, weights: dict, lut: ax.Lut, device="cuda", packed=True, **topo):
         self.dev = torch.device(device)
         self.lut, self.bits = lut, lut.bits
         self.specs = layer_specs(**topo)
@@ -83,6 +83,13 @@ class ApproxResNet:
                     q = qp
             self.qw[name] = q
         self.fc_bias = torch.as_tensor(weights["fc.b"]).to(self.dev, torch.float32).contiguous()
+        # prepared weights for the packed-table kernel (delta8 tables, C % 16 == 0, K >= 128)
+        self.wp = {}
+        if packed and lut.repr == "delta8":
+            for name, kind, cout, cin, k, stride, pad in self.specs:
+                if kind == "conv" and cin % 16 == 0 and cin * k * k >= 128:
+                    self.wp[name] = ax.WPack(lut, self.qw[name].reshape(cout, -1))
+        self.n_sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._bufs = {}
         self.calibrated = False
         self.timing_hook = None     # optional callable(kind, stream) around every LUT launch
@@ -147,7 +154,12 @@ class ApproxResNet:
         ep = ax.make_epilogue(self._s(name), self._sw(name), y_nhwc=True, **ep_kw)
         if self.timing_hook:
             self.timing_hook("pre", stream)
-        ax.axq_lut_conv2d_ep(d, xq, self.qw[name], self.lut, ep, stream)
+        wp = self.wp.get(name)
+        if wp is not None and ax.prefer_packed(N * _out(H, k, stride, pad) * _out(W, k, stride, pad),
+                                               cout, self.n_sms):
+            ax.axq_lut_conv2d_wp(d, xq, wp, ep, stream=stream)
+        else:
+            ax.axq_lut_conv2d_ep(d, xq, self.qw[name], self.lut, ep, stream)
         if self.timing_hook:
             self.timing_hook("post", stream)
 
