@@ -246,7 +246,9 @@ class ConvWL:
         c = datagen.config2()
         self.c = c
         self.lut = Lut(8, c.lut)
-        self.layer = ApproxConv2d(torch.from_numpy(c.W).to(dev), None, self.lut, c.stride, c.pad)
+        # BJ configs[2]'s input is ReLU(N(0,1)): non-negative codes (half-range packed tables)
+        self.layer = ApproxConv2d(torch.from_numpy(c.W).to(dev), None, self.lut, c.stride, c.pad,
+                                  a_nonneg=True)
         self.x_host = torch.from_numpy(c.x).pin_memory()
         self.x = self.x_host.to(dev)
         Nb, C, H, W = self.x.shape

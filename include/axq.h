@@ -181,16 +181,20 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
  * the tensor cores.  Results are bit-identical to axq_lut_gemm / axq_lut_conv2d.
  * axq_wpack_create: W device int8 [N][ldw] (N x K, conv: KRSC flattened, K = R*S*C); the
  *   LUT handle must have representation AXQ_LUT_DELTA8 (else AXQ_ERR_UNSUPPORTED).
- *   Allocates N/16 * K/16 * 64 KiB (+ a packed weight copy) of device memory, synchronizes.
- *   The handle keeps no reference to W or lut.
+ *   a_nonneg = 1 promises that every activation code the handle will be used with is >= 0
+ *   (e.g. quantized ReLU outputs): the tables then hold ua = 0..127 only (half the bytes, a
+ *   deeper pipeline).  A negative code with such a handle gives unspecified (but memory-safe)
+ *   results.  Allocates N/16 * K/16 * 64 KiB (32 KiB with a_nonneg) plus a packed weight copy
+ *   of device memory, synchronizes.  The handle keeps no reference to W or lut.
  * axq_lut_gemm_wp / axq_lut_conv2d_wp: as axq_lut_gemm_dq / axq_lut_conv2d_dq (same epilogue
- *   semantics; the split-K workspace is ignored).  With ep == NULL the raw int32 result goes
- *   to C ([M][ldc]) / Y (NHWC).  Requirements (else AXQ_ERR_UNSUPPORTED): A / X 16-byte
+ *   semantics; with ep->workspace the library may split K when the tiles alone cannot fill
+ *   the GPU).  With ep == NULL the raw int32 result goes to C ([M][ldc]) / Y (NHWC), which is
+ *   then also used as the split-K accumulator.  Requirements (else AXQ_ERR_UNSUPPORTED): A / X 16-byte
  *   aligned, lda % 16 == 0 (GEMM), C % 16 == 0 and groups == 1 (conv).
  * ------------------------------------------------------------------------------- */
 typedef struct axq_wpack* axq_wpack_t;
 axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K, int64_t ldw,
-                            axq_wpack_t* out);
+                            int a_nonneg, axq_wpack_t* out);
 axq_status axq_wpack_destroy(axq_wpack_t wp);
 axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* device_bytes);
 axq_status axq_lut_gemm_wp(int64_t M, const int8_t* A, int64_t lda, axq_wpack_t wp,

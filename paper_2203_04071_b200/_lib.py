@@ -91,7 +91,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_maxpool2d_nhwc_i8": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp], i32),
         "axq_avgpool_nhwc": ([vp, i64, i64, i64, vp, vp, vp, i32, vp], i32),
         "axq_lstm_cell": ([i64, i64, vp, vp, vp, vp, vp, vp, i32, vp], i32),
-        "axq_wpack_create": ([vp, vp, i64, i64, i64, ctypes.POINTER(vp)], i32),
+        "axq_wpack_create": ([vp, vp, i64, i64, i64, i32, ctypes.POINTER(vp)], i32),
         "axq_wpack_destroy": ([vp], i32),
         "axq_wpack_info": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "axq_lut_gemm_wp": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
@@ -325,13 +325,16 @@ def axq_lstm_cell(gates_ih, gates_hh, c, h_out, q_h=None, d_scale_h=None, bits=8
 class WPack:
     """Owns an axq_wpack_t: weight-specialised E tables of a layer (delta8 LUTs only)."""
 
-    def __init__(self, lut: Lut, W, K: int | None = None):
-        """W: device int8 [N][K] (conv: KRSC flattened)."""
+    def __init__(self, lut: Lut, W, K: int | None = None, a_nonneg: bool = False):
+        """W: device int8 [N][K] (conv: KRSC flattened).  a_nonneg: every activation code will
+        be >= 0 (ReLU outputs) -> half-range tables."""
         N = W.shape[0]
         K = W.numel() // N if K is None else K
         h = ctypes.c_void_p()
         _check("axq_wpack_create", load().axq_wpack_create(lut.handle, _ptr(W), N, K,
-                                                           W.stride(0), ctypes.byref(h)))
+                                                           W.stride(0), int(bool(a_nonneg)),
+                                                           ctypes.byref(h)))
+        self.a_nonneg = bool(a_nonneg)
         self.handle = h
         self.N, self.K = N, K
         nb = ctypes.c_int64()
@@ -354,9 +357,9 @@ P4_BM, P4_TN = 1024, 16
 
 
 def prefer_packed(M: int, N: int, n_sms: int) -> bool:
-    """Packed-table kernel only when its 1024 x 16 tiles fill the GPU (else the per-row-gather
-    kernel, which can split K, is used)."""
-    return ((M + P4_BM - 1) // P4_BM) * ((N + P4_TN - 1) // P4_TN) >= n_sms
+    """Packed-table kernel from 1024 rows up (it picks 1024- or 512-row tiles and a K split
+    itself, axq p4_plan); below that the per-row-gather kernel wastes fewer lanes."""
+    return M >= P4_BM
 
 
 def axq_wpack_create(lut: Lut, W) -> WPack:

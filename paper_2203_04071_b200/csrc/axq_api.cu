@@ -18,6 +18,7 @@
 
 struct axq_wpack {
     int device;
+    int half;
     int32_t t00;
     int64_t N, K, Kp;
     uint32_t* tables;
@@ -479,7 +480,7 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
 // Prepared weights + packed-table (P4) kernel
 // ---------------------------------------------------------------------------------------
 axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K, int64_t ldw,
-                            axq_wpack_t* out) {
+                            int a_nonneg, axq_wpack_t* out) {
     if (!out || N <= 0 || K <= 0 || ldw < K || !W) return AXQ_ERR_INVALID;
     *out = nullptr;
     axq_status s = check_lut(lut);
@@ -493,14 +494,15 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
     w->N = N;
     w->K = K;
     w->Kp = (K + 15) / 16 * 16;
+    w->half = a_nonneg ? 1 : 0;
     const int64_t nb = (N + axq::p4::TN - 1) / axq::p4::TN;
-    const size_t tb = (size_t)nb * w->Kp * 4 * 256 * 4, wb = (size_t)nb * w->Kp * axq::p4::TN;
+    const size_t tb = (size_t)nb * w->Kp * 4 * (w->half ? 128 : 256) * 4, wb = (size_t)nb * w->Kp * axq::p4::TN;
     w->bytes = (int64_t)(tb + wb);
     cudaError_t e = cudaMalloc(&w->tables, tb);
     if (e == cudaSuccess) e = cudaMalloc(&w->wpk, wb);
     if (e == cudaSuccess) {
         int rc = axq::p4_pack(W, N, K, ldw, w->Kp, reinterpret_cast<const int8_t*>(lut->d_table),
-                              w->tables, w->wpk, 0);
+                              w->tables, w->wpk, w->half, 0);
         e = rc ? (cudaError_t)rc : cudaDeviceSynchronize();
     }
     if (e != cudaSuccess) {
@@ -540,18 +542,38 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     a.Kp = wp->Kp;
     a.is_conv = conv ? 1 : 0;
     a.one = 1u;
+    a.half = wp->half;
     a.mm.t00 = wp->t00;
+    axq::EpiArgs epi{};
     if (ep) {
         axq_status s = check_epilogue(ep, a.mm.N, conv);
         if (s != AXQ_OK) return s;
-        a.mm.ep = to_epi(ep, conv && !ep->y_nhwc, (int64_t)a.mm.Ho * a.mm.Wo);
+        epi = to_epi(ep, conv && !ep->y_nhwc, (int64_t)a.mm.Ho * a.mm.Wo);
+    } else if (!C || ldc < a.mm.N) {
+        return AXQ_ERR_INVALID;
+    }
+    if (a.mm.M == 0) return AXQ_OK;
+    // raw output may always split K (atomics into C); the fused epilogue needs a workspace
+    const bool can_split = ep ? (ep->workspace != nullptr) : true;
+    axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
+    if (a.splits > 1) {
+        int32_t* acc = ep ? ep->workspace : C;
+        const int64_t ld = ep ? a.mm.N : ldc;
+        cudaError_t e = cudaMemset2DAsync(acc, ld * 4, 0, a.mm.N * 4, a.mm.M, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        a.mm.C_out = acc;
+        a.mm.ldc = ld;
+        int rc = axq::launch_p4(a, st);
+        if (rc) return cuda_fail((cudaError_t)rc);
+        return ep ? launch_epilogue(a.mm.M, a.mm.N, acc, ld, epi, st) : AXQ_OK;
+    }
+    if (ep) {
+        a.mm.ep = epi;
         a.mm.C_out = nullptr;
     } else {
-        if (!C || ldc < a.mm.N) return AXQ_ERR_INVALID;
         a.mm.C_out = C;
         a.mm.ldc = ldc;
     }
-    if (a.mm.M == 0) return AXQ_OK;
     int rc = axq::launch_p4(a, st);
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }

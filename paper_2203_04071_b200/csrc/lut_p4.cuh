@@ -126,8 +126,16 @@ __device__ __forceinline__ const int8_t* p4_a_src(const P4Args& P, const RowInfo
     return p.A + ri.base + k0;
 }
 
+template <int RPL, bool HALF>
 __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
     using namespace p4;
+    using G = Geo<HALF>;
+    constexpr int STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ;
+    constexpr int SMEM_TBL = G::SMEM_TBL, SMEM_A = G::SMEM_A, SMEM_W = G::SMEM_W;
+    constexpr int SMEM_BAR = G::SMEM_BAR, SMEM_SCR = G::SMEM_SCR;
+    constexpr int BMR = WARPS * 32 * RPL;    // rows per CTA tile (1024 or 512)
+    constexpr int MT = 2 * RPL;              // m16 tiles per warp
+    constexpr int WROWS = 32 * RPL;          // rows per warp
     extern __shared__ __align__(1024) uint8_t p4_smem[];
     uint8_t* smem = p4_smem;
     const MMArgs& p = P.mm;
@@ -141,64 +149,92 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
     }
     __syncthreads();
 
-    const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + TN - 1) / TN;
-    const int64_t n_work = m_tiles * n_tiles;
-    const int nstages = (int)(P.Kp / KS);
-    uint32_t phase_bits = 0;   // parity of the next wait, one bit per stage buffer
+    const int64_t m_tiles = (p.M + BMR - 1) / BMR, n_blocks = (p.N + TN - 1) / TN;
+    const int splits = P.splits > 0 ? P.splits : 1;
+    const int64_t n_work = m_tiles * n_blocks * splits;
+    const int nst_all = (int)(P.Kp / KS);
+    const int sps = P.stages_per_split > 0 ? P.stages_per_split : nst_all;
+
+    // ---- work decomposition: tile -> (n block, m tile, k split) -> stage range ----
+    auto decode = [&](int64_t tile, int64_t& nb, int64_t& m0, int& s_b, int& s_e) {
+        const int ks = (int)(tile % splits);
+        const int64_t rest = tile / splits;
+        const int64_t mt = rest % m_tiles;
+        nb = rest / m_tiles;
+        m0 = mt * BMR;
+        s_b = ks * sps;
+        s_e = min(nst_all, s_b + sps);
+    };
+
+    // ---- producer state: a flat per-CTA stream of (tile, stage) items, STAGES buffers ----
+    int64_t i_tile = blockIdx.x, i_nb = 0, i_m0 = 0;
+    int i_st = 0, i_se = 0;
+    RowInfo irow[RPL];
+    auto set_issue_tile = [&]() {
+        if (i_tile >= n_work) return;
+        decode(i_tile, i_nb, i_m0, i_st, i_se);
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+            irow[i] = P.is_conv ? make_row<LOAD_CONV>(p, i_m0 + tid + i * NT)
+                                : make_row<LOAD_GEMM>(p, i_m0 + tid + i * NT);
+    };
+    uint32_t issued = 0;   // items issued by this CTA (buffer = index % STAGES)
+    auto issue_next = [&]() {
+        if (i_tile >= n_work) return;
+        const int buf = (int)(issued % STAGES);
+        const int64_t k0 = (int64_t)i_st * KS;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+            uint32_t nbytes;
+            const int8_t* src = p4_a_src(P, irow[i], k0, nbytes);
+            cp_async16(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS, src, nbytes);
+        }
+        cp_async_commit();
+        if (tid == 0) {
+            const uint32_t bar = bar0 + 8 * buf;
+            const uint32_t* tbl_g = P.tables + ((size_t)i_nb * P.Kp + (size_t)i_st * KS) * 4 * G::TROWS;
+            const int8_t* w_g = P.wpk + ((size_t)i_nb * (P.Kp / KS) + i_st) * W_STAGE;
+            mbar_expect_tx(bar, TBL_STAGE + W_STAGE);
+            bulk_g2s(s_base + SMEM_TBL + buf * TBL_STAGE, tbl_g, TBL_STAGE, bar);
+            bulk_g2s(s_base + SMEM_W + buf * W_STAGE, w_g, W_STAGE, bar);
+        }
+        ++issued;
+        if (++i_st >= i_se) {
+            i_tile += gridDim.x;
+            set_issue_tile();
+        }
+    };
+    set_issue_tile();
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) issue_next();
+
+    int* scr = reinterpret_cast<int*>(smem + SMEM_SCR + warp * SCR_WARP);
+    const int g = lane >> 2, t4 = lane & 3;
+    // element (row, col) of the warp scratch, XOR-swizzled so that a lane reading its row
+    // and a thread writing its mma fragment are (nearly) conflict free
+    auto sidx = [](int row, int col) { return row * TN + (col ^ (row & 15)); };
+    const uint32_t one = P.one;
+    uint32_t consumed = 0;   // items consumed (buffer = index % STAGES, phase = index / STAGES)
 
     for (int64_t tile = blockIdx.x; tile < n_work; tile += gridDim.x) {
-        const int64_t nb = tile / m_tiles;               // column block (tables shared in L2)
-        const int64_t m0 = (tile - nb * m_tiles) * BM;
+        int64_t nb, m0;
+        int s_b, s_e;
+        decode(tile, nb, m0, s_b, s_e);
         const int64_t n0 = nb * TN;
-        const uint32_t* tbl_g = P.tables + (size_t)nb * P.Kp * 4 * 256;
-        const int8_t* w_g = P.wpk + (size_t)nb * (P.Kp / KS) * W_STAGE;
-
-        // rows this thread copies (A tile rows tid and tid + 512)
-        RowInfo crow[2];
-        if (P.is_conv) {
-            crow[0] = make_row<LOAD_CONV>(p, m0 + tid);
-            crow[1] = make_row<LOAD_CONV>(p, m0 + tid + NT);
-        } else {
-            crow[0] = make_row<LOAD_GEMM>(p, m0 + tid);
-            crow[1] = make_row<LOAD_GEMM>(p, m0 + tid + NT);
-        }
-
-        auto issue = [&](int st) {
-            const int buf = st % STAGES;
-            const int64_t k0 = (int64_t)st * KS;
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                uint32_t nbytes;
-                const int8_t* src = p4_a_src(P, crow[i], k0, nbytes);
-                cp_async16(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS, src, nbytes);
-            }
-            cp_async_commit();
-            if (tid == 0) {
-                const uint32_t bar = bar0 + 8 * buf;
-                mbar_expect_tx(bar, TBL_STAGE + W_STAGE);
-                bulk_g2s(s_base + SMEM_TBL + buf * TBL_STAGE, tbl_g + (size_t)st * 4 * 256 * KS, TBL_STAGE, bar);
-                bulk_g2s(s_base + SMEM_W + buf * W_STAGE, w_g + (size_t)st * W_STAGE, W_STAGE, bar);
-            }
-        };
 
         uint32_t pacc[RPL][4][2];   // packed 16-bit E sums: [row][quad][even (c0,c2) / odd (c1,c3)]
 #pragma unroll
         for (int r = 0; r < RPL; ++r)
 #pragma unroll
             for (int q = 0; q < 4; ++q) pacc[r][q][0] = pacc[r][q][1] = 0u;
-        int cacc[4][2][4];     // exact part: 4 m16 tiles x 2 n8 tiles x mma C fragment
+        int cacc[MT][2][4];         // exact part: m16 tiles x 2 n8 tiles x mma C fragment
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) cacc[i][j][c] = 0;
 
-        int* scr = reinterpret_cast<int*>(smem + SMEM_SCR + warp * SCR_WARP);
-        const int g = lane >> 2, t4 = lane & 3;
-        // element (row, col) of the warp scratch, XOR-swizzled so that a lane reading its row
-        // and a thread writing its mma fragment are (nearly) conflict free
-        auto sidx = [](int row, int col) { return row * TN + (col ^ (row & 15)); };
         // packed lane sums -> scratch (lane layout) -> added into the mma fragments
         auto flush = [&]() {
 #pragma unroll
@@ -215,7 +251,7 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
             }
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                     const int row = i * 16 + g, col = j * 8 + 2 * t4;
@@ -226,32 +262,28 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
                 }
             __syncwarp();
         };
-        const uint32_t one = P.one;
 
-        for (int st = 0; st < STAGES && st < nstages; ++st) issue(st);
-
-        for (int st = 0; st < nstages; ++st) {
-            const int buf = st % STAGES;
-            // groups in flight here: stages <= st + STAGES - 2 (st >= 1) or 0..STAGES-1 (st = 0)
-            if (st == 0 && nstages > 1) cp_async_wait<STAGES - 1>(); else cp_async_wait<0>();
-            mbar_wait(bar0 + 8 * buf, (phase_bits >> buf) & 1u);
-            phase_bits ^= 1u << buf;
-            __syncthreads();                                   // stage st visible to all
-            if (st >= 1 && st - 1 + STAGES < nstages) {
-                // buffer of stage st-1 is free (everyone passed its compute): refill it
-                issue(st - 1 + STAGES);
-            }
+        for (int st = s_b; st < s_e; ++st) {
+            const int buf = (int)(consumed % STAGES);
+            // this item's cp.async group is complete once at most (later items in flight)
+            // groups remain outstanding
+            const uint32_t later = issued - consumed - 1;
+            if (later >= 2) cp_async_wait<2>(); else if (later == 1) cp_async_wait<1>(); else cp_async_wait<0>();
+            mbar_wait(bar0 + 8 * buf, (consumed / STAGES) & 1u);
+            ++consumed;
+            __syncthreads();                 // item visible to all; the previous buffer is free
+            if (consumed >= 2) issue_next(); // refill the buffer the previous item used
             const uint8_t* tb = smem + SMEM_TBL + buf * TBL_STAGE;
             const uint8_t* at = smem + SMEM_A + buf * A_STAGE;
 
-            // ---- exact part on the tensor cores: 4 m16 x 2 n8 tiles, k = 16 ----
+            // ---- exact part on the tensor cores: MT m16 x 2 n8 tiles, k = 16 ----
             {
                 uint32_t b0, b1;
                 ldmatrix_x2(s_base + SMEM_W + buf * W_STAGE + (lane & 15) * KS, b0, b1);
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < RPL; ++h) {
                     uint32_t a0, a1, a2, a3;
-                    ldmatrix_x4(s_base + SMEM_A + buf * A_STAGE + (warp * 64 + h * 32 + lane) * KS, a0, a1, a2, a3);
+                    ldmatrix_x4(s_base + SMEM_A + buf * A_STAGE + (warp * WROWS + h * 32 + lane) * KS, a0, a1, a2, a3);
                     mma_s8_16816(cacc[2 * h][0], a0, a1, b0);
                     mma_s8_16816(cacc[2 * h][1], a0, a1, b1);
                     mma_s8_16816(cacc[2 * h + 1][0], a2, a3, b0);
@@ -261,15 +293,15 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
             // ---- E lookups: 4 per 32-bit shared load, packed 16-bit accumulation ----
 #pragma unroll
             for (int r = 0; r < RPL; ++r) {
-                const uint4 av = *reinterpret_cast<const uint4*>(at + (warp * 64 + r * 32 + lane) * KS);
+                const uint4 av = *reinterpret_cast<const uint4*>(at + (warp * WROWS + r * 32 + lane) * KS);
                 const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
                 for (int kk = 0; kk < KS; ++kk) {
                     const uint32_t ua = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
-                    const uint8_t* row_t = tb + kk * 4 * 1024 + ua * 4u;
+                    const uint8_t* row_t = tb + kk * 4 * TQ + ua * 4u;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint32_t v = *reinterpret_cast<const uint32_t*>(row_t + q * 1024);
+                        const uint32_t v = *reinterpret_cast<const uint32_t*>(row_t + q * TQ);
                         const uint32_t ev = __byte_perm(v, 0u, 0x4240u);   // [b0, 0, b2, 0]
                         const uint32_t od = __byte_perm(v, 0u, 0x4341u);   // [b1, 0, b3, 0]
                         asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[r][q][0]) : "r"(ev), "r"(one));
@@ -277,13 +309,15 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
                     }
                 }
             }
-            if ((st + 1) % FLUSH_STAGES == 0 || st + 1 == nstages) flush();
+            if ((st - s_b + 1) % FLUSH_STAGES == 0 || st + 1 == s_e) flush();
         }
+        // bias of the packed sums and the storage-padding lookups (counted by the split that
+        // holds the end of K)
+        int corr = E_BIAS * KS * (s_e - s_b);
+        if (s_e == nst_all) corr += (int)(((P.Kp - p.K) + p.pad_lookups) * (int64_t)p.t00);
         // the int32 total of every output: write the mma fragments to the scratch, read rows
-        const int64_t corr_n = (P.Kp - p.K) + p.pad_lookups;   // storage-padding lookups (0,0)
-        const int corr = (int)(corr_n * (int64_t)p.t00) + E_BIAS * (int)P.Kp;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int row = i * 16 + g, col = j * 8 + 2 * t4;
@@ -300,21 +334,27 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
             for (int n = 0; n < TN; ++n) eacc[r][n] = scr[sidx(r * 32 + lane, n)] - corr;
         __syncwarp();
 
-        // ---- fused epilogue (same pinned order as lut_mm.cuh) ----
+        // ---- output: atomic int32 (split K), raw int32, or the fused epilogue ----
         const EpiArgs& e = p.ep;
         const bool raw = p.C_out != nullptr;
         const float sc = raw ? 0.f : __fmul_rn(*e.sa, *e.sw);
         const float s_out = (!raw && e.q) ? *e.s_out : 1.f;
-        const float qm = (float)((1 << ((e.q ? e.bits_out : 8) - 1)) - 1);
+        const float qm = (float)((1 << ((!raw && e.q ? e.bits_out : 8) - 1)) - 1);
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
-            const int64_t m = m0 + warp * 64 + r * 32 + lane;
+            const int64_t m = m0 + warp * WROWS + r * 32 + lane;
             if (m >= p.M) continue;
-            if (raw) {   // raw int32 output
+            if (raw) {
                 int32_t* c = p.C_out + m * p.ldc + n0;
+                if (splits > 1) {
 #pragma unroll
-                for (int n = 0; n < TN; ++n)
-                    if (n0 + n < p.N) c[n] = eacc[r][n];
+                    for (int n = 0; n < TN; ++n)
+                        if (n0 + n < p.N) atomicAdd(c + n, eacc[r][n]);
+                } else {
+#pragma unroll
+                    for (int n = 0; n < TN; ++n)
+                        if (n0 + n < p.N) c[n] = eacc[r][n];
+                }
                 continue;
             }
             const bool vec = (n0 + TN <= p.N) && !e.y_nchw &&
@@ -359,21 +399,21 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
                 }
             }
         }
-        __syncthreads();   // every warp done with the stage buffers before the next prologue
     }
 }
 
 // ---- weight preparation: E tables and the packed weight tile (once per layer) ----
-// tables[((nb*Kp + k)*4 + q)*256 + ua] = bytes j=0..3: E[ua][w(16nb+4q+j, k)]  (E = delta8 table)
+// tables[((nb*Kp + k)*4 + q)*rows + ua] = bytes j=0..3: E[ua][w(16nb+4q+j, k)] + 128 (E = delta8
+// table); rows = 256, or 128 when only non-negative activation codes will be looked up
 __global__ void p4_pack_tables_kernel(const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw,
                                       int64_t Kp, const int8_t* __restrict__ dtab,
-                                      uint32_t* __restrict__ tables) {
+                                      uint32_t* __restrict__ tables, int rows) {
     const int64_t n_blocks = (N + p4::TN - 1) / p4::TN;
-    const int64_t total = n_blocks * Kp * 4 * 256;
+    const int64_t total = n_blocks * Kp * 4 * rows;
     const int64_t gs = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
-        const int ua = (int)(i & 255);
-        int64_t t = i >> 8;
+        const int ua = (int)(i % rows);
+        int64_t t = i / rows;
         const int q = (int)(t & 3);
         t >>= 2;
         const int64_t k = t % Kp, nb = t / Kp;

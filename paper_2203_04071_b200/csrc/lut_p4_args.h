@@ -10,31 +10,41 @@ namespace p4 {
 constexpr int TN = 16;                     // output columns per CTA tile (4 quads)
 constexpr int WARPS = 16;
 constexpr int NT = WARPS * 32;             // 512 threads
-constexpr int RPL = 2;                     // rows per lane (lookups)
-constexpr int BM = WARPS * 32 * RPL;       // 1024 rows per CTA tile
 constexpr int KS = 16;                     // k per stage
-constexpr int STAGES = 2;
-constexpr int TBL_STAGE = KS * (TN / 4) * 1024;   // 64 KiB of E tables per stage
-constexpr int A_STAGE = BM * KS;                  // 16 KiB activation tile per stage
-constexpr int W_STAGE = TN * KS;                  // 256 B weight tile per stage
-constexpr int SMEM_TBL = 0;
-constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
-constexpr int SMEM_W = SMEM_A + STAGES * A_STAGE;
-constexpr int SMEM_BAR = SMEM_W + STAGES * W_STAGE;
-constexpr int SMEM_SCR = SMEM_BAR + 64;           // per-warp int32 [64 rows][16 cols] scratch
-constexpr int SCR_WARP = 64 * TN * 4;
-constexpr int SMEM_BYTES = SMEM_SCR + WARPS * SCR_WARP;
-constexpr int FLUSH_STAGES = 16;                  // 16-bit packed E sums: flush every 256 k
-constexpr int E_BIAS = 128;                       // tables hold E + 128 (unsigned bytes)
+constexpr int A_STAGE = 1024 * KS;         // activation tile per stage (1024 rows max)
+constexpr int W_STAGE = TN * KS;           // 256 B weight tile per stage
+constexpr int SCR_WARP = 64 * TN * 4;      // per-warp int32 [64 rows][16 cols] scratch
+constexpr int FLUSH_STAGES = 16;           // 16-bit packed E sums: flush every 256 k
+constexpr int E_BIAS = 128;                // tables hold E + 128 (unsigned bytes)
+
+// Table geometry: full range (ua = 0..255, any activation code) or half range (ua = 0..127,
+// non-negative activation codes, e.g. ReLU outputs): half the table bytes, one more stage.
+template <bool HALF>
+struct Geo {
+    static constexpr int TROWS = HALF ? 128 : 256;         // entries per (k, quad) table
+    static constexpr int TQ = TROWS * 4;                   // bytes per (k, quad) table
+    static constexpr int TBL_STAGE = KS * (TN / 4) * TQ;   // 32 / 64 KiB per stage
+    static constexpr int STAGES = HALF ? 3 : 2;
+    static constexpr int SMEM_TBL = 0;
+    static constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
+    static constexpr int SMEM_W = SMEM_A + STAGES * A_STAGE;
+    static constexpr int SMEM_BAR = SMEM_W + STAGES * W_STAGE;
+    static constexpr int SMEM_SCR = SMEM_BAR + 64;
+    static constexpr int SMEM_BYTES = SMEM_SCR + WARPS * SCR_WARP;
+};
 }  // namespace p4
 
 struct P4Args {
     MMArgs mm;                  // geometry, loader info, t00, epilogue (k_split unused)
-    const uint32_t* tables;     // [n_blocks][Kp][4][256] u32
+    const uint32_t* tables;     // [n_blocks][Kp][4][256 or 128] u32
     const int8_t* wpk;          // [n_blocks][Kp/16][16 n][16 k]
     int64_t Kp;                 // K rounded up to a multiple of 16
     int is_conv;
-    uint32_t one;               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)
+    uint32_t one;
+    int splits;                 // K splits (>1: atomic int32 into C_out, epilogue run after)
+    int stages_per_split;       // 16-k stages per split
+    int rpl;                    // rows per lane: 2 (1024-row tiles) or 1 (512-row tiles)
+    int half;                   // tables cover ua = 0..127 only (non-negative activations)               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)
 };
 
 }  // namespace axq

@@ -28,7 +28,9 @@ int launch_mm_i32(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid,
 // P4 kernel (lut_p4.cuh); declared here with an opaque argument struct.
 struct P4Args;
 int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int8_t* dtab,
-            uint32_t* tables, int8_t* wpk, cudaStream_t st);
+            uint32_t* tables, int8_t* wpk, int half, cudaStream_t st);
 int launch_p4(const P4Args& a, cudaStream_t st);
+void p4_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& rpl, int& splits,
+             int& sps);
 
 }  // namespace axq

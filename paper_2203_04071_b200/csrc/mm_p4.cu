@@ -5,34 +5,66 @@
 namespace axq {
 
 int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int8_t* dtab,
-            uint32_t* tables, int8_t* wpk, cudaStream_t st) {
+            uint32_t* tables, int8_t* wpk, int half, cudaStream_t st) {
     const int64_t nb = (N + p4::TN - 1) / p4::TN;
-    const int64_t t1 = nb * Kp * 4 * 256, t2 = nb * Kp * p4::TN;
+    const int rows = half ? 128 : 256;
+    const int64_t t1 = nb * Kp * 4 * rows, t2 = nb * Kp * p4::TN;
     p4_pack_tables_kernel<<<(unsigned)std::min<int64_t>((t1 + 255) / 256, 148 * 16), 256, 0, st>>>(
-        W, N, K, ldw, Kp, dtab, tables);
+        W, N, K, ldw, Kp, dtab, tables, rows);
     p4_pack_w_kernel<<<(unsigned)std::min<int64_t>((t2 + 255) / 256, 148 * 16), 256, 0, st>>>(W, N, K, ldw, Kp, wpk);
     return (int)cudaGetLastError();
 }
 
-int launch_p4(const P4Args& a, cudaStream_t st) {
+template <int RPL, bool HALF>
+static int launch_p4_t(const P4Args& a, cudaStream_t st) {
     static unsigned configured = 0;
-    static int sms[32] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
     dev &= 31;
     if (!(configured & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(lut_p4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             p4::SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(lut_p4_kernel<RPL, HALF>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             p4::Geo<HALF>::SMEM_BYTES);
         if (e != cudaSuccess) return (int)e;
-        int n = 0;
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        sms[dev] = n > 0 ? n : 148;
         configured |= 1u << dev;
     }
-    const int64_t work = ((a.mm.M + p4::BM - 1) / p4::BM) * ((a.mm.N + p4::TN - 1) / p4::TN);
-    const unsigned g = (unsigned)std::min<int64_t>(work, sms[dev]);
-    lut_p4_kernel<<<g, p4::NT, p4::SMEM_BYTES, st>>>(a);
+    const int64_t bm = (int64_t)p4::WARPS * 32 * RPL;
+    const int64_t work = ((a.mm.M + bm - 1) / bm) * ((a.mm.N + p4::TN - 1) / p4::TN) * a.splits;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = (unsigned)std::min<int64_t>(work, sms > 0 ? sms : 148);
+    lut_p4_kernel<RPL, HALF><<<g, p4::NT, p4::Geo<HALF>::SMEM_BYTES, st>>>(a);
     return (int)cudaGetLastError();
+}
+
+int launch_p4(const P4Args& a, cudaStream_t st) {
+    if (a.half) return a.rpl == 1 ? launch_p4_t<1, true>(a, st) : launch_p4_t<2, true>(a, st);
+    return a.rpl == 1 ? launch_p4_t<1, false>(a, st) : launch_p4_t<2, false>(a, st);
+}
+
+// Tile shape and K split.  Large problems: 1024- or 512-row tiles, whichever needs fewer
+// persistent-CTA waves per row (512-row tiles cost ~8% more per lookup: the table fill is
+// amortised over half the rows); no split (its atomics and extra epilogue pass cost more than
+// a partial wave).  Problems whose 512-row tiles cannot fill the SMs: split K (exact, int32
+// atomics) until they do, keeping >= 4 stages (64 k) per split.
+void p4_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& rpl, int& splits,
+             int& sps) {
+    const int64_t nst = Kp / p4::KS, nb = (N + p4::TN - 1) / p4::TN;
+    const int64_t t2 = ((M + 1023) / 1024) * nb, t1 = ((M + 511) / 512) * nb;
+    splits = 1;
+    sps = (int)nst;
+    if (t1 >= sms || !can_split) {
+        const double c2 = (double)((t2 + sms - 1) / sms) * 1024.0;
+        const double c1 = (double)((t1 + sms - 1) / sms) * 512.0 * 1.08;
+        rpl = (c1 < c2) ? 1 : 2;
+        return;
+    }
+    rpl = 1;
+    int64_t s = (sms + t1 - 1) / t1;                   // enough parts to cover every SM
+    s = std::min<int64_t>(s, std::max<int64_t>(1, nst / 4));
+    const int64_t per = (nst + s - 1) / s;
+    sps = (int)per;
+    splits = (int)((nst + per - 1) / per);
 }
 
 }  // namespace axq

@@ -65,7 +65,9 @@ class ApproxConv2d:
     """Conv2d with every multiply a LUT lookup; NCHW fp32 in/out, implicit im2col."""
 
     def __init__(self, weight: torch.Tensor, bias: torch.Tensor | None, lut: ax.Lut,
-                 stride=(1, 1), padding=(0, 0), device="cuda", packed=True):
+                 stride=(1, 1), padding=(0, 0), device="cuda", packed=True, a_nonneg=False):
+        """a_nonneg: the layer input is non-negative (e.g. a ReLU output), so its codes are >= 0
+        and the packed kernel may use half-range tables."""
         self.lut = lut
         self.bits = lut.bits
         w = weight.to(device=device, dtype=torch.float32).contiguous()   # [K][C][R][S]
@@ -82,7 +84,7 @@ class ApproxConv2d:
         self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
         self.wp = None
         if packed and lut.repr == "delta8" and self.C % 16 == 0 and self.C * self.R * self.S >= 128:
-            self.wp = ax.WPack(lut, self.qw.reshape(self.Kout, -1))
+            self.wp = ax.WPack(lut, self.qw.reshape(self.Kout, -1), a_nonneg=a_nonneg)
         self.n_sms = torch.cuda.get_device_properties(torch.device(device)).multi_processor_count
         self.d_amax_a = torch.empty(1, device=device)
         self.d_scale_a = torch.empty(1, device=device)

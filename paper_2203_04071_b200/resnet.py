@@ -83,12 +83,13 @@ class ApproxResNet:
                     q = qp
             self.qw[name] = q
         self.fc_bias = torch.as_tensor(weights["fc.b"]).to(self.dev, torch.float32).contiguous()
-        # prepared weights for the packed-table kernel (delta8 tables, C % 16 == 0, K >= 128)
+        # prepared weights for the packed-table kernel (delta8 tables, C % 16 == 0, K >= 64)
         self.wp = {}
         if packed and lut.repr == "delta8":
             for name, kind, cout, cin, k, stride, pad in self.specs:
-                if kind == "conv" and cin % 16 == 0 and cin * k * k >= 128:
-                    self.wp[name] = ax.WPack(lut, self.qw[name].reshape(cout, -1))
+                if kind == "conv" and cin % 16 == 0 and cin * k * k >= 64:
+                    # every conv input here is a quantized ReLU output: codes >= 0
+                    self.wp[name] = ax.WPack(lut, self.qw[name].reshape(cout, -1), a_nonneg=True)
         self.n_sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._bufs = {}
         self.calibrated = False

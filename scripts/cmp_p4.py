@@ -29,7 +29,7 @@ for name, N, H, W, C, K, R, st, pd in shapes:
     q = torch.empty(N, Ho, Wo, K, dtype=torch.int8, device="cuda")
     so = torch.tensor([0.05], device="cuda")
     ep = ax.make_epilogue(sa, sw, y=y, ldy=K, y_nhwc=True, relu=True, q_out=q, ldq=K, d_scale_out=so, bits_out=8)
-    wp = ax.WPack(lut, w.reshape(K, -1))
+    wp = ax.WPack(lut, w.reshape(K, -1), a_nonneg=True)
     t1 = bench(lambda: ax.axq_lut_conv2d_ep(d, x, w, lut, ep))
     y1 = y.clone()
     t2 = bench(lambda: ax.axq_lut_conv2d_wp(d, x, wp, ep))

@@ -41,15 +41,16 @@ for b in [s[0][:-3] for s in layer_specs() if s[0].endswith(".c1")]:
     h2, w2, e = conv(b + ".c2", h1, w1); order.append(e)
     h, w, e = conv(b + ".c3", h2, w2); order.append(e)
 order.append(("fc", batch * 1000 * 2048, (batch, 1000, 2048)))
-luts = [d for d in fw if "lut_mm" in d["name"]]
+luts = [d for d in fw if ("lut_mm" in d["name"] or "lut_p4" in d["name"])]
 tot = totl = 0.0
 for (n, lk, mnk), d in zip(order, luts):
     t = float(d["gpu__time_duration.sum"]) / 1e3
     tot += t
     totl += lk
-    print("%-11s M=%7d N=%5d K=%5d grid=%-6s %8.1f us %6.0f Glk/s frac %.2f" % (
-        n, *mnk, d.get("launch__grid_size", "?"), t, lk / t / 1e3, lk / t / 1e3 / 9306.24))
+    print("%-11s M=%7d N=%5d K=%5d %-3s grid=%-6s %8.1f us %6.0f Glk/s frac %.2f" % (
+        n, *mnk, "p4" if "lut_p4" in d["name"] else "v1", d.get("launch__grid_size", "?"), t,
+        lk / t / 1e3, lk / t / 1e3 / 9306.24))
 print("LUT kernels: %.2f ms, %.0f Glk/s, frac %.3f" % (tot / 1e3, totl / tot / 1e3, totl / tot / 1e3 / 9306.24))
 for d in fw:
-    if "lut_mm" not in d["name"]:
+    if "lut_mm" not in d["name"] and "lut_p4" not in d["name"]:
         print("  %-60s %8.1f us" % (d["name"][:60], float(d["gpu__time_duration.sum"]) / 1e3))

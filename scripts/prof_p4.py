@@ -15,7 +15,7 @@ d = ax.conv_desc(N, H, W, C, K, 3, 3, (1, 1), (1, 1))
 sa = torch.tensor([0.01], device="cuda"); sw = torch.tensor([0.01], device="cuda")
 y = torch.empty(N, K, H, W, device="cuda")
 ep = ax.make_epilogue(sa, sw, y=y)
-wp = ax.WPack(lut, w.reshape(K, -1))
+wp = ax.WPack(lut, w.reshape(K, -1), a_nonneg=True)
 for _ in range(2):
     if which == "p4":
         ax.axq_lut_conv2d_wp(d, x, wp, ep)

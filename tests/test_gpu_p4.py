@@ -92,3 +92,60 @@ def test_p4_config2_full(ax):
     for img in (0, 127):
         acc = oracle.lut_conv2d(oracle.quantize(c.x[img:img + 1], sa, 8), qw, c.lut, 8, (1, 1), (1, 1))
         np.testing.assert_array_equal(y[img:img + 1].cpu().numpy(), oracle.dequantize(acc, sa, sw, None, 1))
+
+
+@pytest.mark.parametrize("M,N,K", [(1600, 512, 4608), (700, 64, 640), (6272, 256, 2304)])
+def test_p4_small_m_split_k_fused(ax, M, N, K):
+    """Small-M shapes take 512-row tiles and an exact split-K (atomics + epilogue kernel)."""
+    T = datagen.lut_randerr(8, 0, 2)
+    A = datagen.random_int8(400 + M, (M, K))
+    W = datagen.random_int8(500 + N, (N, K))
+    ref = oracle.lut_gemm(A, W, T, 8)
+    lut = ax.Lut(8, T)
+    wp = ax.WPack(lut, _t(W))
+    dA = _t(A)
+    C = torch.empty(M, N, dtype=torch.int32, device=DEV)
+    ax.axq_lut_gemm_wp(dA, wp, None, C)
+    np.testing.assert_array_equal(C.cpu().numpy(), ref)
+    sa, sw = np.float32(0.013), np.float32(0.002)
+    dsa, dsw = _t(np.array([sa])), _t(np.array([sw]))
+    bias = datagen.normal(6, 6, (N,), 0.1)
+    db = _t(bias)
+    y = torch.empty(M, N, device=DEV)
+    ws = torch.empty(M * N, dtype=torch.int32, device=DEV)
+    ep = ax.make_epilogue(dsa, dsw, bias=db, y=y, ldy=N, workspace=ws)
+    ax.axq_lut_gemm_wp(dA, wp, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.dequantize(ref, sa, sw, bias))
+
+
+@pytest.mark.parametrize("M,N,K", [(3000, 48, 576), (1100, 16, 2048), (600, 40, 100)])
+def test_p4_half_range_nonneg(ax, M, N, K):
+    """a_nonneg handles (tables for codes 0..127) on non-negative activations."""
+    T = datagen.lut_randerr(8, 0, 2)
+    A = (datagen.random_int8(600 + M, (M, K)).astype(np.int64) & 127).astype(np.int8)
+    W = datagen.random_int8(700 + N, (N, K))
+    ref = oracle.lut_gemm(A, W, T, 8)
+    lut = ax.Lut(8, T)
+    wp = ax.WPack(lut, _t(W), a_nonneg=True)
+    C = torch.empty(M, N, dtype=torch.int32, device=DEV)
+    Kp = (K + 15) // 16 * 16
+    dA = torch.zeros(M, Kp, dtype=torch.int8, device=DEV)     # lda % 16 == 0
+    dA[:, :K] = _t(A)
+    ax.axq_lut_gemm_wp(dA.narrow(1, 0, K), wp, None, C)
+    np.testing.assert_array_equal(C.cpu().numpy(), ref)
+
+
+def test_p4_half_range_conv_relu_input(ax):
+    c = datagen.config2(batch=3)
+    sa = oracle.scale(oracle.amax(c.x), 8)
+    qw, sw = oracle.quantize_tensor(c.W, 8)
+    qx = oracle.quantize(c.x, sa, 8)
+    assert qx.min() >= 0
+    ref = oracle.lut_conv2d(qx, qw, c.lut, 8, (1, 1), (1, 1))
+    lut = ax.Lut(8, c.lut)
+    wp = ax.WPack(lut, _t(qw.transpose(0, 2, 3, 1).reshape(64, -1)), a_nonneg=True)
+    d = ax.conv_desc(3, 56, 56, 64, 64, 3, 3, (1, 1), (1, 1))
+    Y = torch.empty(3, 56, 56, 64, dtype=torch.int32, device=DEV)
+    ax.axq_lut_conv2d_wp(d, _t(qx.transpose(0, 2, 3, 1)), wp, None, Y)
+    np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
