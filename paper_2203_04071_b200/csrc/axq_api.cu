@@ -590,7 +590,8 @@ axq_status axq_lut_gemm_wp(int64_t M, const int8_t* A, int64_t lda, axq_wpack_t 
 axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_t wp,
                              const axq_epilogue* ep, int32_t* Y, void* stream) {
     if (!wp || !d) return AXQ_ERR_INVALID;
-    if (d->groups != 1 || (d->C & 15) || !aligned16(X)) return AXQ_ERR_UNSUPPORTED;
+    if (d->groups != 1 || (d->C & 3) || (reinterpret_cast<uintptr_t>(X) & 3)) return AXQ_ERR_UNSUPPORTED;
+    const bool c4 = (d->C & 15) || !aligned16(X);
     if (d->K != wp->N || d->R * d->S * d->C != wp->K) return AXQ_ERR_INVALID;
     axq::P4Args a{};
     int loader = 0;
@@ -609,6 +610,7 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
     p.ph = (int)d->pad_h; p.pw = (int)d->pad_w; p.dh = (int)d->dil_h; p.dw = (int)d->dil_w;
     const int64_t cv = d->c_valid ? d->c_valid : d->C;
     p.pad_lookups = (int32_t)(d->R * d->S * (d->C - cv));
+    a.c4 = c4 ? 1 : 0;
     return p4_run(a, wp, ep, true, Y, d->K, S(stream));
 }
 

@@ -69,6 +69,11 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
                  : "memory");
 }
 
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 
 template <int N>
@@ -183,11 +188,30 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
         if (i_tile >= n_work) return;
         const int buf = (int)(issued % STAGES);
         const int64_t k0 = (int64_t)i_st * KS;
+        if (P.c4) {
+            // C % 4 == 0 (small C, e.g. the padded network input): 4 taps of 4 bytes per 16 k
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-            uint32_t nbytes;
-            const int8_t* src = p4_a_src(P, irow[i], k0, nbytes);
-            cp_async16(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS, src, nbytes);
+            for (int j = 0; j < 4; ++j) {
+                const int64_t k = k0 + 4 * j;
+                const int rs = (int)(k / p.C);
+                const int c = (int)(k - (int64_t)rs * p.C);
+                const int r = rs / p.S, s_ = rs - r * p.S;
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    const RowInfo& ri = irow[i];
+                    const int hi = ri.hb + r * p.dh, wi = ri.wb + s_ * p.dw;
+                    const bool ok = ri.valid && k < p.K && hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd;
+                    const int8_t* src = ok ? p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c : p.A;
+                    cp_async4(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS + 4 * j, src, ok ? 4u : 0u);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                uint32_t nbytes;
+                const int8_t* src = p4_a_src(P, irow[i], k0, nbytes);
+                cp_async16(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS, src, nbytes);
+            }
         }
         cp_async_commit();
         if (tid == 0) {

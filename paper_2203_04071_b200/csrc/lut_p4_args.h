@@ -44,7 +44,8 @@ struct P4Args {
     int splits;                 // K splits (>1: atomic int32 into C_out, epilogue run after)
     int stages_per_split;       // 16-k stages per split
     int rpl;                    // rows per lane: 2 (1024-row tiles) or 1 (512-row tiles)
-    int half;                   // tables cover ua = 0..127 only (non-negative activations)               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)
+    int half;                   // tables cover ua = 0..127 only (non-negative activations)
+    int c4;                     // conv with C % 16 != 0 (C % 4 == 0): 4-byte tap copies               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)
 };
 
 }  // namespace axq

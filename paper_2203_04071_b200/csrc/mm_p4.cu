@@ -44,9 +44,9 @@ int launch_p4(const P4Args& a, cudaStream_t st) {
 
 // Tile shape and K split.  Large problems: 1024- or 512-row tiles, whichever needs fewer
 // persistent-CTA waves per row (512-row tiles cost ~8% more per lookup: the table fill is
-// amortised over half the rows); no split (its atomics and extra epilogue pass cost more than
-// a partial wave).  Problems whose 512-row tiles cannot fill the SMs: split K (exact, int32
-// atomics) until they do, keeping >= 4 stages (64 k) per split.
+// amortised over half the rows); no split (measured: its atomics and extra epilogue pass cost
+// more than a partial wave).  Problems whose 512-row tiles cannot fill the SMs: split K
+// (exact, int32 atomics) until they do, keeping >= 4 stages (64 k) per split.
 void p4_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& rpl, int& splits,
              int& sps) {
     const int64_t nst = Kp / p4::KS, nb = (N + p4::TN - 1) / p4::TN;

@@ -87,8 +87,11 @@ class ApproxResNet:
         self.wp = {}
         if packed and lut.repr == "delta8":
             for name, kind, cout, cin, k, stride, pad in self.specs:
-                if kind == "conv" and cin % 16 == 0 and cin * k * k >= 64:
-                    # every conv input here is a quantized ReLU output: codes >= 0
+                if kind == "conv" and name == "stem":
+                    # the network input is signed: full-range tables, padded C = 4 (4-byte copies)
+                    self.wp[name] = ax.WPack(lut, self.qw[name].reshape(cout, -1), a_nonneg=False)
+                elif kind == "conv" and cin % 16 == 0 and cin * k * k >= 64:
+                    # every other conv input is a quantized ReLU output: codes >= 0
                     self.wp[name] = ax.WPack(lut, self.qw[name].reshape(cout, -1), a_nonneg=True)
         self.n_sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._bufs = {}

@@ -149,3 +149,22 @@ def test_p4_half_range_conv_relu_input(ax):
     Y = torch.empty(3, 56, 56, 64, dtype=torch.int32, device=DEV)
     ax.axq_lut_conv2d_wp(d, _t(qx.transpose(0, 2, 3, 1)), wp, None, Y)
     np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
+
+
+def test_p4_conv_c4_padded_stem(ax):
+    """C = 3 stored as C = 4 (zero channel, c_valid = 3): the 4-byte-copy operand path."""
+    X = datagen.random_int8(130, (2, 3, 20, 18))
+    Wt = datagen.random_int8(131, (16, 3, 7, 7))
+    T = datagen.lut_randerr(8, 0, 2)
+    ref = oracle.lut_conv2d(X, Wt, T, 8, (2, 2), (3, 3))
+    Xp = np.zeros((2, 20, 18, 4), np.int8)
+    Xp[..., :3] = X.transpose(0, 2, 3, 1)
+    Wp = np.zeros((16, 7, 7, 4), np.int8)
+    Wp[..., :3] = Wt.transpose(0, 2, 3, 1)
+    lut = ax.Lut(8, T)
+    wp = ax.WPack(lut, _t(Wp.reshape(16, -1)))
+    d = ax.conv_desc(2, 20, 18, 4, 16, 7, 7, (2, 2), (3, 3), c_valid=3)
+    Ho, Wo = ax.axq_conv2d_out_hw(d)
+    Y = torch.empty(2, Ho, Wo, 16, dtype=torch.int32, device=DEV)
+    ax.axq_lut_conv2d_wp(d, _t(Xp), wp, None, Y)
+    np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
