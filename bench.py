@@ -341,10 +341,11 @@ class LstmWL:
         self.x_host = torch.from_numpy(c.x).pin_memory()
         self.x = self.x_host.to(dev)
         self.nets = {}
+        self.replay = {}
         for b in (4, 6, 8):
             n = ApproxLSTM(c.W_ih, c.W_hh, c.b_ih, c.b_hh, Lut(b, c.luts[b]), dev)
             n.calibrate(self.x)
-            n.timing_hook = timer
+            self.replay[b] = n.capture(self.x)      # 128-step static forward as a CUDA graph
             self.nets[b] = n
         torch.cuda.synchronize()
         T, B, _ = self.x.shape
@@ -358,14 +359,18 @@ class LstmWL:
         self.per_bit_ms = {}
         self.desc = {"workload": "BJ configs[4]: LSTM input 512, hidden 1024, seq 128, batch 64, "
                                  "approximate ih/hh gate GEMMs at b = 4, 6, 8 (randerr LUTs), "
-                                 "static scales calibrated untimed", "lookups_per_bitwidth": per_b}
+                                 "static scales calibrated untimed; each forward replayed as one "
+                                 "CUDA graph", "lookups_per_bitwidth": per_b}
+        self.timer = timer
 
     def step(self, stream, dist):
         import torch
         for b, n in self.nets.items():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            n.forward(self.x, stream)
+            self.timer("pre", stream)    # graph replay: the LUT-kernel time is bounded by the
+            self.replay[b]()             # whole forward (GEMMs + cell kernels), conservative
+            self.timer("post", stream)
             e1.record(stream)
             self.per_bit_ms.setdefault(b, []).append((e0, e1))
 

@@ -99,15 +99,19 @@ axq_status launch_mm(int epi, int loader, int repr, const axq::MMArgs& p, const 
 Cfg pick_cfg(int64_t M, int loader, int repr) {
     const bool big_ok = repr != AXQ_LUT_I32 &&
                         (loader == axq::LOAD_GEMM || loader == axq::LOAD_CONV || loader == axq::LOAD_CONV_C4);
+    if (big_ok && loader == axq::LOAD_GEMM && M <= 64) return axq::CFG_TINY;
     return (M > 2048 && big_ok) ? CFG_BIG : CFG_SMALL;
 }
+
+inline int64_t cfg_bm(const Cfg& c) { return (int64_t)32 * c.R * (c.nsplit ? 1 : c.warps); }
+inline int64_t cfg_bn(const Cfg& c) { return (int64_t)c.tn * (c.nsplit ? c.warps : 1); }
 
 // K-splitting so that small M*N problems still fill the SMs (exact: integer atomics).
 int64_t pick_k_split(int64_t M, int64_t N, int64_t K, const Cfg& c, bool allow) {
     int64_t kr = ((K + axq::KC - 1) / axq::KC) * axq::KC;
     if (!allow || K <= 0) return std::max<int64_t>(kr, axq::KC);
-    int64_t bm = (int64_t)c.warps * 32 * c.R;
-    int64_t tiles = ((M + bm - 1) / bm) * ((N + c.tn - 1) / c.tn);
+    int64_t bm = cfg_bm(c);
+    int64_t tiles = ((M + bm - 1) / bm) * ((N + cfg_bn(c) - 1) / cfg_bn(c));
     int64_t want = (int64_t)sm_count() * 2;
     if (tiles >= want) return kr;
     int64_t splits = (want + tiles - 1) / tiles;
@@ -343,8 +347,8 @@ static axq_status run_mm(axq::MMArgs& p, int loader, axq_lut_t lut, const axq::E
     const bool can_split = epi ? (workspace != nullptr) : true;
     p.k_split = pick_k_split(p.M, p.N, p.K, c, can_split);
     const int64_t splits = p.K > 0 ? (p.K + p.k_split - 1) / p.k_split : 1;
-    const int64_t bm = (int64_t)c.warps * 32 * c.R;
-    dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + c.tn - 1) / c.tn), (unsigned)splits);
+    const int64_t bm = cfg_bm(c), bn = cfg_bn(c);
+    dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + bn - 1) / bn), (unsigned)splits);
     if (!epi) {
         p.C_out = C_raw;
         p.ldc = ldc;

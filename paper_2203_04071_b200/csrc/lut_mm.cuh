@@ -191,11 +191,14 @@ __device__ __forceinline__ uint4 load_w(const MMArgs& p, int64_t n, int64_t k0, 
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16) ? 1 : (WARPS >= 8 ? 2 : 3))
+// NSPLIT: warps split the CTA's columns instead of its rows (small M, e.g. the LSTM's
+// recurrent GEMM with M = 64): CTA tile = (32 R) rows x (WARPS TN) columns.
+template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, bool NSPLIT = false>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16 || NSPLIT) ? 1 : (WARPS >= 8 ? 2 : 3))
 lut_mm_kernel(const MMArgs p) {
     constexpr int NT = WARPS * 32;
-    constexpr int BM = WARPS * 32 * R;
+    constexpr int BM = NSPLIT ? 32 * R : WARPS * 32 * R;
+    constexpr int CTN = NSPLIT ? WARPS * TN : TN;   // columns per CTA tile
     extern __shared__ __align__(16) int8_t smem[];
     // layout: [table (table_bytes, 0 for I32)] [W tiles: 2 x KC/4 x TN words]
     int8_t* lut_s = smem;
@@ -203,7 +206,7 @@ lut_mm_kernel(const MMArgs p) {
     uint32_t* w_s = reinterpret_cast<uint32_t*>(smem + tbytes);
     const int32_t* lut_g = reinterpret_cast<const int32_t*>(p.table);
 
-    uint32_t* tap_s = w_s + 2 * (KC / 4) * TN;   // LOAD_CONV_C4 tap table (K/4 entries)
+    uint32_t* tap_s = w_s + 2 * (KC / 4) * CTN;  // LOAD_CONV_C4 tap table (K/4 entries)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool wvec = ((p.ldw & 15) == 0) && ((reinterpret_cast<uintptr_t>(p.W) & 15) == 0);
 
@@ -226,14 +229,15 @@ lut_mm_kernel(const MMArgs p) {
         }
     }
 
-    const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + TN - 1) / TN;
+    const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + CTN - 1) / CTN;
     const int64_t n_split = (p.K + p.k_split - 1) / p.k_split;
     const int64_t n_work = m_tiles * n_tiles * (n_split > 0 ? n_split : 1);
     for (int64_t tile = blockIdx.x; tile < n_work; tile += gridDim.x) {
     const int64_t ks = n_split > 0 ? tile % n_split : 0;
     const int64_t mn = n_split > 0 ? tile / n_split : tile;
     const int64_t m0 = (mn / n_tiles) * BM;
-    const int64_t n0 = (mn % n_tiles) * TN;
+    const int64_t nc0 = (mn % n_tiles) * CTN;            // CTA's first column
+    const int64_t n0 = nc0 + (NSPLIT ? warp * TN : 0);   // this warp's first column
     const int64_t kb = ks * p.k_split;
     const int64_t ke = min(p.K, kb + p.k_split);
     const int nchunks = (int)((ke - kb + KC - 1) / KC);
@@ -241,7 +245,7 @@ lut_mm_kernel(const MMArgs p) {
     RowInfo rows[R];
 #pragma unroll
     for (int r = 0; r < R; ++r)
-        rows[r] = make_row<LOADER>(p, m0 + (int64_t)(warp * R + r) * 32 + lane);
+        rows[r] = make_row<LOADER>(p, m0 + (int64_t)((NSPLIT ? 0 : warp * R) + r) * 32 + lane);
 
     int acc[R][TN];
 #pragma unroll
@@ -254,12 +258,12 @@ lut_mm_kernel(const MMArgs p) {
     if (nchunks > 0) {
 #pragma unroll
         for (int r = 0; r < R; ++r) a_cur[r] = load_a<LOADER>(p, rows[r], kb, tap_s);
-        if (tid < TN) {
-            uint4 wv = load_w(p, n0 + tid, kb, wvec);
-            w_s[0 * TN + tid] = wv.x;
-            w_s[1 * TN + tid] = wv.y;
-            w_s[2 * TN + tid] = wv.z;
-            w_s[3 * TN + tid] = wv.w;
+        if (tid < CTN) {
+            uint4 wv = load_w(p, nc0 + tid, kb, wvec);
+            w_s[0 * CTN + tid] = wv.x;
+            w_s[1 * CTN + tid] = wv.y;
+            w_s[2 * CTN + tid] = wv.z;
+            w_s[3 * CTN + tid] = wv.w;
         }
     }
     __syncthreads();
@@ -270,9 +274,9 @@ lut_mm_kernel(const MMArgs p) {
         if (has_next) {
 #pragma unroll
             for (int r = 0; r < R; ++r) a_nxt[r] = load_a<LOADER>(p, rows[r], kn, tap_s);
-            if (tid < TN) w_nxt = load_w(p, n0 + tid, kn, wvec);
+            if (tid < CTN) w_nxt = load_w(p, nc0 + tid, kn, wvec);
         }
-        const uint32_t* ws = w_s + (ci & 1) * (4 * TN);
+        const uint32_t* ws = w_s + (ci & 1) * (4 * CTN) + (NSPLIT ? warp * TN : 0);
 #pragma unroll
         for (int kq = 0; kq < 4; ++kq) {
             uint32_t a4[R], alo[R], ahi[R];
@@ -284,7 +288,7 @@ lut_mm_kernel(const MMArgs p) {
             }
 #pragma unroll
             for (int n4 = 0; n4 < TN / 4; ++n4) {
-                const uint4 wv = *reinterpret_cast<const uint4*>(ws + kq * TN + n4 * 4);
+                const uint4 wv = *reinterpret_cast<const uint4*>(ws + kq * CTN + n4 * 4);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t w4 = (j == 0) ? wv.x : (j == 1) ? wv.y : (j == 2) ? wv.z : wv.w;
@@ -309,12 +313,12 @@ lut_mm_kernel(const MMArgs p) {
         if (has_next) {
 #pragma unroll
             for (int r = 0; r < R; ++r) a_cur[r] = a_nxt[r];
-            if (tid < TN) {
-                uint32_t* wd = w_s + ((ci + 1) & 1) * (4 * TN);
-                wd[0 * TN + tid] = w_nxt.x;
-                wd[1 * TN + tid] = w_nxt.y;
-                wd[2 * TN + tid] = w_nxt.z;
-                wd[3 * TN + tid] = w_nxt.w;
+            if (tid < CTN) {
+                uint32_t* wd = w_s + ((ci + 1) & 1) * (4 * CTN);
+                wd[0 * CTN + tid] = w_nxt.x;
+                wd[1 * CTN + tid] = w_nxt.y;
+                wd[2 * CTN + tid] = w_nxt.z;
+                wd[3 * CTN + tid] = w_nxt.w;
             }
         }
         __syncthreads();

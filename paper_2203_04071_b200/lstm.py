@@ -126,6 +126,26 @@ class ApproxLSTM:
         assert self.calibrated, "calibrate() first (static scales)"
         return self.run(x, False, stream)
 
+    def capture(self, x):
+        """Record the static forward on x (a fixed device buffer) as a CUDA graph: the 128
+        sequential steps are ~4 short launches each, which the host cannot issue as fast as the
+        GPU runs them.  Returns a replay callable (same results as forward(x))."""
+        assert self.calibrated, "calibrate() first (static scales)"
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self.run(x, False, side)           # warm-up: kernel attributes, workspaces
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.run(x, False, torch.cuda.current_stream(self.dev))
+        self._graph = g
+
+        def replay():
+            g.replay()
+            return out
+        return replay
+
     __call__ = forward
 
     def lookups(self, T, B) -> int:

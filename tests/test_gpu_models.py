@@ -96,3 +96,18 @@ def test_lstm_config4_full(bits):
     hs_ref, c_ref = orc.forward((s_x, s_h))
     np.testing.assert_array_equal(hs.cpu().numpy(), hs_ref)
     np.testing.assert_array_equal(cT.cpu().numpy(), c_ref)
+
+
+def test_lstm_cuda_graph_replay_matches_forward():
+    from paper_2203_04071_b200 import Lut
+    from paper_2203_04071_b200.lstm import ApproxLSTM
+    c = datagen.config4(T=9, B=4, I=64, H=48)
+    net = ApproxLSTM(c.W_ih, c.W_hh, c.b_ih, c.b_hh, Lut(8, c.luts[8]), DEV)
+    xd = torch.from_numpy(c.x).to(DEV)
+    net.calibrate(xd)
+    hs, cT = net.forward(xd)
+    hs, cT = hs.clone(), cT.clone()
+    replay = net.capture(xd)
+    hs2, cT2 = replay()
+    torch.cuda.synchronize()
+    assert torch.equal(hs, hs2) and torch.equal(cT, cT2)

@@ -389,3 +389,12 @@ def test_lstm_cell(ax):
     np.testing.assert_array_equal(c.cpu().numpy(), c_ref)
     np.testing.assert_array_equal(h.cpu().numpy(), h_ref)
     np.testing.assert_array_equal(q.cpu().numpy(), oracle.quantize(h_ref, s, 8))
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 1024), (37, 300, 129), (64, 512, 77), (1, 1000, 2048)])
+def test_gemm_small_m_column_split_tiles(ax, M, N, K):
+    """M <= 64 takes the column-split tile (warps over N), with and without split-K."""
+    A = datagen.random_int8(900 + M, (M, K))
+    W = datagen.random_int8(901 + N, (N, K))
+    T = datagen.lut_randerr(8, 4, 18)
+    np.testing.assert_array_equal(gpu_gemm(ax, A, W, T, 8), oracle.lut_gemm(A, W, T, 8))
