@@ -9,6 +9,9 @@ if ROOT not in sys.path:
 
 
 def pytest_configure(config):
+    # Build the native library (and the oracle's C) up front so a fresh checkout collects.
+    import __graft_entry__
+    __graft_entry__._build_lib()
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
