@@ -596,6 +596,7 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
     if (!wp || !d) return AXQ_ERR_INVALID;
     if (d->groups != 1 || (d->C & 3) || (reinterpret_cast<uintptr_t>(X) & 3)) return AXQ_ERR_UNSUPPORTED;
     const bool c4 = (d->C & 15) || !aligned16(X);
+    if (c4 && wp->Kp > axq::p4::TAP_BYTES) return AXQ_ERR_UNSUPPORTED;   // tap table capacity
     if (d->K != wp->N || d->R * d->S * d->C != wp->K) return AXQ_ERR_INVALID;
     axq::P4Args a{};
     int loader = 0;

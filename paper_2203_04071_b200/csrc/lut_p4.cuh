@@ -111,26 +111,6 @@ __device__ __forceinline__ void mma_s8_16816(int (&d)[4], uint32_t a0, uint32_t 
         : "r"(a0), "r"(a1), "r"(b0));
 }
 
-// Source address / valid bytes of the 16 activation bytes a[m][k0 .. k0+15].
-__device__ __forceinline__ const int8_t* p4_a_src(const P4Args& P, const RowInfo& ri, int64_t k0,
-                                                  uint32_t& bytes) {
-    const MMArgs& p = P.mm;
-    bytes = 0;
-    if (!ri.valid || k0 >= p.K) return p.A;
-    if (P.is_conv) {
-        const int rs = (int)(k0 / p.C);
-        const int c0 = (int)(k0 - (int64_t)rs * p.C);
-        const int r = rs / p.S, s = rs - r * p.S;
-        const int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
-        if (hi < 0 || hi >= p.H || wi < 0 || wi >= p.Wd) return p.A;   // padding tap: zeros
-        bytes = 16;
-        return p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c0;
-    }
-    const int64_t rem = p.K - k0;
-    bytes = rem >= 16 ? 16u : (uint32_t)rem;
-    return p.A + ri.base + k0;
-}
-
 template <int RPL, bool HALF>
 __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
     using namespace p4;
@@ -148,6 +128,19 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
     const uint32_t s_base = smem_u32(smem);
     const uint32_t bar0 = s_base + SMEM_BAR;
 
+    if (P.c4) {
+        // tap table of the 4-byte loader: entry g covers k = 4g .. 4g+3 (one tap, C % 4 == 0)
+        uint32_t* tap_w = reinterpret_cast<uint32_t*>(smem + G::SMEM_TAP);
+        const int ng = (int)(P.Kp / 4);
+        for (int g = tid; g < ng; g += NT) {
+            uint32_t e = ~0u;
+            if (4 * (int64_t)g < p.K) {
+                const int k = 4 * g, rs = k / p.C, c = k - rs * p.C, r = rs / p.S, s_ = rs - r * p.S;
+                e = (uint32_t)(r * p.dh) | ((uint32_t)(s_ * p.dw) << 8) | ((uint32_t)c << 16);
+            }
+            tap_w[g] = e;
+        }
+    }
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -172,45 +165,76 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
     };
 
     // ---- producer state: a flat per-CTA stream of (tile, stage) items, STAGES buffers ----
+    // Per row: the offset of its receptive-field origin (conv) or row start (GEMM), computed
+    // once per tile.  Per item: the filter tap (r, s) and channel c0 of k0, advanced
+    // incrementally (no divisions on the per-stage path).
     int64_t i_tile = blockIdx.x, i_nb = 0, i_m0 = 0;
     int i_st = 0, i_se = 0;
+    int t_r = 0, t_s = 0, t_c = 0;
     RowInfo irow[RPL];
+    int64_t roff[RPL];
     auto set_issue_tile = [&]() {
         if (i_tile >= n_work) return;
         decode(i_tile, i_nb, i_m0, i_st, i_se);
 #pragma unroll
-        for (int i = 0; i < RPL; ++i)
+        for (int i = 0; i < RPL; ++i) {
             irow[i] = P.is_conv ? make_row<LOAD_CONV>(p, i_m0 + tid + i * NT)
                                 : make_row<LOAD_GEMM>(p, i_m0 + tid + i * NT);
+            roff[i] = irow[i].base + (P.is_conv ? ((int64_t)irow[i].hb * p.Wd + irow[i].wb) * p.C : 0);
+        }
+        if (P.is_conv && !P.c4) {
+            const int k0 = i_st * KS, rs = k0 / p.C;
+            t_c = k0 - rs * p.C;
+            t_r = rs / p.S;
+            t_s = rs - t_r * p.S;
+        }
     };
+    const uint32_t* tap_s = reinterpret_cast<const uint32_t*>(smem + G::SMEM_TAP);
     uint32_t issued = 0;   // items issued by this CTA (buffer = index % STAGES)
     auto issue_next = [&]() {
         if (i_tile >= n_work) return;
         const int buf = (int)(issued % STAGES);
         const int64_t k0 = (int64_t)i_st * KS;
+        const uint32_t a_dst = s_base + SMEM_A + buf * A_STAGE + tid * KS;
         if (P.c4) {
-            // C % 4 == 0 (small C, e.g. the padded network input): 4 taps of 4 bytes per 16 k
+            // C % 4 == 0 (small C, e.g. the padded network input): 4 taps of 4 bytes per 16 k,
+            // tap geometry from the shared tap table (r*dh | s*dw << 8 | c << 16; ~0u past K)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int64_t k = k0 + 4 * j;
-                const int rs = (int)(k / p.C);
-                const int c = (int)(k - (int64_t)rs * p.C);
-                const int r = rs / p.S, s_ = rs - r * p.S;
+                const uint32_t tv = tap_s[i_st * 4 + j];
+                const int rdh = (int)(tv & 0xffu), sdw = (int)((tv >> 8) & 0xffu);
+                const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + (int)(tv >> 16);
 #pragma unroll
                 for (int i = 0; i < RPL; ++i) {
                     const RowInfo& ri = irow[i];
-                    const int hi = ri.hb + r * p.dh, wi = ri.wb + s_ * p.dw;
-                    const bool ok = ri.valid && k < p.K && hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd;
-                    const int8_t* src = ok ? p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c : p.A;
-                    cp_async4(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS + 4 * j, src, ok ? 4u : 0u);
+                    const bool ok = ri.valid && tv != ~0u && (unsigned)(ri.hb + rdh) < (unsigned)p.H &&
+                                    (unsigned)(ri.wb + sdw) < (unsigned)p.Wd;
+                    cp_async4(a_dst + i * NT * KS + 4 * j, ok ? p.A + roff[i] + toff : p.A, ok ? 4u : 0u);
                 }
             }
-        } else {
+        } else if (P.is_conv) {
+            // C % 16 == 0: the 16 k of the item lie inside one filter tap
+            const int rdh = t_r * p.dh, sdw = t_s * p.dw;
+            const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + t_c;
 #pragma unroll
             for (int i = 0; i < RPL; ++i) {
-                uint32_t nbytes;
-                const int8_t* src = p4_a_src(P, irow[i], k0, nbytes);
-                cp_async16(s_base + SMEM_A + buf * A_STAGE + (tid + i * NT) * KS, src, nbytes);
+                const RowInfo& ri = irow[i];
+                const bool ok = ri.valid && (unsigned)(ri.hb + rdh) < (unsigned)p.H &&
+                                (unsigned)(ri.wb + sdw) < (unsigned)p.Wd;
+                cp_async16(a_dst + i * NT * KS, ok ? p.A + roff[i] + toff : p.A, ok ? 16u : 0u);
+            }
+            t_c += KS;
+            if (t_c >= p.C) {
+                t_c = 0;
+                if (++t_s == p.S) { t_s = 0; ++t_r; }
+            }
+        } else {
+            const int64_t rem = p.K - k0;
+            const uint32_t nb = rem >= 16 ? 16u : (rem > 0 ? (uint32_t)rem : 0u);
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                const bool ok = irow[i].valid && nb > 0;
+                cp_async16(a_dst + i * NT * KS, ok ? p.A + roff[i] + k0 : p.A, ok ? nb : 0u);
             }
         }
         cp_async_commit();
@@ -413,6 +437,20 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) w |= (uint32_t)(uint8_t)epi_quant(v[j], s_out, qm) << (8 * j);
                         *reinterpret_cast<uint32_t*>(e.q + m * e.ldq + nn) = w;
+                    }
+                }
+            } else if (e.y_nchw) {
+                // NCHW fp32 output: lanes are consecutive pixels, so each column's stores are
+                // coalesced; the (image, pixel) split is computed once per row
+                const int64_t img = m / e.hw, pix = m - img * e.hw;
+                float* yb = e.y ? e.y + (img * p.N + n0) * e.hw + pix : nullptr;
+#pragma unroll
+                for (int n = 0; n < TN; ++n) {
+                    const int64_t nn = n0 + n;
+                    if (nn < p.N) {
+                        const float v = epi_value(eacc[r][n], m, nn, sc, e);
+                        if (yb) __stcs(yb + n * e.hw, v);
+                        if (e.q) e.q[m * e.ldq + nn] = epi_quant(v, s_out, qm);
                     }
                 }
             } else {

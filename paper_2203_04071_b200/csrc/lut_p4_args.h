@@ -16,6 +16,7 @@ constexpr int W_STAGE = TN * KS;           // 256 B weight tile per stage
 constexpr int SCR_WARP = 64 * TN * 4;      // per-warp int32 [64 rows][16 cols] scratch
 constexpr int FLUSH_STAGES = 16;           // 16-bit packed E sums: flush every 256 k
 constexpr int E_BIAS = 128;                // tables hold E + 128 (unsigned bytes)
+constexpr int TAP_BYTES = 2048;            // tap table of the 4-byte conv loader: Kp <= 2048
 
 // Table geometry: full range (ua = 0..255, any activation code) or half range (ua = 0..127,
 // non-negative activation codes, e.g. ReLU outputs): half the table bytes, one more stage.
@@ -30,7 +31,8 @@ struct Geo {
     static constexpr int SMEM_W = SMEM_A + STAGES * A_STAGE;
     static constexpr int SMEM_BAR = SMEM_W + STAGES * W_STAGE;
     static constexpr int SMEM_SCR = SMEM_BAR + 64;
-    static constexpr int SMEM_BYTES = SMEM_SCR + WARPS * SCR_WARP;
+    static constexpr int SMEM_TAP = SMEM_SCR + WARPS * SCR_WARP;   // 4-byte loader tap table
+    static constexpr int SMEM_BYTES = SMEM_TAP + TAP_BYTES;
 };
 }  // namespace p4
 
