@@ -202,6 +202,12 @@ axq_status axq_lut_gemm_wp(int64_t M, const int8_t* A, int64_t lda, axq_wpack_t 
                            const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream);
 axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_t wp,
                              const axq_epilogue* ep, int32_t* Y, void* stream);
+/* axq_wpack_kernel: selects the kernel behind axq_lut_gemm_wp / axq_lut_conv2d_wp for the
+ *   calling process (all results are bit-identical; this is a performance switch for
+ *   measurement): 0 = default (P4), 1 = P4 (exact part on mma.sync, 16 warps, 512- or
+ *   1024-row tiles), 2 = P4T (exact part on tcgen05.mma with TMEM accumulators, 32 warps,
+ *   1024-row tiles).  Returns the previous setting, or -1 for an unknown value (unchanged). */
+int axq_wpack_kernel(int variant);
 
 /* ---------------------------------------------------------------------------------
  * Dequantize (unfused), same pinned formula as the epilogue.

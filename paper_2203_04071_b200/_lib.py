@@ -27,7 +27,7 @@ EXPORTED = [
     "axq_dequantize", "axq_dequantize_nhwc_to_nchw", "axq_epilogue_apply",
     "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
     "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
-    "axq_lut_conv2d_wp",
+    "axq_lut_conv2d_wp", "axq_wpack_kernel",
 ]
 
 
@@ -93,6 +93,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_lstm_cell": ([i64, i64, vp, vp, vp, vp, vp, vp, i32, vp], i32),
         "axq_wpack_create": ([vp, vp, i64, i64, i64, i32, ctypes.POINTER(vp)], i32),
         "axq_wpack_destroy": ([vp], i32),
+        "axq_wpack_kernel": ([i32], i32),
         "axq_wpack_info": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "axq_lut_gemm_wp": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_lut_conv2d_wp": ([ctypes.POINTER(axq_conv_desc), vp, vp,
@@ -164,6 +165,14 @@ class Lut:
 
 def axq_lut_create(bits: int, host_table: np.ndarray) -> Lut:
     return Lut(bits, host_table)
+
+
+def axq_wpack_kernel(variant: int) -> int:
+    """Select the packed-table kernel (0 default = P4, 1 P4, 2 P4T); returns the previous."""
+    r = load().axq_wpack_kernel(int(variant))
+    if r < 0:
+        raise ValueError("unknown packed-table kernel variant %r" % variant)
+    return r
 
 
 def axq_lut_destroy(lut: Lut) -> None:

@@ -22,6 +22,21 @@ NVCC_FLAGS = [
 ]
 
 
+def _local_deps(src: Path, seen=None) -> set:
+    """The source and every repo header it includes, transitively (for incremental builds)."""
+    import re
+    seen = set() if seen is None else seen
+    if src in seen or not src.exists():
+        return seen
+    seen.add(src)
+    for inc in re.findall(r'#include\s+"([^"]+)"', src.read_text()):
+        for base in (src.parent, ROOT / "include"):
+            if (base / inc).exists():
+                _local_deps((base / inc).resolve(), seen)
+                break
+    return seen
+
+
 def stale() -> bool:
     if not LIB.exists():
         return True
@@ -40,6 +55,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def cc(src: Path) -> Path:
         obj = objdir / (src.stem + ".o")
+        if not force and obj.exists() and all(
+                d.stat().st_mtime <= obj.stat().st_mtime for d in _local_deps(src)):
+            return obj
         cmd = [NVCC, *comp, *(["-Xptxas", "-v"] if verbose else []), "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:

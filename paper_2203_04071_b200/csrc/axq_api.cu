@@ -536,6 +536,15 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
+static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4), 1 P4, 2 P4T
+
+int axq_wpack_kernel(int variant) {
+    if (variant < 0 || variant > 2) return -1;
+    const int prev = g_wpack_kernel;
+    g_wpack_kernel = variant;
+    return prev;
+}
+
 static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep, bool conv,
                          int32_t* C, int64_t ldc, cudaStream_t st) {
     int dev = 0;
@@ -559,7 +568,14 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     if (a.mm.M == 0) return AXQ_OK;
     // raw output may always split K (atomics into C); the fused epilogue needs a workspace
     const bool can_split = ep ? (ep->workspace != nullptr) : true;
-    axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
+    const bool use_p4t = g_wpack_kernel == 2;
+    if (use_p4t)
+        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.splits, a.stages_per_split);
+    else
+        axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
+    auto launch = [&](const axq::P4Args& x) { return use_p4t ? axq::launch_p4t(x, st) : axq::launch_p4(x, st); };
+    // column-block-fastest order when all of the layer's tables fit comfortably in L2
+    a.nb_fast = (wp->bytes <= ((int64_t)24 << 20)) ? 1 : 0;
     if (a.splits > 1) {
         int32_t* acc = ep ? ep->workspace : C;
         const int64_t ld = ep ? a.mm.N : ldc;
@@ -567,7 +583,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         if (e != cudaSuccess) return cuda_fail(e);
         a.mm.C_out = acc;
         a.mm.ldc = ld;
-        int rc = axq::launch_p4(a, st);
+        int rc = launch(a);
         if (rc) return cuda_fail((cudaError_t)rc);
         return ep ? launch_epilogue(a.mm.M, a.mm.N, acc, ld, epi, st) : AXQ_OK;
     }
@@ -578,7 +594,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         a.mm.C_out = C;
         a.mm.ldc = ldc;
     }
-    int rc = axq::launch_p4(a, st);
+    int rc = launch(a);
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }
 

@@ -111,8 +111,114 @@ __device__ __forceinline__ void mma_s8_16816(int (&d)[4], uint32_t a0, uint32_t 
         : "r"(a0), "r"(a1), "r"(b0));
 }
 
+// Per-tile output of one warp (rows mw .. mw + 32*RPL - 1, columns n0 .. n0+TN-1): the int32
+// totals wait in the warp's shared scratch.  Not inlined, so the register allocation of the
+// lookup loop does not depend on which epilogue features exist.
+template <int RPL>
+__device__ __noinline__ void p4_epilogue(const P4Args& P, const int* scr, int64_t mw, int64_t n0, int corr,
+                                         int splits, int lane) {
+    using namespace p4;
+    const MMArgs& p = P.mm;
+    auto sidx = [](int row, int col) { return row * TN + (col ^ (row & 15)); };
+    const EpiArgs& e = p.ep;
+    const bool raw = p.C_out != nullptr;
+    const bool vec = !raw && (n0 + TN <= p.N) && !e.y_nchw &&
+                     (!e.y || (((e.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.y) & 15) == 0))) &&
+                     (!e.residual || (((e.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.residual) & 15) == 0))) &&
+                     (!e.bias || ((reinterpret_cast<uintptr_t>(e.bias) & 15) == 0)) &&
+                     (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
+    const bool q16 = vec && e.q && ((e.ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 15) == 0);
+
+    // ---- output: atomic int32 (split K), raw int32, or the fused epilogue ----
+    const float sc = raw ? 0.f : __fmul_rn(*e.sa, *e.sw);
+    const float s_out = (!raw && e.q) ? *e.s_out : 1.f;
+    const float qm = (float)((1 << ((!raw && e.q ? e.bits_out : 8) - 1)) - 1);
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+        const int64_t m = mw + r * 32 + lane;
+        if (m >= p.M) continue;
+        int eacc[TN];
+#pragma unroll
+        for (int n = 0; n < TN; ++n) eacc[n] = scr[sidx(r * 32 + lane, n)] - corr;
+        if (raw) {
+            int32_t* c = p.C_out + m * p.ldc + n0;
+            if (splits > 1) {
+#pragma unroll
+                for (int n = 0; n < TN; ++n)
+                    if (n0 + n < p.N) atomicAdd(c + n, eacc[n]);
+            } else {
+#pragma unroll
+                for (int n = 0; n < TN; ++n)
+                    if (n0 + n < p.N) c[n] = eacc[n];
+            }
+            continue;
+        }
+        if (vec) {
+            // all of the row's residual loads first: one latency per row, not per 4 columns
+            float4 res[TN / 4];
+            if (e.residual) {
+                const float4* rp = reinterpret_cast<const float4*>(e.residual + m * e.ldr + n0);
+#pragma unroll
+                for (int j = 0; j < TN / 4; ++j) res[j] = __ldg(rp + j);
+            }
+            uint32_t qw[TN / 4];
+#pragma unroll
+            for (int n = 0; n < TN; n += 4) {
+                const int64_t nn = n0 + n;
+                float v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(eacc[n + j]), sc);
+                if (e.bias) {
+                    const float4 b = *reinterpret_cast<const float4*>(e.bias + nn);
+                    v[0] = __fadd_rn(v[0], b.x); v[1] = __fadd_rn(v[1], b.y);
+                    v[2] = __fadd_rn(v[2], b.z); v[3] = __fadd_rn(v[3], b.w);
+                }
+                if (e.residual) {
+                    const float4 rr = res[n / 4];
+                    v[0] = __fadd_rn(v[0], rr.x); v[1] = __fadd_rn(v[1], rr.y);
+                    v[2] = __fadd_rn(v[2], rr.z); v[3] = __fadd_rn(v[3], rr.w);
+                }
+                if (e.relu) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = v[j] > 0.f ? v[j] : 0.f;
+                }
+                if (e.y) *reinterpret_cast<float4*>(e.y + m * e.ldy + nn) = make_float4(v[0], v[1], v[2], v[3]);
+                if (e.q) {
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) w |= (uint32_t)(uint8_t)epi_quant(v[j], s_out, qm) << (8 * j);
+                    qw[n / 4] = w;
+                    if (!q16) *reinterpret_cast<uint32_t*>(e.q + m * e.ldq + nn) = w;
+                }
+            }
+            if (q16) *reinterpret_cast<uint4*>(e.q + m * e.ldq + n0) = make_uint4(qw[0], qw[1], qw[2], qw[3]);
+        } else if (e.y_nchw) {
+            // NCHW fp32 output: lanes are consecutive pixels, so each column's stores are
+            // coalesced; the (image, pixel) split is computed once per row
+            const int64_t img = m / e.hw, pix = m - img * e.hw;
+            float* yb = e.y ? e.y + (img * p.N + n0) * e.hw + pix : nullptr;
+#pragma unroll
+            for (int n = 0; n < TN; ++n) {
+                const int64_t nn = n0 + n;
+                if (nn < p.N) {
+                    const float v = epi_value(eacc[n], m, nn, sc, e);
+                    if (yb) __stcs(yb + n * e.hw, v);
+                    if (e.q) e.q[m * e.ldq + nn] = epi_quant(v, s_out, qm);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int n = 0; n < TN; ++n) {
+                const int64_t nn = n0 + n;
+                if (nn < p.N) epi_store(epi_value(eacc[n], m, nn, sc, e), m, nn, p.N, e, s_out, qm);
+            }
+        }
+    }
+    __syncwarp();
+}
+
 template <int RPL, bool HALF>
-__global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
+__global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const __grid_constant__ P4Args P) {
     using namespace p4;
     using G = Geo<HALF>;
     constexpr int STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ;
@@ -157,8 +263,14 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
     auto decode = [&](int64_t tile, int64_t& nb, int64_t& m0, int& s_b, int& s_e) {
         const int ks = (int)(tile % splits);
         const int64_t rest = tile / splits;
-        const int64_t mt = rest % m_tiles;
-        nb = rest / m_tiles;
+        int64_t mt;
+        if (P.nb_fast) {
+            nb = rest % n_blocks;
+            mt = rest / n_blocks;
+        } else {
+            mt = rest % m_tiles;
+            nb = rest / m_tiles;
+        }
         m0 = mt * BMR;
         s_b = ks * sps;
         s_e = min(nst_all, s_b + sps);
@@ -269,6 +381,17 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
         int s_b, s_e;
         decode(tile, nb, m0, s_b, s_e);
         const int64_t n0 = nb * TN;
+        if (p.C_out == nullptr && p.ep.residual && n0 + TN <= p.N) {
+            // the epilogue's residual rows (TN fp32 each): pull them into L2 while the
+            // lookups run, so the epilogue does not stall on HBM latency
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+                const int64_t m = m0 + warp * WROWS + r * 32 + lane;
+                if (m < p.M)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.ep.residual + m * p.ep.ldr + n0),
+                                 "r"(TN * 4) : "memory");
+            }
+        }
 
         uint32_t pacc[RPL][4][2];   // packed 16-bit E sums: [row][quad][even (c0,c2) / odd (c1,c3)]
 #pragma unroll
@@ -375,92 +498,7 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const P4Args P) {
                 scr[sidx(row + 8, col + 1)] = cacc[i][j][3];
             }
         __syncwarp();
-        int eacc[RPL][TN];
-#pragma unroll
-        for (int r = 0; r < RPL; ++r)
-#pragma unroll
-            for (int n = 0; n < TN; ++n) eacc[r][n] = scr[sidx(r * 32 + lane, n)] - corr;
-        __syncwarp();
-
-        // ---- output: atomic int32 (split K), raw int32, or the fused epilogue ----
-        const EpiArgs& e = p.ep;
-        const bool raw = p.C_out != nullptr;
-        const float sc = raw ? 0.f : __fmul_rn(*e.sa, *e.sw);
-        const float s_out = (!raw && e.q) ? *e.s_out : 1.f;
-        const float qm = (float)((1 << ((!raw && e.q ? e.bits_out : 8) - 1)) - 1);
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-            const int64_t m = m0 + warp * WROWS + r * 32 + lane;
-            if (m >= p.M) continue;
-            if (raw) {
-                int32_t* c = p.C_out + m * p.ldc + n0;
-                if (splits > 1) {
-#pragma unroll
-                    for (int n = 0; n < TN; ++n)
-                        if (n0 + n < p.N) atomicAdd(c + n, eacc[r][n]);
-                } else {
-#pragma unroll
-                    for (int n = 0; n < TN; ++n)
-                        if (n0 + n < p.N) c[n] = eacc[r][n];
-                }
-                continue;
-            }
-            const bool vec = (n0 + TN <= p.N) && !e.y_nchw &&
-                             (!e.y || (((e.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.y) & 15) == 0))) &&
-                             (!e.residual || (((e.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.residual) & 15) == 0))) &&
-                             (!e.bias || ((reinterpret_cast<uintptr_t>(e.bias) & 15) == 0)) &&
-                             (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
-            if (vec) {
-#pragma unroll
-                for (int n = 0; n < TN; n += 4) {
-                    const int64_t nn = n0 + n;
-                    float v[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(eacc[r][n + j]), sc);
-                    if (e.bias) {
-                        const float4 b = *reinterpret_cast<const float4*>(e.bias + nn);
-                        v[0] = __fadd_rn(v[0], b.x); v[1] = __fadd_rn(v[1], b.y);
-                        v[2] = __fadd_rn(v[2], b.z); v[3] = __fadd_rn(v[3], b.w);
-                    }
-                    if (e.residual) {
-                        const float4 rr = __ldg(reinterpret_cast<const float4*>(e.residual + m * e.ldr + nn));
-                        v[0] = __fadd_rn(v[0], rr.x); v[1] = __fadd_rn(v[1], rr.y);
-                        v[2] = __fadd_rn(v[2], rr.z); v[3] = __fadd_rn(v[3], rr.w);
-                    }
-                    if (e.relu) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) v[j] = v[j] > 0.f ? v[j] : 0.f;
-                    }
-                    if (e.y) *reinterpret_cast<float4*>(e.y + m * e.ldy + nn) = make_float4(v[0], v[1], v[2], v[3]);
-                    if (e.q) {
-                        uint32_t w = 0;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) w |= (uint32_t)(uint8_t)epi_quant(v[j], s_out, qm) << (8 * j);
-                        *reinterpret_cast<uint32_t*>(e.q + m * e.ldq + nn) = w;
-                    }
-                }
-            } else if (e.y_nchw) {
-                // NCHW fp32 output: lanes are consecutive pixels, so each column's stores are
-                // coalesced; the (image, pixel) split is computed once per row
-                const int64_t img = m / e.hw, pix = m - img * e.hw;
-                float* yb = e.y ? e.y + (img * p.N + n0) * e.hw + pix : nullptr;
-#pragma unroll
-                for (int n = 0; n < TN; ++n) {
-                    const int64_t nn = n0 + n;
-                    if (nn < p.N) {
-                        const float v = epi_value(eacc[r][n], m, nn, sc, e);
-                        if (yb) __stcs(yb + n * e.hw, v);
-                        if (e.q) e.q[m * e.ldq + nn] = epi_quant(v, s_out, qm);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int n = 0; n < TN; ++n) {
-                    const int64_t nn = n0 + n;
-                    if (nn < p.N) epi_store(epi_value(eacc[r][n], m, nn, sc, e), m, nn, p.N, e, s_out, qm);
-                }
-            }
-        }
+        p4_epilogue<RPL>(P, scr, m0 + warp * WROWS, n0, corr, splits, lane);
     }
 }
 

@@ -47,7 +47,10 @@ struct P4Args {
     int stages_per_split;       // 16-k stages per split
     int rpl;                    // rows per lane: 2 (1024-row tiles) or 1 (512-row tiles)
     int half;                   // tables cover ua = 0..127 only (non-negative activations)
-    int c4;                     // conv with C % 16 != 0 (C % 4 == 0): 4-byte tap copies               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)
+    int c4;                     // conv with C % 16 != 0 (C % 4 == 0): 4-byte tap copies
+    int nb_fast;                // tile order: column block fastest (the layer's tables stay in
+                                // L2 and each activation tile is read from HBM once) instead of
+                                // row tile fastest (concurrent CTAs share one table stream)               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)
 };
 
 }  // namespace axq

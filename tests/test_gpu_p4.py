@@ -11,11 +11,15 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.fixture(scope="module")
-def ax():
+@pytest.fixture(scope="module", params=[1, 2], ids=["p4", "p4t"])
+def ax(request):
+    """Every test runs on both packed-table kernels: P4 (mma.sync exact part) and P4T
+    (tcgen05.mma exact part, TMEM accumulators)."""
     from paper_2203_04071_b200 import _lib
     _lib.load()
-    return _lib
+    prev = _lib.axq_wpack_kernel(request.param)
+    yield _lib
+    _lib.axq_wpack_kernel(prev)
 
 
 def _t(a):
