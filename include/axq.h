@@ -123,7 +123,9 @@ axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_
  *                                    layer with bits_out, same rule as axq_quantize)
  * Zero-initialise the struct and set what is needed.  workspace: NULL, or device int32
  * scratch of M*N elements that lets the library split K across CTAs when M*N alone cannot
- * fill the GPU (results identical).  Layout of y: GEMM -> [M][ldy]; conv -> NCHW unless
+ * fill the GPU, or (packed-table P4T kernel) cut tiles at stream-K boundaries (results
+ * identical).  A workspace must be ZERO-FILLED when first passed; every call returns it
+ * zero-filled again, so one buffer can be reused across calls and layers.  Layout of y: GEMM -> [M][ldy]; conv -> NCHW unless
  * y_nhwc = 1 ([N*Ho*Wo][ldy]).  q_out is always [M][ldq] (conv: NHWC). */
 typedef struct axq_epilogue {
     const float* d_scale_a;   /* device fp32 scalar: activation scale (required) */
@@ -206,7 +208,9 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
  *   calling process (all results are bit-identical; this is a performance switch for
  *   measurement): 0 = default (P4), 1 = P4 (exact part on mma.sync, 16 warps, 512- or
  *   1024-row tiles), 2 = P4T (exact part on tcgen05.mma with TMEM accumulators, 32 warps,
- *   1024-row tiles).  Returns the previous setting, or -1 for an unknown value (unchanged). */
+ *   1024-row tiles), 3 = P4W (P4T warp-specialised: 4 producer warps stream the operands,
+ *   28 consumer warps look up, 896-row tiles).  Returns the previous setting, or -1 for an
+ *   unknown value (unchanged). */
 int axq_wpack_kernel(int variant);
 
 /* ---------------------------------------------------------------------------------

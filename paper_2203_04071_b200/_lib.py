@@ -104,6 +104,10 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         f.argtypes = args
         f.restype = res
     _lib = L
+    v = os.environ.get("AXQ_WPACK_KERNEL")   # measurement switch (include/axq.h axq_wpack_kernel)
+    if v:
+        if L.axq_wpack_kernel(int(v)) < 0:
+            raise ValueError("AXQ_WPACK_KERNEL=%s: unknown packed-table kernel" % v)
     return L
 
 

@@ -45,6 +45,20 @@ inline axq_status cuda_fail(cudaError_t e) {
     return AXQ_ERR_CUDA;
 }
 
+// Stream-K tile counters of the P4T kernel, one zero-filled block per device (the kernel leaves
+// them zero).  Allocated by axq_wpack_create, so no hot call allocates.
+static int32_t* g_sk_cnt[64];
+static int32_t* streamk_counters(int dev) { return (dev >= 0 && dev < 64) ? g_sk_cnt[dev] : nullptr; }
+static cudaError_t ensure_streamk_counters(int dev) {
+    if (dev < 0 || dev >= 64 || g_sk_cnt[dev]) return cudaSuccess;
+    int32_t* c = nullptr;
+    cudaError_t e = cudaMalloc(&c, 4096 * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemset(c, 0, 4096 * sizeof(int32_t));
+    if (e == cudaSuccess) g_sk_cnt[dev] = c;
+    return e;
+}
+
+
 inline axq_status check_launch() {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);
@@ -335,8 +349,8 @@ static axq::EpiArgs to_epi(const axq_epilogue* ep, bool nchw, int64_t hw) {
 }
 
 static axq_status launch_epilogue(int64_t M, int64_t N, const int32_t* acc, int64_t ldacc,
-                                  const axq::EpiArgs& e, cudaStream_t st) {
-    axq::epilogue_kernel<<<stream_grid(M * N, 256 * 4), 256, 0, st>>>(M, N, acc, ldacc, e);
+                                  const axq::EpiArgs& e, cudaStream_t st, int32_t* zero_acc = nullptr) {
+    axq::epilogue_kernel<<<stream_grid(M * N, 256 * 4), 256, 0, st>>>(M, N, acc, ldacc, e, zero_acc);
     return check_launch();
 }
 
@@ -366,7 +380,7 @@ static axq_status run_mm(axq::MMArgs& p, int loader, axq_lut_t lut, const axq::E
         if (e != cudaSuccess) return cuda_fail(e);
         axq_status s = launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, st);
         if (s != AXQ_OK) return s;
-        return launch_epilogue(p.M, p.N, workspace, p.N, *epi, st);
+        return launch_epilogue(p.M, p.N, workspace, p.N, *epi, st, workspace);
     }
     p.ep = *epi;
     return launch_mm(axq::EPI_FUSED, loader, lut->repr, p, c, grid, st);
@@ -494,10 +508,14 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
     if (s != AXQ_OK) return s;
     axq_wpack* w = new axq_wpack();
     cudaGetDevice(&w->device);
+    if (ensure_streamk_counters(w->device) != cudaSuccess) {
+        delete w;
+        return cuda_fail(cudaGetLastError());
+    }
     w->t00 = lut->t00;
     w->N = N;
     w->K = K;
-    w->Kp = (K + 15) / 16 * 16;
+    w->Kp = (K + 31) / 32 * 32;   // a whole number of 32-k stages (P4T half-range tables)
     w->half = a_nonneg ? 1 : 0;
     const int64_t nb = (N + axq::p4::TN - 1) / axq::p4::TN;
     const size_t tb = (size_t)nb * w->Kp * 4 * (w->half ? 128 : 256) * 4, wb = (size_t)nb * w->Kp * axq::p4::TN;
@@ -536,10 +554,10 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
-static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4), 1 P4, 2 P4T
+static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4), 1 P4, 2 P4T, 3 P4W
 
 int axq_wpack_kernel(int variant) {
-    if (variant < 0 || variant > 2) return -1;
+    if (variant < 0 || variant > 3) return -1;
     const int prev = g_wpack_kernel;
     g_wpack_kernel = variant;
     return prev;
@@ -568,12 +586,29 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     if (a.mm.M == 0) return AXQ_OK;
     // raw output may always split K (atomics into C); the fused epilogue needs a workspace
     const bool can_split = ep ? (ep->workspace != nullptr) : true;
-    const bool use_p4t = g_wpack_kernel == 2;
-    if (use_p4t)
-        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.splits, a.stages_per_split);
+    const int variant = g_wpack_kernel == 0 ? 1 : g_wpack_kernel;   // default: P4
+    const bool use_tc = variant >= 2;                                 // P4T / P4W: tcgen05 exact part
+    const int bm = variant == 3 ? 896 : 1024;
+    if (use_tc)
+        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, wp->half, bm, sm_count(), can_split, a.splits, a.stages_per_split);
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
-    auto launch = [&](const axq::P4Args& x) { return use_p4t ? axq::launch_p4t(x, st) : axq::launch_p4(x, st); };
+    auto launch = [&](const axq::P4Args& x) {
+        return variant == 3 ? axq::launch_p4w(x, st) : variant == 2 ? axq::launch_p4t(x, st) : axq::launch_p4(x, st);
+    };
+    if (use_tc && ep && ep->workspace) {
+        // stream-K whenever whole tiles would leave a partial wave (exact int32 pieces in the
+        // zero-filled workspace; finished by the kernel itself, no extra launch)
+        const int64_t tiles = ((a.mm.M + bm - 1) / bm) * ((a.mm.N + axq::p4::TN - 1) / axq::p4::TN);
+        int32_t* cnt = streamk_counters(dev);
+        if (cnt && tiles % sm_count() != 0) {
+            a.streamk = 1;
+            a.splits = 1;
+            a.stages_per_split = 0;
+            a.ws = ep->workspace;
+            a.cnt = cnt;
+        }
+    }
     // column-block-fastest order when all of the layer's tables fit comfortably in L2
     a.nb_fast = (wp->bytes <= ((int64_t)24 << 20)) ? 1 : 0;
     if (a.splits > 1) {
@@ -585,7 +620,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         a.mm.ldc = ld;
         int rc = launch(a);
         if (rc) return cuda_fail((cudaError_t)rc);
-        return ep ? launch_epilogue(a.mm.M, a.mm.N, acc, ld, epi, st) : AXQ_OK;
+        return ep ? launch_epilogue(a.mm.M, a.mm.N, acc, ld, epi, st, acc) : AXQ_OK;
     }
     if (ep) {
         a.mm.ep = epi;

@@ -56,8 +56,10 @@ __device__ __forceinline__ void epi_store(float v, int64_t m, int64_t n, int64_t
 }
 
 // Stand-alone epilogue over an int32 [M][N] accumulator (split-K path).
+// zero_acc: the workspace-accumulator form re-zeroes what it read, so a workspace is left
+// zero-filled for the stream-K kernel (lut_p4t.cuh), which relies on that.
 static __global__ void epilogue_kernel(int64_t M, int64_t N, const int32_t* __restrict__ acc,
-                                int64_t ldacc, const EpiArgs e) {
+                                int64_t ldacc, const EpiArgs e, int32_t* zero_acc = nullptr) {
     const float sc = __fmul_rn(*e.sa, *e.sw);
     const float s_out = e.q ? *e.s_out : 1.f;
     const float qm = (float)((1 << (e.bits_out > 0 ? e.bits_out - 1 : 7)) - 1);
@@ -66,6 +68,7 @@ static __global__ void epilogue_kernel(int64_t M, int64_t N, const int32_t* __re
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
         const int64_t m = i / N, n = i - m * N;
         epi_store(epi_value(acc[m * ldacc + n], m, n, sc, e), m, n, N, e, s_out, qm);
+        if (zero_acc) zero_acc[m * ldacc + n] = 0;
     }
 }
 

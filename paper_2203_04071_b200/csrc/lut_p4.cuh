@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const __grid_constant
 #pragma unroll
             for (int i = 0; i < RPL; ++i) {
                 const RowInfo& ri = irow[i];
-                const bool ok = ri.valid && (unsigned)(ri.hb + rdh) < (unsigned)p.H &&
+                const bool ok = ri.valid && k0 < p.K && (unsigned)(ri.hb + rdh) < (unsigned)p.H &&
                                 (unsigned)(ri.wb + sdw) < (unsigned)p.Wd;
                 cp_async16(a_dst + i * NT * KS, ok ? p.A + roff[i] + toff : p.A, ok ? 16u : 0u);
             }

@@ -48,6 +48,9 @@ struct P4Args {
     int rpl;                    // rows per lane: 2 (1024-row tiles) or 1 (512-row tiles)
     int half;                   // tables cover ua = 0..127 only (non-negative activations)
     int c4;                     // conv with C % 16 != 0 (C % 4 == 0): 4-byte tap copies
+    int streamk;                // P4T: stream-K decomposition (needs ws and cnt)
+    int32_t* ws;                // stream-K workspace int32 [M][N], zero on entry, left zero
+    int32_t* cnt;               // stream-K tile counters (>= gridDim.x), zero on entry, left zero
     int nb_fast;                // tile order: column block fastest (the layer's tables stay in
                                 // L2 and each activation tile is read from HBM once) instead of
                                 // row tile fastest (concurrent CTAs share one table stream)               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)

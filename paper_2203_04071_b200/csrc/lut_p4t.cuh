@@ -32,19 +32,19 @@ namespace p4t {
 constexpr int WARPS = 32;
 constexpr int NT = WARPS * 32;             // 1024 threads
 constexpr int BM = NT;                     // 1024 rows per CTA tile, one per lane
-constexpr int KS = p4::KS;                 // 16 k per stage
 constexpr int TN = p4::TN;                 // 16 columns
-constexpr int A_STAGE = BM * KS;           // 16 KiB
-constexpr int W_STAGE = 512;               // [16 n][16 k] weights + 256 zero bytes (K chunk 2)
+constexpr int W_STAGE = 512;               // [2 K chunks][16 n][16 k] (KS = 16: chunk 2 zero)
 constexpr int TMEM_COLS = 256;             // [0,128): exact part, [128,256): E sums
-constexpr int FLUSH_STAGES = p4::FLUSH_STAGES;
 
-template <bool HALF>
+// KS = k per stage: 32 for half-range tables (64 KiB per stage), 16 for full-range ones.
+template <bool HALF, int KS>
 struct Geo {
     static constexpr int TROWS = HALF ? 128 : 256;
     static constexpr int TQ = TROWS * 4;
-    static constexpr int TBL_STAGE = KS * (TN / 4) * TQ;   // 32 / 64 KiB
-    static constexpr int STAGES = HALF ? 4 : 2;
+    static constexpr int TBL_STAGE = KS * (TN / 4) * TQ;   // 64 KiB (32 KiB for HALF, KS 16)
+    static constexpr int A_STAGE = BM * KS;                // KS / 16 planes of [BM][16 B]
+    static constexpr int STAGES = (HALF && KS == 16) ? 4 : 2;
+    static constexpr int FLUSH_STAGES = 256 / KS;          // 16-bit packed sums: every 256 k
     static constexpr int SMEM_TBL = 0;
     static constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
     static constexpr int SMEM_W = SMEM_A + STAGES * A_STAGE;
@@ -52,6 +52,8 @@ struct Geo {
     static constexpr int SMEM_TAP = SMEM_BAR + 8 * (2 * STAGES + 2);
     static constexpr int SMEM_BYTES = SMEM_TAP + p4::TAP_BYTES;
 };
+template <bool HALF>
+__host__ __device__ constexpr int ks_of() { return HALF ? 32 : 16; }
 }  // namespace p4t
 
 // ---- tcgen05 helpers ----
@@ -190,8 +192,10 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
 template <bool HALF>
 __global__ void __launch_bounds__(p4t::NT, 1) lut_p4t_kernel(const __grid_constant__ P4Args P) {
     using namespace p4t;
-    using G = p4t::Geo<HALF>;
-    constexpr int STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ;
+    constexpr int KS = ks_of<HALF>();
+    using G = p4t::Geo<HALF, KS>;
+    constexpr int STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ, A_STAGE = G::A_STAGE;
+    constexpr int NPL = KS / 16;               // activation planes per stage
     constexpr int SMEM_TBL = G::SMEM_TBL, SMEM_A = G::SMEM_A, SMEM_W = G::SMEM_W;
     extern __shared__ __align__(1024) uint8_t p4t_smem[];
     uint8_t* smem = p4t_smem;
@@ -215,9 +219,10 @@ __global__ void __launch_bounds__(p4t::NT, 1) lut_p4t_kernel(const __grid_consta
             tap_w[g] = e;
         }
     }
-    // zero K chunk 2 of every weight buffer (read by the MMA through the async proxy)
-    for (int i = tid; i < STAGES * 64; i += NT)
-        reinterpret_cast<uint32_t*>(smem + SMEM_W + (i >> 6) * W_STAGE + 256)[i & 63] = 0u;
+    // KS = 16: zero K chunk 2 of every weight buffer (read by the MMA through the async proxy)
+    if (KS == 16)
+        for (int i = tid; i < STAGES * 64; i += NT)
+            reinterpret_cast<uint32_t*>(smem + SMEM_W + (i >> 6) * W_STAGE + 256)[i & 63] = 0u;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     if (tid == 0) {
         for (int s = 0; s < 2 * STAGES + 1; ++s) mbar_init(bar_full + 8 * s, 1);
@@ -245,32 +250,66 @@ __global__ void __launch_bounds__(p4t::NT, 1) lut_p4t_kernel(const __grid_consta
     const int64_t n_work = m_tiles * n_blocks * splits;
     const int nst_all = (int)(P.Kp / KS);
     const int sps = P.stages_per_split > 0 ? P.stages_per_split : nst_all;
+    // Stream-K (fused epilogue with a workspace), data-parallel + stream-K hybrid: the whole
+    // waves of tiles run round-robin (concurrent CTAs share one table stream); the T % grid
+    // tail tiles' (tile, stage) iterations are cut into gridDim.x equal contiguous ranges.  A
+    // tail tile cut by a range boundary is summed exactly in the int32 workspace and finished
+    // by whichever contributor completes its stage count.
+    const bool sk = P.streamk != 0;
+    const int64_t G_ = gridDim.x;
+    const int64_t t_all = m_tiles * n_blocks;
+    const int64_t t_dp = sk ? (t_all / G_) * G_ : 0;
+    const int64_t it_sk = (t_all - t_dp) * (int64_t)nst_all;
+    auto sk_begin = [&](int64_t c) { return t_dp * nst_all + (c * it_sk) / G_; };
 
-    auto decode = [&](int64_t tile, int64_t& nb, int64_t& m0, int& s_b, int& s_e) {
-        const int ks = (int)(tile % splits);
-        const int64_t rest = tile / splits;
-        int64_t mt;
-        if (P.nb_fast) {
-            nb = rest % n_blocks;
-            mt = rest / n_blocks;
-        } else {
-            mt = rest % m_tiles;
-            nb = rest / m_tiles;
+    // segments: (tile, stage range) in this CTA's order; cur < 0 encodes the round-robin phase
+    struct Gen { int64_t cur, end; bool dp; };
+    auto gen_init = [&](Gen& g) {
+        if (sk) { g.dp = t_dp > 0; g.cur = blockIdx.x; g.end = t_dp; if (!g.dp) { g.cur = sk_begin(blockIdx.x); g.end = sk_begin(blockIdx.x + 1); } }
+        else { g.dp = true; g.cur = blockIdx.x; g.end = n_work; }
+    };
+    auto gen_next = [&](Gen& g, int64_t& t, int& s_b, int& s_e) -> bool {
+        if (g.dp) {
+            if (g.cur < g.end) {
+                const int ks = (int)(g.cur % splits);
+                t = g.cur / splits;
+                s_b = ks * sps;
+                s_e = min(nst_all, s_b + sps);
+                g.cur += G_;
+                return true;
+            }
+            if (!sk) return false;
+            g.dp = false;
+            g.cur = sk_begin(blockIdx.x);
+            g.end = sk_begin(blockIdx.x + 1);
         }
+        if (g.cur >= g.end) return false;
+        t = g.cur / nst_all;
+        s_b = (int)(g.cur - t * nst_all);
+        const int64_t rem = s_b + (g.end - g.cur);
+        s_e = (int)(rem < (int64_t)nst_all ? rem : (int64_t)nst_all);
+        g.cur += s_e - s_b;
+        return true;
+    };
+    auto tile_mn = [&](int64_t t, int64_t& nb, int64_t& m0) {
+        int64_t mt;
+        if (P.nb_fast) { nb = t % n_blocks; mt = t / n_blocks; }
+        else { mt = t % m_tiles; nb = t / m_tiles; }
         m0 = mt * BM;
-        s_b = ks * sps;
-        s_e = min(nst_all, s_b + sps);
     };
 
     // ---- producer: a flat per-CTA stream of (tile, stage) items over STAGES buffers ----
-    int64_t i_tile = blockIdx.x, i_nb = 0, i_m0 = 0;
+    Gen pg;
+    gen_init(pg);
+    int64_t i_t = 0, i_nb = 0, i_m0 = 0;
     int i_st = 0, i_se = 0;
+    bool i_done = false;
     int t_r = 0, t_s = 0, t_c = 0;
     RowInfo irow;
     int64_t roff = 0;
     auto set_issue_tile = [&]() {
-        if (i_tile >= n_work) return;
-        decode(i_tile, i_nb, i_m0, i_st, i_se);
+        if (!gen_next(pg, i_t, i_st, i_se)) { i_done = true; return; }
+        tile_mn(i_t, i_nb, i_m0);
         irow = P.is_conv ? make_row<LOAD_CONV>(p, i_m0 + tid) : make_row<LOAD_GEMM>(p, i_m0 + tid);
         roff = irow.base + (P.is_conv ? ((int64_t)irow.hb * p.Wd + irow.wb) * p.C : 0);
         if (P.is_conv && !P.c4) {
@@ -283,66 +322,70 @@ __global__ void __launch_bounds__(p4t::NT, 1) lut_p4t_kernel(const __grid_consta
     const uint32_t* tap_s = reinterpret_cast<const uint32_t*>(smem + G::SMEM_TAP);
     uint32_t issued = 0;
     auto issue_next = [&]() {
-        if (i_tile >= n_work) return;
+        if (i_done) return;
         const int buf = (int)(issued % STAGES);
         if (issued >= (uint32_t)STAGES)   // the MMA of this buffer's previous item must be done
             mbar_wait(bar_mma + 8 * buf, ((issued / STAGES) - 1) & 1u);
-        const int64_t k0 = (int64_t)i_st * KS;
-        const uint32_t a_dst = s_base + SMEM_A + buf * A_STAGE + tid * KS;
-        if (P.c4) {
+        const uint32_t a_dst = s_base + SMEM_A + buf * A_STAGE + tid * 16;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t tv = tap_s[i_st * 4 + j];
-                const int rdh = (int)(tv & 0xffu), sdw = (int)((tv >> 8) & 0xffu);
-                const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + (int)(tv >> 16);
-                const bool ok = irow.valid && tv != ~0u && (unsigned)(irow.hb + rdh) < (unsigned)p.H &&
+        for (int pl = 0; pl < NPL; ++pl) {
+            const int64_t k0 = (int64_t)i_st * KS + 16 * pl;
+            const uint32_t dst = a_dst + pl * (BM * 16);
+            if (P.c4) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t tv = tap_s[(int)(k0 >> 2) + j];
+                    const int rdh = (int)(tv & 0xffu), sdw = (int)((tv >> 8) & 0xffu);
+                    const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + (int)(tv >> 16);
+                    const bool ok = irow.valid && tv != ~0u && (unsigned)(irow.hb + rdh) < (unsigned)p.H &&
+                                    (unsigned)(irow.wb + sdw) < (unsigned)p.Wd;
+                    cp_async4(dst + 4 * j, ok ? p.A + roff + toff : p.A, ok ? 4u : 0u);
+                }
+            } else if (P.is_conv) {
+                const int rdh = t_r * p.dh, sdw = t_s * p.dw;
+                const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + t_c;
+                const bool ok = irow.valid && k0 < p.K && (unsigned)(irow.hb + rdh) < (unsigned)p.H &&
                                 (unsigned)(irow.wb + sdw) < (unsigned)p.Wd;
-                cp_async4(a_dst + 4 * j, ok ? p.A + roff + toff : p.A, ok ? 4u : 0u);
+                cp_async16(dst, ok ? p.A + roff + toff : p.A, ok ? 16u : 0u);
+                t_c += 16;
+                if (t_c >= p.C) {
+                    t_c = 0;
+                    if (++t_s == p.S) { t_s = 0; ++t_r; }
+                }
+            } else {
+                const int64_t rem = p.K - k0;
+                const uint32_t nb = rem >= 16 ? 16u : (rem > 0 ? (uint32_t)rem : 0u);
+                const bool ok = irow.valid && nb > 0;
+                cp_async16(dst, ok ? p.A + roff + k0 : p.A, ok ? nb : 0u);
             }
-        } else if (P.is_conv) {
-            const int rdh = t_r * p.dh, sdw = t_s * p.dw;
-            const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + t_c;
-            const bool ok = irow.valid && (unsigned)(irow.hb + rdh) < (unsigned)p.H &&
-                            (unsigned)(irow.wb + sdw) < (unsigned)p.Wd;
-            cp_async16(a_dst, ok ? p.A + roff + toff : p.A, ok ? 16u : 0u);
-            t_c += KS;
-            if (t_c >= p.C) {
-                t_c = 0;
-                if (++t_s == p.S) { t_s = 0; ++t_r; }
-            }
-        } else {
-            const int64_t rem = p.K - k0;
-            const uint32_t nb = rem >= 16 ? 16u : (rem > 0 ? (uint32_t)rem : 0u);
-            const bool ok = irow.valid && nb > 0;
-            cp_async16(a_dst, ok ? p.A + roff + k0 : p.A, ok ? nb : 0u);
         }
         cp_async_commit();
         if (tid == 0) {
             const uint32_t bar = bar_full + 8 * buf;
             const uint32_t* tbl_g = P.tables + ((size_t)i_nb * P.Kp + (size_t)i_st * KS) * 4 * G::TROWS;
-            const int8_t* w_g = P.wpk + ((size_t)i_nb * (P.Kp / KS) + i_st) * p4::W_STAGE;
-            mbar_expect_tx(bar, TBL_STAGE + p4::W_STAGE);
+            const int8_t* w_g = P.wpk + ((size_t)i_nb * (P.Kp / 16) + (size_t)i_st * NPL) * p4::W_STAGE;
+            mbar_expect_tx(bar, TBL_STAGE + NPL * p4::W_STAGE);
             bulk_g2s(s_base + SMEM_TBL + buf * TBL_STAGE, tbl_g, TBL_STAGE, bar);
-            bulk_g2s(s_base + SMEM_W + buf * W_STAGE, w_g, p4::W_STAGE, bar);
+            bulk_g2s(s_base + SMEM_W + buf * W_STAGE, w_g, NPL * p4::W_STAGE, bar);
         }
         ++issued;
-        if (++i_st >= i_se) {
-            i_tile += gridDim.x;
-            set_issue_tile();
-        }
+        if (++i_st >= i_se) set_issue_tile();
     };
     set_issue_tile();
 #pragma unroll
     for (int i = 0; i < STAGES; ++i) issue_next();
 
-    const uint32_t one = P.one;
     uint32_t consumed = 0, tiles_done = 0;
-
-    for (int64_t tile = blockIdx.x; tile < n_work; tile += gridDim.x) {
+    int* fin_flag = reinterpret_cast<int*>(smem + G::SMEM_BAR + 8 * (2 * STAGES + 1) + 4);
+    Gen cg;
+    int64_t tile;
+    int s_b, s_e;
+    gen_init(cg);
+    while (gen_next(cg, tile, s_b, s_e)) {
         int64_t nb, m0;
-        int s_b, s_e;
-        decode(tile, nb, m0, s_b, s_e);
+        tile_mn(tile, nb, m0);
         const int64_t n0 = nb * TN;
+        const bool wlive = m0 + warp * 32 < p.M;   // rows past M: no lookups (ragged last tile)
         if (p.C_out == nullptr && p.ep.residual && n0 + TN <= p.N && m0 + tid < p.M)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.ep.residual + (m0 + tid) * p.ep.ldr + n0),
                          "r"(TN * 4)
@@ -393,7 +436,8 @@ __global__ void __launch_bounds__(p4t::NT, 1) lut_p4t_kernel(const __grid_consta
                 const uint64_t bdesc = umma_desc_kmajor(s_base + SMEM_W + buf * W_STAGE, 256u, 128u);
 #pragma unroll
                 for (int j = 0; j < BM / 128; ++j)
-                    umma_i8(tmem + (uint32_t)j * TN, umma_desc_kmajor(a0 + j * 128 * KS, 0u, 128u), bdesc, IDESC,
+                    umma_i8(tmem + (uint32_t)j * TN,
+                            umma_desc_kmajor(a0 + j * 128 * 16, KS == 32 ? (uint32_t)(BM * 16) : 0u, 128u), bdesc, IDESC,
                             st == s_b ? 0u : 1u);
                 umma_commit(bar_mma + 8 * buf);
                 if (st + 1 == s_e) umma_commit(bar_tile);
@@ -402,23 +446,29 @@ __global__ void __launch_bounds__(p4t::NT, 1) lut_p4t_kernel(const __grid_consta
             const uint8_t* tb = smem + SMEM_TBL + buf * TBL_STAGE;
             const uint8_t* at = smem + SMEM_A + buf * A_STAGE;
 
-            // ---- E lookups: 4 per 32-bit shared load, packed 16-bit accumulation ----
-            const uint4 av = *reinterpret_cast<const uint4*>(at + tid * KS);
-            const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+            // ---- E lookups: 4 per 32-bit shared load, packed 16-bit accumulation; the loads
+            //      of two consecutive k are summed by one 3-input add per accumulator ----
 #pragma unroll
-            for (int kk = 0; kk < KS; ++kk) {
-                const uint32_t ua = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
-                const uint8_t* row_t = tb + kk * 4 * TQ + ua * 4u;
+            for (int pl = 0; pl < NPL; ++pl) {
+                if (!wlive) break;
+                const uint4 av = *reinterpret_cast<const uint4*>(at + pl * (BM * 16) + tid * 16);
+                const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t v = *reinterpret_cast<const uint32_t*>(row_t + q * TQ);
-                    const uint32_t ev = __byte_perm(v, 0u, 0x4240u);   // [b0, 0, b2, 0]
-                    const uint32_t od = __byte_perm(v, 0u, 0x4341u);   // [b1, 0, b3, 0]
-                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(ev), "r"(one));
-                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(od), "r"(one));
+                for (int kk = 0; kk < 16; kk += 2) {
+                    const uint32_t ua0 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
+                    const uint32_t ua1 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + ((kk + 1) & 3));
+                    const uint8_t* r0 = tb + (pl * 16 + kk) * 4 * TQ + ua0 * 4u;
+                    const uint8_t* r1 = tb + (pl * 16 + kk + 1) * 4 * TQ + ua1 * 4u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t v0 = *reinterpret_cast<const uint32_t*>(r0 + q * TQ);
+                        const uint32_t v1 = *reinterpret_cast<const uint32_t*>(r1 + q * TQ);
+                        pacc[q][0] += __byte_perm(v0, 0u, 0x4240u) + __byte_perm(v1, 0u, 0x4240u);
+                        pacc[q][1] += __byte_perm(v0, 0u, 0x4341u) + __byte_perm(v1, 0u, 0x4341u);
+                    }
                 }
             }
-            if ((st - s_b + 1) % FLUSH_STAGES == 0 || st + 1 == s_e) flush();
+            if ((st - s_b + 1) % G::FLUSH_STAGES == 0 || st + 1 == s_e) flush();
         }
         int corr = p4::E_BIAS * KS * (s_e - s_b);
         if (s_e == nst_all) corr += (int)(((P.Kp - p.K) + p.pad_lookups) * (int64_t)p.t00);
@@ -435,7 +485,41 @@ __global__ void __launch_bounds__(p4t::NT, 1) lut_p4t_kernel(const __grid_consta
 #pragma unroll
         for (int n = 0; n < 16; ++n) eacc[n] = (int)(ex[n] + es[n]) - corr;
         const int64_t m = m0 + tid;
-        if (m < p.M) p4t_store_row(P, m, n0, eacc, splits);
+        if (sk && !(s_b == 0 && s_e == nst_all)) {
+            // a stream-K piece: add it to the workspace; the contributor that completes the
+            // tile's stage count reads the exact total back (and re-zeroes the workspace)
+            int* wrow = P.ws + m * p.N + n0;
+            if (m < p.M) {
+#pragma unroll
+                for (int n = 0; n < TN; ++n)
+                    if (n0 + n < p.N) atomicAdd(wrow + n, eacc[n]);
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                const int64_t x = (tile - t_dp) * nst_all;   // the tile's first tail iteration
+                int64_t c = (x * G_) / it_sk;
+                while (c + 1 < G_ && sk_begin(c + 1) - t_dp * nst_all <= x) ++c;
+                const int old = atomicAdd(P.cnt + c, s_e - s_b);
+                const int fin = (old + (s_e - s_b) == nst_all) ? 1 : 0;
+                if (fin) P.cnt[c] = 0;
+                *fin_flag = fin;
+            }
+            __syncthreads();
+            if (*fin_flag) {
+                __threadfence();
+                if (m < p.M) {
+#pragma unroll
+                    for (int n = 0; n < TN; ++n) {
+                        eacc[n] = (n0 + n < p.N) ? __ldcg(wrow + n) : 0;
+                        if (n0 + n < p.N) wrow[n] = 0;
+                    }
+                    p4t_store_row(P, m, n0, eacc, 1);
+                }
+            }
+        } else if (m < p.M) {
+            p4t_store_row(P, m, n0, eacc, splits);
+        }
     }
     tc_fence_before();
     __syncthreads();

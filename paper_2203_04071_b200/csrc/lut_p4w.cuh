@@ -1,0 +1,430 @@
+// lut_p4w.cuh -- "P4W": warp-specialised packed-table LUT-GEMM / implicit-im2col LUT-conv
+// (sm_100a).  Same result as lut_p4.cuh / lut_p4t.cuh: acc[m][n] = sum_k LUT[a[m][k]][w[n][k]]
+// in int32, exact, as  sum_k a*w (tcgen05.mma kind::i8, TMEM)  +  sum_k E[a][w] (packed tables).
+//
+// Roles inside one persistent CTA (1024 threads, one CTA per SM):
+//  * 4 producer warps (warps 28..31) stream the operands of each (tile, stage) item into a
+//    ring of STAGES shared-memory buffers: the activation rows by cp.async (implicit im2col,
+//    zero-fill = padding taps), completion signalled with cp.async.mbarrier.arrive; the packed
+//    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
+//    the consumer warps released it (empty barrier) and the MMA that read it completed.
+//  * 28 consumer warps (896 rows, one per lane) only wait for full buffers, do the lookups
+//    (4 per 32-bit LDS, two k summed per 3-input add) and release the buffer; consumer warp
+//    0's lane 0 also issues the exact-part MMAs (7 slices of 128 rows, M = 128, N = 16, K = 32)
+//    into one of two TMEM accumulator sets, so the next tile's MMAs never wait for this
+//    tile's epilogue reads.  No CTA-wide barrier in the steady state.
+//  * Row 32*w + lane of a tile is TMEM lane 32*(w % 4) + lane of MMA slice w / 4, so every
+//    consumer warp reads exactly the TMEM lane quarter it may access.
+//  * Tile order, stream-K tail (exact int32 pieces in the zero-filled workspace), split-K for
+//    raw output and the fused epilogue follow lut_p4t.cuh.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lut_p4t.cuh"
+
+namespace axq {
+
+namespace p4w {
+constexpr int CW = 28;                     // consumer warps
+constexpr int PW = 4;                      // producer warps
+constexpr int NT = (CW + PW) * 32;         // 1024 threads
+constexpr int BM = CW * 32;                // 896 rows per tile
+constexpr int SLICES = BM / 128;           // 7 MMA slices
+constexpr int PT = PW * 32;                // 128 producer threads
+constexpr int RPT = BM / PT;               // 7 rows per producer thread
+constexpr int TN = p4::TN;
+constexpr int W_STAGE = 512;
+constexpr int TMEM_COLS = 512;             // exact sets at 0 and 128, E sums at 256
+
+template <bool HALF>
+struct Geo {
+    static constexpr int KS = HALF ? 32 : 16;
+    static constexpr int TROWS = HALF ? 128 : 256;
+    static constexpr int TQ = TROWS * 4;
+    static constexpr int TBL_STAGE = KS * (TN / 4) * TQ;   // 64 KiB
+    static constexpr int A_STAGE = BM * KS;                // KS / 16 planes of [BM][16 B]
+    static constexpr int STAGES = 2;
+    static constexpr int FLUSH_STAGES = 256 / KS;
+    static constexpr int SMEM_TBL = 0;
+    static constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
+    static constexpr int SMEM_W = SMEM_A + STAGES * A_STAGE;
+    static constexpr int SMEM_ROW = SMEM_W + STAGES * W_STAGE;     // producer row info [BM] x 16 B
+    static constexpr int SMEM_BAR = SMEM_ROW + BM * 16;
+    // full[S], empty[S], mma[S], tile_full[2], tmem_free[2], then tmem address, flag
+    static constexpr int NBAR = 3 * STAGES + 4;
+    static constexpr int SMEM_MISC = SMEM_BAR + 8 * NBAR;
+    static constexpr int SMEM_TAP = SMEM_MISC + 16;
+    static constexpr int SMEM_BYTES = SMEM_TAP + p4::TAP_BYTES;
+};
+}  // namespace p4w
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void consumer_sync() {   // named barrier 1: the 896 consumer threads
+    asm volatile("bar.sync 1, %0;\n" ::"n"(p4w::BM) : "memory");
+}
+
+template <bool HALF>
+__global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_constant__ P4Args P) {
+    using namespace p4w;
+    using G = p4w::Geo<HALF>;
+    constexpr int KS = G::KS, STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ, A_STAGE = G::A_STAGE;
+    constexpr int NPL = KS / 16;
+    extern __shared__ __align__(1024) uint8_t p4w_smem[];
+    uint8_t* smem = p4w_smem;
+    const MMArgs& p = P.mm;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t s_base = smem_u32(smem);
+    const uint32_t bar_full = s_base + G::SMEM_BAR;
+    const uint32_t bar_empty = bar_full + 8 * STAGES;
+    const uint32_t bar_mma = bar_empty + 8 * STAGES;
+    const uint32_t bar_tfull = bar_mma + 8 * STAGES;     // [2]
+    const uint32_t bar_tfree = bar_tfull + 16;           // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + G::SMEM_MISC);
+    int* fin_flag = reinterpret_cast<int*>(smem + G::SMEM_MISC + 4);
+
+    if (P.c4) {
+        uint32_t* tap_w = reinterpret_cast<uint32_t*>(smem + G::SMEM_TAP);
+        const int ng = (int)(P.Kp / 4);
+        for (int g = tid; g < ng; g += NT) {
+            uint32_t e = ~0u;
+            if (4 * (int64_t)g < p.K) {
+                const int k = 4 * g, rs = k / p.C, c = k - rs * p.C, r = rs / p.S, s_ = rs - r * p.S;
+                e = (uint32_t)(r * p.dh) | ((uint32_t)(s_ * p.dw) << 8) | ((uint32_t)c << 16);
+            }
+            tap_w[g] = e;
+        }
+    }
+    if (KS == 16)   // K chunk 2 of the weight buffers is zero (the MMA's K is 32)
+        for (int i = tid; i < STAGES * 64; i += NT)
+            reinterpret_cast<uint32_t*>(smem + G::SMEM_W + (i >> 6) * W_STAGE + 256)[i & 63] = 0u;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(bar_full + 8 * s, PT + 1);     // 128 cp.async arrivals + expect_tx
+            mbar_init(bar_empty + 8 * s, CW);
+            mbar_init(bar_mma + 8 * s, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(bar_tfull + 8 * s, 1);
+            mbar_init(bar_tfree + 8 * s, CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // ---- work decomposition (shared by both roles): as lut_p4t.cuh ----
+    const int64_t m_tiles = (p.M + BM - 1) / BM, n_blocks = (p.N + TN - 1) / TN;
+    const int splits = P.splits > 0 ? P.splits : 1;
+    const int64_t n_work = m_tiles * n_blocks * splits;
+    const int nst_all = (int)(P.Kp / KS);
+    const int sps = P.stages_per_split > 0 ? P.stages_per_split : nst_all;
+    const bool sk = P.streamk != 0;
+    const int64_t G_ = gridDim.x;
+    const int64_t t_all = m_tiles * n_blocks;
+    const int64_t t_dp = sk ? (t_all / G_) * G_ : 0;
+    const int64_t it_sk = (t_all - t_dp) * (int64_t)nst_all;
+    auto sk_begin = [&](int64_t c) { return t_dp * nst_all + (c * it_sk) / G_; };
+    struct Gen { int64_t cur, end; bool dp; };
+    auto gen_init = [&](Gen& g) {
+        g.dp = !sk || t_dp > 0;
+        g.cur = blockIdx.x;
+        g.end = sk ? t_dp : n_work;
+        if (!g.dp) { g.cur = sk_begin(blockIdx.x); g.end = sk_begin(blockIdx.x + 1); }
+    };
+    auto gen_next = [&](Gen& g, int64_t& t, int& s_b, int& s_e) -> bool {
+        if (g.dp) {
+            if (g.cur < g.end) {
+                const int ks = (int)(g.cur % splits);
+                t = g.cur / splits;
+                s_b = ks * sps;
+                s_e = min(nst_all, s_b + sps);
+                g.cur += G_;
+                return true;
+            }
+            if (!sk) return false;
+            g.dp = false;
+            g.cur = sk_begin(blockIdx.x);
+            g.end = sk_begin(blockIdx.x + 1);
+        }
+        if (g.cur >= g.end) return false;
+        t = g.cur / nst_all;
+        s_b = (int)(g.cur - t * nst_all);
+        const int64_t rem = s_b + (g.end - g.cur);
+        s_e = (int)(rem < (int64_t)nst_all ? rem : (int64_t)nst_all);
+        g.cur += s_e - s_b;
+        return true;
+    };
+    auto tile_mn = [&](int64_t t, int64_t& nb, int64_t& m0) {
+        int64_t mt;
+        if (P.nb_fast) { nb = t % n_blocks; mt = t / n_blocks; }
+        else { mt = t % m_tiles; nb = t / m_tiles; }
+        m0 = mt * BM;
+    };
+
+    if (warp >= CW) {
+        // =============================== producer warps ===============================
+        const int pt = tid - BM;
+        const uint32_t* tap_s = reinterpret_cast<const uint32_t*>(smem + G::SMEM_TAP);
+        int4* rowinfo = reinterpret_cast<int4*>(smem + G::SMEM_ROW);   // {roff lo, roff hi, hb, wb | valid}
+        Gen g;
+        gen_init(g);
+        int64_t t;
+        int s_b, s_e;
+        uint32_t item = 0;
+        while (gen_next(g, t, s_b, s_e)) {
+            int64_t nb, m0;
+            tile_mn(t, nb, m0);
+#pragma unroll 1
+            for (int i = 0; i < RPT; ++i) {
+                const int r = pt + i * PT;
+                const RowInfo ri = P.is_conv ? make_row<LOAD_CONV>(p, m0 + r) : make_row<LOAD_GEMM>(p, m0 + r);
+                const int64_t ro = ri.base + (P.is_conv ? ((int64_t)ri.hb * p.Wd + ri.wb) * p.C : 0);
+                rowinfo[r] = make_int4((int)(ro & 0xffffffff), (int)(ro >> 32), ri.hb,
+                                       ri.valid ? ri.wb : (int)0x80000000);
+            }
+            int t_r = 0, t_s = 0, t_c = 0;
+            if (P.is_conv && !P.c4) {
+                const int k0 = s_b * KS, rs = k0 / p.C;
+                t_c = k0 - rs * p.C;
+                t_r = rs / p.S;
+                t_s = rs - t_r * p.S;
+            }
+            for (int st = s_b; st < s_e; ++st, ++item) {
+                const int buf = (int)(item % STAGES);
+                if (item >= (uint32_t)STAGES) {
+                    const uint32_t ph = ((item / STAGES) - 1) & 1u;
+                    mbar_wait(bar_empty + 8 * buf, ph);
+                    mbar_wait(bar_mma + 8 * buf, ph);
+                }
+#pragma unroll
+                for (int pl = 0; pl < NPL; ++pl) {
+                    const int64_t k0 = (int64_t)st * KS + 16 * pl;
+                    const uint32_t dst0 = s_base + G::SMEM_A + buf * A_STAGE + pl * (BM * 16);
+                    if (P.c4) {
+                        uint32_t tv[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) tv[j] = tap_s[(int)(k0 >> 2) + j];
+#pragma unroll 1
+                        for (int i = 0; i < RPT; ++i) {
+                            const int r = pt + i * PT;
+                            const int4 ri = rowinfo[r];
+                            const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int rdh = (int)(tv[j] & 0xffu), sdw = (int)((tv[j] >> 8) & 0xffu);
+                                const bool ok = ri.w != (int)0x80000000 && tv[j] != ~0u &&
+                                                (unsigned)(ri.z + rdh) < (unsigned)p.H &&
+                                                (unsigned)(ri.w + sdw) < (unsigned)p.Wd;
+                                const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + (int)(tv[j] >> 16);
+                                cp_async4(dst0 + r * 16 + 4 * j, ok ? p.A + ro + toff : p.A, ok ? 4u : 0u);
+                            }
+                        }
+                    } else if (P.is_conv) {
+                        const int rdh = t_r * p.dh, sdw = t_s * p.dw;
+                        const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + t_c;
+                        const bool kin = k0 < p.K;
+#pragma unroll 1
+                        for (int i = 0; i < RPT; ++i) {
+                            const int r = pt + i * PT;
+                            const int4 ri = rowinfo[r];
+                            const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
+                            const bool ok = kin && ri.w != (int)0x80000000 && (unsigned)(ri.z + rdh) < (unsigned)p.H &&
+                                            (unsigned)(ri.w + sdw) < (unsigned)p.Wd;
+                            cp_async16(dst0 + r * 16, ok ? p.A + ro + toff : p.A, ok ? 16u : 0u);
+                        }
+                        t_c += 16;
+                        if (t_c >= p.C) {
+                            t_c = 0;
+                            if (++t_s == p.S) { t_s = 0; ++t_r; }
+                        }
+                    } else {
+                        const int64_t rem = p.K - k0;
+                        const uint32_t nbytes = rem >= 16 ? 16u : (rem > 0 ? (uint32_t)rem : 0u);
+#pragma unroll 1
+                        for (int i = 0; i < RPT; ++i) {
+                            const int r = pt + i * PT;
+                            const int4 ri = rowinfo[r];
+                            const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
+                            const bool ok = ri.w != (int)0x80000000 && nbytes > 0;
+                            cp_async16(dst0 + r * 16, ok ? p.A + ro + k0 : p.A, ok ? nbytes : 0u);
+                        }
+                    }
+                }
+                cp_async_mbar_arrive(bar_full + 8 * buf);
+                if (pt == 0) {
+                    const uint32_t bar = bar_full + 8 * buf;
+                    const uint32_t* tbl_g = P.tables + ((size_t)nb * P.Kp + (size_t)st * KS) * 4 * G::TROWS;
+                    const int8_t* w_g = P.wpk + ((size_t)nb * (P.Kp / 16) + (size_t)st * NPL) * p4::W_STAGE;
+                    mbar_expect_tx(bar, TBL_STAGE + NPL * p4::W_STAGE);
+                    bulk_g2s(s_base + G::SMEM_TBL + buf * TBL_STAGE, tbl_g, TBL_STAGE, bar);
+                    bulk_g2s(s_base + G::SMEM_W + buf * W_STAGE, w_g, NPL * p4::W_STAGE, bar);
+                }
+            }
+        }
+    } else {
+        // =============================== consumer warps ===============================
+        const uint32_t t_lane = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t slice_col = (uint32_t)(warp >> 2) * TN;
+        const uint32_t t_e = tmem + t_lane + 256u + slice_col;
+        constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) | ((128u >> 4) << 24);
+        const bool mma_thread = (tid == 0);
+        Gen g;
+        gen_init(g);
+        int64_t tile;
+        int s_b, s_e;
+        uint32_t item = 0, tcount = 0;
+        while (gen_next(g, tile, s_b, s_e)) {
+            int64_t nb, m0;
+            tile_mn(tile, nb, m0);
+            const int64_t n0 = nb * TN;
+            const uint32_t tb = tcount & 1u;
+            const bool wlive = m0 + warp * 32 < p.M;
+            uint32_t pacc[4][2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pacc[q][0] = pacc[q][1] = 0u;
+            bool e_first = true;
+            for (int st = s_b; st < s_e; ++st, ++item) {
+                const int buf = (int)(item % STAGES);
+                mbar_wait(bar_full + 8 * buf, (item / STAGES) & 1u);
+                if (mma_thread) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> MMA
+                    if (st == s_b && tcount >= 2) mbar_wait(bar_tfree + 8 * tb, ((tcount >> 1) - 1) & 1u);
+                    tc_fence_after();
+                    const uint32_t a0 = s_base + G::SMEM_A + buf * A_STAGE;
+                    const uint64_t bdesc = umma_desc_kmajor(s_base + G::SMEM_W + buf * W_STAGE, 256u, 128u);
+#pragma unroll
+                    for (int j = 0; j < SLICES; ++j)
+                        umma_i8(tmem + tb * 128u + (uint32_t)j * TN,
+                                umma_desc_kmajor(a0 + j * 128 * 16, KS == 32 ? (uint32_t)(BM * 16) : 0u, 128u), bdesc,
+                                IDESC, st == s_b ? 0u : 1u);
+                    umma_commit(bar_mma + 8 * buf);
+                    if (st + 1 == s_e) umma_commit(bar_tfull + 8 * tb);
+                }
+                const uint8_t* tbs = smem + G::SMEM_TBL + buf * TBL_STAGE;
+                const uint8_t* at = smem + G::SMEM_A + buf * A_STAGE;
+                if (wlive) {
+#pragma unroll
+                    for (int pl = 0; pl < NPL; ++pl) {
+                        const uint4 av = *reinterpret_cast<const uint4*>(at + pl * (BM * 16) + tid * 16);
+                        const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                        for (int kk = 0; kk < 16; kk += 2) {
+                            const uint32_t ua0 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
+                            const uint32_t ua1 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + ((kk + 1) & 3));
+                            const uint8_t* r0 = tbs + (pl * 16 + kk) * 4 * TQ + ua0 * 4u;
+                            const uint8_t* r1 = tbs + (pl * 16 + kk + 1) * 4 * TQ + ua1 * 4u;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint32_t v0 = *reinterpret_cast<const uint32_t*>(r0 + q * TQ);
+                                const uint32_t v1 = *reinterpret_cast<const uint32_t*>(r1 + q * TQ);
+                                pacc[q][0] += __byte_perm(v0, 0u, 0x4240u) + __byte_perm(v1, 0u, 0x4240u);
+                                pacc[q][1] += __byte_perm(v0, 0u, 0x4341u) + __byte_perm(v1, 0u, 0x4341u);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_empty + 8 * buf);
+                if ((st - s_b + 1) % G::FLUSH_STAGES == 0 || st + 1 == s_e) {
+                    uint32_t ev[16];
+                    if (!e_first) {
+                        tmem_ld16(t_e, ev);
+                        tmem_wait_ld();
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) ev[j] = 0u;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        ev[4 * q + 0] += pacc[q][0] & 0xffffu;
+                        ev[4 * q + 2] += pacc[q][0] >> 16;
+                        ev[4 * q + 1] += pacc[q][1] & 0xffffu;
+                        ev[4 * q + 3] += pacc[q][1] >> 16;
+                        pacc[q][0] = pacc[q][1] = 0u;
+                    }
+                    tmem_st16(t_e, ev);
+                    tmem_wait_st();
+                    e_first = false;
+                }
+            }
+            int corr = p4::E_BIAS * KS * (s_e - s_b);
+            if (s_e == nst_all) corr += (int)(((P.Kp - p.K) + p.pad_lookups) * (int64_t)p.t00);
+            // exact part of this tile: TMEM set tb, complete once tile_full[tb] flips
+            mbar_wait(bar_tfull + 8 * tb, (tcount >> 1) & 1u);
+            tc_fence_after();
+            uint32_t ex[16], es[16];
+            tmem_ld16(tmem + t_lane + tb * 128u + slice_col, ex);
+            tmem_ld16(t_e, es);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_tfree + 8 * tb);   // set tb may be overwritten
+            ++tcount;
+            int eacc[16];
+#pragma unroll
+            for (int n = 0; n < 16; ++n) eacc[n] = (int)(ex[n] + es[n]) - corr;
+            const int64_t m = m0 + tid;
+            if (sk && !(s_b == 0 && s_e == nst_all)) {
+                int* wrow = P.ws + m * p.N + n0;
+                if (m < p.M) {
+#pragma unroll
+                    for (int n = 0; n < TN; ++n)
+                        if (n0 + n < p.N) atomicAdd(wrow + n, eacc[n]);
+                }
+                __threadfence();
+                consumer_sync();
+                if (tid == 0) {
+                    const int64_t x = (tile - t_dp) * nst_all;
+                    int64_t c = (x * G_) / it_sk;
+                    while (c + 1 < G_ && sk_begin(c + 1) - t_dp * nst_all <= x) ++c;
+                    const int old = atomicAdd(P.cnt + c, s_e - s_b);
+                    const int fin = (old + (s_e - s_b) == nst_all) ? 1 : 0;
+                    if (fin) P.cnt[c] = 0;
+                    *fin_flag = fin;
+                }
+                consumer_sync();
+                const int fin = *fin_flag;
+                consumer_sync();   // fin_flag is reused by the next piece
+                if (fin) {
+                    __threadfence();
+                    if (m < p.M) {
+#pragma unroll
+                        for (int n = 0; n < TN; ++n) {
+                            eacc[n] = (n0 + n < p.N) ? __ldcg(wrow + n) : 0;
+                            if (n0 + n < p.N) wrow[n] = 0;
+                        }
+                        p4t_store_row(P, m, n0, eacc, 1);
+                    }
+                }
+            } else if (m < p.M) {
+                p4t_store_row(P, m, n0, eacc, splits);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+}  // namespace axq

@@ -1,6 +1,7 @@
 // mm_p4.cu -- host side of the P4 LUT kernel (lut_p4.cuh): weight packing and launch.
 #include "lut_p4.cuh"
 #include "lut_p4t.cuh"
+#include "lut_p4w.cuh"
 #include "mm_launch.h"
 
 namespace axq {
@@ -46,15 +47,17 @@ static int launch_p4t_t(const P4Args& a, cudaStream_t st) {
     dev &= 31;
     if (!(configured & (1u << dev))) {
         cudaError_t e = cudaFuncSetAttribute(lut_p4t_kernel<HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             p4t::Geo<HALF>::SMEM_BYTES);
+                                             p4t::Geo<HALF, p4t::ks_of<HALF>()>::SMEM_BYTES);
         if (e != cudaSuccess) return (int)e;
         configured |= 1u << dev;
     }
-    const int64_t work = ((a.mm.M + p4t::BM - 1) / p4t::BM) * ((a.mm.N + p4::TN - 1) / p4::TN) * a.splits;
+    const int64_t tiles = ((a.mm.M + p4t::BM - 1) / p4t::BM) * ((a.mm.N + p4::TN - 1) / p4::TN);
+    // stream-K: every SM gets a share of the (tile, stage) iterations
+    const int64_t work = a.streamk ? tiles * (a.Kp / p4t::ks_of<HALF>()) : tiles * a.splits;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned g = (unsigned)std::min<int64_t>(work, sms > 0 ? sms : 148);
-    lut_p4t_kernel<HALF><<<g, p4t::NT, p4t::Geo<HALF>::SMEM_BYTES, st>>>(a);
+    lut_p4t_kernel<HALF><<<g, p4t::NT, p4t::Geo<HALF, p4t::ks_of<HALF>()>::SMEM_BYTES, st>>>(a);
     return (int)cudaGetLastError();
 }
 
@@ -62,15 +65,40 @@ int launch_p4t(const P4Args& a, cudaStream_t st) {
     return a.half ? launch_p4t_t<true>(a, st) : launch_p4t_t<false>(a, st);
 }
 
+template <bool HALF>
+static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
+    static unsigned configured = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev &= 31;
+    if (!(configured & (1u << dev))) {
+        cudaError_t e = cudaFuncSetAttribute(lut_p4w_kernel<HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             p4w::Geo<HALF>::SMEM_BYTES);
+        if (e != cudaSuccess) return (int)e;
+        configured |= 1u << dev;
+    }
+    const int64_t tiles = ((a.mm.M + p4w::BM - 1) / p4w::BM) * ((a.mm.N + p4::TN - 1) / p4::TN);
+    const int64_t work = a.streamk ? tiles * (a.Kp / p4w::Geo<HALF>::KS) : tiles * a.splits;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = (unsigned)std::min<int64_t>(work, sms > 0 ? sms : 148);
+    lut_p4w_kernel<HALF><<<g, p4w::NT, p4w::Geo<HALF>::SMEM_BYTES, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int launch_p4w(const P4Args& a, cudaStream_t st) {
+    return a.half ? launch_p4w_t<true>(a, st) : launch_p4w_t<false>(a, st);
+}
+
 // P4T tiles are 1024 rows: split K (exact, int32 atomics) only when they cannot fill the SMs.
-void p4t_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& splits, int& sps) {
-    const int64_t nst = Kp / p4::KS, nb = (N + p4::TN - 1) / p4::TN;
-    const int64_t t = ((M + p4t::BM - 1) / p4t::BM) * nb;
+void p4t_plan(int64_t M, int64_t N, int64_t Kp, int half, int bm, int sms, bool can_split, int& splits, int& sps) {
+    const int64_t nst = Kp / (half ? 32 : 16), nb = (N + p4::TN - 1) / p4::TN;
+    const int64_t t = ((M + bm - 1) / bm) * nb;
     splits = 1;
     sps = (int)nst;
     if (t >= sms || !can_split) return;
     int64_t s = (sms + t - 1) / t;
-    s = std::min<int64_t>(s, std::max<int64_t>(1, nst / 4));
+    s = std::min<int64_t>(s, std::max<int64_t>(1, nst / 2));
     const int64_t per = (nst + s - 1) / s;
     sps = (int)per;
     splits = (int)((nst + per - 1) / per);

@@ -38,7 +38,7 @@ class ApproxLinear:
         b = self._bufs.get(M)
         if b is None:
             b = dict(qa=torch.empty(M, self.K, dtype=torch.int8, device=device),
-                     ws=torch.empty(M, self.N, dtype=torch.int32, device=device))
+                     ws=torch.zeros(M, self.N, dtype=torch.int32, device=device))
             self._bufs[M] = b
         return b
 

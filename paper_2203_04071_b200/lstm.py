@@ -67,8 +67,8 @@ class ApproxLSTM:
                 hs=torch.empty(T, B, self.H, dtype=f32, device=d),
                 h0=torch.zeros(B, self.H, dtype=f32, device=d),
                 c=torch.empty(B, self.H, dtype=f32, device=d),
-                ws_ih=torch.empty(T * B * self.H4, dtype=torch.int32, device=d),
-                ws=torch.empty(B * self.H4, dtype=torch.int32, device=d))
+                ws_ih=torch.zeros(T * B * self.H4, dtype=torch.int32, device=d),
+                ws=torch.zeros(B * self.H4, dtype=torch.int32, device=d))
         return self._bufs[key]
 
     def run(self, x: torch.Tensor, calibrate: bool, stream=None):

@@ -145,7 +145,7 @@ class ApproxResNet:
         b["fc_q"] = torch.empty(N, cfin, dtype=i8, device=dev)
         b["logits"] = torch.empty(N, self.spec["fc"][2], dtype=f32, device=dev)
         ws_elems = max(ws_elems, N * self.spec["fc"][2], b["stem_q"].numel())
-        b["ws"] = torch.empty(ws_elems, dtype=torch.int32, device=dev)
+        b["ws"] = torch.zeros(ws_elems, dtype=torch.int32, device=dev)
         b["shapes"] = shapes
         self._bufs[key] = b
         return b

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.fixture(scope="module", params=[1, 2], ids=["p4", "p4t"])
+@pytest.fixture(scope="module", params=[1, 2, 3], ids=["p4", "p4t", "p4w"])
 def ax(request):
     """Every test runs on both packed-table kernels: P4 (mma.sync exact part) and P4T
     (tcgen05.mma exact part, TMEM accumulators)."""
@@ -116,7 +116,7 @@ def test_p4_small_m_split_k_fused(ax, M, N, K):
     bias = datagen.normal(6, 6, (N,), 0.1)
     db = _t(bias)
     y = torch.empty(M, N, device=DEV)
-    ws = torch.empty(M * N, dtype=torch.int32, device=DEV)
+    ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
     ep = ax.make_epilogue(dsa, dsw, bias=db, y=y, ldy=N, workspace=ws)
     ax.axq_lut_gemm_wp(dA, wp, ep)
     torch.cuda.synchronize()
