@@ -206,7 +206,7 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
                              const axq_epilogue* ep, int32_t* Y, void* stream);
 /* axq_wpack_kernel: selects the kernel behind axq_lut_gemm_wp / axq_lut_conv2d_wp for the
  *   calling process (all results are bit-identical; this is a performance switch for
- *   measurement): 0 = default (P4), 1 = P4 (exact part on mma.sync, 16 warps, 512- or
+ *   measurement): 0 = default (P4W; P4 for the 4-byte-tap conv loader), 1 = P4 (exact part on mma.sync, 16 warps, 512- or
  *   1024-row tiles), 2 = P4T (exact part on tcgen05.mma with TMEM accumulators, 32 warps,
  *   1024-row tiles), 3 = P4W (P4T warp-specialised: 4 producer warps stream the operands,
  *   28 consumer warps look up, 896-row tiles).  Returns the previous setting, or -1 for an

@@ -172,7 +172,7 @@ def axq_lut_create(bits: int, host_table: np.ndarray) -> Lut:
 
 
 def axq_wpack_kernel(variant: int) -> int:
-    """Select the packed-table kernel (0 default = P4, 1 P4, 2 P4T); returns the previous."""
+    """Select the packed-table kernel (0 default = P4W (P4 for C % 16 != 0 convs), 1 P4, 2 P4T, 3 P4W); returns the previous."""
     r = load().axq_wpack_kernel(int(variant))
     if r < 0:
         raise ValueError("unknown packed-table kernel variant %r" % variant)

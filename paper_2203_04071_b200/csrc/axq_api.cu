@@ -47,14 +47,23 @@ inline axq_status cuda_fail(cudaError_t e) {
 
 // Stream-K tile counters of the P4T kernel, one zero-filled block per device (the kernel leaves
 // them zero).  Allocated by axq_wpack_create, so no hot call allocates.
+// P4W also keeps its stream-K pieces in library-owned per-CTA slots: [SMs][2][896][16] int32.
 static int32_t* g_sk_cnt[64];
+static int32_t* g_sk_part[64];
 static int32_t* streamk_counters(int dev) { return (dev >= 0 && dev < 64) ? g_sk_cnt[dev] : nullptr; }
+static int32_t* streamk_parts(int dev) { return (dev >= 0 && dev < 64) ? g_sk_part[dev] : nullptr; }
+int sm_count();
 static cudaError_t ensure_streamk_counters(int dev) {
     if (dev < 0 || dev >= 64 || g_sk_cnt[dev]) return cudaSuccess;
     int32_t* c = nullptr;
+    int32_t* part = nullptr;
     cudaError_t e = cudaMalloc(&c, 4096 * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMemset(c, 0, 4096 * sizeof(int32_t));
-    if (e == cudaSuccess) g_sk_cnt[dev] = c;
+    if (e == cudaSuccess) e = cudaMalloc(&part, (size_t)sm_count() * 2 * 896 * 16 * sizeof(int32_t));
+    if (e == cudaSuccess) {
+        g_sk_cnt[dev] = c;
+        g_sk_part[dev] = part;
+    }
     return e;
 }
 
@@ -554,7 +563,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
-static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4), 1 P4, 2 P4T, 3 P4W
+static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 2 P4T, 3 P4W
 
 int axq_wpack_kernel(int variant) {
     if (variant < 0 || variant > 3) return -1;
@@ -586,7 +595,9 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     if (a.mm.M == 0) return AXQ_OK;
     // raw output may always split K (atomics into C); the fused epilogue needs a workspace
     const bool can_split = ep ? (ep->workspace != nullptr) : true;
-    const int variant = g_wpack_kernel == 0 ? 1 : g_wpack_kernel;   // default: P4
+    // default: P4W, except the 4-byte-tap conv loader (e.g. the padded 3-channel stem), where
+    // P4's 2 rows per lane measure faster
+    const int variant = g_wpack_kernel != 0 ? g_wpack_kernel : (a.c4 ? 1 : 3);
     const bool use_tc = variant >= 2;                                 // P4T / P4W: tcgen05 exact part
     const int bm = variant == 3 ? 896 : 1024;
     if (use_tc)
@@ -605,7 +616,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
             a.streamk = 1;
             a.splits = 1;
             a.stages_per_split = 0;
-            a.ws = ep->workspace;
+            a.ws = variant == 3 ? streamk_parts(dev) : ep->workspace;
             a.cnt = cnt;
         }
     }

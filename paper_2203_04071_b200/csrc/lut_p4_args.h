@@ -49,7 +49,8 @@ struct P4Args {
     int half;                   // tables cover ua = 0..127 only (non-negative activations)
     int c4;                     // conv with C % 16 != 0 (C % 4 == 0): 4-byte tap copies
     int streamk;                // P4T: stream-K decomposition (needs ws and cnt)
-    int32_t* ws;                // stream-K workspace int32 [M][N], zero on entry, left zero
+    int32_t* ws;                // stream-K pieces: P4T int32 [M][N] (zero on entry, left zero);
+                                // P4W per-CTA partial slots [grid][2][896][16]
     int32_t* cnt;               // stream-K tile counters (>= gridDim.x), zero on entry, left zero
     int nb_fast;                // tile order: column block fastest (the layer's tables stay in
                                 // L2 and each activation tile is read from HBM once) instead of

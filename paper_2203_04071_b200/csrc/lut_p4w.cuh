@@ -382,21 +382,24 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
             for (int n = 0; n < 16; ++n) eacc[n] = (int)(ex[n] + es[n]) - corr;
             const int64_t m = m0 + tid;
             if (sk && !(s_b == 0 && s_e == nst_all)) {
-                int* wrow = P.ws + m * p.N + n0;
-                if (m < p.M) {
+                // a stream-K piece: park it in this CTA's partial slot (0: the first piece of its
+                // range, 1: the last); the contributor completing the tile's stage count sums
+                // the other contributors' slots (exact int32) and runs the epilogue
+                const int64_t x0 = t_dp * nst_all + (tile - t_dp) * nst_all;   // tile's first iteration
+                const int64_t my_b = sk_begin(blockIdx.x);
+                const int slot = my_b >= x0 ? 0 : 1;
+                int4* part = reinterpret_cast<int4*>(P.ws + (((int64_t)blockIdx.x * 2 + slot) * BM + tid) * TN);
 #pragma unroll
-                    for (int n = 0; n < TN; ++n)
-                        if (n0 + n < p.N) atomicAdd(wrow + n, eacc[n]);
-                }
+                for (int j = 0; j < TN / 4; ++j)
+                    __stcg(part + j, make_int4(eacc[4 * j], eacc[4 * j + 1], eacc[4 * j + 2], eacc[4 * j + 3]));
                 __threadfence();
                 consumer_sync();
+                int64_t c_first = ((x0 - t_dp * nst_all) * G_) / it_sk;
+                while (c_first + 1 < G_ && sk_begin(c_first + 1) <= x0) ++c_first;
                 if (tid == 0) {
-                    const int64_t x = (tile - t_dp) * nst_all;
-                    int64_t c = (x * G_) / it_sk;
-                    while (c + 1 < G_ && sk_begin(c + 1) - t_dp * nst_all <= x) ++c;
-                    const int old = atomicAdd(P.cnt + c, s_e - s_b);
+                    const int old = atomicAdd(P.cnt + c_first, s_e - s_b);
                     const int fin = (old + (s_e - s_b) == nst_all) ? 1 : 0;
-                    if (fin) P.cnt[c] = 0;
+                    if (fin) P.cnt[c_first] = 0;
                     *fin_flag = fin;
                 }
                 consumer_sync();
@@ -404,14 +407,19 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                 consumer_sync();   // fin_flag is reused by the next piece
                 if (fin) {
                     __threadfence();
-                    if (m < p.M) {
+                    const int64_t x1 = x0 + nst_all;   // one past the tile's last iteration
+                    for (int64_t c = c_first; c < G_ && sk_begin(c) < x1; ++c) {
+                        const int64_t cb = sk_begin(c);
+                        if (c == blockIdx.x || cb == sk_begin(c + 1)) continue;   // self / empty range
+                        const int4* op = reinterpret_cast<const int4*>(
+                            P.ws + (((int64_t)c * 2 + (cb >= x0 ? 0 : 1)) * BM + tid) * TN);
 #pragma unroll
-                        for (int n = 0; n < TN; ++n) {
-                            eacc[n] = (n0 + n < p.N) ? __ldcg(wrow + n) : 0;
-                            if (n0 + n < p.N) wrow[n] = 0;
+                        for (int j = 0; j < TN / 4; ++j) {
+                            const int4 v = __ldcg(op + j);
+                            eacc[4 * j] += v.x; eacc[4 * j + 1] += v.y; eacc[4 * j + 2] += v.z; eacc[4 * j + 3] += v.w;
                         }
-                        p4t_store_row(P, m, n0, eacc, 1);
                     }
+                    if (m < p.M) p4t_store_row(P, m, n0, eacc, 1);
                 }
             } else if (m < p.M) {
                 p4t_store_row(P, m, n0, eacc, splits);
