@@ -36,8 +36,16 @@ __device__ __forceinline__ float epi_value(int32_t acc, int64_t m, int64_t n, fl
     return v;
 }
 
+// IEEE round-to-nearest x / s (A3) with x == 0 answered without the division: 0 / s = +0
+// exactly, and a zero dividend would otherwise send the whole warp down __fdiv_rn's slow
+// path (ReLU outputs are half zeros).  Bit-identical to __fdiv_rn(x, s) for every x, s != 0.
+__device__ __forceinline__ float div_rn_nz(float x, float s) {
+    const float t = __fdiv_rn(x == 0.f ? s : x, s);
+    return x == 0.f ? __int_as_float(__float_as_int(x) ^ (__float_as_int(s) & 0x80000000)) : t;
+}
+
 __device__ __forceinline__ int8_t epi_quant(float v, float s, float qm) {
-    float t = __fdiv_rn(v, s);
+    float t = div_rn_nz(v, s);
     t = fminf(fmaxf(t, -qm), qm);
     return (int8_t)__float2int_rn(t);
 }

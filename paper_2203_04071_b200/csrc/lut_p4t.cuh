@@ -130,15 +130,15 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
                      (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
     if (vec) {
         const bool q16 = e.q && ((e.ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 15) == 0);
-        float4 res[TN / 4];
-        if (e.residual) {
-            const float4* rp = reinterpret_cast<const float4*>(e.residual + m * e.ldr + n0);
-#pragma unroll
-            for (int j = 0; j < TN / 4; ++j) res[j] = __ldg(rp + j);
-        }
+        // residual groups are loaded one ahead (8 live registers, not 16: the P4W consumer
+        // runs at 64 registers per thread)
+        const float4* rp = e.residual ? reinterpret_cast<const float4*>(e.residual + m * e.ldr + n0) : nullptr;
+        float4 rnext = rp ? __ldg(rp) : make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t qw[TN / 4];
 #pragma unroll
         for (int n = 0; n < TN; n += 4) {
+            const float4 rcur = rnext;
+            if (rp && n + 4 < TN) rnext = __ldg(rp + (n + 4) / 4);
             const int64_t nn = n0 + n;
             float v[4];
 #pragma unroll
@@ -149,7 +149,7 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
                 v[2] = __fadd_rn(v[2], b.z); v[3] = __fadd_rn(v[3], b.w);
             }
             if (e.residual) {
-                const float4 rr = res[n / 4];
+                const float4 rr = rcur;
                 v[0] = __fadd_rn(v[0], rr.x); v[1] = __fadd_rn(v[1], rr.y);
                 v[2] = __fadd_rn(v[2], rr.z); v[3] = __fadd_rn(v[3], rr.w);
             }

@@ -12,13 +12,14 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "epilogue.cuh"
 
 namespace axq {
 
 __device__ __forceinline__ float qmax_of(int bits) { return (float)((1 << (bits - 1)) - 1); }
 
 __device__ __forceinline__ int8_t quantize_one(float x, float s, float qmax) {
-    float t = __fdiv_rn(x, s);
+    float t = div_rn_nz(x, s);
     t = fminf(fmaxf(t, -qmax), qmax);
     return (int8_t)__float2int_rn(t);
 }
