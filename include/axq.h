@@ -259,6 +259,21 @@ axq_status axq_lstm_cell(int64_t B, int64_t Hd, const float* gates_ih, const flo
                          float* c, float* h_out, int8_t* q_h, const float* d_scale_h, int bits,
                          void* stream);
 
+/* axq_lstm_recurrent: the whole static-scale recurrence of BASELINE.json configs[4] in one
+ *   persistent (cooperative) launch -- per step t = 0..T-1 exactly the chain
+ *   axq_lut_gemm_dq(hq_{t-1}, W_hh; bias b_hh) -> axq_lstm_cell (A18),
+ *   with h_{-1} = c_{-1} = 0 and hq_t = quantize(h_t, *d_scale_h, bits).
+ *   gates_ih: fp32 [T][B][4H] = fl(x_t W_ih^T dequantized + b_ih) (the hoisted input GEMM);
+ *   qw_hh: int8 [4H][H] codes; d_scale_w_hh, d_scale_h: device fp32 scalars; b_hh fp32 [4H];
+ *   lut: delta8 handle of the same bit width; hs: fp32 [T][B][H] (all h_t); c_out: fp32
+ *   [B][H] (c_{T-1}); workspace: device bytes >= 2*B*H + 256, no contents required.
+ *   Needs H % 16 == 0 and a grid of ceil(H / #SMs) * ceil(B / 32) <= 16 warps per SM that
+ *   fits co-resident (else AXQ_ERR_UNSUPPORTED: use the per-step calls). */
+axq_status axq_lstm_recurrent(int64_t T, int64_t B, int64_t H, const float* gates_ih,
+                              const int8_t* qw_hh, const float* d_scale_w_hh, const float* b_hh,
+                              const float* d_scale_h, int bits, axq_lut_t lut, float* hs,
+                              float* c_out, int8_t* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

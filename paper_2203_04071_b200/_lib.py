@@ -27,7 +27,7 @@ EXPORTED = [
     "axq_dequantize", "axq_dequantize_nhwc_to_nchw", "axq_epilogue_apply",
     "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
     "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
-    "axq_lut_conv2d_wp", "axq_wpack_kernel",
+    "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_lstm_recurrent",
 ]
 
 
@@ -94,6 +94,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_create": ([vp, vp, i64, i64, i64, i32, ctypes.POINTER(vp)], i32),
         "axq_wpack_destroy": ([vp], i32),
         "axq_wpack_kernel": ([i32], i32),
+        "axq_lstm_recurrent": ([i64, i64, i64, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp], i32),
         "axq_wpack_info": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "axq_lut_gemm_wp": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_lut_conv2d_wp": ([ctypes.POINTER(axq_conv_desc), vp, vp,
@@ -392,3 +393,13 @@ def axq_lut_conv2d_wp(desc: axq_conv_desc, X_nhwc, wp: WPack, ep: axq_epilogue |
     _check("axq_lut_conv2d_wp", load().axq_lut_conv2d_wp(
         ctypes.byref(desc), _ptr(X_nhwc), wp.handle, ctypes.byref(ep) if ep is not None else None,
         _ptr(Y), _stream(stream)))
+
+
+def axq_lstm_recurrent(gates_ih, qw_hh, d_scale_w_hh, b_hh, d_scale_h, bits: int, lut: Lut, hs, c_out,
+                       workspace, stream=None) -> None:
+    """The static-scale LSTM recurrence in one persistent launch (include/axq.h).  Raises
+    AxqError with status AXQ_ERR_UNSUPPORTED when the shape cannot run co-resident."""
+    T, B, H = hs.shape
+    _check("axq_lstm_recurrent", load().axq_lstm_recurrent(
+        T, B, H, _ptr(gates_ih), _ptr(qw_hh), _ptr(d_scale_w_hh), _ptr(b_hh), _ptr(d_scale_h),
+        int(bits), lut.handle, _ptr(hs), _ptr(c_out), _ptr(workspace), _stream(stream)))

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "lut_p4_args.h"
+#include "lstm_rec_args.h"
 #include "mm_launch.h"
 #include "glue_kernels.cuh"
 #include "quant_kernels.cuh"
@@ -761,6 +762,34 @@ axq_status axq_lstm_cell(int64_t B, int64_t Hd, const float* gates_ih, const flo
     axq::lstm_cell_kernel<<<stream_grid(B * Hd, 256), 256, 0, S(stream)>>>(
         B, Hd, gates_ih, gates_hh, c, h_out, q_h, d_scale_h, q_h ? bits : 8);
     return check_launch();
+}
+
+axq_status axq_lstm_recurrent(int64_t T, int64_t B, int64_t H, const float* gates_ih,
+                              const int8_t* qw_hh, const float* d_scale_w_hh, const float* b_hh,
+                              const float* d_scale_h, int bits, axq_lut_t lut, float* hs,
+                              float* c_out, int8_t* workspace, void* stream) {
+    if (T < 0 || B < 0 || H < 0) return AXQ_ERR_INVALID;
+    if (T == 0 || B == 0 || H == 0) return AXQ_OK;
+    if (!gates_ih || !qw_hh || !d_scale_w_hh || !b_hh || !d_scale_h || !hs || !c_out || !workspace)
+        return AXQ_ERR_INVALID;
+    axq_status s = check_lut(lut);
+    if (s != AXQ_OK) return s;
+    if (bits != lut->bits) return AXQ_ERR_INVALID;
+    if (lut->repr != AXQ_LUT_DELTA8) return AXQ_ERR_UNSUPPORTED;
+    s = overflow_guard(lut, H);
+    if (s != AXQ_OK) return s;
+    if (T > INT32_MAX || B > INT32_MAX || H > INT32_MAX || (reinterpret_cast<uintptr_t>(workspace) & 15) ||
+        (reinterpret_cast<uintptr_t>(qw_hh) & 15))
+        return AXQ_ERR_UNSUPPORTED;
+    axq::LstmRecArgs a{};
+    a.T = (int)T; a.B = (int)B; a.H = (int)H;
+    a.gih = gates_ih; a.qw = qw_hh; a.sw = d_scale_w_hh; a.b_hh = b_hh; a.sh = d_scale_h;
+    a.bits = bits; a.table = reinterpret_cast<const int8_t*>(lut->d_table);
+    a.hs = hs; a.c_out = c_out; a.hq = workspace;
+    a.bar = reinterpret_cast<unsigned int*>(workspace + ((2 * B * H + 15) / 16) * 16);
+    const int rc = axq::launch_lstm_rec(a, sm_count(), S(stream));
+    if (rc == -1) return AXQ_ERR_UNSUPPORTED;
+    return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }
 
 }  // extern "C"

@@ -35,6 +35,8 @@ int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, cons
 int launch_p4(const P4Args& a, cudaStream_t st);
 int launch_p4t(const P4Args& a, cudaStream_t st);   // tcgen05 exact part, 32 warps (lut_p4t.cuh)
 int launch_p4w(const P4Args& a, cudaStream_t st);   // warp-specialised P4T (lut_p4w.cuh)
+struct LstmRecArgs;
+int launch_lstm_rec(const LstmRecArgs& a, int sms, cudaStream_t st);   // lstm_rec.cuh
 void p4t_plan(int64_t M, int64_t N, int64_t Kp, int half, int bm, int sms, bool can_split, int& splits, int& sps);
 void p4_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& rpl, int& splits,
              int& sps);

@@ -7,7 +7,10 @@ quantized approximate Linears (own input and weight scales, A18), gates in PyTor
 i, f, g, o.  The input projection of all T steps is hoisted into one LUT-GEMM
 (M = T*B); each step runs one LUT-GEMM (M = B) with the bias epilogue and one cell kernel
 that applies the pinned sigmoid / tanh, updates c and writes h both in fp32 and as int8 codes
-for the next step (static scale).  The static forward can be captured in a CUDA graph.
+for the next step (static scale).  The static (calibrated) forward runs the whole recurrence
+in ONE persistent launch (axq_lstm_recurrent: each CTA owns hidden units, a grid barrier per
+step) when the shape fits; the per-step chain remains for calibration and other shapes.  The
+static forward can be captured in a CUDA graph.
 
 calibrate(x): every quantization dynamic (per-tensor max of that tensor); s_x = scale of
 max|x| over all steps, s_h = scale of max_t max|h_t| (reading A7').
@@ -50,6 +53,10 @@ class ApproxLSTM:
         self._bufs = {}
         self.calibrated = False
         self.timing_hook = None     # optional callable(kind, stream) around every LUT launch
+        # static forward: the whole recurrence in one persistent launch (axq_lstm_recurrent)
+        # when the shape allows it; "steps" forces one LUT-GEMM + one cell launch per step
+        self.recurrent = "auto"
+        self._persistent_ok = lut.repr == "delta8"
 
     def _hook(self, kind, stream):
         if self.timing_hook:
@@ -68,7 +75,8 @@ class ApproxLSTM:
                 h0=torch.zeros(B, self.H, dtype=f32, device=d),
                 c=torch.empty(B, self.H, dtype=f32, device=d),
                 ws_ih=torch.zeros(T * B * self.H4, dtype=torch.int32, device=d),
-                ws=torch.zeros(B * self.H4, dtype=torch.int32, device=d))
+                ws=torch.zeros(B * self.H4, dtype=torch.int32, device=d),
+                ws_rec=torch.empty(2 * B * self.H + 256, dtype=torch.int8, device=d))
         return self._bufs[key]
 
     def run(self, x: torch.Tensor, calibrate: bool, stream=None):
@@ -93,6 +101,18 @@ class ApproxLSTM:
             ax.axq_lut_gemm_ep(b["qx"], self.qw_ih, self.lut, ep, stream)
         self._hook("post", stream)
         c, qh, ghh, hs = b["c"], b["qh"], b["ghh"], b["hs"]
+        if not calibrate and self.recurrent == "auto" and self._persistent_ok:
+            self._hook("pre", stream)
+            try:
+                ax.axq_lstm_recurrent(gih, self.qw_hh, self.sw_hh, self.b_hh, self.s_h, bits,
+                                      self.lut, hs, c, b["ws_rec"], stream)
+                self._hook("post", stream)
+                return hs, c
+            except ax.AxqError as e:          # shape not co-resident: per-step launches
+                if e.status != ax.AXQ_ERR_UNSUPPORTED:
+                    raise
+                self._persistent_ok = False
+                self._hook("post", stream)
         with torch.cuda.stream(stream):
             c.zero_()
             qh.zero_()

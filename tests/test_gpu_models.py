@@ -111,3 +111,27 @@ def test_lstm_cuda_graph_replay_matches_forward():
     hs2, cT2 = replay()
     torch.cuda.synchronize()
     assert torch.equal(hs, hs2) and torch.equal(cT, cT2)
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_lstm_persistent_matches_step_chain(bits):
+    """The one-launch recurrence (axq_lstm_recurrent) is bit-identical to the per-step chain
+    (LUT-GEMM + epilogue + cell launches), on a shape with a ragged batch row group."""
+    from paper_2203_04071_b200 import Lut
+    from paper_2203_04071_b200.lstm import ApproxLSTM
+    c = datagen.config4(T=9, B=40, I=64, H=96)
+    net = ApproxLSTM(c.W_ih, c.W_hh, c.b_ih, c.b_hh, Lut(bits, c.luts[bits]), DEV)
+    xd = torch.from_numpy(c.x).to(DEV)
+    net.calibrate(xd)
+    net.recurrent = "steps"
+    hs1, c1 = (t.clone() for t in net.forward(xd))
+    net.recurrent = "auto"
+    hs2, c2 = net.forward(xd)
+    assert net._persistent_ok
+    torch.cuda.synchronize()
+    assert torch.equal(hs1, hs2) and torch.equal(c1, c2)
+    orc = models.LstmOracle(c, bits)
+    s_x, s_h = orc.calibrate()
+    hs_ref, c_ref = orc.forward((s_x, s_h))
+    np.testing.assert_array_equal(hs2.cpu().numpy(), hs_ref)
+    np.testing.assert_array_equal(c2.cpu().numpy(), c_ref)
