@@ -127,8 +127,8 @@ Cfg pick_cfg(int64_t M, int loader, int repr) {
     return (M > 2048 && big_ok) ? CFG_BIG : CFG_SMALL;
 }
 
-inline int64_t cfg_bm(const Cfg& c) { return (int64_t)32 * c.R * (c.nsplit ? 1 : c.warps); }
-inline int64_t cfg_bn(const Cfg& c) { return (int64_t)c.tn * (c.nsplit ? c.warps : 1); }
+inline int64_t cfg_bm(const Cfg& c) { return (int64_t)32 * c.R * (c.warps / c.wc); }
+inline int64_t cfg_bn(const Cfg& c) { return (int64_t)c.tn * c.wc; }
 
 // K-splitting so that small M*N problems still fill the SMs (exact: integer atomics).
 int64_t pick_k_split(int64_t M, int64_t N, int64_t K, const Cfg& c, bool allow) {
@@ -136,8 +136,10 @@ int64_t pick_k_split(int64_t M, int64_t N, int64_t K, const Cfg& c, bool allow) 
     if (!allow || K <= 0) return std::max<int64_t>(kr, axq::KC);
     int64_t bm = cfg_bm(c);
     int64_t tiles = ((M + bm - 1) / bm) * ((N + cfg_bn(c) - 1) / cfg_bn(c));
-    int64_t want = (int64_t)sm_count() * 2;
-    if (tiles >= want) return kr;
+    // 16-warp MID tiles: one wave of SMs suffices (no split from 3/4 of the SMs up)
+    const bool mid = c.warps == axq::CFG_MID.warps && c.wc == axq::CFG_MID.wc;
+    int64_t want = (int64_t)sm_count() * (mid ? 1 : 2);
+    if (tiles >= (mid ? want * 3 / 4 : want)) return kr;
     int64_t splits = (want + tiles - 1) / tiles;
     int64_t max_splits = std::max<int64_t>(1, kr / (4 * axq::KC));  // >= 64 k per split
     splits = std::min(splits, max_splits);

@@ -191,14 +191,16 @@ __device__ __forceinline__ uint4 load_w(const MMArgs& p, int64_t n, int64_t k0, 
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// NSPLIT: warps split the CTA's columns instead of its rows (small M, e.g. the LSTM's
+// WC: the CTA's warps form a (WARPS/WC) x WC grid over rows x columns; WC = WARPS splits
+// only the columns (small M, e.g. the LSTM's
 // recurrent GEMM with M = 64): CTA tile = (32 R) rows x (WARPS TN) columns.
-template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, bool NSPLIT = false>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16 || NSPLIT) ? 1 : (WARPS >= 8 ? 2 : 3))
+template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, int WC = 1>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16 || WC > 1) ? 1 : (WARPS >= 8 ? 2 : 3))
 lut_mm_kernel(const MMArgs p) {
     constexpr int NT = WARPS * 32;
-    constexpr int BM = NSPLIT ? 32 * R : WARPS * 32 * R;
-    constexpr int CTN = NSPLIT ? WARPS * TN : TN;   // columns per CTA tile
+    constexpr int WR = WARPS / WC;                 // warps along the rows
+    constexpr int BM = WR * 32 * R;
+    constexpr int CTN = WC * TN;                   // columns per CTA tile
     extern __shared__ __align__(16) int8_t smem[];
     // layout: [table (table_bytes, 0 for I32)] [W tiles: 2 x KC/4 x TN words]
     int8_t* lut_s = smem;
@@ -237,7 +239,8 @@ lut_mm_kernel(const MMArgs p) {
     const int64_t mn = n_split > 0 ? tile / n_split : tile;
     const int64_t m0 = (mn / n_tiles) * BM;
     const int64_t nc0 = (mn % n_tiles) * CTN;            // CTA's first column
-    const int64_t n0 = nc0 + (NSPLIT ? warp * TN : 0);   // this warp's first column
+    const int wr = warp % WR, wc = warp / WR;
+    const int64_t n0 = nc0 + wc * TN;                    // this warp's first column
     const int64_t kb = ks * p.k_split;
     const int64_t ke = min(p.K, kb + p.k_split);
     const int nchunks = (int)((ke - kb + KC - 1) / KC);
@@ -245,7 +248,7 @@ lut_mm_kernel(const MMArgs p) {
     RowInfo rows[R];
 #pragma unroll
     for (int r = 0; r < R; ++r)
-        rows[r] = make_row<LOADER>(p, m0 + (int64_t)((NSPLIT ? 0 : warp * R) + r) * 32 + lane);
+        rows[r] = make_row<LOADER>(p, m0 + (int64_t)(wr * R + r) * 32 + lane);
 
     int acc[R][TN];
 #pragma unroll
@@ -276,7 +279,7 @@ lut_mm_kernel(const MMArgs p) {
             for (int r = 0; r < R; ++r) a_nxt[r] = load_a<LOADER>(p, rows[r], kn, tap_s);
             if (tid < CTN) w_nxt = load_w(p, nc0 + tid, kn, wvec);
         }
-        const uint32_t* ws = w_s + (ci & 1) * (4 * CTN) + (NSPLIT ? warp * TN : 0);
+        const uint32_t* ws = w_s + (ci & 1) * (4 * CTN) + wc * TN;
 #pragma unroll
         for (int kq = 0; kq < 4; ++kq) {
             uint32_t a4[R], alo[R], ahi[R];

@@ -5,10 +5,10 @@
 
 namespace axq {
 
-template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, bool NSPLIT = false>
+template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, int WC = 1>
 int launch_one(const MMArgs& p, dim3 grid, cudaStream_t st) {
-    auto kern = lut_mm_kernel<REPR, TN, R, WARPS, LOADER, EPI, NSPLIT>;
-    const int smem = (REPR == REPR_I32 ? 0 : p.table_bytes) + 2 * (KC / 4) * TN * (NSPLIT ? WARPS : 1) * 4 +
+    auto kern = lut_mm_kernel<REPR, TN, R, WARPS, LOADER, EPI, WC>;
+    const int smem = (REPR == REPR_I32 ? 0 : p.table_bytes) + 2 * (KC / 4) * TN * WC * 4 +
                      (LOADER == LOAD_CONV_C4 ? 4 * (MAX_TAP_GROUPS + 4) : 0);
     static unsigned configured = 0;  // bit per device
     static int resident[32] = {0};   // CTAs per SM, per device
@@ -38,9 +38,11 @@ template <int REPR, int LOADER, int EPI>
 int launch_cfg(const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st) {
     constexpr bool big_ok = (REPR != REPR_I32) && (LOADER == LOAD_GEMM || LOADER == LOAD_CONV || LOADER == LOAD_CONV_C4);
     if constexpr (big_ok) {
-        if (c.nsplit && LOADER == LOAD_GEMM)
-            return launch_one<REPR, CFG_TINY.tn, CFG_TINY.R, CFG_TINY.warps, LOADER, EPI, true>(p, grid, st);
-        if (c.warps == CFG_BIG.warps && c.R == CFG_BIG.R && !c.nsplit)
+        if (c.wc == CFG_TINY.wc && c.warps == CFG_TINY.warps && LOADER == LOAD_GEMM)
+            return launch_one<REPR, CFG_TINY.tn, CFG_TINY.R, CFG_TINY.warps, LOADER, EPI, CFG_TINY.wc>(p, grid, st);
+        if (c.wc == CFG_MID.wc && c.warps == CFG_MID.warps && LOADER == LOAD_GEMM)
+            return launch_one<REPR, CFG_MID.tn, CFG_MID.R, CFG_MID.warps, LOADER, EPI, CFG_MID.wc>(p, grid, st);
+        if (c.warps == CFG_BIG.warps && c.R == CFG_BIG.R && c.wc == 1)
             return launch_one<REPR, CFG_BIG.tn, CFG_BIG.R, CFG_BIG.warps, LOADER, EPI>(p, grid, st);
     }
     return launch_one<REPR, CFG_SMALL.tn, CFG_SMALL.R, CFG_SMALL.warps, LOADER, EPI>(p, grid, st);

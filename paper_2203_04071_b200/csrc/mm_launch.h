@@ -13,15 +13,19 @@ constexpr int MAX_TAP_GROUPS = 1024;
 
 struct Cfg {
     int warps, R, tn;
-    bool nsplit;   // warps split the columns (CTA tile 32R x warps*tn)
+    int wc;        // warps along the columns (CTA tile 32R*(warps/wc) x wc*tn)
 };
 // BIG: 8 warps x 1 row per lane x 32 columns (256 x 32 CTA tile), two resident CTAs per SM
 // (each with its own table copy) so one CTA's epilogue overlaps the other's lookups;
 // SMALL: 4 warps x 1 x 32 (128 x 32).
-constexpr Cfg CFG_BIG{8, 1, 32, false};
-constexpr Cfg CFG_SMALL{4, 1, 32, false};
+constexpr Cfg CFG_BIG{8, 1, 32, 1};
+constexpr Cfg CFG_SMALL{4, 1, 32, 1};
 // TINY (M <= 64): 8 warps x 32 columns each over the same 64 rows (2 rows per lane).
-constexpr Cfg CFG_TINY{8, 2, 32, true};
+constexpr Cfg CFG_TINY{8, 2, 32, 8};
+// MID: 16 warps as 2 row groups x 8 column groups of 4 columns (64 x 32 CTA tile, whole K
+// per tile).  Measured no faster than SMALL + K split on the 256-row linear layer of BJ
+// configs[1] (86 vs 83 us), so pick_cfg does not select it; kept instantiated for A/B runs.
+constexpr Cfg CFG_MID{16, 1, 4, 8};
 
 // Return 0 or a cudaError_t code.
 int launch_mm_delta8(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
