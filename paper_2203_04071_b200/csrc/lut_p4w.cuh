@@ -9,7 +9,8 @@
 //    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
 //    the consumer warps released it (empty barrier) and the MMA that read it completed.
 //  * 28 consumer warps (896 rows, one per lane) only wait for full buffers, do the lookups
-//    (4 per 32-bit LDS, two k summed per 3-input add) and release the buffer; consumer warp
+//    (4 per 32-bit LDS; the adds split between the ALU pipe -- two k per 3-input add -- and
+//    the FMA pipe -- multiply-add by an opaque 1) and release the buffer; consumer warp
 //    0's lane 0 also issues the exact-part MMAs (7 slices of 128 rows, M = 128, N = 16, K = 32)
 //    into one of two TMEM accumulator sets, so the next tile's MMAs never wait for this
 //    tile's epilogue reads.  No CTA-wide barrier in the steady state.
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
         const uint32_t t_e = tmem + t_lane + 256u + slice_col;
         constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) | ((128u >> 4) << 24);
         const bool mma_thread = (tid == 0);
+        const uint32_t one = P.one;   // = 1, opaque to the compiler (keeps those adds on the FMA pipe)
         Gen g;
         gen_init(g);
         int64_t tile;
@@ -334,8 +336,17 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                             for (int q = 0; q < 4; ++q) {
                                 const uint32_t v0 = *reinterpret_cast<const uint32_t*>(r0 + q * TQ);
                                 const uint32_t v1 = *reinterpret_cast<const uint32_t*>(r1 + q * TQ);
-                                pacc[q][0] += __byte_perm(v0, 0u, 0x4240u) + __byte_perm(v1, 0u, 0x4240u);
-                                pacc[q][1] += __byte_perm(v0, 0u, 0x4341u) + __byte_perm(v1, 0u, 0x4341u);
+                                const uint32_t e0 = __byte_perm(v0, 0u, 0x4240u), e1 = __byte_perm(v1, 0u, 0x4240u);
+                                const uint32_t o0 = __byte_perm(v0, 0u, 0x4341u), o1 = __byte_perm(v1, 0u, 0x4341u);
+                                if (q < 2) {     // ALU pipe: one 3-input add per accumulator
+                                    pacc[q][0] += e0 + e1;
+                                    pacc[q][1] += o0 + o1;
+                                } else {         // FMA pipe: multiply-adds by an opaque 1
+                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e0), "r"(one));
+                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e1), "r"(one));
+                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o0), "r"(one));
+                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o1), "r"(one));
+                                }
                             }
                         }
                     }
