@@ -60,7 +60,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("AXQ_LIB", LIB_PATH))   # AXQ_LIB: A/B builds
     if not p.exists():
         raise ImportError("libaxq.so not built at %s (run __graft_entry__.build())" % p)
     L = ctypes.CDLL(str(p))

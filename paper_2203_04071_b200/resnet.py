@@ -271,6 +271,26 @@ class ApproxResNet:
     def calibrate(self, x, stream=None):
         return self.run(x, True, stream)
 
+    def capture(self, x):
+        """Record the static forward on x (a fixed device buffer) as one CUDA graph (55 LUT
+        launches + glue, no host work between them); returns a replay callable that returns the
+        logits buffer (same values as forward(x))."""
+        assert self.calibrated, "calibrate() first (static per-layer scales)"
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self.run(x, False, side)              # warm-up: kernel attributes, buffers
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.run(x, False, torch.cuda.current_stream(self.dev))
+        self._graphs = getattr(self, "_graphs", []) + [g]
+
+        def replay():
+            g.replay()
+            return out
+        return replay
+
     def forward(self, x, stream=None):
         assert self.calibrated, "calibrate() first (static per-layer scales)"
         return self.run(x, False, stream)
