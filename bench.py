@@ -36,6 +36,7 @@ import numpy as np  # noqa: E402
 
 SM_COUNT_NOMINAL = 148
 LANES = 32
+DESIGN_LOOKUPS_PER_CLK = 1024.0 / 11.0   # ALU-pipe bound of the P4W inner loop
 
 
 def parse():
@@ -492,8 +493,10 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "int8",
             "data": "synthetic (seeded; DESIGN.md input recipe), random-init weights",
             "config": cfg,
-            "roofline": {"bound": "smem", "kernel": "LUT kernels (lut_p4_kernel / lut_mm_kernel: "
-                         "all LUT-GEMM/conv launches of the step, CUDA events around each)",
+            "roofline": {"bound": "smem", "kernel": "LUT kernels (lut_p4w_kernel packed-table "
+                         "tcgen05 path, lut_p4_kernel for the 4-byte-tap stem, lut_mm_kernel for "
+                         "small M, lstm_rec_kernel for the LSTM recurrence: all LUT launches of the "
+                         "step, CUDA events around each on the launching stream)",
                          "achieved": round(achieved, 2), "peak": round(roof, 2),
                          "unit": "Glookup/s", "frac": round(achieved / roof, 4),
                          "peak_basis": "BASELINE metric's smem-lookup roofline: %d SMs x 32 lanes "
@@ -507,6 +510,14 @@ def run_ours(args, rank, world, local_rank):
                                               "at 1 table byte per lookup (no design can exceed it)",
                          "frac_at_measured_clock": round(achieved / (sm * LANES * f_meas / 1e9), 4)
                          if f_meas else None,
+                         "design_roofline": {
+                             "bound": "alu", "peak": round(sm * f_max / 1e9 * DESIGN_LOOKUPS_PER_CLK, 2),
+                             "unit": "Glookup/s",
+                             "frac": round(achieved / (sm * f_max / 1e9 * DESIGN_LOOKUPS_PER_CLK), 4),
+                             "basis": "packed-table inner loop: 22 ALU-pipe warp instructions "
+                                      "(PRMT, IADD3) per 1024 lookups; ALU pipe 2 warp "
+                                      "instructions per SM clock (B300_MICROARCH rt_SMSP = 2) -> "
+                                      "93.1 lookups per SM clock (DESIGN.md 5.4)"},
                          "kernel_ms_per_step": round(kmean, 4),
                          "kernel_share_of_step": round(kmean / (total_ms / args.steps), 4),
                          "traffic": committed_traffic(wl.name)},
