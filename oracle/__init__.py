@@ -56,6 +56,14 @@ def lib():
         L.orc_lut_conv2d.restype = i64
         L.orc_dequantize.argtypes = [i64, vp, f32, f32, vp, i64, i64, vp]
         L.orc_dequantize.restype = None
+        L.orc_amax_rows.argtypes = [vp, i64, i64, vp]
+        L.orc_amax_rows.restype = None
+        L.orc_quantize_rows.argtypes = [vp, i64, i64, vp, i32, vp]
+        L.orc_quantize_rows.restype = None
+        L.orc_hist_calib.argtypes = [vp, i64, i32, i64, i64, ctypes.POINTER(f32)]
+        L.orc_hist_calib.restype = i64
+        L.orc_dequantize_pc.argtypes = [i64, vp, f32, vp, vp, i64, i64, vp]
+        L.orc_dequantize_pc.restype = None
         L.orc_set_threads.argtypes = [i32]
         L.orc_set_threads.restype = None
         L.orc_max_threads.argtypes = []
@@ -181,3 +189,60 @@ def conv2d(x, W, bias, lut, bits: int, stride=(1, 1), pad=(0, 0)):
     qw, sw = quantize_tensor(W, bits)
     acc = lut_conv2d(qa, qw, lut, bits, stride, pad)
     return dequantize(acc, sa, sw, bias, channel_axis=1), acc, (qa, sa, qw, sw)
+
+
+# ---- NEXT-1: the paper's quantizer -- per-channel weights, 99.9 % histogram activations
+#      (readings A30-A32) ----
+
+HIST_BINS = 2048
+PERCENTILE = (999, 1000)      # 99.9 %
+
+
+def amax_rows(W) -> np.ndarray:
+    """Per-output-channel max |W| (A31); W [rows][...] flattened per row."""
+    W = _c(W, np.float32)
+    rows = W.shape[0]
+    cols = W.size // rows
+    a = np.empty(rows, np.float32)
+    lib().orc_amax_rows(_p(W), rows, cols, _p(a))
+    return a
+
+
+def scale_rows(amax_r, bits: int) -> np.ndarray:
+    """Per-channel scales: orc_scale of each channel's amax (A4 per channel)."""
+    return np.array([scale(a, bits) for a in np.asarray(amax_r, np.float32)], np.float32)
+
+
+def quantize_rows(W, s_r, bits: int) -> np.ndarray:
+    W = _c(W, np.float32)
+    rows = W.shape[0]
+    cols = W.size // rows
+    s = _c(s_r, np.float32)
+    assert s.size == rows
+    q = np.empty(W.shape, np.int8)
+    lib().orc_quantize_rows(_p(W), rows, cols, _p(s), int(bits), _p(q))
+    return q
+
+
+def hist_calib_max(x, bins: int = HIST_BINS, percentile=PERCENTILE):
+    """(calib_max, bin index) of the histogram percentile calibrator (A30)."""
+    x = _c(x, np.float32)
+    cm = ctypes.c_float()
+    b = lib().orc_hist_calib(_p(x), x.size, int(bins), int(percentile[0]), int(percentile[1]),
+                             ctypes.byref(cm))
+    return np.float32(cm.value), int(b)
+
+
+def dequantize_pc(acc, s_a, s_w, bias=None, channel_axis: int = -1) -> np.ndarray:
+    """y = fl(fl(acc * fl(s_a * s_w[ch])) + bias[ch]) (A32)."""
+    acc = _c(acc, np.int32)
+    y = np.empty(acc.shape, np.float32)
+    ax = channel_axis % acc.ndim
+    nch = acc.shape[ax]
+    inner = int(np.prod(acc.shape[ax + 1:], dtype=np.int64))
+    sw = _c(s_w, np.float32)
+    assert sw.size == nch
+    b = None if bias is None else _c(bias, np.float32)
+    lib().orc_dequantize_pc(acc.size, _p(acc), float(np.float32(s_a)), _p(sw),
+                            None if b is None else _p(b), nch, inner, _p(y))
+    return y

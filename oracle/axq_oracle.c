@@ -21,6 +21,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -156,6 +157,65 @@ void orc_dequantize(int64_t count, const int32_t* acc, float s_a, float s_w,
         float v = (float)acc[i];
         v = v * sc;
         if (bias) v = v + bias[(i / inner) % nch];
+        y[i] = v;
+    }
+}
+
+/* ===================== NEXT-1: the paper's own quantizer =====================
+ * "weight ranges are per channel while activation ranges are per tensor"; activations
+ * are calibrated by "the histogram calibrator for a 99.9% percentile" which "learns
+ * offline calib_max, the absolute maximum input value representable in the quantized space"
+ * (P:94).  Readings A30-A32 fix what the paper leaves open. */
+
+/* Per-output-channel amax of a weight tensor stored [rows][cols] (rows = output channels;
+ * conv weights flattened per output channel).  Max-abs statistic (A31). */
+void orc_amax_rows(const float* W, int64_t rows, int64_t cols, float* amax_r) {
+    for (int64_t r = 0; r < rows; ++r) amax_r[r] = orc_amax(W + r * cols, cols);
+}
+
+/* q[r][c] = clamp(rint(W[r][c] / s[r])) -- O4 with the row's own scale. */
+void orc_quantize_rows(const float* W, int64_t rows, int64_t cols, const float* s_r, int bits,
+                       int8_t* q) {
+    for (int64_t r = 0; r < rows; ++r) orc_quantize(W + r * cols, cols, s_r[r], bits, q + r * cols);
+}
+
+/* Histogram percentile calib_max (A30): bins of width w = fl(amax / bins) over [0, amax];
+ * |x| falls in bin min(trunc(fl(|x| / w)), bins - 1); calib_max is the upper edge
+ * fl((i + 1) * w) of the first bin i whose cumulative count c satisfies
+ * c * p_den >= n * p_num (percentile p = p_num / p_den, 99.9 % = 999 / 1000).  amax == 0 gives
+ * calib_max = 0 (the scale rule then returns 1, A4).  Also returns the bin index. */
+int64_t orc_hist_calib(const float* x, int64_t n, int bins, int64_t p_num, int64_t p_den,
+                       float* calib_max) {
+    float a = orc_amax(x, n);
+    *calib_max = 0.0f;
+    if (a == 0.0f || n == 0) return -1;
+    float w = a / (float)bins;
+    int64_t* cnt = (int64_t*)calloc((size_t)bins, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i) {
+        float t = fabsf(x[i]) / w;
+        int64_t b = (int64_t)t;          /* t >= 0: truncation is floor */
+        if (b > bins - 1) b = bins - 1;
+        cnt[b] += 1;
+    }
+    int64_t cum = 0, hit = bins - 1;
+    for (int64_t b = 0; b < bins; ++b) {
+        cum += cnt[b];
+        if (cum * p_den >= n * p_num) { hit = b; break; }
+    }
+    free(cnt);
+    *calib_max = (float)(hit + 1) * w;
+    return hit;
+}
+
+/* O7 with per-channel weight scales (A32): y = fl(fl((float)acc * fl(s_a * s_w[ch])) + b[ch]). */
+void orc_dequantize_pc(int64_t count, const int32_t* acc, float s_a, const float* s_w,
+                       const float* bias, int64_t nch, int64_t inner, float* y) {
+    for (int64_t i = 0; i < count; ++i) {
+        int64_t ch = (i / inner) % nch;
+        float sc = s_a * s_w[ch];
+        float v = (float)acc[i];
+        v = v * sc;
+        if (bias) v = v + bias[ch];
         y[i] = v;
     }
 }

@@ -21,7 +21,8 @@ import numpy as np
 
 import datagen
 
-from . import (amax, dequantize, lut_conv2d, lut_gemm, quantize, scale)
+from . import (amax, amax_rows, dequantize, dequantize_pc, hist_calib_max, lut_conv2d, lut_gemm,
+               quantize, quantize_rows, scale, scale_rows)
 
 F32 = np.float32
 
@@ -121,25 +122,43 @@ class ResNetOracle:
     per-layer activation scales (reading A7').  forward(x, scales): the same network with those
     static scales (inputs beyond the calibrated range clamp, A2)."""
 
-    def __init__(self, lut, bits=8, config=3, **topo):
+    def __init__(self, lut, bits=8, config=3, quantizer="max", **topo):
+        """quantizer "max": per-tensor max calibration of weights and activations (BJ north
+        star).  "paper": the paper's own quantizer (NEXT-1) -- per-output-channel
+        weight scales (A31) and 99.9 % histogram calib_max for activations (A30)."""
         self.layers = resnet_layers(**topo)
         self.W = resnet_weights(self.layers, config)
         self.lut, self.bits = lut, bits
+        self.quantizer = quantizer
         self.wq = {}
         for l in self.layers:
             w = self.W[l["name"]]
-            s = scale(amax(w), bits)
-            self.wq[l["name"]] = (quantize(w, s, bits), s)
+            if quantizer == "paper":
+                s = scale_rows(amax_rows(w), bits)
+                self.wq[l["name"]] = (quantize_rows(w, s, bits), s)
+            else:
+                s = scale(amax(w), bits)
+                self.wq[l["name"]] = (quantize(w, s, bits), s)
 
     def _scale(self, name, x, scales, calib):
         if calib:
-            scales[name] = scale(amax(x), self.bits)
+            if self.quantizer == "paper":
+                scales[name] = scale(hist_calib_max(x)[0], self.bits)
+            else:
+                scales[name] = scale(amax(x), self.bits)
         return scales[name]
+
+    def _deq_layer(self, acc, sa, sw, bias=None, channel_axis=1):
+        if self.quantizer == "paper":
+            return dequantize_pc(acc, sa, sw, bias, channel_axis)
+        if bias is None:
+            return _deq(acc, sa, sw)
+        return dequantize(acc, sa, sw, bias, channel_axis)
 
     def _conv(self, name, xq, sa, layer):
         q, sw = self.wq[name]
         acc = lut_conv2d(xq, q, self.lut, self.bits, (layer["stride"],) * 2, (layer["pad"],) * 2)
-        return _deq(acc, sa, sw)
+        return self._deq_layer(acc, sa, sw)
 
     def run(self, x, scales=None, trace=None):
         calib = scales is None
@@ -175,7 +194,7 @@ class ResNetOracle:
         s_fc = self._scale("fc", p, scales, calib)
         q, sw = self.wq["fc"]
         acc = lut_gemm(quantize(p, s_fc, b), q, self.lut, b)
-        logits = dequantize(acc, s_fc, sw, self.W["fc.b"])
+        logits = self._deq_layer(acc, s_fc, sw, self.W["fc.b"], -1)
         return logits, scales
 
     def calibrate(self, x):
