@@ -92,6 +92,30 @@ axq_status axq_amax(const float* x, int64_t n, float* d_amax, void* stream);
 axq_status axq_scale(const float* d_amax, int bits, float* d_scale, void* stream);
 axq_status axq_quantize(const float* x, int64_t n, const float* d_scale, int bits,
                         int8_t* q, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * NEXT-1: the paper's own quantizer ("we implemented the histogram calibrator for a
+ * 99.9% percentile ... weight ranges are per channel while activation ranges are per
+ * tensor"; readings A30-A32).  All device pointers, asynchronous on `stream`.
+ * axq_amax_rows: d_amax[r] = max_c |W[r][c]| for W fp32 [rows][cols] (row = output channel,
+ *   conv weights flattened KRSC or KCRS per output channel).
+ * axq_scale_vec: d_scale[i] = d_amax[i] / (2^(bits-1)-1), 0 -> 1 (axq_scale per element).
+ * axq_quantize_rows: q[r][c] = clamp(rint(W[r][c] / d_scale_rows[r])) (axq_quantize per row).
+ * axq_calib_histogram: d_hist[bins] (uint32, zeroed by the call) = counts of |x| over the
+ *   bins of width fl(*d_amax / bins) on [0, *d_amax]: bin = min(trunc(fl(|x| / w)), bins-1).
+ *   d_amax must hold max|x| (axq_amax).  bins <= 8192; n < 2^32.
+ * axq_calib_percentile: calib_max = fl((i+1) * w) for the first bin i whose cumulative count c
+ *   has c * p_den >= n * p_num (99.9 % = 999 / 1000); writes it to d_calib_max (nullable) and
+ *   the scale calib_max / qmax (0 -> 1) to d_scale (nullable). */
+axq_status axq_amax_rows(const float* W, int64_t rows, int64_t cols, float* d_amax, void* stream);
+axq_status axq_scale_vec(const float* d_amax, int64_t n, int bits, float* d_scale, void* stream);
+axq_status axq_quantize_rows(const float* W, int64_t rows, int64_t cols, const float* d_scale_rows,
+                             int bits, int8_t* q, void* stream);
+axq_status axq_calib_histogram(const float* x, int64_t n, const float* d_amax, int bins,
+                               uint32_t* d_hist, void* stream);
+axq_status axq_calib_percentile(const uint32_t* d_hist, int bins, int64_t n, const float* d_amax,
+                                int64_t p_num, int64_t p_den, int bits, float* d_calib_max,
+                                float* d_scale, void* stream);
 axq_status axq_quantize_nchw_to_nhwc(const float* x, int64_t N, int64_t C, int64_t H,
                                      int64_t W, int64_t Cq, const float* d_scale, int bits,
                                      int8_t* q, void* stream);
@@ -142,6 +166,9 @@ typedef struct axq_epilogue {
     int64_t ldq;
     const float* d_scale_out; /* device fp32 scalar, required with q_out */
     int32_t bits_out;         /* 2..8, required with q_out */
+    const float* d_scale_w_ch;/* device fp32 [N] per-output-channel weight scales or NULL
+                                 (NEXT-1, "weight ranges are per channel"): column n then
+                                 uses fl(s_a * s_w[n]) in place of fl(s_a * s_w) (A32) */
 } axq_epilogue;
 
 axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
@@ -242,6 +269,11 @@ axq_status axq_epilogue_apply(int64_t M, int64_t N, const int32_t* acc, int64_t 
 axq_status axq_maxpool2d_nhwc_i8(const int8_t* x, int64_t N, int64_t H, int64_t W, int64_t C,
                                  int64_t R, int64_t S, int64_t stride, int64_t pad, int8_t* y,
                                  void* stream);
+/* axq_maxpool2d_nhwc_f32: the same pooling on fp32 NHWC (used by the paper quantizer's
+ *   calibration pass, where the pooled real values are histogrammed). */
+axq_status axq_maxpool2d_nhwc_f32(const float* x, int64_t N, int64_t H, int64_t W, int64_t C,
+                                  int64_t R, int64_t S, int64_t stride, int64_t pad, float* y,
+                                  void* stream);
 axq_status axq_avgpool_nhwc(const float* x, int64_t N, int64_t HW, int64_t C, float* y,
                             int8_t* q, const float* d_scale, int bits, void* stream);
 

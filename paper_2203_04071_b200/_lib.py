@@ -28,6 +28,8 @@ EXPORTED = [
     "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
     "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
     "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_lstm_recurrent",
+    "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
+    "axq_calib_percentile", "axq_maxpool2d_nhwc_f32",
 ]
 
 
@@ -43,7 +45,8 @@ class axq_epilogue(ctypes.Structure):
                 ("workspace", ctypes.c_void_p), ("residual", ctypes.c_void_p),
                 ("ldr", ctypes.c_int64), ("relu", ctypes.c_int32), ("y_nhwc", ctypes.c_int32),
                 ("q_out", ctypes.c_void_p), ("ldq", ctypes.c_int64),
-                ("d_scale_out", ctypes.c_void_p), ("bits_out", ctypes.c_int32)]
+                ("d_scale_out", ctypes.c_void_p), ("bits_out", ctypes.c_int32),
+                ("d_scale_w_ch", ctypes.c_void_p)]
 
 
 class axq_conv_desc(ctypes.Structure):
@@ -94,13 +97,22 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_create": ([vp, vp, i64, i64, i64, i32, ctypes.POINTER(vp)], i32),
         "axq_wpack_destroy": ([vp], i32),
         "axq_wpack_kernel": ([i32], i32),
+        "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
+        "axq_maxpool2d_nhwc_f32": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp], i32),
+        "axq_scale_vec": ([vp, i64, i32, vp, vp], i32),
+        "axq_quantize_rows": ([vp, i64, i64, vp, i32, vp, vp], i32),
+        "axq_calib_histogram": ([vp, i64, vp, i32, vp, vp], i32),
+        "axq_calib_percentile": ([vp, i32, i64, vp, i64, i64, i32, vp, vp, vp], i32),
         "axq_lstm_recurrent": ([i64, i64, i64, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp], i32),
         "axq_wpack_info": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "axq_lut_gemm_wp": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_lut_conv2d_wp": ([ctypes.POINTER(axq_conv_desc), vp, vp,
                                ctypes.POINTER(axq_epilogue), vp, vp], i32),
     }
+    ab = "AXQ_LIB" in os.environ           # an older A/B build may lack newer entry points
     for name, (args, res) in sig.items():
+        if ab and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -224,11 +236,16 @@ def axq_lut_gemm(A, W, lut: Lut, C, stream=None) -> None:
 
 def make_epilogue(d_scale_a, d_scale_w, bias=None, y=None, ldy=0, workspace=None,
                   residual=None, ldr=0, relu=False, y_nhwc=False, q_out=None, ldq=0,
-                  d_scale_out=None, bits_out=0) -> axq_epilogue:
-    return axq_epilogue(_ptr(d_scale_a), _ptr(d_scale_w), _ptr(bias), _ptr(y), int(ldy),
-                        _ptr(workspace), _ptr(residual), int(ldr), int(bool(relu)),
-                        int(bool(y_nhwc)), _ptr(q_out), int(ldq), _ptr(d_scale_out),
-                        int(bits_out))
+                  d_scale_out=None, bits_out=0, d_scale_w_ch=None) -> axq_epilogue:
+    """d_scale_w: the per-tensor weight scale (device scalar); d_scale_w_ch: per-output-channel
+    weight scales [N] (NEXT-1), which take precedence when given."""
+    ep = axq_epilogue(_ptr(d_scale_a), _ptr(d_scale_w), _ptr(bias), _ptr(y), int(ldy),
+                      _ptr(workspace), _ptr(residual), int(ldr), int(bool(relu)),
+                      int(bool(y_nhwc)), _ptr(q_out), int(ldq), _ptr(d_scale_out),
+                      int(bits_out), _ptr(d_scale_w_ch))
+    # the struct holds raw device pointers: keep the tensors alive as long as it lives
+    ep._keep = (d_scale_a, d_scale_w, bias, y, workspace, residual, q_out, d_scale_out, d_scale_w_ch)
+    return ep
 
 
 def _epilogue(d_scale_a, d_scale_w, bias, y, ldy, workspace):
@@ -403,3 +420,44 @@ def axq_lstm_recurrent(gates_ih, qw_hh, d_scale_w_hh, b_hh, d_scale_h, bits: int
     _check("axq_lstm_recurrent", load().axq_lstm_recurrent(
         T, B, H, _ptr(gates_ih), _ptr(qw_hh), _ptr(d_scale_w_hh), _ptr(b_hh), _ptr(d_scale_h),
         int(bits), lut.handle, _ptr(hs), _ptr(c_out), _ptr(workspace), _stream(stream)))
+
+
+# ---- NEXT-1: the paper's quantizer (per-channel weights, 99.9 % histogram calib_max) ----
+HIST_BINS = 2048
+PERCENTILE = (999, 1000)
+
+
+def axq_amax_rows(W, d_amax, stream=None) -> None:
+    rows = W.shape[0]
+    _check("axq_amax_rows", load().axq_amax_rows(_ptr(W), rows, W.numel() // rows, _ptr(d_amax),
+                                                 _stream(stream)))
+
+
+def axq_scale_vec(d_amax, bits: int, d_scale, stream=None) -> None:
+    _check("axq_scale_vec", load().axq_scale_vec(_ptr(d_amax), d_amax.numel(), int(bits), _ptr(d_scale),
+                                                 _stream(stream)))
+
+
+def axq_quantize_rows(W, d_scale_rows, bits: int, q, stream=None) -> None:
+    rows = W.shape[0]
+    _check("axq_quantize_rows", load().axq_quantize_rows(_ptr(W), rows, W.numel() // rows,
+                                                         _ptr(d_scale_rows), int(bits), _ptr(q),
+                                                         _stream(stream)))
+
+
+def axq_calib_histogram(x, d_amax, d_hist, stream=None) -> None:
+    _check("axq_calib_histogram", load().axq_calib_histogram(_ptr(x), x.numel(), _ptr(d_amax),
+                                                             d_hist.numel(), _ptr(d_hist), _stream(stream)))
+
+
+def axq_calib_percentile(d_hist, n: int, d_amax, bits: int, d_calib_max=None, d_scale=None,
+                         percentile=PERCENTILE, stream=None) -> None:
+    _check("axq_calib_percentile", load().axq_calib_percentile(
+        _ptr(d_hist), d_hist.numel(), int(n), _ptr(d_amax), int(percentile[0]), int(percentile[1]),
+        int(bits), _ptr(d_calib_max), _ptr(d_scale), _stream(stream)))
+
+
+def axq_maxpool2d_nhwc_f32(x, R: int, S: int, stride: int, pad: int, y, stream=None) -> None:
+    N, H, W, C = x.shape
+    _check("axq_maxpool2d_nhwc_f32", load().axq_maxpool2d_nhwc_f32(
+        _ptr(x), N, H, W, C, R, S, stride, pad, _ptr(y), _stream(stream)))

@@ -291,6 +291,53 @@ axq_status axq_scale(const float* d_amax, int bits, float* d_scale, void* stream
     return check_launch();
 }
 
+// ---- NEXT-1: the paper's quantizer (A30-A32) ----
+axq_status axq_amax_rows(const float* W, int64_t rows, int64_t cols, float* d_amax, void* stream) {
+    if (rows < 0 || cols < 0 || (rows > 0 && (!W || !d_amax))) return AXQ_ERR_INVALID;
+    if (rows == 0) return AXQ_OK;
+    if (cols == 0) return cudaMemsetAsync(d_amax, 0, rows * sizeof(float), S(stream)) == cudaSuccess ? AXQ_OK : AXQ_ERR_CUDA;
+    axq::amax_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 148 * 8), 256, 0, S(stream)>>>(W, rows, cols, d_amax);
+    return check_launch();
+}
+
+axq_status axq_scale_vec(const float* d_amax, int64_t n, int bits, float* d_scale, void* stream) {
+    if (n < 0 || bits < 2 || bits > 8 || (n > 0 && (!d_amax || !d_scale))) return AXQ_ERR_INVALID;
+    if (n == 0) return AXQ_OK;
+    axq::scale_vec_kernel<<<stream_grid(n, 256), 256, 0, S(stream)>>>(d_amax, n, bits, d_scale);
+    return check_launch();
+}
+
+axq_status axq_quantize_rows(const float* W, int64_t rows, int64_t cols, const float* d_scale_rows,
+                             int bits, int8_t* q, void* stream) {
+    if (rows < 0 || cols < 0 || bits < 2 || bits > 8) return AXQ_ERR_INVALID;
+    if (rows == 0 || cols == 0) return AXQ_OK;
+    if (!W || !d_scale_rows || !q) return AXQ_ERR_INVALID;
+    axq::quantize_rows_kernel<<<stream_grid(rows * cols, 256 * 4), 256, 0, S(stream)>>>(W, rows, cols, d_scale_rows,
+                                                                                    bits, q);
+    return check_launch();
+}
+
+axq_status axq_calib_histogram(const float* x, int64_t n, const float* d_amax, int bins,
+                               uint32_t* d_hist, void* stream) {
+    if (n < 0 || bins < 1 || bins > 8192 || !d_amax || !d_hist || (n > 0 && !x)) return AXQ_ERR_INVALID;
+    cudaError_t e = cudaMemsetAsync(d_hist, 0, (size_t)bins * sizeof(uint32_t), S(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (n == 0) return AXQ_OK;
+    axq::hist_kernel<<<stream_grid(n, 256 * 8), 256, (size_t)bins * 4, S(stream)>>>(x, n, d_amax, bins, d_hist);
+    return check_launch();
+}
+
+axq_status axq_calib_percentile(const uint32_t* d_hist, int bins, int64_t n, const float* d_amax,
+                                int64_t p_num, int64_t p_den, int bits, float* d_calib_max,
+                                float* d_scale, void* stream) {
+    if (!d_hist || bins < 1 || n < 0 || !d_amax || p_num < 0 || p_den <= 0 || p_num > p_den ||
+        bits < 2 || bits > 8 || (!d_calib_max && !d_scale))
+        return AXQ_ERR_INVALID;
+    axq::percentile_kernel<<<1, 32, 0, S(stream)>>>(d_hist, bins, n, d_amax, p_num, p_den, bits, d_calib_max,
+                                                    d_scale);
+    return check_launch();
+}
+
 axq_status axq_quantize(const float* x, int64_t n, const float* d_scale, int bits, int8_t* q,
                         void* stream) {
     if (n < 0 || !d_scale || bits < 2 || bits > 8 || (n > 0 && (!x || !q))) return AXQ_ERR_INVALID;
@@ -345,6 +392,7 @@ static axq::EpiArgs to_epi(const axq_epilogue* ep, bool nchw, int64_t hw) {
     axq::EpiArgs e{};
     e.sa = ep->d_scale_a;
     e.sw = ep->d_scale_w;
+    e.sw_ch = ep->d_scale_w_ch;
     e.bias = ep->bias;
     e.residual = ep->residual;
     e.ldr = ep->ldr;
@@ -740,6 +788,21 @@ axq_status axq_maxpool2d_nhwc_i8(const int8_t* x, int64_t N, int64_t H, int64_t 
         axq::maxpool_nhwc_i8_bytes_kernel<<<stream_grid(N * Ho * Wo * C, 256), 256, 0, S(stream)>>>(
             x, N, (int)H, (int)W, (int)C, (int)R, (int)Sz, (int)stride, (int)pad, (int)Ho, (int)Wo, y);
     }
+    return check_launch();
+}
+
+axq_status axq_maxpool2d_nhwc_f32(const float* x, int64_t N, int64_t H, int64_t W, int64_t C,
+                                  int64_t R, int64_t Sz, int64_t stride, int64_t pad, float* y,
+                                  void* stream) {
+    if (N < 0 || H <= 0 || W <= 0 || C <= 0 || R <= 0 || Sz <= 0 || stride <= 0 || pad < 0 ||
+        pad >= R || pad >= Sz)
+        return AXQ_ERR_INVALID;
+    const int64_t Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - Sz) / stride + 1;
+    if (Ho <= 0 || Wo <= 0) return AXQ_ERR_INVALID;
+    if (N == 0) return AXQ_OK;
+    if (!x || !y) return AXQ_ERR_INVALID;
+    axq::maxpool_nhwc_f32_kernel<<<stream_grid(N * Ho * Wo * C, 256), 256, 0, S(stream)>>>(
+        x, N, (int)H, (int)W, (int)C, (int)R, (int)Sz, (int)stride, (int)pad, (int)Ho, (int)Wo, y);
     return check_launch();
 }
 

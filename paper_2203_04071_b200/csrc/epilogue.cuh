@@ -25,11 +25,18 @@ struct EpiArgs {
     int64_t ldq;
     const float* s_out;     // device scalar
     int bits_out;
+    const float* sw_ch;     // per-output-channel weight scales [N] or null (NEXT-1, A32)
 };
+
+// The dequantization factor of column n: fl(s_a * s_w) (per tensor, precomputed as sc) or
+// fl(s_a * s_w[n]) with per-channel weight scales (A32).
+__device__ __forceinline__ float epi_sc(const EpiArgs& e, float sc, int64_t n) {
+    return e.sw_ch ? __fmul_rn(*e.sa, e.sw_ch[n]) : sc;
+}
 
 __device__ __forceinline__ float epi_value(int32_t acc, int64_t m, int64_t n, float sc,
                                            const EpiArgs& e) {
-    float v = __fmul_rn(__int2float_rn(acc), sc);
+    float v = __fmul_rn(__int2float_rn(acc), epi_sc(e, sc, n));
     if (e.bias) v = __fadd_rn(v, e.bias[n]);
     if (e.residual) v = __fadd_rn(v, e.residual[m * e.ldr + n]);
     if (e.relu) v = v > 0.f ? v : 0.f;

@@ -41,6 +41,34 @@ __global__ void maxpool_nhwc_i8_kernel(const int8_t* __restrict__ x, int64_t N, 
     }
 }
 
+// fp32 NHWC max pooling (out-of-image taps ignored, A17): the calibration pass of the paper
+// quantizer needs the pooled real values (a percentile does not commute with pooling as the
+// max does)
+__global__ void maxpool_nhwc_f32_kernel(const float* __restrict__ x, int64_t N, int H, int W, int C, int R,
+                                        int S, int stride, int pad, int Ho, int Wo, float* __restrict__ y) {
+    const int64_t total = N * Ho * Wo * (int64_t)C;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
+        const int c = (int)(i % C);
+        int64_t t = i / C;
+        const int wo = (int)(t % Wo);
+        t /= Wo;
+        const int ho = (int)(t % Ho);
+        const int64_t n = t / Ho;
+        float m = -INFINITY;
+        for (int r = 0; r < R; ++r) {
+            const int hi = ho * stride - pad + r;
+            if (hi < 0 || hi >= H) continue;
+            for (int s = 0; s < S; ++s) {
+                const int wi = wo * stride - pad + s;
+                if (wi < 0 || wi >= W) continue;
+                m = fmaxf(m, __ldg(x + ((n * H + hi) * W + wi) * C + c));
+            }
+        }
+        y[i] = m;
+    }
+}
+
 __global__ void maxpool_nhwc_i8_bytes_kernel(const int8_t* __restrict__ x, int64_t N, int H, int W,
                                              int C, int R, int S, int stride, int pad, int Ho,
                                              int Wo, int8_t* __restrict__ y) {

@@ -384,7 +384,7 @@ lut_mm_kernel(const MMArgs p) {
                     const int64_t nn = n0 + n;
                     float v[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(acc[r][n + j]), sc);
+                    for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(acc[r][n + j]), epi_sc(e, sc, nn + j));
                     if (e.bias) {
                         const float4 b = *reinterpret_cast<const float4*>(e.bias + nn);
                         v[0] = __fadd_rn(v[0], b.x); v[1] = __fadd_rn(v[1], b.y);

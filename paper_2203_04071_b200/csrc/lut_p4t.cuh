@@ -142,7 +142,7 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
             const int64_t nn = n0 + n;
             float v[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(eacc[n + j]), sc);
+            for (int j = 0; j < 4; ++j) v[j] = __fmul_rn(__int2float_rn(eacc[n + j]), epi_sc(e, sc, nn + j));
             if (e.bias) {
                 const float4 b = *reinterpret_cast<const float4*>(e.bias + nn);
                 v[0] = __fadd_rn(v[0], b.x); v[1] = __fadd_rn(v[1], b.y);

@@ -201,4 +201,90 @@ __global__ void dequant_nhwc_to_nchw_kernel(const int32_t* __restrict__ acc, int
     }
 }
 
+// ===================== NEXT-1: the paper's quantizer (A30-A32) =====================
+
+// Per-output-channel amax of W [rows][cols] (A31): one block per row (grid-stride over rows).
+__global__ void amax_rows_kernel(const float* __restrict__ W, int64_t rows, int64_t cols,
+                                 float* __restrict__ amax_r) {
+    __shared__ float wm[32];
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float* w = W + r * cols;
+        float m = 0.f;
+        for (int64_t i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(w[i]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (lane == 0) wm[wid] = m;
+        __syncthreads();
+        if (wid == 0) {
+            m = lane < (int)(blockDim.x >> 5) ? wm[lane] : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) amax_r[r] = m;
+        }
+        __syncthreads();
+    }
+}
+
+// s[i] = amax[i] / qmax, amax == 0 -> 1 (the scalar rule of scale_kernel, per element)
+__global__ void scale_vec_kernel(const float* __restrict__ amax, int64_t n, int bits, float* __restrict__ s) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float a = amax[i];
+        s[i] = (a == 0.f) ? 1.0f : __fdiv_rn(a, qmax_of(bits));
+    }
+}
+
+// q[r][c] = quantize(W[r][c], s[r])
+__global__ void quantize_rows_kernel(const float* __restrict__ W, int64_t rows, int64_t cols,
+                                     const float* __restrict__ s_r, int bits, int8_t* __restrict__ q) {
+    const float qm = qmax_of(bits);
+    const int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        q[i] = quantize_one(W[i], s_r[i / cols], qm);
+}
+
+// Histogram of |x| over [0, amax] (A30): bin = min(trunc(fl(|x| / fl(amax / bins))), bins - 1).
+// Per-block shared counts, then one atomicAdd per non-empty bin (counts are integers: exact).
+__global__ void hist_kernel(const float* __restrict__ x, int64_t n, const float* __restrict__ d_amax,
+                            int bins, unsigned int* __restrict__ hist) {
+    extern __shared__ unsigned int hs[];
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) hs[b] = 0u;
+    __syncthreads();
+    const float a = *d_amax;
+    if (a > 0.f) {
+        const float w = __fdiv_rn(a, (float)bins);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            const float t = div_rn_nz(fabsf(x[i]), w);
+            int b = (int)t;
+            b = b > bins - 1 ? bins - 1 : b;
+            atomicAdd(hs + b, 1u);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < bins; b += blockDim.x)
+        if (hs[b]) atomicAdd(hist + b, hs[b]);
+}
+
+// calib_max = fl((i + 1) * w) for the first bin i with cum * p_den >= n * p_num; s = calib_max / qmax
+// (0 -> 1).  One warp: per-lane partial sums of 64-bin chunks, then a serial walk (untimed).
+__global__ void percentile_kernel(const unsigned int* __restrict__ hist, int bins, int64_t n,
+                                  const float* __restrict__ d_amax, int64_t p_num, int64_t p_den,
+                                  int bits, float* __restrict__ d_calib_max, float* __restrict__ d_scale) {
+    if (threadIdx.x != 0) return;
+    const float a = *d_amax;
+    float cm = 0.f;
+    if (a > 0.f && n > 0) {
+        const float w = __fdiv_rn(a, (float)bins);
+        int64_t cum = 0;
+        int hit = bins - 1;
+        for (int b = 0; b < bins; ++b) {
+            cum += hist[b];
+            if (cum * p_den >= n * p_num) { hit = b; break; }
+        }
+        cm = __fmul_rn((float)(hit + 1), w);
+    }
+    if (d_calib_max) *d_calib_max = cm;
+    if (d_scale) *d_scale = (cm == 0.f) ? 1.0f : __fdiv_rn(cm, qmax_of(bits));
+}
+
 }  // namespace axq

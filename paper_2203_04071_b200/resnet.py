@@ -51,7 +51,14 @@ def _out(h, k, s, p):
 
 
 class ApproxResNet:
-    def __init__(self, weights: dict, lut: ax.Lut, device="cuda", packed=True, **topo):
+    def __init__(self, weights: dict, lut: ax.Lut, device="cuda", packed=True, quantizer="max",
+                 **topo):
+        """quantizer "max": per-tensor max calibration (BASELINE.json north star, the bench
+        configuration).  "paper": the paper's own quantizer (NEXT-1): per-output-
+        channel weight scales and the 99.9 % histogram calib_max for every activation
+        (readings A30-A32)."""
+        assert quantizer in ("max", "paper")
+        self.quantizer = quantizer
         self.dev = torch.device(device)
         self.lut, self.bits = lut, lut.bits
         self.specs = layer_specs(**topo)
@@ -67,13 +74,23 @@ class ApproxResNet:
         self.s_act = torch.ones(n, device=self.dev)      # per-layer input scales
         self.s_w = torch.ones(n, device=self.dev)        # per-layer weight scales
         self.qw = {}
+        self.s_w_ch = {}                                  # per-channel weight scales (paper)
+        self.hist = torch.zeros(ax.HIST_BINS, dtype=torch.int32, device=self.dev)
         for name, kind, cout, cin, k, stride, pad in self.specs:
             w = torch.as_tensor(weights[name]).to(self.dev, torch.float32).contiguous()
             i = self.slot[name]
             q = torch.empty(w.shape, dtype=torch.int8, device=self.dev)
-            ax.axq_amax(w, self.d_amax[i:i + 1])
-            ax.axq_scale(self.d_amax[i:i + 1], self.bits, self.s_w[i:i + 1])
-            ax.axq_quantize(w, self.s_w[i:i + 1], self.bits, q)
+            if quantizer == "paper":
+                a = torch.empty(cout, device=self.dev)
+                sc = torch.empty(cout, device=self.dev)
+                ax.axq_amax_rows(w, a)
+                ax.axq_scale_vec(a, self.bits, sc)
+                ax.axq_quantize_rows(w, sc, self.bits, q)
+                self.s_w_ch[name] = sc
+            else:
+                ax.axq_amax(w, self.d_amax[i:i + 1])
+                ax.axq_scale(self.d_amax[i:i + 1], self.bits, self.s_w[i:i + 1])
+                ax.axq_quantize(w, self.s_w[i:i + 1], self.bits, q)
             if kind == "conv":
                 q = q.permute(0, 2, 3, 1).contiguous()                    # KRSC
                 if name == "stem" and cin % 4:
@@ -122,6 +139,7 @@ class ApproxResNet:
         b["stem_f"] = torch.empty(N, h, w, C, dtype=f32, device=dev)       # calibration only
         h, w = _out(h, 3, 2, 1), _out(w, 3, 2, 1)
         b["pool_q"] = torch.empty(N, h, w, C, dtype=i8, device=dev)
+        b["pool_f32"] = torch.empty(N, h, w, C, dtype=f32, device=dev)     # calibration only
         shapes = {}
         ws_elems = 0
         for blk in self.blocks:
@@ -155,7 +173,8 @@ class ApproxResNet:
         C = xq.shape[-1]
         d = ax.conv_desc(N, H, W, C, cout, k, k, (stride, stride), (pad, pad),
                          c_valid=cin if C != cin else 0)
-        ep = ax.make_epilogue(self._s(name), self._sw(name), y_nhwc=True, **ep_kw)
+        ep = ax.make_epilogue(self._s(name), self._sw(name), y_nhwc=True,
+                              d_scale_w_ch=self.s_w_ch.get(name), **ep_kw)
         if self.timing_hook:
             self.timing_hook("pre", stream)
         wp = self.wp.get(name)
@@ -170,7 +189,12 @@ class ApproxResNet:
     def _calib_scale(self, name, t, stream):
         i = self.slot[name]
         ax.axq_amax(t, self.d_amax[i:i + 1], stream)
-        ax.axq_scale(self.d_amax[i:i + 1], self.bits, self.s_act[i:i + 1], stream)
+        if self.quantizer == "paper":      # 99.9 % histogram calib_max (A30)
+            ax.axq_calib_histogram(t, self.d_amax[i:i + 1], self.hist, stream)
+            ax.axq_calib_percentile(self.hist, t.numel(), self.d_amax[i:i + 1], self.bits,
+                                    d_scale=self.s_act[i:i + 1], stream=stream)
+        else:
+            ax.axq_scale(self.d_amax[i:i + 1], self.bits, self.s_act[i:i + 1], stream)
 
     # ---------------------------------------------------------------------------------
     def run(self, x: torch.Tensor, calibrate: bool, stream=None) -> torch.Tensor:
@@ -190,8 +214,14 @@ class ApproxResNet:
             f = b["stem_f"]
             self._conv("stem", b["qx"], N, H, W, stream, y=f, ldy=f.shape[-1], relu=True,
                        workspace=ws)
-            # amax(maxpool(v)) == amax(v): every stem output lies in some pooling window
-            self._calib_scale(first, f, stream)
+            if self.quantizer == "paper":
+                # a percentile does not commute with pooling: histogram the pooled values
+                pf = b["pool_f32"]
+                ax.axq_maxpool2d_nhwc_f32(f, 3, 3, 2, 1, pf, stream)
+                self._calib_scale(first, pf, stream)
+            else:
+                # amax(maxpool(v)) == amax(v): every stem output lies in some pooling window
+                self._calib_scale(first, f, stream)
             ax.axq_quantize(f, self._s(first), bits, b["stem_q"], stream)
         else:
             q = b["stem_q"]
@@ -258,7 +288,7 @@ class ApproxResNet:
             ax.axq_avgpool_nhwc(f_in, q=b["fc_q"], d_scale=self._s("fc"), bits=bits, stream=stream)
         lg = b["logits"]
         ep = ax.make_epilogue(self._s("fc"), self._sw("fc"), bias=self.fc_bias, y=lg,
-                              ldy=lg.shape[-1], workspace=ws)
+                              ldy=lg.shape[-1], workspace=ws, d_scale_w_ch=self.s_w_ch.get("fc"))
         if self.timing_hook:
             self.timing_hook("pre", stream)
         ax.axq_lut_gemm_ep(b["fc_q"], self.qw["fc"], self.lut, ep, stream)
