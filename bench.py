@@ -36,6 +36,7 @@ import numpy as np  # noqa: E402
 
 SM_COUNT_NOMINAL = 148
 LANES = 32
+QUANTIZER = "max"
 DESIGN_LOOKUPS_PER_CLK = 1024.0 / 11.0   # ALU-pipe bound of the P4W inner loop
 
 
@@ -46,6 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet", choices=["resnet", "conv", "linear", "lstm"])
+    ap.add_argument("--quantizer", default="max", choices=["max", "paper"],
+                    help="resnet only: 'paper' = per-channel weights + 99.9%% histogram "
+                         "activations (NEXT-1, P:93-95) instead of BASELINE's per-tensor max")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
@@ -202,7 +206,9 @@ class ResNetWL:
         self.x_host = torch.from_numpy(x_all[a:b]).pin_memory()
         self.x = self.x_host.to(dev)
         self.lut = Lut(8, datagen.lut_randerr(8, 0, 2))          # A15: c0's table
-        self.net = ApproxResNet(datagen.network_weights(layer_specs(), 3), self.lut, dev)
+        self.quantizer = QUANTIZER
+        self.net = ApproxResNet(datagen.network_weights(layer_specs(), 3), self.lut, dev,
+                                quantizer=QUANTIZER)
         self.net.calibrate(torch.from_numpy(x_all[:8]).to(dev))   # static scales, untimed
         torch.cuda.synchronize()
         self.net.timing_hook = timer
@@ -216,7 +222,10 @@ class ResNetWL:
         self.desc = {"workload": "BJ configs[3]: ResNet-50-shaped approximate forward (53 convs + "
                                  "fc, every multiply a LUT lookup), x fp32 [256,3,224,224] N(0,1), "
                                  "Kaiming weights, randerr int8 LUT (c0's), static per-layer "
-                                 "max calibration on images 0-7 (untimed)",
+                                 + ("max calibration" if QUANTIZER == "max" else
+                                    "99.9% histogram calibration with per-channel weight scales "
+                                    "(the paper's quantizer, NEXT-1)") +
+                                 " on images 0-7 (untimed)",
                      "global_batch": total, "batch_per_gpu": self.per,
                      "lookups_per_image": self.net.lookups_per_image()}
 
@@ -408,6 +417,8 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=dev)
 
     timer = KernelTimer()
+    global QUANTIZER
+    QUANTIZER = args.quantizer
     wl = WORKLOADS[args.workload](dev, rank, world, timer)
     stream = torch.cuda.current_stream()
     # L2 flush buffer (> 126 MB L2) written before every timed step, outside the timed region

@@ -323,7 +323,14 @@ axq_status axq_calib_histogram(const float* x, int64_t n, const float* d_amax, i
     cudaError_t e = cudaMemsetAsync(d_hist, 0, (size_t)bins * sizeof(uint32_t), S(stream));
     if (e != cudaSuccess) return cuda_fail(e);
     if (n == 0) return AXQ_OK;
-    axq::hist_kernel<<<stream_grid(n, 256 * 8), 256, (size_t)bins * 4, S(stream)>>>(x, n, d_amax, bins, d_hist);
+    const int copies = bins <= 2048 ? 8 : (bins <= 4096 ? 4 : 2);   // per-warp sub-histograms
+    const size_t sm = (size_t)bins * copies * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(axq::hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        attr = true;
+    }
+    axq::hist_kernel<<<stream_grid(n / 4 + 1, 256 * 8), 256, sm, S(stream)>>>(x, n, d_amax, bins, copies, d_hist);
     return check_launch();
 }
 
@@ -333,7 +340,7 @@ axq_status axq_calib_percentile(const uint32_t* d_hist, int bins, int64_t n, con
     if (!d_hist || bins < 1 || n < 0 || !d_amax || p_num < 0 || p_den <= 0 || p_num > p_den ||
         bits < 2 || bits > 8 || (!d_calib_max && !d_scale))
         return AXQ_ERR_INVALID;
-    axq::percentile_kernel<<<1, 32, 0, S(stream)>>>(d_hist, bins, n, d_amax, p_num, p_den, bits, d_calib_max,
+    axq::percentile_kernel<<<1, 1024, 0, S(stream)>>>(d_hist, bins, n, d_amax, p_num, p_den, bits, d_calib_max,
                                                     d_scale);
     return check_launch();
 }

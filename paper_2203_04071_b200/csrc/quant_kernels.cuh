@@ -244,45 +244,88 @@ __global__ void quantize_rows_kernel(const float* __restrict__ W, int64_t rows, 
 }
 
 // Histogram of |x| over [0, amax] (A30): bin = min(trunc(fl(|x| / fl(amax / bins))), bins - 1).
-// Per-block shared counts, then one atomicAdd per non-empty bin (counts are integers: exact).
+// One shared sub-histogram per warp (ReLU / normal data pile into a few bins: per-warp copies
+// keep the shared atomics from serialising across the block), summed into one atomicAdd per
+// non-empty bin (counts are integers: exact, order-free).
 __global__ void hist_kernel(const float* __restrict__ x, int64_t n, const float* __restrict__ d_amax,
-                            int bins, unsigned int* __restrict__ hist) {
+                            int bins, int copies, unsigned int* __restrict__ hist) {
     extern __shared__ unsigned int hs[];
-    for (int b = threadIdx.x; b < bins; b += blockDim.x) hs[b] = 0u;
+    for (int b = threadIdx.x; b < bins * copies; b += blockDim.x) hs[b] = 0u;
     __syncthreads();
     const float a = *d_amax;
+    unsigned int* mine = hs + (size_t)((threadIdx.x >> 5) % copies) * bins;
     if (a > 0.f) {
         const float w = __fdiv_rn(a, (float)bins);
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-            const float t = div_rn_nz(fabsf(x[i]), w);
-            int b = (int)t;
-            b = b > bins - 1 ? bins - 1 : b;
-            atomicAdd(hs + b, 1u);
+        const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+        const int64_t n4 = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) ? n / 4 : 0;
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += gs) {
+            const float4 v = __ldcs(x4 + i);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int b = (int)div_rn_nz(fabsf(vv[j]), w);
+                atomicAdd(mine + (b > bins - 1 ? bins - 1 : b), 1u);
+            }
+        }
+        for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += gs) {
+            const int b = (int)div_rn_nz(fabsf(x[i]), w);
+            atomicAdd(mine + (b > bins - 1 ? bins - 1 : b), 1u);
         }
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < bins; b += blockDim.x)
-        if (hs[b]) atomicAdd(hist + b, hs[b]);
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) {
+        unsigned int t = 0;
+        for (int c = 0; c < copies; ++c) t += hs[(size_t)c * bins + b];
+        if (t) atomicAdd(hist + b, t);
+    }
 }
 
 // calib_max = fl((i + 1) * w) for the first bin i with cum * p_den >= n * p_num; s = calib_max / qmax
-// (0 -> 1).  One warp: per-lane partial sums of 64-bin chunks, then a serial walk (untimed).
+// (0 -> 1).  One block: each thread owns a contiguous run of bins; a block-wide exclusive scan
+// of the run totals gives every bin's cumulative count; the first crossing wins (atomicMin).
 __global__ void percentile_kernel(const unsigned int* __restrict__ hist, int bins, int64_t n,
                                   const float* __restrict__ d_amax, int64_t p_num, int64_t p_den,
                                   int bits, float* __restrict__ d_calib_max, float* __restrict__ d_scale) {
-    if (threadIdx.x != 0) return;
+    __shared__ long long wsum[32];
+    __shared__ int first;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (bins + nt - 1) / nt, b0 = tid * per, b1 = min(bins, b0 + per);
+    long long run = 0;
+    for (int b = b0; b < b1; ++b) run += hist[b];
+    // inclusive warp scan, then across warps
+    long long inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    if (tid == 0) first = bins - 1;
+    __syncthreads();
+    if (wid == 0) {
+        long long v = lane < (nt >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane < (nt >> 5)) wsum[lane] = v;
+    }
+    __syncthreads();
+    long long cum = inc - run + (wid > 0 ? wsum[wid - 1] : 0);   // count before bin b0
+    for (int b = b0; b < b1; ++b) {
+        cum += hist[b];
+        if (cum * p_den >= n * p_num) {
+            atomicMin(&first, b);
+            break;
+        }
+    }
+    __syncthreads();
+    if (tid != 0) return;
     const float a = *d_amax;
     float cm = 0.f;
-    if (a > 0.f && n > 0) {
-        const float w = __fdiv_rn(a, (float)bins);
-        int64_t cum = 0;
-        int hit = bins - 1;
-        for (int b = 0; b < bins; ++b) {
-            cum += hist[b];
-            if (cum * p_den >= n * p_num) { hit = b; break; }
-        }
-        cm = __fmul_rn((float)(hit + 1), w);
-    }
+    if (a > 0.f && n > 0) cm = __fmul_rn((float)(first + 1), __fdiv_rn(a, (float)bins));
     if (d_calib_max) *d_calib_max = cm;
     if (d_scale) *d_scale = (cm == 0.f) ? 1.0f : __fdiv_rn(cm, qmax_of(bits));
 }
