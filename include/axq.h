@@ -36,7 +36,7 @@ typedef enum {
     AXQ_ERR_INVALID = 1,     /* null pointer, extent < 0, bad leading dimension, bits not in
                                 [2,8], misaligned pointer where alignment is documented */
     AXQ_ERR_OVERFLOW = 2,    /* K * max|LUT| >= 2^31: an int32 accumulator could overflow */
-    AXQ_ERR_UNSUPPORTED = 3, /* a documented-but-unimplemented case (e.g. groups > 1) */
+    AXQ_ERR_UNSUPPORTED = 3, /* a documented-but-unimplemented case (e.g. groups > 1 on _wp) */
     AXQ_ERR_CUDA = 4         /* a CUDA call failed; see axq_last_cuda_error() */
 } axq_status;
 
@@ -183,7 +183,12 @@ axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int
  * where x(...) = X value inside the image and 0 at a padded tap -- the 0 is still looked
  * up (A11), exactly as the zero entries of the paper's im2col matrix are multiplied.
  * X: int8 NHWC [N][H][W][C];  Wt: int8 [C_out][R][S][C] (KRSC);  Y: int32 NHWC
- * [N][H_out][W_out][C_out].  groups must be 1 (others: AXQ_ERR_UNSUPPORTED).
+ * [N][H_out][W_out][C_out].
+ * groups = G > 1 (NEXT-3: grouped and depthwise convolution): C and C_out divisible by G,
+ *   Wt is [C_out][R][S][C/G], output channel co reads input channels g*C/G .. (g+1)*C/G - 1
+ *   with g = co / (C_out/G); the sum runs over those C/G channels only.  c_valid must be 0.
+ *   Runs on a resident-table kernel (a grouped layer has too few lookups per output to
+ *   amortise packed tables); the _wp entry points require groups == 1.
  * ------------------------------------------------------------------------------- */
 typedef struct axq_conv_desc {
     int64_t N, H, W, C;       /* input (C = channels as stored, i.e. the NHWC row length) */

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "lut_p4_args.h"
+#include "gconv.cuh"
 #include "lstm_rec_args.h"
 #include "mm_launch.h"
 #include "glue_kernels.cuh"
@@ -500,6 +501,78 @@ axq_status axq_conv2d_out_hw(const axq_conv_desc* d, int64_t* Ho, int64_t* Wo) {
     return AXQ_OK;
 }
 
+// groups > 1 (NEXT-3): grouped / depthwise conv on the resident-table kernel (gconv.cuh)
+static axq_status gconv_run(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt, axq_lut_t lut,
+                            const axq_epilogue* ep, int32_t* Y, cudaStream_t st) {
+    if (d->groups < 1 || d->C % d->groups || d->K % d->groups) return AXQ_ERR_INVALID;
+    if (d->c_valid != 0 && d->c_valid != d->C) return AXQ_ERR_UNSUPPORTED;
+    int64_t Ho, Wo;
+    axq_status s = axq_conv2d_out_hw(d, &Ho, &Wo);
+    if (s != AXQ_OK) return s;
+    if (Ho <= 0 || Wo <= 0) return AXQ_ERR_INVALID;
+    s = check_lut(lut);
+    if (s != AXQ_OK) return s;
+    s = overflow_guard(lut, d->R * d->S * (d->C / d->groups));
+    if (s != AXQ_OK) return s;
+    if (d->N > 0 && d->K > 0 && (!X || !Wt)) return AXQ_ERR_INVALID;
+    if (d->H * d->W * d->C >= (int64_t)1 << 31 || Ho * Wo >= (int64_t)1 << 31) return AXQ_ERR_INVALID;
+    if (d->N * Ho * Wo >= (int64_t)1 << 31) return AXQ_ERR_UNSUPPORTED;   // 32-bit pixel indexing
+    axq::GConvArgs a{};
+    a.X = X; a.W = Wt; a.M = d->N * Ho * Wo;
+    a.N = (int)d->N; a.H = (int)d->H; a.Wd = (int)d->W; a.C = (int)d->C; a.K = (int)d->K;
+    a.R = (int)d->R; a.S = (int)d->S; a.G = (int)d->groups; a.Ho = (int)Ho; a.Wo = (int)Wo;
+    a.sh = (int)d->stride_h; a.sw = (int)d->stride_w; a.ph = (int)d->pad_h; a.pw = (int)d->pad_w;
+    a.dh = (int)d->dil_h; a.dw = (int)d->dil_w;
+    a.table = lut->d_table;
+    a.table_bytes = lut->table_bytes;
+    if (ep) {
+        s = check_epilogue(ep, d->K, true);
+        if (s != AXQ_OK) return s;
+        a.ep = to_epi(ep, !ep->y_nhwc, Ho * Wo);
+        a.C_out = nullptr;
+    } else {
+        if (!Y) return AXQ_ERR_INVALID;
+        a.C_out = Y;
+    }
+    if (a.M == 0 || a.K == 0) return AXQ_OK;
+    const int64_t cin_g = d->C / d->groups, cout_g = d->K / d->groups;
+    if (cin_g % 4 == 0 && cin_g >= 16 && lut->repr != AXQ_LUT_I32 &&
+        (reinterpret_cast<uintptr_t>(X) & 3) == 0) {
+        // wide groups: one dense implicit-im2col LUT-GEMM per group on the v1 kernel, the group's
+        // channels addressed through the pixel stride (cs) and the outputs through offsets
+        const int64_t Kg = d->R * d->S * cin_g, hw = Ho * Wo;
+        for (int64_t g = 0; g < d->groups; ++g) {
+            axq::MMArgs p{};
+            p.A = X + g * cin_g; p.lda = 0; p.W = Wt + g * cout_g * Kg; p.ldw = Kg;
+            p.M = a.M; p.N = cout_g; p.K = Kg;
+            p.H = a.H; p.Wd = a.Wd; p.C = (int)cin_g; p.cs = a.C; p.Ho = a.Ho; p.Wo = a.Wo;
+            p.S = a.S; p.sh = a.sh; p.sw = a.sw; p.ph = a.ph; p.pw = a.pw; p.dh = a.dh; p.dw = a.dw;
+            fill_common(p, lut);
+            const int loader = (cin_g % 16 == 0 && aligned16(X) && (a.C % 16) == 0) ? axq::LOAD_CONV
+                             : (Kg <= 4 * axq::MAX_TAP_GROUPS && d->R * d->dil_h < 256 && d->S * d->dil_w < 256)
+                                   ? axq::LOAD_CONV_C4 : axq::LOAD_CONV_BYTES;
+            axq_status r;
+            if (ep) {
+                axq::EpiArgs e = a.ep;
+                const int64_t off = g * cout_g;
+                if (e.y) e.y += e.y_nchw ? off * hw : off;
+                if (e.y_nchw) e.nchw_ld = d->K;
+                if (e.bias) e.bias += off;
+                if (e.residual) e.residual += off;
+                if (e.q) e.q += off;
+                if (e.sw_ch) e.sw_ch += off;
+                r = run_mm(p, loader, lut, &e, ep->workspace, nullptr, 0, st);
+            } else {
+                r = run_mm(p, loader, lut, nullptr, nullptr, Y + g * cout_g, d->K, st);
+            }
+            if (r != AXQ_OK) return r;
+        }
+        return AXQ_OK;
+    }
+    const int rc = axq::launch_gconv(lut->repr, a, st);
+    return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
+}
+
 static axq_status conv_setup(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
                              axq_lut_t lut, axq::MMArgs& p, int& loader) {
     if (!d) return AXQ_ERR_INVALID;
@@ -538,6 +611,7 @@ static axq_status conv_setup(const axq_conv_desc* d, const int8_t* X, const int8
 
 axq_status axq_lut_conv2d(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
                           axq_lut_t lut, int32_t* Y, void* stream) {
+    if (d && d->groups != 1) return gconv_run(d, X, Wt, lut, nullptr, Y, S(stream));
     axq::MMArgs p;
     int loader;
     axq_status s = conv_setup(d, X, Wt, lut, p, loader);
@@ -549,6 +623,10 @@ axq_status axq_lut_conv2d(const axq_conv_desc* d, const int8_t* X, const int8_t*
 
 axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8_t* Wt,
                              axq_lut_t lut, const axq_epilogue* ep, void* stream) {
+    if (d && d->groups != 1) {
+        if (!ep) return AXQ_ERR_INVALID;
+        return gconv_run(d, X, Wt, lut, ep, nullptr, S(stream));
+    }
     axq::MMArgs p;
     int loader;
     axq_status s = conv_setup(d, X, Wt, lut, p, loader);

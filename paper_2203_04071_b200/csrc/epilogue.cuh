@@ -26,6 +26,7 @@ struct EpiArgs {
     const float* s_out;     // device scalar
     int bits_out;
     const float* sw_ch;     // per-output-channel weight scales [N] or null (NEXT-1, A32)
+    int64_t nchw_ld;        // NCHW: channels per image (0 -> N; a group's slice: all channels)
 };
 
 // The dequantization factor of column n: fl(s_a * s_w) (per tensor, precomputed as sc) or
@@ -62,7 +63,7 @@ __device__ __forceinline__ void epi_store(float v, int64_t m, int64_t n, int64_t
     if (e.y) {
         if (e.y_nchw) {
             const int64_t img = m / e.hw, pix = m - img * e.hw;
-            __stcs(e.y + (img * N + n) * e.hw + pix, v);
+            __stcs(e.y + (img * (e.nchw_ld ? e.nchw_ld : N) + n) * e.hw + pix, v);
         } else {
             e.y[m * e.ldy + n] = v;
         }

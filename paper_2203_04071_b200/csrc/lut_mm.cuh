@@ -48,6 +48,7 @@ struct MMArgs {
     int64_t M, N, K;
     // conv geometry
     int H, Wd, C, Ho, Wo, S, sh, sw, ph, pw, dh, dw;
+    int cs;             // conv: NHWC pixel stride in channels (0 -> C; grouped conv: all C)
     const void* table;  // device table (representation-specific layout, [uw][ua])
     int table_bytes;
     int32_t t00;        // LUT[0][0] (value of one storage-padding lookup)
@@ -96,7 +97,7 @@ __device__ __forceinline__ RowInfo make_row(const MMArgs& p, int64_t m) {
         int64_t img = mm / hw;
         int64_t rem = mm - img * hw;
         int ho = (int)(rem / p.Wo), wo = (int)(rem - (int64_t)ho * p.Wo);
-        ri.base = img * (int64_t)p.H * p.Wd * p.C;
+        ri.base = img * (int64_t)p.H * p.Wd * (p.cs ? p.cs : p.C);
         ri.hb = ho * p.sh - p.ph;
         ri.wb = wo * p.sw - p.pw;
     }
@@ -136,7 +137,7 @@ __device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int6
         int r = rs / p.S, s = rs - r * p.S;
         int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
         if (ri.valid && k0 < p.K && hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
-            v = ldg16(p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c0);
+            v = ldg16(p.A + ri.base + ((int64_t)hi * p.Wd + wi) * (p.cs ? p.cs : p.C) + c0);
         return v;
     } else if constexpr (LOADER == LOAD_CONV_C4) {
         // C % 4 == 0 (small C, e.g. the padded network input): each 4-byte group of the chunk
@@ -153,7 +154,7 @@ __device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int6
                     const int wi = ri.wb + (int)((tv[j] >> 8) & 0xff);
                     if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
                         w[j] = __ldg(reinterpret_cast<const uint32_t*>(
-                            p.A + ri.base + ((int64_t)hi * p.Wd + wi) * p.C + (tv[j] >> 16)));
+                            p.A + ri.base + ((int64_t)hi * p.Wd + wi) * (p.cs ? p.cs : p.C) + (tv[j] >> 16)));
                 }
             }
             v = make_uint4(w[0], w[1], w[2], w[3]);
@@ -170,7 +171,7 @@ __device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int6
                     int r = rs / p.S, s = rs - r * p.S;
                     int hi = ri.hb + r * p.dh, wi = ri.wb + s * p.dw;
                     if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
-                        w[j >> 2] |= (uint32_t)(uint8_t)p.A[ri.base + ((int64_t)hi * p.Wd + wi) * p.C + c]
+                        w[j >> 2] |= (uint32_t)(uint8_t)p.A[ri.base + ((int64_t)hi * p.Wd + wi) * (p.cs ? p.cs : p.C) + c]
                                      << (8 * (j & 3));
                 }
             }

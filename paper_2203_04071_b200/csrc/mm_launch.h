@@ -40,6 +40,8 @@ int launch_p4(const P4Args& a, cudaStream_t st);
 int launch_p4t(const P4Args& a, cudaStream_t st);   // tcgen05 exact part, 32 warps (lut_p4t.cuh)
 int launch_p4w(const P4Args& a, cudaStream_t st);   // warp-specialised P4T (lut_p4w.cuh)
 struct LstmRecArgs;
+struct GConvArgs;
+int launch_gconv(int repr, const GConvArgs& a, cudaStream_t st);   // gconv.cuh (groups > 1)
 int launch_lstm_rec(const LstmRecArgs& a, int sms, cudaStream_t st);   // lstm_rec.cuh
 void p4t_plan(int64_t M, int64_t N, int64_t Kp, int half, int bm, int sms, bool can_split, int& splits, int& sps);
 void p4_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& rpl, int& splits,

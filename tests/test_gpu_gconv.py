@@ -1,0 +1,107 @@
+"""GPU parity of grouped and depthwise approximate convolution (NEXT-3; P:119 groups, the conv
+of Eq. 2) against the oracle's direct seven-loop conv with groups: raw int32 bit-exact
+for every table representation, and the fused dequantizing epilogue."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def ax():
+    from paper_2203_04071_b200 import _lib
+    _lib.load()
+    return _lib
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _table(kind):
+    if kind == "randerr":
+        return datagen.lut_randerr(8, 0, 2), 8
+    if kind == "int16":
+        return datagen.random_lut(33, 8), 8                                     # |T| <= 2^14
+    if kind == "int32":
+        return np.random.default_rng(41).integers(-10**6, 10**6, 1 << 16).astype(np.int32), 8
+    return datagen.lut_randerr(4, 4, 14), 4
+
+
+# N, C, H, W, K, R, S, stride, pad, dil, groups
+CASES = [(2, 32, 10, 9, 32, 3, 3, 1, 1, 1, 32),     # depthwise 3x3
+         (1, 16, 12, 12, 32, 3, 3, 2, 1, 1, 16),    # depthwise, channel multiplier 2, stride 2
+         (2, 24, 8, 11, 36, 1, 1, 1, 0, 1, 3),      # grouped 1x1 (ShuffleNet-like, G = 3)
+         (1, 32, 9, 9, 64, 5, 5, 1, 2, 1, 4),       # grouped 5x5
+         (1, 8, 13, 7, 8, 3, 3, 1, 2, 2, 8),        # depthwise, dilation 2
+         (3, 12, 5, 6, 12, 3, 1, 2, 0, 1, 2),       # rectangular kernel, no padding
+         (2, 64, 10, 10, 64, 3, 3, 1, 1, 1, 2),     # wide groups: per-group dense GEMM (16-B loads)
+         (1, 48, 7, 9, 96, 1, 1, 2, 0, 1, 3),       # wide groups, 1x1 stride 2
+         (1, 80, 6, 6, 40, 3, 3, 1, 1, 1, 4)]       # wide groups, C/G = 20 (4-byte loads)
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("kind", ["randerr", "int16", "int32", "b4"])
+def test_grouped_conv_raw(ax, case, kind):
+    Nb, C, H, Wd, K, R, S, st, pd, dl, G = case
+    T, bits = _table(kind)
+    X = datagen.random_int8(300 + C + G, (Nb, C, H, Wd), bits)
+    Wt = datagen.random_int8(400 + K + G, (K, C // G, R, S), bits)
+    ref = oracle.lut_conv2d(X, Wt, T, bits, (st, st), (pd, pd), (dl, dl), groups=G)
+    lut = ax.Lut(bits, T)
+    d = ax.conv_desc(Nb, H, Wd, C, K, R, S, (st, st), (pd, pd), (dl, dl), groups=G)
+    Ho, Wo = ax.axq_conv2d_out_hw(d)
+    Y = torch.empty(Nb, Ho, Wo, K, dtype=torch.int32, device=DEV)
+    ax.axq_lut_conv2d(d, _t(X.transpose(0, 2, 3, 1)), _t(Wt.transpose(0, 2, 3, 1)), lut, Y)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
+
+
+def test_depthwise_fused_nchw(ax):
+    Nb, C, H, Wd = 4, 64, 14, 14
+    x = np.maximum(datagen.normal(35, 1, (Nb, C, H, Wd)), 0).astype(np.float32)
+    rng = np.random.default_rng(42)
+    w = (rng.standard_normal((C, 1, 3, 3)) * 0.3).astype(np.float32)
+    b = rng.standard_normal(C).astype(np.float32)
+    T = datagen.lut_randerr(8, 0, 2)
+    qa, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(w, 8)
+    acc = oracle.lut_conv2d(qa, qw, T, 8, (1, 1), (1, 1), groups=C)
+    ref = oracle.dequantize(acc, sa, sw, b, channel_axis=1)
+    lut = ax.Lut(8, T)
+    d = ax.conv_desc(Nb, H, Wd, C, C, 3, 3, (1, 1), (1, 1), groups=C)
+    y = torch.empty(Nb, C, H, Wd, device=DEV)
+    dsa, dsw, db = torch.tensor([sa], device=DEV), torch.tensor([sw], device=DEV), _t(b)
+    ep = ax.make_epilogue(dsa, dsw, bias=db, y=y)
+    ax.axq_lut_conv2d_ep(d, _t(qa.transpose(0, 2, 3, 1)), _t(qw.transpose(0, 2, 3, 1)), lut, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), ref)
+
+
+def test_wide_groups_fused_nchw_per_channel(ax):
+    """Per-group dense path with the fused epilogue: NCHW output slices, bias and per-channel
+    weight scales offset per group, split-K workspace reused across groups."""
+    Nb, C, H, Wd, K, G = 2, 64, 12, 12, 96, 2
+    rng = np.random.default_rng(50)
+    X = datagen.random_int8(51, (Nb, C, H, Wd))
+    Wt = datagen.random_int8(52, (K, C // G, 3, 3))
+    T = datagen.lut_randerr(8, 0, 2)
+    s_w = rng.uniform(1e-4, 1e-2, K).astype(np.float32)
+    b = rng.standard_normal(K).astype(np.float32)
+    s_a = np.float32(0.02)
+    ref = oracle.dequantize_pc(oracle.lut_conv2d(X, Wt, T, 8, (1, 1), (1, 1), groups=G), s_a, s_w, b,
+                               channel_axis=1)
+    lut = ax.Lut(8, T)
+    d = ax.conv_desc(Nb, H, Wd, C, K, 3, 3, (1, 1), (1, 1), groups=G)
+    y = torch.empty(Nb, K, H, Wd, device=DEV)
+    ws = torch.zeros(Nb * H * Wd * K, dtype=torch.int32, device=DEV)
+    dsa, dsw, dones, db = torch.tensor([s_a], device=DEV), _t(s_w), torch.ones(1, device=DEV), _t(b)
+    ep = ax.make_epilogue(dsa, dones, bias=db, y=y, workspace=ws, d_scale_w_ch=dsw)
+    ax.axq_lut_conv2d_ep(d, _t(X.transpose(0, 2, 3, 1)), _t(Wt.transpose(0, 2, 3, 1)), lut, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), ref)
