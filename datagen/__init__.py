@@ -143,6 +143,13 @@ def random_int8(seed: int, shape, bits: int = 8, full_range: bool = True) -> np.
                                                 dtype=np.int64).astype(np.int8)
 
 
+def random_int16(seed: int, shape, bits: int) -> np.ndarray:
+    """Uniform b-bit signed codes in [-(2^(b-1) - 1), 2^(b-1) - 1] as int16 (NEXT-2 operands)."""
+    q = (1 << (bits - 1)) - 1
+    return np.random.default_rng(seed).integers(-q, q, size=shape, endpoint=True,
+                                                dtype=np.int64).astype(np.int16)
+
+
 def random_lut(seed: int, bits: int) -> np.ndarray:
     """A fully random ACU (no structure at all) for parity cases: every entry in
     [-2^(2b-2), 2^(2b-2)], so int16/int8 table representations are exercised where they fit."""

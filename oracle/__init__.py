@@ -64,6 +64,10 @@ def lib():
         L.orc_hist_calib.restype = i64
         L.orc_dequantize_pc.argtypes = [i64, vp, f32, vp, vp, i64, i64, vp]
         L.orc_dequantize_pc.restype = None
+        L.orc_quantize16.argtypes = [vp, i64, f32, i32, vp]
+        L.orc_quantize16.restype = None
+        L.orc_lut_gemm16.argtypes = [i64, i64, i64, vp, vp, i32, vp, vp]
+        L.orc_lut_gemm16.restype = i64
         L.orc_set_threads.argtypes = [i32]
         L.orc_set_threads.restype = None
         L.orc_max_threads.argtypes = []
@@ -246,3 +250,28 @@ def dequantize_pc(acc, s_a, s_w, bias=None, channel_axis: int = -1) -> np.ndarra
     lib().orc_dequantize_pc(acc.size, _p(acc), float(np.float32(s_a)), _p(sw),
                             None if b is None else _p(b), nch, inner, _p(y))
     return y
+
+
+# ---- NEXT-2: wide ACUs (b = 9..12) with int16 operand codes ----
+
+def quantize16(x, s, bits: int) -> np.ndarray:
+    x = _c(x, np.float32)
+    q = np.empty(x.shape, np.int16)
+    lib().orc_quantize16(_p(x), x.size, float(np.float32(s)), int(bits), _p(q))
+    return q
+
+
+def lut_gemm16(A, W, lut, bits: int) -> np.ndarray:
+    """A int16 [M][K], W int16 [N][K] codes of b <= 16 bits -> int32 [M][N]."""
+    A = _c(A, np.int16)
+    W = _c(W, np.int16)
+    T = _c(lut, np.int32)
+    assert T.size == 1 << (2 * bits)
+    M, K = A.shape
+    N, K2 = W.shape
+    assert K == K2
+    C = np.empty((M, N), np.int32)
+    bad = lib().orc_lut_gemm16(M, N, K, _p(A), _p(W), int(bits), _p(T), _p(C))
+    if bad:
+        raise OverflowError("%d outputs exceed int32" % bad)
+    return C

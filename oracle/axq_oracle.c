@@ -219,3 +219,36 @@ void orc_dequantize_pc(int64_t count, const int32_t* acc, float s_a, const float
         y[i] = v;
     }
 }
+
+/* ===================== NEXT-2: wide ACUs (b = 9..12) =====================
+ * The paper also emulates 12-bit multipliers (mul12s, "one with 12-bit precision").
+ * Codes no longer fit int8, so operands are int16 two's-complement codes; everything else is
+ * O4 / O5 unchanged: q = clamp(rint(x / s)) with qmax = 2^(b-1) - 1, and
+ * acc = sum_k T[(u(a) << b) | u(w)] with u = the b-bit pattern. */
+void orc_quantize16(const float* x, int64_t n, float s, int bits, int16_t* q) {
+    float qmax = (float)((1 << (bits - 1)) - 1);
+    for (int64_t i = 0; i < n; ++i) {
+        float t = x[i] / s;
+        if (t > qmax) t = qmax;
+        if (t < -qmax) t = -qmax;
+        q[i] = (int16_t)rintf(t);
+    }
+}
+
+int64_t orc_lut_gemm16(int64_t M, int64_t N, int64_t K, const int16_t* A, const int16_t* W,
+                       int bits, const int32_t* T, int32_t* C) {
+    int64_t bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+    for (int64_t m = 0; m < M; ++m) {
+        for (int64_t n = 0; n < N; ++n) {
+            int64_t acc = 0;
+            for (int64_t k = 0; k < K; ++k) {
+                int64_t idx = (ubits(A[m * K + k], bits) << bits) | ubits(W[n * K + k], bits);
+                acc += T[idx];
+            }
+            if (acc > INT32_MAX || acc < INT32_MIN) bad++;
+            C[m * N + n] = (int32_t)acc;
+        }
+    }
+    return bad;
+}
