@@ -45,7 +45,10 @@ typedef enum {
     AXQ_LUT_DELTA8 = 0, /* int8 E = LUT - a*w, shared-memory resident (64 KiB), exact part
                            added with dp4a */
     AXQ_LUT_I16 = 1,    /* int16 LUT values, shared-memory resident (128 KiB) */
-    AXQ_LUT_I32 = 2     /* int32 values read through L1/L2 (correctness path) */
+    AXQ_LUT_I32 = 2,    /* int32 values read through L1/L2 (correctness path) */
+    AXQ_LUT_WIDE16 = 3, /* b = 9..12 (NEXT-2): int16 E = LUT - a*w, [uw][ua] in b-bit patterns,
+                           read through L1/L2 (2^(2b+1) bytes: 32 MiB at b = 12) */
+    AXQ_LUT_WIDE32 = 4  /* b = 9..12 with E beyond int16: int32 LUT values through L1/L2 */
 } axq_lut_repr;
 
 typedef struct axq_lut* axq_lut_t;
@@ -63,7 +66,9 @@ int axq_version(void);
  *
  * axq_lut_create: host_table is a HOST int32 array of 2^(2*bits) entries, entry
  *   (ua << bits) | uw = ACU(a, w), ua / uw the b-bit two's-complement patterns of the
- *   activation a and the weight w (first index = ACTIVATION, A8).  bits in [2,8].
+ *   activation a and the weight w (first index = ACTIVATION, A8).  bits in [2,12];
+ *   bits 9..12 (NEXT-2, the paper's 12-bit multipliers) give a WIDE16 / WIDE32 handle that
+ *   only axq_lut_gemm16 accepts (the int8 entry points return AXQ_ERR_UNSUPPORTED).
  *   The library copies the table, picks the device representation (axq_lut_repr),
  *   uploads it to the current device and synchronizes.  *out receives the handle.
  * axq_lut_destroy: frees the handle (synchronizes the device first).  NULL is a no-op.
@@ -306,6 +311,21 @@ axq_status axq_lstm_cell(int64_t B, int64_t Hd, const float* gates_ih, const flo
  *   [B][H] (c_{T-1}); workspace: device bytes >= 2*B*H + 256, no contents required.
  *   Needs H % 16 == 0 and a grid of ceil(H / #SMs) * ceil(B / 32) <= 16 warps per SM that
  *   fits co-resident (else AXQ_ERR_UNSUPPORTED: use the per-step calls). */
+/* ---------------------------------------------------------------------------------
+ * NEXT-2: wide ACUs (b = 9..12, "one with 12-bit precision") with int16
+ * operand codes.
+ * axq_quantize16: q = clamp(rint(x / *d_scale)) to +-(2^(bits-1)-1) as int16 (axq_quantize's
+ *   rule, A1-A3), bits in [2, 16].  (axq_scale accepts bits up to 16.)
+ * axq_lut_gemm16: acc[m][n] = sum_k LUT[A[m*lda+k]][W[n*ldw+k]] with int16 codes and a WIDE16 /
+ *   WIDE32 handle; ep NULL -> raw int32 C [M][ldc], else the fused epilogue of axq_lut_gemm_dq
+ *   (row layout; no workspace used).  Guard: K * max|LUT| < 2^31 (else AXQ_ERR_OVERFLOW).
+ * ------------------------------------------------------------------------------- */
+axq_status axq_quantize16(const float* x, int64_t n, const float* d_scale, int bits, int16_t* q,
+                          void* stream);
+axq_status axq_lut_gemm16(int64_t M, int64_t N, int64_t K, const int16_t* A, int64_t lda,
+                          const int16_t* W, int64_t ldw, axq_lut_t lut, const axq_epilogue* ep,
+                          int32_t* C, int64_t ldc, void* stream);
+
 axq_status axq_lstm_recurrent(int64_t T, int64_t B, int64_t H, const float* gates_ih,
                               const int8_t* qw_hh, const float* d_scale_w_hh, const float* b_hh,
                               const float* d_scale_h, int bits, axq_lut_t lut, float* hs,

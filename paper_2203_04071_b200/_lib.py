@@ -16,7 +16,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libaxq.so"
 
 AXQ_OK, AXQ_ERR_INVALID, AXQ_ERR_OVERFLOW, AXQ_ERR_UNSUPPORTED, AXQ_ERR_CUDA = range(5)
-REPR_NAMES = {0: "delta8", 1: "int16", 2: "int32"}
+REPR_NAMES = {0: "delta8", 1: "int16", 2: "int32", 3: "wide16", 4: "wide32"}
 
 EXPORTED = [
     "axq_last_cuda_error", "axq_status_string", "axq_version",
@@ -29,7 +29,7 @@ EXPORTED = [
     "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
     "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_lstm_recurrent",
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
-    "axq_calib_percentile", "axq_maxpool2d_nhwc_f32",
+    "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
 ]
 
 
@@ -98,6 +98,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_destroy": ([vp], i32),
         "axq_wpack_kernel": ([i32], i32),
         "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
+        "axq_quantize16": ([vp, i64, vp, i32, vp, vp], i32),
+        "axq_lut_gemm16": ([i64, i64, i64, vp, i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_maxpool2d_nhwc_f32": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp], i32),
         "axq_scale_vec": ([vp, i64, i32, vp, vp], i32),
         "axq_quantize_rows": ([vp, i64, i64, vp, i32, vp, vp], i32),
@@ -461,3 +463,20 @@ def axq_maxpool2d_nhwc_f32(x, R: int, S: int, stride: int, pad: int, y, stream=N
     N, H, W, C = x.shape
     _check("axq_maxpool2d_nhwc_f32", load().axq_maxpool2d_nhwc_f32(
         _ptr(x), N, H, W, C, R, S, stride, pad, _ptr(y), _stream(stream)))
+
+
+# ---- NEXT-2: wide ACUs (b = 9..12) with int16 codes ----
+def axq_quantize16(x, d_scale, bits: int, q, stream=None) -> None:
+    assert q.dtype == __import__("torch").int16 and q.numel() == x.numel()
+    _check("axq_quantize16", load().axq_quantize16(_ptr(x), x.numel(), _ptr(d_scale), int(bits), _ptr(q),
+                                                   _stream(stream)))
+
+
+def axq_lut_gemm16(A, W, lut: Lut, ep: axq_epilogue | None = None, C=None, stream=None) -> None:
+    """A int16 [M][K], W int16 [N][K] codes; raw int32 C [M][N] or the fused epilogue."""
+    M, K = A.shape
+    N = W.shape[0]
+    _check("axq_lut_gemm16", load().axq_lut_gemm16(
+        M, N, K, _ptr(A), A.stride(0), _ptr(W), W.stride(0), lut.handle,
+        ctypes.byref(ep) if ep is not None else None, _ptr(C), C.stride(0) if C is not None else 0,
+        _stream(stream)))

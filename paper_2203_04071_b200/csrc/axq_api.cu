@@ -13,6 +13,7 @@
 
 #include "lut_p4_args.h"
 #include "gconv.cuh"
+#include "wide_args.h"
 #include "lstm_rec_args.h"
 #include "mm_launch.h"
 #include "glue_kernels.cuh"
@@ -151,6 +152,7 @@ int64_t pick_k_split(int64_t M, int64_t N, int64_t K, const Cfg& c, bool allow) 
 
 axq_status check_lut(axq_lut_t lut) {
     if (!lut || !lut->d_table) return AXQ_ERR_INVALID;
+    if (lut->bits > 8) return AXQ_ERR_UNSUPPORTED;   // wide tables: axq_lut_gemm16 only
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev != lut->device) return AXQ_ERR_INVALID;
@@ -191,9 +193,60 @@ int axq_version(void) { return 100; }
 // ---------------------------------------------------------------------------------------
 // ACU table
 // ---------------------------------------------------------------------------------------
+// NEXT-2: wide ACUs (b = 9..12).  Device layout [uw][ua] in the b-bit pattern space; int16 E =
+// LUT - a*w when every E fits (delta16), else int32 LUT values.
+static axq_status lut_create_wide(int bits, const int32_t* host_table, axq_lut_t* out) {
+    const int64_t n = (int64_t)1 << bits, mask = n - 1;
+    int64_t tmin = INT32_MAX, tmax = INT32_MIN;
+    bool d16 = true;
+    for (int64_t ua = 0; ua < n; ++ua)
+        for (int64_t uw = 0; uw < n; ++uw) {
+            const int64_t v = host_table[(ua << bits) | uw];
+            tmin = std::min(tmin, v);
+            tmax = std::max(tmax, v);
+            const int64_t a = ua >= n / 2 ? ua - n : ua, w = uw >= n / 2 ? uw - n : uw;
+            const int64_t e = v - a * w;
+            if (e < INT16_MIN || e > INT16_MAX) d16 = false;
+        }
+    const int esz = d16 ? 2 : 4;
+    std::vector<uint8_t> dev_tab((size_t)(n * n) * esz);
+    for (int64_t uw = 0; uw < n; ++uw)
+        for (int64_t ua = 0; ua < n; ++ua) {
+            const int64_t a = ua >= n / 2 ? ua - n : ua, w = uw >= n / 2 ? uw - n : uw;
+            const int32_t v = host_table[(ua << bits) | uw];
+            const size_t idx = (size_t)((uw << bits) | ua);
+            if (d16) {
+                const int16_t e = (int16_t)(v - a * w);
+                std::memcpy(&dev_tab[idx * 2], &e, 2);
+            } else {
+                std::memcpy(&dev_tab[idx * 4], &v, 4);
+            }
+        }
+    (void)mask;
+    axq_lut* L = new axq_lut();
+    L->bits = bits;
+    L->repr = d16 ? AXQ_LUT_WIDE16 : AXQ_LUT_WIDE32;
+    cudaGetDevice(&L->device);
+    L->tmin = (int32_t)tmin;
+    L->tmax = (int32_t)tmax;
+    L->t00 = host_table[0];
+    L->absmax = std::max<int64_t>(std::llabs(tmin), std::llabs(tmax));
+    L->table_bytes = (int)std::min<size_t>(dev_tab.size(), (size_t)INT32_MAX);
+    cudaError_t e = cudaMalloc(&L->d_table, dev_tab.size());
+    if (e == cudaSuccess) e = cudaMemcpy(L->d_table, dev_tab.data(), dev_tab.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (L->d_table) cudaFree(L->d_table);
+        delete L;
+        return cuda_fail(e);
+    }
+    *out = L;
+    return AXQ_OK;
+}
+
 axq_status axq_lut_create(int bits, const int32_t* host_table, axq_lut_t* out) {
-    if (!out || !host_table || bits < 2 || bits > 8) return AXQ_ERR_INVALID;
+    if (!out || !host_table || bits < 2 || bits > 12) return AXQ_ERR_INVALID;
     *out = nullptr;
+    if (bits > 8) return lut_create_wide(bits, host_table, out);
     const int n = 1 << bits, mask = n - 1;
     int64_t tmin = INT32_MAX, tmax = INT32_MIN;
     bool delta_ok = true;
@@ -287,7 +340,7 @@ axq_status axq_amax(const float* x, int64_t n, float* d_amax, void* stream) {
 }
 
 axq_status axq_scale(const float* d_amax, int bits, float* d_scale, void* stream) {
-    if (!d_amax || !d_scale || bits < 2 || bits > 8) return AXQ_ERR_INVALID;
+    if (!d_amax || !d_scale || bits < 2 || bits > 16) return AXQ_ERR_INVALID;
     axq::scale_kernel<<<1, 1, 0, S(stream)>>>(d_amax, bits, d_scale);
     return check_launch();
 }
@@ -912,6 +965,43 @@ axq_status axq_lstm_cell(int64_t B, int64_t Hd, const float* gates_ih, const flo
     axq::lstm_cell_kernel<<<stream_grid(B * Hd, 256), 256, 0, S(stream)>>>(
         B, Hd, gates_ih, gates_hh, c, h_out, q_h, d_scale_h, q_h ? bits : 8);
     return check_launch();
+}
+
+// ---- NEXT-2: wide ACUs, int16 codes ----
+axq_status axq_quantize16(const float* x, int64_t n, const float* d_scale, int bits, int16_t* q,
+                          void* stream) {
+    if (n < 0 || !d_scale || bits < 2 || bits > 16 || (n > 0 && (!x || !q))) return AXQ_ERR_INVALID;
+    if (n == 0) return AXQ_OK;
+    const int rc = axq::launch_quantize16(x, n, d_scale, bits, q, sm_count(), S(stream));
+    return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
+}
+
+axq_status axq_lut_gemm16(int64_t M, int64_t N, int64_t K, const int16_t* A, int64_t lda,
+                          const int16_t* W, int64_t ldw, axq_lut_t lut, const axq_epilogue* ep,
+                          int32_t* C, int64_t ldc, void* stream) {
+    if (!lut || !lut->d_table || M < 0 || N < 0 || K < 0) return AXQ_ERR_INVALID;
+    if (lut->repr != AXQ_LUT_WIDE16 && lut->repr != AXQ_LUT_WIDE32) return AXQ_ERR_UNSUPPORTED;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != lut->device) return AXQ_ERR_INVALID;
+    if (M > 0 && N > 0 && K > 0 && (!A || !W || lda < K || ldw < K)) return AXQ_ERR_INVALID;
+    axq_status s = overflow_guard(lut, K);
+    if (s != AXQ_OK) return s;
+    axq::WideArgs a{};
+    a.A = A; a.lda = lda; a.W = W; a.ldw = ldw; a.M = M; a.N = N; a.K = K; a.bits = lut->bits;
+    a.table = lut->d_table; a.delta16 = lut->repr == AXQ_LUT_WIDE16;
+    if (ep) {
+        s = check_epilogue(ep, N, false);
+        if (s != AXQ_OK) return s;
+        a.ep = to_epi(ep, false, 0);
+    } else {
+        if (!C || ldc < N) return AXQ_ERR_INVALID;
+        a.C_out = C;
+        a.ldc = ldc;
+    }
+    if (M == 0 || N == 0) return AXQ_OK;
+    const int rc = axq::launch_wide(a, sm_count(), S(stream));
+    return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }
 
 axq_status axq_lstm_recurrent(int64_t T, int64_t B, int64_t H, const float* gates_ih,

@@ -41,6 +41,10 @@ int launch_p4t(const P4Args& a, cudaStream_t st);   // tcgen05 exact part, 32 wa
 int launch_p4w(const P4Args& a, cudaStream_t st);   // warp-specialised P4T (lut_p4w.cuh)
 struct LstmRecArgs;
 struct GConvArgs;
+struct WideArgs;
+int launch_wide(const WideArgs& a, int sms, cudaStream_t st);   // wide.cuh (NEXT-2)
+int launch_quantize16(const float* x, int64_t n, const float* d_scale, int bits, int16_t* q, int sms,
+                      cudaStream_t st);
 int launch_gconv(int repr, const GConvArgs& a, cudaStream_t st);   // gconv.cuh (groups > 1)
 int launch_lstm_rec(const LstmRecArgs& a, int sms, cudaStream_t st);   // lstm_rec.cuh
 void p4t_plan(int64_t M, int64_t N, int64_t Kp, int half, int bm, int sms, bool can_split, int& splits, int& sps);

@@ -60,7 +60,11 @@ def test_invalid_arguments_rejected_on_host(L):
     assert L.axq_lut_gemm(1, 1, 1, None, 1, None, 1, None, None, 1, None) == AXQ_ERR_INVALID
     assert L.axq_dequantize(4, 4, None, 4, None, None, None, None, 4, None) == AXQ_ERR_INVALID
     d = axq_conv_desc(1, 8, 8, 4, 4, 3, 3, 1, 1, 1, 1, 1, 1, 2)
-    assert L.axq_lut_conv2d(ctypes.byref(d), None, None, None, None, None) == AXQ_ERR_UNSUPPORTED
+    # groups > 1 is supported (NEXT-3): with no table handle the call is invalid, and a group
+    # count that does not divide the channels is invalid too
+    assert L.axq_lut_conv2d(ctypes.byref(d), None, None, None, None, None) == AXQ_ERR_INVALID
+    d3 = axq_conv_desc(1, 8, 8, 4, 4, 3, 3, 1, 1, 1, 1, 1, 1, 3)
+    assert L.axq_lut_conv2d(ctypes.byref(d3), None, None, None, None, None) == AXQ_ERR_INVALID
     ho, wo = ctypes.c_int64(), ctypes.c_int64()
     assert L.axq_conv2d_out_hw(ctypes.byref(d), ctypes.byref(ho), ctypes.byref(wo)) == AXQ_OK
     assert (ho.value, wo.value) == (8, 8)
