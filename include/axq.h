@@ -279,6 +279,15 @@ axq_status axq_epilogue_apply(int64_t M, int64_t N, const int32_t* acc, int64_t 
 axq_status axq_maxpool2d_nhwc_i8(const int8_t* x, int64_t N, int64_t H, int64_t W, int64_t C,
                                  int64_t R, int64_t S, int64_t stride, int64_t pad, int8_t* y,
                                  void* stream);
+/* axq_im2col_nhwc_i8: the explicit im2col matrix of P:119 from int8 NHWC codes X [N][H][W][C]
+ *   (only channels 0..c_valid-1 used; 0 = all): A[m][k], m = (img, ho, wo), k = (r*S + s)*cv + c
+ *   for k < K = R*S*cv, the code at (ho*stride_h - pad_h + r, wo*stride_w - pad_w + s) or 0 at a
+ *   padded tap; A[m][K..lda) = 0.  lda % 16 == 0, lda >= K, A 16-byte aligned.  Used for the
+ *   3-channel stem, whose implicit im2col would pad C to 4 (33 % more lookups): the matrix then
+ *   goes through axq_lut_gemm_wp with K = R*S*3. */
+axq_status axq_im2col_nhwc_i8(const int8_t* X, int64_t N, int64_t H, int64_t W, int64_t C, int64_t c_valid,
+                              int64_t R, int64_t S, int64_t stride_h, int64_t stride_w, int64_t pad_h,
+                              int64_t pad_w, int8_t* A, int64_t lda, void* stream);
 /* axq_maxpool2d_nhwc_f32: the same pooling on fp32 NHWC (used by the paper quantizer's
  *   calibration pass, where the pooled real values are histogrammed). */
 axq_status axq_maxpool2d_nhwc_f32(const float* x, int64_t N, int64_t H, int64_t W, int64_t C,

@@ -30,6 +30,7 @@ EXPORTED = [
     "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_lstm_recurrent",
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
+    "axq_im2col_nhwc_i8",
 ]
 
 
@@ -99,6 +100,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_kernel": ([i32], i32),
         "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
         "axq_quantize16": ([vp, i64, vp, i32, vp, vp], i32),
+        "axq_im2col_nhwc_i8": ([vp] + [i64] * 11 + [vp, i64, vp], i32),
         "axq_lut_gemm16": ([i64, i64, i64, vp, i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_maxpool2d_nhwc_f32": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp], i32),
         "axq_scale_vec": ([vp, i64, i32, vp, vp], i32),
@@ -480,3 +482,11 @@ def axq_lut_gemm16(A, W, lut: Lut, ep: axq_epilogue | None = None, C=None, strea
         M, N, K, _ptr(A), A.stride(0), _ptr(W), W.stride(0), lut.handle,
         ctypes.byref(ep) if ep is not None else None, _ptr(C), C.stride(0) if C is not None else 0,
         _stream(stream)))
+
+
+def axq_im2col_nhwc_i8(X, c_valid: int, R: int, S: int, stride, pad, A, stream=None) -> None:
+    """Explicit im2col of int8 NHWC codes into A [M][lda] (k = (r, s, c), zero padded)."""
+    N, H, W, C = X.shape
+    _check("axq_im2col_nhwc_i8", load().axq_im2col_nhwc_i8(
+        _ptr(X), N, H, W, C, int(c_valid), R, S, stride[0], stride[1], pad[0], pad[1], _ptr(A),
+        A.stride(0), _stream(stream)))

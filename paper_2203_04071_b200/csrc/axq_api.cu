@@ -929,6 +929,27 @@ axq_status axq_maxpool2d_nhwc_i8(const int8_t* x, int64_t N, int64_t H, int64_t 
     return check_launch();
 }
 
+axq_status axq_im2col_nhwc_i8(const int8_t* X, int64_t N, int64_t H, int64_t W, int64_t C, int64_t c_valid,
+                              int64_t R, int64_t Sz, int64_t stride_h, int64_t stride_w, int64_t pad_h,
+                              int64_t pad_w, int8_t* A, int64_t lda, void* stream) {
+    if (N < 0 || H <= 0 || W <= 0 || C <= 0 || R <= 0 || Sz <= 0 || stride_h <= 0 || stride_w <= 0 ||
+        pad_h < 0 || pad_w < 0)
+        return AXQ_ERR_INVALID;
+    const int64_t cv = c_valid ? c_valid : C;
+    const int64_t K = R * Sz * cv;
+    if (cv > C || lda < K || (lda & 15) || lda > 8192 || R > 255 || Sz > 255) return AXQ_ERR_INVALID;
+    const int64_t Ho = (H + 2 * pad_h - R) / stride_h + 1, Wo = (W + 2 * pad_w - Sz) / stride_w + 1;
+    if (Ho <= 0 || Wo <= 0) return AXQ_ERR_INVALID;
+    if (N == 0) return AXQ_OK;
+    if (!X || !A || (reinterpret_cast<uintptr_t>(A) & 15)) return AXQ_ERR_INVALID;
+    const int64_t M = N * Ho * Wo;
+    axq::im2col_nhwc_i8_kernel<<<stream_grid(M * (lda / 16), 256), 256, lda * 4, S(stream)>>>(
+        X, M, (int)H, (int)W, (int)C, (int)Ho, (int)Wo, (int)stride_h, (int)stride_w, (int)pad_h, (int)pad_w,
+        (int)Sz, (int)cv, (int)K, (int)lda, A);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? AXQ_OK : cuda_fail(e);
+}
+
 axq_status axq_maxpool2d_nhwc_f32(const float* x, int64_t N, int64_t H, int64_t W, int64_t C,
                                   int64_t R, int64_t Sz, int64_t stride, int64_t pad, float* y,
                                   void* stream) {

@@ -141,4 +141,44 @@ __global__ void lstm_cell_kernel(int64_t B, int64_t Hd, const float* __restrict_
     }
 }
 
+// ---- explicit im2col of int8 NHWC codes (the stem: C = 3 valid channels stored as 4) ----
+// A[m][k] for k = (r*S + s)*cv + c < K = R*S*cv: X[img][hi][wi][c] inside the image, 0 at a
+// padded tap (the paper's im2col, P:119 -- a padded 0 is still looked up downstream, A11);
+// k in [K, lda) is 0 (storage padding).  taps[k] = (r*dh) | (s*dw) << 8 | c << 16, ~0 past K.
+__global__ void im2col_nhwc_i8_kernel(const int8_t* __restrict__ X, int64_t M, int H, int W, int C,
+                                      int Ho, int Wo, int sh, int sw, int ph, int pw, int S, int cv, int K,
+                                      int lda, int8_t* __restrict__ A) {
+    extern __shared__ uint32_t taps[];
+    for (int k = threadIdx.x; k < lda; k += blockDim.x) {
+        uint32_t t = ~0u;
+        if (k < K) {
+            const int rs = k / cv, c = k - rs * cv, r = rs / S, s_ = rs - r * S;
+            t = (uint32_t)r | ((uint32_t)s_ << 8) | ((uint32_t)c << 16);
+        }
+        taps[k] = t;
+    }
+    __syncthreads();
+    const int chunks = lda / 16;
+    const int64_t total = M * chunks;
+    const int64_t hw = (int64_t)Ho * Wo;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = i / chunks;
+        const int j = (int)(i - m * chunks);
+        const int64_t img = m / hw, rem = m - img * hw;
+        const int ho = (int)(rem / Wo), wo = (int)(rem - (int64_t)ho * Wo);
+        const int hb = ho * sh - ph, wb = wo * sw - pw;
+        const int8_t* xb = X + img * (int64_t)H * W * C;
+        uint32_t w4[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const uint32_t t = taps[16 * j + b];
+            if (t == ~0u) continue;
+            const int hi = hb + (int)(t & 0xffu), wi = wb + (int)((t >> 8) & 0xffu);
+            if ((unsigned)hi < (unsigned)H && (unsigned)wi < (unsigned)W)
+                w4[b >> 2] |= (uint32_t)(uint8_t)__ldg(xb + ((int64_t)hi * W + wi) * C + (int)(t >> 16)) << (8 * (b & 3));
+        }
+        reinterpret_cast<uint4*>(A + m * lda)[j] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+}
+
 }  // namespace axq

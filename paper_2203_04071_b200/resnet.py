@@ -93,6 +93,8 @@ class ApproxResNet:
                 ax.axq_quantize(w, self.s_w[i:i + 1], self.bits, q)
             if kind == "conv":
                 q = q.permute(0, 2, 3, 1).contiguous()                    # KRSC
+                if name == "stem":
+                    self.qw_stem_gemm = q.reshape(cout, -1).contiguous()   # [64][7*7*3] (r, s, c)
                 if name == "stem" and cin % 4:
                     cpad = (cin + 3) // 4 * 4
                     qp = torch.zeros(cout, k, k, cpad, dtype=torch.int8, device=self.dev)
@@ -102,7 +104,11 @@ class ApproxResNet:
         self.fc_bias = torch.as_tensor(weights["fc.b"]).to(self.dev, torch.float32).contiguous()
         # prepared weights for the packed-table kernel (delta8 tables, C % 16 == 0, K >= 64)
         self.wp = {}
+        self.wp_stem_gemm = None
         if packed and lut.repr == "delta8":
+            # the 3-channel stem as an explicit-im2col GEMM with K = 7*7*3 = 147 (the implicit
+            # loader pads C to 4: 196 lookups per output instead of 147)
+            self.wp_stem_gemm = ax.WPack(lut, self.qw_stem_gemm, a_nonneg=False)
             for name, kind, cout, cin, k, stride, pad in self.specs:
                 if kind == "conv" and name == "stem":
                     # the network input is signed: full-range tables, padded C = 4 (4-byte copies)
@@ -134,6 +140,9 @@ class ApproxResNet:
         cq = (cin + 3) // 4 * 4
         b["qx"] = torch.empty(N, H, W, cq, dtype=i8, device=dev)
         h, w = _out(H, 7, 2, 3), _out(W, 7, 2, 3)
+        if self.wp_stem_gemm is not None:
+            kst = self.qw_stem_gemm.shape[1]
+            b["stem_A"] = torch.empty(N * h * w, (kst + 31) // 32 * 32, dtype=i8, device=dev)
         C = self.spec["stem"][2]
         b["stem_q"] = torch.empty(N, h, w, C, dtype=i8, device=dev)
         b["stem_f"] = torch.empty(N, h, w, C, dtype=f32, device=dev)       # calibration only
@@ -170,6 +179,19 @@ class ApproxResNet:
 
     def _conv(self, name, xq, N, H, W, stream, **ep_kw):
         _, _, cout, cin, k, stride, pad = self.spec[name]
+        if name == "stem" and self.wp_stem_gemm is not None:
+            # explicit im2col (k = (r, s, c), 3 channels) + packed-table GEMM, same sums (A11:
+            # padded taps are 0 codes in the matrix and are looked up)
+            A = self._bufs[(N, H, W)]["stem_A"]
+            ax.axq_im2col_nhwc_i8(xq, cin, k, k, (stride, stride), (pad, pad), A, stream)
+            ep = ax.make_epilogue(self._s(name), self._sw(name), d_scale_w_ch=self.s_w_ch.get(name),
+                                  **ep_kw)
+            if self.timing_hook:
+                self.timing_hook("pre", stream)
+            ax.axq_lut_gemm_wp(A[:, :self.qw_stem_gemm.shape[1]], self.wp_stem_gemm, ep, stream=stream)
+            if self.timing_hook:
+                self.timing_hook("post", stream)
+            return
         C = xq.shape[-1]
         d = ax.conv_desc(N, H, W, C, cout, k, k, (stride, stride), (pad, pad),
                          c_valid=cin if C != cin else 0)

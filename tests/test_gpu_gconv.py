@@ -105,3 +105,25 @@ def test_wide_groups_fused_nchw_per_channel(ax):
     ax.axq_lut_conv2d_ep(d, _t(X.transpose(0, 2, 3, 1)), _t(Wt.transpose(0, 2, 3, 1)), lut, ep)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(y.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 4, 20, 18, 7, 2, 3), (1, 5, 8, 9, 9, 3, 1, 1), (3, 16, 16, 5, 6, 1, 1, 0)])
+def test_im2col_nhwc_i8(ax, shape):
+    """Explicit im2col (axq_im2col_nhwc_i8) against a direct numpy construction: k = (r, s, c) over
+    the c_valid channels, 0 at padded taps and past K."""
+    N, cv, C, H, W, R, st, pd = shape
+    X = datagen.random_int8(90 + C, (N, H, W, C))
+    Ho, Wo = (H + 2 * pd - R) // st + 1, (W + 2 * pd - R) // st + 1
+    K = R * R * cv
+    lda = (K + 15) // 16 * 16 + 16
+    Xp = np.zeros((N, H + 2 * pd, W + 2 * pd, C), np.int8)
+    Xp[:, pd:pd + H, pd:pd + W] = X
+    ref = np.zeros((N * Ho * Wo, lda), np.int8)
+    for ho in range(Ho):
+        for wo in range(Wo):
+            patch = Xp[:, ho * st:ho * st + R, wo * st:wo * st + R, :cv].reshape(N, -1)
+            ref[np.arange(N) * Ho * Wo + ho * Wo + wo, :K] = patch
+    A = torch.full((N * Ho * Wo, lda), 77, dtype=torch.int8, device=DEV)
+    ax.axq_im2col_nhwc_i8(_t(X), cv, R, R, (st, st), (pd, pd), A)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(A.cpu().numpy(), ref)
