@@ -943,6 +943,12 @@ axq_status axq_im2col_nhwc_i8(const int8_t* X, int64_t N, int64_t H, int64_t W, 
     if (N == 0) return AXQ_OK;
     if (!X || !A || (reinterpret_cast<uintptr_t>(A) & 15)) return AXQ_ERR_INVALID;
     const int64_t M = N * Ho * Wo;
+    if (C == 4 && cv == 3 && R == 7 && Sz == 7 && lda == 160 && (reinterpret_cast<uintptr_t>(X) & 3) == 0) {
+        axq::im2col_c4_kernel<7, 7, 3, 160><<<stream_grid(M, 256), 256, 0, S(stream)>>>(
+            X, M, (int)H, (int)W, (int)Ho, (int)Wo, (int)stride_h, (int)stride_w, (int)pad_h, (int)pad_w, A);
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? AXQ_OK : cuda_fail(e);
+    }
     axq::im2col_nhwc_i8_kernel<<<stream_grid(M * (lda / 16), 256), 256, lda * 4, S(stream)>>>(
         X, M, (int)H, (int)W, (int)C, (int)Ho, (int)Wo, (int)stride_h, (int)stride_w, (int)pad_h, (int)pad_w,
         (int)Sz, (int)cv, (int)K, (int)lda, A);

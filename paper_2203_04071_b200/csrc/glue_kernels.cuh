@@ -181,4 +181,44 @@ __global__ void im2col_nhwc_i8_kernel(const int8_t* __restrict__ X, int64_t M, i
     }
 }
 
+// The stem's shape specialised (C = 4 stored, 3 valid channels, R x S taps): one thread builds
+// one whole row in registers -- one 4-byte load per tap (its 3 channels), bytes placed at
+// compile-time positions -- then writes it with 16-byte stores.
+template <int R, int S, int CV, int LDA>
+__global__ void im2col_c4_kernel(const int8_t* __restrict__ X, int64_t M, int H, int W, int Ho, int Wo,
+                                 int sh, int sw, int ph, int pw, int8_t* __restrict__ A) {
+    constexpr int K = R * S * CV, NW = LDA / 4;
+    const int64_t hw = (int64_t)Ho * Wo;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t img = m / hw, rem = m - img * hw;
+        const int ho = (int)(rem / Wo), wo = (int)(rem - (int64_t)ho * Wo);
+        const int hb = ho * sh - ph, wb = wo * sw - pw;
+        const uint32_t* xb = reinterpret_cast<const uint32_t*>(X) + img * (int64_t)H * W;
+        uint32_t out[NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) out[i] = 0u;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int hi = hb + r;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int wi = wb + s;
+                const uint32_t v = ((unsigned)hi < (unsigned)H && (unsigned)wi < (unsigned)W)
+                                       ? __ldg(xb + (int64_t)hi * W + wi) : 0u;
+#pragma unroll
+                for (int c = 0; c < CV; ++c) {
+                    constexpr int dummy = 0;
+                    (void)dummy;
+                    const int k = (r * S + s) * CV + c;
+                    out[k >> 2] |= ((v >> (8 * c)) & 0xffu) << (8 * (k & 3));
+                }
+            }
+        }
+        (void)K;
+        uint4* dst = reinterpret_cast<uint4*>(A + m * LDA);
+#pragma unroll
+        for (int i = 0; i < NW / 4; ++i) dst[i] = make_uint4(out[4 * i], out[4 * i + 1], out[4 * i + 2], out[4 * i + 3]);
+    }
+}
+
 }  // namespace axq
