@@ -235,6 +235,23 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
 typedef struct axq_wpack* axq_wpack_t;
 axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K, int64_t ldw,
                             int a_nonneg, axq_wpack_t* out);
+/* a_nonneg is a flag word: AXQ_WPACK_NONNEG (= 1, the promise above) and
+ * AXQ_WPACK_ACTIVATIONS (= 2): W holds ACTIVATION codes x [N][K] (a small matrix, e.g. a
+ * 256-row linear-layer input) and the tables are specialised on them (byte = E[x][u] for a
+ * weight code u) for axq_lut_gemm_xs.
+ * axq_wpack_repack: re-packs new codes W [N][ldw] (same N, K) into wp, asynchronously on
+ *   `stream` (no allocation: the per-call activation tables of axq_lut_gemm_xs).
+ * axq_lut_gemm_xs: acc[m][n] = sum_k LUT[x[m][k]][W[n][k]] for the activations x packed in
+ *   xp (AXQ_WPACK_ACTIVATIONS) and weight codes W [N][ldw] (16-byte aligned, ldw % 16 == 0):
+ *   the packed-table kernel with the weights as its row operand, written back in the normal
+ *   layout -- raw int32 C [M][ldc] or the fused epilogue (bias / per-channel scale indexed by
+ *   n, y [M][ldy], q_out [M][ldq]).  Results identical to axq_lut_gemm_dq.  Suits small M
+ *   with large N*K: the tables are M x K x 1 KiB / 4 and are built per call. */
+#define AXQ_WPACK_NONNEG 1
+#define AXQ_WPACK_ACTIVATIONS 2
+axq_status axq_wpack_repack(axq_wpack_t wp, const int8_t* W, int64_t ldw, void* stream);
+axq_status axq_lut_gemm_xs(int64_t N, const int8_t* W, int64_t ldw, axq_wpack_t xp,
+                           const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream);
 axq_status axq_wpack_destroy(axq_wpack_t wp);
 axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* device_bytes);
 axq_status axq_lut_gemm_wp(int64_t M, const int8_t* A, int64_t lda, axq_wpack_t wp,

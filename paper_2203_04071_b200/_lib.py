@@ -30,7 +30,7 @@ EXPORTED = [
     "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_lstm_recurrent",
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
-    "axq_im2col_nhwc_i8",
+    "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
 ]
 
 
@@ -101,6 +101,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
         "axq_quantize16": ([vp, i64, vp, i32, vp, vp], i32),
         "axq_im2col_nhwc_i8": ([vp] + [i64] * 11 + [vp, i64, vp], i32),
+        "axq_wpack_repack": ([vp, vp, i64, vp], i32),
+        "axq_lut_gemm_xs": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_lut_gemm16": ([i64, i64, i64, vp, i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_maxpool2d_nhwc_f32": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, vp, vp], i32),
         "axq_scale_vec": ([vp, i64, i32, vp, vp], i32),
@@ -360,15 +362,16 @@ def axq_lstm_cell(gates_ih, gates_hh, c, h_out, q_h=None, d_scale_h=None, bits=8
 class WPack:
     """Owns an axq_wpack_t: weight-specialised E tables of a layer (delta8 LUTs only)."""
 
-    def __init__(self, lut: Lut, W, K: int | None = None, a_nonneg: bool = False):
+    def __init__(self, lut: Lut, W, K: int | None = None, a_nonneg: bool = False,
+                 activations: bool = False):
         """W: device int8 [N][K] (conv: KRSC flattened).  a_nonneg: every activation code will
         be >= 0 (ReLU outputs) -> half-range tables."""
         N = W.shape[0]
         K = W.numel() // N if K is None else K
         h = ctypes.c_void_p()
+        flags = (1 if a_nonneg else 0) | (2 if activations else 0)
         _check("axq_wpack_create", load().axq_wpack_create(lut.handle, _ptr(W), N, K,
-                                                           W.stride(0), int(bool(a_nonneg)),
-                                                           ctypes.byref(h)))
+                                                           W.stride(0), flags, ctypes.byref(h)))
         self.a_nonneg = bool(a_nonneg)
         self.handle = h
         self.N, self.K = N, K
@@ -490,3 +493,15 @@ def axq_im2col_nhwc_i8(X, c_valid: int, R: int, S: int, stride, pad, A, stream=N
     _check("axq_im2col_nhwc_i8", load().axq_im2col_nhwc_i8(
         _ptr(X), N, H, W, C, int(c_valid), R, S, stride[0], stride[1], pad[0], pad[1], _ptr(A),
         A.stride(0), _stream(stream)))
+
+
+def axq_wpack_repack(wp: WPack, W, stream=None) -> None:
+    _check("axq_wpack_repack", load().axq_wpack_repack(wp.handle, _ptr(W), W.stride(0), _stream(stream)))
+
+
+def axq_lut_gemm_xs(W, xp: WPack, ep: axq_epilogue | None = None, C=None, stream=None) -> None:
+    """acc[m][n] = sum_k LUT[x[m][k]][W[n][k]] with x packed in xp (activations=True)."""
+    N = W.shape[0]
+    _check("axq_lut_gemm_xs", load().axq_lut_gemm_xs(
+        N, _ptr(W), W.stride(0), xp.handle, ctypes.byref(ep) if ep is not None else None, _ptr(C),
+        C.stride(0) if C is not None else 0, _stream(stream)))

@@ -22,6 +22,10 @@
 struct axq_wpack {
     int device;
     int half;
+    int swap;                  // tables specialised on activations (axq_lut_gemm_xs)
+    const int8_t* dtab;        // packing table: the LUT's [uw][ua] delta8 table, or (swap) a
+                               // transposed [ua][uw] copy owned by the wpack (dtab_own)
+    int8_t* dtab_own;
     int32_t t00;
     int64_t N, K, Kp;
     uint32_t* tables;
@@ -714,15 +718,31 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
     w->N = N;
     w->K = K;
     w->Kp = (K + 31) / 32 * 32;   // a whole number of 32-k stages (P4T half-range tables)
-    w->half = a_nonneg ? 1 : 0;
+    w->half = (a_nonneg & AXQ_WPACK_NONNEG) ? 1 : 0;
+    w->swap = (a_nonneg & AXQ_WPACK_ACTIVATIONS) ? 1 : 0;
+    w->dtab = reinterpret_cast<const int8_t*>(lut->d_table);
+    w->dtab_own = nullptr;
+    if (w->swap) {   // activation packing reads E[x][*] rows: keep a transposed copy
+        std::vector<int8_t> h(65536), ht(65536);
+        cudaError_t e0 = cudaMemcpy(h.data(), lut->d_table, 65536, cudaMemcpyDeviceToHost);
+        for (int uw = 0; uw < 256 && e0 == cudaSuccess; ++uw)
+            for (int ua = 0; ua < 256; ++ua) ht[(ua << 8) | uw] = h[(uw << 8) | ua];
+        if (e0 == cudaSuccess) e0 = cudaMalloc(&w->dtab_own, 65536);
+        if (e0 == cudaSuccess) e0 = cudaMemcpy(w->dtab_own, ht.data(), 65536, cudaMemcpyHostToDevice);
+        if (e0 != cudaSuccess) {
+            cudaFree(w->dtab_own);
+            delete w;
+            return cuda_fail(e0);
+        }
+        w->dtab = w->dtab_own;
+    }
     const int64_t nb = (N + axq::p4::TN - 1) / axq::p4::TN;
     const size_t tb = (size_t)nb * w->Kp * 4 * (w->half ? 128 : 256) * 4, wb = (size_t)nb * w->Kp * axq::p4::TN;
     w->bytes = (int64_t)(tb + wb);
     cudaError_t e = cudaMalloc(&w->tables, tb);
     if (e == cudaSuccess) e = cudaMalloc(&w->wpk, wb);
     if (e == cudaSuccess) {
-        int rc = axq::p4_pack(W, N, K, ldw, w->Kp, reinterpret_cast<const int8_t*>(lut->d_table),
-                              w->tables, w->wpk, w->half, 0);
+        int rc = axq::p4_pack(W, N, K, ldw, w->Kp, w->dtab, w->tables, w->wpk, w->half, w->swap, 0);
         e = rc ? (cudaError_t)rc : cudaDeviceSynchronize();
     }
     if (e != cudaSuccess) {
@@ -735,11 +755,22 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
     return AXQ_OK;
 }
 
+axq_status axq_wpack_repack(axq_wpack_t wp, const int8_t* W, int64_t ldw, void* stream) {
+    if (!wp || !W || ldw < wp->K) return AXQ_ERR_INVALID;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != wp->device) return AXQ_ERR_INVALID;
+    const int rc = axq::p4_pack(W, wp->N, wp->K, ldw, wp->Kp, wp->dtab, wp->tables, wp->wpk, wp->half, wp->swap,
+                                S(stream));
+    return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
+}
+
 axq_status axq_wpack_destroy(axq_wpack_t wp) {
     if (!wp) return AXQ_OK;
     cudaDeviceSynchronize();
     cudaFree(wp->tables);
     cudaFree(wp->wpk);
+    if (wp->dtab_own) cudaFree(wp->dtab_own);
     delete wp;
     return AXQ_OK;
 }
@@ -775,10 +806,11 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     a.mm.t00 = wp->t00;
     axq::EpiArgs epi{};
     if (ep) {
-        axq_status s = check_epilogue(ep, a.mm.N, conv);
+        axq_status s = check_epilogue(ep, a.transposed ? a.mm.M : a.mm.N, conv);
         if (s != AXQ_OK) return s;
         epi = to_epi(ep, conv && !ep->y_nhwc, (int64_t)a.mm.Ho * a.mm.Wo);
-    } else if (!C || ldc < a.mm.N) {
+        if (a.transposed && (ep->ldy < a.mm.M && ep->y)) return AXQ_ERR_INVALID;
+    } else if (!C || ldc < (a.transposed ? a.mm.M : a.mm.N)) {
         return AXQ_ERR_INVALID;
     }
     if (a.mm.M == 0) return AXQ_OK;
@@ -790,7 +822,8 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     const bool use_tc = variant >= 2;                                 // P4T / P4W: tcgen05 exact part
     const int bm = variant == 3 ? 896 : 1024;
     if (use_tc)
-        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, wp->half, bm, sm_count(), can_split, a.splits, a.stages_per_split);
+        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, wp->half, bm, sm_count(), can_split && !a.transposed, a.splits,
+                      a.stages_per_split);
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
     auto launch = [&](const axq::P4Args& x) {
@@ -831,6 +864,19 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     }
     int rc = launch(a);
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
+}
+
+axq_status axq_lut_gemm_xs(int64_t N, const int8_t* W, int64_t ldw, axq_wpack_t xp,
+                           const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream) {
+    // acc[m][n] = sum_k LUT[x[m][k]][W[n][k]] with x packed (activation-specialised) in xp: the
+    // P4W kernel runs with the weight rows as its row operand and writes the result transposed
+    if (!xp || !xp->swap || N < 0 || (N > 0 && (!W || ldw < xp->K))) return AXQ_ERR_INVALID;
+    if (!aligned16(W) || (ldw & 15)) return AXQ_ERR_UNSUPPORTED;
+    if (g_wpack_kernel == 1 || g_wpack_kernel == 2) return AXQ_ERR_UNSUPPORTED;   // P4W only
+    axq::P4Args a{};
+    a.mm.A = W; a.mm.lda = ldw; a.mm.M = N; a.mm.N = xp->N; a.mm.K = xp->K;
+    a.transposed = 1;
+    return p4_run(a, xp, ep, false, C, ldc, S(stream));
 }
 
 axq_status axq_lut_gemm_wp(int64_t M, const int8_t* A, int64_t lda, axq_wpack_t wp,

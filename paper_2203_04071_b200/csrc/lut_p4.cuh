@@ -503,29 +503,40 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const __grid_constant
 }
 
 // ---- weight preparation: E tables and the packed weight tile (once per layer) ----
-// tables[((nb*Kp + k)*4 + q)*rows + ua] = bytes j=0..3: E[ua][w(16nb+4q+j, k)] + 128 (E = delta8
-// table); rows = 256, or 128 when only non-negative activation codes will be looked up
+// tables[((nb*Kp + k)*4 + q)*rows + u] = bytes j=0..3: E[u][w(16nb+4q+j, k)] + 128 (E = delta8
+// table); rows = 256, or 128 when only non-negative codes u will be looked up.
+// swap = 1 specialises the tables on the FIRST (activation) operand instead: the packed codes
+// are activations x and the looked-up row code u is a weight, so the byte is E[x][u] + 128
+// (used to build tables from a small activation matrix per call, axq_lut_gemm_xs); the
+// caller then passes the transposed table ([ua][uw]) so the reads stay row-contiguous.
+// One block per (nb, k): the 16 packed codes are read once, the 4 x rows words written.
 __global__ void p4_pack_tables_kernel(const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw,
                                       int64_t Kp, const int8_t* __restrict__ dtab,
-                                      uint32_t* __restrict__ tables, int rows) {
+                                      uint32_t* __restrict__ tables, int rows, int swap) {
+    __shared__ int codes[p4::TN];
     const int64_t n_blocks = (N + p4::TN - 1) / p4::TN;
-    const int64_t total = n_blocks * Kp * 4 * rows;
-    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += gs) {
-        const int ua = (int)(i % rows);
-        int64_t t = i / rows;
-        const int q = (int)(t & 3);
-        t >>= 2;
-        const int64_t k = t % Kp, nb = t / Kp;
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t n = nb * p4::TN + 4 * q + j;
-            const int w = (n < N && k < K) ? (int)W[n * ldw + k] : 0;
-            const uint8_t e = (uint8_t)((int)dtab[((w & 0xff) << 8) | ua] + p4::E_BIAS);
-            word |= (uint32_t)e << (8 * j);
+    for (int64_t blk = blockIdx.x; blk < n_blocks * Kp; blk += gridDim.x) {
+        const int64_t k = blk % Kp, nb = blk / Kp;
+        __syncthreads();
+        if (threadIdx.x < p4::TN) {
+            const int64_t n = nb * p4::TN + threadIdx.x;
+            codes[threadIdx.x] = (n < N && k < K) ? (int)W[n * ldw + k] : 0;
         }
-        tables[i] = word;
+        __syncthreads();
+        uint32_t* dst = tables + blk * 4 * rows;
+        for (int idx = threadIdx.x; idx < 4 * rows; idx += blockDim.x) {
+            const int q = idx / rows, u = idx - q * rows;
+            uint32_t word = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = codes[4 * q + j] & 0xff;
+                // dtab is [uw][ua] (E[ua][uw] at (uw << 8) | ua) for weight packing, and the
+                // transposed copy [ua][uw] for activation packing: both read contiguous rows
+                const int e = (int)__ldg(dtab + ((c << 8) | u));
+                word |= (uint32_t)(uint8_t)(e + p4::E_BIAS) << (8 * j);
+            }
+            dst[idx] = word;
+        }
     }
 }
 

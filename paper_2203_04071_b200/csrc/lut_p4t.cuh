@@ -107,6 +107,32 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
     using namespace p4;
     const MMArgs& p = P.mm;
     const EpiArgs& e = p.ep;
+    if (P.transposed) {
+        // axq_lut_gemm_xs: rows are weight rows (bias / per-channel scale index), columns are
+        // activation rows; lanes = consecutive weight rows -> coalesced along the output row
+        if (p.C_out != nullptr) {
+#pragma unroll
+            for (int n = 0; n < TN; ++n)
+                if (n0 + n < p.N) p.C_out[(n0 + n) * p.ldc + m] = eacc[n];
+            return;
+        }
+        const float sc_r = e.sw_ch ? __fmul_rn(*e.sa, e.sw_ch[m]) : __fmul_rn(*e.sa, *e.sw);
+        const float b = e.bias ? e.bias[m] : 0.f;
+        const float s_out = e.q ? *e.s_out : 1.f;
+        const float qm = (float)((1 << ((e.q ? e.bits_out : 8) - 1)) - 1);
+#pragma unroll
+        for (int n = 0; n < TN; ++n) {
+            const int64_t nn = n0 + n;
+            if (nn >= p.N) continue;
+            float v = __fmul_rn(__int2float_rn(eacc[n]), sc_r);
+            if (e.bias) v = __fadd_rn(v, b);
+            if (e.residual) v = __fadd_rn(v, e.residual[nn * e.ldr + m]);
+            if (e.relu) v = v > 0.f ? v : 0.f;
+            if (e.y) e.y[nn * e.ldy + m] = v;
+            if (e.q) e.q[nn * e.ldq + m] = epi_quant(v, s_out, qm);
+        }
+        return;
+    }
     if (p.C_out != nullptr) {
         int32_t* c = p.C_out + m * p.ldc + n0;
         if (splits > 1) {

@@ -35,7 +35,7 @@ int launch_mm_i32(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid,
 // P4 kernel (lut_p4.cuh); declared here with an opaque argument struct.
 struct P4Args;
 int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int8_t* dtab,
-            uint32_t* tables, int8_t* wpk, int half, cudaStream_t st);
+            uint32_t* tables, int8_t* wpk, int half, int swap, cudaStream_t st);
 int launch_p4(const P4Args& a, cudaStream_t st);
 int launch_p4t(const P4Args& a, cudaStream_t st);   // tcgen05 exact part, 32 warps (lut_p4t.cuh)
 int launch_p4w(const P4Args& a, cudaStream_t st);   // warp-specialised P4T (lut_p4w.cuh)

@@ -7,12 +7,12 @@
 namespace axq {
 
 int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int8_t* dtab,
-            uint32_t* tables, int8_t* wpk, int half, cudaStream_t st) {
+            uint32_t* tables, int8_t* wpk, int half, int swap, cudaStream_t st) {
     const int64_t nb = (N + p4::TN - 1) / p4::TN;
     const int rows = half ? 128 : 256;
-    const int64_t t1 = nb * Kp * 4 * rows, t2 = nb * Kp * p4::TN;
-    p4_pack_tables_kernel<<<(unsigned)std::min<int64_t>((t1 + 255) / 256, 148 * 16), 256, 0, st>>>(
-        W, N, K, ldw, Kp, dtab, tables, rows);
+    const int64_t t2 = nb * Kp * p4::TN;
+    p4_pack_tables_kernel<<<(unsigned)std::min<int64_t>(nb * Kp, 148 * 64), 256, 0, st>>>(
+        W, N, K, ldw, Kp, dtab, tables, rows, swap);
     p4_pack_w_kernel<<<(unsigned)std::min<int64_t>((t2 + 255) / 256, 148 * 16), 256, 0, st>>>(W, N, K, ldw, Kp, wpk);
     return (int)cudaGetLastError();
 }

@@ -172,3 +172,48 @@ def test_p4_conv_c4_padded_stem(ax):
     Y = torch.empty(2, Ho, Wo, 16, dtype=torch.int32, device=DEV)
     ax.axq_lut_conv2d_wp(d, _t(Xp), wp, None, Y)
     np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 1024, 1024), (100, 300, 77), (17, 900, 256), (1000, 64, 96)])
+def test_gemm_xs_activation_specialised(ax, M, N, K):
+    """axq_lut_gemm_xs (tables specialised on the activations, built per call, weights as the
+    kernel's row operand, result written back in the normal layout): raw int32 and the fused
+    epilogue with bias, per-channel weight scales and requantized codes, against the oracle.
+    Runs on the default (P4W) kernel only."""
+    T = datagen.lut_randerr(8, 0, 2)
+    A = datagen.random_int8(500 + M, (M, K))
+    W = datagen.random_int8(600 + N, (N, K))
+    acc = oracle.lut_gemm(A, W, T, 8)
+    lut = ax.Lut(8, T)
+    Kp = (K + 15) // 16 * 16
+    dA = torch.zeros(M, Kp, dtype=torch.int8, device=DEV)
+    dA[:, :K] = _t(A)
+    dW = torch.zeros(N, Kp, dtype=torch.int8, device=DEV)
+    dW[:, :K] = _t(W)
+    prev = ax.axq_wpack_kernel(3)
+    try:
+        xp = ax.WPack(lut, dA.narrow(1, 0, K), activations=True)
+        ax.axq_wpack_repack(xp, dA.narrow(1, 0, K))          # the per-call path
+        C = torch.empty(M, N, dtype=torch.int32, device=DEV)
+        ax.axq_lut_gemm_xs(dW.narrow(1, 0, K), xp, None, C)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(C.cpu().numpy(), acc)
+        rng = np.random.default_rng(M + N)
+        s_w = rng.uniform(1e-4, 1e-2, N).astype(np.float32)
+        b = rng.standard_normal(N).astype(np.float32)
+        s_a, s_o = np.float32(0.013), np.float32(0.02)
+        y_ref = oracle.dequantize_pc(acc, s_a, s_w, b)
+        q_ref = oracle.quantize(y_ref, s_o, 8)
+        y = torch.empty(M, N, device=DEV)
+        q = torch.empty(M, N, dtype=torch.int8, device=DEV)
+        ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
+        dsa, dso, ones, dsw, db = (torch.tensor([s_a], device=DEV), torch.tensor([s_o], device=DEV),
+                                   torch.ones(1, device=DEV), _t(s_w), _t(b))
+        ep = ax.make_epilogue(dsa, ones, bias=db, y=y, ldy=N, workspace=ws, q_out=q, ldq=N,
+                              d_scale_out=dso, bits_out=8, d_scale_w_ch=dsw)
+        ax.axq_lut_gemm_xs(dW.narrow(1, 0, K), xp, ep)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+        np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
+    finally:
+        ax.axq_wpack_kernel(prev)
