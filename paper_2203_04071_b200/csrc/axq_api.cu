@@ -783,6 +783,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
+static int64_t g_p4w_ks16_max_k = 0;   // AXQ_P4W_KS16_MAX_K: measured slower, off
 static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 2 P4T, 3 P4W
 
 int axq_wpack_kernel(int variant) {
@@ -821,8 +822,16 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     const int variant = g_wpack_kernel != 0 ? g_wpack_kernel : (a.c4 ? 1 : 3);
     const bool use_tc = variant >= 2;                                 // P4T / P4W: tcgen05 exact part
     const int bm = variant == 3 ? 896 : 1024;
+    // k per stage: P4T 32 (half) / 16; P4W the same, except half-range tables with K <= 128
+    // (short tiles: 16-k stages, 4 deep)
+    static bool env_read = false;
+    if (!env_read) {
+        if (const char* v = std::getenv("AXQ_P4W_KS16_MAX_K")) g_p4w_ks16_max_k = std::atoll(v);
+        env_read = true;
+    }
+    a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
     if (use_tc)
-        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, wp->half, bm, sm_count(), can_split && !a.transposed, a.splits,
+        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, a.ks, bm, sm_count(), can_split && !a.transposed, a.splits,
                       a.stages_per_split);
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);

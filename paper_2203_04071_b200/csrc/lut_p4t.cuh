@@ -102,8 +102,43 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 // Output of one lane's row (16 columns, int32 totals in v): raw / atomic int32 or the fused
 // epilogue (P4's, one row per lane).
+// Per-launch epilogue constants (loaded once per CTA, not per tile).
+struct EpiConst {
+    float sc, s_out, qm;
+};
+__device__ __forceinline__ EpiConst p4t_epi_const(const P4Args& P) {
+    const EpiArgs& e = P.mm.ep;
+    EpiConst k{0.f, 1.f, 127.f};
+    if (P.mm.C_out == nullptr) {
+        k.sc = __fmul_rn(*e.sa, *e.sw);
+        k.s_out = e.q ? *e.s_out : 1.f;
+        k.qm = (float)((1 << ((e.q ? e.bits_out : 8) - 1)) - 1);
+    }
+    return k;
+}
+
+// the row-layout vector epilogue applies (16-byte aligned fp32 rows, 4-byte aligned codes)
+__device__ __forceinline__ bool p4t_vec_ok(const P4Args& P, int64_t n0) {
+    const MMArgs& p = P.mm;
+    const EpiArgs& e = p.ep;
+    return !P.transposed && p.C_out == nullptr && (n0 + p4::TN <= p.N) && !e.y_nchw &&
+           (!e.y || (((e.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.y) & 15) == 0))) &&
+           (!e.residual || (((e.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.residual) & 15) == 0))) &&
+           (!e.bias || ((reinterpret_cast<uintptr_t>(e.bias) & 15) == 0)) &&
+           (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
+}
+
+__device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
+                                              int splits, const EpiConst& kc, const float4* res_pre);
+
 __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
                                               int splits) {
+    p4t_store_row(P, m, n0, eacc, splits, p4t_epi_const(P), nullptr);
+}
+
+// res_pre: the row's 4 residual float4 groups already loaded (vector path only), or null
+__device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
+                                              int splits, const EpiConst& kc, const float4* res_pre) {
     using namespace p4;
     const MMArgs& p = P.mm;
     const EpiArgs& e = p.ep;
@@ -146,25 +181,23 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
         }
         return;
     }
-    const float sc = __fmul_rn(*e.sa, *e.sw);
-    const float s_out = e.q ? *e.s_out : 1.f;
-    const float qm = (float)((1 << ((e.q ? e.bits_out : 8) - 1)) - 1);
-    const bool vec = (n0 + TN <= p.N) && !e.y_nchw &&
-                     (!e.y || (((e.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.y) & 15) == 0))) &&
-                     (!e.residual || (((e.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.residual) & 15) == 0))) &&
-                     (!e.bias || ((reinterpret_cast<uintptr_t>(e.bias) & 15) == 0)) &&
-                     (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
+    const float sc = kc.sc, s_out = kc.s_out, qm = kc.qm;
+    const bool vec = p4t_vec_ok(P, n0);
     if (vec) {
         const bool q16 = e.q && ((e.ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 15) == 0);
         // residual groups are loaded one ahead (8 live registers, not 16: the P4W consumer
         // runs at 64 registers per thread)
-        const float4* rp = e.residual ? reinterpret_cast<const float4*>(e.residual + m * e.ldr + n0) : nullptr;
-        float4 rnext = rp ? __ldg(rp) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4* rp = (e.residual && !res_pre) ? reinterpret_cast<const float4*>(e.residual + m * e.ldr + n0)
+                                                    : nullptr;
+        float4 rnext = res_pre ? res_pre[0] : (rp ? __ldg(rp) : make_float4(0.f, 0.f, 0.f, 0.f));
         uint32_t qw[TN / 4];
 #pragma unroll
         for (int n = 0; n < TN; n += 4) {
             const float4 rcur = rnext;
-            if (rp && n + 4 < TN) rnext = __ldg(rp + (n + 4) / 4);
+            if (n + 4 < TN) {
+                if (res_pre) rnext = res_pre[(n + 4) / 4];
+                else if (rp) rnext = __ldg(rp + (n + 4) / 4);
+            }
             const int64_t nn = n0 + n;
             float v[4];
 #pragma unroll

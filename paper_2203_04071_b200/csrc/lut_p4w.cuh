@@ -38,14 +38,16 @@ constexpr int TN = p4::TN;
 constexpr int W_STAGE = 512;
 constexpr int TMEM_COLS = 512;             // exact sets at 0 and 128, E sums at 256
 
-template <bool HALF>
+template <bool HALF, int KSX = (HALF ? 32 : 16)>
 struct Geo {
-    static constexpr int KS = HALF ? 32 : 16;
+    static constexpr int KS = KSX;
     static constexpr int TROWS = HALF ? 128 : 256;
     static constexpr int TQ = TROWS * 4;
     static constexpr int TBL_STAGE = KS * (TN / 4) * TQ;   // 64 KiB
     static constexpr int A_STAGE = BM * KS;                // KS / 16 planes of [BM][16 B]
-    static constexpr int STAGES = 2;
+    // half-range tables in 16-k stages (small-K layers): 4 stages of 32 KiB, a deeper pipeline
+    // across the short tiles; otherwise 2 stages of 64 KiB
+    static constexpr int STAGES = (HALF && KS == 16) ? 4 : 2;
     static constexpr int FLUSH_STAGES = 256 / KS;
     static constexpr int SMEM_TBL = 0;
     static constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
@@ -72,10 +74,13 @@ __device__ __forceinline__ void consumer_sync() {   // named barrier 1: the 896 
     asm volatile("bar.sync 1, %0;\n" ::"n"(p4w::BM) : "memory");
 }
 
-template <bool HALF>
+// RES: a separate instantiation for layers with a residual input, whose epilogue loads the
+// residual rows before waiting on the tile's MMAs (their latency overlaps the wait).  Kept out
+// of the other layers' instantiation: its extra live registers would spill into their loop.
+template <bool HALF, int KSX, bool RES = false>
 __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_constant__ P4Args P) {
     using namespace p4w;
-    using G = p4w::Geo<HALF>;
+    using G = p4w::Geo<HALF, KSX>;
     constexpr int KS = G::KS, STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ, A_STAGE = G::A_STAGE;
     constexpr int NPL = KS / 16;
     extern __shared__ __align__(1024) uint8_t p4w_smem[];
@@ -286,6 +291,7 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
         const uint32_t t_e = tmem + t_lane + 256u + slice_col;
         constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) | ((128u >> 4) << 24);
         const bool mma_thread = (tid == 0);
+        const EpiConst kconst = p4t_epi_const(P);   // per-launch epilogue scalars, loaded once
         const uint32_t one = P.one;   // = 1, opaque to the compiler (keeps those adds on the FMA pipe)
         Gen g;
         gen_init(g);
@@ -377,6 +383,16 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
             }
             int corr = p4::E_BIAS * KS * (s_e - s_b);
             if (s_e == nst_all) corr += (int)(((P.Kp - p.K) + p.pad_lookups) * (int64_t)p.t00);
+            // the row's residual groups: issued before the wait on the tile's MMAs, so their
+            // latency overlaps it (the K loop's registers are free here)
+            const int64_t m_row = m0 + tid;
+            const bool pre = RES && p.ep.residual != nullptr && m_row < p.M && p4t_vec_ok(P, n0);
+            float4 res[TN / 4];
+            if (pre) {
+                const float4* rp = reinterpret_cast<const float4*>(p.ep.residual + m_row * p.ep.ldr + n0);
+#pragma unroll
+                for (int j = 0; j < TN / 4; ++j) res[j] = __ldg(rp + j);
+            }
             // exact part of this tile: TMEM set tb, complete once tile_full[tb] flips
             mbar_wait(bar_tfull + 8 * tb, (tcount >> 1) & 1u);
             tc_fence_after();
@@ -430,10 +446,10 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                             eacc[4 * j] += v.x; eacc[4 * j + 1] += v.y; eacc[4 * j + 2] += v.z; eacc[4 * j + 3] += v.w;
                         }
                     }
-                    if (m < p.M) p4t_store_row(P, m, n0, eacc, 1);
+                    if (m < p.M) p4t_store_row(P, m, n0, eacc, 1, kconst, pre ? res : nullptr);
                 }
             } else if (m < p.M) {
-                p4t_store_row(P, m, n0, eacc, splits);
+                p4t_store_row(P, m, n0, eacc, splits, kconst, pre ? res : nullptr);
             }
         }
     }

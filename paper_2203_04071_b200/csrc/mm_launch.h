@@ -47,7 +47,7 @@ int launch_quantize16(const float* x, int64_t n, const float* d_scale, int bits,
                       cudaStream_t st);
 int launch_gconv(int repr, const GConvArgs& a, cudaStream_t st);   // gconv.cuh (groups > 1)
 int launch_lstm_rec(const LstmRecArgs& a, int sms, cudaStream_t st);   // lstm_rec.cuh
-void p4t_plan(int64_t M, int64_t N, int64_t Kp, int half, int bm, int sms, bool can_split, int& splits, int& sps);
+void p4t_plan(int64_t M, int64_t N, int64_t Kp, int ks, int bm, int sms, bool can_split, int& splits, int& sps);
 void p4_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& rpl, int& splits,
              int& sps);
 

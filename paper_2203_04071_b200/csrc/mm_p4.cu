@@ -65,34 +65,37 @@ int launch_p4t(const P4Args& a, cudaStream_t st) {
     return a.half ? launch_p4t_t<true>(a, st) : launch_p4t_t<false>(a, st);
 }
 
-template <bool HALF>
+template <bool HALF, int KSX, bool RES = false>
 static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     static unsigned configured = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     dev &= 31;
     if (!(configured & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(lut_p4w_kernel<HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             p4w::Geo<HALF>::SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(lut_p4w_kernel<HALF, KSX, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             p4w::Geo<HALF, KSX>::SMEM_BYTES);
         if (e != cudaSuccess) return (int)e;
         configured |= 1u << dev;
     }
     const int64_t tiles = ((a.mm.M + p4w::BM - 1) / p4w::BM) * ((a.mm.N + p4::TN - 1) / p4::TN);
-    const int64_t work = a.streamk ? tiles * (a.Kp / p4w::Geo<HALF>::KS) : tiles * a.splits;
+    const int64_t work = a.streamk ? tiles * (a.Kp / KSX) : tiles * a.splits;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned g = (unsigned)std::min<int64_t>(work, sms > 0 ? sms : 148);
-    lut_p4w_kernel<HALF><<<g, p4w::NT, p4w::Geo<HALF>::SMEM_BYTES, st>>>(a);
+    lut_p4w_kernel<HALF, KSX, RES><<<g, p4w::NT, p4w::Geo<HALF, KSX>::SMEM_BYTES, st>>>(a);
     return (int)cudaGetLastError();
 }
 
 int launch_p4w(const P4Args& a, cudaStream_t st) {
-    return a.half ? launch_p4w_t<true>(a, st) : launch_p4w_t<false>(a, st);
+    if (!a.half) return launch_p4w_t<false, 16>(a, st);
+    if (a.ks == 16) return launch_p4w_t<true, 16>(a, st);
+    if (a.mm.ep.residual != nullptr && a.mm.C_out == nullptr) return launch_p4w_t<true, 32, true>(a, st);
+    return launch_p4w_t<true, 32>(a, st);
 }
 
 // P4T tiles are 1024 rows: split K (exact, int32 atomics) only when they cannot fill the SMs.
-void p4t_plan(int64_t M, int64_t N, int64_t Kp, int half, int bm, int sms, bool can_split, int& splits, int& sps) {
-    const int64_t nst = Kp / (half ? 32 : 16), nb = (N + p4::TN - 1) / p4::TN;
+void p4t_plan(int64_t M, int64_t N, int64_t Kp, int ks, int bm, int sms, bool can_split, int& splits, int& sps) {
+    const int64_t nst = Kp / ks, nb = (N + p4::TN - 1) / p4::TN;
     const int64_t t = ((M + bm - 1) / bm) * nb;
     splits = 1;
     sps = (int)nst;
