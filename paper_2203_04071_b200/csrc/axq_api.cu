@@ -783,6 +783,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
+static int64_t g_sk_min_stages = 1;    // AXQ_SK_MIN_STAGES: measured best at 1 (every SM takes a piece)
 static int64_t g_p4w_ks16_max_k = 0;   // AXQ_P4W_KS16_MAX_K: measured slower, off
 static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 2 P4T, 3 P4W
 
@@ -827,6 +828,8 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     static bool env_read = false;
     if (!env_read) {
         if (const char* v = std::getenv("AXQ_P4W_KS16_MAX_K")) g_p4w_ks16_max_k = std::atoll(v);
+        if (const char* v = std::getenv("AXQ_SK_MIN_STAGES")) g_sk_min_stages = std::max(1LL, std::atoll(v));
+        if (const char* v = std::getenv("AXQ_P4W_PDL")) axq::g_p4w_pdl = std::atoi(v);
         env_read = true;
     }
     a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
@@ -847,6 +850,9 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
             a.streamk = 1;
             a.splits = 1;
             a.stages_per_split = 0;
+            // pieces of at least ~4 stages: a small tail is shared by fewer CTAs
+            const int64_t tail_it = (tiles % sm_count()) * (wp->Kp / a.ks);
+            a.sk_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), tail_it / g_sk_min_stages));
             a.ws = variant == 3 ? streamk_parts(dev) : ep->workspace;
             a.cnt = cnt;
         }

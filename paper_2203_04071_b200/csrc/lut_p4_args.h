@@ -52,6 +52,7 @@ struct P4Args {
     int32_t* ws;                // stream-K pieces: P4T int32 [M][N] (zero on entry, left zero);
                                 // P4W per-CTA partial slots [grid][2][896][16]
     int32_t* cnt;               // stream-K tile counters (>= gridDim.x), zero on entry, left zero
+    int sk_ctas;                // P4W stream-K: CTAs sharing the tail (0 = all)
     int ks;                     // P4W: k per stage (16 or 32; 16 with half tables = 4 stages)
     int transposed;             // P4W: output element (row r, col c) goes to [c][r] (gemm_xs)
     int nb_fast;                // tile order: column block fastest (the layer's tables stay in

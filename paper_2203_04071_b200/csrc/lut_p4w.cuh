@@ -134,6 +134,10 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // programmatic dependent launch: let the next layer's CTAs start their prologue on SMs this
+    // grid frees, and wait here (prologue done) until the previous layer's outputs are complete
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
     // ---- work decomposition (shared by both roles): as lut_p4t.cuh ----
     const int64_t m_tiles = (p.M + BM - 1) / BM, n_blocks = (p.N + TN - 1) / TN;
@@ -146,7 +150,10 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
     const int64_t t_all = m_tiles * n_blocks;
     const int64_t t_dp = sk ? (t_all / G_) * G_ : 0;
     const int64_t it_sk = (t_all - t_dp) * (int64_t)nst_all;
-    auto sk_begin = [&](int64_t c) { return t_dp * nst_all + (c * it_sk) / G_; };
+    // the tail is cut among the first G_sk CTAs only (pieces of >= a few stages; the host
+    // picks sk_ctas), the rest get empty ranges
+    const int64_t G_sk = (P.sk_ctas > 0 && P.sk_ctas < G_) ? P.sk_ctas : G_;
+    auto sk_begin = [&](int64_t c) { return t_dp * nst_all + ((c < G_sk ? c : G_sk) * it_sk) / G_sk; };
     struct Gen { int64_t cur, end; bool dp; };
     auto gen_init = [&](Gen& g) {
         g.dp = !sk || t_dp > 0;
@@ -421,8 +428,8 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                     __stcg(part + j, make_int4(eacc[4 * j], eacc[4 * j + 1], eacc[4 * j + 2], eacc[4 * j + 3]));
                 __threadfence();
                 consumer_sync();
-                int64_t c_first = ((x0 - t_dp * nst_all) * G_) / it_sk;
-                while (c_first + 1 < G_ && sk_begin(c_first + 1) <= x0) ++c_first;
+                int64_t c_first = ((x0 - t_dp * nst_all) * G_sk) / it_sk;
+                while (c_first + 1 < G_sk && sk_begin(c_first + 1) <= x0) ++c_first;
                 if (tid == 0) {
                     const int old = atomicAdd(P.cnt + c_first, s_e - s_b);
                     const int fin = (old + (s_e - s_b) == nst_all) ? 1 : 0;
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                 if (fin) {
                     __threadfence();
                     const int64_t x1 = x0 + nst_all;   // one past the tile's last iteration
-                    for (int64_t c = c_first; c < G_ && sk_begin(c) < x1; ++c) {
+                    for (int64_t c = c_first; c < G_sk && sk_begin(c) < x1; ++c) {
                         const int64_t cb = sk_begin(c);
                         if (c == blockIdx.x || cb == sk_begin(c + 1)) continue;   // self / empty range
                         const int4* op = reinterpret_cast<const int4*>(

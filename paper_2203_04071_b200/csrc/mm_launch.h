@@ -38,7 +38,8 @@ int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, cons
             uint32_t* tables, int8_t* wpk, int half, int swap, cudaStream_t st);
 int launch_p4(const P4Args& a, cudaStream_t st);
 int launch_p4t(const P4Args& a, cudaStream_t st);   // tcgen05 exact part, 32 warps (lut_p4t.cuh)
-int launch_p4w(const P4Args& a, cudaStream_t st);   // warp-specialised P4T (lut_p4w.cuh)
+int launch_p4w(const P4Args& a, cudaStream_t st);
+extern int g_p4w_pdl;   // warp-specialised P4T (lut_p4w.cuh)
 struct LstmRecArgs;
 struct GConvArgs;
 struct WideArgs;

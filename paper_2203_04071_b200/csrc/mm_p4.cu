@@ -65,6 +65,8 @@ int launch_p4t(const P4Args& a, cudaStream_t st) {
     return a.half ? launch_p4t_t<true>(a, st) : launch_p4t_t<false>(a, st);
 }
 
+int g_p4w_pdl = 1;   // programmatic dependent launch of P4W (AXQ_P4W_PDL=0 disables)
+
 template <bool HALF, int KSX, bool RES = false>
 static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     static unsigned configured = 0;
@@ -82,8 +84,21 @@ static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned g = (unsigned)std::min<int64_t>(work, sms > 0 ? sms : 148);
-    lut_p4w_kernel<HALF, KSX, RES><<<g, p4w::NT, p4w::Geo<HALF, KSX>::SMEM_BYTES, st>>>(a);
-    return (int)cudaGetLastError();
+    // launched with programmatic stream serialization: the kernel's griddepcontrol.wait (after
+    // its prologue) orders it after the previous kernel on the stream
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(p4w::NT);
+    cfg.dynamicSmemBytes = p4w::Geo<HALF, KSX>::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_p4w_pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    P4Args args = a;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, lut_p4w_kernel<HALF, KSX, RES>, args);
+    return (int)(e != cudaSuccess ? e : cudaGetLastError());
 }
 
 int launch_p4w(const P4Args& a, cudaStream_t st) {
