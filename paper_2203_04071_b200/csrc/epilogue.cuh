@@ -58,6 +58,20 @@ __device__ __forceinline__ int8_t epi_quant(float v, float s, float qm) {
     return (int8_t)__float2int_rn(t);
 }
 
+// clamp(rint(fl(v / s))) from a precomputed r = RN(1/s), bit-identical to epi_quant: t = RN(v*r)
+// is within 3 ulp of fl(v/s), so when t sits more than 4 ulp away from a rounding boundary
+// (k + 1/2) both round to the same integer; near a boundary (rare) or for NaN the IEEE division
+// decides.  |t| beyond qm + 3/4 clamps either way.  Saves the per-element division.
+__device__ __forceinline__ int8_t epi_quant_r(float v, float s, float r, float qm) {
+    const float t = __fmul_rn(v, r);
+    const float at = fabsf(t);
+    if (at >= qm + 0.75f) return (int8_t)(t > 0.f ? (int)qm : -(int)qm);
+    const float ti = rintf(t);
+    if (fabsf(t - ti) <= __fsub_rn(0.5f, __fmul_rn(at, 4.76837158e-7f)))   // 4 * 2^-23 relative
+        return (int8_t)__float2int_rn(fminf(fmaxf(ti, -qm), qm));          // rint then clamp == clamp then rint
+    return epi_quant(v, s, qm);
+}
+
 __device__ __forceinline__ void epi_store(float v, int64_t m, int64_t n, int64_t N,
                                           const EpiArgs& e, float s_out, float qm) {
     if (e.y) {

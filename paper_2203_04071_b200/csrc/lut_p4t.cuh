@@ -104,15 +104,16 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 // epilogue (P4's, one row per lane).
 // Per-launch epilogue constants (loaded once per CTA, not per tile).
 struct EpiConst {
-    float sc, s_out, qm;
+    float sc, s_out, qm, r_out;   // r_out = RN(1 / s_out) for epi_quant_r
 };
 __device__ __forceinline__ EpiConst p4t_epi_const(const P4Args& P) {
     const EpiArgs& e = P.mm.ep;
-    EpiConst k{0.f, 1.f, 127.f};
+    EpiConst k{0.f, 1.f, 127.f, 1.f};
     if (P.mm.C_out == nullptr) {
         k.sc = __fmul_rn(*e.sa, *e.sw);
         k.s_out = e.q ? *e.s_out : 1.f;
         k.qm = (float)((1 << ((e.q ? e.bits_out : 8) - 1)) - 1);
+        k.r_out = __frcp_rn(k.s_out);
     }
     return k;
 }
@@ -128,15 +129,19 @@ __device__ __forceinline__ bool p4t_vec_ok(const P4Args& P, int64_t n0) {
            (!e.q || (((e.ldq & 3) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 3) == 0)));
 }
 
+template <bool FASTQ = false>
 __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
                                               int splits, const EpiConst& kc, const float4* res_pre);
 
 __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
                                               int splits) {
-    p4t_store_row(P, m, n0, eacc, splits, p4t_epi_const(P), nullptr);
+    p4t_store_row<false>(P, m, n0, eacc, splits, p4t_epi_const(P), nullptr);
 }
 
-// res_pre: the row's 4 residual float4 groups already loaded (vector path only), or null
+// res_pre: the row's 4 residual float4 groups already loaded (vector path only), or null.
+// FASTQ: requantize through the reciprocal (epi_quant_r) -- used by the residual-layer
+// instantiation only (elsewhere its registers cost more than the division it saves)
+template <bool FASTQ>
 __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
                                               int splits, const EpiConst& kc, const float4* res_pre) {
     using namespace p4;
@@ -220,7 +225,9 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
             if (e.q) {
                 uint32_t w = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) w |= (uint32_t)(uint8_t)epi_quant(v[j], s_out, qm) << (8 * j);
+                for (int j = 0; j < 4; ++j)
+                    w |= (uint32_t)(uint8_t)(FASTQ ? epi_quant_r(v[j], s_out, kc.r_out, qm) : epi_quant(v[j], s_out, qm))
+                         << (8 * j);
                 qw[n / 4] = w;
                 if (!q16) *reinterpret_cast<uint32_t*>(e.q + m * e.ldq + nn) = w;
             }

@@ -57,7 +57,8 @@ struct Geo {
     // full[S], empty[S], mma[S], tile_full[2], tmem_free[2], then tmem address, flag
     static constexpr int NBAR = 3 * STAGES + 4;
     static constexpr int SMEM_MISC = SMEM_BAR + 8 * NBAR;
-    static constexpr int SMEM_TAP = SMEM_MISC + 16;
+    static constexpr int SMEM_KC = SMEM_MISC + 16;                 // EpiConst (16 B)
+    static constexpr int SMEM_TAP = SMEM_KC + 16;
     static constexpr int SMEM_BYTES = SMEM_TAP + p4::TAP_BYTES;
 };
 }  // namespace p4w
@@ -298,7 +299,11 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
         const uint32_t t_e = tmem + t_lane + 256u + slice_col;
         constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) | ((128u >> 4) << 24);
         const bool mma_thread = (tid == 0);
-        const EpiConst kconst = p4t_epi_const(P);   // per-launch epilogue scalars, loaded once
+        // per-launch epilogue scalars: loaded once into shared memory (not held in registers
+        // across the lookup loop)
+        EpiConst& kconst = *reinterpret_cast<EpiConst*>(smem + G::SMEM_KC);
+        if (tid == 0) kconst = p4t_epi_const(P);
+        consumer_sync();
         const uint32_t one = P.one;   // = 1, opaque to the compiler (keeps those adds on the FMA pipe)
         Gen g;
         gen_init(g);
@@ -453,10 +458,10 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                             eacc[4 * j] += v.x; eacc[4 * j + 1] += v.y; eacc[4 * j + 2] += v.z; eacc[4 * j + 3] += v.w;
                         }
                     }
-                    if (m < p.M) p4t_store_row(P, m, n0, eacc, 1, kconst, pre ? res : nullptr);
+                    if (m < p.M) p4t_store_row<RES>(P, m, n0, eacc, 1, kconst, pre ? res : nullptr);
                 }
             } else if (m < p.M) {
-                p4t_store_row(P, m, n0, eacc, splits, kconst, pre ? res : nullptr);
+                p4t_store_row<RES>(P, m, n0, eacc, splits, kconst, pre ? res : nullptr);
             }
         }
     }

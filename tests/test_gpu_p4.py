@@ -217,3 +217,29 @@ def test_gemm_xs_activation_specialised(ax, M, N, K):
         np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
     finally:
         ax.axq_wpack_kernel(prev)
+
+
+@pytest.mark.parametrize("s_out", [2.0, 0.5, 3.0, 0.1, 7.3])
+def test_requantize_ties_and_boundaries(ax, s_out):
+    """The packed-table epilogue's requantize (reciprocal fast path + exact fallback) against the
+    oracle's IEEE division: s_a*s_w = 1 makes y the integer sums, so s_out = 2 puts every odd sum
+    exactly on a .5 tie (half-even), and the other scales land near rounding boundaries."""
+    M, N, K = 2048, 48, 64
+    T = datagen.lut_randerr(8, 0, 2)
+    A = datagen.random_int8(801, (M, K), full_range=False)
+    W = datagen.random_int8(802, (N, K))
+    acc = oracle.lut_gemm(A, W, T, 8)
+    y_ref = oracle.dequantize(acc, np.float32(1.0), np.float32(1.0))
+    q_ref = oracle.quantize(y_ref, np.float32(s_out), 8)
+    lut = ax.Lut(8, T)
+    wp = ax.WPack(lut, _t(W))
+    y = torch.empty(M, N, device=DEV)
+    q = torch.empty(M, N, dtype=torch.int8, device=DEV)
+    ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
+    one = torch.ones(1, device=DEV)
+    so = torch.tensor([s_out], device=DEV)
+    ep = ax.make_epilogue(one, one, y=y, ldy=N, workspace=ws, q_out=q, ldq=N, d_scale_out=so, bits_out=8)
+    ax.axq_lut_gemm_wp(_t(A), wp, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+    np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
