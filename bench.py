@@ -216,7 +216,10 @@ class ResNetWL:
         self.lookups_total = total * self.net.lookups_per_image()
         self.logits_all = torch.empty(total, 1000, device=dev)
         self.out_host = torch.empty(total, 1000).pin_memory()
-        self.launches = 53 + 1 + 1 + 1 + 1 + 0      # 53 convs, fc, quantize, maxpool, avgpool
+        # 53 convs, stem im2col, fc (table build + GEMM when activation-specialised), quantize,
+        # maxpool, avgpool (static fallback; the bench counts launches with CUPTI)
+        fc_x = any("fc_xp" in b for b in self.net._bufs.values())
+        self.launches = 53 + 1 + (3 if fc_x else 1) + 3
         self.in_bytes = self.x.numel() * 4
         self.out_bytes = self.logits_all.numel() * 4 if rank == 0 else 0
         self.desc = {"workload": "BJ configs[3]: ResNet-50-shaped approximate forward (53 convs + "
@@ -316,13 +319,15 @@ class LinearWL:
         self.timer = timer
         self.lookups_rank = M * self.layer.N * self.layer.K
         self.lookups_total = self.lookups_rank * world
-        self.launches = 5
+        self.launches = 3 + (3 if self.layer.use_xspec(M) else 1)   # amax, scale, quantize + LUT
         self.in_bytes, self.out_bytes = self.x.numel() * 4, self.y.numel() * 4
         self.desc = {"workload": "BJ configs[1]: approximate linear, x fp32 [256x1024] N(0,1), W "
                                  "[1024x1024] N(0,0.02), bias N(0,0.01), trunc4 LUT, fp32 output",
-                     "kernel_path": "activation-specialised packed tables built per call "
-                                    "(axq_wpack_repack) + P4W (axq_lut_gemm_xs)"
-                                    if self.layer.use_xspec(M) else "per-row gather (v1)"}
+                     "kernel_path": {"xspec": "activation-specialised packed tables built per "
+                                              "call (axq_wpack_repack) + 512-row P4W "
+                                              "(axq_lut_gemm_xs)",
+                                     "wpack": "weight-specialised packed tables + P4W",
+                                     "gather": "per-row gather (v1)"}[self.layer.path(M)]}
 
     def step(self, stream, dist):
         ax, L = self.ax, self.layer
@@ -363,7 +368,7 @@ class LstmWL:
         per_b = self.nets[8].lookups(T, B)
         self.lookups_rank = 3 * per_b
         self.lookups_total = self.lookups_rank * world
-        self.launches = 3 * (2 + T * 5)
+        self.launches = 3 * 3   # per bit width: quantize x, ih GEMM, persistent recurrence
         self.in_bytes = self.x.numel() * 4
         self.out_bytes = 3 * T * B * 1024 * 4
         self.h_host = torch.empty(3, T, B, 1024).pin_memory()
@@ -407,6 +412,22 @@ class LstmWL:
 WORKLOADS = {"resnet": ResNetWL, "conv": ConvWL, "linear": LinearWL, "lstm": LstmWL}
 
 
+def count_launches(wl, stream, dist):
+    """Kernels of this library (namespace axq::) one step launches, counted by the CUDA profiler
+    (CUPTI activity records, graph replays included) over one untimed step; None when the
+    profiler is unavailable (the workload's static count is reported instead)."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            wl.step(stream, dist)
+            torch.cuda.synchronize()
+        n = sum(1 for e in prof.events() if "axq::" in e.name)
+        return n if n > 0 else None
+    except Exception:
+        return None
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -427,6 +448,8 @@ def run_ours(args, rank, world, local_rank):
 
     for _ in range(max(args.warmup, 0)):
         wl.step(stream, dist)
+    torch.cuda.synchronize()
+    launches_step = count_launches(wl, stream, dist)
     torch.cuda.synchronize()
     if hasattr(wl, "per_bit_ms"):
         wl.per_bit_ms.clear()
@@ -535,7 +558,9 @@ def run_ours(args, rank, world, local_rank):
                          "traffic": committed_traffic(wl.name)},
             "clocks": clocks,
             "e2e": e2e,
-            "gpu_launches": wl.launches * args.steps,
+            "gpu_launches": (launches_step if launches_step else wl.launches) * args.steps,
+            "gpu_launches_source": "CUPTI (torch.profiler) count of axq:: kernels in one untimed "
+                                   "step x steps" if launches_step else "static per-step count x steps",
         }
     if dist:
         dist.barrier()

@@ -783,6 +783,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
+static int g_p4w_cw = 0;                // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
 static int64_t g_sk_min_stages = 1;    // AXQ_SK_MIN_STAGES: measured best at 1 (every SM takes a piece)
 static int64_t g_p4w_ks16_max_k = 0;   // AXQ_P4W_KS16_MAX_K: measured slower, off
 static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 2 P4T, 3 P4W
@@ -822,7 +823,9 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     // P4's 2 rows per lane measure faster
     const int variant = g_wpack_kernel != 0 ? g_wpack_kernel : (a.c4 ? 1 : 3);
     const bool use_tc = variant >= 2;                                 // P4T / P4W: tcgen05 exact part
-    const int bm = variant == 3 ? 896 : 1024;
+    // P4W shape: 512-row tiles (16 consumer warps) for small row counts, where 896-row tiles
+    // would leave lanes idle or cut a ragged second tile; not for residual epilogues or the
+    // half-range 16-k stages (no such instantiation)
     // k per stage: P4T 32 (half) / 16; P4W the same, except half-range tables with K <= 128
     // (short tiles: 16-k stages, 4 deep)
     static bool env_read = false;
@@ -830,9 +833,16 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         if (const char* v = std::getenv("AXQ_P4W_KS16_MAX_K")) g_p4w_ks16_max_k = std::atoll(v);
         if (const char* v = std::getenv("AXQ_SK_MIN_STAGES")) g_sk_min_stages = std::max(1LL, std::atoll(v));
         if (const char* v = std::getenv("AXQ_P4W_PDL")) axq::g_p4w_pdl = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_P4W_CW")) g_p4w_cw = std::atoi(v);
         env_read = true;
     }
     a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
+    const bool res_ep = ep && ep->residual;
+    a.cw = 28;
+    if (variant == 3 && !res_ep && !a.c4 && (!wp->half || a.ks == 32) && g_p4w_cw != 28 &&
+        (g_p4w_cw == 16 || a.mm.M <= 1024))
+        a.cw = 16;
+    const int bm = variant == 3 ? axq::p4w_bm(a.cw) : 1024;
     if (use_tc)
         axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, a.ks, bm, sm_count(), can_split && !a.transposed, a.splits,
                       a.stages_per_split);

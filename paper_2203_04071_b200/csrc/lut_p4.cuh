@@ -509,33 +509,59 @@ __global__ void __launch_bounds__(p4::NT, 1) lut_p4_kernel(const __grid_constant
 // are activations x and the looked-up row code u is a weight, so the byte is E[x][u] + 128
 // (used to build tables from a small activation matrix per call, axq_lut_gemm_xs); the
 // caller then passes the transposed table ([ua][uw]) so the reads stay row-contiguous.
-// One block per (nb, k): the 16 packed codes are read once, the 4 x rows words written.
-__global__ void p4_pack_tables_kernel(const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw,
-                                      int64_t Kp, const int8_t* __restrict__ dtab,
-                                      uint32_t* __restrict__ tables, int rows, int swap) {
-    __shared__ int codes[p4::TN];
+// Persistent blocks with the 64 KiB packing table staged in shared memory.  Work items are
+// (nb, 64-k chunk): the chunk's 16 x 64 packed codes are read once (coalesced), then per k each
+// thread writes 4 consecutive words of one quad: the 4 codes' table rows are read 4 bytes at a
+// time (u .. u+3), biased (E + 128 == E ^ 0x80 for an int8 E) and byte-transposed with 8
+// PRMTs, one 16-byte store.  (A [k][u][quad] layout -- one 16-byte lookup load per k in the
+// GEMM kernels -- measured slower there: more bank-conflict wavefronts per lookup.)
+constexpr int PACK_THREADS = 256;
+constexpr int PACK_KC = 64;
+__global__ void __launch_bounds__(PACK_THREADS) p4_pack_tables_kernel(
+        const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw, int64_t Kp,
+        const int8_t* __restrict__ dtab, uint32_t* __restrict__ tables, int rows, int swap) {
+    extern __shared__ __align__(16) uint8_t pk_tab[];   // [256 codes][256 u]
+    __shared__ uint8_t codes[p4::TN][PACK_KC];
+    {   // all 16 loads of a thread in flight at once (not 16 dependent L2 round trips)
+        uint4 v[65536 / 16 / PACK_THREADS];
+#pragma unroll
+        for (int i = 0; i < 65536 / 16 / PACK_THREADS; ++i)
+            v[i] = __ldg(reinterpret_cast<const uint4*>(dtab) + threadIdx.x + i * PACK_THREADS);
+#pragma unroll
+        for (int i = 0; i < 65536 / 16 / PACK_THREADS; ++i)
+            reinterpret_cast<uint4*>(pk_tab)[threadIdx.x + i * PACK_THREADS] = v[i];
+    }
     const int64_t n_blocks = (N + p4::TN - 1) / p4::TN;
-    for (int64_t blk = blockIdx.x; blk < n_blocks * Kp; blk += gridDim.x) {
-        const int64_t k = blk % Kp, nb = blk / Kp;
+    const int64_t k_chunks = (Kp + PACK_KC - 1) / PACK_KC;
+    const int per_q = rows / 4;                          // uint4 groups per quad
+    const int q = threadIdx.x / per_q, u4 = (threadIdx.x - q * per_q) * 4;
+    const bool active = threadIdx.x < 4 * per_q;
+    for (int64_t item = blockIdx.x; item < n_blocks * k_chunks; item += gridDim.x) {
+        const int64_t nb = item / k_chunks, k0 = (item - nb * k_chunks) * PACK_KC;
+        const int kn = (int)min((int64_t)PACK_KC, Kp - k0);
         __syncthreads();
-        if (threadIdx.x < p4::TN) {
-            const int64_t n = nb * p4::TN + threadIdx.x;
-            codes[threadIdx.x] = (n < N && k < K) ? (int)W[n * ldw + k] : 0;
+        for (int i = threadIdx.x; i < p4::TN * PACK_KC; i += PACK_THREADS) {
+            const int j = i / PACK_KC, kk = i - j * PACK_KC;
+            const int64_t n = nb * p4::TN + j, k = k0 + kk;
+            codes[j][kk] = (n < N && k < K) ? (uint8_t)W[n * ldw + k] : 0;
         }
         __syncthreads();
-        uint32_t* dst = tables + blk * 4 * rows;
-        for (int idx = threadIdx.x; idx < 4 * rows; idx += blockDim.x) {
-            const int q = idx / rows, u = idx - q * rows;
-            uint32_t word = 0;
+        if (!active) continue;
+        uint32_t* dst = tables + (nb * Kp + k0) * 4 * rows + q * rows + u4;
+#pragma unroll 2
+        for (int kk = 0; kk < kn; ++kk) {
+            uint32_t w[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int c = codes[4 * q + j] & 0xff;
-                // dtab is [uw][ua] (E[ua][uw] at (uw << 8) | ua) for weight packing, and the
-                // transposed copy [ua][uw] for activation packing: both read contiguous rows
-                const int e = (int)__ldg(dtab + ((c << 8) | u));
-                word |= (uint32_t)(uint8_t)(e + p4::E_BIAS) << (8 * j);
-            }
-            dst[idx] = word;
+            for (int j = 0; j < 4; ++j)
+                w[j] = *reinterpret_cast<const uint32_t*>(pk_tab + ((int)codes[4 * q + j][kk] << 8) + u4) ^ 0x80808080u;
+            const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140), hi01 = __byte_perm(w[0], w[1], 0x7362);
+            const uint32_t lo23 = __byte_perm(w[2], w[3], 0x5140), hi23 = __byte_perm(w[2], w[3], 0x7362);
+            uint4 o;
+            o.x = __byte_perm(lo01, lo23, 0x5410);
+            o.y = __byte_perm(lo01, lo23, 0x7632);
+            o.z = __byte_perm(hi01, hi23, 0x5410);
+            o.w = __byte_perm(hi01, hi23, 0x7632);
+            *reinterpret_cast<uint4*>(dst + (int64_t)kk * 4 * rows) = o;
         }
     }
 }

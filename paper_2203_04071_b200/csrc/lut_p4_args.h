@@ -55,9 +55,10 @@ struct P4Args {
     int sk_ctas;                // P4W stream-K: CTAs sharing the tail (0 = all)
     int ks;                     // P4W: k per stage (16 or 32; 16 with half tables = 4 stages)
     int transposed;             // P4W: output element (row r, col c) goes to [c][r] (gemm_xs)
+    int cw;                     // P4W consumer warps (tile rows / 32): 28 (default) or 16
     int nb_fast;                // tile order: column block fastest (the layer's tables stay in
                                 // L2 and each activation tile is read from HBM once) instead of
-                                // row tile fastest (concurrent CTAs share one table stream)               // = 1 (opaque to the compiler: keeps the adds on the FMA pipe)
+                                // row tile fastest (concurrent CTAs share one table stream)
 };
 
 }  // namespace axq

@@ -27,27 +27,46 @@
 namespace axq {
 
 namespace p4w {
-constexpr int CW = 28;                     // consumer warps
 constexpr int PW = 4;                      // producer warps
-constexpr int NT = (CW + PW) * 32;         // 1024 threads
-constexpr int BM = CW * 32;                // 896 rows per tile
-constexpr int SLICES = BM / 128;           // 7 MMA slices
-constexpr int PT = PW * 32;                // 128 producer threads
-constexpr int RPT = BM / PT;               // 7 rows per producer thread
 constexpr int TN = p4::TN;
 constexpr int W_STAGE = 512;
 constexpr int TMEM_COLS = 512;             // exact sets at 0 and 128, E sums at 256
 
-template <bool HALF, int KSX = (HALF ? 32 : 16)>
+// CTA shape: CWX consumer warps (one tile row per lane).  28 (896-row tiles, 1024 threads) is
+// the default; 16 (512-row tiles, 640 threads) serves small row counts (M <= 1024), where 896-row
+// tiles would leave most lanes idle or cut a ragged second tile.
+template <int CWX>
+struct Shape {
+    static constexpr int CW = CWX;                 // consumer warps
+    static constexpr int NT = (CW + PW) * 32;      // threads
+    static constexpr int BM = CW * 32;             // rows per tile
+    static constexpr int SLICES = BM / 128;        // MMA slices of 128 rows
+    static constexpr int PT = PW * 32;             // 128 producer threads
+    static constexpr int RPT = BM / PT;            // rows per producer thread
+    static_assert(BM % 128 == 0, "tile rows must be whole MMA slices");
+};
+constexpr int CW = 28;
+constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots are sized for it)
+
+#ifndef P4W_SMALL_FULL_STAGES
+#define P4W_SMALL_FULL_STAGES 3
+#endif
+template <bool HALF, int KSX = (HALF ? 32 : 16), int CWX = 28>
 struct Geo {
+    static constexpr int BM = Shape<CWX>::BM;
     static constexpr int KS = KSX;
     static constexpr int TROWS = HALF ? 128 : 256;
     static constexpr int TQ = TROWS * 4;
     static constexpr int TBL_STAGE = KS * (TN / 4) * TQ;   // 64 KiB
     static constexpr int A_STAGE = BM * KS;                // KS / 16 planes of [BM][16 B]
     // half-range tables in 16-k stages (small-K layers): 4 stages of 32 KiB, a deeper pipeline
-    // across the short tiles; otherwise 2 stages of 64 KiB
-    static constexpr int STAGES = (HALF && KS == 16) ? 4 : 2;
+    // across the short tiles; the 512-row shape with full-range tables: 3 stages of 64 KiB
+    // (few rows per table byte: the table stream, not the lookups, sets the pace); otherwise 2
+    static constexpr bool SMALL_FULL = (CWX == 16 && !HALF);
+    static constexpr int STAGES = (HALF && KS == 16) ? 4 : SMALL_FULL ? P4W_SMALL_FULL_STAGES : 2;
+    // the 4-byte-tap conv loader's tap table (not in the SMALL_FULL shape: no room; the host
+    // never picks it for such layers)
+    static constexpr bool HAS_TAP = !SMALL_FULL;
     static constexpr int FLUSH_STAGES = 256 / KS;
     static constexpr int SMEM_TBL = 0;
     static constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
@@ -59,7 +78,8 @@ struct Geo {
     static constexpr int SMEM_MISC = SMEM_BAR + 8 * NBAR;
     static constexpr int SMEM_KC = SMEM_MISC + 16;                 // EpiConst (16 B)
     static constexpr int SMEM_TAP = SMEM_KC + 16;
-    static constexpr int SMEM_BYTES = SMEM_TAP + p4::TAP_BYTES;
+    static constexpr int SMEM_BYTES = SMEM_TAP + (HAS_TAP ? p4::TAP_BYTES : 0);
+    static_assert(SMEM_BYTES <= 232448, "P4W shared memory exceeds 227 KiB");
 };
 }  // namespace p4w
 
@@ -71,17 +91,20 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void consumer_sync() {   // named barrier 1: the 896 consumer threads
-    asm volatile("bar.sync 1, %0;\n" ::"n"(p4w::BM) : "memory");
+template <int BM_>
+__device__ __forceinline__ void consumer_sync() {   // named barrier 1: the BM_ consumer threads
+    asm volatile("bar.sync 1, %0;\n" ::"n"(BM_) : "memory");
 }
 
 // RES: a separate instantiation for layers with a residual input, whose epilogue loads the
 // residual rows before waiting on the tile's MMAs (their latency overlaps the wait).  Kept out
 // of the other layers' instantiation: its extra live registers would spill into their loop.
-template <bool HALF, int KSX, bool RES = false>
-__global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_constant__ P4Args P) {
+template <bool HALF, int KSX, bool RES = false, int CWX = 28>
+__global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const __grid_constant__ P4Args P) {
     using namespace p4w;
-    using G = p4w::Geo<HALF, KSX>;
+    using G = p4w::Geo<HALF, KSX, CWX>;
+    using S = p4w::Shape<CWX>;
+    constexpr int CW = S::CW, NT = S::NT, BM = S::BM, SLICES = S::SLICES, PT = S::PT, RPT = S::RPT;
     constexpr int KS = G::KS, STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ, A_STAGE = G::A_STAGE;
     constexpr int NPL = KS / 16;
     extern __shared__ __align__(1024) uint8_t p4w_smem[];
@@ -97,7 +120,7 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + G::SMEM_MISC);
     int* fin_flag = reinterpret_cast<int*>(smem + G::SMEM_MISC + 4);
 
-    if (P.c4) {
+    if (G::HAS_TAP && P.c4) {
         uint32_t* tap_w = reinterpret_cast<uint32_t*>(smem + G::SMEM_TAP);
         const int ng = (int)(P.Kp / 4);
         for (int g = tid; g < ng; g += NT) {
@@ -303,7 +326,7 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
         // across the lookup loop)
         EpiConst& kconst = *reinterpret_cast<EpiConst*>(smem + G::SMEM_KC);
         if (tid == 0) kconst = p4t_epi_const(P);
-        consumer_sync();
+        consumer_sync<BM>();
         const uint32_t one = P.one;   // = 1, opaque to the compiler (keeps those adds on the FMA pipe)
         Gen g;
         gen_init(g);
@@ -432,7 +455,7 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                 for (int j = 0; j < TN / 4; ++j)
                     __stcg(part + j, make_int4(eacc[4 * j], eacc[4 * j + 1], eacc[4 * j + 2], eacc[4 * j + 3]));
                 __threadfence();
-                consumer_sync();
+                consumer_sync<BM>();
                 int64_t c_first = ((x0 - t_dp * nst_all) * G_sk) / it_sk;
                 while (c_first + 1 < G_sk && sk_begin(c_first + 1) <= x0) ++c_first;
                 if (tid == 0) {
@@ -441,9 +464,9 @@ __global__ void __launch_bounds__(p4w::NT, 1) lut_p4w_kernel(const __grid_consta
                     if (fin) P.cnt[c_first] = 0;
                     *fin_flag = fin;
                 }
-                consumer_sync();
+                consumer_sync<BM>();
                 const int fin = *fin_flag;
-                consumer_sync();   // fin_flag is reused by the next piece
+                consumer_sync<BM>();   // fin_flag is reused by the next piece
                 if (fin) {
                     __threadfence();
                     const int64_t x1 = x0 + nst_all;   // one past the tile's last iteration

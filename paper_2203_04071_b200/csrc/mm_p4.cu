@@ -11,8 +11,18 @@ int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, cons
     const int64_t nb = (N + p4::TN - 1) / p4::TN;
     const int rows = half ? 128 : 256;
     const int64_t t2 = nb * Kp * p4::TN;
-    p4_pack_tables_kernel<<<(unsigned)std::min<int64_t>(nb * Kp, 148 * 64), 256, 0, st>>>(
-        W, N, K, ldw, Kp, dtab, tables, rows, swap);
+    static unsigned pack_configured = 0;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (!(pack_configured & (1u << (dev & 31)))) {
+        cudaError_t e = cudaFuncSetAttribute(p4_pack_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        if (e != cudaSuccess) return (int)e;
+        pack_configured |= 1u << (dev & 31);
+    }
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = nb * ((Kp + PACK_KC - 1) / PACK_KC);
+    p4_pack_tables_kernel<<<(unsigned)std::min<int64_t>(items, (int64_t)(sms > 0 ? sms : 148) * 3), PACK_THREADS,
+                            65536, st>>>(W, N, K, ldw, Kp, dtab, tables, rows, swap);
     p4_pack_w_kernel<<<(unsigned)std::min<int64_t>((t2 + 255) / 256, 148 * 16), 256, 0, st>>>(W, N, K, ldw, Kp, wpk);
     return (int)cudaGetLastError();
 }
@@ -67,19 +77,21 @@ int launch_p4t(const P4Args& a, cudaStream_t st) {
 
 int g_p4w_pdl = 1;   // programmatic dependent launch of P4W (AXQ_P4W_PDL=0 disables)
 
-template <bool HALF, int KSX, bool RES = false>
+template <bool HALF, int KSX, bool RES = false, int CWX = 28>
 static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
+    using G = p4w::Geo<HALF, KSX, CWX>;
+    using S = p4w::Shape<CWX>;
     static unsigned configured = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     dev &= 31;
     if (!(configured & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(lut_p4w_kernel<HALF, KSX, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             p4w::Geo<HALF, KSX>::SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(lut_p4w_kernel<HALF, KSX, RES, CWX>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
         if (e != cudaSuccess) return (int)e;
         configured |= 1u << dev;
     }
-    const int64_t tiles = ((a.mm.M + p4w::BM - 1) / p4w::BM) * ((a.mm.N + p4::TN - 1) / p4::TN);
+    const int64_t tiles = ((a.mm.M + S::BM - 1) / S::BM) * ((a.mm.N + p4::TN - 1) / p4::TN);
     const int64_t work = a.streamk ? tiles * (a.Kp / KSX) : tiles * a.splits;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -88,8 +100,8 @@ static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     // its prologue) orders it after the previous kernel on the stream
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(g);
-    cfg.blockDim = dim3(p4w::NT);
-    cfg.dynamicSmemBytes = p4w::Geo<HALF, KSX>::SMEM_BYTES;
+    cfg.blockDim = dim3(S::NT);
+    cfg.dynamicSmemBytes = G::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -97,14 +109,23 @@ static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     P4Args args = a;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, lut_p4w_kernel<HALF, KSX, RES>, args);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, lut_p4w_kernel<HALF, KSX, RES, CWX>, args);
     return (int)(e != cudaSuccess ? e : cudaGetLastError());
 }
 
+int p4w_bm(int cw) { return cw == 16 ? p4w::Shape<16>::BM : p4w::Shape<28>::BM; }
+
 int launch_p4w(const P4Args& a, cudaStream_t st) {
+    const bool res = a.mm.ep.residual != nullptr && a.mm.C_out == nullptr;
+    if (a.cw == 16) {   // small-row-count shape (512-row tiles), chosen by the host (p4w_cw_ok)
+        if (res || a.c4) return (int)cudaErrorInvalidValue;
+        if (!a.half) return launch_p4w_t<false, 16, false, 16>(a, st);
+        if (a.ks == 32) return launch_p4w_t<true, 32, false, 16>(a, st);
+        return (int)cudaErrorInvalidValue;
+    }
     if (!a.half) return launch_p4w_t<false, 16>(a, st);
     if (a.ks == 16) return launch_p4w_t<true, 16>(a, st);
-    if (a.mm.ep.residual != nullptr && a.mm.C_out == nullptr) return launch_p4w_t<true, 32, true>(a, st);
+    if (res) return launch_p4w_t<true, 32, true>(a, st);
     return launch_p4w_t<true, 32>(a, st);
 }
 

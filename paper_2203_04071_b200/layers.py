@@ -34,37 +34,66 @@ class ApproxLinear:
         self.d_scale_a = torch.empty(1, device=device)
         self._bufs = {}
 
-    xspec = False   # measured on BJ configs[1] (256 x 1024 x 1024): table build 80 us + P4W
-                    # 115 us vs 83 us for the per-row gather, so it is opt-in
+    # Kernel path by input rows M (xspec: None = automatic, True / False force the
+    # activation-specialised path).  Measured (L2 flushed), e.g. K = 1024, N = 1024:
+    #   M = 128: per-row gather 54 us = activation-specialised 55 us
+    #   M = 256: gather 79, activation-specialised tables (build 17 + 512-row P4W 49) 68 us
+    #   M = 512: gather 118, weight-specialised packed tables (512-row P4W) 77 us
+    # and at K = 2048, N = 1000 (the ResNet fc): M = 32 gather 48 vs 77; M = 256 gather 132 vs 110.
+    xspec = None
+    XS_MIN_M, WP_MIN_M = 192, 384
+
+    def _packable(self) -> bool:
+        return self.lut.repr == "delta8" and self.K % 16 == 0 and self.K >= 64 and self.N >= 256
+
+    def path(self, M: int) -> str:
+        """'gather' (per-row gather kernel), 'xspec' (tables of this call's activations, built
+        per call) or 'wpack' (tables of the weights, built once)."""
+        if self.xspec is True and self._packable() and M <= 2048:
+            return "xspec"
+        if self.xspec is False or not self._packable():
+            return "gather"
+        if self.XS_MIN_M <= M < self.WP_MIN_M and self.N >= 2 * M:
+            return "xspec"
+        if M >= self.WP_MIN_M:
+            return "wpack"
+        return "gather"
 
     def use_xspec(self, M: int) -> bool:
-        """Activation-specialised packed tables (axq_lut_gemm_xs) for a small input matrix
-        against a large weight matrix; the per-row gather kernel otherwise."""
-        return (self.xspec and self.lut.repr == "delta8" and M <= 2048 and self.K % 16 == 0
-                and self.N >= 256 and self.K >= 64)
+        return self.path(M) == "xspec"
 
     def buffers(self, M: int, device):
         b = self._bufs.get(M)
         if b is None:
             b = dict(qa=torch.empty(M, self.K, dtype=torch.int8, device=device),
                      ws=torch.zeros(M, self.N, dtype=torch.int32, device=device))
-            if self.use_xspec(M):
+            pth = self.path(M)
+            if pth == "xspec":
                 # per-call activation tables (M x K x 1 KiB / 4 B) and their packed operand tile
                 b["xp"] = ax.WPack(self.lut, b["qa"], activations=True)
+            elif pth == "wpack" and self._wp is None:
+                self._wp = ax.WPack(self.lut, self.qw)          # 256 x K x N bytes, once
             self._bufs[M] = b
         return b
+
+    _wp = None
 
     def gemm_q(self, qa, d_scale_a, y, stream=None, hook=None):
         """LUT-GEMM + fused dequantize + bias of the quantized input qa [M][K] into y [M][N]."""
         M = qa.shape[0]
         b = self.buffers(M, qa.device)
+        pth = self.path(M)
         if hook:
             hook("pre", stream)
-        if "xp" in b:
+        if pth == "xspec":
             ax.axq_wpack_repack(b["xp"], qa, stream)           # tables of this call's activations
             ep = ax.make_epilogue(d_scale_a, self.d_scale_w, bias=self.bias, y=y, ldy=y.stride(0),
                                   workspace=b["ws"])
             ax.axq_lut_gemm_xs(self.qw, b["xp"], ep, stream=stream)
+        elif pth == "wpack":
+            ep = ax.make_epilogue(d_scale_a, self.d_scale_w, bias=self.bias, y=y, ldy=y.stride(0),
+                                  workspace=b["ws"])
+            ax.axq_lut_gemm_wp(qa, self._wp, ep, stream=stream)
         else:
             ax.axq_lut_gemm_dq(qa, self.qw, self.lut, d_scale_a, self.d_scale_w, self.bias, y,
                                workspace=b["ws"], stream=stream)

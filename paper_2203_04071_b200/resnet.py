@@ -171,6 +171,11 @@ class ApproxResNet:
         b["pool_f"] = torch.empty(N, cfin, dtype=f32, device=dev)
         b["fc_q"] = torch.empty(N, cfin, dtype=i8, device=dev)
         b["logits"] = torch.empty(N, self.spec["fc"][2], dtype=f32, device=dev)
+        ncls = self.spec["fc"][2]
+        if self.lut.repr == "delta8" and cfin % 16 == 0 and 192 <= N < 384 and ncls >= 2 * N:
+            # fc: few images against 1000 classes -> activation-specialised packed tables, built
+            # per forward from fc_q (axq_wpack_repack) + the 512-row P4W GEMM (axq_lut_gemm_xs)
+            b["fc_xp"] = ax.WPack(self.lut, b["fc_q"], activations=True)
         ws_elems = max(ws_elems, N * self.spec["fc"][2], b["stem_q"].numel())
         b["ws"] = torch.zeros(ws_elems, dtype=torch.int32, device=dev)
         b["shapes"] = shapes
@@ -313,7 +318,11 @@ class ApproxResNet:
                               ldy=lg.shape[-1], workspace=ws, d_scale_w_ch=self.s_w_ch.get("fc"))
         if self.timing_hook:
             self.timing_hook("pre", stream)
-        ax.axq_lut_gemm_ep(b["fc_q"], self.qw["fc"], self.lut, ep, stream)
+        if "fc_xp" in b:
+            ax.axq_wpack_repack(b["fc_xp"], b["fc_q"], stream)
+            ax.axq_lut_gemm_xs(self.qw["fc"], b["fc_xp"], ep, stream=stream)
+        else:
+            ax.axq_lut_gemm_ep(b["fc_q"], self.qw["fc"], self.lut, ep, stream)
         if self.timing_hook:
             self.timing_hook("post", stream)
         if calibrate:

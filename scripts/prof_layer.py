@@ -1,6 +1,7 @@
 """One ResNet-shaped packed-table conv layer with the ResNet epilogue, for ncu captures and
 timing: python scripts/prof_layer.py N H W C K R stride [resid] [reps]
-(resid = 1: fp32 residual + ReLU + fp32 y + int8 q_out, the block-output epilogue; 0: ReLU + q_out)."""
+(resid = 1: fp32 residual + ReLU + fp32 y + int8 q_out, the block-output epilogue; 0: ReLU + q_out;
+2: fp32 y only, the projection shortcut)."""
 import os
 import sys
 
@@ -25,7 +26,10 @@ M = N * Ho * Wo
 sa = torch.tensor([0.01], device="cuda"); sw = torch.tensor([0.01], device="cuda"); so = torch.tensor([0.05], device="cuda")
 q = torch.empty(M, K, dtype=torch.int8, device="cuda")
 ws = torch.zeros(M * K, dtype=torch.int32, device="cuda")
-if resid:
+if resid == 2:   # projection-shortcut epilogue: fp32 y only
+    y = torch.empty(M, K, device="cuda")
+    ep = ax.make_epilogue(sa, sw, y=y, ldy=K, workspace=ws, y_nhwc=True)
+elif resid:
     y = torch.empty(M, K, device="cuda")
     r = torch.randn(M, K, device="cuda")
     ep = ax.make_epilogue(sa, sw, y=y, ldy=K, workspace=ws, residual=r, ldr=K, relu=True, y_nhwc=True,

@@ -231,6 +231,28 @@ def test_config1_linear_full(ax):
     np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
 
 
+@pytest.mark.parametrize("path", ["gather", "xspec", "wpack"])
+def test_config1_linear_paths(ax, path):
+    """The three kernel paths of ApproxLinear (per-row gather, activation-specialised tables
+    built per call, weight-specialised tables) give the oracle's output bit for bit."""
+    from paper_2203_04071_b200.layers import ApproxLinear
+    c = datagen.config1()
+    lut = ax.Lut(8, c.lut)
+    layer = ApproxLinear(_t(c.W), _t(c.b), lut)
+    if path == "gather":
+        layer.xspec = False
+    elif path == "xspec":
+        layer.xspec = True
+    else:
+        layer.XS_MIN_M, layer.WP_MIN_M = 1 << 30, 1
+    assert layer.path(c.x.shape[0]) == path
+    y_ref, _, _ = oracle.linear(c.x, c.W, c.b, c.lut, 8)
+    for _ in range(2):   # the second call reuses the per-M buffers / tables
+        y = layer(_t(c.x))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+
+
 CONV_SHAPES = [
     # N, C, H, W, K, R, S, stride, pad
     (2, 64, 14, 14, 64, 3, 3, 1, 1),
