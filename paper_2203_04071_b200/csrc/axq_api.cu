@@ -783,6 +783,9 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
+static int g_p4w_main_cw = 28;         // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
+static int64_t g_p4w_main_cw_max_k = 1 << 30;   // ... for layers with K up to this
+static int g_p4w_res_cw = 16;          // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape
 static int g_p4w_cw = 0;                // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
 static int64_t g_sk_min_stages = 1;    // AXQ_SK_MIN_STAGES: measured best at 1 (every SM takes a piece)
 static int64_t g_p4w_ks16_max_k = 0;   // AXQ_P4W_KS16_MAX_K: measured slower, off
@@ -834,6 +837,9 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         if (const char* v = std::getenv("AXQ_SK_MIN_STAGES")) g_sk_min_stages = std::max(1LL, std::atoll(v));
         if (const char* v = std::getenv("AXQ_P4W_PDL")) axq::g_p4w_pdl = std::atoi(v);
         if (const char* v = std::getenv("AXQ_P4W_CW")) g_p4w_cw = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_P4W_RES_CW")) g_p4w_res_cw = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_P4W_MAIN_CW")) g_p4w_main_cw = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
         env_read = true;
     }
     a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
@@ -842,6 +848,12 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     if (variant == 3 && !res_ep && !a.c4 && (!wp->half || a.ks == 32) && g_p4w_cw != 28 &&
         (g_p4w_cw == 16 || a.mm.M <= 1024))
         a.cw = 16;
+    if (variant == 3 && res_ep && wp->half && a.ks == 32 && !a.c4 &&
+        (g_p4w_res_cw == 16 || g_p4w_res_cw == 20 || g_p4w_res_cw == 24))
+        a.cw = g_p4w_res_cw;
+    if (variant == 3 && !res_ep && wp->half && a.ks == 32 && !a.c4 && a.cw == 28 &&
+        (g_p4w_main_cw == 20 || g_p4w_main_cw == 24) && wp->Kp <= g_p4w_main_cw_max_k)
+        a.cw = g_p4w_main_cw;
     const int bm = variant == 3 ? axq::p4w_bm(a.cw) : 1024;
     if (use_tc)
         axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, a.ks, bm, sm_count(), can_split && !a.transposed, a.splits,

@@ -39,8 +39,9 @@ int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, cons
 int launch_p4(const P4Args& a, cudaStream_t st);
 int launch_p4t(const P4Args& a, cudaStream_t st);   // tcgen05 exact part, 32 warps (lut_p4t.cuh)
 int launch_p4w(const P4Args& a, cudaStream_t st);
-// P4W tile rows of a shape (cw consumer warps: 28 -> 896, 16 -> 512); launch_p4w serves cw = 16
-// for non-residual layers (full-range, or half-range 32-k tables) and falls back to 28 otherwise
+// P4W tile rows of a shape (cw consumer warps: 28 -> 896, 24 -> 768, 20 -> 640, 16 -> 512);
+// launch_p4w serves cw = 16 for non-residual layers (full-range, or half-range 32-k tables),
+// 20 / 24 for residual layers (half-range 32-k tables), 28 otherwise
 int p4w_bm(int cw);
 extern int g_p4w_pdl;   // warp-specialised P4T (lut_p4w.cuh)
 struct LstmRecArgs;

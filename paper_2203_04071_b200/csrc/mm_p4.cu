@@ -113,20 +113,36 @@ static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     return (int)(e != cudaSuccess ? e : cudaGetLastError());
 }
 
-int p4w_bm(int cw) { return cw == 16 ? p4w::Shape<16>::BM : p4w::Shape<28>::BM; }
+int p4w_bm(int cw) { return cw * 32; }
 
 int launch_p4w(const P4Args& a, cudaStream_t st) {
     const bool res = a.mm.ep.residual != nullptr && a.mm.C_out == nullptr;
-    if (a.cw == 16) {   // small-row-count shape (512-row tiles), chosen by the host (p4w_cw_ok)
-        if (res || a.c4) return (int)cudaErrorInvalidValue;
-        if (!a.half) return launch_p4w_t<false, 16, false, 16>(a, st);
-        if (a.ks == 32) return launch_p4w_t<true, 32, false, 16>(a, st);
-        return (int)cudaErrorInvalidValue;
+    const int cw = a.cw ? a.cw : 28;
+    constexpr int BAD = (int)cudaErrorInvalidValue;
+    if (a.c4 && cw != 28) return BAD;           // the 4-byte-tap table lives in the 28-warp shapes
+    if (!a.half) {                              // full-range tables, 16-k stages
+        if (cw == 16 && !res) return launch_p4w_t<false, 16, false, 16>(a, st);
+        return cw == 28 ? launch_p4w_t<false, 16>(a, st) : BAD;
     }
-    if (!a.half) return launch_p4w_t<false, 16>(a, st);
-    if (a.ks == 16) return launch_p4w_t<true, 16>(a, st);
-    if (res) return launch_p4w_t<true, 32, true>(a, st);
-    return launch_p4w_t<true, 32>(a, st);
+    if (a.ks == 16) return cw == 28 ? launch_p4w_t<true, 16>(a, st) : BAD;
+    if (res) {
+        // residual epilogue: fewer consumer warps leave more registers per thread, so the row's
+        // residual loaded before the tile's MMA wait does not spill
+        switch (cw) {
+            case 16: return launch_p4w_t<true, 32, true, 16>(a, st);
+            case 20: return launch_p4w_t<true, 32, true, 20>(a, st);
+            case 24: return launch_p4w_t<true, 32, true, 24>(a, st);
+            case 28: return launch_p4w_t<true, 32, true>(a, st);
+            default: return BAD;
+        }
+    }
+    switch (cw) {
+        case 16: return launch_p4w_t<true, 32, false, 16>(a, st);
+        case 20: return launch_p4w_t<true, 32, false, 20>(a, st);
+        case 24: return launch_p4w_t<true, 32, false, 24>(a, st);
+        case 28: return launch_p4w_t<true, 32>(a, st);
+        default: return BAD;
+    }
 }
 
 // P4T tiles are 1024 rows: split K (exact, int32 atomics) only when they cannot fill the SMs.
