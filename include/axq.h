@@ -266,6 +266,14 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
  *   28 consumer warps look up, 896-row tiles).  Returns the previous setting, or -1 for an
  *   unknown value (unchanged). */
 int axq_wpack_kernel(int variant);
+/* axq_wpack_shapes: consumer-warp counts of the P4W shapes for the calling process (tile rows =
+ *   32 x warps; a performance switch, all results bit-identical).  main_cw: non-residual layers
+ *   with half-range 32-k tables -- 28 (default), 24 or 20; res_cw: layers with a residual
+ *   epilogue (half-range 32-k) -- 16 (default), 20, 24 or 28; small_cw: non-residual layers
+ *   with M <= 1024 -- 16 (default) or 28 (off).  0 leaves a value unchanged.  The environment
+ *   (AXQ_P4W_MAIN_CW, AXQ_P4W_RES_CW, AXQ_P4W_CW) is read before the first call applies.
+ *   Returns AXQ_ERR_INVALID (nothing changed) for any other value. */
+axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw);
 
 /* ---------------------------------------------------------------------------------
  * Dequantize (unfused), same pinned formula as the epilogue.

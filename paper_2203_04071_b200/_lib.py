@@ -27,7 +27,7 @@ EXPORTED = [
     "axq_dequantize", "axq_dequantize_nhwc_to_nchw", "axq_epilogue_apply",
     "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
     "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
-    "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_lstm_recurrent",
+    "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_wpack_shapes", "axq_lstm_recurrent",
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
@@ -98,6 +98,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_create": ([vp, vp, i64, i64, i64, i32, ctypes.POINTER(vp)], i32),
         "axq_wpack_destroy": ([vp], i32),
         "axq_wpack_kernel": ([i32], i32),
+        "axq_wpack_shapes": ([i32, i32, i32], i32),
         "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
         "axq_quantize16": ([vp, i64, vp, i32, vp, vp], i32),
         "axq_im2col_nhwc_i8": ([vp] + [i64] * 11 + [vp, i64, vp], i32),
@@ -188,6 +189,11 @@ class Lut:
 
 def axq_lut_create(bits: int, host_table: np.ndarray) -> Lut:
     return Lut(bits, host_table)
+
+
+def axq_wpack_shapes(main_cw: int = 0, res_cw: int = 0, small_cw: int = 0) -> None:
+    """P4W consumer-warp counts (include/axq.h axq_wpack_shapes); 0 leaves a value unchanged."""
+    _check("axq_wpack_shapes", load().axq_wpack_shapes(int(main_cw), int(res_cw), int(small_cw)))
 
 
 def axq_wpack_kernel(variant: int) -> int:

@@ -791,6 +791,31 @@ static int64_t g_sk_min_stages = 1;    // AXQ_SK_MIN_STAGES: measured best at 1 
 static int64_t g_p4w_ks16_max_k = 0;   // AXQ_P4W_KS16_MAX_K: measured slower, off
 static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 2 P4T, 3 P4W
 
+static void p4w_read_env() {
+    static bool env_read = false;
+    if (env_read) return;
+    if (const char* v = std::getenv("AXQ_P4W_KS16_MAX_K")) g_p4w_ks16_max_k = std::atoll(v);
+    if (const char* v = std::getenv("AXQ_SK_MIN_STAGES")) g_sk_min_stages = std::max(1LL, std::atoll(v));
+    if (const char* v = std::getenv("AXQ_P4W_PDL")) axq::g_p4w_pdl = std::atoi(v);
+    if (const char* v = std::getenv("AXQ_P4W_CW")) g_p4w_cw = std::atoi(v);
+    if (const char* v = std::getenv("AXQ_P4W_RES_CW")) g_p4w_res_cw = std::atoi(v);
+    if (const char* v = std::getenv("AXQ_P4W_MAIN_CW")) g_p4w_main_cw = std::atoi(v);
+    if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
+    env_read = true;
+}
+
+axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw) {
+    p4w_read_env();
+    if ((main_cw && main_cw != 20 && main_cw != 24 && main_cw != 28) ||
+        (res_cw && res_cw != 16 && res_cw != 20 && res_cw != 24 && res_cw != 28) ||
+        (small_cw && small_cw != 16 && small_cw != 28))
+        return AXQ_ERR_INVALID;
+    if (main_cw) g_p4w_main_cw = main_cw;
+    if (res_cw) g_p4w_res_cw = res_cw;
+    if (small_cw) g_p4w_cw = small_cw == 16 ? 0 : 28;
+    return AXQ_OK;
+}
+
 int axq_wpack_kernel(int variant) {
     if (variant < 0 || variant > 3) return -1;
     const int prev = g_wpack_kernel;
@@ -831,17 +856,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     // half-range 16-k stages (no such instantiation)
     // k per stage: P4T 32 (half) / 16; P4W the same, except half-range tables with K <= 128
     // (short tiles: 16-k stages, 4 deep)
-    static bool env_read = false;
-    if (!env_read) {
-        if (const char* v = std::getenv("AXQ_P4W_KS16_MAX_K")) g_p4w_ks16_max_k = std::atoll(v);
-        if (const char* v = std::getenv("AXQ_SK_MIN_STAGES")) g_sk_min_stages = std::max(1LL, std::atoll(v));
-        if (const char* v = std::getenv("AXQ_P4W_PDL")) axq::g_p4w_pdl = std::atoi(v);
-        if (const char* v = std::getenv("AXQ_P4W_CW")) g_p4w_cw = std::atoi(v);
-        if (const char* v = std::getenv("AXQ_P4W_RES_CW")) g_p4w_res_cw = std::atoi(v);
-        if (const char* v = std::getenv("AXQ_P4W_MAIN_CW")) g_p4w_main_cw = std::atoi(v);
-        if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
-        env_read = true;
-    }
+    p4w_read_env();
     a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
     const bool res_ep = ep && ep->residual;
     a.cw = 28;
