@@ -529,9 +529,10 @@ def run_ours(args, rank, world, local_rank):
             "data": "synthetic (seeded; DESIGN.md input recipe), random-init weights",
             "config": cfg,
             "roofline": {"bound": "smem", "kernel": "LUT kernels (lut_p4w_kernel packed-table "
-                         "tcgen05 path, lut_p4_kernel for the 4-byte-tap stem, lut_mm_kernel for "
-                         "small M, lstm_rec_kernel for the LSTM recurrence: all LUT launches of the "
-                         "step, CUDA events around each on the launching stream)",
+                         "tcgen05 path in its 896- and 512-row shapes, p4_pack_tables_kernel for "
+                         "per-call activation tables, lut_mm_kernel for small M, lstm_rec_kernel "
+                         "for the LSTM recurrence: all LUT launches of the step, CUDA events "
+                         "around each on the launching stream)",
                          "achieved": round(achieved, 2), "peak": round(roof, 2),
                          "unit": "Glookup/s", "frac": round(achieved / roof, 4),
                          "peak_basis": "BASELINE metric's smem-lookup roofline: %d SMs x 32 lanes "
