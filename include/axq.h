@@ -276,6 +276,34 @@ int axq_wpack_kernel(int variant);
 axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw);
 
 /* ---------------------------------------------------------------------------------
+ * NEXT-4: straight-through-estimator backward of an approximate linear layer
+ * (§III.A.2 "Retraining": QAT "based on Straight Through Estimator (STE)
+ * derivative approximation", "fake quantization modules which work with quantized floating
+ * point values").  Under the STE the quantizer and the ACU are the identity in the backward
+ * pass (A36), so with the fake-quantized operands fq(q) = fl32(s * q):
+ *   gx[m][k] = [|x[m][k]| <= clip_a] * sum_n gy[m][n] * fq(qw[n][k])      (fp32 [M][K])
+ *   gw[n][k] = [|w[n][k]| <= clip_w] * sum_m gy[m][n] * fq(qa[m][k])      (fp32 [N][K])
+ *   gb[n]    = sum_m gy[m][n]                                             (fp32 [N])
+ * gy: fp32 [M][N] dL/dy; qa int8 [M][K] / qw int8 [N][K]: the codes the forward used, with
+ * their device scales; x fp32 [M][K] / w fp32 [N][K]: the unquantized operands, with the
+ * calibrated clip ranges (device scalars, e.g. amax; a value with |v| > clip gets no gradient);
+ * x / w null: no mask.  All buffers contiguous, on the current device; gx / gw / gb nullable
+ * (not computed).  workspace (nullable, workspace_elems floats, caller-owned, no contents
+ * required): room for up to 16 K-split partial products of the larger gradient (16 * max(M, N)
+ * * K floats covers every case); used to split the summed dimension when the output alone cannot
+ * fill the SMs (the splits are added in a fixed order, so results are deterministic).  fp32 FMA
+ * accumulation (not bit-exact against a different summation order: within the fp32
+ * dot-product bound).  Asynchronous on stream.  AXQ_ERR_INVALID for negative extents or a
+ * missing operand of a requested gradient.
+ * --------------------------------------------------------------------------------- */
+axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float* gy,
+                                   const int8_t* qa, const float* d_scale_a, const float* x,
+                                   const float* d_clip_a, const int8_t* qw, const float* d_scale_w,
+                                   const float* w, const float* d_clip_w, float* gx, float* gw,
+                                   float* gb, float* workspace, int64_t workspace_elems,
+                                   void* stream);
+
+/* ---------------------------------------------------------------------------------
  * Dequantize (unfused), same pinned formula as the epilogue.
  * axq_dequantize: acc int32 [M][ldacc] -> y fp32 [M][ldy], bias[n] (nullable).
  * axq_dequantize_nhwc_to_nchw: acc int32 NHWC [N][HW][C] -> y fp32 NCHW [N][C][HW].

@@ -28,6 +28,7 @@ EXPORTED = [
     "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
     "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
     "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_wpack_shapes", "axq_lstm_recurrent",
+    "axq_ste_linear_backward",
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
@@ -99,6 +100,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_destroy": ([vp], i32),
         "axq_wpack_kernel": ([i32], i32),
         "axq_wpack_shapes": ([i32, i32, i32], i32),
+        "axq_ste_linear_backward": ([i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp], i32),
         "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
         "axq_quantize16": ([vp, i64, vp, i32, vp, vp], i32),
         "axq_im2col_nhwc_i8": ([vp] + [i64] * 11 + [vp, i64, vp], i32),
@@ -189,6 +191,20 @@ class Lut:
 
 def axq_lut_create(bits: int, host_table: np.ndarray) -> Lut:
     return Lut(bits, host_table)
+
+
+def axq_ste_linear_backward(gy, qa, d_scale_a, qw, d_scale_w, x=None, d_clip_a=None, w=None,
+                            d_clip_w=None, gx=None, gw=None, gb=None, workspace=None,
+                            stream=None) -> None:
+    """NEXT-4 STE backward of an approximate linear layer (include/axq.h): gy [M][N], qa [M][K],
+    qw [N][K] -> gx [M][K], gw [N][K], gb [N] (each optional); workspace: fp32 tensor for
+    K-split partial products (optional)."""
+    M, N = gy.shape
+    K = qa.shape[1] if qa is not None else qw.shape[1]
+    _check("axq_ste_linear_backward", load().axq_ste_linear_backward(
+        M, N, K, _ptr(gy), _ptr(qa), _ptr(d_scale_a), _ptr(x), _ptr(d_clip_a), _ptr(qw),
+        _ptr(d_scale_w), _ptr(w), _ptr(d_clip_w), _ptr(gx), _ptr(gw), _ptr(gb), _ptr(workspace),
+        workspace.numel() if workspace is not None else 0, _stream(stream)))
 
 
 def axq_wpack_shapes(main_cw: int = 0, res_cw: int = 0, small_cw: int = 0) -> None:

@@ -1158,3 +1158,8 @@ axq_status axq_lstm_recurrent(int64_t T, int64_t B, int64_t H, const float* gate
 }
 
 }  // extern "C"
+
+namespace axq {
+// for the other translation units' entry points (mm_ste.cu): record a failed CUDA call
+axq_status cuda_fail_ext(int e) { return cuda_fail((cudaError_t)e); }
+}  // namespace axq

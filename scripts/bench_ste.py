@@ -1,0 +1,50 @@
+"""NEXT-4 measurement: the STE backward of an approximate linear layer (axq_ste_linear_backward:
+gx, gw, gb with clip masks) on BJ configs[1]'s shape and the ResNet fc, L2 flushed before each
+call.  Prints one JSON object: ms, GFLOP/s (2 GEMMs x 2 M N K flops) and the fraction of the
+fp32 FMA peak (148 SMs x 128 lanes x 2 flops x 1.965 GHz = 74.4 TFLOP/s)."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2203_04071_b200 import _lib as ax  # noqa: E402
+
+PEAK = 148 * 128 * 2 * 1.965e9
+
+
+def run(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    gy = torch.randn(M, N, device="cuda", generator=g)
+    x = torch.randn(M, K, device="cuda", generator=g)
+    w = torch.randn(N, K, device="cuda", generator=g) * 0.02
+    qa = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda", generator=g)
+    qw = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda", generator=g)
+    s = torch.tensor([0.01], device="cuda")
+    clip = torch.tensor([3.0], device="cuda")
+    gx, gw, gb = torch.empty(M, K, device="cuda"), torch.empty(N, K, device="cuda"), torch.empty(N, device="cuda")
+    ws = torch.empty(16 * max(M, N) * K, device="cuda")
+    flush = torch.empty(64 << 20, device="cuda")
+    ts = []
+    for i in range(13):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        ax.axq_ste_linear_backward(gy, qa, s, qw, s, x=x, d_clip_a=clip, w=w, d_clip_w=clip,
+                                   gx=gx, gw=gw, gb=gb, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    fl = 2 * 2 * M * N * K
+    return {"M": M, "N": N, "K": K, "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
+            "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3)}
+
+
+if __name__ == "__main__":
+    out = {"metric": "STE backward (NEXT-4) GFLOP/s", "peak_tflops_fp32_fma": round(PEAK / 1e12, 1),
+           "shapes": [run(256, 1024, 1024), run(256, 1000, 2048), run(2048, 4096, 1024)]}
+    print(json.dumps(out))

@@ -1,0 +1,92 @@
+"""GPU parity of the NEXT-4 STE backward (axq_ste_linear_backward) against the oracle.  fp32 FMA
+sums in a different order than the oracle's fp64 products: each gradient must lie within the
+fp32 dot-product bound gamma_n * sum|terms| (n = summed length, gamma_n = n u / (1 - n u),
+u = 2^-24) plus the oracle's own final rounding."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+U = 2.0 ** -24
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _bound(n, absprod, ref):
+    g = n * U / (1 - n * U)
+    return g * absprod + U * np.abs(ref) + 1e-30
+
+
+def _check(ax, M, N, K, seed, masked, split):
+    x = datagen.normal(60 + seed, 1, (M, K))
+    W = datagen.normal(60 + seed, 2, (N, K), 0.05)
+    qa, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(W, 8)
+    gy = datagen.normal(60 + seed, 3, (M, N))
+    clip_a = np.float32(np.quantile(np.abs(x), 0.8)) if masked and x.size else np.float32(0)
+    clip_w = np.float32(np.quantile(np.abs(W), 0.8)) if masked and W.size else np.float32(0)
+    if masked:
+        ref = oracle.ste_linear_backward(gy, qa, sa, qw, sw, x, clip_a, W, clip_w)
+    else:
+        ref = oracle.ste_linear_backward(gy, qa, sa, qw, sw)
+    gx = torch.full((M, K), np.nan, device=DEV)
+    gw = torch.full((N, K), np.nan, device=DEV)
+    gb = torch.full((N,), np.nan, device=DEV)
+    f = lambda v: _t(np.array([v], dtype=np.float32))
+    kw = dict(x=_t(x), d_clip_a=f(clip_a), w=_t(W), d_clip_w=f(clip_w)) if masked else {}
+    ws = torch.full((16 * max(M, N) * K,), np.nan, device=DEV) if split else None
+    ax.axq_ste_linear_backward(_t(gy), _t(qa), f(sa), _t(qw), f(sw), gx=gx, gw=gw, gb=gb,
+                               workspace=ws, **kw)
+    torch.cuda.synchronize()
+    wf, xf = np.abs(oracle.fake_quant(qw, sw)).astype(np.float64), np.abs(oracle.fake_quant(qa, sa)).astype(np.float64)
+    ag = np.abs(gy).astype(np.float64)
+    for got, r, n, absprod in ((gx, ref[0], N, ag @ wf), (gw, ref[1], M, ag.T @ xf),
+                               (gb, ref[2], M, ag.sum(0))):
+        got = got.cpu().numpy()
+        assert np.isfinite(got).all()
+        err = np.abs(got.astype(np.float64) - r.astype(np.float64))
+        assert (err <= _bound(n, absprod, r)).all(), float(err.max())
+        assert ((got == 0) == (r == 0)).all() if masked else True
+
+
+@pytest.fixture(scope="module")
+def ax():
+    from paper_2203_04071_b200 import _lib
+    _lib.load()
+    return _lib
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 1024, 1024), (37, 50, 70), (1, 1, 1), (300, 129, 257),
+                                   (130, 1000, 2048)])
+@pytest.mark.parametrize("masked", [False, True])
+@pytest.mark.parametrize("split", [False, True], ids=["one-pass", "split-k"])
+def test_ste_backward(ax, M, N, K, masked, split):
+    _check(ax, M, N, K, M + N, masked, split)
+
+
+def test_ste_backward_empty(ax):
+    """M = 0: gw and gb are empty sums (zero)."""
+    gy = torch.zeros(0, 8, device=DEV)
+    qa = torch.zeros(0, 5, dtype=torch.int8, device=DEV)
+    qw = torch.ones(8, 5, dtype=torch.int8, device=DEV)
+    s = torch.ones(1, device=DEV)
+    gw = torch.full((8, 5), 7.0, device=DEV)
+    gb = torch.full((8,), 7.0, device=DEV)
+    ax.axq_ste_linear_backward(gy, qa, s, qw, s, gw=gw, gb=gb)
+    torch.cuda.synchronize()
+    assert (gw == 0).all() and (gb == 0).all()
+
+
+def test_ste_backward_invalid(ax):
+    gy = torch.zeros(4, 8, device=DEV)
+    qw = torch.ones(8, 5, dtype=torch.int8, device=DEV)
+    gx = torch.empty(4, 5, device=DEV)
+    with pytest.raises(ax.AxqError):   # gx requested without the weight scale
+        ax.axq_ste_linear_backward(gy, torch.zeros(4, 5, dtype=torch.int8, device=DEV), None, qw,
+                                   None, gx=gx)
