@@ -419,7 +419,10 @@ axq_status axq_quantize_nchw_to_nhwc(const float* x, int64_t N, int64_t C, int64
     if (N == 0 || Cq == 0 || H == 0 || W == 0) return AXQ_OK;
     if (!x || !q || N > 65535) return AXQ_ERR_INVALID;
     const int64_t HW = H * W;
-    if (Cq <= 16) {  // few channels (network input): one pixel per thread
+    if (Cq == 4 && C <= 4 && N * HW < ((int64_t)1 << 30) && (reinterpret_cast<uintptr_t>(q) & 3) == 0) {
+        axq::quantize_nchw_to_nhwc_c4_kernel<<<stream_grid(N * HW, 256), 256, 0, S(stream)>>>(
+            x, (int)C, (int)HW, (int)(N * HW), d_scale, bits, q);
+    } else if (Cq <= 16) {  // few channels (network input): one pixel per thread
         axq::quantize_nchw_to_nhwc_small_kernel<<<stream_grid(N * HW, 256), 256, 0, S(stream)>>>(
             x, N, C, HW, Cq, d_scale, bits, q);
     } else {
@@ -1017,7 +1020,11 @@ axq_status axq_maxpool2d_nhwc_i8(const int8_t* x, int64_t N, int64_t H, int64_t 
     if (Ho <= 0 || Wo <= 0) return AXQ_ERR_INVALID;
     if (N == 0) return AXQ_OK;
     if (!x || !y) return AXQ_ERR_INVALID;
-    if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 3) == 0) {
+    if ((C & 15) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+        N * Ho * Wo * (C / 16) < ((int64_t)1 << 31) && N * H * W * C < ((int64_t)1 << 40)) {
+        axq::maxpool_nhwc_i8x16_kernel<<<stream_grid(N * Ho * Wo * (C / 16), 256), 256, 0, S(stream)>>>(
+            x, (int)N, (int)H, (int)W, (int)C, (int)R, (int)Sz, (int)stride, (int)pad, (int)Ho, (int)Wo, y);
+    } else if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 3) == 0) {
         axq::maxpool_nhwc_i8_kernel<<<stream_grid(N * Ho * Wo * (C / 4), 256), 256, 0, S(stream)>>>(
             x, N, (int)H, (int)W, (int)C, (int)R, (int)Sz, (int)stride, (int)pad, (int)Ho, (int)Wo, y);
     } else {

@@ -41,6 +41,36 @@ __global__ void maxpool_nhwc_i8_kernel(const int8_t* __restrict__ x, int64_t N, 
     }
 }
 
+// 16 channels per thread (C % 16 == 0, 16-byte aligned), 32-bit indices (the caller checks the
+// item count): the ResNet maxpool after the stem is HBM/L2 bound, not index-math bound
+__global__ void maxpool_nhwc_i8x16_kernel(const int8_t* __restrict__ x, int N, int H, int W, int C, int R,
+                                          int S, int stride, int pad, int Ho, int Wo,
+                                          int8_t* __restrict__ y) {
+    const int C16 = C >> 4;
+    const int total = N * Ho * Wo * C16;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int c16 = i % C16;
+        int t = i / C16;
+        const int wo = t % Wo;
+        t /= Wo;
+        const int ho = t % Ho;
+        const int n = t / Ho;
+        uint4 m = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);   // -128
+        for (int r = 0; r < R; ++r) {
+            const int hi = ho * stride - pad + r;
+            if (hi < 0 || hi >= H) continue;
+            for (int s_ = 0; s_ < S; ++s_) {
+                const int wi = wo * stride - pad + s_;
+                if (wi < 0 || wi >= W) continue;
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((int64_t)(n * H + hi) * W + wi) * C) + c16);
+                m.x = __vmaxs4(m.x, v.x); m.y = __vmaxs4(m.y, v.y);
+                m.z = __vmaxs4(m.z, v.z); m.w = __vmaxs4(m.w, v.w);
+            }
+        }
+        reinterpret_cast<uint4*>(y + ((int64_t)(n * Ho + ho) * Wo + wo) * C)[c16] = m;
+    }
+}
+
 // fp32 NHWC max pooling (out-of-image taps ignored, A17): the calibration pass of the paper
 // quantizer needs the pooled real values (a percentile does not commute with pooling as the
 // max does)
@@ -185,39 +215,49 @@ __global__ void im2col_nhwc_i8_kernel(const int8_t* __restrict__ X, int64_t M, i
 // one whole row in registers -- one 4-byte load per tap (its 3 channels), bytes placed at
 // compile-time positions -- then writes it with 16-byte stores.
 template <int R, int S, int CV, int LDA>
-__global__ void im2col_c4_kernel(const int8_t* __restrict__ X, int64_t M, int H, int W, int Ho, int Wo,
-                                 int sh, int sw, int ph, int pw, int8_t* __restrict__ A) {
-    constexpr int K = R * S * CV, NW = LDA / 4;
+__global__ void __launch_bounds__(256) im2col_c4_kernel(const int8_t* __restrict__ X, int64_t M, int H, int W,
+                                                        int Ho, int Wo, int sh, int sw, int ph, int pw,
+                                                        int8_t* __restrict__ A) {
+    // a block builds 256 consecutive rows in shared memory, then writes the contiguous
+    // 256 x LDA-byte block with coalesced 16-byte stores (per-thread row stores at a 160-byte
+    // stride left most of each store's sectors partial)
+    constexpr int NW = LDA / 4, NV = LDA / 16;
+    __shared__ uint4 tile[256 * NV];
     const int64_t hw = (int64_t)Ho * Wo;
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t img = m / hw, rem = m - img * hw;
-        const int ho = (int)(rem / Wo), wo = (int)(rem - (int64_t)ho * Wo);
-        const int hb = ho * sh - ph, wb = wo * sw - pw;
-        const uint32_t* xb = reinterpret_cast<const uint32_t*>(X) + img * (int64_t)H * W;
-        uint32_t out[NW];
+    for (int64_t mb = (int64_t)blockIdx.x * 256; mb < M; mb += (int64_t)gridDim.x * 256) {
+        const int64_t m = mb + threadIdx.x;
+        if (m < M) {
+            const int64_t img = m / hw, rem = m - img * hw;
+            const int ho = (int)(rem / Wo), wo = (int)(rem - (int64_t)ho * Wo);
+            const int hb = ho * sh - ph, wb = wo * sw - pw;
+            const uint32_t* xb = reinterpret_cast<const uint32_t*>(X) + img * (int64_t)H * W;
+            uint32_t out[NW];
 #pragma unroll
-        for (int i = 0; i < NW; ++i) out[i] = 0u;
+            for (int i = 0; i < NW; ++i) out[i] = 0u;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int hi = hb + r;
+            for (int r = 0; r < R; ++r) {
+                const int hi = hb + r;
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int wi = wb + s;
-                const uint32_t v = ((unsigned)hi < (unsigned)H && (unsigned)wi < (unsigned)W)
-                                       ? __ldg(xb + (int64_t)hi * W + wi) : 0u;
+                for (int s = 0; s < S; ++s) {
+                    const int wi = wb + s;
+                    const uint32_t v = ((unsigned)hi < (unsigned)H && (unsigned)wi < (unsigned)W)
+                                           ? __ldg(xb + (int64_t)hi * W + wi) : 0u;
 #pragma unroll
-                for (int c = 0; c < CV; ++c) {
-                    constexpr int dummy = 0;
-                    (void)dummy;
-                    const int k = (r * S + s) * CV + c;
-                    out[k >> 2] |= ((v >> (8 * c)) & 0xffu) << (8 * (k & 3));
+                    for (int c = 0; c < CV; ++c) {
+                        const int k = (r * S + s) * CV + c;
+                        out[k >> 2] |= ((v >> (8 * c)) & 0xffu) << (8 * (k & 3));
+                    }
                 }
             }
-        }
-        (void)K;
-        uint4* dst = reinterpret_cast<uint4*>(A + m * LDA);
 #pragma unroll
-        for (int i = 0; i < NW / 4; ++i) dst[i] = make_uint4(out[4 * i], out[4 * i + 1], out[4 * i + 2], out[4 * i + 3]);
+            for (int i = 0; i < NV; ++i)
+                tile[threadIdx.x * NV + i] = make_uint4(out[4 * i], out[4 * i + 1], out[4 * i + 2], out[4 * i + 3]);
+        }
+        __syncthreads();
+        const int rows = (int)min((int64_t)256, M - mb);
+        uint4* dst = reinterpret_cast<uint4*>(A + mb * LDA);
+        for (int j = threadIdx.x; j < rows * NV; j += 256) dst[j] = tile[j];
+        __syncthreads();
     }
 }
 

@@ -134,6 +134,39 @@ quantize_nchw_to_nhwc_kernel(const float* __restrict__ x, int64_t C, int64_t HW,
     }
 }
 
+// C <= 4 into Cq = 4 (the network input, C = 3 padded), N * HW < 2^31: one pixel per thread,
+// 32-bit indices, requantize through the reciprocal with the exact fallback (epi_quant_r, the
+// same integer as the IEEE division of A3)
+__global__ void quantize_nchw_to_nhwc_c4_kernel(const float* __restrict__ x, int C, int HW, int total,
+                                                const float* __restrict__ d_scale, int bits,
+                                                int8_t* __restrict__ q) {
+    const float s = *d_scale, qm = qmax_of(bits), r = __frcp_rn(s);
+    const int gs = gridDim.x * blockDim.x;
+    // 4 pixels per thread per iteration, all loads issued before any is used (memory-level
+    // parallelism: one pixel at a time left the kernel latency-bound)
+    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += 4 * gs) {
+        float v[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * gs;
+            const int img = i / HW, hw = i - img * HW;
+            const float* xp = x + (int64_t)img * C * HW + hw;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[u][c] = (i < total && c < C) ? __ldcs(xp + c * HW) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * gs;
+            if (i >= total) break;
+            uint32_t w = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c < C) w |= (uint32_t)(uint8_t)epi_quant_r(v[u][c], s, r, qm) << (8 * c);
+            reinterpret_cast<uint32_t*>(q)[i] = w;
+        }
+    }
+}
+
 // Few channels (the network input, C = 3 padded to Cq = 4): one pixel per thread.
 __global__ void quantize_nchw_to_nhwc_small_kernel(const float* __restrict__ x, int64_t N,
                                                    int64_t C, int64_t HW, int64_t Cq,

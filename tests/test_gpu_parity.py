@@ -201,6 +201,20 @@ def test_quantize_nchw_to_nhwc(ax):
     np.testing.assert_array_equal(q.cpu().numpy(), oracle.quantize(x, s, 8).transpose(0, 2, 3, 1))
 
 
+@pytest.mark.parametrize("C,Cq", [(3, 4), (4, 4), (1, 4), (3, 8)])
+def test_quantize_nchw_to_nhwc_few_channels(ax, C, Cq):
+    """The network-input path (C <= 4 into 4-byte pixels: reciprocal requantize with the exact
+    fallback) and the generic few-channel path give the oracle's codes; padded channels are 0."""
+    x = datagen.normal(143, C, (5, C, 19, 23), 2.0)
+    x[0, 0, 0, :8] = np.float32([0.5, 1.5, -2.5, 2.5, 126.5, -126.5, 0.0, -0.0]) * np.float32(0.04)
+    s = np.float32(0.04)
+    ref = np.zeros((5, 19, 23, Cq), np.int8)
+    ref[..., :C] = oracle.quantize(x, s, 8).transpose(0, 2, 3, 1)
+    q = torch.full((5, 19, 23, Cq), 99, dtype=torch.int8, device=DEV)
+    ax.axq_quantize_nchw_to_nhwc(_t(x), torch.tensor([s], device=DEV), 8, q)
+    np.testing.assert_array_equal(q.cpu().numpy(), ref)
+
+
 def test_dequantize(ax):
     rng = np.random.default_rng(3)
     acc = rng.integers(-2**31, 2**31, size=(37, 19), dtype=np.int64).astype(np.int32)
@@ -373,6 +387,11 @@ def test_maxpool_int8(ax):
     ax.axq_maxpool2d_nhwc_i8(_t(x), 3, 3, 2, 1, y)
     ref = _maxpool(x.transpose(0, 3, 1, 2).astype(np.float32)).transpose(0, 2, 3, 1)
     np.testing.assert_array_equal(y.cpu().numpy(), ref.astype(np.int8))
+    x16 = datagen.random_int8(142, (3, 15, 12, 48))        # C % 16 == 0: 16-channel kernel
+    y16 = torch.empty(3, 8, 6, 48, dtype=torch.int8, device=DEV)
+    ax.axq_maxpool2d_nhwc_i8(_t(x16), 3, 3, 2, 1, y16)
+    ref16 = _maxpool(x16.transpose(0, 3, 1, 2).astype(np.float32)).transpose(0, 2, 3, 1)
+    np.testing.assert_array_equal(y16.cpu().numpy(), ref16.astype(np.int8))
     x3 = datagen.random_int8(141, (1, 9, 9, 6))            # C % 4 != 0: byte kernel
     y3 = torch.empty(1, 5, 5, 6, dtype=torch.int8, device=DEV)
     ax.axq_maxpool2d_nhwc_i8(_t(x3), 3, 3, 2, 1, y3)
