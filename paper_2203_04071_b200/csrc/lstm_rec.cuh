@@ -31,6 +31,10 @@ namespace axq {
 namespace lstmr {
 constexpr int NT = 1024;                   // 32 warps: units x row groups x K splits
 constexpr int TABLE = 65536;
+// h_{t-1} rows in shared memory are H + 16 bytes apart: the lanes of a warp (consecutive batch
+// rows) read 16 bytes of their own rows at the same k; at a multiple-of-128-byte stride all of
+// them hit the same 4 banks (8-way replays per quarter warp), at H + 16 they spread over all 32
+constexpr int H_PAD = 16;
 }
 
 __global__ void __launch_bounds__(lstmr::NT, 1) lstm_rec_kernel(const __grid_constant__ LstmRecArgs a) {
@@ -42,8 +46,9 @@ __global__ void __launch_bounds__(lstmr::NT, 1) lstm_rec_kernel(const __grid_con
     const int rg = (B + 31) / 32;
     int8_t* tab_s = lr_smem;                           // 64 KiB
     int8_t* w_s = tab_s + TABLE;                       // [nu][4][H]
-    int8_t* h_s = w_s + (size_t)nu * 4 * H;            // [B][H]
-    int* red_s = reinterpret_cast<int*>(h_s + (size_t)B * H);   // [32 warps][4][32 lanes]
+    int8_t* h_s = w_s + (size_t)nu * 4 * H;            // [B][H + H_PAD]
+    const int HS = H + H_PAD;                          // h_s row stride (bytes)
+    int* red_s = reinterpret_cast<int*>(h_s + (size_t)B * HS);  // [32 warps][4][32 lanes]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // warp -> (unit u, row group r, K part ks): the K loop of a (unit, row group) is split
     // over KSP warps (more warps in flight per SM), partial sums reduced through shared memory
@@ -78,19 +83,26 @@ __global__ void __launch_bounds__(lstmr::NT, 1) lstm_rec_kernel(const __grid_con
     for (int t = 0; t < a.T; ++t) {
         // h_{t-1} codes -> shared (h_{-1} = 0); L2 reads: other CTAs wrote them this launch
         {
-            uint4* dst = reinterpret_cast<uint4*>(h_s);
             const int n16 = B * hv;
+            const int hsv = HS / 16;
+            uint4* dst = reinterpret_cast<uint4*>(h_s);
             if (t == 0) {
-                for (int i = tid; i < n16; i += NT) dst[i] = make_uint4(0, 0, 0, 0);
+                for (int i = tid; i < n16; i += NT) {
+                    const int bb = i / hv, kc = i - bb * hv;
+                    dst[bb * hsv + kc] = make_uint4(0, 0, 0, 0);
+                }
             } else {
                 const uint4* src = reinterpret_cast<const uint4*>(a.hq + (size_t)((t - 1) & 1) * B * H);
-                for (int i = tid; i < n16; i += NT) dst[i] = __ldcg(src + i);
+                for (int i = tid; i < n16; i += NT) {
+                    const int bb = i / hv, kc = i - bb * hv;
+                    dst[bb * hsv + kc] = __ldcg(src + i);
+                }
             }
         }
         __syncthreads();
         int acc[4] = {0, 0, 0, 0};
         if (live) {
-            const uint4* hrow = reinterpret_cast<const uint4*>(h_s + (size_t)b * H);
+            const uint4* hrow = reinterpret_cast<const uint4*>(h_s + (size_t)b * HS);
             const uint4* wrow = reinterpret_cast<const uint4*>(w_s + (size_t)u * 4 * H);
             const int kc0 = (ks * hv) / KSP, kc1 = ((ks + 1) * hv) / KSP;
 #pragma unroll 2

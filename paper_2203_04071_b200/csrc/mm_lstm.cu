@@ -9,7 +9,8 @@ int launch_lstm_rec(const LstmRecArgs& a, int sms, cudaStream_t st) {
     int G = sms < a.H ? sms : a.H;
     const int nu = (a.H + G - 1) / G;
     if (nu * rg > lstmr::NT / 32 || (a.H % 16) != 0) return -1;
-    const size_t smem = lstmr::TABLE + (size_t)nu * 4 * a.H + (size_t)a.B * a.H + (lstmr::NT / 32) * 4 * 32 * 4;
+    const size_t smem = lstmr::TABLE + (size_t)nu * 4 * a.H + (size_t)a.B * (a.H + lstmr::H_PAD) +
+                        (lstmr::NT / 32) * 4 * 32 * 4;
     if (smem > 227 * 1024) return -1;
     static size_t configured[32] = {0};
     int dev = 0;
