@@ -129,6 +129,17 @@ axq_status launch_mm(int epi, int loader, int repr, const axq::MMArgs& p, const 
 Cfg pick_cfg(int64_t M, int loader, int repr) {
     const bool big_ok = repr != AXQ_LUT_I32 &&
                         (loader == axq::LOAD_GEMM || loader == axq::LOAD_CONV || loader == axq::LOAD_CONV_C4);
+    static int forced = -1;   // AXQ_V1_CFG (measurement switch): 1 SMALL, 2 BIG, 3 TINY, 4 MID
+    if (forced < 0) {
+        const char* v = std::getenv("AXQ_V1_CFG");
+        forced = v ? std::atoi(v) : 0;
+    }
+    if (forced && big_ok && loader == axq::LOAD_GEMM) {
+        if (forced == 2) return CFG_BIG;
+        if (forced == 3) return axq::CFG_TINY;
+        if (forced == 4) return axq::CFG_MID;
+        return CFG_SMALL;
+    }
     if (big_ok && loader == axq::LOAD_GEMM && M <= 64) return axq::CFG_TINY;
     return (M > 2048 && big_ok) ? CFG_BIG : CFG_SMALL;
 }
@@ -790,7 +801,9 @@ static int g_p4w_main_cw = 28;         // AXQ_P4W_MAIN_CW: consumer warps of the
 static int64_t g_p4w_main_cw_max_k = 1 << 30;   // ... for layers with K up to this
 static int g_p4w_res_cw = 16;          // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape
 static int g_p4w_cw = 0;                // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
-static int64_t g_sk_min_stages = 1;    // AXQ_SK_MIN_STAGES: measured best at 1 (every SM takes a piece)
+static int64_t g_sk_min_stages = 4;    // AXQ_SK_MIN_STAGES: stream-K pieces of >= 4 stages (measured
+                                       // with the 512-row residual shape: 1 -> 4 saves 0.3-0.7 ms per
+                                       // forward at 256-32 images; 6 is worse again)
 static int64_t g_p4w_ks16_max_k = 0;   // AXQ_P4W_KS16_MAX_K: measured slower, off
 static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 2 P4T, 3 P4W
 
