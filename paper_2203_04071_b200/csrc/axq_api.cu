@@ -801,6 +801,9 @@ static int g_p4w_main_cw = 28;         // AXQ_P4W_MAIN_CW: consumer warps of the
 static int64_t g_p4w_main_cw_max_k = 1 << 30;   // ... for layers with K up to this
 static int g_p4w_res_cw = 16;          // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape
 static int g_p4w_cw = 0;                // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
+static int64_t g_sk_full_waves = 8;    // AXQ_SK_FULL_WAVES: P4W layers of fewer than this many waves of
+                                       // tiles cut every iteration (no whole-wave phase): measured
+                                       // 73.5 -> 73.2 ms at 256 images, 10.79 -> 10.60 at 32 (4, 16 close)
 static int64_t g_sk_min_stages = 4;    // AXQ_SK_MIN_STAGES: stream-K pieces of >= 4 stages (measured
                                        // with the 512-row residual shape: 1 -> 4 saves 0.3-0.7 ms per
                                        // forward at 256-32 images; 6 is worse again)
@@ -816,6 +819,7 @@ static void p4w_read_env() {
     if (const char* v = std::getenv("AXQ_P4W_CW")) g_p4w_cw = std::atoi(v);
     if (const char* v = std::getenv("AXQ_P4W_RES_CW")) g_p4w_res_cw = std::atoi(v);
     if (const char* v = std::getenv("AXQ_P4W_MAIN_CW")) g_p4w_main_cw = std::atoi(v);
+    if (const char* v = std::getenv("AXQ_SK_FULL_WAVES")) g_sk_full_waves = std::atoll(v);
     if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
     env_read = true;
 }
@@ -900,11 +904,12 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         const int64_t tiles = ((a.mm.M + bm - 1) / bm) * ((a.mm.N + axq::p4::TN - 1) / axq::p4::TN);
         int32_t* cnt = streamk_counters(dev);
         if (cnt && tiles % sm_count() != 0) {
-            a.streamk = 1;
+            const bool full = variant == 3 && tiles < g_sk_full_waves * sm_count();
+            a.streamk = full ? 2 : 1;
             a.splits = 1;
             a.stages_per_split = 0;
             // pieces of at least ~4 stages: a small tail is shared by fewer CTAs
-            const int64_t tail_it = (tiles % sm_count()) * (wp->Kp / a.ks);
+            const int64_t tail_it = (full ? tiles : tiles % sm_count()) * (wp->Kp / a.ks);
             a.sk_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), tail_it / g_sk_min_stages));
             a.ws = variant == 3 ? streamk_parts(dev) : ep->workspace;
             a.cnt = cnt;

@@ -48,7 +48,8 @@ struct P4Args {
     int rpl;                    // rows per lane: 2 (1024-row tiles) or 1 (512-row tiles)
     int half;                   // tables cover ua = 0..127 only (non-negative activations)
     int c4;                     // conv with C % 16 != 0 (C % 4 == 0): 4-byte tap copies
-    int streamk;                // P4T: stream-K decomposition (needs ws and cnt)
+    int streamk;                // stream-K decomposition (needs ws and cnt): 1 whole waves + cut
+                                // tail; 2 (P4W) every iteration cut, one slice per CTA
     int32_t* ws;                // stream-K pieces: P4T int32 [M][N] (zero on entry, left zero);
                                 // P4W per-CTA partial slots [grid][2][896][16]
     int32_t* cnt;               // stream-K tile counters (>= gridDim.x), zero on entry, left zero

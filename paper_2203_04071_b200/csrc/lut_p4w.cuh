@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     const bool sk = P.streamk != 0;
     const int64_t G_ = gridDim.x;
     const int64_t t_all = m_tiles * n_blocks;
-    const int64_t t_dp = sk ? (t_all / G_) * G_ : 0;
+    // streamk 1: whole waves round-robin, then the tail cut; 2: every (tile, stage) iteration cut
+    // into one contiguous slice per CTA (no wave quantisation at a few waves)
+    const int64_t t_dp = sk ? (P.streamk == 2 ? 0 : (t_all / G_) * G_) : 0;
     const int64_t it_sk = (t_all - t_dp) * (int64_t)nst_all;
     // the tail is cut among the first G_sk CTAs only (pieces of >= a few stages; the host
     // picks sk_ctas), the rest get empty ranges
