@@ -35,6 +35,8 @@ def _table(kind):
 
 # N, C, H, W, K, R, S, stride, pad, dil, groups
 CASES = [(2, 32, 10, 9, 32, 3, 3, 1, 1, 1, 32),     # depthwise 3x3
+         (2, 64, 11, 37, 64, 3, 3, 2, 1, 1, 64),    # depthwise 3x3 stride 2, 2 channel blocks, ragged tiles
+         (1, 96, 9, 70, 96, 3, 3, 1, 0, 1, 96),     # depthwise 3x3, no padding, 3 column tiles
          (1, 16, 12, 12, 32, 3, 3, 2, 1, 1, 16),    # depthwise, channel multiplier 2, stride 2
          (2, 24, 8, 11, 36, 1, 1, 1, 0, 1, 3),      # grouped 1x1 (ShuffleNet-like, G = 3)
          (1, 32, 9, 9, 64, 5, 5, 1, 2, 1, 4),       # grouped 5x5
