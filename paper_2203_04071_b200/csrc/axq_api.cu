@@ -826,7 +826,7 @@ static void p4w_read_env() {
 
 axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw) {
     p4w_read_env();
-    if ((main_cw && main_cw != 20 && main_cw != 24 && main_cw != 28) ||
+    if ((main_cw && main_cw != 16 && main_cw != 20 && main_cw != 24 && main_cw != 28) ||
         (res_cw && res_cw != 16 && res_cw != 20 && res_cw != 24 && res_cw != 28) ||
         (small_cw && small_cw != 16 && small_cw != 28))
         return AXQ_ERR_INVALID;
@@ -887,7 +887,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         (g_p4w_res_cw == 16 || g_p4w_res_cw == 20 || g_p4w_res_cw == 24))
         a.cw = g_p4w_res_cw;
     if (variant == 3 && !res_ep && wp->half && a.ks == 32 && !a.c4 && a.cw == 28 &&
-        (g_p4w_main_cw == 20 || g_p4w_main_cw == 24) && wp->Kp <= g_p4w_main_cw_max_k)
+        (g_p4w_main_cw == 16 || g_p4w_main_cw == 20 || g_p4w_main_cw == 24) && wp->Kp <= g_p4w_main_cw_max_k)
         a.cw = g_p4w_main_cw;
     const int bm = variant == 3 ? axq::p4w_bm(a.cw) : 1024;
     if (use_tc)
