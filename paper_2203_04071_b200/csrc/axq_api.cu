@@ -880,8 +880,11 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
     const bool res_ep = ep && ep->residual;
     a.cw = 28;
+    // 512-row tiles when they pad fewer rows than 896-row ones (M <= 1024 always: one or two
+    // nearly empty 896-row tiles), e.g. the LSTM input projection (M = 8192 = 16 x 512, 9.1 x 896)
+    const int64_t pad512 = (a.mm.M + 511) / 512 * 512 - a.mm.M, pad896 = (a.mm.M + 895) / 896 * 896 - a.mm.M;
     if (variant == 3 && !res_ep && !a.c4 && (!wp->half || a.ks == 32) && g_p4w_cw != 28 &&
-        (g_p4w_cw == 16 || a.mm.M <= 1024))
+        (g_p4w_cw == 16 || a.mm.M <= 1024 || pad512 < pad896))
         a.cw = 16;
     if (variant == 3 && res_ep && wp->half && a.ks == 32 && !a.c4 &&
         (g_p4w_res_cw == 16 || g_p4w_res_cw == 20 || g_p4w_res_cw == 24))
