@@ -8,7 +8,7 @@
 //   gx[m][k] = [|x[m][k]| <= clip_a] * sum_n gy[m][n] * fl(s_w * qw[n][k])
 //   gw[n][k] = [|w[n][k]| <= clip_w] * sum_m gy[m][n] * fl(s_a * qa[m][k])
 //   gb[n]    = sum_m gy[m][n]
-// Both products are one fp32 SIMT GEMM kernel (128 x 128 x 8 tiles, 8 x 8 outputs per thread,
+// Both products are one fp32 SIMT GEMM kernel (128 x 128 x 16 tiles, 8 x 8 outputs per thread,
 // fp32 FMA accumulation): the int8 operand is dequantized while it is staged into shared memory
 // and the STE mask is applied in the epilogue.  fp32 FMA, not tensor cores: the result is
 // compared with the fp64 oracle under the fp32 dot-product error bound (tests/test_gpu_ste.py).
@@ -21,7 +21,7 @@
 namespace axq {
 axq_status cuda_fail_ext(int e);   // axq_api.cu: records the code for axq_last_cuda_error()
 namespace ste {
-constexpr int BM = 128, BN = 128, BK = 8, NT = 256;
+constexpr int BM = 128, BN = 128, BK = 16, NT = 256;
 }
 
 // C[i][j] = mask(i, j) * sum_p A(i, p) * fl(s_b * B[p][j]),  A(i, p) = TA ? A[p*lda + i] : A[i*lda + p]
