@@ -289,9 +289,9 @@ axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw);
  * calibrated clip ranges (device scalars, e.g. amax; a value with |v| > clip gets no gradient);
  * x / w null: no mask.  All buffers contiguous, on the current device; gx / gw / gb nullable
  * (not computed).  workspace (nullable, workspace_elems floats, caller-owned, no contents
- * required): room for up to 16 K-split partial products of the larger gradient (16 * max(M, N)
- * * K floats covers every case); used to split the summed dimension when the output alone cannot
- * fill the SMs (the splits are added in a fixed order, so results are deterministic).  fp32 FMA
+ * required): room for K-split partial products (up to 128 slices of one gradient; fewer when
+ * the room is smaller, none without it); used to split the summed dimension when the output
+ * alone cannot fill the SMs (the splits are added in a fixed order: deterministic).  fp32 FMA
  * accumulation (not bit-exact against a different summation order: within the fp32
  * dot-product bound).  Asynchronous on stream.  AXQ_ERR_INVALID for negative extents or a
  * missing operand of a requested gradient.
@@ -302,6 +302,25 @@ axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float*
                                    const float* w, const float* d_clip_w, float* gx, float* gw,
                                    float* gb, float* workspace, int64_t workspace_elems,
                                    void* stream);
+
+/* axq_ste_conv2d_backward: the same STE backward for a convolution (groups = 1, dilation 1,
+ *   c_valid 0; the conv is the GEMM of its im2col matrix).  gy fp32 NHWC [N][Ho][Wo][K]
+ *   (dL/dy), qx int8 NHWC [N][H][W][C] / qw int8 [K][R][S][C]: the forward's codes with their
+ *   device scales; x fp32 NHWC / w fp32 [K][R][S][C] + clips: the STE masks (nullable).
+ *     gw[k][(r,s,c)] = [|w| <= clip_w] * sum_m gy[m][k] * fq(im2col(qx)[m][(r,s,c)])
+ *     gx[n][h][w][c] = [|x| <= clip_a] * sum over the (m, r, s) whose window places tap (r, s)
+ *                      on (h, w) of sum_k gy[m][k] * fq(qw[k][(r,s,c)])   (the adjoint of im2col)
+ *     gb[k] = sum_m gy[m][k]
+ *   Workspaces (caller-owned): cols int8 [M][ldcols] (ldcols >= R*S*C, multiple of 16; needed
+ *   for gw), gcols fp32 [M][R*S*C] (needed for gx), workspace / workspace_elems as
+ *   axq_ste_linear_backward (optional).  fp32 accumulation, deterministic.  AXQ_ERR_INVALID for
+ *   other conv shapes or a missing operand of a requested gradient. */
+axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const float* gy, const int8_t* qx,
+                                   const float* d_scale_a, const float* x, const float* d_clip_a,
+                                   const int8_t* qw, const float* d_scale_w, const float* w,
+                                   const float* d_clip_w, float* gx, float* gw, float* gb,
+                                   int8_t* cols, int64_t ldcols, float* gcols, float* workspace,
+                                   int64_t workspace_elems, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * Dequantize (unfused), same pinned formula as the epilogue.

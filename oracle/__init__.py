@@ -303,3 +303,36 @@ def ste_linear_backward(gy, qa, s_a, qw, s_w, x=None, clip_a=None, w=None, clip_
     if w is not None:
         gw = np.where(np.abs(np.asarray(w, dtype=np.float32)) <= np.float32(clip_w), gw, 0.0)
     return gx.astype(np.float32), gw.astype(np.float32), gb.astype(np.float32)
+
+
+def ste_conv2d_backward(gy, qx, s_a, qw, s_w, stride=(1, 1), pad=(0, 0), x=None, clip_a=None,
+                        w=None, clip_w=None):
+    """STE backward of an approximate conv (P:107-109 over the conv of P:119; reading A36), NHWC:
+    gy [N][Ho][Wo][K], qx [N][H][W][C], qw [K][R][S][C] -> (gx [N][H][W][C], gw [K][R][S][C],
+    gb [K]) fp32.  The layer differentiates as the conv of the fake-quantized operands: gw is the
+    correlation of the zero-padded fq(x) with gy, gx the transposed conv of gy with fq(w); fp64
+    sums, one rounding to fp32; inputs outside their clip get no gradient."""
+    gy64 = np.asarray(gy, dtype=np.float32).astype(np.float64)
+    xf = fake_quant(qx, s_a).astype(np.float64)
+    wf = fake_quant(qw, s_w).astype(np.float64)
+    N, H, W, C = xf.shape
+    K, R, S, _ = wf.shape
+    _, Ho, Wo, _ = gy64.shape
+    sh, sw = stride
+    ph, pw = pad
+    xp = np.zeros((N, H + 2 * ph + sh * R, W + 2 * pw + sw * S, C))
+    xp[:, ph:ph + H, pw:pw + W, :] = xf
+    gxp = np.zeros_like(xp)
+    gw = np.zeros((K, R, S, C))
+    for r in range(R):
+        for s_ in range(S):
+            win = xp[:, r:r + sh * Ho:sh, s_:s_ + sw * Wo:sw, :]          # [N][Ho][Wo][C]
+            gw[:, r, s_, :] = np.einsum("nhwk,nhwc->kc", gy64, win)
+            gxp[:, r:r + sh * Ho:sh, s_:s_ + sw * Wo:sw, :] += np.einsum("nhwk,kc->nhwc", gy64, wf[:, r, s_, :])
+    gx = gxp[:, ph:ph + H, pw:pw + W, :]
+    gb = gy64.sum(axis=(0, 1, 2))
+    if x is not None:
+        gx = np.where(np.abs(np.asarray(x, dtype=np.float32)) <= np.float32(clip_a), gx, 0.0)
+    if w is not None:
+        gw = np.where(np.abs(np.asarray(w, dtype=np.float32)) <= np.float32(clip_w), gw, 0.0)
+    return gx.astype(np.float32), gw.astype(np.float32), gb.astype(np.float32)

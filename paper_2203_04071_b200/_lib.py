@@ -28,7 +28,7 @@ EXPORTED = [
     "axq_maxpool2d_nhwc_i8", "axq_avgpool_nhwc", "axq_lstm_cell",
     "axq_wpack_create", "axq_wpack_destroy", "axq_wpack_info", "axq_lut_gemm_wp",
     "axq_lut_conv2d_wp", "axq_wpack_kernel", "axq_wpack_shapes", "axq_lstm_recurrent",
-    "axq_ste_linear_backward",
+    "axq_ste_linear_backward", "axq_ste_conv2d_backward",
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
@@ -101,6 +101,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_kernel": ([i32], i32),
         "axq_wpack_shapes": ([i32, i32, i32], i32),
         "axq_ste_linear_backward": ([i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp], i32),
+        "axq_ste_conv2d_backward": ([ctypes.POINTER(axq_conv_desc)] + [vp] * 13 + [i64, vp, vp, i64, vp], i32),
         "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
         "axq_quantize16": ([vp, i64, vp, i32, vp, vp], i32),
         "axq_im2col_nhwc_i8": ([vp] + [i64] * 11 + [vp, i64, vp], i32),
@@ -204,6 +205,26 @@ def axq_ste_linear_backward(gy, qa, d_scale_a, qw, d_scale_w, x=None, d_clip_a=N
     _check("axq_ste_linear_backward", load().axq_ste_linear_backward(
         M, N, K, _ptr(gy), _ptr(qa), _ptr(d_scale_a), _ptr(x), _ptr(d_clip_a), _ptr(qw),
         _ptr(d_scale_w), _ptr(w), _ptr(d_clip_w), _ptr(gx), _ptr(gw), _ptr(gb), _ptr(workspace),
+        workspace.numel() if workspace is not None else 0, _stream(stream)))
+
+
+def axq_ste_conv2d_backward(d, gy, qx, d_scale_a, qw, d_scale_w, x=None, d_clip_a=None, w=None,
+                            d_clip_w=None, gx=None, gw=None, gb=None, cols=None, gcols=None,
+                            workspace=None, stream=None) -> None:
+    """NEXT-4 STE backward of an approximate conv (include/axq.h): gy NHWC [N][Ho][Wo][K], qx
+    NHWC int8, qw [K][R][S][C] int8 -> gx NHWC, gw [K][R][S][C], gb [K]; cols / gcols are the
+    im2col workspaces (allocated here when None)."""
+    import torch
+    Ho, Wo = gy.shape[1], gy.shape[2]
+    M, Kc = d.N * Ho * Wo, d.R * d.S * d.C
+    if gw is not None and cols is None:
+        cols = torch.empty(M, (Kc + 15) // 16 * 16, dtype=torch.int8, device=gy.device)
+    if gx is not None and gcols is None:
+        gcols = torch.empty(M, Kc, dtype=torch.float32, device=gy.device)
+    _check("axq_ste_conv2d_backward", load().axq_ste_conv2d_backward(
+        ctypes.byref(d), _ptr(gy), _ptr(qx), _ptr(d_scale_a), _ptr(x), _ptr(d_clip_a), _ptr(qw),
+        _ptr(d_scale_w), _ptr(w), _ptr(d_clip_w), _ptr(gx), _ptr(gw), _ptr(gb), _ptr(cols),
+        cols.stride(0) if cols is not None else 0, _ptr(gcols), _ptr(workspace),
         workspace.numel() if workspace is not None else 0, _stream(stream)))
 
 

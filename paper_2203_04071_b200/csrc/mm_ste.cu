@@ -141,6 +141,28 @@ __global__ void ste_reduce_kernel(int S, int64_t MN, int64_t N, const float* __r
     }
 }
 
+// Column sums over many rows, deterministic: block (column group of 32, row block rb) sums its
+// rows per warp (rows w, w + 8, ...), the 8 warps in order, into part[rb][n]; ste_colsum_kernel
+// then adds the row blocks in order.
+constexpr int COLSUM_RB = 128;
+__global__ void __launch_bounds__(256) ste_colsum_part_kernel(int64_t M, int64_t N, const float* __restrict__ gy,
+                                                              int64_t ldg, float* __restrict__ part) {
+    __shared__ float red[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = (int64_t)blockIdx.x * 32 + lane;
+    const int64_t rows = (M + gridDim.y - 1) / gridDim.y, r0 = (int64_t)blockIdx.y * rows, r1 = min(M, r0 + rows);
+    float s = 0.f;
+    if (n < N)
+        for (int64_t m = r0 + warp; m < r1; m += 8) s = __fadd_rn(s, gy[m * ldg + n]);
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && n < N) {
+        float t = red[0][lane];
+        for (int w = 1; w < 8; ++w) t = __fadd_rn(t, red[w][lane]);
+        part[(int64_t)blockIdx.y * N + n] = t;
+    }
+}
+
 // gb[n] = sum_m gy[m][n], sequential in m (one thread per column, coalesced rows)
 __global__ void ste_colsum_kernel(int64_t M, int64_t N, const float* __restrict__ gy, int64_t ldg,
                                   float* __restrict__ gb) {
@@ -151,6 +173,77 @@ __global__ void ste_colsum_kernel(int64_t M, int64_t N, const float* __restrict_
     gb[n] = s;
 }
 
+}  // namespace axq
+
+
+namespace axq {
+// One STE product C[Mg][Ng] = mask * A(Mg x Kg) . fq(B[Kg][ldb]) (R: mask operand [Mg][Ng] or null):
+// split K (deterministic, through the workspace) until ~2 CTAs per SM
+static void ste_product(bool ta, int64_t Mg, int64_t Ng, int64_t Kg, const float* A, int64_t lda,
+                        const int8_t* B, int64_t ldb, const float* sB, float* C, int64_t ldc, const float* R,
+                        const float* clip, float* workspace, int64_t workspace_elems, cudaStream_t st) {
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = ((Ng + ste::BN - 1) / ste::BN) * ((Mg + ste::BM - 1) / ste::BM);
+    // (a conv's weight gradient sums over all N*Ho*Wo positions into a few tiles: up to 128 slices)
+    int64_t S = std::min<int64_t>({(2 * (int64_t)sms + tiles - 1) / tiles, 128, std::max<int64_t>(1, Kg / 64)});
+    S = workspace ? std::min<int64_t>(S, workspace_elems / std::max<int64_t>(1, Mg * ldc)) : 1;
+    if (S < 2) S = 1;
+    const int64_t kc = ((Kg + S - 1) / S + ste::BK - 1) / ste::BK * ste::BK;
+    S = (Kg + kc - 1) / kc;
+    dim3 grid((unsigned)((Ng + ste::BN - 1) / ste::BN), (unsigned)((Mg + ste::BM - 1) / ste::BM), (unsigned)S);
+    float* out = S > 1 ? workspace : C;
+    if (ta) ste_gemm_kernel<true><<<grid, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, kc);
+    else ste_gemm_kernel<false><<<grid, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, kc);
+    if (S > 1)
+        ste_reduce_kernel<<<(unsigned)std::min<int64_t>((Mg * ldc + 255) / 256, 8 * sms), 256, 0, st>>>(
+            (int)S, Mg * ldc, Ng, workspace, C, R, clip);
+}
+
+// gb = column sums of gy [M][N]: two deterministic passes through the workspace when M is large
+static void ste_colsum(int64_t M, int64_t N, const float* gy, float* gb, float* workspace, int64_t workspace_elems,
+                       cudaStream_t st) {
+    if (M >= 4096 && workspace && workspace_elems >= COLSUM_RB * N) {
+        ste_colsum_part_kernel<<<dim3((unsigned)((N + 31) / 32), COLSUM_RB), 256, 0, st>>>(M, N, gy, N, workspace);
+        ste_colsum_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(COLSUM_RB, N, workspace, N, gb);
+    } else {
+        ste_colsum_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(M, N, gy, N, gb);
+    }
+}
+
+// gx[n][h][w][c] = mask * sum_{r, s} gcols[(n, ho, wo)][(r, s, c)] over the output positions whose
+// window covers (h, w) (the adjoint of im2col; r, s in ascending order: deterministic)
+__global__ void ste_col2im_kernel(int64_t total, int H, int W, int C, int R, int S, int sh, int sw, int ph,
+                                  int pw, int Ho, int Wo, const float* __restrict__ gcols, int64_t ldg,
+                                  const float* __restrict__ x, const float* __restrict__ clip,
+                                  float* __restrict__ gx) {
+    const float cl = x ? *clip : 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % C);
+        int64_t t = i / C;
+        const int w_ = (int)(t % W);
+        t /= W;
+        const int h = (int)(t % H);
+        const int64_t n = t / H;
+        float acc = 0.f;
+        for (int r = 0; r < R; ++r) {
+            const int hh = h + ph - r;
+            if (hh < 0 || hh % sh) continue;
+            const int ho = hh / sh;
+            if (ho >= Ho) continue;
+            for (int s_ = 0; s_ < S; ++s_) {
+                const int ww = w_ + pw - s_;
+                if (ww < 0 || ww % sw) continue;
+                const int wo = ww / sw;
+                if (wo >= Wo) continue;
+                acc = __fadd_rn(acc, gcols[((n * Ho + ho) * Wo + wo) * ldg + ((int64_t)r * S + s_) * C + c]);
+            }
+        }
+        if (x && !(fabsf(x[i]) <= cl)) acc = 0.f;
+        gx[i] = acc;
+    }
+}
 }  // namespace axq
 
 extern "C" axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float* gy,
@@ -173,28 +266,60 @@ extern "C" axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, c
     if (gx && (!qw || !d_scale_w || (x && !d_clip_a))) return AXQ_ERR_INVALID;
     if (gw && (!qa || !d_scale_a || (w && !d_clip_w))) return AXQ_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // one product: split K (deterministic, through the workspace) until ~2 CTAs per SM
-    auto product = [&](bool ta, int64_t Mg, int64_t Ng, int64_t Kg, const float* A, int64_t lda,
-                       const int8_t* B, const float* sB, float* C, const float* R, const float* clip) {
-        const int64_t tiles = ((Ng + ste::BN - 1) / ste::BN) * ((Mg + ste::BM - 1) / ste::BM);
-        int64_t S = std::min<int64_t>({(2 * (int64_t)sms + tiles - 1) / tiles, 16, std::max<int64_t>(1, Kg / 64)});
-        if (!workspace || S * Mg * Ng > workspace_elems) S = 1;
-        const int64_t kc = ((Kg + S - 1) / S + ste::BK - 1) / ste::BK * ste::BK;
-        S = (Kg + kc - 1) / kc;
-        dim3 grid((unsigned)((Ng + ste::BN - 1) / ste::BN), (unsigned)((Mg + ste::BM - 1) / ste::BM), (unsigned)S);
-        float* out = S > 1 ? workspace : C;
-        if (ta) ste_gemm_kernel<true><<<grid, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, Ng, sB, out, Ng, R, Ng, clip, kc);
-        else ste_gemm_kernel<false><<<grid, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, Ng, sB, out, Ng, R, Ng, clip, kc);
-        if (S > 1)
-            ste_reduce_kernel<<<(unsigned)std::min<int64_t>((Mg * Ng + 255) / 256, 8 * sms), 256, 0, st>>>(
-                (int)S, Mg * Ng, Ng, workspace, C, R, clip);
-    };
-    if (gx && K > 0) product(false, M, K, N, gy, N, qw, d_scale_w, gx, x, d_clip_a);   // gy . fq(W)
-    if (gw && K > 0) product(true, N, K, M, gy, N, qa, d_scale_a, gw, w, d_clip_w);    // gy^T . fq(X)
-    if (gb) ste_colsum_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(M, N, gy, N, gb);
+    if (gx && K > 0) ste_product(false, M, K, N, gy, N, qw, K, d_scale_w, gx, K, x, d_clip_a, workspace, workspace_elems, st);
+    if (gw && K > 0) ste_product(true, N, K, M, gy, N, qa, K, d_scale_a, gw, K, w, d_clip_w, workspace, workspace_elems, st);
+    if (gb) ste_colsum(M, N, gy, gb, workspace, workspace_elems, st);
     const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
+}
+
+// NEXT-4 for convolution (groups = 1, dilation 1): the STE backward through the explicit im2col
+// of the forward's codes (the conv is the GEMM of its im2col matrix), see include/axq.h.
+extern "C" axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const float* gy, const int8_t* qx,
+                                              const float* d_scale_a, const float* x, const float* d_clip_a,
+                                              const int8_t* qw, const float* d_scale_w, const float* w,
+                                              const float* d_clip_w, float* gx, float* gw, float* gb,
+                                              int8_t* cols, int64_t ldcols, float* gcols, float* workspace,
+                                              int64_t workspace_elems, void* stream) {
+    using namespace axq;
+    if (!d || d->groups != 1 || d->dil_h != 1 || d->dil_w != 1 || (d->c_valid && d->c_valid != d->C) ||
+        d->N < 0 || d->H <= 0 || d->W <= 0 || d->C <= 0 || d->K <= 0 || d->R <= 0 || d->S <= 0 ||
+        d->stride_h <= 0 || d->stride_w <= 0 || d->pad_h < 0 || d->pad_w < 0)
+        return AXQ_ERR_INVALID;
+    const int64_t Ho = (d->H + 2 * d->pad_h - d->R) / d->stride_h + 1, Wo = (d->W + 2 * d->pad_w - d->S) / d->stride_w + 1;
+    if (Ho <= 0 || Wo <= 0) return AXQ_ERR_INVALID;
+    const int64_t M = d->N * Ho * Wo, Kc = d->R * d->S * d->C, No = d->K;
+    if (M >= ((int64_t)1 << 31) || d->N * d->H * d->W * d->C >= ((int64_t)1 << 40)) return AXQ_ERR_INVALID;
+    if (!gy && M > 0) return AXQ_ERR_INVALID;
+    if (gw && (!qx || !d_scale_a || !cols || ldcols < Kc || (ldcols & 15) || (w && !d_clip_w))) return AXQ_ERR_INVALID;
+    if (gx && (!qw || !d_scale_w || !gcols || (x && !d_clip_a))) return AXQ_ERR_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (M == 0) {   // empty sums
+        if (gx) e = cudaMemsetAsync(gx, 0, d->N * d->H * d->W * d->C * sizeof(float), st);
+        if (e == cudaSuccess && gw) e = cudaMemsetAsync(gw, 0, No * Kc * sizeof(float), st);
+        if (e == cudaSuccess && gb) e = cudaMemsetAsync(gb, 0, No * sizeof(float), st);
+        return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
+    }
+    if (gw) {   // gw[k][(r, s, c)] = mask * sum_m gy[m][k] * fq(im2col(qx)[m][(r, s, c)])
+        const axq_status r = axq_im2col_nhwc_i8(qx, d->N, d->H, d->W, d->C, 0, d->R, d->S, d->stride_h, d->stride_w,
+                                                d->pad_h, d->pad_w, cols, ldcols, stream);
+        if (r != AXQ_OK) return r;
+        ste_product(true, No, Kc, M, gy, No, cols, ldcols, d_scale_a, gw, Kc, w, d_clip_w, workspace,
+                    workspace_elems, st);
+    }
+    if (gx) {   // gcols = gy . fq(W) [M][(r, s, c)], then the adjoint of im2col, masked
+        ste_product(false, M, Kc, No, gy, No, qw, Kc, d_scale_w, gcols, Kc, nullptr, nullptr, workspace,
+                    workspace_elems, st);
+        const int64_t total = d->N * d->H * d->W * d->C;
+        int sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        ste_col2im_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 16 * sms), 256, 0, st>>>(
+            total, (int)d->H, (int)d->W, (int)d->C, (int)d->R, (int)d->S, (int)d->stride_h, (int)d->stride_w,
+            (int)d->pad_h, (int)d->pad_w, (int)Ho, (int)Wo, gcols, Kc, x, d_clip_a, gx);
+    }
+    if (gb) ste_colsum(M, No, gy, gb, workspace, workspace_elems, st);
+    e = cudaGetLastError();
     return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
 }

@@ -25,7 +25,7 @@ def run(M, N, K):
     s = torch.tensor([0.01], device="cuda")
     clip = torch.tensor([3.0], device="cuda")
     gx, gw, gb = torch.empty(M, K, device="cuda"), torch.empty(N, K, device="cuda"), torch.empty(N, device="cuda")
-    ws = torch.empty(16 * max(M, N) * K, device="cuda")
+    ws = torch.empty(128 * min(M, N) * K, device="cuda")
     flush = torch.empty(64 << 20, device="cuda")
     ts = []
     for i in range(13):
@@ -44,7 +44,39 @@ def run(M, N, K):
             "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3)}
 
 
+def run_conv(N, C, H, K, R, st):
+    pd = R // 2
+    Ho = (H + 2 * pd - R) // st + 1
+    g = torch.Generator(device="cuda").manual_seed(2)
+    gy = torch.randn(N, Ho, Ho, K, device="cuda", generator=g)
+    qx = torch.randint(-127, 128, (N, H, H, C), dtype=torch.int8, device="cuda", generator=g)
+    qw = torch.randint(-127, 128, (K, R, R, C), dtype=torch.int8, device="cuda", generator=g)
+    s = torch.tensor([0.01], device="cuda")
+    gx, gw, gb = torch.empty(N, H, H, C, device="cuda"), torch.empty(K, R, R, C, device="cuda"), torch.empty(K, device="cuda")
+    M, Kc = N * Ho * Ho, R * R * C
+    cols = torch.empty(M, (Kc + 15) // 16 * 16, dtype=torch.int8, device="cuda")
+    gcols = torch.empty(M, Kc, device="cuda")
+    ws = torch.empty(128 * K * Kc, device="cuda")
+    d = ax.conv_desc(N, H, H, C, K, R, R, (st, st), (pd, pd))
+    flush = torch.empty(64 << 20, device="cuda")
+    ts = []
+    for i in range(8):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        ax.axq_ste_conv2d_backward(d, gy, qx, s, qw, s, gx=gx, gw=gw, gb=gb, cols=cols, gcols=gcols, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    fl = 2 * 2 * M * K * Kc
+    return {"conv": [N, C, H, K, R, st], "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
+            "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3)}
+
+
 if __name__ == "__main__":
     out = {"metric": "STE backward (NEXT-4) GFLOP/s", "peak_tflops_fp32_fma": round(PEAK / 1e12, 1),
-           "shapes": [run(256, 1024, 1024), run(256, 1000, 2048), run(2048, 4096, 1024)]}
+           "shapes": [run(256, 1024, 1024), run(256, 1000, 2048), run(2048, 4096, 1024)],
+           "conv_shapes": [run_conv(32, 64, 56, 64, 3, 1), run_conv(32, 256, 14, 256, 3, 1)]}
     print(json.dumps(out))

@@ -90,3 +90,40 @@ def test_ste_backward_invalid(ax):
     with pytest.raises(ax.AxqError):   # gx requested without the weight scale
         ax.axq_ste_linear_backward(gy, torch.zeros(4, 5, dtype=torch.int8, device=DEV), None, qw,
                                    None, gx=gx)
+
+
+CONV_SHAPES = [(2, 8, 9, 9, 16, 3, 3, 1, 1), (1, 16, 11, 10, 24, 3, 3, 2, 1), (3, 32, 6, 7, 20, 1, 1, 1, 0),
+               (2, 64, 14, 14, 64, 3, 3, 1, 1), (1, 3, 20, 18, 8, 7, 7, 2, 3)]
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES)
+@pytest.mark.parametrize("masked", [False, True])
+def test_ste_conv_backward(ax, shape, masked):
+    N, C, H, W, K, R, S, st, pd = shape
+    x = datagen.normal(90 + C, 1, (N, H, W, C))
+    wt = datagen.normal(90 + C, 2, (K, R, S, C), 0.2)
+    qx, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(wt, 8)
+    Ho, Wo = (H + 2 * pd - R) // st + 1, (W + 2 * pd - S) // st + 1
+    gy = datagen.normal(90 + C, 3, (N, Ho, Wo, K))
+    clip_a = np.float32(np.quantile(np.abs(x), 0.8)) if masked else None
+    clip_w = np.float32(np.quantile(np.abs(wt), 0.8)) if masked else None
+    mk = dict(x=x, clip_a=clip_a, w=wt, clip_w=clip_w) if masked else {}
+    ref = oracle.ste_conv2d_backward(gy, qx, sa, qw, sw, (st, st), (pd, pd), **mk)
+    # sum of |terms| per output: the same products over absolute values
+    absref = oracle.ste_conv2d_backward(np.abs(gy), np.abs(qx.astype(np.int64)).astype(np.int8), sa,
+                                        np.abs(qw.astype(np.int64)).astype(np.int8), sw, (st, st), (pd, pd))
+    f = lambda v: _t(np.array([v], dtype=np.float32))
+    d = ax.conv_desc(N, H, W, C, K, R, S, (st, st), (pd, pd))
+    gx = torch.full((N, H, W, C), np.nan, device=DEV)
+    gw = torch.full((K, R, S, C), np.nan, device=DEV)
+    gb = torch.full((K,), np.nan, device=DEV)
+    kw = dict(x=_t(x), d_clip_a=f(clip_a), w=_t(wt), d_clip_w=f(clip_w)) if masked else {}
+    ax.axq_ste_conv2d_backward(d, _t(gy), _t(qx), f(sa), _t(qw), f(sw), gx=gx, gw=gw, gb=gb, **kw)
+    torch.cuda.synchronize()
+    M = N * Ho * Wo
+    for got, r, a_, n in ((gx, ref[0], absref[0], K * R * S), (gw, ref[1], absref[1], M), (gb, ref[2], absref[2], M)):
+        got = got.cpu().numpy()
+        assert np.isfinite(got).all()
+        err = np.abs(got.astype(np.float64) - r.astype(np.float64))
+        assert (err <= _bound(n, a_.astype(np.float64), r)).all(), float(err.max())

@@ -73,3 +73,40 @@ def test_ste_brute_force_tiny():
             s = sum(float(gy[m, n]) * float(np.float32(sa) * np.float32(qa[m, k])) for m in range(M))
             assert gw[n, k] == np.float32(s)
         assert gb[n] == np.float32(sum(float(gy[m, n]) for m in range(M)))
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 7, 6, 4, 3, 3, 1, 1), (1, 5, 9, 8, 6, 3, 3, 2, 1),
+                                   (2, 4, 5, 5, 3, 1, 1, 1, 0), (1, 2, 8, 7, 5, 5, 3, 2, 2)])
+def test_ste_conv_matches_autograd(shape):
+    """The conv STE backward equals torch autograd of conv2d on the fake-quantized operands."""
+    N, C, H, W, K, R, S, st, pd = shape
+    x = datagen.normal(70 + C, 1, (N, H, W, C))
+    wt = datagen.normal(70 + C, 2, (K, R, S, C), 0.2)
+    qx, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(wt, 8)
+    Ho, Wo = (H + 2 * pd - R) // st + 1, (W + 2 * pd - S) // st + 1
+    gy = datagen.normal(70 + C, 3, (N, Ho, Wo, K))
+    xf = torch.tensor(oracle.fake_quant(qx, sa).transpose(0, 3, 1, 2), dtype=torch.float64, requires_grad=True)
+    wf = torch.tensor(oracle.fake_quant(qw, sw).transpose(0, 3, 1, 2), dtype=torch.float64, requires_grad=True)
+    b = torch.zeros(K, dtype=torch.float64, requires_grad=True)
+    y = torch.nn.functional.conv2d(xf, wf, b, stride=st, padding=pd)
+    y.backward(torch.tensor(gy.transpose(0, 3, 1, 2), dtype=torch.float64))
+    gx, gw, gb = oracle.ste_conv2d_backward(gy, qx, sa, qw, sw, (st, st), (pd, pd))
+    np.testing.assert_allclose(gx, xf.grad.numpy().transpose(0, 2, 3, 1).astype(np.float32), rtol=2e-7, atol=1e-9)
+    np.testing.assert_allclose(gw, wf.grad.numpy().transpose(0, 2, 3, 1).astype(np.float32), rtol=2e-7, atol=1e-9)
+    np.testing.assert_allclose(gb, b.grad.numpy().astype(np.float32), rtol=2e-7, atol=1e-9)
+
+
+def test_ste_conv_1x1_equals_linear():
+    """A 1x1 stride-1 conv is the linear layer over pixels: both STE backwards agree."""
+    N, H, W, C, K = 2, 3, 4, 5, 6
+    x = datagen.normal(80, 1, (N, H, W, C))
+    wt = datagen.normal(80, 2, (K, 1, 1, C), 0.2)
+    qx, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(wt, 8)
+    gy = datagen.normal(80, 3, (N, H, W, K))
+    gx, gw, gb = oracle.ste_conv2d_backward(gy, qx, sa, qw, sw)
+    lx, lw, lb = oracle.ste_linear_backward(gy.reshape(-1, K), qx.reshape(-1, C), sa, qw.reshape(K, C), sw)
+    np.testing.assert_allclose(gx.reshape(-1, C), lx, rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(gw.reshape(K, C), lw, rtol=1e-6, atol=1e-9)
+    np.testing.assert_array_equal(gb, lb)
