@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(ste::NT) ste_gemm_kernel(int64_t M, int64_t N,
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     const float sb = *s_b;
     constexpr int LA = BM * BK / NT, LB = BN * BK / NT;
-    float ra[LA], rb[LB];
+    float ra[LA];
+    int rb[LB];   // raw codes: converted in stash(), after the current tile's FMAs (not stalling on the load)
     auto fetch = [&](int64_t k0) {
 #pragma unroll
         for (int i = 0; i < LA; ++i) {
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(ste::NT) ste_gemm_kernel(int64_t M, int64_t N,
             const int idx = tid + i * NT;
             const int kk = idx / BN, c = idx - kk * BN;
             const int64_t k = k0 + kk, n = n0 + c;
-            rb[i] = (k < ke && n < N) ? __fmul_rn(sb, (float)B[k * ldb + n]) : 0.f;   // fake-quant value
+            rb[i] = (k < ke && n < N) ? (int)B[k * ldb + n] : 0;
         }
     };
     auto stash = [&](int buf) {
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(ste::NT) ste_gemm_kernel(int64_t M, int64_t N,
         for (int i = 0; i < LB; ++i) {
             const int idx = tid + i * NT;
             const int kk = idx / BN, c = idx - kk * BN;
-            Bs[buf][kk][c] = rb[i];
+            Bs[buf][kk][c] = __fmul_rn(sb, (float)rb[i]);   // fake-quant value fl(s * q)
         }
     };
     float acc[8][8];
