@@ -19,8 +19,11 @@
  *     bit-identical for every tiling, split-K factor and GPU count (A23).
  *   - fp32 steps are pinned (IEEE division, round-half-even, no FMA contraction) so that
  *     quantized codes match the oracle bit for bit (A1, A3, A14).
- *   - Reentrant; LUT handles are immutable after creation, one per device, usable from
- *     any stream.
+ *   - Reentrant: calls from several host threads, and launches in flight on several
+ *     streams, never share library-owned mutable state.  LUT and weight-pack handles are
+ *     immutable after creation (one per device) and usable from any stream.  The only
+ *     per-call scratch is the caller's epilogue workspace (axq_epilogue.workspace): one
+ *     workspace must not be used by two launches that may run concurrently.
  */
 #ifndef AXQ_H
 #define AXQ_H
@@ -52,6 +55,20 @@ typedef enum {
 } axq_lut_repr;
 
 typedef struct axq_lut* axq_lut_t;
+
+/* Kernel family of the last LUT launch made by the calling thread (axq_last_path): low byte
+ * the kernel, plus flags.  Observability for tests and measurement; no effect on results. */
+#define AXQ_PATH_V1 1         /* lut_mm_kernel: per-lane gather from the resident table */
+#define AXQ_PATH_P4 2         /* lut_p4_kernel: packed tables, mma.sync exact part */
+#define AXQ_PATH_P4W 3        /* lut_p4w_kernel: packed tables, tcgen05 exact part, warp roles */
+#define AXQ_PATH_GCONV 4      /* grouped / depthwise resident-table kernels (NEXT-3) */
+#define AXQ_PATH_WIDE 5       /* wide (b = 9..12) kernels (NEXT-2) */
+#define AXQ_PATH_LSTM_REC 6   /* persistent LSTM recurrence */
+#define AXQ_PATH_F32A 7       /* quantize-on-load kernel (axq_lut_gemm_f32a / axq_lut_conv2d_f32) */
+#define AXQ_PATH_P4W16 8      /* lut_p4w16_kernel: packed int16 E tables (|E| beyond int8) */
+#define AXQ_PATH_SPLITK 0x100 /* K split across CTAs (int32 atomics + epilogue pass) */
+#define AXQ_PATH_STREAMK 0x200/* stream-K pieces in the caller's workspace */
+axq_status axq_last_path(int* out);
 
 /* Returns the CUDA error code of the last AXQ_ERR_CUDA on this thread (0 if none). */
 int axq_last_cuda_error(void);
@@ -151,11 +168,15 @@ axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_
  *     q_out[m][n] = clamp(rint(fl(v / *d_scale_out)))   if q_out  (requantize for the next
  *                                    layer with bits_out, same rule as axq_quantize)
  * Zero-initialise the struct and set what is needed.  workspace: NULL, or device int32
- * scratch of M*N elements that lets the library split K across CTAs when M*N alone cannot
- * fill the GPU, or (packed-table P4T kernel) cut tiles at stream-K boundaries (results
- * identical).  A workspace must be ZERO-FILLED when first passed; every call returns it
- * zero-filled again, so one buffer can be reused across calls and layers.  Layout of y: GEMM -> [M][ldy]; conv -> NCHW unless
- * y_nhwc = 1 ([N*Ho*Wo][ldy]).  q_out is always [M][ldq] (conv: NHWC). */
+ * scratch (16-byte aligned) of workspace_elems elements (0 = M*N, the minimum) owned by the
+ * caller.  It lets the library split K across CTAs when the M*N outputs alone cannot fill
+ * the GPU (needs >= M*N elements), or let the packed-table P4W kernel cut tiles at stream-K
+ * boundaries (needs >= axq_workspace_elems(M, N) elements: 256 tile counters, then per-CTA
+ * partial slots).  Results are identical with or without it.  A workspace must be
+ * ZERO-FILLED when first passed; every call leaves its first 256 elements zero again (the
+ * rest is scratch), so one buffer can be reused across calls and layers ON ONE STREAM -- two
+ * launches that may run concurrently need two workspaces.  Layout of y: GEMM -> [M][ldy];
+ * conv -> NCHW unless y_nhwc = 1 ([N*Ho*Wo][ldy]).  q_out is always [M][ldq] (conv: NHWC). */
 typedef struct axq_epilogue {
     const float* d_scale_a;   /* device fp32 scalar: activation scale (required) */
     const float* d_scale_w;   /* device fp32 scalar: weight scale (required) */
@@ -174,7 +195,13 @@ typedef struct axq_epilogue {
     const float* d_scale_w_ch;/* device fp32 [N] per-output-channel weight scales or NULL
                                  (NEXT-1, "weight ranges are per channel"): column n then
                                  uses fl(s_a * s_w[n]) in place of fl(s_a * s_w) (A32) */
+    int64_t workspace_elems;  /* int32 elements of workspace; 0 = M*N */
 } axq_epilogue;
+
+/* axq_workspace_elems: the epilogue workspace size (int32 elements) that enables every
+ * work decomposition for an M x N output on the current device: max(M*N, 256 + 2 * SMs *
+ * 896 * 16).  -1 for negative extents. */
+int64_t axq_workspace_elems(int64_t M, int64_t N);
 
 axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
                            const int8_t* W, int64_t ldw, axq_lut_t lut,
@@ -260,12 +287,12 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
                              const axq_epilogue* ep, int32_t* Y, void* stream);
 /* axq_wpack_kernel: selects the kernel behind axq_lut_gemm_wp / axq_lut_conv2d_wp for the
  *   calling process (all results are bit-identical; this is a performance switch for
- *   measurement): 0 = default (P4W; P4 for the 4-byte-tap conv loader), 1 = P4 (exact part on mma.sync, 16 warps, 512- or
- *   1024-row tiles), 2 = P4T (exact part on tcgen05.mma with TMEM accumulators, 32 warps,
- *   1024-row tiles), 3 = P4W (P4T warp-specialised: 4 producer warps stream the operands,
- *   28 consumer warps look up, 896-row tiles).  Returns the previous setting, or -1 for an
- *   unknown value (unchanged). */
-int axq_wpack_kernel(int variant);
+ *   measurement): 0 = default (P4W; P4 for the 4-byte-tap conv loader), 1 = P4 (exact part on
+ *   mma.sync, 16 warps, 512- or 1024-row tiles), 3 = P4W (exact part on tcgen05.mma with TMEM
+ *   accumulators, warp-specialised: 4 producer warps stream the operands, 16-28 consumer warps
+ *   look up, 512- or 896-row tiles).  Returns the previous setting, or -1 for an unknown value
+ *   (unchanged). */
+int axq_wpack_kernel(int variant);   /* 2 (the former P4T variant) is retired: returns -1 */
 /* axq_wpack_shapes: consumer-warp counts of the P4W shapes for the calling process (tile rows =
  *   32 x warps; a performance switch, all results bit-identical).  main_cw: non-residual layers
  *   with half-range 32-k tables -- 28 (default), 24 or 20; res_cw: layers with a residual

@@ -32,7 +32,13 @@ EXPORTED = [
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
+    "axq_last_path", "axq_workspace_elems",
 ]
+
+# axq_last_path kernel families (include/axq.h AXQ_PATH_*)
+PATH_NAMES = {1: "v1", 2: "p4", 3: "p4w", 4: "gconv", 5: "wide", 6: "lstm_rec", 7: "f32a",
+              8: "p4w16"}
+PATH_SPLITK, PATH_STREAMK = 0x100, 0x200
 
 
 class AxqError(RuntimeError):
@@ -48,7 +54,7 @@ class axq_epilogue(ctypes.Structure):
                 ("ldr", ctypes.c_int64), ("relu", ctypes.c_int32), ("y_nhwc", ctypes.c_int32),
                 ("q_out", ctypes.c_void_p), ("ldq", ctypes.c_int64),
                 ("d_scale_out", ctypes.c_void_p), ("bits_out", ctypes.c_int32),
-                ("d_scale_w_ch", ctypes.c_void_p)]
+                ("d_scale_w_ch", ctypes.c_void_p), ("workspace_elems", ctypes.c_int64)]
 
 
 class axq_conv_desc(ctypes.Structure):
@@ -74,6 +80,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_last_cuda_error": ([], i32),
         "axq_status_string": ([i32], ctypes.c_char_p),
         "axq_version": ([], i32),
+        "axq_last_path": ([ctypes.POINTER(i32)], i32),
+        "axq_workspace_elems": ([i64, i64], i64),
         "axq_lut_create": ([i32, vp, ctypes.POINTER(vp)], i32),
         "axq_lut_destroy": ([vp], i32),
         "axq_lut_info": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -233,8 +241,20 @@ def axq_wpack_shapes(main_cw: int = 0, res_cw: int = 0, small_cw: int = 0) -> No
     _check("axq_wpack_shapes", load().axq_wpack_shapes(int(main_cw), int(res_cw), int(small_cw)))
 
 
+def axq_last_path() -> tuple[str, int]:
+    """(kernel family, flags) of the calling thread's last LUT launch (include/axq.h)."""
+    v = ctypes.c_int()
+    _check("axq_last_path", load().axq_last_path(ctypes.byref(v)))
+    return PATH_NAMES.get(v.value & 0xff, "none"), v.value & ~0xff
+
+
+def axq_workspace_elems(M: int, N: int) -> int:
+    """Epilogue workspace size (int32 elements) enabling every decomposition for M x N outputs."""
+    return int(load().axq_workspace_elems(int(M), int(N)))
+
+
 def axq_wpack_kernel(variant: int) -> int:
-    """Select the packed-table kernel (0 default = P4W (P4 for C % 16 != 0 convs), 1 P4, 2 P4T, 3 P4W); returns the previous."""
+    """Select the packed-table kernel (0 default = P4W (P4 for C % 16 != 0 convs), 1 P4, 3 P4W); returns the previous."""
     r = load().axq_wpack_kernel(int(variant))
     if r < 0:
         raise ValueError("unknown packed-table kernel variant %r" % variant)
@@ -288,10 +308,13 @@ def make_epilogue(d_scale_a, d_scale_w, bias=None, y=None, ldy=0, workspace=None
                   d_scale_out=None, bits_out=0, d_scale_w_ch=None) -> axq_epilogue:
     """d_scale_w: the per-tensor weight scale (device scalar); d_scale_w_ch: per-output-channel
     weight scales [N] (NEXT-1), which take precedence when given."""
+    if workspace is not None:
+        assert workspace.is_cuda and workspace.element_size() == 4 and workspace.is_contiguous()
     ep = axq_epilogue(_ptr(d_scale_a), _ptr(d_scale_w), _ptr(bias), _ptr(y), int(ldy),
                       _ptr(workspace), _ptr(residual), int(ldr), int(bool(relu)),
                       int(bool(y_nhwc)), _ptr(q_out), int(ldq), _ptr(d_scale_out),
-                      int(bits_out), _ptr(d_scale_w_ch))
+                      int(bits_out), _ptr(d_scale_w_ch),
+                      int(workspace.numel()) if workspace is not None else 0)
     # the struct holds raw device pointers: keep the tensors alive as long as it lives
     ep._keep = (d_scale_a, d_scale_w, bias, y, workspace, residual, q_out, d_scale_out, d_scale_w_ch)
     return ep

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -46,34 +47,14 @@ struct axq_lut {
 namespace {
 
 thread_local int g_last_cuda = 0;
+thread_local int g_last_path = 0;   // axq_last_path: AXQ_PATH_* of the last LUT launch on this thread
 
 inline axq_status cuda_fail(cudaError_t e) {
     g_last_cuda = (int)e;
     return AXQ_ERR_CUDA;
 }
 
-// Stream-K tile counters of the P4T kernel, one zero-filled block per device (the kernel leaves
-// them zero).  Allocated by axq_wpack_create, so no hot call allocates.
-// P4W also keeps its stream-K pieces in library-owned per-CTA slots: [SMs][2][896][16] int32.
-static int32_t* g_sk_cnt[64];
-static int32_t* g_sk_part[64];
-static int32_t* streamk_counters(int dev) { return (dev >= 0 && dev < 64) ? g_sk_cnt[dev] : nullptr; }
-static int32_t* streamk_parts(int dev) { return (dev >= 0 && dev < 64) ? g_sk_part[dev] : nullptr; }
 int sm_count();
-static cudaError_t ensure_streamk_counters(int dev) {
-    if (dev < 0 || dev >= 64 || g_sk_cnt[dev]) return cudaSuccess;
-    int32_t* c = nullptr;
-    int32_t* part = nullptr;
-    cudaError_t e = cudaMalloc(&c, 4096 * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMemset(c, 0, 4096 * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&part, (size_t)sm_count() * 2 * 896 * 16 * sizeof(int32_t));
-    if (e == cudaSuccess) {
-        g_sk_cnt[dev] = c;
-        g_sk_part[dev] = part;
-    }
-    return e;
-}
-
 
 inline axq_status check_launch() {
     cudaError_t e = cudaGetLastError();
@@ -457,6 +438,14 @@ static axq_status gemm_common(int64_t M, int64_t N, int64_t K, const int8_t* A, 
     return overflow_guard(lut, K);
 }
 
+// The caller's epilogue workspace if it can hold `need` int32 elements (split-K accumulators),
+// else null (no K split).  workspace_elems == 0 means "M*N", the documented minimum.
+static int32_t* ws_if_fits(const axq_epilogue* ep, int64_t need) {
+    if (!ep || !ep->workspace) return nullptr;
+    if (ep->workspace_elems > 0 && ep->workspace_elems < need) return nullptr;
+    return ep->workspace;
+}
+
 static axq_status check_epilogue(const axq_epilogue* ep, int64_t N, bool conv) {
     if (!ep || !ep->d_scale_a || !ep->d_scale_w) return AXQ_ERR_INVALID;
     const bool rows = !conv || ep->y_nhwc;
@@ -502,6 +491,7 @@ static axq_status run_mm(axq::MMArgs& p, int loader, axq_lut_t lut, const axq::E
     const int64_t splits = p.K > 0 ? (p.K + p.k_split - 1) / p.k_split : 1;
     const int64_t bm = cfg_bm(c), bn = cfg_bn(c);
     dim3 grid((unsigned)((p.M + bm - 1) / bm), (unsigned)((p.N + bn - 1) / bn), (unsigned)splits);
+    g_last_path = AXQ_PATH_V1 | (splits > 1 ? AXQ_PATH_SPLITK : 0);
     if (!epi) {
         p.C_out = C_raw;
         p.ldc = ldc;
@@ -556,7 +546,7 @@ axq_status axq_lut_gemm_dq(int64_t M, int64_t N, int64_t K, const int8_t* A, int
     fill_common(p, lut);
     axq::EpiArgs e = to_epi(ep, false, 0);
     int loader = (aligned16(A) && (lda & 15) == 0) ? axq::LOAD_GEMM : axq::LOAD_GEMM_BYTES;
-    return run_mm(p, loader, lut, &e, ep->workspace, nullptr, 0, S(stream));
+    return run_mm(p, loader, lut, &e, ws_if_fits(ep, p.M * p.N), nullptr, 0, S(stream));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -632,7 +622,7 @@ static axq_status gconv_run(const axq_conv_desc* d, const int8_t* X, const int8_
                 if (e.residual) e.residual += off;
                 if (e.q) e.q += off;
                 if (e.sw_ch) e.sw_ch += off;
-                r = run_mm(p, loader, lut, &e, ep->workspace, nullptr, 0, st);
+                r = run_mm(p, loader, lut, &e, ws_if_fits(ep, p.M * p.N), nullptr, 0, st);
             } else {
                 r = run_mm(p, loader, lut, nullptr, nullptr, Y + g * cout_g, d->K, st);
             }
@@ -640,6 +630,7 @@ static axq_status gconv_run(const axq_conv_desc* d, const int8_t* X, const int8_
         }
         return AXQ_OK;
     }
+    g_last_path = AXQ_PATH_GCONV;
     const int rc = axq::launch_gconv(lut->repr, a, st);
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }
@@ -707,7 +698,7 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
     if (p.M == 0 || p.N == 0) return AXQ_OK;
     const bool nchw = !ep->y_nhwc;
     axq::EpiArgs e = to_epi(ep, nchw, (int64_t)p.Ho * p.Wo);
-    return run_mm(p, loader, lut, &e, ep->workspace, nullptr, 0, S(stream));
+    return run_mm(p, loader, lut, &e, ws_if_fits(ep, p.M * p.N), nullptr, 0, S(stream));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -724,10 +715,6 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
     if (s != AXQ_OK) return s;
     axq_wpack* w = new axq_wpack();
     cudaGetDevice(&w->device);
-    if (ensure_streamk_counters(w->device) != cudaSuccess) {
-        delete w;
-        return cuda_fail(cudaGetLastError());
-    }
     w->t00 = lut->t00;
     w->N = N;
     w->K = K;
@@ -797,31 +784,33 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
     return AXQ_OK;
 }
 
-static int g_p4w_main_cw = 28;         // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
-static int64_t g_p4w_main_cw_max_k = 1 << 30;   // ... for layers with K up to this
-static int g_p4w_res_cw = 16;          // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape
-static int g_p4w_cw = 0;                // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
-static int64_t g_sk_full_waves = 8;    // AXQ_SK_FULL_WAVES: P4W layers of fewer than this many waves of
-                                       // tiles cut every iteration (no whole-wave phase): measured
-                                       // 73.5 -> 73.2 ms at 256 images, 10.79 -> 10.60 at 32 (4, 16 close)
-static int64_t g_sk_min_stages = 4;    // AXQ_SK_MIN_STAGES: stream-K pieces of >= 4 stages (measured
-                                       // with the 512-row residual shape: 1 -> 4 saves 0.3-0.7 ms per
-                                       // forward at 256-32 images; 6 is worse again)
-static int64_t g_p4w_ks16_max_k = 0;   // AXQ_P4W_KS16_MAX_K: measured slower, off
-static int g_wpack_kernel = 0;   // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 2 P4T, 3 P4W
+// Kernel-choice knobs (measurement switches).  Atomics: a setter racing a launch on another
+// thread sees either value, both of which give bit-identical results.
+static std::atomic<int> g_p4w_main_cw{28};        // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
+static std::atomic<int64_t> g_p4w_main_cw_max_k{1 << 30};   // ... for layers with K up to this
+static std::atomic<int> g_p4w_res_cw{16};         // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape
+static std::atomic<int> g_p4w_cw{0};              // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
+static std::atomic<int64_t> g_sk_full_waves{8};   // AXQ_SK_FULL_WAVES: P4W layers of fewer than this many waves of
+                                                  // tiles cut every iteration (no whole-wave phase): measured
+                                                  // 73.5 -> 73.2 ms at 256 images, 10.79 -> 10.60 at 32 (4, 16 close)
+static std::atomic<int64_t> g_sk_min_stages{4};   // AXQ_SK_MIN_STAGES: stream-K pieces of >= 4 stages (measured
+                                                  // with the 512-row residual shape: 1 -> 4 saves 0.3-0.7 ms per
+                                                  // forward at 256-32 images; 6 is worse again)
+static std::atomic<int64_t> g_p4w_ks16_max_k{0};  // AXQ_P4W_KS16_MAX_K: measured slower, off
+static std::atomic<int> g_wpack_kernel{0};        // axq_wpack_kernel: 0 default (P4W; P4 for c4 convs), 1 P4, 3 P4W
 
 static void p4w_read_env() {
-    static bool env_read = false;
-    if (env_read) return;
-    if (const char* v = std::getenv("AXQ_P4W_KS16_MAX_K")) g_p4w_ks16_max_k = std::atoll(v);
-    if (const char* v = std::getenv("AXQ_SK_MIN_STAGES")) g_sk_min_stages = std::max(1LL, std::atoll(v));
-    if (const char* v = std::getenv("AXQ_P4W_PDL")) axq::g_p4w_pdl = std::atoi(v);
-    if (const char* v = std::getenv("AXQ_P4W_CW")) g_p4w_cw = std::atoi(v);
-    if (const char* v = std::getenv("AXQ_P4W_RES_CW")) g_p4w_res_cw = std::atoi(v);
-    if (const char* v = std::getenv("AXQ_P4W_MAIN_CW")) g_p4w_main_cw = std::atoi(v);
-    if (const char* v = std::getenv("AXQ_SK_FULL_WAVES")) g_sk_full_waves = std::atoll(v);
-    if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
-    env_read = true;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (const char* v = std::getenv("AXQ_P4W_KS16_MAX_K")) g_p4w_ks16_max_k = std::atoll(v);
+        if (const char* v = std::getenv("AXQ_SK_MIN_STAGES")) g_sk_min_stages = std::max(1LL, std::atoll(v));
+        if (const char* v = std::getenv("AXQ_P4W_PDL")) axq::g_p4w_pdl = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_P4W_CW")) g_p4w_cw = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_P4W_RES_CW")) g_p4w_res_cw = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_P4W_MAIN_CW")) g_p4w_main_cw = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_SK_FULL_WAVES")) g_sk_full_waves = std::atoll(v);
+        if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
+    });
 }
 
 axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw) {
@@ -837,10 +826,26 @@ axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw) {
 }
 
 int axq_wpack_kernel(int variant) {
-    if (variant < 0 || variant > 3) return -1;
-    const int prev = g_wpack_kernel;
-    g_wpack_kernel = variant;
-    return prev;
+    if (variant < 0 || variant > 3 || variant == 2) return -1;   // 2 was the superseded P4T kernel
+    return g_wpack_kernel.exchange(variant);
+}
+
+// Stream-K scratch of the P4W kernel, carved from the caller's epilogue workspace (so two
+// launches on two streams with two workspaces never share it): [STREAMK_CNT] int32 tile
+// counters (zero on entry, left zero by the kernel), then one pair of [BM][16] int32 partial
+// slots per CTA.
+static constexpr int64_t STREAMK_CNT = 256;
+static int64_t streamk_elems(int bm) { return STREAMK_CNT + (int64_t)sm_count() * 2 * bm * axq::p4::TN; }
+
+axq_status axq_last_path(int* out) {
+    if (!out) return AXQ_ERR_INVALID;
+    *out = g_last_path;
+    return AXQ_OK;
+}
+
+int64_t axq_workspace_elems(int64_t M, int64_t N) {
+    if (M < 0 || N < 0) return -1;
+    return std::max<int64_t>(M * N, streamk_elems(896));
 }
 
 static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep, bool conv,
@@ -865,17 +870,22 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         return AXQ_ERR_INVALID;
     }
     if (a.mm.M == 0) return AXQ_OK;
-    // raw output may always split K (atomics into C); the fused epilogue needs a workspace
-    const bool can_split = ep ? (ep->workspace != nullptr) : true;
+    // raw output may always split K (atomics into C); the fused epilogue needs a workspace of
+    // M*N elements for that
+    const int64_t ws_elems = (ep && ep->workspace) ? (ep->workspace_elems > 0 ? ep->workspace_elems
+                                                                             : a.mm.M * a.mm.N) : 0;
+    const int64_t out_rows = a.transposed ? a.mm.N : a.mm.M, out_cols = a.transposed ? a.mm.M : a.mm.N;
+    const bool can_split = ep ? (ws_elems >= out_rows * out_cols) : true;
     // default: P4W, except the 4-byte-tap conv loader (e.g. the padded 3-channel stem), where
     // P4's 2 rows per lane measure faster
-    const int variant = g_wpack_kernel != 0 ? g_wpack_kernel : (a.c4 ? 1 : 3);
-    const bool use_tc = variant >= 2;                                 // P4T / P4W: tcgen05 exact part
+    const int kv = g_wpack_kernel.load();
+    const int variant = kv != 0 ? kv : (a.c4 ? 1 : 3);
+    const bool use_tc = variant == 3;                                 // P4W: tcgen05 exact part
     // P4W shape: 512-row tiles (16 consumer warps) for small row counts, where 896-row tiles
     // would leave lanes idle or cut a ragged second tile; not for residual epilogues or the
     // half-range 16-k stages (no such instantiation)
-    // k per stage: P4T 32 (half) / 16; P4W the same, except half-range tables with K <= 128
-    // (short tiles: 16-k stages, 4 deep)
+    // k per stage: 32 for half-range tables, 16 for full-range ones, except half-range tables
+    // with K <= AXQ_P4W_KS16_MAX_K (16-k stages, 4 deep)
     p4w_read_env();
     a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
     const bool res_ep = ep && ep->residual;
@@ -883,39 +893,40 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     // 512-row tiles when they pad fewer rows than 896-row ones (M <= 1024 always: one or two
     // nearly empty 896-row tiles), e.g. the LSTM input projection (M = 8192 = 16 x 512, 9.1 x 896)
     const int64_t pad512 = (a.mm.M + 511) / 512 * 512 - a.mm.M, pad896 = (a.mm.M + 895) / 896 * 896 - a.mm.M;
-    if (variant == 3 && !res_ep && !a.c4 && (!wp->half || a.ks == 32) && g_p4w_cw != 28 &&
-        (g_p4w_cw == 16 || a.mm.M <= 1024 || pad512 < pad896))
+    const int cw_forced = g_p4w_cw, res_cw = g_p4w_res_cw, main_cw = g_p4w_main_cw;
+    if (variant == 3 && !res_ep && !a.c4 && (!wp->half || a.ks == 32) && cw_forced != 28 &&
+        (cw_forced == 16 || a.mm.M <= 1024 || pad512 < pad896))
         a.cw = 16;
-    if (variant == 3 && res_ep && wp->half && a.ks == 32 && !a.c4 &&
-        (g_p4w_res_cw == 16 || g_p4w_res_cw == 20 || g_p4w_res_cw == 24))
-        a.cw = g_p4w_res_cw;
+    if (variant == 3 && res_ep && wp->half && a.ks == 32 && !a.c4 && (res_cw == 16 || res_cw == 20 || res_cw == 24))
+        a.cw = res_cw;
     if (variant == 3 && !res_ep && wp->half && a.ks == 32 && !a.c4 && a.cw == 28 &&
-        (g_p4w_main_cw == 16 || g_p4w_main_cw == 20 || g_p4w_main_cw == 24) && wp->Kp <= g_p4w_main_cw_max_k)
-        a.cw = g_p4w_main_cw;
+        (main_cw == 16 || main_cw == 20 || main_cw == 24) && wp->Kp <= g_p4w_main_cw_max_k)
+        a.cw = main_cw;
     const int bm = variant == 3 ? axq::p4w_bm(a.cw) : 1024;
     if (use_tc)
-        axq::p4t_plan(a.mm.M, a.mm.N, wp->Kp, a.ks, bm, sm_count(), can_split && !a.transposed, a.splits,
+        axq::p4w_plan(a.mm.M, a.mm.N, wp->Kp, a.ks, bm, sm_count(), can_split && !a.transposed, a.splits,
                       a.stages_per_split);
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
-    auto launch = [&](const axq::P4Args& x) {
-        return variant == 3 ? axq::launch_p4w(x, st) : variant == 2 ? axq::launch_p4t(x, st) : axq::launch_p4(x, st);
-    };
-    if (use_tc && ep && ep->workspace) {
+    auto launch = [&](const axq::P4Args& x) { return variant == 3 ? axq::launch_p4w(x, st) : axq::launch_p4(x, st); };
+    int path = variant == 3 ? AXQ_PATH_P4W : AXQ_PATH_P4;
+    if (use_tc && ep && ep->workspace && ws_elems >= streamk_elems(bm) &&
+        (reinterpret_cast<uintptr_t>(ep->workspace) & 15) == 0) {
         // stream-K whenever whole tiles would leave a partial wave (exact int32 pieces in the
-        // zero-filled workspace; finished by the kernel itself, no extra launch)
+        // caller's workspace; finished by the kernel itself, no extra launch)
         const int64_t tiles = ((a.mm.M + bm - 1) / bm) * ((a.mm.N + axq::p4::TN - 1) / axq::p4::TN);
-        int32_t* cnt = streamk_counters(dev);
-        if (cnt && tiles % sm_count() != 0) {
-            const bool full = variant == 3 && tiles < g_sk_full_waves * sm_count();
+        if (tiles % sm_count() != 0) {
+            const bool full = tiles < g_sk_full_waves * sm_count();
             a.streamk = full ? 2 : 1;
             a.splits = 1;
             a.stages_per_split = 0;
             // pieces of at least ~4 stages: a small tail is shared by fewer CTAs
             const int64_t tail_it = (full ? tiles : tiles % sm_count()) * (wp->Kp / a.ks);
-            a.sk_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), tail_it / g_sk_min_stages));
-            a.ws = variant == 3 ? streamk_parts(dev) : ep->workspace;
-            a.cnt = cnt;
+            a.sk_ctas = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sm_count(), STREAMK_CNT,
+                                                                      tail_it / g_sk_min_stages}));
+            a.cnt = ep->workspace;
+            a.ws = ep->workspace + STREAMK_CNT;
+            path |= AXQ_PATH_STREAMK;
         }
     }
     // column-block-fastest order when all of the layer's tables fit comfortably in L2
@@ -927,6 +938,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         if (e != cudaSuccess) return cuda_fail(e);
         a.mm.C_out = acc;
         a.mm.ldc = ld;
+        g_last_path = path | AXQ_PATH_SPLITK;
         int rc = launch(a);
         if (rc) return cuda_fail((cudaError_t)rc);
         return ep ? launch_epilogue(a.mm.M, a.mm.N, acc, ld, epi, st, acc) : AXQ_OK;
@@ -938,6 +950,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         a.mm.C_out = C;
         a.mm.ldc = ldc;
     }
+    g_last_path = path;
     int rc = launch(a);
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }
@@ -948,7 +961,7 @@ axq_status axq_lut_gemm_xs(int64_t N, const int8_t* W, int64_t ldw, axq_wpack_t 
     // P4W kernel runs with the weight rows as its row operand and writes the result transposed
     if (!xp || !xp->swap || N < 0 || (N > 0 && (!W || ldw < xp->K))) return AXQ_ERR_INVALID;
     if (!aligned16(W) || (ldw & 15)) return AXQ_ERR_UNSUPPORTED;
-    if (g_wpack_kernel == 1 || g_wpack_kernel == 2) return AXQ_ERR_UNSUPPORTED;   // P4W only
+    if (g_wpack_kernel.load() == 1) return AXQ_ERR_UNSUPPORTED;   // P4W only
     axq::P4Args a{};
     a.mm.A = W; a.mm.lda = ldw; a.mm.M = N; a.mm.N = xp->N; a.mm.K = xp->K;
     a.transposed = 1;
@@ -1153,6 +1166,7 @@ axq_status axq_lut_gemm16(int64_t M, int64_t N, int64_t K, const int16_t* A, int
         a.ldc = ldc;
     }
     if (M == 0 || N == 0) return AXQ_OK;
+    g_last_path = AXQ_PATH_WIDE;
     const int rc = axq::launch_wide(a, sm_count(), S(stream));
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }
@@ -1180,6 +1194,7 @@ axq_status axq_lstm_recurrent(int64_t T, int64_t B, int64_t H, const float* gate
     a.bits = bits; a.table = reinterpret_cast<const int8_t*>(lut->d_table);
     a.hs = hs; a.c_out = c_out; a.hq = workspace;
     a.bar = reinterpret_cast<unsigned int*>(workspace + ((2 * B * H + 15) / 16) * 16);
+    g_last_path = AXQ_PATH_LSTM_REC;
     const int rc = axq::launch_lstm_rec(a, sm_count(), S(stream));
     if (rc == -1) return AXQ_ERR_UNSUPPORTED;
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;

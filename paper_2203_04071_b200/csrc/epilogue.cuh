@@ -87,7 +87,7 @@ __device__ __forceinline__ void epi_store(float v, int64_t m, int64_t n, int64_t
 
 // Stand-alone epilogue over an int32 [M][N] accumulator (split-K path).
 // zero_acc: the workspace-accumulator form re-zeroes what it read, so a workspace is left
-// zero-filled for the stream-K kernel (lut_p4t.cuh), which relies on that.
+// zero-filled for the stream-K kernel (lut_p4w.cuh), which relies on that.
 static __global__ void epilogue_kernel(int64_t M, int64_t N, const int32_t* __restrict__ acc,
                                 int64_t ldacc, const EpiArgs e, int32_t* zero_acc = nullptr) {
     const float sc = __fmul_rn(*e.sa, *e.sw);

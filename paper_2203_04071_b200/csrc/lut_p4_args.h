@@ -50,9 +50,9 @@ struct P4Args {
     int c4;                     // conv with C % 16 != 0 (C % 4 == 0): 4-byte tap copies
     int streamk;                // stream-K decomposition (needs ws and cnt): 1 whole waves + cut
                                 // tail; 2 (P4W) every iteration cut, one slice per CTA
-    int32_t* ws;                // stream-K pieces: P4T int32 [M][N] (zero on entry, left zero);
-                                // P4W per-CTA partial slots [grid][2][896][16]
-    int32_t* cnt;               // stream-K tile counters (>= gridDim.x), zero on entry, left zero
+    int32_t* ws;                // P4W stream-K per-CTA partial slots [grid][2][BM][16] (caller's
+                                // epilogue workspace, after the counters)
+    int32_t* cnt;               // stream-K tile counters (>= sk_ctas), zero on entry, left zero
     int sk_ctas;                // P4W stream-K: CTAs sharing the tail (0 = all)
     int ks;                     // P4W: k per stage (16 or 32; 16 with half tables = 4 stages)
     int transposed;             // P4W: output element (row r, col c) goes to [c][r] (gemm_xs)

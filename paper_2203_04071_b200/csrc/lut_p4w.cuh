@@ -1,5 +1,5 @@
 // lut_p4w.cuh -- "P4W": warp-specialised packed-table LUT-GEMM / implicit-im2col LUT-conv
-// (sm_100a).  Same result as lut_p4.cuh / lut_p4t.cuh: acc[m][n] = sum_k LUT[a[m][k]][w[n][k]]
+// (sm_100a).  Same result as lut_p4.cuh / lut_mm.cuh: acc[m][n] = sum_k LUT[a[m][k]][w[n][k]]
 // in int32, exact, as  sum_k a*w (tcgen05.mma kind::i8, TMEM)  +  sum_k E[a][w] (packed tables).
 //
 // Roles inside one persistent CTA (1024 threads, one CTA per SM):
@@ -17,12 +17,13 @@
 //  * Row 32*w + lane of a tile is TMEM lane 32*(w % 4) + lane of MMA slice w / 4, so every
 //    consumer warp reads exactly the TMEM lane quarter it may access.
 //  * Tile order, stream-K tail (exact int32 pieces in the zero-filled workspace), split-K for
-//    raw output and the fused epilogue follow lut_p4t.cuh.
+//    raw output and the fused epilogue (tc_common.cuh).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "lut_p4t.cuh"
+#include "lut_p4.cuh"
+#include "tc_common.cuh"
 
 namespace axq {
 
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
-    // ---- work decomposition (shared by both roles): as lut_p4t.cuh ----
+    // ---- work decomposition (shared by both roles) ----
     const int64_t m_tiles = (p.M + BM - 1) / BM, n_blocks = (p.N + TN - 1) / TN;
     const int splits = P.splits > 0 ? P.splits : 1;
     const int64_t n_work = m_tiles * n_blocks * splits;

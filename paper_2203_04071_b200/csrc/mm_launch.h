@@ -37,7 +37,6 @@ struct P4Args;
 int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int8_t* dtab,
             uint32_t* tables, int8_t* wpk, int half, int swap, cudaStream_t st);
 int launch_p4(const P4Args& a, cudaStream_t st);
-int launch_p4t(const P4Args& a, cudaStream_t st);   // tcgen05 exact part, 32 warps (lut_p4t.cuh)
 int launch_p4w(const P4Args& a, cudaStream_t st);
 // P4W tile rows of a shape (cw consumer warps: 28 -> 896, 24 -> 768, 20 -> 640, 16 -> 512);
 // launch_p4w serves cw = 16 for non-residual layers (full-range, or half-range 32-k tables),
@@ -52,7 +51,7 @@ int launch_quantize16(const float* x, int64_t n, const float* d_scale, int bits,
                       cudaStream_t st);
 int launch_gconv(int repr, const GConvArgs& a, cudaStream_t st);   // gconv.cuh (groups > 1)
 int launch_lstm_rec(const LstmRecArgs& a, int sms, cudaStream_t st);   // lstm_rec.cuh
-void p4t_plan(int64_t M, int64_t N, int64_t Kp, int ks, int bm, int sms, bool can_split, int& splits, int& sps);
+void p4w_plan(int64_t M, int64_t N, int64_t Kp, int ks, int bm, int sms, bool can_split, int& splits, int& sps);
 void p4_plan(int64_t M, int64_t N, int64_t Kp, int sms, bool can_split, int& rpl, int& splits,
              int& sps);
 

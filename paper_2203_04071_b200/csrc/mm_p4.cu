@@ -1,6 +1,5 @@
 // mm_p4.cu -- host side of the P4 LUT kernel (lut_p4.cuh): weight packing and launch.
 #include "lut_p4.cuh"
-#include "lut_p4t.cuh"
 #include "lut_p4w.cuh"
 #include "mm_launch.h"
 
@@ -47,32 +46,6 @@ static int launch_p4_t(const P4Args& a, cudaStream_t st) {
     const unsigned g = (unsigned)std::min<int64_t>(work, sms > 0 ? sms : 148);
     lut_p4_kernel<RPL, HALF><<<g, p4::NT, p4::Geo<HALF>::SMEM_BYTES, st>>>(a);
     return (int)cudaGetLastError();
-}
-
-template <bool HALF>
-static int launch_p4t_t(const P4Args& a, cudaStream_t st) {
-    static unsigned configured = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    dev &= 31;
-    if (!(configured & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(lut_p4t_kernel<HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             p4t::Geo<HALF, p4t::ks_of<HALF>()>::SMEM_BYTES);
-        if (e != cudaSuccess) return (int)e;
-        configured |= 1u << dev;
-    }
-    const int64_t tiles = ((a.mm.M + p4t::BM - 1) / p4t::BM) * ((a.mm.N + p4::TN - 1) / p4::TN);
-    // stream-K: every SM gets a share of the (tile, stage) iterations
-    const int64_t work = a.streamk ? tiles * (a.Kp / p4t::ks_of<HALF>()) : tiles * a.splits;
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned g = (unsigned)std::min<int64_t>(work, sms > 0 ? sms : 148);
-    lut_p4t_kernel<HALF><<<g, p4t::NT, p4t::Geo<HALF, p4t::ks_of<HALF>()>::SMEM_BYTES, st>>>(a);
-    return (int)cudaGetLastError();
-}
-
-int launch_p4t(const P4Args& a, cudaStream_t st) {
-    return a.half ? launch_p4t_t<true>(a, st) : launch_p4t_t<false>(a, st);
 }
 
 int g_p4w_pdl = 1;   // programmatic dependent launch of P4W (AXQ_P4W_PDL=0 disables)
@@ -145,8 +118,8 @@ int launch_p4w(const P4Args& a, cudaStream_t st) {
     }
 }
 
-// P4T tiles are 1024 rows: split K (exact, int32 atomics) only when they cannot fill the SMs.
-void p4t_plan(int64_t M, int64_t N, int64_t Kp, int ks, int bm, int sms, bool can_split, int& splits, int& sps) {
+// Tensor-core packed-table tiles (P4W, bm rows): split K (exact, int32 atomics) only when they cannot fill the SMs.
+void p4w_plan(int64_t M, int64_t N, int64_t Kp, int ks, int bm, int sms, bool can_split, int& splits, int& sps) {
     const int64_t nst = Kp / ks, nb = (N + p4::TN - 1) / p4::TN;
     const int64_t t = ((M + bm - 1) / bm) * nb;
     splits = 1;

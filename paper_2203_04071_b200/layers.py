@@ -66,7 +66,8 @@ class ApproxLinear:
         b = self._bufs.get(M)
         if b is None:
             b = dict(qa=torch.empty(M, self.K, dtype=torch.int8, device=device),
-                     ws=torch.zeros(M, self.N, dtype=torch.int32, device=device))
+                     ws=torch.zeros(ax.axq_workspace_elems(M, self.N), dtype=torch.int32,
+                                            device=device))
             pth = self.path(M)
             if pth == "xspec":
                 # per-call activation tables (M x K x 1 KiB / 4 B) and their packed operand tile

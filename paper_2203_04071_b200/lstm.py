@@ -74,8 +74,8 @@ class ApproxLSTM:
                 hs=torch.empty(T, B, self.H, dtype=f32, device=d),
                 h0=torch.zeros(B, self.H, dtype=f32, device=d),
                 c=torch.empty(B, self.H, dtype=f32, device=d),
-                ws_ih=torch.zeros(T * B * self.H4, dtype=torch.int32, device=d),
-                ws=torch.zeros(B * self.H4, dtype=torch.int32, device=d),
+                ws_ih=torch.zeros(ax.axq_workspace_elems(T * B, self.H4), dtype=torch.int32, device=d),
+                ws=torch.zeros(ax.axq_workspace_elems(B, self.H4), dtype=torch.int32, device=d),
                 ws_rec=torch.empty(2 * B * self.H + 256, dtype=torch.int8, device=d))
         return self._bufs[key]
 

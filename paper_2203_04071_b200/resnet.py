@@ -176,7 +176,8 @@ class ApproxResNet:
             # fc: few images against 1000 classes -> activation-specialised packed tables, built
             # per forward from fc_q (axq_wpack_repack) + the 512-row P4W GEMM (axq_lut_gemm_xs)
             b["fc_xp"] = ax.WPack(self.lut, b["fc_q"], activations=True)
-        ws_elems = max(ws_elems, N * self.spec["fc"][2], b["stem_q"].numel())
+        ws_elems = max(ws_elems, N * self.spec["fc"][2], b["stem_q"].numel(),
+                       ax.axq_workspace_elems(1, 1))      # P4W stream-K counters + partial slots
         b["ws"] = torch.zeros(ws_elems, dtype=torch.int32, device=dev)
         b["shapes"] = shapes
         self._bufs[key] = b

@@ -11,15 +11,20 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.fixture(scope="module", params=[1, 2, 3], ids=["p4", "p4t", "p4w"])
+@pytest.fixture(scope="module", params=[1, 3], ids=["p4", "p4w"])
 def ax(request):
-    """Every test runs on both packed-table kernels: P4 (mma.sync exact part) and P4T
-    (tcgen05.mma exact part, TMEM accumulators)."""
+    """Every test runs on both packed-table kernels: P4 (mma.sync exact part) and P4W
+    (tcgen05.mma exact part, TMEM accumulators, warp-specialised)."""
     from paper_2203_04071_b200 import _lib
     _lib.load()
+    global VARIANT
     prev = _lib.axq_wpack_kernel(request.param)
+    VARIANT = request.param
     yield _lib
     _lib.axq_wpack_kernel(prev)
+
+
+VARIANT = 0
 
 
 def _t(a):
@@ -99,8 +104,11 @@ def test_p4_config2_full(ax):
 
 
 @pytest.mark.parametrize("M,N,K", [(1600, 512, 4608), (700, 64, 640), (6272, 256, 2304)])
-def test_p4_small_m_split_k_fused(ax, M, N, K):
-    """Small-M shapes take 512-row tiles and an exact split-K (atomics + epilogue kernel)."""
+@pytest.mark.parametrize("ws_kind", ["mn", "full"])
+def test_p4_small_m_split_k_fused(ax, M, N, K, ws_kind):
+    """Small-M shapes: with an M*N workspace an exact split-K (atomics + epilogue kernel); with
+    axq_workspace_elems (P4W) stream-K pieces in the caller's workspace.  Both bit-exact, and
+    the path taken is the one claimed."""
     T = datagen.lut_randerr(8, 0, 2)
     A = datagen.random_int8(400 + M, (M, K))
     W = datagen.random_int8(500 + N, (N, K))
@@ -116,11 +124,20 @@ def test_p4_small_m_split_k_fused(ax, M, N, K):
     bias = datagen.normal(6, 6, (N,), 0.1)
     db = _t(bias)
     y = torch.empty(M, N, device=DEV)
-    ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
+    n_ws = M * N if ws_kind == "mn" else ax.axq_workspace_elems(M, N)
+    ws = torch.zeros(n_ws, dtype=torch.int32, device=DEV)
     ep = ax.make_epilogue(dsa, dsw, bias=db, y=y, ldy=N, workspace=ws)
     ax.axq_lut_gemm_wp(dA, wp, ep)
+    kern, flags = ax.axq_last_path()
     torch.cuda.synchronize()
     np.testing.assert_array_equal(y.cpu().numpy(), oracle.dequantize(ref, sa, sw, bias))
+    assert kern == {1: "p4", 3: "p4w"}[VARIANT]
+    if VARIANT == 3 and ws_kind == "full":
+        assert flags & ax.PATH_STREAMK, "stream-K expected with a full workspace"
+    if VARIANT == 3 and ws_kind == "mn" and M * N < ax.axq_workspace_elems(M, N):
+        assert not flags & ax.PATH_STREAMK
+    # the counters region is left zero (the workspace can be reused by the next call)
+    assert int(ws[:256].abs().sum().item()) == 0
 
 
 @pytest.mark.parametrize("M,N,K", [(3000, 48, 576), (1100, 16, 2048), (600, 40, 100)])
@@ -206,7 +223,7 @@ def test_gemm_xs_activation_specialised(ax, M, N, K):
         q_ref = oracle.quantize(y_ref, s_o, 8)
         y = torch.empty(M, N, device=DEV)
         q = torch.empty(M, N, dtype=torch.int8, device=DEV)
-        ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
+        ws = torch.zeros(ax.axq_workspace_elems(M, N), dtype=torch.int32, device=DEV)
         dsa, dso, ones, dsw, db = (torch.tensor([s_a], device=DEV), torch.tensor([s_o], device=DEV),
                                    torch.ones(1, device=DEV), _t(s_w), _t(b))
         ep = ax.make_epilogue(dsa, ones, bias=db, y=y, ldy=N, workspace=ws, q_out=q, ldq=N,
@@ -235,7 +252,7 @@ def test_requantize_ties_and_boundaries(ax, s_out):
     wp = ax.WPack(lut, _t(W))
     y = torch.empty(M, N, device=DEV)
     q = torch.empty(M, N, dtype=torch.int8, device=DEV)
-    ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
+    ws = torch.zeros(ax.axq_workspace_elems(M, N), dtype=torch.int32, device=DEV)
     one = torch.ones(1, device=DEV)
     so = torch.tensor([s_out], device=DEV)
     ep = ax.make_epilogue(one, one, y=y, ldy=N, workspace=ws, q_out=q, ldq=N, d_scale_out=so, bits_out=8)
@@ -243,3 +260,36 @@ def test_requantize_ties_and_boundaries(ax, s_out):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
     np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
+
+
+def test_two_streams_concurrent(ax):
+    """Reentrancy (include/axq.h): two packed-table layers in flight on two streams, each with its
+    own workspace, both taking stream-K (every CTA writes partial slots and tile counters).  The
+    scratch lives in each caller's workspace, so the interleaved launches stay bit-exact."""
+    if VARIANT != 3:
+        pytest.skip("stream-K is a P4W decomposition")
+    T = datagen.lut_randerr(8, 0, 2)
+    cases = []
+    for i, (M, N, K) in enumerate([(1600, 512, 1024), (700, 256, 640)]):
+        A = datagen.random_int8(900 + i, (M, K))
+        W = datagen.random_int8(910 + i, (N, K))
+        cases.append((M, N, A, W, oracle.lut_gemm(A, W, T, 8)))
+    lut = ax.Lut(8, T)
+    one = torch.ones(1, device=DEV)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    run = []
+    for (M, N, A, W, ref), st in zip(cases, streams):
+        wp = ax.WPack(lut, _t(W))
+        ws = torch.zeros(ax.axq_workspace_elems(M, N), dtype=torch.int32, device=DEV)
+        ys = [torch.empty(M, N, device=DEV) for _ in range(6)]
+        run.append((wp, ws, _t(A), ys, st, ref))
+    torch.cuda.synchronize()
+    for it in range(6):                      # interleaved launches, no host sync in between
+        for wp, ws, dA, ys, st, ref in run:
+            ep = ax.make_epilogue(one, one, y=ys[it], ldy=ys[it].shape[1], workspace=ws)
+            ax.axq_lut_gemm_wp(dA, wp, ep, stream=st)
+            assert ax.axq_last_path()[1] & ax.PATH_STREAMK
+    torch.cuda.synchronize()
+    for wp, ws, dA, ys, st, ref in run:
+        for y in ys:
+            np.testing.assert_array_equal(y.cpu().numpy(), ref.astype(np.float32))

@@ -91,7 +91,7 @@ def test_gemm_per_channel_epilogue(ax, M, N, K, kernel):
     ref = oracle.dequantize_pc(oracle.lut_gemm(A, W, T, 8), s_a, s_w, b)
     lut = ax.Lut(8, T)
     y = torch.empty(M, N, device=DEV)
-    ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
+    ws = torch.zeros(ax.axq_workspace_elems(M, N), dtype=torch.int32, device=DEV)
     sa = torch.tensor([s_a], device=DEV)
     ones = torch.ones(1, device=DEV)
     db, dsw = _t(b), _t(s_w)          # the epilogue struct holds raw pointers: keep them alive

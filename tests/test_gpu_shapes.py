@@ -71,7 +71,7 @@ def test_shape_residual_epilogue(ax, M, N, K):
     wp = ax.WPack(lut, _t(W), a_nonneg=True)
     y = torch.empty(M, N, device=DEV)
     q = torch.empty(M, N, dtype=torch.int8, device=DEV)
-    ws = torch.zeros(M * N, dtype=torch.int32, device=DEV)
+    ws = torch.zeros(ax.axq_workspace_elems(M, N), dtype=torch.int32, device=DEV)
     dsa, dsw, dso = _t(np.array([sa])), _t(np.array([sw])), _t(np.array([so]))
     dr = _t(r)
     ep = ax.make_epilogue(dsa, dsw, y=y, ldy=N, workspace=ws, residual=dr, ldr=N, relu=True,
