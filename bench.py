@@ -212,6 +212,11 @@ class ResNetWL:
                                 quantizer=QUANTIZER)
         self.net.calibrate(torch.from_numpy(x_all[:8]).to(dev))   # static scales, untimed
         torch.cuda.synchronize()
+        # every rank built the tables / weights / scales from the seed; confirm
+        from paper_2203_04071_b200.shard import verify_replicas
+        self.checksum = verify_replicas(self.net.replicated_state() +
+                                        [torch.from_numpy(datagen.lut_randerr(8, 0, 2))],
+                                        _dist_or_none(world), device=dev)
         self.net.timing_hook = timer
         self.lookups_rank = self.per * self.net.lookups_per_image()
         self.lookups_total = total * self.net.lookups_per_image()
@@ -248,9 +253,8 @@ class ResNetWL:
 
 class ConvWL:
     name = "conv"
-    scaling = "weak"
+    scaling = "strong"
     pipelined_e2e = True
-    pipelined_out = True
 
     def __init__(self, dev, rank, world, timer):
         import torch
@@ -258,50 +262,74 @@ class ConvWL:
         from paper_2203_04071_b200 import Lut
         from paper_2203_04071_b200 import _lib as ax
         from paper_2203_04071_b200.layers import ApproxConv2d
+        from paper_2203_04071_b200.shard import shard_range, verify_replicas
         self.ax = ax
         c = datagen.config2()
         self.c = c
         self.lut = Lut(8, c.lut)
+        self.world, self.rank = world, rank
         # BJ configs[2]'s input is ReLU(N(0,1)): non-negative codes (half-range packed tables)
         self.layer = ApproxConv2d(torch.from_numpy(c.W).to(dev), None, self.lut, c.stride, c.pad,
                                   a_nonneg=True)
-        self.x_host = torch.from_numpy(c.x).pin_memory()
+        total = c.x.shape[0]
+        a, b = shard_range(total, world, rank)        # images per rank
+        self.total, self.per = total, b - a
+        self.x_host = torch.from_numpy(c.x[a:b]).pin_memory()
         self.x = self.x_host.to(dev)
         Nb, C, H, W = self.x.shape
         self.d = self.layer.desc(Nb, H, W)
         Ho, Wo = ax.axq_conv2d_out_hw(self.d)
         self.y = torch.empty(Nb, self.layer.Kout, Ho, Wo, device=dev)
+        self.y_all = torch.empty(total, self.layer.Kout, Ho, Wo, device=dev) if world > 1 else self.y
         self.qx = torch.empty(Nb, H, W, C, dtype=torch.int8, device=dev)
-        self.y_host = torch.empty(self.y.shape).pin_memory()
+        self.pipelined_out = world == 1
+        self.y_host = torch.empty(self.y_all.shape if rank == 0 else self.y.shape).pin_memory()
         self.timer = timer
-        self.lookups_rank = Nb * Ho * Wo * self.layer.Kout * C * 9
-        self.lookups_total = self.lookups_rank * world
+        per_img = Ho * Wo * self.layer.Kout * C * 9
+        self.lookups_rank = Nb * per_img
+        self.lookups_total = total * per_img
         self.launches = 4
-        self.in_bytes, self.out_bytes = self.x.numel() * 4, self.y.numel() * 4
+        self.in_bytes = self.x.numel() * 4
+        self.out_bytes = self.y_host.numel() * 4
+        self.checksum = verify_replicas([c.lut, self.layer.qw, self.layer.d_scale_w],
+                                        _dist_or_none(world), device=dev)
         self.desc = {"workload": "BJ configs[2]: approximate conv2d, x fp32 [128,64,56,56] "
                                  "ReLU(N(0,1)), W 64x64x3x3 Kaiming, stride 1 pad 1, int8 dynamic "
-                                 "per-tensor max calibration, randerr LUT, implicit im2col, fp32 "
-                                 "NCHW output", "batch_per_gpu": Nb}
+                                 "per-tensor max calibration (N > 1: all_reduce(MAX) of the shard "
+                                 "amax, then the same scale as one GPU), randerr LUT, implicit "
+                                 "im2col, fp32 NCHW output (N > 1: all-gathered)",
+                     "global_batch": total, "batch_per_gpu": Nb}
 
     def step(self, stream, dist):
+        from paper_2203_04071_b200.shard import all_reduce_max_, gather_rows
         ax, L = self.ax, self.layer
         ax.axq_amax(self.x, L.d_amax_a, stream)
+        all_reduce_max_(L.d_amax_a, dist)             # G > 1 == G = 1 (reading A7)
         ax.axq_scale(L.d_amax_a, 8, L.d_scale_a, stream)
         ax.axq_quantize_nchw_to_nhwc(self.x, L.d_scale_a, 8, self.qx, stream)
         self.timer("pre", stream)
         L.conv_q(self.d, self.qx, L.d_scale_a, self.y, stream=stream)
         self.timer("post", stream)
+        if self.world > 1:
+            gather_rows(self.y, self.y_all, self.total, dist)   # a8: collect the outputs
 
     def h2d(self):
         self.x.copy_(self.x_host, non_blocking=True)
 
     def d2h(self):
-        self.y_host.copy_(self.y, non_blocking=True)
+        self.y_host.copy_(self.y_all if self.rank == 0 else self.y, non_blocking=True)
+
+
+def _dist_or_none(world):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    return dist
 
 
 class LinearWL:
     name = "linear"
-    scaling = "weak"
+    scaling = "strong"
     pipelined_e2e = False   # 1 MB copies: the cross-stream waits cost more than the overlap saves
 
     def __init__(self, dev, rank, world, timer):
@@ -310,23 +338,33 @@ class LinearWL:
         from paper_2203_04071_b200 import Lut
         from paper_2203_04071_b200 import _lib as ax
         from paper_2203_04071_b200.layers import ApproxLinear
+        from paper_2203_04071_b200.shard import shard_range, verify_replicas
         self.ax = ax
         c = datagen.config1()
         self.lut = Lut(8, c.lut)
+        self.world, self.rank = world, rank
         self.layer = ApproxLinear(torch.from_numpy(c.W).to(dev), torch.from_numpy(c.b).to(dev), self.lut)
-        self.x_host = torch.from_numpy(c.x).pin_memory()
+        total = c.x.shape[0]
+        a, b = shard_range(total, world, rank)        # rows per rank
+        self.total = total
+        self.x_host = torch.from_numpy(c.x[a:b]).pin_memory()
         self.x = self.x_host.to(dev)
         M = self.x.shape[0]
         self.y = torch.empty(M, self.layer.N, device=dev)
+        self.y_all = torch.empty(total, self.layer.N, device=dev) if world > 1 else self.y
         self.bufs = self.layer.buffers(M, dev)
-        self.y_host = torch.empty(self.y.shape).pin_memory()
+        self.y_host = torch.empty(self.y_all.shape if rank == 0 else self.y.shape).pin_memory()
         self.timer = timer
         self.lookups_rank = M * self.layer.N * self.layer.K
-        self.lookups_total = self.lookups_rank * world
+        self.lookups_total = total * self.layer.N * self.layer.K
         self.launches = 3 + (3 if self.layer.use_xspec(M) else 1)   # amax, scale, quantize + LUT
-        self.in_bytes, self.out_bytes = self.x.numel() * 4, self.y.numel() * 4
+        self.in_bytes, self.out_bytes = self.x.numel() * 4, self.y_host.numel() * 4
+        self.checksum = verify_replicas([c.lut, self.layer.qw, self.layer.d_scale_w, self.layer.bias],
+                                        _dist_or_none(world), device=dev)
         self.desc = {"workload": "BJ configs[1]: approximate linear, x fp32 [256x1024] N(0,1), W "
-                                 "[1024x1024] N(0,0.02), bias N(0,0.01), trunc4 LUT, fp32 output",
+                                 "[1024x1024] N(0,0.02), bias N(0,0.01), trunc4 LUT, fp32 output "
+                                 "(N > 1: rows sharded, all_reduce(MAX) of the amax, outputs "
+                                 "all-gathered)", "global_batch": total, "batch_per_gpu": M,
                      "kernel_path": {"xspec": "activation-specialised packed tables built per "
                                               "call (axq_wpack_repack) + 512-row P4W "
                                               "(axq_lut_gemm_xs)",
@@ -334,18 +372,22 @@ class LinearWL:
                                      "gather": "per-row gather (v1)"}[self.layer.path(M)]}
 
     def step(self, stream, dist):
+        from paper_2203_04071_b200.shard import all_reduce_max_, gather_rows
         ax, L = self.ax, self.layer
         ax.axq_amax(self.x, L.d_amax_a, stream)
+        all_reduce_max_(L.d_amax_a, dist)             # G > 1 == G = 1 (reading A7)
         ax.axq_scale(L.d_amax_a, 8, L.d_scale_a, stream)
         ax.axq_quantize(self.x, L.d_scale_a, 8, self.bufs["qa"], stream)
         # LUT work = the per-call activation-table build + the packed-table GEMM (timed together)
         L.gemm_q(self.bufs["qa"], L.d_scale_a, self.y, stream, hook=self.timer)
+        if self.world > 1:
+            gather_rows(self.y, self.y_all, self.total, dist)
 
     def h2d(self):
         self.x.copy_(self.x_host, non_blocking=True)
 
     def d2h(self):
-        self.y_host.copy_(self.y, non_blocking=True)
+        self.y_host.copy_(self.y_all if self.rank == 0 else self.y, non_blocking=True)
 
 
 class LstmWL:
@@ -479,8 +521,12 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     total_ms = sum(step_ms)
+    per_rank_ms = [round(total_ms / args.steps, 4)]
     if dist:
         t = torch.tensor([total_ms], device=dev)
+        parts = [torch.zeros(1, device=dev) for _ in range(world)]
+        dist.all_gather(parts, t)
+        per_rank_ms = [round(p.item() / args.steps, 4) for p in parts]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = t.item()
 
@@ -597,6 +643,7 @@ def run_ours(args, rank, world, local_rank):
         result = {
             "metric": "approximate GMAC/s (LUT lookups/s) per B200 and % of smem-lookup roofline",
             "value": round(value, 3), "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
+            "per_rank_ms_per_step": per_rank_ms, "replica_checksum": getattr(wl, "checksum", None),
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
             "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "int8",
             "data": "synthetic (seeded; DESIGN.md input recipe), random-init weights",
@@ -748,11 +795,34 @@ def run_reference(args, rank):
                     "d2h_bytes_per_step": 0}}
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` run directly: launch the N ranks (one per GPU, NCCL) ourselves,
+        # exactly as the driver's torchrun command would
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE %d" % (args.gpus, world))
+    if world > 1:
+        # the communicator set-up lines (ranks, NVLink / NVLS transport) go to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         res = run_reference(args, rank)
         if res is not None:

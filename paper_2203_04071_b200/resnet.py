@@ -330,6 +330,15 @@ class ApproxResNet:
             self.calibrated = True
         return lg
 
+    def replicated_state(self) -> list:
+        """The state every rank must hold identically under batch sharding:
+        weight codes, static per-layer scales, per-channel weight scales, the fc bias.  Fed to
+        shard.verify_replicas together with the host ACU table."""
+        st = [self.s_act, self.s_w, self.fc_bias]
+        st += [self.qw[k] for k in sorted(self.qw)]
+        st += [self.s_w_ch[k] for k in sorted(self.s_w_ch)]
+        return st
+
     def calibrate(self, x, stream=None):
         return self.run(x, True, stream)
 

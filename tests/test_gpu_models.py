@@ -63,6 +63,22 @@ def test_resnet50_config3_full_batch_sampled():
         np.testing.assert_array_equal(y[i:i + 1], ref)
 
 
+def test_resnet50_config3_per_rank_batch_32():
+    """The per-rank batch the N = 8 bench runs (256 / 8 = 32 images, images 32-63 = rank 1's
+    shard): its layers pick different tile shapes and stream-K plans than the 256-image batch.
+    Calibration on images 0-7 as in the bench; the oracle recomputes three images."""
+    lut = datagen.lut_randerr(8, 0, 2)
+    net = _gpu_resnet(lut, 8, 3)
+    orc = models.ResNetOracle(lut, 8, config=3)
+    xc = datagen.config3_images(8)
+    x = datagen.config3_images(32, start=32)
+    net.calibrate(torch.from_numpy(xc).to(DEV))
+    scales = orc.calibrate(xc)
+    y = net.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    for i in (0, 13, 31):
+        np.testing.assert_array_equal(y[i:i + 1], orc.forward(x[i:i + 1], scales))
+
+
 @pytest.mark.parametrize("bits", [4, 6, 8])
 def test_lstm_reduced_bit_exact(bits):
     from paper_2203_04071_b200 import Lut
