@@ -239,6 +239,29 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
                              axq_lut_t lut, const axq_epilogue* ep, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * Quantize-on-load variants: the quantizer of P:74 ("real_value = A x quantized_value") fused
+ * into the operand load of the LUT-GEMM / LUT-conv, so the fp32 activations are read once and
+ * no int8 copy is written (the paper puts quantize + dequantize at ~10 % of the time).
+ * axq_lut_gemm_f32a: A fp32 [M][lda] (row m at A + m*lda) with its device scale *d_scale_a
+ *   (e.g. from axq_amax + axq_scale); every element is quantized exactly as axq_quantize does
+ *   (A1-A3: IEEE x / s, symmetric clamp to the LUT's bit width, round half to even) inside the
+ *   load, then summed as axq_lut_gemm.  ep NULL -> raw int32 C [M][ldc]; else the fused
+ *   epilogue of axq_lut_gemm_dq (ep->d_scale_a is normally the same scale pointer).
+ * axq_lut_conv2d_f32: X fp32 NCHW [N][C][H][W] (the paper's layout; d->c_valid must be
+ *   0), quantized on load with *d_scale_a; padded taps are the code 0 (A11).  Wt int8 KRSC.
+ *   ep NULL -> raw int32 Y NHWC [N][Ho][Wo][K]; else the fused epilogue (NCHW fp32 y unless
+ *   ep->y_nhwc).  groups must be 1.
+ * Results are bit-identical to axq_quantize(_nchw_to_nhwc) followed by the int8 entry point
+ * (tested).  Errors as the int8 entry points; AXQ_ERR_INVALID if d_scale_a is NULL.
+ * ------------------------------------------------------------------------------- */
+axq_status axq_lut_gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                             const float* d_scale_a, const int8_t* W, int64_t ldw, axq_lut_t lut,
+                             const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream);
+axq_status axq_lut_conv2d_f32(const axq_conv_desc* d, const float* X, const float* d_scale_a,
+                              const int8_t* Wt, axq_lut_t lut, const axq_epilogue* ep, int32_t* Y,
+                              void* stream);
+
+/* ---------------------------------------------------------------------------------
  * Prepared weights for the packed-table kernel.  For a delta8 table
  * (LUT = a*w + E with E in int8) the weights of a layer are known before inference ("learns
  * offline"), so the product row E[.][w] of every weight can be laid out once:

@@ -32,7 +32,7 @@ EXPORTED = [
     "axq_amax_rows", "axq_scale_vec", "axq_quantize_rows", "axq_calib_histogram",
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
-    "axq_last_path", "axq_workspace_elems",
+    "axq_last_path", "axq_workspace_elems", "axq_lut_gemm_f32a", "axq_lut_conv2d_f32",
 ]
 
 # axq_last_path kernel families (include/axq.h AXQ_PATH_*)
@@ -82,6 +82,10 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_version": ([], i32),
         "axq_last_path": ([ctypes.POINTER(i32)], i32),
         "axq_workspace_elems": ([i64, i64], i64),
+        "axq_lut_gemm_f32a": ([i64, i64, i64, vp, i64, vp, vp, i64, vp, ctypes.POINTER(axq_epilogue),
+                               vp, i64, vp], i32),
+        "axq_lut_conv2d_f32": ([ctypes.POINTER(axq_conv_desc), vp, vp, vp, vp,
+                                ctypes.POINTER(axq_epilogue), vp, vp], i32),
         "axq_lut_create": ([i32, vp, ctypes.POINTER(vp)], i32),
         "axq_lut_destroy": ([vp], i32),
         "axq_lut_info": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -392,6 +396,28 @@ def axq_lut_conv2d_ep(desc: axq_conv_desc, X_nhwc, W_krsc, lut: Lut, ep: axq_epi
     _check("axq_lut_conv2d_dq", load().axq_lut_conv2d_dq(ctypes.byref(desc), _ptr(X_nhwc),
                                                          _ptr(W_krsc), lut.handle,
                                                          ctypes.byref(ep), _stream(stream)))
+
+
+def axq_lut_gemm_f32a(A, d_scale_a, W, lut: Lut, ep: axq_epilogue | None = None, C=None,
+                      stream=None) -> None:
+    """Quantize-on-load LUT-GEMM: A fp32 [M][K] (row stride A.stride(0)) with its device scale,
+    W int8 [N][K]; raw int32 C [M][N] or the fused epilogue."""
+    assert A.dtype.is_floating_point and A.element_size() == 4 and A.stride(1) == 1
+    M, K = A.shape
+    N = W.shape[0]
+    _check("axq_lut_gemm_f32a", load().axq_lut_gemm_f32a(
+        M, N, K, _ptr(A), A.stride(0), _ptr(d_scale_a), _ptr(W), W.stride(0), lut.handle,
+        ctypes.byref(ep) if ep is not None else None, _ptr(C), C.stride(0) if C is not None else 0,
+        _stream(stream)))
+
+
+def axq_lut_conv2d_f32(desc: axq_conv_desc, X_nchw, d_scale_a, W_krsc, lut: Lut,
+                       ep: axq_epilogue | None = None, Y_nhwc=None, stream=None) -> None:
+    """Quantize-on-load LUT conv: X fp32 NCHW (contiguous) with its device scale."""
+    assert X_nchw.is_contiguous() and X_nchw.element_size() == 4
+    _check("axq_lut_conv2d_f32", load().axq_lut_conv2d_f32(
+        ctypes.byref(desc), _ptr(X_nchw), _ptr(d_scale_a), _ptr(W_krsc), lut.handle,
+        ctypes.byref(ep) if ep is not None else None, _ptr(Y_nhwc), _stream(stream)))
 
 
 def axq_epilogue_apply(acc, ep: axq_epilogue, stream=None) -> None:

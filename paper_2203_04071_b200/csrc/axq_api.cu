@@ -702,6 +702,77 @@ axq_status axq_lut_conv2d_dq(const axq_conv_desc* d, const int8_t* X, const int8
 }
 
 // ---------------------------------------------------------------------------------------
+// Quantize-on-load variants (SURVEY §8(b) conventions; P:74 quantizer fused into the operand
+// load, "~10% Q/DQ"): fp32 activations + their device scale, quantized by the loader of
+// the resident-table kernel with axq_quantize's pinned rule, so the result equals the unfused
+// axq_quantize -> axq_lut_gemm(_dq) / axq_lut_conv2d(_dq) chain bit for bit.
+// ---------------------------------------------------------------------------------------
+axq_status axq_lut_gemm_f32a(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                             const float* d_scale_a, const int8_t* W, int64_t ldw, axq_lut_t lut,
+                             const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream) {
+    axq_status s = gemm_common(M, N, K, reinterpret_cast<const int8_t*>(A), lda, W, ldw, lut);
+    if (s != AXQ_OK) return s;
+    if (!d_scale_a) return AXQ_ERR_INVALID;
+    if (ep) {
+        s = check_epilogue(ep, N, false);
+        if (s != AXQ_OK) return s;
+    } else if (M > 0 && N > 0 && (!C || ldc < N)) {
+        return AXQ_ERR_INVALID;
+    }
+    if (M == 0 || N == 0) return AXQ_OK;
+    if (K == 0 && !ep) {
+        cudaError_t e = cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, S(stream));
+        return e == cudaSuccess ? AXQ_OK : cuda_fail(e);
+    }
+    axq::MMArgs p{};
+    p.Af = A; p.lda = lda; p.W = W; p.ldw = ldw; p.M = M; p.N = N; p.K = K;
+    p.qscale = d_scale_a; p.qbits = lut->bits;
+    fill_common(p, lut);
+    axq_status r;
+    if (ep) {
+        axq::EpiArgs e = to_epi(ep, false, 0);
+        r = run_mm(p, axq::LOAD_GEMM_F32, lut, &e, ws_if_fits(ep, M * N), nullptr, 0, S(stream));
+    } else {
+        r = run_mm(p, axq::LOAD_GEMM_F32, lut, nullptr, nullptr, C, ldc, S(stream));
+    }
+    g_last_path = AXQ_PATH_F32A | (g_last_path & AXQ_PATH_SPLITK);
+    return r;
+}
+
+axq_status axq_lut_conv2d_f32(const axq_conv_desc* d, const float* X, const float* d_scale_a,
+                              const int8_t* Wt, axq_lut_t lut, const axq_epilogue* ep, int32_t* Y,
+                              void* stream) {
+    if (!d || !d_scale_a) return AXQ_ERR_INVALID;
+    if (d->c_valid != 0 && d->c_valid != d->C) return AXQ_ERR_UNSUPPORTED;   // no storage padding in NCHW fp32
+    axq::MMArgs p;
+    int loader;
+    axq_status s = conv_setup(d, reinterpret_cast<const int8_t*>(X), Wt, lut, p, loader);
+    if (s != AXQ_OK) return s;
+    if (ep) {
+        s = check_epilogue(ep, d->K, true);
+        if (s != AXQ_OK) return s;
+    } else if (p.M > 0 && p.N > 0 && !Y) {
+        return AXQ_ERR_INVALID;
+    }
+    if (p.M == 0 || p.N == 0) return AXQ_OK;
+    if (d->C * d->H * d->W * d->N >= ((int64_t)1 << 40)) return AXQ_ERR_UNSUPPORTED;
+    p.A = nullptr;
+    p.Af = X;
+    p.qscale = d_scale_a;
+    p.qbits = lut->bits;
+    p.pad_lookups = 0;
+    axq_status r;
+    if (ep) {
+        axq::EpiArgs e = to_epi(ep, !ep->y_nhwc, (int64_t)p.Ho * p.Wo);
+        r = run_mm(p, axq::LOAD_CONV_F32, lut, &e, ws_if_fits(ep, p.M * p.N), nullptr, 0, S(stream));
+    } else {
+        r = run_mm(p, axq::LOAD_CONV_F32, lut, nullptr, nullptr, Y, p.N, S(stream));
+    }
+    g_last_path = AXQ_PATH_F32A | (g_last_path & AXQ_PATH_SPLITK);
+    return r;
+}
+
+// ---------------------------------------------------------------------------------------
 // Prepared weights + packed-table (P4) kernel
 // ---------------------------------------------------------------------------------------
 axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K, int64_t ldw,

@@ -38,7 +38,11 @@ constexpr int KC = 16;
 
 enum { REPR_DELTA8 = 0, REPR_I16 = 1, REPR_I32 = 2 };
 enum { EPI_RAW = 0, EPI_RAW_ATOMIC = 1, EPI_FUSED = 2 };
-enum { LOAD_GEMM = 0, LOAD_CONV = 1, LOAD_GEMM_BYTES = 2, LOAD_CONV_BYTES = 3, LOAD_CONV_C4 = 4 };
+enum { LOAD_GEMM = 0, LOAD_CONV = 1, LOAD_GEMM_BYTES = 2, LOAD_CONV_BYTES = 3, LOAD_CONV_C4 = 4,
+       // quantize-on-load (SURVEY §8(b) axq_lut_gemm_f32a / axq_lut_conv2d_f32): the operand is
+       // fp32 (GEMM rows [M][lda]; conv NCHW) and each element is quantized with the pinned
+       // rule of axq_quantize (A1-A3) as it is loaded -- the codes equal the unfused chain's
+       LOAD_GEMM_F32 = 5, LOAD_CONV_F32 = 6 };
 
 struct MMArgs {
     const int8_t* A;  // GEMM: [M][lda]; conv: NHWC input X
@@ -49,6 +53,9 @@ struct MMArgs {
     // conv geometry
     int H, Wd, C, Ho, Wo, S, sh, sw, ph, pw, dh, dw;
     int cs;             // conv: NHWC pixel stride in channels (0 -> C; grouped conv: all C)
+    const float* Af;    // LOAD_GEMM_F32 / LOAD_CONV_F32: fp32 operand (A / X unused)
+    const float* qscale;  // ... its device quantization scale
+    int qbits;          // ... and bit width
     const void* table;  // device table (representation-specific layout, [uw][ua])
     int table_bytes;
     int32_t t00;        // LUT[0][0] (value of one storage-padding lookup)
@@ -88,7 +95,7 @@ __device__ __forceinline__ RowInfo make_row(const MMArgs& p, int64_t m) {
     RowInfo ri;
     ri.m = m;
     ri.valid = m < p.M;
-    if constexpr (LOADER == LOAD_GEMM || LOADER == LOAD_GEMM_BYTES) {
+    if constexpr (LOADER == LOAD_GEMM || LOADER == LOAD_GEMM_BYTES || LOADER == LOAD_GEMM_F32) {
         ri.base = m * p.lda;
         ri.hb = ri.wb = 0;
     } else {
@@ -106,11 +113,61 @@ __device__ __forceinline__ RowInfo make_row(const MMArgs& p, int64_t m) {
 
 // Load the 16 activation bytes a[m][k0 .. k0+15] (zeros beyond K or out of range rows;
 // zeros at semantic conv padding taps, which ARE looked up).
+// One element quantized as axq_quantize does (A1-A3: IEEE x / s, clamp, round half to even).
+__device__ __forceinline__ uint32_t qload_byte(float x, float s, float qm) {
+    float t = div_rn_nz(x, s);
+    t = fminf(fmaxf(t, -qm), qm);
+    return (uint32_t)(uint8_t)(int8_t)__float2int_rn(t);
+}
+
 template <int LOADER>
 __device__ __forceinline__ uint4 load_a(const MMArgs& p, const RowInfo& ri, int64_t k0,
-                                      const uint32_t* tap_s) {
+                                      const uint32_t* tap_s, float qs = 1.f, float qm = 127.f) {
     uint4 v = make_uint4(0, 0, 0, 0);
-    if constexpr (LOADER == LOAD_GEMM) {
+    if constexpr (LOADER == LOAD_GEMM_F32) {
+        if (ri.valid) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            const float* row = p.Af + ri.base + k0;
+            if (k0 + KC <= p.K && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 f = __ldg(reinterpret_cast<const float4*>(row) + j);
+                    w[j] = qload_byte(f.x, qs, qm) | (qload_byte(f.y, qs, qm) << 8) |
+                           (qload_byte(f.z, qs, qm) << 16) | (qload_byte(f.w, qs, qm) << 24);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < KC; ++j)
+                    if (k0 + j < p.K) w[j >> 2] |= qload_byte(__ldg(row + j), qs, qm) << (8 * (j & 3));
+            }
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return v;
+    } else if constexpr (LOADER == LOAD_CONV_F32) {
+        // NCHW fp32 input, k = (r, s, c) (KRSC weights); a padded tap is code 0 (A11)
+        if (ri.valid && k0 < p.K) {
+            uint32_t w[4] = {0, 0, 0, 0};
+            int rs = (int)(k0 / p.C);
+            int c = (int)(k0 - (int64_t)rs * p.C);
+            int r = rs / p.S, s_ = rs - r * p.S;
+            const int64_t hw = (int64_t)p.H * p.Wd;
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                if (k0 + j < p.K) {
+                    const int hi = ri.hb + r * p.dh, wi = ri.wb + s_ * p.dw;
+                    if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.Wd)
+                        w[j >> 2] |= qload_byte(__ldg(p.Af + ri.base + (int64_t)c * hw + (int64_t)hi * p.Wd + wi),
+                                                qs, qm) << (8 * (j & 3));
+                }
+                if (++c == p.C) {
+                    c = 0;
+                    if (++s_ == p.S) { s_ = 0; ++r; }
+                }
+            }
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        return v;
+    } else if constexpr (LOADER == LOAD_GEMM) {
         if (ri.valid && k0 + KC <= p.K) return ldg16(p.A + ri.base + k0);
         if (ri.valid) {
             uint32_t w[4] = {0, 0, 0, 0};
@@ -232,6 +289,11 @@ lut_mm_kernel(const MMArgs p) {
         }
     }
 
+    float qs = 1.f, qm = 127.f;
+    if constexpr (LOADER == LOAD_GEMM_F32 || LOADER == LOAD_CONV_F32) {
+        qs = __ldg(p.qscale);
+        qm = (float)((1 << (p.qbits - 1)) - 1);
+    }
     const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + CTN - 1) / CTN;
     const int64_t n_split = (p.K + p.k_split - 1) / p.k_split;
     const int64_t n_work = m_tiles * n_tiles * (n_split > 0 ? n_split : 1);
@@ -261,7 +323,7 @@ lut_mm_kernel(const MMArgs p) {
     uint4 w_nxt = make_uint4(0, 0, 0, 0);
     if (nchunks > 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) a_cur[r] = load_a<LOADER>(p, rows[r], kb, tap_s);
+        for (int r = 0; r < R; ++r) a_cur[r] = load_a<LOADER>(p, rows[r], kb, tap_s, qs, qm);
         if (tid < CTN) {
             uint4 wv = load_w(p, nc0 + tid, kb, wvec);
             w_s[0 * CTN + tid] = wv.x;
@@ -277,7 +339,7 @@ lut_mm_kernel(const MMArgs p) {
         const int64_t kn = kb + (int64_t)(ci + 1) * KC;
         if (has_next) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) a_nxt[r] = load_a<LOADER>(p, rows[r], kn, tap_s);
+            for (int r = 0; r < R; ++r) a_nxt[r] = load_a<LOADER>(p, rows[r], kn, tap_s, qs, qm);
             if (tid < CTN) w_nxt = load_w(p, nc0 + tid, kn, wvec);
         }
         const uint32_t* ws = w_s + (ci & 1) * (4 * CTN) + wc * TN;

@@ -55,6 +55,8 @@ int launch_loader(int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStre
         case LOAD_GEMM_BYTES: return launch_cfg<REPR, LOAD_GEMM_BYTES, EPI>(p, c, grid, st);
         case LOAD_CONV: return launch_cfg<REPR, LOAD_CONV, EPI>(p, c, grid, st);
         case LOAD_CONV_C4: return launch_cfg<REPR, LOAD_CONV_C4, EPI>(p, c, grid, st);
+        case LOAD_GEMM_F32: return launch_cfg<REPR, LOAD_GEMM_F32, EPI>(p, c, grid, st);
+        case LOAD_CONV_F32: return launch_cfg<REPR, LOAD_CONV_F32, EPI>(p, c, grid, st);
         default: return launch_cfg<REPR, LOAD_CONV_BYTES, EPI>(p, c, grid, st);
     }
 }
