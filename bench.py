@@ -38,6 +38,9 @@ SM_COUNT_NOMINAL = 148
 LANES = 32
 QUANTIZER = "max"
 DESIGN_LOOKUPS_PER_CLK = 1024.0 / 11.0   # ALU-pipe bound of the P4W inner loop
+DESIGN_BASIS = ("packed-table inner loop: 22 ALU-pipe warp instructions (PRMT, IADD3) per 1024 "
+                "lookups; ALU pipe 2 warp instructions per SM clock (B300_MICROARCH rt_SMSP = 2) "
+                "-> 93.1 lookups per SM clock (DESIGN.md 5.4)")
 
 
 def parse():
@@ -46,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="resnet", choices=["resnet", "conv", "linear", "lstm"])
+    ap.add_argument("--workload", default="resnet", choices=["resnet", "conv", "linear", "lstm", "gemm"])
     ap.add_argument("--quantizer", default="max", choices=["max", "paper"],
                     help="resnet only: 'paper' = per-channel weights + 99.9%% histogram "
                          "activations (NEXT-1, P:93-95) instead of BASELINE's per-tensor max")
@@ -54,7 +57,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
     if a.steps is None:
-        a.steps = {"resnet": 10, "lstm": 5, "conv": 50, "linear": 200}[a.workload]
+        a.steps = {"resnet": 10, "lstm": 5, "conv": 50, "linear": 200, "gemm": 200}[a.workload]
     return a
 
 
@@ -390,6 +393,51 @@ class LinearWL:
         self.y_host.copy_(self.y_all if self.rank == 0 else self.y, non_blocking=True)
 
 
+class GemmWL:
+    """BJ configs[0]: one raw LUT-GEMM (A int8 64x256, W int8 256x64, randerr LUT, int32 out).
+    Latency-sized (1 M lookups): reported in microseconds; replicas at N > 1."""
+    name = "gemm"
+    scaling = "weak"
+    pipelined_e2e = False
+
+    def __init__(self, dev, rank, world, timer):
+        import torch
+        import datagen
+        from paper_2203_04071_b200 import Lut
+        from paper_2203_04071_b200 import _lib as ax
+        self.ax = ax
+        c = datagen.config0()
+        self.lut = Lut(8, c.lut)
+        self.A_host = torch.from_numpy(c.A).pin_memory()
+        self.A = self.A_host.to(dev)
+        self.W = torch.from_numpy(c.W).to(dev)
+        self.C = torch.empty(64, 64, dtype=torch.int32, device=dev)
+        self.C_host = torch.empty(64, 64, dtype=torch.int32).pin_memory()
+        self.x, self.x_host = self.A, self.A_host
+        self.timer = timer
+        self.lookups_rank = 64 * 64 * 256
+        self.lookups_total = self.lookups_rank * world
+        self.launches = 1
+        self.in_bytes, self.out_bytes = self.A.numel(), self.C.numel() * 4
+        self.desc = {"workload": "BJ configs[0]: raw LUT-GEMM A int8 [64x256] x W int8 [256x64], "
+                                 "randerr LUT (exact product + U[-64,64]), int32 output",
+                     "global_batch": 64}
+
+    def step(self, stream, dist):
+        self.timer("pre", stream)
+        self.ax.axq_lut_gemm(self.A, self.W, self.lut, self.C, stream)
+        self.timer("post", stream)
+
+    def h2d(self):
+        self.A.copy_(self.A_host, non_blocking=True)
+
+    def d2h(self):
+        self.C_host.copy_(self.C, non_blocking=True)
+
+    def extra(self):
+        return {}
+
+
 class LstmWL:
     name = "lstm"
     scaling = "weak"
@@ -455,7 +503,118 @@ class LstmWL:
         return out
 
 
-WORKLOADS = {"resnet": ResNetWL, "conv": ConvWL, "linear": LinearWL, "lstm": LstmWL}
+WORKLOADS = {"resnet": ResNetWL, "conv": ConvWL, "linear": LinearWL, "lstm": LstmWL, "gemm": GemmWL}
+
+
+def _time_ms(fn, stream, reps=20, warm=3, flush=None):
+    """Median CUDA-event time of fn() on `stream` (L2 flushed before each rep when given)."""
+    import torch
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def imma_reference(wl, stream, flush):
+    """SURVEY §8(d) speed reference row: the EXACT int8 GEMM of the same shape on cuBLASLt IMMA
+    (torch._int_mm), labelled as such -- it computes sum a*w, not the approximate sums.  c2 uses
+    this library's im2col of the int8 codes + _int_mm (the explicit im2col GEMM of P:119)."""
+    import torch
+    from paper_2203_04071_b200 import _lib as ax
+    dev = stream.device
+    out = {"label": "exact int8 GEMM (cuBLASLt IMMA via torch._int_mm): a speed reference, NOT the "
+                    "approximate path (no lookups)"}
+    try:
+        if wl.name == "gemm":
+            A, W = wl.A, wl.W
+            Wt = W.t().contiguous()
+            ms = _time_ms(lambda: torch._int_mm(A, Wt), stream, flush=flush)
+            out.update(shape="M64 N64 K256", ms=round(ms, 5), macs=64 * 64 * 256)
+        elif wl.name == "linear":
+            q = wl.bufs["qa"]
+            Wt = wl.layer.qw.t().contiguous()
+            ms = _time_ms(lambda: torch._int_mm(q, Wt), stream, flush=flush)
+            M = q.shape[0]
+            out.update(shape="M%d N1024 K1024" % M, ms=round(ms, 5), macs=M * 1024 * 1024)
+        elif wl.name == "conv":
+            Nb, H, W_, C = wl.qx.shape
+            Ho, Wo = ax.axq_conv2d_out_hw(wl.d)
+            cols = torch.empty(Nb * Ho * Wo, 576, dtype=torch.int8, device=dev)
+            Wt = wl.layer.qw.reshape(wl.layer.Kout, -1).t().contiguous()
+            im = lambda: ax.axq_im2col_nhwc_i8(wl.qx, 0, 3, 3, (1, 1), (1, 1), cols, stream)
+            im()
+            gm = lambda: torch._int_mm(cols, Wt)
+            ms_g = _time_ms(gm, stream, flush=flush)
+            ms_i = _time_ms(im, stream, flush=flush)
+            out.update(shape="im2col [%d x 576] x [576 x 64]" % cols.shape[0], ms=round(ms_g + ms_i, 5),
+                       gemm_ms=round(ms_g, 5), im2col_ms=round(ms_i, 5), macs=cols.shape[0] * 576 * 64)
+        else:
+            return None
+        out["gmacs"] = round(out["macs"] / (out["ms"] * 1e-3) / 1e9, 2)
+    except Exception as e:      # reported, never fatal: it is a reference row only
+        out["error"] = repr(e)[:200]
+    return out
+
+
+def qdq_split(wl, stream, flush):
+    """the unfused Q | GEMM | DQ split of c1 / c2 (the analogue of P:320's ~10 %
+    quantize + dequantize share): amax + scale + quantize, the LUT kernel with raw int32
+    output, and the stand-alone dequantize, each timed alone (L2 flushed), next to the fused
+    step."""
+    import torch
+    from paper_2203_04071_b200 import _lib as ax
+    L = wl.layer
+    if wl.name == "conv":
+        Nb, H, W_, C = wl.qx.shape
+        Ho, Wo = ax.axq_conv2d_out_hw(wl.d)
+        acc = torch.empty(Nb, Ho, Wo, L.Kout, dtype=torch.int32, device=wl.x.device)
+
+        def q():
+            ax.axq_amax(wl.x, L.d_amax_a, stream)
+            ax.axq_scale(L.d_amax_a, 8, L.d_scale_a, stream)
+            ax.axq_quantize_nchw_to_nhwc(wl.x, L.d_scale_a, 8, wl.qx, stream)
+
+        def g():
+            ax.axq_lut_conv2d_wp(wl.d, wl.qx, L.wp, None, acc, stream)
+
+        def dq():
+            ax.axq_dequantize_nhwc_to_nchw(acc, L.d_scale_a, L.d_scale_w, None, wl.y, stream)
+    elif wl.name == "linear":
+        qa = wl.bufs["qa"]
+        acc = torch.empty(qa.shape[0], L.N, dtype=torch.int32, device=wl.x.device)
+
+        def q():
+            ax.axq_amax(wl.x, L.d_amax_a, stream)
+            ax.axq_scale(L.d_amax_a, 8, L.d_scale_a, stream)
+            ax.axq_quantize(wl.x, L.d_scale_a, 8, qa, stream)
+
+        def g():
+            if L.path(qa.shape[0]) == "xspec":
+                ax.axq_wpack_repack(wl.bufs["xp"], qa, stream)
+                ax.axq_lut_gemm_xs(L.qw, wl.bufs["xp"], None, acc, stream=stream)
+            else:
+                ax.axq_lut_gemm(qa, L.qw, L.lut, acc, stream)
+
+        def dq():
+            ax.axq_dequantize(acc, L.d_scale_a, L.d_scale_w, L.bias, wl.y, stream)
+    else:
+        return None
+    tq, tg, tdq = (_time_ms(f, stream, flush=flush) for f in (q, g, dq))
+    tot = tq + tg + tdq
+    return {"q_ms": round(tq, 5), "lut_gemm_ms": round(tg, 5), "dq_ms": round(tdq, 5),
+            "qdq_share": round((tq + tdq) / tot, 4),
+            "paper": "P:320: quantization + dequantization ~10 % of the time (Xeon, AVX2)",
+            "note": "unfused pieces timed alone; the bench step fuses DQ (and for ResNet layers Q) "
+                    "into the LUT kernel's epilogue"}
 
 
 def count_launches(wl, stream, dist):
@@ -630,6 +789,7 @@ def run_ours(args, rank, world, local_rank):
         clocks = clk.summary()
         f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
         roof = sm * LANES * f_max / 1e9                                  # Glookups/s
+        smem_peak = sm * 128 * f_max / 1e9                               # 1 B per lookup
         kmean = statistics.mean(kern_ms)
         achieved = wl.lookups_rank / (kmean * 1e-3) / 1e9
         value = wl.lookups_total * args.steps / (total_ms * 1e-3) / 1e9
@@ -653,36 +813,43 @@ def run_ours(args, rank, world, local_rank):
                          "per-call activation tables, lut_mm_kernel for small M, lstm_rec_kernel "
                          "for the LSTM recurrence: all LUT launches of the step, CUDA events "
                          "around each on the launching stream)",
-                         "achieved": round(achieved, 2), "peak": round(roof, 2),
-                         "unit": "Glookup/s", "frac": round(achieved / roof, 4),
-                         "peak_basis": "BASELINE metric's smem-lookup roofline: %d SMs x 32 lanes "
-                                       "x %.0f MHz (%s sm_max_mhz) = one 32-lane shared-memory "
-                                       "wavefront per SM clock, one lookup per lane; the packed-"
-                                       "table kernel serves 4 lookups per lane per load, so frac "
-                                       "can exceed 1 (DESIGN.md §5)" % (sm, f_max / 1e6, peak_src),
-                         "peak_bytes_bound": round(roof * 4, 2),
-                         "frac_bytes_bound": round(achieved / (roof * 4), 4),
-                         "bytes_bound_basis": "shared-memory bandwidth 32 banks x 4 B per SM clock "
-                                              "at 1 table byte per lookup (no design can exceed it)",
-                         "frac_at_measured_clock": round(achieved / (sm * LANES * f_meas / 1e9), 4)
+                         "achieved": round(achieved, 2), "peak": round(smem_peak, 2),
+                         "unit": "Glookup/s", "frac": round(achieved / smem_peak, 4),
+                         "peak_basis": "shared-memory byte bound: %d SMs x 128 B per SM clock "
+                                       "(32 banks x 4 B) x %.0f MHz (%s sm_max_mhz) at 1 table "
+                                       "byte per lookup (int8 E entries) -- no table-lookup "
+                                       "design can exceed it (DESIGN.md 5.4)"
+                                       % (sm, f_max / 1e6, peak_src),
+                         "frac_at_measured_clock": round(achieved / (sm * 128 * f_meas / 1e9), 4)
                          if f_meas else None,
                          "design_roofline": {
                              "bound": "alu", "peak": round(sm * f_max / 1e9 * DESIGN_LOOKUPS_PER_CLK, 2),
                              "unit": "Glookup/s",
                              "frac": round(achieved / (sm * f_max / 1e9 * DESIGN_LOOKUPS_PER_CLK), 4),
-                             "basis": "packed-table inner loop: 22 ALU-pipe warp instructions "
-                                      "(PRMT, IADD3) per 1024 lookups; ALU pipe 2 warp "
-                                      "instructions per SM clock (B300_MICROARCH rt_SMSP = 2) -> "
-                                      "93.1 lookups per SM clock (DESIGN.md 5.4)"},
+                             "basis": DESIGN_BASIS},
+                         "metric_roofline": {
+                             "peak": round(roof, 2), "unit": "Glookup/s", "frac": round(achieved / roof, 4),
+                             "basis": "BASELINE metric's smem-lookup roofline: %d SMs x 32 lanes x "
+                                      "%.0f MHz, one 32-lane wavefront per SM clock with one "
+                                      "lookup per lane; the packed tables serve 4 lookups per "
+                                      "lane per load, so this frac exceeds 1" % (sm, f_max / 1e6)},
                          "kernel_ms_per_step": round(kmean, 4),
                          "kernel_share_of_step": round(kmean / (total_ms / args.steps), 4),
-                         "traffic": committed_traffic(wl.name)},
+                         "traffic": committed_traffic(wl.name),
+                         "traffic_basis": "dram__bytes_read.sum + dram__bytes_write.sum summed "
+                                          "over the step's LUT-kernel launches, one ncu capture "
+                                          "(profiles/traffic.json); per step, like achieved"},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": (launches_step if launches_step else wl.launches) * args.steps,
+            "us_per_step": round(total_ms / args.steps * 1e3, 2) if wl.name == "gemm" else None,
             "gpu_launches_source": "CUPTI (torch.profiler) count of axq:: kernels in one untimed "
                                    "step x steps" if launches_step else "static per-step count x steps",
         }
+    if rank == 0 and world == 1 and wl.name in ("gemm", "linear", "conv"):
+        result["speed_reference_imma"] = imma_reference(wl, stream, flush)
+        if wl.name in ("linear", "conv"):
+            result["qdq_split"] = qdq_split(wl, stream, flush)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -716,6 +883,10 @@ class OracleSample:
             self.c = datagen.config1()
             self.per_unit = 256 * 1024 * 1024
             self.unit = "full layer"
+        elif workload == "gemm":
+            self.c = datagen.config0()
+            self.per_unit = 64 * 64 * 256
+            self.unit = "full GEMM"
         else:
             from oracle import models
             c = datagen.config4()
@@ -738,6 +909,9 @@ class OracleSample:
         elif self.w == "linear":
             for _ in range(n):
                 o.linear(self.c.x, self.c.W, self.c.b, self.c.lut, 8)
+        elif self.w == "gemm":
+            for _ in range(n):
+                o.lut_gemm(self.c.A, self.c.W, self.c.lut, 8)
         else:
             c = self.lstm.c
             keep = c.x
@@ -750,18 +924,30 @@ class OracleSample:
 
 
 def cpu_baseline(args, budget_s: float = 12.0):
+    """The oracle as it stands on the host cores: all threads (the reported value) and one
+    thread on the same sample, with the measured OpenMP speedup."""
     import oracle
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
     s = OracleSample(args.workload)
     t1 = s.run(1)
-    cap = {"resnet": 8, "conv": 128, "linear": 50, "lstm": 128}[args.workload]
+    cap = {"resnet": 8, "conv": 128, "linear": 50, "lstm": 128, "gemm": 2000}[args.workload]
     n = int(max(1, min(cap, budget_s / max(t1, 1e-3))))
     t = s.run(n) if n > 1 else t1
-    return {"value": round(n * s.per_unit / t / 1e9, 4), "unit": "GMAC/s",
-            "cores": oracle.max_threads(), "kind": "oracle",
+    used = oracle.max_threads()
+    # one thread on a smaller sample (about budget_s / 3 of work)
+    oracle.set_threads(1)
+    n1 = int(max(1, min(n, (budget_s / 3) / max(t1 * used, 1e-3))))
+    ts = s.run(n1)
+    oracle.set_threads(cores)
+    v_all = n * s.per_unit / t / 1e9
+    v_one = n1 * s.per_unit / ts / 1e9
+    return {"value": round(v_all, 4), "unit": "GMAC/s", "cores": used, "kind": "oracle",
             "sample": "%d %s(s) of the same workload, %.1f s (OpenMP parallel-for over the "
-                      "outermost loop, all host cores)" % (n, s.unit, t)}
+                      "outermost loop, all host cores)" % (n, s.unit, t),
+            "single_thread": {"value": round(v_one, 4), "unit": "GMAC/s", "cores": 1,
+                              "sample": "%d %s(s), %.1f s" % (n1, s.unit, ts)},
+            "omp_speedup": round(v_all / v_one, 2)}
 
 
 def run_reference(args, rank):
@@ -777,8 +963,9 @@ def run_reference(args, rank):
     tot = sum(ts)
     value = s.per_unit * args.steps / tot / 1e9
     base = {"resnet": ("BJ configs[3] ResNet-50-shaped approximate forward", "strong"),
-            "conv": ("BJ configs[2] approximate conv2d", "weak"),
-            "linear": ("BJ configs[1] approximate linear", "weak"),
+            "conv": ("BJ configs[2] approximate conv2d", "strong"),
+            "linear": ("BJ configs[1] approximate linear", "strong"),
+            "gemm": ("BJ configs[0] raw LUT-GEMM", "weak"),
             "lstm": ("BJ configs[4] LSTM, b=8", "weak")}[args.workload]
     sample = "1 %s per step (a bounded sample of the same workload)" % s.unit
     return {"metric": "approximate GMAC/s (LUT lookups/s) per B200 and % of smem-lookup roofline",
