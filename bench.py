@@ -597,12 +597,8 @@ def qdq_split(wl, stream, flush):
             ax.axq_scale(L.d_amax_a, 8, L.d_scale_a, stream)
             ax.axq_quantize(wl.x, L.d_scale_a, 8, qa, stream)
 
-        def g():
-            if L.path(qa.shape[0]) == "xspec":
-                ax.axq_wpack_repack(wl.bufs["xp"], qa, stream)
-                ax.axq_lut_gemm_xs(L.qw, wl.bufs["xp"], None, acc, stream=stream)
-            else:
-                ax.axq_lut_gemm(qa, L.qw, L.lut, acc, stream)
+        def g():   # raw int32 output: the per-row-gather kernel with its exact split-K
+            ax.axq_lut_gemm(qa, L.qw, L.lut, acc, stream)
 
         def dq():
             ax.axq_dequantize(acc, L.d_scale_a, L.d_scale_w, L.bias, wl.y, stream)

@@ -30,6 +30,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "async_copy.cuh"
 #include "epilogue.cuh"
 
 namespace axq {
@@ -271,10 +272,17 @@ lut_mm_kernel(const MMArgs p) {
     const bool wvec = ((p.ldw & 15) == 0) && ((reinterpret_cast<uintptr_t>(p.W) & 15) == 0);
 
     // ---- stage the ACU table in shared memory (once per CTA: the kernel is persistent) ----
+    // one bulk copy (TMA, mbarrier complete_tx): the whole 64 / 128 KiB in flight at once, so a
+    // small problem (BJ configs[0]) pays one memory latency for it, not one per 16-byte round
+    __shared__ __align__(8) uint64_t tbl_bar;
     if constexpr (REPR != REPR_I32) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.table);
-        uint4* dst = reinterpret_cast<uint4*>(lut_s);
-        for (int i = tid; i < tbytes / 16; i += NT) dst[i] = __ldg(src + i);
+        const uint32_t bar = smem_u32(&tbl_bar);
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            mbar_expect_tx(bar, (uint32_t)tbytes);
+            bulk_g2s(smem_u32(lut_s), p.table, (uint32_t)tbytes, bar);
+        }
     }
     if constexpr (LOADER == LOAD_CONV_C4) {
         // entry g (k = 4g .. 4g+3): r*dh | s*dw << 8 | c << 16, padded with zeros
@@ -293,6 +301,10 @@ lut_mm_kernel(const MMArgs p) {
     if constexpr (LOADER == LOAD_GEMM_F32 || LOADER == LOAD_CONV_F32) {
         qs = __ldg(p.qscale);
         qm = (float)((1 << (p.qbits - 1)) - 1);
+    }
+    if constexpr (REPR != REPR_I32) {
+        __syncthreads();                       // barrier initialised before anyone waits on it
+        mbar_wait(smem_u32(&tbl_bar), 0u);
     }
     const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + CTN - 1) / CTN;
     const int64_t n_split = (p.K + p.k_split - 1) / p.k_split;

@@ -9,8 +9,8 @@
 //    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
 //    the consumer warps released it (empty barrier) and the MMA that read it completed.
 //  * 28 consumer warps (896 rows, one per lane) only wait for full buffers, do the lookups
-//    (4 per 32-bit LDS; the adds split between the ALU pipe -- two k per 3-input add -- and
-//    the FMA pipe -- multiply-add by an opaque 1) and release the buffer; consumer warp
+//    (4 per 32-bit LDS, accumulated as even-byte lanes on the ALU pipe and shifted words on
+//    the FMA pipe, decoded exactly at each flush) and release the buffer; consumer warp
 //    0's lane 0 also issues the exact-part MMAs (7 slices of 128 rows, M = 128, N = 16, K = 32)
 //    into one of two TMEM accumulator sets, so the next tile's MMAs never wait for this
 //    tile's epilogue reads.  No CTA-wide barrier in the steady state.
@@ -330,7 +330,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
         EpiConst& kconst = *reinterpret_cast<EpiConst*>(smem + G::SMEM_KC);
         if (tid == 0) kconst = p4t_epi_const(P);
         consumer_sync<BM>();
-        const uint32_t one = P.one;   // = 1, opaque to the compiler (keeps those adds on the FMA pipe)
+        // 2^24, opaque to the compiler: mad.hi(v, 2^24, acc) = acc + (v >> 8) stays one IMAD.HI
+        // on the FMA pipe instead of becoming a shift + add on the ALU pipe
+        const uint32_t sh24 = P.one << 24;
         Gen g;
         gen_init(g);
         int64_t tile;
@@ -342,9 +344,15 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             const int64_t n0 = nb * TN;
             const uint32_t tb = tcount & 1u;
             const bool wlive = m0 + warp * 32 < p.M;
-            uint32_t pacc[4][2];
+            // Per quad q the packed word v holds the biased bytes b_j = E + 128 of columns 4q+j.
+            // Two accumulators recover the four per-column sums S_j exactly:
+            //   pa[q] = sum (v & 0x00ff00ff) = S0 + 2^16 S2      (LOP3 + 3-input IADD3, ALU pipe)
+            //   po[q] = sum (v >> 8)         = S1 + 2^8 S2 + 2^16 S3   (one IMAD.HI, FMA pipe)
+            // With at most 256 words between flushes every S_j <= 255 * 256 < 2^16, so
+            // S0 = pa & 0xffff, S2 = pa >> 16, and po - 2^8 S2 = S1 + 2^16 S3 (mod 2^32).
+            uint32_t pa[4], po[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) pacc[q][0] = pacc[q][1] = 0u;
+            for (int q = 0; q < 4; ++q) pa[q] = po[q] = 0u;
             bool e_first = true;
             for (int st = s_b; st < s_e; ++st, ++item) {
                 const int buf = (int)(item % STAGES);
@@ -380,17 +388,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                             for (int q = 0; q < 4; ++q) {
                                 const uint32_t v0 = *reinterpret_cast<const uint32_t*>(r0 + q * TQ);
                                 const uint32_t v1 = *reinterpret_cast<const uint32_t*>(r1 + q * TQ);
-                                const uint32_t e0 = __byte_perm(v0, 0u, 0x4240u), e1 = __byte_perm(v1, 0u, 0x4240u);
-                                const uint32_t o0 = __byte_perm(v0, 0u, 0x4341u), o1 = __byte_perm(v1, 0u, 0x4341u);
-                                if (q < 2) {     // ALU pipe: one 3-input add per accumulator
-                                    pacc[q][0] += e0 + e1;
-                                    pacc[q][1] += o0 + o1;
-                                } else {         // FMA pipe: multiply-adds by an opaque 1
-                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e0), "r"(one));
-                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e1), "r"(one));
-                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o0), "r"(one));
-                                    asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o1), "r"(one));
-                                }
+                                pa[q] += (v0 & 0x00ff00ffu) + (v1 & 0x00ff00ffu);
+                                asm("mad.hi.u32 %0, %1, %2, %0;\n" : "+r"(po[q]) : "r"(v0), "r"(sh24));
+                                asm("mad.hi.u32 %0, %1, %2, %0;\n" : "+r"(po[q]) : "r"(v1), "r"(sh24));
                             }
                         }
                     }
@@ -408,11 +408,12 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        ev[4 * q + 0] += pacc[q][0] & 0xffffu;
-                        ev[4 * q + 2] += pacc[q][0] >> 16;
-                        ev[4 * q + 1] += pacc[q][1] & 0xffffu;
-                        ev[4 * q + 3] += pacc[q][1] >> 16;
-                        pacc[q][0] = pacc[q][1] = 0u;
+                        const uint32_t s2 = pa[q] >> 16, t = po[q] - (s2 << 8);
+                        ev[4 * q + 0] += pa[q] & 0xffffu;
+                        ev[4 * q + 1] += t & 0xffffu;
+                        ev[4 * q + 2] += s2;
+                        ev[4 * q + 3] += t >> 16;
+                        pa[q] = po[q] = 0u;
                     }
                     tmem_st16(t_e, ev);
                     tmem_wait_st();
