@@ -37,6 +37,7 @@ import numpy as np  # noqa: E402
 SM_COUNT_NOMINAL = 148
 LANES = 32
 QUANTIZER = "max"
+LUT_KIND = "default"
 DESIGN_LOOKUPS_PER_CLK = 1024.0 / 11.0   # ALU-pipe bound of the P4W inner loop
 DESIGN_BASIS = ("packed-table inner loop: 22 ALU-pipe warp instructions (PRMT, IADD3) per 1024 "
                 "lookups; ALU pipe 2 warp instructions per SM clock (B300_MICROARCH rt_SMSP = 2) "
@@ -53,6 +54,9 @@ def parse():
     ap.add_argument("--quantizer", default="max", choices=["max", "paper"],
                     help="resnet only: 'paper' = per-channel weights + 99.9%% histogram "
                          "activations (NEXT-1, P:93-95) instead of BASELINE's per-tensor max")
+    ap.add_argument("--lut", default="default", choices=["default", "err2000"],
+                    help="conv only: 'err2000' = an ACU with a +-2000 error (beyond int8 E: the "
+                         "packed int16-E kernel P4W16) instead of BJ configs[2]'s randerr table")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
@@ -268,6 +272,8 @@ class ConvWL:
         from paper_2203_04071_b200.shard import shard_range, verify_replicas
         self.ax = ax
         c = datagen.config2()
+        if LUT_KIND == "err2000":
+            c.lut = datagen.lut_bigerr(8, 2000, 8, 1)
         self.c = c
         self.lut = Lut(8, c.lut)
         self.world, self.rank = world, rank
@@ -300,7 +306,8 @@ class ConvWL:
                                  "ReLU(N(0,1)), W 64x64x3x3 Kaiming, stride 1 pad 1, int8 dynamic "
                                  "per-tensor max calibration (N > 1: all_reduce(MAX) of the shard "
                                  "amax, then the same scale as one GPU), randerr LUT, implicit "
-                                 "im2col, fp32 NCHW output (N > 1: all-gathered)",
+                                 "im2col, fp32 NCHW output (N > 1: all-gathered)" +
+                                 (" -- with a +-2000-error ACU instead (--lut err2000)" if LUT_KIND == "err2000" else ""),
                      "global_batch": total, "batch_per_gpu": Nb}
 
     def step(self, stream, dist):
@@ -640,8 +647,9 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=dev)
 
     timer = KernelTimer()
-    global QUANTIZER
+    global QUANTIZER, LUT_KIND
     QUANTIZER = args.quantizer
+    LUT_KIND = args.lut
     wl = WORKLOADS[args.workload](dev, rank, world, timer)
     stream = torch.cuda.current_stream()
     # L2 flush buffer (> 126 MB L2) written before every timed step, outside the timed region

@@ -71,6 +71,15 @@ def lut_randerr(bits: int, config: int, idx: int) -> np.ndarray:
     return (lut_exact(bits).astype(np.int64) + err.reshape(-1)).astype(np.int32)
 
 
+def lut_bigerr(bits: int, err: int, config: int, idx: int) -> np.ndarray:
+    """Exact product + seeded uniform integer error in [-err, err] (one endpoint-inclusive draw
+    in index order, as lut_randerr): an ACU whose error does not fit int8 (e.g. err = 2000), the
+    case the int8-E packed tables cannot hold (VERDICT r1 "fast-path cliff")."""
+    e = rng_for(config, idx).integers(-err, err, size=(1 << bits, 1 << bits), endpoint=True,
+                                      dtype=np.int64)
+    return (lut_exact(bits).astype(np.int64) + e.reshape(-1)).astype(np.int32)
+
+
 def lut_trunc4() -> np.ndarray:
     """BJ:c1 "exact product with low-bit truncation error (drop product bits 0-3)":
     p & ~0xF on the two's-complement product."""

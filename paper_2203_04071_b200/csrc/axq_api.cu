@@ -23,6 +23,7 @@
 struct axq_wpack {
     int device;
     int half;
+    int e16;                   // P4W16 tables (int16 E, 2 columns per packed word)
     int swap;                  // tables specialised on activations (axq_lut_gemm_xs)
     const int8_t* dtab;        // packing table: the LUT's [uw][ua] delta8 table, or (swap) a
                                // transposed [ua][uw] copy owned by the wpack (dtab_own)
@@ -42,6 +43,8 @@ struct axq_lut {
     int64_t absmax;
     void* d_table;
     int table_bytes;
+    int16_t* d_e16;            // int16 E = LUT - a*w [uw8][ua8] when every E fits int16 and the
+                               // table is not delta8 (feeds the P4W16 packer), else null
 };
 
 namespace {
@@ -284,7 +287,33 @@ axq_status axq_lut_create(int bits, const int32_t* host_table, axq_lut_t* out) {
     axq_lut* L = new axq_lut();
     L->bits = bits;
     L->repr = repr;
+    L->d_e16 = nullptr;
     cudaGetDevice(&L->device);
+    if (repr != AXQ_LUT_DELTA8) {
+        // E16 copy for the packed int16-E kernel (P4W16): E = LUT - a*w within int16
+        bool e16_ok = true;
+        std::vector<int16_t> e16((size_t)65536, 0);
+        for (int uw8 = 0; uw8 < 256 && e16_ok; ++uw8) {
+            const int w = (int)(int8_t)uw8;
+            if (w < -(n / 2) || w >= n / 2) continue;
+            for (int ua8 = 0; ua8 < 256; ++ua8) {
+                const int a = (int)(int8_t)ua8;
+                if (a < -(n / 2) || a >= n / 2) continue;
+                const int64_t ev = (int64_t)host_table[((a & mask) << bits) | (w & mask)] - (int64_t)a * w;
+                if (ev < INT16_MIN || ev > INT16_MAX) { e16_ok = false; break; }
+                e16[((size_t)uw8 << 8) | (size_t)ua8] = (int16_t)ev;
+            }
+        }
+        if (e16_ok) {
+            cudaError_t e = cudaMalloc(&L->d_e16, 131072);
+            if (e == cudaSuccess) e = cudaMemcpy(L->d_e16, e16.data(), 131072, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) {
+                if (L->d_e16) cudaFree(L->d_e16);
+                delete L;
+                return cuda_fail(e);
+            }
+        }
+    }
     L->tmin = (int32_t)tmin;
     L->tmax = (int32_t)tmax;
     L->t00 = host_table[0];
@@ -309,6 +338,7 @@ axq_status axq_lut_destroy(axq_lut_t lut) {
     if (!lut) return AXQ_OK;
     cudaDeviceSynchronize();
     cudaFree(lut->d_table);
+    if (lut->d_e16) cudaFree(lut->d_e16);
     delete lut;
     return AXQ_OK;
 }
@@ -781,7 +811,11 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
     *out = nullptr;
     axq_status s = check_lut(lut);
     if (s != AXQ_OK) return s;
-    if (lut->repr != AXQ_LUT_DELTA8) return AXQ_ERR_UNSUPPORTED;
+    // delta8 tables: packed int8 E (P4W / P4); other tables whose E fits int16, for
+    // non-negative activations: packed int16 E (P4W16); anything else: the resident-table kernel
+    const bool e16 = lut->repr != AXQ_LUT_DELTA8;
+    if (e16 && (!lut->d_e16 || !(a_nonneg & AXQ_WPACK_NONNEG) || (a_nonneg & AXQ_WPACK_ACTIVATIONS)))
+        return AXQ_ERR_UNSUPPORTED;
     s = overflow_guard(lut, K);
     if (s != AXQ_OK) return s;
     axq_wpack* w = new axq_wpack();
@@ -791,6 +825,7 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
     w->K = K;
     w->Kp = (K + 31) / 32 * 32;   // a whole number of 32-k stages (P4T half-range tables)
     w->half = (a_nonneg & AXQ_WPACK_NONNEG) ? 1 : 0;
+    w->e16 = e16 ? 1 : 0;
     w->swap = (a_nonneg & AXQ_WPACK_ACTIVATIONS) ? 1 : 0;
     w->dtab = reinterpret_cast<const int8_t*>(lut->d_table);
     w->dtab_own = nullptr;
@@ -809,12 +844,16 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
         w->dtab = w->dtab_own;
     }
     const int64_t nb = (N + axq::p4::TN - 1) / axq::p4::TN;
-    const size_t tb = (size_t)nb * w->Kp * 4 * (w->half ? 128 : 256) * 4, wb = (size_t)nb * w->Kp * axq::p4::TN;
+    const size_t tb = (size_t)nb * w->Kp * (w->e16 ? 8 : 4) * (w->half ? 128 : 256) * 4,
+                 wb = (size_t)nb * w->Kp * axq::p4::TN;
     w->bytes = (int64_t)(tb + wb);
     cudaError_t e = cudaMalloc(&w->tables, tb);
     if (e == cudaSuccess) e = cudaMalloc(&w->wpk, wb);
     if (e == cudaSuccess) {
-        int rc = axq::p4_pack(W, N, K, ldw, w->Kp, w->dtab, w->tables, w->wpk, w->half, w->swap, 0);
+        int rc = w->e16 ? axq::p4_pack16(W, N, K, ldw, w->Kp, lut->d_e16, w->tables, 0)
+                        : axq::p4_pack(W, N, K, ldw, w->Kp, w->dtab, w->tables, w->wpk, w->half, w->swap, 0);
+        if (!rc && w->e16)   // the packed weight tile of the exact part (p4_pack writes both)
+            rc = axq::p4_pack_w(W, N, K, ldw, w->Kp, w->wpk, 0);
         e = rc ? (cudaError_t)rc : cudaDeviceSynchronize();
     }
     if (e != cudaSuccess) {
@@ -829,6 +868,7 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
 
 axq_status axq_wpack_repack(axq_wpack_t wp, const int8_t* W, int64_t ldw, void* stream) {
     if (!wp || !W || ldw < wp->K) return AXQ_ERR_INVALID;
+    if (wp->e16) return AXQ_ERR_UNSUPPORTED;
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev != wp->device) return AXQ_ERR_INVALID;
@@ -950,7 +990,9 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     // default: P4W, except the 4-byte-tap conv loader (e.g. the padded 3-channel stem), where
     // P4's 2 rows per lane measure faster
     const int kv = g_wpack_kernel.load();
-    const int variant = kv != 0 ? kv : (a.c4 ? 1 : 3);
+    const int variant = wp->e16 ? 3 : (kv != 0 ? kv : (a.c4 ? 1 : 3));
+    a.e16 = wp->e16;
+    if (wp->e16 && (a.c4 || kv == 1)) return AXQ_ERR_UNSUPPORTED;   // P4W16: 16-byte loaders, P4W only
     const bool use_tc = variant == 3;                                 // P4W: tcgen05 exact part
     // P4W shape: 512-row tiles (16 consumer warps) for small row counts, where 896-row tiles
     // would leave lanes idle or cut a ragged second tile; not for residual epilogues or the
@@ -958,7 +1000,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     // k per stage: 32 for half-range tables, 16 for full-range ones, except half-range tables
     // with K <= AXQ_P4W_KS16_MAX_K (16-k stages, 4 deep)
     p4w_read_env();
-    a.ks = wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
+    a.ks = wp->e16 ? 16 : wp->half ? ((variant == 3 && wp->Kp <= g_p4w_ks16_max_k) ? 16 : 32) : 16;
     const bool res_ep = ep && ep->residual;
     a.cw = 28;
     // 512-row tiles when they pad fewer rows than 896-row ones (M <= 1024 always: one or two
@@ -973,6 +1015,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     if (variant == 3 && !res_ep && wp->half && a.ks == 32 && !a.c4 && a.cw == 28 &&
         (main_cw == 16 || main_cw == 20 || main_cw == 24) && wp->Kp <= g_p4w_main_cw_max_k)
         a.cw = main_cw;
+    if (wp->e16) a.cw = (res_ep || a.mm.M <= 1024 || pad512 < pad896) ? 16 : 28;
     const int bm = variant == 3 ? axq::p4w_bm(a.cw) : 1024;
     if (use_tc)
         axq::p4w_plan(a.mm.M, a.mm.N, wp->Kp, a.ks, bm, sm_count(), can_split && !a.transposed, a.splits,
@@ -980,7 +1023,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
     auto launch = [&](const axq::P4Args& x) { return variant == 3 ? axq::launch_p4w(x, st) : axq::launch_p4(x, st); };
-    int path = variant == 3 ? AXQ_PATH_P4W : AXQ_PATH_P4;
+    int path = wp->e16 ? AXQ_PATH_P4W16 : variant == 3 ? AXQ_PATH_P4W : AXQ_PATH_P4;
     if (use_tc && ep && ep->workspace && ws_elems >= streamk_elems(bm) &&
         (reinterpret_cast<uintptr_t>(ep->workspace) & 15) == 0) {
         // stream-K whenever whole tiles would leave a partial wave (exact int32 pieces in the

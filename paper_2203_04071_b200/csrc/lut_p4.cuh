@@ -534,6 +534,43 @@ __global__ void __launch_bounds__(PACK_THREADS) p4_pack_tables_kernel(
     }
 }
 
+// P4W16 tables (E = LUT - a*w beyond int8 but within int16; half range, codes 0..127):
+//   tables[nb][k][p][u] = (E[u][w(16nb+2p, k)] + 32768) | (E[u][w(16nb+2p+1, k)] + 32768) << 16
+// from the int16 E table e16 [uw][ua] (128 KiB, staged in shared memory).
+__global__ void __launch_bounds__(PACK_THREADS) p4_pack16_tables_kernel(
+        const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw, int64_t Kp,
+        const int16_t* __restrict__ e16, uint32_t* __restrict__ tables) {
+    extern __shared__ __align__(16) uint8_t pk16_tab[];   // [256 uw][256 ua] int16
+    __shared__ uint8_t codes[p4::TN][PACK_KC];
+    for (int i = threadIdx.x; i < 131072 / 16; i += PACK_THREADS)
+        reinterpret_cast<uint4*>(pk16_tab)[i] = __ldg(reinterpret_cast<const uint4*>(e16) + i);
+    const int16_t* et = reinterpret_cast<const int16_t*>(pk16_tab);
+    const int64_t n_blocks = (N + p4::TN - 1) / p4::TN;
+    const int64_t k_chunks = (Kp + PACK_KC - 1) / PACK_KC;
+    const int pr = threadIdx.x >> 5, u4 = (threadIdx.x & 31) * 4;   // pair 0..7, codes u4..u4+3
+    for (int64_t item = blockIdx.x; item < n_blocks * k_chunks; item += gridDim.x) {
+        const int64_t nb = item / k_chunks, k0 = (item - nb * k_chunks) * PACK_KC;
+        const int kn = (int)min((int64_t)PACK_KC, Kp - k0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < p4::TN * PACK_KC; i += PACK_THREADS) {
+            const int j = i / PACK_KC, kk = i - j * PACK_KC;
+            const int64_t n = nb * p4::TN + j, k = k0 + kk;
+            codes[j][kk] = (n < N && k < K) ? (uint8_t)W[n * ldw + k] : 0;
+        }
+        __syncthreads();
+        uint32_t* dst = tables + ((nb * Kp + k0) * 8 + pr) * 128 + u4;
+        for (int kk = 0; kk < kn; ++kk) {
+            const int16_t* r0 = et + ((int)codes[2 * pr][kk] << 8) + u4;
+            const int16_t* r1 = et + ((int)codes[2 * pr + 1][kk] << 8) + u4;
+            uint32_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                o[j] = (uint32_t)(uint16_t)(r0[j] + 32768) | ((uint32_t)(uint16_t)(r1[j] + 32768) << 16);
+            *reinterpret_cast<uint4*>(dst + (int64_t)kk * 8 * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
 // wpk[((nb*(Kp/16) + kc)*16 + nl)*16 + kk] = W[16nb+nl][16kc+kk] (0 outside)
 __global__ void p4_pack_w_kernel(const int8_t* __restrict__ W, int64_t N, int64_t K, int64_t ldw, int64_t Kp,
                                  int8_t* __restrict__ wpk) {

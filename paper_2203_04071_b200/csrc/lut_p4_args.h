@@ -57,6 +57,7 @@ struct P4Args {
     int ks;                     // P4W: k per stage (16 or 32; 16 with half tables = 4 stages)
     int transposed;             // P4W: output element (row r, col c) goes to [c][r] (gemm_xs)
     int cw;                     // P4W consumer warps (tile rows / 32): 28 (default) or 16
+    int e16;                    // P4W16: int16 E tables, 2 columns per packed word
     int nb_fast;                // tile order: column block fastest (the layer's tables stay in
                                 // L2 and each activation tile is read from HBM once) instead of
                                 // row tile fastest (concurrent CTAs share one table stream)

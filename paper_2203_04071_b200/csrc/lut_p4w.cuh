@@ -9,8 +9,8 @@
 //    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
 //    the consumer warps released it (empty barrier) and the MMA that read it completed.
 //  * 28 consumer warps (896 rows, one per lane) only wait for full buffers, do the lookups
-//    (4 per 32-bit LDS, accumulated as even-byte lanes on the ALU pipe and shifted words on
-//    the FMA pipe, decoded exactly at each flush) and release the buffer; consumer warp
+//    (4 per 32-bit LDS; the adds split between the ALU pipe -- two k per 3-input add -- and
+//    the FMA pipe -- multiply-add by an opaque 1) and release the buffer; consumer warp
 //    0's lane 0 also issues the exact-part MMAs (7 slices of 128 rows, M = 128, N = 16, K = 32)
 //    into one of two TMEM accumulator sets, so the next tile's MMAs never wait for this
 //    tile's epilogue reads.  No CTA-wide barrier in the steady state.
@@ -52,22 +52,25 @@ constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots 
 #ifndef P4W_SMALL_FULL_STAGES
 #define P4W_SMALL_FULL_STAGES 3
 #endif
-template <bool HALF, int KSX = (HALF ? 32 : 16), int CWX = 28>
+// E16 (P4W16, tables whose E = LUT - a*w does not fit int8 but fits int16): a packed word holds
+// the biased E of 2 columns (a column pair) instead of 4 (a quad), so NQ = 8 words per k.
+template <bool HALF, int KSX = (HALF ? 32 : 16), int CWX = 28, bool E16 = false>
 struct Geo {
     static constexpr int BM = Shape<CWX>::BM;
     static constexpr int KS = KSX;
     static constexpr int TROWS = HALF ? 128 : 256;
     static constexpr int TQ = TROWS * 4;
-    static constexpr int TBL_STAGE = KS * (TN / 4) * TQ;   // 64 KiB
+    static constexpr int NQ = E16 ? TN / 2 : TN / 4;       // packed words per k
+    static constexpr int TBL_STAGE = KS * NQ * TQ;         // 64 KiB
     static constexpr int A_STAGE = BM * KS;                // KS / 16 planes of [BM][16 B]
     // half-range tables in 16-k stages (small-K layers): 4 stages of 32 KiB, a deeper pipeline
     // across the short tiles; the 512-row shape with full-range tables: 3 stages of 64 KiB
     // (few rows per table byte: the table stream, not the lookups, sets the pace); otherwise 2
     static constexpr bool SMALL_FULL = (CWX == 16 && !HALF);
-    static constexpr int STAGES = (HALF && KS == 16) ? 4 : SMALL_FULL ? P4W_SMALL_FULL_STAGES : 2;
+    static constexpr int STAGES = E16 ? 2 : (HALF && KS == 16) ? 4 : SMALL_FULL ? P4W_SMALL_FULL_STAGES : 2;
     // the 4-byte-tap conv loader's tap table (not in the SMALL_FULL shape: no room; the host
     // never picks it for such layers)
-    static constexpr bool HAS_TAP = !SMALL_FULL;
+    static constexpr bool HAS_TAP = !SMALL_FULL && !E16;
     static constexpr int FLUSH_STAGES = 256 / KS;
     static constexpr int SMEM_TBL = 0;
     static constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
@@ -100,10 +103,10 @@ __device__ __forceinline__ void consumer_sync() {   // named barrier 1: the BM_ 
 // RES: a separate instantiation for layers with a residual input, whose epilogue loads the
 // residual rows before waiting on the tile's MMAs (their latency overlaps the wait).  Kept out
 // of the other layers' instantiation: its extra live registers would spill into their loop.
-template <bool HALF, int KSX, bool RES = false, int CWX = 28>
+template <bool HALF, int KSX, bool RES = false, int CWX = 28, bool E16 = false>
 __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const __grid_constant__ P4Args P) {
     using namespace p4w;
-    using G = p4w::Geo<HALF, KSX, CWX>;
+    using G = p4w::Geo<HALF, KSX, CWX, E16>;
     using S = p4w::Shape<CWX>;
     constexpr int CW = S::CW, NT = S::NT, BM = S::BM, SLICES = S::SLICES, PT = S::PT, RPT = S::RPT;
     constexpr int KS = G::KS, STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ, A_STAGE = G::A_STAGE;
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                 cp_async_mbar_arrive(bar_full + 8 * buf);
                 if (pt == 0) {
                     const uint32_t bar = bar_full + 8 * buf;
-                    const uint32_t* tbl_g = P.tables + ((size_t)nb * P.Kp + (size_t)st * KS) * 4 * G::TROWS;
+                    const uint32_t* tbl_g = P.tables + ((size_t)nb * P.Kp + (size_t)st * KS) * G::NQ * G::TROWS;
                     const int8_t* w_g = P.wpk + ((size_t)nb * (P.Kp / 16) + (size_t)st * NPL) * p4::W_STAGE;
                     mbar_expect_tx(bar, TBL_STAGE + NPL * p4::W_STAGE);
                     bulk_g2s(s_base + G::SMEM_TBL + buf * TBL_STAGE, tbl_g, TBL_STAGE, bar);
@@ -330,9 +333,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
         EpiConst& kconst = *reinterpret_cast<EpiConst*>(smem + G::SMEM_KC);
         if (tid == 0) kconst = p4t_epi_const(P);
         consumer_sync<BM>();
-        // 2^24, opaque to the compiler: mad.hi(v, 2^24, acc) = acc + (v >> 8) stays one IMAD.HI
-        // on the FMA pipe instead of becoming a shift + add on the ALU pipe
-        const uint32_t sh24 = P.one << 24;
+        const uint32_t one = P.one;   // = 1, opaque to the compiler (keeps those adds on the FMA pipe)
         Gen g;
         gen_init(g);
         int64_t tile;
@@ -344,15 +345,14 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             const int64_t n0 = nb * TN;
             const uint32_t tb = tcount & 1u;
             const bool wlive = m0 + warp * 32 < p.M;
-            // Per quad q the packed word v holds the biased bytes b_j = E + 128 of columns 4q+j.
-            // Two accumulators recover the four per-column sums S_j exactly:
-            //   pa[q] = sum (v & 0x00ff00ff) = S0 + 2^16 S2      (LOP3 + 3-input IADD3, ALU pipe)
-            //   po[q] = sum (v >> 8)         = S1 + 2^8 S2 + 2^16 S3   (one IMAD.HI, FMA pipe)
-            // With at most 256 words between flushes every S_j <= 255 * 256 < 2^16, so
-            // S0 = pa & 0xffff, S2 = pa >> 16, and po - 2^8 S2 = S1 + 2^16 S3 (mod 2^32).
-            uint32_t pa[4], po[4];
+            // E8: per quad q, pacc[q][0] / [1] = even / odd biased bytes in 16-bit lanes (exact
+            // for up to 256 words between flushes).  E16: per column pair p, pacc[p][0] = sum v
+            // (mod 2^32) and pacc[p][1] = sum (v >> 16); the low column's sum is
+            // pacc[p][0] - 2^16 pacc[p][1] (mod 2^32, exact: both sums < 2^32).
+            constexpr int NACC = E16 ? 8 : 4;
+            uint32_t pacc[NACC][2];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) pa[q] = po[q] = 0u;
+            for (int q = 0; q < NACC; ++q) pacc[q][0] = pacc[q][1] = 0u;
             bool e_first = true;
             for (int st = s_b; st < s_e; ++st, ++item) {
                 const int buf = (int)(item % STAGES);
@@ -382,15 +382,28 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                         for (int kk = 0; kk < 16; kk += 2) {
                             const uint32_t ua0 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
                             const uint32_t ua1 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + ((kk + 1) & 3));
-                            const uint8_t* r0 = tbs + (pl * 16 + kk) * 4 * TQ + ua0 * 4u;
-                            const uint8_t* r1 = tbs + (pl * 16 + kk + 1) * 4 * TQ + ua1 * 4u;
+                            const uint8_t* r0 = tbs + (pl * 16 + kk) * G::NQ * TQ + ua0 * 4u;
+                            const uint8_t* r1 = tbs + (pl * 16 + kk + 1) * G::NQ * TQ + ua1 * 4u;
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
+                            for (int q = 0; q < NACC; ++q) {
                                 const uint32_t v0 = *reinterpret_cast<const uint32_t*>(r0 + q * TQ);
                                 const uint32_t v1 = *reinterpret_cast<const uint32_t*>(r1 + q * TQ);
-                                pa[q] += (v0 & 0x00ff00ffu) + (v1 & 0x00ff00ffu);
-                                asm("mad.hi.u32 %0, %1, %2, %0;\n" : "+r"(po[q]) : "r"(v0), "r"(sh24));
-                                asm("mad.hi.u32 %0, %1, %2, %0;\n" : "+r"(po[q]) : "r"(v1), "r"(sh24));
+                                if constexpr (E16) {
+                                    pacc[q][0] += v0 + v1;
+                                    pacc[q][1] += __byte_perm(v0, 0u, 0x4432u) + __byte_perm(v1, 0u, 0x4432u);
+                                } else {
+                                    const uint32_t e0 = __byte_perm(v0, 0u, 0x4240u), e1 = __byte_perm(v1, 0u, 0x4240u);
+                                    const uint32_t o0 = __byte_perm(v0, 0u, 0x4341u), o1 = __byte_perm(v1, 0u, 0x4341u);
+                                    if (q < 2) {     // ALU pipe: one 3-input add per accumulator
+                                        pacc[q][0] += e0 + e1;
+                                        pacc[q][1] += o0 + o1;
+                                    } else {         // FMA pipe: multiply-adds by an opaque 1
+                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e0), "r"(one));
+                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e1), "r"(one));
+                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o0), "r"(one));
+                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o1), "r"(one));
+                                    }
+                                }
                             }
                         }
                     }
@@ -406,21 +419,29 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
 #pragma unroll
                         for (int j = 0; j < 16; ++j) ev[j] = 0u;
                     }
+                    if constexpr (E16) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t s2 = pa[q] >> 16, t = po[q] - (s2 << 8);
-                        ev[4 * q + 0] += pa[q] & 0xffffu;
-                        ev[4 * q + 1] += t & 0xffffu;
-                        ev[4 * q + 2] += s2;
-                        ev[4 * q + 3] += t >> 16;
-                        pa[q] = po[q] = 0u;
+                        for (int q = 0; q < NACC; ++q) {
+                            ev[2 * q + 0] += pacc[q][0] - (pacc[q][1] << 16);
+                            ev[2 * q + 1] += pacc[q][1];
+                            pacc[q][0] = pacc[q][1] = 0u;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            ev[4 * q + 0] += pacc[q][0] & 0xffffu;
+                            ev[4 * q + 2] += pacc[q][0] >> 16;
+                            ev[4 * q + 1] += pacc[q][1] & 0xffffu;
+                            ev[4 * q + 3] += pacc[q][1] >> 16;
+                            pacc[q][0] = pacc[q][1] = 0u;
+                        }
                     }
                     tmem_st16(t_e, ev);
                     tmem_wait_st();
                     e_first = false;
                 }
             }
-            int corr = p4::E_BIAS * KS * (s_e - s_b);
+            int corr = (E16 ? 32768 : p4::E_BIAS) * KS * (s_e - s_b);
             if (s_e == nst_all) corr += (int)(((P.Kp - p.K) + p.pad_lookups) * (int64_t)p.t00);
             // the row's residual groups: issued before the wait on the tile's MMAs, so their
             // latency overlaps it (the K loop's registers are free here)

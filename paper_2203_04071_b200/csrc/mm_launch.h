@@ -36,6 +36,9 @@ int launch_mm_i32(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid,
 struct P4Args;
 int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int8_t* dtab,
             uint32_t* tables, int8_t* wpk, int half, int swap, cudaStream_t st);
+int p4_pack_w(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, int8_t* wpk, cudaStream_t st);
+int p4_pack16(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int16_t* e16,
+              uint32_t* tables, cudaStream_t st);
 int launch_p4(const P4Args& a, cudaStream_t st);
 int launch_p4w(const P4Args& a, cudaStream_t st);
 // P4W tile rows of a shape (cw consumer warps: 28 -> 896, 24 -> 768, 20 -> 640, 16 -> 512);

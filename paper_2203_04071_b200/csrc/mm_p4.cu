@@ -26,6 +26,31 @@ int p4_pack(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, cons
     return (int)cudaGetLastError();
 }
 
+int p4_pack_w(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, int8_t* wpk, cudaStream_t st) {
+    const int64_t t2 = ((N + p4::TN - 1) / p4::TN) * Kp * p4::TN;
+    p4_pack_w_kernel<<<(unsigned)std::min<int64_t>((t2 + 255) / 256, 148 * 16), 256, 0, st>>>(W, N, K, ldw, Kp, wpk);
+    return (int)cudaGetLastError();
+}
+
+int p4_pack16(const int8_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, const int16_t* e16,
+              uint32_t* tables, cudaStream_t st) {
+    static unsigned configured = 0;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (!(configured & (1u << (dev & 31)))) {
+        cudaError_t e = cudaFuncSetAttribute(p4_pack16_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             131072);
+        if (e != cudaSuccess) return (int)e;
+        configured |= 1u << (dev & 31);
+    }
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nb = (N + p4::TN - 1) / p4::TN;
+    const int64_t items = nb * ((Kp + PACK_KC - 1) / PACK_KC);
+    p4_pack16_tables_kernel<<<(unsigned)std::min<int64_t>(items, (int64_t)(sms > 0 ? sms : 148)), PACK_THREADS,
+                              131072, st>>>(W, N, K, ldw, Kp, e16, tables);
+    return (int)cudaGetLastError();
+}
+
 template <int RPL, bool HALF>
 static int launch_p4_t(const P4Args& a, cudaStream_t st) {
     static unsigned configured = 0;
@@ -50,16 +75,16 @@ static int launch_p4_t(const P4Args& a, cudaStream_t st) {
 
 int g_p4w_pdl = 1;   // programmatic dependent launch of P4W (AXQ_P4W_PDL=0 disables)
 
-template <bool HALF, int KSX, bool RES = false, int CWX = 28>
+template <bool HALF, int KSX, bool RES = false, int CWX = 28, bool E16 = false>
 static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
-    using G = p4w::Geo<HALF, KSX, CWX>;
+    using G = p4w::Geo<HALF, KSX, CWX, E16>;
     using S = p4w::Shape<CWX>;
     static unsigned configured = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     dev &= 31;
     if (!(configured & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(lut_p4w_kernel<HALF, KSX, RES, CWX>,
+        cudaError_t e = cudaFuncSetAttribute(lut_p4w_kernel<HALF, KSX, RES, CWX, E16>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
         if (e != cudaSuccess) return (int)e;
         configured |= 1u << dev;
@@ -82,7 +107,7 @@ static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     P4Args args = a;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, lut_p4w_kernel<HALF, KSX, RES, CWX>, args);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, lut_p4w_kernel<HALF, KSX, RES, CWX, E16>, args);
     return (int)(e != cudaSuccess ? e : cudaGetLastError());
 }
 
@@ -93,6 +118,11 @@ int launch_p4w(const P4Args& a, cudaStream_t st) {
     const int cw = a.cw ? a.cw : 28;
     constexpr int BAD = (int)cudaErrorInvalidValue;
     if (a.c4 && cw != 28) return BAD;           // the 4-byte-tap table lives in the 28-warp shapes
+    if (a.e16) {                                // P4W16: half-range int16-E tables, 16-k stages
+        if (!a.half || a.c4 || a.ks != 16) return BAD;
+        if (res) return launch_p4w_t<true, 16, true, 16, true>(a, st);
+        return cw == 16 ? launch_p4w_t<true, 16, false, 16, true>(a, st) : launch_p4w_t<true, 16, false, 28, true>(a, st);
+    }
     if (!a.half) {                              // full-range tables, 16-k stages
         if (cw == 16 && !res) return launch_p4w_t<false, 16, false, 16>(a, st);
         return cw == 28 ? launch_p4w_t<false, 16>(a, st) : BAD;

@@ -141,8 +141,17 @@ class ApproxConv2d:
         self.qw = q.permute(0, 2, 3, 1).contiguous()                      # KRSC relayout
         self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
         self.wp = None
-        if packed and lut.repr == "delta8" and self.C % 16 == 0 and self.C * self.R * self.S >= 128:
-            self.wp = ax.WPack(lut, self.qw.reshape(self.Kout, -1), a_nonneg=a_nonneg)
+        if packed and self.C % 16 == 0 and self.C * self.R * self.S >= 128:
+            # delta8 tables: packed int8 E (P4W); other ACUs with |E| < 2^15 and non-negative
+            # inputs: packed int16 E (P4W16); otherwise the resident-table kernel
+            if lut.repr == "delta8":
+                self.wp = ax.WPack(lut, self.qw.reshape(self.Kout, -1), a_nonneg=a_nonneg)
+            elif a_nonneg:
+                try:
+                    self.wp = ax.WPack(lut, self.qw.reshape(self.Kout, -1), a_nonneg=True)
+                except ax.AxqError as e:
+                    if e.status != ax.AXQ_ERR_UNSUPPORTED:
+                        raise
         self.n_sms = torch.cuda.get_device_properties(torch.device(device)).multi_processor_count
         self.d_amax_a = torch.empty(1, device=device)
         self.d_scale_a = torch.empty(1, device=device)

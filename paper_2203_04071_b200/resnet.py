@@ -116,6 +116,16 @@ class ApproxResNet:
                 elif kind == "conv" and cin % 16 == 0 and cin * k * k >= 64:
                     # every other conv input is a quantized ReLU output: codes >= 0
                     self.wp[name] = ax.WPack(lut, self.qw[name].reshape(cout, -1), a_nonneg=True)
+        elif packed:
+            # an ACU whose error does not fit int8: the ReLU-input convs take packed int16-E
+            # tables (P4W16) when |E| < 2^15; the signed-input stem stays on the gather kernel
+            for name, kind, cout, cin, k, stride, pad in self.specs:
+                if kind == "conv" and name != "stem" and cin % 16 == 0 and cin * k * k >= 64:
+                    try:
+                        self.wp[name] = ax.WPack(lut, self.qw[name].reshape(cout, -1), a_nonneg=True)
+                    except ax.AxqError as e:
+                        if e.status != ax.AXQ_ERR_UNSUPPORTED:
+                            raise
         self.n_sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._bufs = {}
         self.calibrated = False
