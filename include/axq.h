@@ -65,7 +65,8 @@ typedef struct axq_lut* axq_lut_t;
 #define AXQ_PATH_WIDE 5       /* wide (b = 9..12) kernels (NEXT-2) */
 #define AXQ_PATH_LSTM_REC 6   /* persistent LSTM recurrence */
 #define AXQ_PATH_F32A 7       /* quantize-on-load kernel (axq_lut_gemm_f32a / axq_lut_conv2d_f32) */
-#define AXQ_PATH_P4W16 8      /* lut_p4w16_kernel: packed int16 E tables (|E| beyond int8) */
+#define AXQ_PATH_P4W16 8      /* lut_p4w_kernel<E16>: packed int16 E tables (|E| beyond int8) */
+#define AXQ_PATH_WIDEPK 9     /* lut_widepk_kernel: packed wide (b = 9..12) tables (NEXT-2) */
 #define AXQ_PATH_SPLITK 0x100 /* K split across CTAs (int32 atomics + epilogue pass) */
 #define AXQ_PATH_STREAMK 0x200/* stream-K pieces in the caller's workspace */
 axq_status axq_last_path(int* out);
@@ -456,6 +457,21 @@ axq_status axq_quantize16(const float* x, int64_t n, const float* d_scale, int b
 axq_status axq_lut_gemm16(int64_t M, int64_t N, int64_t K, const int16_t* A, int64_t lda,
                           const int16_t* W, int64_t ldw, axq_lut_t lut, const axq_epilogue* ep,
                           int32_t* C, int64_t ldc, void* stream);
+
+/* NEXT-2 packed ("populate the CPU cores cache with the LUTs", P:322 wider = slower):
+ * the wide table tiled by the weights.  For every k and every quad of 4 output columns the four
+ * weights select a 2^b-entry slab of the table, T[k][q][ua] = 4 x (E[ua][w(4q+j,k)] + 2^15),
+ * staged into shared memory by bulk copies and read with one 64-bit load per 4 lookups.
+ * axq_wpack16_create: W int16 codes [N][ldw] (N x K) and a WIDE16 handle (else
+ *   AXQ_ERR_UNSUPPORTED; also for K >= 65528).  Allocates N * Kp * 2^(b+1) bytes of tables
+ *   (512 MiB for N = K = 256 at b = 12) plus packed weights; synchronizes.
+ * axq_lut_gemm16_wp: acc[m][n] = sum_k LUT[A[m][k]][W[n][k]] for int16 codes A [M][lda]
+ *   (bit-identical to axq_lut_gemm16); raw int32 C [M][ldc] (ep NULL) or the fused epilogue
+ *   (row layout).  Free the pack with axq_wpack_destroy. */
+axq_status axq_wpack16_create(axq_lut_t lut, const int16_t* W, int64_t N, int64_t K, int64_t ldw,
+                              axq_wpack_t* out);
+axq_status axq_lut_gemm16_wp(int64_t M, const int16_t* A, int64_t lda, axq_wpack_t wp,
+                             const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream);
 
 axq_status axq_lstm_recurrent(int64_t T, int64_t B, int64_t H, const float* gates_ih,
                               const int8_t* qw_hh, const float* d_scale_w_hh, const float* b_hh,

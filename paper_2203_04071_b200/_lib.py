@@ -33,11 +33,12 @@ EXPORTED = [
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
     "axq_last_path", "axq_workspace_elems", "axq_lut_gemm_f32a", "axq_lut_conv2d_f32",
+    "axq_wpack16_create", "axq_lut_gemm16_wp",
 ]
 
 # axq_last_path kernel families (include/axq.h AXQ_PATH_*)
 PATH_NAMES = {1: "v1", 2: "p4", 3: "p4w", 4: "gconv", 5: "wide", 6: "lstm_rec", 7: "f32a",
-              8: "p4w16"}
+              8: "p4w16", 9: "widepk"}
 PATH_SPLITK, PATH_STREAMK = 0x100, 0x200
 
 
@@ -82,6 +83,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_version": ([], i32),
         "axq_last_path": ([ctypes.POINTER(i32)], i32),
         "axq_workspace_elems": ([i64, i64], i64),
+        "axq_wpack16_create": ([vp, vp, i64, i64, i64, ctypes.POINTER(vp)], i32),
+        "axq_lut_gemm16_wp": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_lut_gemm_f32a": ([i64, i64, i64, vp, i64, vp, vp, i64, vp, ctypes.POINTER(axq_epilogue),
                                vp, i64, vp], i32),
         "axq_lut_conv2d_f32": ([ctypes.POINTER(axq_conv_desc), vp, vp, vp, vp,
@@ -577,6 +580,39 @@ def axq_lut_gemm16(A, W, lut: Lut, ep: axq_epilogue | None = None, C=None, strea
         M, N, K, _ptr(A), A.stride(0), _ptr(W), W.stride(0), lut.handle,
         ctypes.byref(ep) if ep is not None else None, _ptr(C), C.stride(0) if C is not None else 0,
         _stream(stream)))
+
+
+class WPack16:
+    """Owns a wide (b = 9..12) weight pack: the table tiled by the weights (axq_wpack16_create)."""
+
+    def __init__(self, lut: Lut, W):
+        """W: device int16 codes [N][K] of a WIDE16 handle's bit width."""
+        assert W.dtype.itemsize == 2 and W.stride(1) == 1
+        N, K = W.shape
+        h = ctypes.c_void_p()
+        _check("axq_wpack16_create", load().axq_wpack16_create(lut.handle, _ptr(W), N, K, W.stride(0),
+                                                               ctypes.byref(h)))
+        self.handle = h
+        self.N, self.K = N, K
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            load().axq_wpack_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def axq_lut_gemm16_wp(A, wp: WPack16, ep: axq_epilogue | None = None, C=None, stream=None) -> None:
+    """A int16 codes [M][K] with a wide weight pack; raw int32 C [M][N] or the fused epilogue."""
+    M = A.shape[0]
+    _check("axq_lut_gemm16_wp", load().axq_lut_gemm16_wp(
+        M, _ptr(A), A.stride(0), wp.handle, ctypes.byref(ep) if ep is not None else None, _ptr(C),
+        C.stride(0) if C is not None else 0, _stream(stream)))
 
 
 def axq_im2col_nhwc_i8(X, c_valid: int, R: int, S: int, stride, pad, A, stream=None) -> None:

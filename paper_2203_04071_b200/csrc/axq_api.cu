@@ -15,6 +15,7 @@
 #include "lut_p4_args.h"
 #include "gconv.cuh"
 #include "wide_args.h"
+#include "wide_pk_geo.h"
 #include "lstm_rec_args.h"
 #include "mm_launch.h"
 #include "glue_kernels.cuh"
@@ -24,6 +25,7 @@ struct axq_wpack {
     int device;
     int half;
     int e16;                   // P4W16 tables (int16 E, 2 columns per packed word)
+    int wide_bits;             // > 0: a wide (b = 9..12) pack for axq_lut_gemm16_wp
     int swap;                  // tables specialised on activations (axq_lut_gemm_xs)
     const int8_t* dtab;        // packing table: the LUT's [uw][ua] delta8 table, or (swap) a
                                // transposed [ua][uw] copy owned by the wpack (dtab_own)
@@ -110,7 +112,7 @@ axq_status launch_mm(int epi, int loader, int repr, const axq::MMArgs& p, const 
 
 // Must agree with mm_launch.cuh::launch_cfg: byte-wise loaders and the int32 table only
 // have the SMALL tile instantiated.
-Cfg pick_cfg(int64_t M, int loader, int repr) {
+Cfg pick_cfg(int64_t M, int64_t N, int loader, int repr) {
     const bool big_ok = repr != AXQ_LUT_I32 &&
                         (loader == axq::LOAD_GEMM || loader == axq::LOAD_CONV || loader == axq::LOAD_CONV_C4);
     static int forced = -1;   // AXQ_V1_CFG (measurement switch): 1 SMALL, 2 BIG, 3 TINY, 4 MID
@@ -124,6 +126,7 @@ Cfg pick_cfg(int64_t M, int loader, int repr) {
         if (forced == 4) return axq::CFG_MID;
         return CFG_SMALL;
     }
+    if (big_ok && loader == axq::LOAD_GEMM && M <= 64 && N <= 64) return axq::CFG_SQ;
     if (big_ok && loader == axq::LOAD_GEMM && M <= 64) return axq::CFG_TINY;
     return (M > 2048 && big_ok) ? CFG_BIG : CFG_SMALL;
 }
@@ -142,7 +145,9 @@ int64_t pick_k_split(int64_t M, int64_t N, int64_t K, const Cfg& c, bool allow) 
     int64_t want = (int64_t)sm_count() * (mid ? 1 : 2);
     if (tiles >= (mid ? want * 3 / 4 : want)) return kr;
     int64_t splits = (want + tiles - 1) / tiles;
-    int64_t max_splits = std::max<int64_t>(1, kr / (4 * axq::KC));  // >= 64 k per split
+    // >= 64 k per split; the SQ tile (tiny GEMMs, latency-bound) down to one 16-k chunk
+    const bool sq = c.warps == axq::CFG_SQ.warps && c.wc == axq::CFG_SQ.wc;
+    int64_t max_splits = std::max<int64_t>(1, kr / ((sq ? 1 : 4) * axq::KC));
     splits = std::min(splits, max_splits);
     int64_t ks = (kr + splits - 1) / splits;
     ks = ((ks + axq::KC - 1) / axq::KC) * axq::KC;
@@ -515,7 +520,7 @@ static axq_status launch_epilogue(int64_t M, int64_t N, const int32_t* acc, int6
 // Common driver: plan split-K, launch the fused or the split (atomic + epilogue) variant.
 static axq_status run_mm(axq::MMArgs& p, int loader, axq_lut_t lut, const axq::EpiArgs* epi,
                          int32_t* workspace, int32_t* C_raw, int64_t ldc, cudaStream_t st) {
-    Cfg c = pick_cfg(p.M, loader, lut->repr);
+    Cfg c = pick_cfg(p.M, p.N, loader, lut->repr);
     const bool can_split = epi ? (workspace != nullptr) : true;
     p.k_split = pick_k_split(p.M, p.N, p.K, c, can_split);
     const int64_t splits = p.K > 0 ? (p.K + p.k_split - 1) / p.k_split : 1;
@@ -868,6 +873,7 @@ axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K
 
 axq_status axq_wpack_repack(axq_wpack_t wp, const int8_t* W, int64_t ldw, void* stream) {
     if (!wp || !W || ldw < wp->K) return AXQ_ERR_INVALID;
+    if (wp->wide_bits) return AXQ_ERR_UNSUPPORTED;
     if (wp->e16) return AXQ_ERR_UNSUPPORTED;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -961,6 +967,7 @@ int64_t axq_workspace_elems(int64_t M, int64_t N) {
 
 static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep, bool conv,
                          int32_t* C, int64_t ldc, cudaStream_t st) {
+    if (wp->wide_bits) return AXQ_ERR_INVALID;   // wide packs: axq_lut_gemm16_wp
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev != wp->device) return AXQ_ERR_INVALID;
@@ -1282,6 +1289,73 @@ axq_status axq_lut_gemm16(int64_t M, int64_t N, int64_t K, const int16_t* A, int
     if (M == 0 || N == 0) return AXQ_OK;
     g_last_path = AXQ_PATH_WIDE;
     const int rc = axq::launch_wide(a, sm_count(), S(stream));
+    return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
+}
+
+// ---- NEXT-2, packed: weight-specialised wide tables (wide_pk.cuh) ----
+axq_status axq_wpack16_create(axq_lut_t lut, const int16_t* W, int64_t N, int64_t K, int64_t ldw,
+                              axq_wpack_t* out) {
+    if (!out || !lut || !lut->d_table || N <= 0 || K <= 0 || ldw < K || !W) return AXQ_ERR_INVALID;
+    *out = nullptr;
+    if (lut->repr != AXQ_LUT_WIDE16) return AXQ_ERR_UNSUPPORTED;   // E must fit int16
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != lut->device) return AXQ_ERR_INVALID;
+    if (K >= 65536 - axq::wpk::KP_ALIGN) return AXQ_ERR_UNSUPPORTED;   // 16-bit-lane sums exact below 2^16 k
+    axq_status s = overflow_guard(lut, K);
+    if (s != AXQ_OK) return s;
+    const int bits = lut->bits, tn = axq::widepk_tn(bits);
+    axq_wpack* w = new axq_wpack();
+    w->device = dev;
+    w->wide_bits = bits;
+    w->t00 = lut->t00;
+    w->N = N;
+    w->K = K;
+    w->Kp = (K + axq::wpk::KP_ALIGN - 1) / axq::wpk::KP_ALIGN * axq::wpk::KP_ALIGN;
+    const int64_t nb = (N + tn - 1) / tn;
+    const size_t tb = (size_t)nb * w->Kp * (tn / 4) * ((size_t)1 << bits) * 8, wb = (size_t)nb * w->Kp * tn * 2;
+    w->bytes = (int64_t)(tb + wb);
+    cudaError_t e = cudaMalloc(&w->tables, tb);
+    if (e == cudaSuccess) e = cudaMalloc(&w->wpk, wb);
+    if (e == cudaSuccess) {
+        const int rc = axq::widepk_pack(W, N, K, ldw, w->Kp, bits, reinterpret_cast<const int16_t*>(lut->d_table),
+                                        reinterpret_cast<uint2*>(w->tables), reinterpret_cast<int16_t*>(w->wpk),
+                                        sm_count(), 0);
+        e = rc ? (cudaError_t)rc : cudaDeviceSynchronize();
+    }
+    if (e != cudaSuccess) {
+        cudaFree(w->tables);
+        cudaFree(w->wpk);
+        delete w;
+        return cuda_fail(e);
+    }
+    *out = w;
+    return AXQ_OK;
+}
+
+axq_status axq_lut_gemm16_wp(int64_t M, const int16_t* A, int64_t lda, axq_wpack_t wp,
+                             const axq_epilogue* ep, int32_t* C, int64_t ldc, void* stream) {
+    if (!wp || !wp->wide_bits || M < 0 || (M > 0 && (!A || lda < wp->K))) return AXQ_ERR_INVALID;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != wp->device) return AXQ_ERR_INVALID;
+    axq::WidePkArgs a{};
+    a.A = A; a.lda = lda; a.M = M; a.N = wp->N; a.K = wp->K; a.Kp = wp->Kp; a.bits = wp->wide_bits;
+    a.tables = reinterpret_cast<const uint2*>(wp->tables);
+    a.wts = reinterpret_cast<const int16_t*>(wp->wpk);
+    a.t00 = wp->t00;
+    if (ep) {
+        axq_status s = check_epilogue(ep, wp->N, false);
+        if (s != AXQ_OK) return s;
+        a.ep = to_epi(ep, false, 0);
+    } else {
+        if (!C || ldc < wp->N) return AXQ_ERR_INVALID;
+        a.C_out = C;
+        a.ldc = ldc;
+    }
+    if (M == 0) return AXQ_OK;
+    g_last_path = AXQ_PATH_WIDEPK;
+    const int rc = axq::launch_widepk(a, sm_count(), S(stream));
     return rc ? cuda_fail((cudaError_t)rc) : AXQ_OK;
 }
 

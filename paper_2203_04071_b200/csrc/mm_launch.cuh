@@ -40,6 +40,8 @@ int launch_cfg(const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st) {
     if constexpr (big_ok) {
         if (c.wc == CFG_TINY.wc && c.warps == CFG_TINY.warps && LOADER == LOAD_GEMM)
             return launch_one<REPR, CFG_TINY.tn, CFG_TINY.R, CFG_TINY.warps, LOADER, EPI, CFG_TINY.wc>(p, grid, st);
+        if (c.wc == CFG_SQ.wc && c.warps == CFG_SQ.warps && LOADER == LOAD_GEMM)
+            return launch_one<REPR, CFG_SQ.tn, CFG_SQ.R, CFG_SQ.warps, LOADER, EPI, CFG_SQ.wc>(p, grid, st);
         if (c.wc == CFG_MID.wc && c.warps == CFG_MID.warps && LOADER == LOAD_GEMM)
             return launch_one<REPR, CFG_MID.tn, CFG_MID.R, CFG_MID.warps, LOADER, EPI, CFG_MID.wc>(p, grid, st);
         if (c.warps == CFG_BIG.warps && c.R == CFG_BIG.R && c.wc == 1)

@@ -26,6 +26,9 @@ constexpr Cfg CFG_TINY{8, 2, 32, 8};
 // per tile).  Measured no faster than SMALL + K split on the 256-row linear layer of BJ
 // configs[1] (86 vs 83 us), so pick_cfg does not select it; kept instantiated for A/B runs.
 constexpr Cfg CFG_MID{16, 1, 4, 8};
+// SQ (M <= 64 and N <= 64, e.g. BJ configs[0]): 4 warps as 2 x 2 over a 64 x 64 tile, K split
+// down to one 16-k chunk per CTA, so a latency-bound small GEMM spreads over many SMs.
+constexpr Cfg CFG_SQ{4, 1, 32, 2};
 
 // Return 0 or a cudaError_t code.
 int launch_mm_delta8(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
@@ -50,6 +53,11 @@ struct LstmRecArgs;
 struct GConvArgs;
 struct WideArgs;
 int launch_wide(const WideArgs& a, int sms, cudaStream_t st);   // wide.cuh (NEXT-2)
+struct WidePkArgs;
+int launch_widepk(const WidePkArgs& a, int sms, cudaStream_t st);   // wide_pk.cuh (NEXT-2 packed)
+int widepk_tn(int bits);
+int widepk_pack(const int16_t* W, int64_t N, int64_t K, int64_t ldw, int64_t Kp, int bits, const int16_t* e16,
+                uint2* tables, int16_t* wts, int sms, cudaStream_t st);
 int launch_quantize16(const float* x, int64_t n, const float* d_scale, int bits, int16_t* q, int sms,
                       cudaStream_t st);
 int launch_gconv(int repr, const GConvArgs& a, cudaStream_t st);   // gconv.cuh (groups > 1)

@@ -1,6 +1,7 @@
 """NEXT-2 measurement: the bitwidth experiment of P:322 on the GPU -- one LUT-GEMM
 (M = 8192, N = 256, K = 256, randerr tables) at b = 8 (int8 codes, resident-table v1 kernel and
-the packed-table P4W kernel) and b = 10, 12 (int16 codes, L2-resident wide tables)."""
+the packed-table P4W kernel) and b = 10, 12 (int16 codes: L2-resident wide tables gathered per
+lookup, and the table tiled by the weights -- axq_lut_gemm16_wp)."""
 import json
 import os
 import sys
@@ -40,8 +41,13 @@ for bits in (10, 12):
     W = torch.from_numpy(datagen.random_int16(4, (N, K), bits)).cuda()
     lut = ax.Lut(bits, datagen.lut_randerr(bits, 9, bits))
     out["b%d_wide" % bits] = timeit(lambda: ax.axq_lut_gemm16(A, W, lut, None, C))
+    wpb = ax.WPack16(lut, W)                       # the table tiled by the weights (packed)
+    out["b%d_packed" % bits] = timeit(lambda: ax.axq_lut_gemm16_wp(A, wpb, None, C))
+    del wpb
 res = {k: {"ms": round(v, 4), "G_lookups_s": round(M * N * K / v / 1e6, 1)} for k, v in out.items()}
 res["ratio_b10_b8v1"] = round(out["b10_wide"] / out["b8_v1"], 2)
 res["ratio_b12_b10"] = round(out["b12_wide"] / out["b10_wide"], 2)
+res["packed_ratio_b10_b8p4w"] = round(out["b10_packed"] / out["b8_p4w"], 2)
+res["packed_ratio_b12_b10"] = round(out["b12_packed"] / out["b10_packed"], 2)
 res["paper"] = "~2.1x per +2 bits on a Xeon with AVX2 (P:322)"
 print(json.dumps(res))

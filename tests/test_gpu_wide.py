@@ -80,3 +80,39 @@ def test_lut_gemm16_fused_and_guards(ax):
         big = torch.zeros(2, 4096, dtype=torch.int16, device=DEV)
         ax.axq_lut_gemm16(big, big, lut, None, torch.zeros(2, 2, dtype=torch.int32, device=DEV))
     assert e.value.status == ax.AXQ_ERR_OVERFLOW
+
+
+@pytest.mark.parametrize("bits", [9, 10, 11, 12])
+@pytest.mark.parametrize("M,N,K", [(300, 37, 129), (1, 1, 1), (2049, 16, 64), (4100, 9, 300)])
+def test_lut_gemm16_packed(ax, bits, M, N, K):
+    """NEXT-2 packed (the table tiled by the weights, axq_lut_gemm16_wp) == the oracle, raw int32
+    and fused epilogue, ragged M / N / K (K padded to whole stages)."""
+    T = datagen.lut_randerr(bits, 9, bits)
+    A = datagen.random_int16(30 + M, (M, K), bits)
+    W = datagen.random_int16(40 + N, (N, K), bits)
+    ref = oracle.lut_gemm16(A, W, T, bits)
+    lut = ax.Lut(bits, T)
+    assert lut.repr == "wide16"
+    wp = ax.WPack16(lut, _t(W))
+    C = torch.empty(M, N, dtype=torch.int32, device=DEV)
+    ax.axq_lut_gemm16_wp(_t(A), wp, None, C)
+    assert ax.axq_last_path()[0] == "widepk"
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(C.cpu().numpy(), ref)
+    sa, sw = np.float32(0.0007), np.float32(0.0011)
+    b = datagen.normal(38, bits, (N,), 0.1)
+    y = torch.empty(M, N, device=DEV)
+    ep = ax.make_epilogue(_t(np.array([sa])), _t(np.array([sw])), bias=_t(b), y=y, ldy=N)
+    ax.axq_lut_gemm16_wp(_t(A), wp, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.dequantize(ref, sa, sw, b))
+
+
+def test_wpack16_refuses_wide32(ax):
+    bits = 10
+    T = (datagen.lut_exact(bits).astype(np.int64)
+         + np.random.default_rng(7).integers(-100000, 100000, 1 << (2 * bits))).astype(np.int32)
+    lut = ax.Lut(bits, T)
+    with pytest.raises(ax.AxqError) as e:
+        ax.WPack16(lut, torch.zeros(4, 8, dtype=torch.int16, device=DEV))
+    assert e.value.status == ax.AXQ_ERR_UNSUPPORTED
