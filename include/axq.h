@@ -342,9 +342,9 @@ axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw);
  * (not computed).  workspace (nullable, workspace_elems floats, caller-owned, no contents
  * required): room for K-split partial products (up to 128 slices of one gradient; fewer when
  * the room is smaller, none without it); used to split the summed dimension when the output
- * alone cannot fill the SMs (the splits are added in a fixed order: deterministic).  fp32 FMA
- * accumulation (not bit-exact against a different summation order: within the fp32
- * dot-product bound).  Asynchronous on stream.  AXQ_ERR_INVALID for negative extents or a
+ * alone cannot fill the SMs (the splits are added in a fixed order: deterministic).  fp32
+ * accumulation on the tensor cores (not bit-exact against a different summation order: within
+ * the fp32 dot-product bound).  Asynchronous on stream.  AXQ_ERR_INVALID for negative extents or a
  * missing operand of a requested gradient.
  * --------------------------------------------------------------------------------- */
 axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float* gy,
@@ -372,6 +372,28 @@ axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const float* gy, cons
                                    const float* d_clip_w, float* gx, float* gw, float* gb,
                                    int8_t* cols, int64_t ldcols, float* gcols, float* workspace,
                                    int64_t workspace_elems, void* stream);
+
+/* The same backwards with per-output-channel weight quantization (the paper's quantizer,
+ * P:95 "weight ranges are per channel"; NEXT-1): d_scale_w_ch [N] (conv: [K]) replaces the
+ * scalar d_scale_w when non-NULL -- fq(qw)[n] = fl32(s_w[n] * qw[n]) -- and d_clip_w_ch [N]
+ * replaces d_clip_w (gw[n][k] masked by |w[n][k]| <= clip_w[n]).  The plain entry points are
+ * these with both NULL.  Both products run on the tensor cores (tcgen05 kind::f16: the fp32
+ * operand split exactly into three bf16 terms, the int8 codes exact in bf16, fp32
+ * accumulation in TMEM; A36'); AXQ_ERR_UNSUPPORTED when a product has more than
+ * 65535 x 128 output columns. */
+axq_status axq_ste_linear_backward_pc(int64_t M, int64_t N, int64_t K, const float* gy,
+                                      const int8_t* qa, const float* d_scale_a, const float* x,
+                                      const float* d_clip_a, const int8_t* qw, const float* d_scale_w,
+                                      const float* d_scale_w_ch, const float* w, const float* d_clip_w,
+                                      const float* d_clip_w_ch, float* gx, float* gw, float* gb,
+                                      float* workspace, int64_t workspace_elems, void* stream);
+axq_status axq_ste_conv2d_backward_pc(const axq_conv_desc* d, const float* gy, const int8_t* qx,
+                                      const float* d_scale_a, const float* x, const float* d_clip_a,
+                                      const int8_t* qw, const float* d_scale_w,
+                                      const float* d_scale_w_ch, const float* w, const float* d_clip_w,
+                                      const float* d_clip_w_ch, float* gx, float* gw, float* gb,
+                                      int8_t* cols, int64_t ldcols, float* gcols, float* workspace,
+                                      int64_t workspace_elems, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * Dequantize (unfused), same pinned formula as the epilogue.

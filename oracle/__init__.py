@@ -280,17 +280,25 @@ def lut_gemm16(A, W, lut, bits: int) -> np.ndarray:
 # ---- NEXT-4: approximation-aware retraining, the STE backward of an approximate linear layer
 #      (§III.A.2; reading A36) ----
 
+def _rows(v, ndim):
+    """A per-tensor scalar, or a per-output-channel vector [rows] broadcast along axis 0."""
+    v = np.asarray(v, dtype=np.float32)
+    return v if v.ndim == 0 else v.reshape((-1,) + (1,) * (ndim - 1))
+
+
 def fake_quant(q, s) -> np.ndarray:
     """The fake-quantized operand the STE differentiates through: fl32(s * q) ("quantized
-    floating point values")."""
-    return (np.float32(s) * np.asarray(q).astype(np.float32)).astype(np.float32)
+    floating point values"); s a scalar or per-row (per-output-channel weight scales, P:95
+    "weight ranges are per channel")."""
+    q = np.asarray(q)
+    return (_rows(s, q.ndim) * q.astype(np.float32)).astype(np.float32)
 
 
 def ste_linear_backward(gy, qa, s_a, qw, s_w, x=None, clip_a=None, w=None, clip_w=None):
     """Gradients of y = dequant(sum_k LUT[qa][qw]) + b under the straight-through estimator
     (P:107-109): the quantizer and the ACU are the identity in the backward pass, so the layer
     differentiates as y = fq(qa) fq(qw)^T + b, and an input outside its calibrated clip range
-    (|v| > clip) gets no gradient.  Plain fp64 matrix products of the fp32 operands, one
+    (|v| > clip) gets no gradient.  s_w / clip_w may be per output channel ([N]).  Plain fp64 matrix products of the fp32 operands, one
     rounding to fp32 at the end.  Returns (gx [M][K], gw [N][K], gb [N]) fp32."""
     gy64 = np.asarray(gy, dtype=np.float32).astype(np.float64)
     wf = fake_quant(qw, s_w).astype(np.float64)
@@ -301,7 +309,7 @@ def ste_linear_backward(gy, qa, s_a, qw, s_w, x=None, clip_a=None, w=None, clip_
     if x is not None:
         gx = np.where(np.abs(np.asarray(x, dtype=np.float32)) <= np.float32(clip_a), gx, 0.0)
     if w is not None:
-        gw = np.where(np.abs(np.asarray(w, dtype=np.float32)) <= np.float32(clip_w), gw, 0.0)
+        gw = np.where(np.abs(np.asarray(w, dtype=np.float32)) <= _rows(clip_w, 2), gw, 0.0)
     return gx.astype(np.float32), gw.astype(np.float32), gb.astype(np.float32)
 
 
@@ -334,5 +342,5 @@ def ste_conv2d_backward(gy, qx, s_a, qw, s_w, stride=(1, 1), pad=(0, 0), x=None,
     if x is not None:
         gx = np.where(np.abs(np.asarray(x, dtype=np.float32)) <= np.float32(clip_a), gx, 0.0)
     if w is not None:
-        gw = np.where(np.abs(np.asarray(w, dtype=np.float32)) <= np.float32(clip_w), gw, 0.0)
+        gw = np.where(np.abs(np.asarray(w, dtype=np.float32)) <= _rows(clip_w, 4), gw, 0.0)
     return gx.astype(np.float32), gw.astype(np.float32), gb.astype(np.float32)

@@ -33,7 +33,8 @@ EXPORTED = [
     "axq_calib_percentile", "axq_maxpool2d_nhwc_f32", "axq_quantize16", "axq_lut_gemm16",
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
     "axq_last_path", "axq_workspace_elems", "axq_lut_gemm_f32a", "axq_lut_conv2d_f32",
-    "axq_wpack16_create", "axq_lut_gemm16_wp",
+    "axq_wpack16_create", "axq_lut_gemm16_wp", "axq_ste_linear_backward_pc",
+    "axq_ste_conv2d_backward_pc",
 ]
 
 # axq_last_path kernel families (include/axq.h AXQ_PATH_*)
@@ -117,6 +118,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_wpack_shapes": ([i32, i32, i32], i32),
         "axq_ste_linear_backward": ([i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp], i32),
         "axq_ste_conv2d_backward": ([ctypes.POINTER(axq_conv_desc)] + [vp] * 13 + [i64, vp, vp, i64, vp], i32),
+        "axq_ste_linear_backward_pc": ([i64, i64, i64] + [vp] * 15 + [i64, vp], i32),
+        "axq_ste_conv2d_backward_pc": ([ctypes.POINTER(axq_conv_desc)] + [vp] * 15 + [i64, vp, vp, i64, vp], i32),
         "axq_amax_rows": ([vp, i64, i64, vp, vp], i32),
         "axq_quantize16": ([vp, i64, vp, i32, vp, vp], i32),
         "axq_im2col_nhwc_i8": ([vp] + [i64] * 11 + [vp, i64, vp], i32),
@@ -209,18 +212,66 @@ def axq_lut_create(bits: int, host_table: np.ndarray) -> Lut:
     return Lut(bits, host_table)
 
 
+def _ste_in(t, name, dtype, shape, dev):
+    """Read-only STE operand: on the device, of the expected dtype and shape; made contiguous
+    (autograd hands out expanded / strided gradients, e.g. stride 0 after y.sum())."""
+    import torch
+    if t is None:
+        return None
+    if t.device != dev or t.dtype != dtype or tuple(t.shape) != tuple(shape):
+        raise ValueError("%s: expected %s %s on %s, got %s %s on %s"
+                         % (name, dtype, tuple(shape), dev, t.dtype, tuple(t.shape), t.device))
+    return t if t.is_contiguous() else t.contiguous()
+
+
+def _ste_out(t, name, shape, dev):
+    import torch
+    if t is None:
+        return None
+    if t.device != dev or t.dtype != torch.float32 or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise ValueError("%s: expected a contiguous fp32 %s tensor on %s" % (name, tuple(shape), dev))
+    return t
+
+
+def _ste_scalar_or_vec(t, name, n, dev):
+    """A device fp32 scale / clip: one element (per tensor) or n (per output channel)."""
+    import torch
+    if t is None:
+        return None, False
+    t = _ste_in(t.reshape(-1), name, torch.float32, (t.numel(),), dev)
+    if t.numel() not in (1, n):
+        raise ValueError("%s: 1 or %d elements, got %d" % (name, n, t.numel()))
+    return t, t.numel() == n and n != 1
+
+
 def axq_ste_linear_backward(gy, qa, d_scale_a, qw, d_scale_w, x=None, d_clip_a=None, w=None,
                             d_clip_w=None, gx=None, gw=None, gb=None, workspace=None,
                             stream=None) -> None:
     """NEXT-4 STE backward of an approximate linear layer (include/axq.h): gy [M][N], qa [M][K],
     qw [N][K] -> gx [M][K], gw [N][K], gb [N] (each optional); workspace: fp32 tensor for
-    K-split partial products (optional)."""
+    K-split partial products (optional).  d_scale_w / d_clip_w: 1 element (per tensor) or N
+    (per output channel, axq_ste_linear_backward_pc).  Inputs are checked and made contiguous."""
+    import torch
+    dev = gy.device
     M, N = gy.shape
     K = qa.shape[1] if qa is not None else qw.shape[1]
-    _check("axq_ste_linear_backward", load().axq_ste_linear_backward(
+    gy = _ste_in(gy, "gy", torch.float32, (M, N), dev)
+    qa = _ste_in(qa, "qa", torch.int8, (M, K), dev)
+    qw = _ste_in(qw, "qw", torch.int8, (N, K), dev)
+    x = _ste_in(x, "x", torch.float32, (M, K), dev)
+    w = _ste_in(w, "w", torch.float32, (N, K), dev)
+    d_scale_a, _ = _ste_scalar_or_vec(d_scale_a, "d_scale_a", 1, dev)
+    d_clip_a, _ = _ste_scalar_or_vec(d_clip_a, "d_clip_a", 1, dev)
+    sw, sw_vec = _ste_scalar_or_vec(d_scale_w, "d_scale_w", N, dev)
+    cw, cw_vec = _ste_scalar_or_vec(d_clip_w, "d_clip_w", N, dev)
+    gx, gw, gb = _ste_out(gx, "gx", (M, K), dev), _ste_out(gw, "gw", (N, K), dev), _ste_out(gb, "gb", (N,), dev)
+    if workspace is not None and (workspace.dtype != torch.float32 or not workspace.is_contiguous()):
+        raise ValueError("workspace: a contiguous fp32 tensor")
+    _check("axq_ste_linear_backward_pc", load().axq_ste_linear_backward_pc(
         M, N, K, _ptr(gy), _ptr(qa), _ptr(d_scale_a), _ptr(x), _ptr(d_clip_a), _ptr(qw),
-        _ptr(d_scale_w), _ptr(w), _ptr(d_clip_w), _ptr(gx), _ptr(gw), _ptr(gb), _ptr(workspace),
-        workspace.numel() if workspace is not None else 0, _stream(stream)))
+        None if sw_vec else _ptr(sw), _ptr(sw) if sw_vec else None, _ptr(w),
+        None if cw_vec else _ptr(cw), _ptr(cw) if cw_vec else None, _ptr(gx), _ptr(gw), _ptr(gb),
+        _ptr(workspace), workspace.numel() if workspace is not None else 0, _stream(stream)))
 
 
 def axq_ste_conv2d_backward(d, gy, qx, d_scale_a, qw, d_scale_w, x=None, d_clip_a=None, w=None,
@@ -228,18 +279,39 @@ def axq_ste_conv2d_backward(d, gy, qx, d_scale_a, qw, d_scale_w, x=None, d_clip_
                             workspace=None, stream=None) -> None:
     """NEXT-4 STE backward of an approximate conv (include/axq.h): gy NHWC [N][Ho][Wo][K], qx
     NHWC int8, qw [K][R][S][C] int8 -> gx NHWC, gw [K][R][S][C], gb [K]; cols / gcols are the
-    im2col workspaces (allocated here when None)."""
+    im2col workspaces (allocated here when None).  Shapes are checked against the descriptor
+    (the kernel sizes everything from it); d_scale_w / d_clip_w may be per output channel."""
     import torch
-    Ho, Wo = gy.shape[1], gy.shape[2]
+    dev = gy.device
+    Ho, Wo = axq_conv2d_out_hw(d)
     M, Kc = d.N * Ho * Wo, d.R * d.S * d.C
+    gy = _ste_in(gy, "gy", torch.float32, (d.N, Ho, Wo, d.K), dev)
+    qx = _ste_in(qx, "qx", torch.int8, (d.N, d.H, d.W, d.C), dev)
+    qw = _ste_in(qw, "qw", torch.int8, (d.K, d.R, d.S, d.C), dev)
+    x = _ste_in(x, "x", torch.float32, (d.N, d.H, d.W, d.C), dev)
+    w = _ste_in(w, "w", torch.float32, (d.K, d.R, d.S, d.C), dev)
+    d_scale_a, _ = _ste_scalar_or_vec(d_scale_a, "d_scale_a", 1, dev)
+    d_clip_a, _ = _ste_scalar_or_vec(d_clip_a, "d_clip_a", 1, dev)
+    sw, sw_vec = _ste_scalar_or_vec(d_scale_w, "d_scale_w", d.K, dev)
+    cw, cw_vec = _ste_scalar_or_vec(d_clip_w, "d_clip_w", d.K, dev)
+    gx = _ste_out(gx, "gx", (d.N, d.H, d.W, d.C), dev)
+    gw = _ste_out(gw, "gw", (d.K, d.R, d.S, d.C), dev)
+    gb = _ste_out(gb, "gb", (d.K,), dev)
     if gw is not None and cols is None:
-        cols = torch.empty(M, (Kc + 15) // 16 * 16, dtype=torch.int8, device=gy.device)
+        cols = torch.empty(M, (Kc + 15) // 16 * 16, dtype=torch.int8, device=dev)
     if gx is not None and gcols is None:
-        gcols = torch.empty(M, Kc, dtype=torch.float32, device=gy.device)
-    _check("axq_ste_conv2d_backward", load().axq_ste_conv2d_backward(
+        gcols = torch.empty(M, Kc, dtype=torch.float32, device=dev)
+    if cols is not None and (cols.dtype != torch.int8 or cols.shape[0] != M or cols.shape[1] < Kc or cols.stride(1) != 1):
+        raise ValueError("cols: int8 [M][>= R*S*C] with unit column stride")
+    if gcols is not None and (gcols.dtype != torch.float32 or tuple(gcols.shape) != (M, Kc) or not gcols.is_contiguous()):
+        raise ValueError("gcols: contiguous fp32 [M][R*S*C]")
+    if workspace is not None and (workspace.dtype != torch.float32 or not workspace.is_contiguous()):
+        raise ValueError("workspace: a contiguous fp32 tensor")
+    _check("axq_ste_conv2d_backward_pc", load().axq_ste_conv2d_backward_pc(
         ctypes.byref(d), _ptr(gy), _ptr(qx), _ptr(d_scale_a), _ptr(x), _ptr(d_clip_a), _ptr(qw),
-        _ptr(d_scale_w), _ptr(w), _ptr(d_clip_w), _ptr(gx), _ptr(gw), _ptr(gb), _ptr(cols),
-        cols.stride(0) if cols is not None else 0, _ptr(gcols), _ptr(workspace),
+        None if sw_vec else _ptr(sw), _ptr(sw) if sw_vec else None, _ptr(w),
+        None if cw_vec else _ptr(cw), _ptr(cw) if cw_vec else None, _ptr(gx), _ptr(gw), _ptr(gb),
+        _ptr(cols), cols.stride(0) if cols is not None else 0, _ptr(gcols), _ptr(workspace),
         workspace.numel() if workspace is not None else 0, _stream(stream)))
 
 

@@ -8,12 +8,15 @@
 //   gx[m][k] = [|x[m][k]| <= clip_a] * sum_n gy[m][n] * fl(s_w * qw[n][k])
 //   gw[n][k] = [|w[n][k]| <= clip_w] * sum_m gy[m][n] * fl(s_a * qa[m][k])
 //   gb[n]    = sum_m gy[m][n]
-// Both products are one fp32 SIMT GEMM kernel (128 x 128 x 16 tiles, 8 x 8 outputs per thread,
-// fp32 FMA accumulation): the int8 operand is dequantized while it is staged into shared memory
-// and the STE mask is applied in the epilogue.  fp32 FMA, not tensor cores: the result is
-// compared with the fp64 oracle under the fp32 dot-product error bound (tests/test_gpu_ste.py).
+// Both products run on the tensor cores (ste_tc_kernel: tcgen05.mma kind::f16, the fp32 operand
+// split exactly into three bf16 terms, the int8 codes exact in bf16, fp32 accumulators in TMEM);
+// the STE mask is applied in the epilogue.  The result is compared with the fp64 oracle under
+// the fp32 dot-product error bound (tests/test_gpu_ste.py).  ste_gemm_kernel, the former fp32
+// SIMT version, is kept as the A/B reference (AXQ_STE_SIMT=1).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "axq.h"
@@ -129,15 +132,215 @@ __global__ void __launch_bounds__(ste::NT) ste_gemm_kernel(int64_t M, int64_t N,
     }
 }
 
-// C[i] = mask(i) * sum_{z < S} part[z][i], the splits added in order (deterministic)
+// ---------------------------------------------------------------------------------------
+// The same product on the 5th-generation tensor cores (tcgen05.mma kind::f16, fp32 accumulators
+// in TMEM).  The int8 codes are exact in bf16; the fp32 operand A is split exactly into three
+// bf16 terms hi + mid + lo (each the round-to-nearest bf16 of the remainder, so |A - hi - mid -
+// lo| <= 2^-27 |A|, below fp32's own unit roundoff), and the three products accumulate into one
+// TMEM accumulator: C = sum_p (hi + mid + lo)(i, p) * q(p, j), times the per-tensor scale s_b in
+// the epilogue, or with a per-p scale s_b[p] folded into A first (fl(A * s_b[p])).
+// CTA tile 128 (i) x 128 (j), 32 p per stage (2 MMAs of K = 16 per term), double-buffered; the
+// 4 warps convert the operands of stage s+1 while the tensor cores run stage s; each thread owns
+// one TMEM lane (row i) in the epilogue.
+// ---------------------------------------------------------------------------------------
+namespace stetc {
+constexpr int BM = 128, BN = 128, BK = 32, NT = 128;
+constexpr int A_TERM = BM * BK * 2;               // one bf16 term of the A tile: 8 KiB
+constexpr int A_STAGE = 3 * A_TERM;               // hi, mid, lo
+constexpr int B_STAGE = BN * BK * 2;              // 8 KiB
+constexpr int STAGE = A_STAGE + B_STAGE;          // 32 KiB
+constexpr int SMEM = 2 * STAGE + 64;              // + mbarriers / TMEM address
+// instruction descriptor: D f32 (bits 4-5 = 1), A / B bf16 (7-9, 10-12 = 1), K-major, N >> 3,
+// M >> 4
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+}  // namespace stetc
+
+__device__ __forceinline__ uint64_t ste_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // SWIZZLE_NONE K-major: core matrices 8 rows x 16 B; LBO between K chunks, SBO between 8-row
+    // groups; descriptor version 1 (sm_100)
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)((lbo >> 4) & 0x3fffu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fffu) << 32) | ((uint64_t)1 << 46);
+}
+
+__device__ __forceinline__ uint16_t bf16_rn_bits(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+// chunk layout of a [rows][32 k] bf16 tile: k chunk c (8 k = 16 B) at c * rows * 16, row r at r * 16
+template <bool TA, bool PCS>
+__global__ void __launch_bounds__(stetc::NT) ste_tc_kernel(int64_t M, int64_t N, int64_t K, const float* __restrict__ A,
+                                                          int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
+                                                          const float* __restrict__ s_b, float* __restrict__ C,
+                                                          int64_t ldc, const float* __restrict__ R, int64_t ldr,
+                                                          const float* __restrict__ clip, int clip_vec, int64_t kc) {
+    using namespace stetc;
+    extern __shared__ __align__(1024) uint8_t st_smem[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t kb = (int64_t)blockIdx.z * kc, ke = min(K, kb + kc);
+    C += (int64_t)blockIdx.z * M * ldc;
+    const bool split = gridDim.z > 1;
+    // row tiles on grid.x (up to 2^31 - 1: a conv's N*Ho*Wo positions), column tiles on grid.y
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(st_smem);
+    const uint32_t bar = s_base + 2 * STAGE;                   // mma-done barriers [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(st_smem + 2 * STAGE + 16);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar + 8));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(tmem_slot)), "n"(BN) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const float sb = PCS ? 1.f : *s_b;
+
+    // operand staging of the p-range [k0, k0 + 32) into stage buffer `buf`: thread t converts
+    // row t of A (3 bf16 terms) and column t of B, 4 chunks of 8 p each
+    auto stage = [&](int buf, int64_t k0) {
+        uint8_t* sa = st_smem + buf * STAGE;
+        uint8_t* sbuf = sa + A_STAGE;
+        const int64_t i = m0 + tid, j = n0 + tid;
+#pragma unroll
+        for (int c = 0; c < BK / 8; ++c) {
+            float a[8];
+            int8_t q[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int64_t p = k0 + c * 8 + e;
+                const bool pin = p < ke;
+                float v = 0.f;
+                if (pin && i < M) {
+                    v = TA ? A[p * lda + i] : A[i * lda + p];
+                    if (PCS) v = __fmul_rn(v, s_b[p]);       // per-channel scale of the summed index
+                }
+                a[e] = v;
+                q[e] = (pin && j < N) ? B[p * ldb + j] : (int8_t)0;
+            }
+            uint32_t hw[4], mw[4], lw[4], bw[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+                uint16_t h[2], md[2], l[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const float x = a[e + u];
+                    h[u] = bf16_rn_bits(x);
+                    const float r1 = __fsub_rn(x, __bfloat162float(__ushort_as_bfloat16(h[u])));
+                    md[u] = bf16_rn_bits(r1);
+                    const float r2 = __fsub_rn(r1, __bfloat162float(__ushort_as_bfloat16(md[u])));
+                    l[u] = bf16_rn_bits(r2);
+                }
+                hw[e / 2] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+                mw[e / 2] = (uint32_t)md[0] | ((uint32_t)md[1] << 16);
+                lw[e / 2] = (uint32_t)l[0] | ((uint32_t)l[1] << 16);
+                bw[e / 2] = (uint32_t)bf16_rn_bits((float)q[e]) | ((uint32_t)bf16_rn_bits((float)q[e + 1]) << 16);
+            }
+            const int off = c * BM * 16 + tid * 16;
+            *reinterpret_cast<uint4*>(sa + 0 * A_TERM + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(sa + 1 * A_TERM + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+            *reinterpret_cast<uint4*>(sa + 2 * A_TERM + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            *reinterpret_cast<uint4*>(sbuf + c * BN * 16 + tid * 16) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+        }
+    };
+
+    const int nst = (int)((ke - kb + BK - 1) / BK);
+    uint32_t mma_phase[2] = {0u, 0u};
+    if (nst > 0) stage(0, kb);
+    for (int s = 0; s < nst; ++s) {
+        const int buf = s & 1;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic stores -> MMA
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint32_t sa = s_base + buf * STAGE, sbb = sa + A_STAGE;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk) {
+                    // K step of 16 = chunks 2kk, 2kk+1: LBO = one chunk (rows x 16 B), SBO = 128 B
+                    const uint64_t ad = ste_desc(sa + t * A_TERM + kk * 2 * BM * 16, BM * 16, 128);
+                    const uint64_t bd = ste_desc(sbb + kk * 2 * BN * 16, BN * 16, 128);
+                    const uint32_t acc = (s > 0 || t > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                                 "l"(ad), "l"(bd), "r"(IDESC), "r"(acc)
+                                 : "memory");
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             bar + 8 * buf) : "memory");
+        }
+        if (s + 1 < nst) {
+            if (s >= 1) {   // buffer buf ^ 1 was read by the MMAs of stage s - 1
+                asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                             "@!p bra W_%=;\n}\n" ::"r"(bar + 8 * (buf ^ 1)), "r"(mma_phase[buf ^ 1]) : "memory");
+                mma_phase[buf ^ 1] ^= 1u;
+            }
+            stage(buf ^ 1, kb + (int64_t)(s + 1) * BK);
+        }
+    }
+    // wait for the last MMAs (and the one before it, if its barrier phase is still pending)
+    if (nst >= 2) {
+        const int b2 = (nst - 2) & 1;
+        asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                     "@!p bra W_%=;\n}\n" ::"r"(bar + 8 * b2), "r"(mma_phase[b2]) : "memory");
+        mma_phase[b2] ^= 1u;
+    }
+    if (nst >= 1) {
+        const int b1 = (nst - 1) & 1;
+        asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                     "@!p bra W_%=;\n}\n" ::"r"(bar + 8 * b1), "r"(mma_phase[b1]) : "memory");
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // ---- epilogue: thread tid owns row m0 + tid (TMEM lane tid) ----
+    const int64_t i = m0 + tid;
+    const float cl = (R && !split) ? (clip_vec ? (i < M ? clip[i] : 0.f) : *clip) : 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (i >= M) continue;
+        if (nst == 0) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = 0u;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int64_t j = n0 + c0 + e;
+            if (j >= N) continue;
+            float x = __uint_as_float(v[e]);
+            if (!PCS) x = __fmul_rn(x, sb);
+            if (R && !split && !(fabsf(R[i * ldr + j]) <= cl)) x = 0.f;   // STE: outside the clip range
+            C[i * ldc + j] = x;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(BN) : "memory");
+}
+
+// C[i] = mask(i) * sum_{z < S} part[z][i], the splits added in order (deterministic); clip_vec:
+// the clip is per row (clip[i / N], a per-channel weight clip), else one scalar
 __global__ void ste_reduce_kernel(int S, int64_t MN, int64_t N, const float* __restrict__ part,
                                   float* __restrict__ C, const float* __restrict__ R,
-                                  const float* __restrict__ clip) {
-    const float cl = R ? *clip : 0.f;
+                                  const float* __restrict__ clip, int clip_vec) {
+    const float cl0 = (R && !clip_vec) ? *clip : 0.f;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
         float v = part[i];
         for (int z = 1; z < S; ++z) v = __fadd_rn(v, part[(int64_t)z * MN + i]);
-        if (R && !(fabsf(R[i]) <= cl)) v = 0.f;
+        if (R && !(fabsf(R[i]) <= (clip_vec ? clip[i / N] : cl0))) v = 0.f;
         C[i] = v;
     }
 }
@@ -178,28 +381,62 @@ __global__ void ste_colsum_kernel(int64_t M, int64_t N, const float* __restrict_
 
 
 namespace axq {
-// One STE product C[Mg][Ng] = mask * A(Mg x Kg) . fq(B[Kg][ldb]) (R: mask operand [Mg][Ng] or null):
-// split K (deterministic, through the workspace) until ~2 CTAs per SM
+// One STE product C[Mg][Ng] = mask * A(Mg x Kg) . fq(B[Kg][ldb]) (R: mask operand [Mg][Ng] or null)
+// on the tensor cores (ste_tc_kernel); sB_vec: the scale is per summed index p (per-channel
+// weight scales of gx), else one scalar; clip_vec: the clip is per output row i (per-channel
+// weight clip of gw).  Split K (deterministic, through the workspace) until ~2 CTAs per SM.
 static void ste_product(bool ta, int64_t Mg, int64_t Ng, int64_t Kg, const float* A, int64_t lda,
-                        const int8_t* B, int64_t ldb, const float* sB, float* C, int64_t ldc, const float* R,
-                        const float* clip, float* workspace, int64_t workspace_elems, cudaStream_t st) {
+                        const int8_t* B, int64_t ldb, const float* sB, bool sB_vec, float* C, int64_t ldc,
+                        const float* R, const float* clip, bool clip_vec, float* workspace, int64_t workspace_elems,
+                        cudaStream_t st) {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = ((Ng + ste::BN - 1) / ste::BN) * ((Mg + ste::BM - 1) / ste::BM);
+    static unsigned configured = 0;
+    if (!(configured & (1u << (dev & 31)))) {
+        cudaFuncSetAttribute(ste_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, stetc::SMEM);
+        cudaFuncSetAttribute(ste_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, stetc::SMEM);
+        cudaFuncSetAttribute(ste_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, stetc::SMEM);
+        cudaFuncSetAttribute(ste_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, stetc::SMEM);
+        configured |= 1u << (dev & 31);
+    }
+    static const bool simt = std::getenv("AXQ_STE_SIMT") != nullptr;   // A/B: the fp32 SIMT GEMM
+    if (simt && !sB_vec && !clip_vec && (Mg + ste::BM - 1) / ste::BM <= 65535) {
+        const int64_t t2 = ((Ng + ste::BN - 1) / ste::BN) * ((Mg + ste::BM - 1) / ste::BM);
+        int64_t S2 = std::min<int64_t>({(2 * (int64_t)sms + t2 - 1) / t2, 128, std::max<int64_t>(1, Kg / 64)});
+        S2 = workspace ? std::min<int64_t>(S2, workspace_elems / std::max<int64_t>(1, Mg * ldc)) : 1;
+        if (S2 < 2) S2 = 1;
+        const int64_t kc2 = ((Kg + S2 - 1) / S2 + ste::BK - 1) / ste::BK * ste::BK;
+        S2 = (Kg + kc2 - 1) / kc2;
+        dim3 g2((unsigned)((Ng + ste::BN - 1) / ste::BN), (unsigned)((Mg + ste::BM - 1) / ste::BM), (unsigned)S2);
+        float* o2 = S2 > 1 ? workspace : C;
+        if (ta) ste_gemm_kernel<true><<<g2, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, o2, ldc, R, ldc, clip, kc2);
+        else ste_gemm_kernel<false><<<g2, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, o2, ldc, R, ldc, clip, kc2);
+        if (S2 > 1)
+            ste_reduce_kernel<<<(unsigned)std::min<int64_t>((Mg * ldc + 255) / 256, 8 * sms), 256, 0, st>>>(
+                (int)S2, Mg * ldc, Ng, workspace, C, R, clip, 0);
+        return;
+    }
+    const int64_t tiles = ((Ng + stetc::BN - 1) / stetc::BN) * ((Mg + stetc::BM - 1) / stetc::BM);
     // (a conv's weight gradient sums over all N*Ho*Wo positions into a few tiles: up to 128 slices)
-    int64_t S = std::min<int64_t>({(2 * (int64_t)sms + tiles - 1) / tiles, 128, std::max<int64_t>(1, Kg / 64)});
+    int64_t S = std::min<int64_t>({(2 * (int64_t)sms + tiles - 1) / tiles, 128, std::max<int64_t>(1, Kg / 128)});
     S = workspace ? std::min<int64_t>(S, workspace_elems / std::max<int64_t>(1, Mg * ldc)) : 1;
     if (S < 2) S = 1;
-    const int64_t kc = ((Kg + S - 1) / S + ste::BK - 1) / ste::BK * ste::BK;
+    const int64_t kc = ((Kg + S - 1) / S + stetc::BK - 1) / stetc::BK * stetc::BK;
     S = (Kg + kc - 1) / kc;
-    dim3 grid((unsigned)((Ng + ste::BN - 1) / ste::BN), (unsigned)((Mg + ste::BM - 1) / ste::BM), (unsigned)S);
+    dim3 grid((unsigned)((Mg + stetc::BM - 1) / stetc::BM), (unsigned)((Ng + stetc::BN - 1) / stetc::BN), (unsigned)S);
     float* out = S > 1 ? workspace : C;
-    if (ta) ste_gemm_kernel<true><<<grid, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, kc);
-    else ste_gemm_kernel<false><<<grid, ste::NT, 0, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, kc);
+    const int cv = clip_vec ? 1 : 0;
+    if (ta) {
+        if (sB_vec) ste_tc_kernel<true, true><<<grid, stetc::NT, stetc::SMEM, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, cv, kc);
+        else ste_tc_kernel<true, false><<<grid, stetc::NT, stetc::SMEM, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, cv, kc);
+    } else {
+        if (sB_vec) ste_tc_kernel<false, true><<<grid, stetc::NT, stetc::SMEM, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, cv, kc);
+        else ste_tc_kernel<false, false><<<grid, stetc::NT, stetc::SMEM, st>>>(Mg, Ng, Kg, A, lda, B, ldb, sB, out, ldc, R, ldc, clip, cv, kc);
+    }
     if (S > 1)
         ste_reduce_kernel<<<(unsigned)std::min<int64_t>((Mg * ldc + 255) / 256, 8 * sms), 256, 0, st>>>(
-            (int)S, Mg * ldc, Ng, workspace, C, R, clip);
+            (int)S, Mg * ldc, Ng, workspace, C, R, clip, cv);
 }
 
 // gb = column sums of gy [M][N]: two deterministic passes through the workspace when M is large
@@ -247,14 +484,16 @@ __global__ void ste_col2im_kernel(int64_t total, int H, int W, int C, int R, int
 }
 }  // namespace axq
 
-extern "C" axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float* gy,
-                                              const int8_t* qa, const float* d_scale_a, const float* x,
-                                              const float* d_clip_a, const int8_t* qw,
-                                              const float* d_scale_w, const float* w,
-                                              const float* d_clip_w, float* gx, float* gw, float* gb,
-                                              float* workspace, int64_t workspace_elems, void* stream) {
+extern "C" axq_status axq_ste_linear_backward_pc(int64_t M, int64_t N, int64_t K, const float* gy,
+                                                 const int8_t* qa, const float* d_scale_a, const float* x,
+                                                 const float* d_clip_a, const int8_t* qw,
+                                                 const float* d_scale_w, const float* d_scale_w_ch,
+                                                 const float* w, const float* d_clip_w,
+                                                 const float* d_clip_w_ch, float* gx, float* gw, float* gb,
+                                                 float* workspace, int64_t workspace_elems, void* stream) {
     using namespace axq;
     if (M < 0 || N < 0 || K < 0) return AXQ_ERR_INVALID;
+    if (M >= ((int64_t)1 << 40) || N >= ((int64_t)1 << 40) || K >= ((int64_t)1 << 40)) return AXQ_ERR_INVALID;
     if (M == 0 || N == 0) {   // empty sums: every gradient that exists is zero
         cudaStream_t st = (cudaStream_t)stream;
         cudaError_t e = cudaSuccess;
@@ -264,25 +503,46 @@ extern "C" axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, c
         return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
     }
     if (!gy) return AXQ_ERR_INVALID;
-    if (gx && (!qw || !d_scale_w || (x && !d_clip_a))) return AXQ_ERR_INVALID;
-    if (gw && (!qa || !d_scale_a || (w && !d_clip_w))) return AXQ_ERR_INVALID;
+    const float* sw = d_scale_w_ch ? d_scale_w_ch : d_scale_w;
+    const float* cw = d_clip_w_ch ? d_clip_w_ch : d_clip_w;
+    if (gx && (!qw || !sw || (x && !d_clip_a))) return AXQ_ERR_INVALID;
+    if (gw && (!qa || !d_scale_a || (w && !cw))) return AXQ_ERR_INVALID;
+    if ((K + 127) / 128 > 65535 || (N + 127) / 128 > 65535) return AXQ_ERR_UNSUPPORTED;   // column tiles: grid.y
     cudaStream_t st = (cudaStream_t)stream;
-    if (gx && K > 0) ste_product(false, M, K, N, gy, N, qw, K, d_scale_w, gx, K, x, d_clip_a, workspace, workspace_elems, st);
-    if (gw && K > 0) ste_product(true, N, K, M, gy, N, qa, K, d_scale_a, gw, K, w, d_clip_w, workspace, workspace_elems, st);
+    if (gx && K > 0)
+        ste_product(false, M, K, N, gy, N, qw, K, sw, d_scale_w_ch != nullptr, gx, K, x, d_clip_a, false, workspace,
+                    workspace_elems, st);
+    if (gw && K > 0)
+        ste_product(true, N, K, M, gy, N, qa, K, d_scale_a, false, gw, K, w, cw, d_clip_w_ch != nullptr, workspace,
+                    workspace_elems, st);
     if (gb) ste_colsum(M, N, gy, gb, workspace, workspace_elems, st);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
 }
 
+extern "C" axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float* gy,
+                                              const int8_t* qa, const float* d_scale_a, const float* x,
+                                              const float* d_clip_a, const int8_t* qw,
+                                              const float* d_scale_w, const float* w,
+                                              const float* d_clip_w, float* gx, float* gw, float* gb,
+                                              float* workspace, int64_t workspace_elems, void* stream) {
+    return axq_ste_linear_backward_pc(M, N, K, gy, qa, d_scale_a, x, d_clip_a, qw, d_scale_w, nullptr, w, d_clip_w,
+                                      nullptr, gx, gw, gb, workspace, workspace_elems, stream);
+}
+
 // NEXT-4 for convolution (groups = 1, dilation 1): the STE backward through the explicit im2col
 // of the forward's codes (the conv is the GEMM of its im2col matrix), see include/axq.h.
-extern "C" axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const float* gy, const int8_t* qx,
-                                              const float* d_scale_a, const float* x, const float* d_clip_a,
-                                              const int8_t* qw, const float* d_scale_w, const float* w,
-                                              const float* d_clip_w, float* gx, float* gw, float* gb,
-                                              int8_t* cols, int64_t ldcols, float* gcols, float* workspace,
-                                              int64_t workspace_elems, void* stream) {
+extern "C" axq_status axq_ste_conv2d_backward_pc(const axq_conv_desc* d, const float* gy, const int8_t* qx,
+                                                 const float* d_scale_a, const float* x, const float* d_clip_a,
+                                                 const int8_t* qw, const float* d_scale_w,
+                                                 const float* d_scale_w_ch, const float* w,
+                                                 const float* d_clip_w, const float* d_clip_w_ch, float* gx,
+                                                 float* gw, float* gb, int8_t* cols, int64_t ldcols,
+                                                 float* gcols, float* workspace, int64_t workspace_elems,
+                                                 void* stream) {
     using namespace axq;
+    const float* sw = d_scale_w_ch ? d_scale_w_ch : d_scale_w;
+    const float* cw = d_clip_w_ch ? d_clip_w_ch : d_clip_w;
     if (!d || d->groups != 1 || d->dil_h != 1 || d->dil_w != 1 || (d->c_valid && d->c_valid != d->C) ||
         d->N < 0 || d->H <= 0 || d->W <= 0 || d->C <= 0 || d->K <= 0 || d->R <= 0 || d->S <= 0 ||
         d->stride_h <= 0 || d->stride_w <= 0 || d->pad_h < 0 || d->pad_w < 0)
@@ -292,8 +552,9 @@ extern "C" axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const floa
     const int64_t M = d->N * Ho * Wo, Kc = d->R * d->S * d->C, No = d->K;
     if (M >= ((int64_t)1 << 31) || d->N * d->H * d->W * d->C >= ((int64_t)1 << 40)) return AXQ_ERR_INVALID;
     if (!gy && M > 0) return AXQ_ERR_INVALID;
-    if (gw && (!qx || !d_scale_a || !cols || ldcols < Kc || (ldcols & 15) || (w && !d_clip_w))) return AXQ_ERR_INVALID;
-    if (gx && (!qw || !d_scale_w || !gcols || (x && !d_clip_a))) return AXQ_ERR_INVALID;
+    if (gw && (!qx || !d_scale_a || !cols || ldcols < Kc || (ldcols & 15) || (w && !cw))) return AXQ_ERR_INVALID;
+    if (gx && (!qw || !sw || !gcols || (x && !d_clip_a))) return AXQ_ERR_INVALID;
+    if ((Kc + 127) / 128 > 65535 || (No + 127) / 128 > 65535) return AXQ_ERR_UNSUPPORTED;   // column tiles
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
     if (M == 0) {   // empty sums
@@ -306,12 +567,12 @@ extern "C" axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const floa
         const axq_status r = axq_im2col_nhwc_i8(qx, d->N, d->H, d->W, d->C, 0, d->R, d->S, d->stride_h, d->stride_w,
                                                 d->pad_h, d->pad_w, cols, ldcols, stream);
         if (r != AXQ_OK) return r;
-        ste_product(true, No, Kc, M, gy, No, cols, ldcols, d_scale_a, gw, Kc, w, d_clip_w, workspace,
-                    workspace_elems, st);
+        ste_product(true, No, Kc, M, gy, No, cols, ldcols, d_scale_a, false, gw, Kc, w, cw, d_clip_w_ch != nullptr,
+                    workspace, workspace_elems, st);
     }
     if (gx) {   // gcols = gy . fq(W) [M][(r, s, c)], then the adjoint of im2col, masked
-        ste_product(false, M, Kc, No, gy, No, qw, Kc, d_scale_w, gcols, Kc, nullptr, nullptr, workspace,
-                    workspace_elems, st);
+        ste_product(false, M, Kc, No, gy, No, qw, Kc, sw, d_scale_w_ch != nullptr, gcols, Kc, nullptr, nullptr, false,
+                    workspace, workspace_elems, st);
         const int64_t total = d->N * d->H * d->W * d->C;
         int sms = 148, dev = 0;
         cudaGetDevice(&dev);
@@ -323,4 +584,14 @@ extern "C" axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const floa
     if (gb) ste_colsum(M, No, gy, gb, workspace, workspace_elems, st);
     e = cudaGetLastError();
     return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
+}
+
+extern "C" axq_status axq_ste_conv2d_backward(const axq_conv_desc* d, const float* gy, const int8_t* qx,
+                                              const float* d_scale_a, const float* x, const float* d_clip_a,
+                                              const int8_t* qw, const float* d_scale_w, const float* w,
+                                              const float* d_clip_w, float* gx, float* gw, float* gb,
+                                              int8_t* cols, int64_t ldcols, float* gcols, float* workspace,
+                                              int64_t workspace_elems, void* stream) {
+    return axq_ste_conv2d_backward_pc(d, gy, qx, d_scale_a, x, d_clip_a, qw, d_scale_w, nullptr, w, d_clip_w, nullptr,
+                                      gx, gw, gb, cols, ldcols, gcols, workspace, workspace_elems, stream);
 }

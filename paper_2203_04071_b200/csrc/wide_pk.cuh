@@ -13,7 +13,7 @@
 // slab BM times (2048 rows at b = 11, 12), which is what bounds the L2 -> shared traffic.
 //
 //  * Per-stage slab: KS k x NQ quads x 2^b codes x 8 B = 64 KiB (b = 12: KS 2, NQ 1; b = 11:
-//    KS 4, NQ 1; b = 10: KS 4, NQ 2; b = 9: KS 4, NQ 4), double-buffered, with the tile's
+//    KS 4, NQ 1; b = 10: KS 4, NQ 2; b = 9: KS 4, NQ 4), three stages in flight, with the tile's
 //    packed weights; one producer warp issues the bulk copies (mbarrier complete_tx), 16
 //    consumer warps look up (lanes = rows, R = 4 / NQ rows per lane).
 //  * E sums: biased 16-bit lanes of a 32-bit word v (columns 2i, 2i+1) accumulated as
@@ -46,7 +46,7 @@ struct Geo {
     static constexpr int KS = 65536 / (NQ * TQB);
     static constexpr int TBL_STAGE = KS * NQ * TQB;              // 64 KiB
     static constexpr int W_STAGE = KS * NQ * 8;                  // packed int16 weights
-    static constexpr int STAGES = 2;
+    static constexpr int STAGES = 3;
     static constexpr int SMEM_W = STAGES * TBL_STAGE;
     static constexpr int SMEM_BAR = SMEM_W + ((STAGES * W_STAGE + 15) / 16) * 16;
     static constexpr int SMEM_BYTES = SMEM_BAR + 8 * 2 * STAGES;
@@ -128,53 +128,54 @@ __global__ void __launch_bounds__(wpk::NT, 1) lut_widepk_kernel(const __grid_con
                 for (int j = 0; j < 4; ++j) ex[r][q][j] = 0;
             }
         uint4 acode[R];
-        for (int st = 0; st < nst; ++st, ++item) {
-            const int k0 = st * KS;
-            if ((k0 & 7) == 0) {       // 8 codes per row, zero beyond K (padded k: a = 0)
+        for (int k8 = 0; k8 < (int)P.Kp; k8 += 8) {
+            // 8 codes per row, zero beyond K (a padded k looks up a = 0)
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int16_t* src = P.A + (valid[r] ? mrow[r] : 0) * P.lda + k0;
-                    if (valid[r] && k0 + 8 <= P.K && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-                        acode[r] = __ldg(reinterpret_cast<const uint4*>(src));
-                    } else {
-                        uint32_t w[4] = {0u, 0u, 0u, 0u};
-                        for (int j = 0; j < 8; ++j)
-                            if (valid[r] && k0 + j < P.K) w[j >> 1] |= (uint32_t)(uint16_t)src[j] << (16 * (j & 1));
-                        acode[r] = make_uint4(w[0], w[1], w[2], w[3]);
-                    }
+            for (int r = 0; r < R; ++r) {
+                const int16_t* src = P.A + (valid[r] ? mrow[r] : 0) * P.lda + k8;
+                if (valid[r] && k8 + 8 <= P.K && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+                    acode[r] = __ldg(reinterpret_cast<const uint4*>(src));
+                } else {
+                    uint32_t w[4] = {0u, 0u, 0u, 0u};
+                    for (int j = 0; j < 8; ++j)
+                        if (valid[r] && k8 + j < P.K) w[j >> 1] |= (uint32_t)(uint16_t)src[j] << (16 * (j & 1));
+                    acode[r] = make_uint4(w[0], w[1], w[2], w[3]);
                 }
             }
-            const int buf = (int)(item % STAGES);
-            mbar_wait(bar_full + 8 * buf, (item / STAGES) & 1u);
-            const uint8_t* tb = wpk_smem + buf * G::TBL_STAGE;
-            const uint8_t* wb = wpk_smem + G::SMEM_W + buf * G::W_STAGE;
 #pragma unroll
-            for (int kk = 0; kk < KS; ++kk) {
-                const int kc = (k0 & 7) + kk;                  // code slot within the 8 loaded
+            for (int sub = 0; sub < 8 / KS; ++sub, ++item) {
+                const int buf = (int)(item % STAGES);
+                mbar_wait(bar_full + 8 * buf, (item / STAGES) & 1u);
+                const uint8_t* tb = wpk_smem + buf * G::TBL_STAGE;
+                const uint8_t* wb = wpk_smem + G::SMEM_W + buf * G::W_STAGE;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const uint2 wv = *reinterpret_cast<const uint2*>(wb + (kk * NQ + q) * 8);   // broadcast
-                    const int w0 = (int)(int16_t)(wv.x & 0xffffu), w1 = (int)(int16_t)(wv.x >> 16);
-                    const int w2 = (int)(int16_t)(wv.y & 0xffffu), w3 = (int)(int16_t)(wv.y >> 16);
+                for (int kk = 0; kk < KS; ++kk) {
+                    const int kc = sub * KS + kk;              // code slot (compile-time after unrolling)
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const uint32_t cw = kc < 2 ? acode[r].x : kc < 4 ? acode[r].y : kc < 6 ? acode[r].z : acode[r].w;
-                        const int a = (int)(int16_t)((kc & 1) ? (cw >> 16) : (cw & 0xffffu));
-                        const uint32_t ua = (uint32_t)a & mask;
-                        const uint2 v = *reinterpret_cast<const uint2*>(tb + ((kk * NQ + q) * G::NCODES + ua) * 8);
-                        pa[r][q][0] += v.x;
-                        ph[r][q][0] += v.x >> 16;
-                        pa[r][q][1] += v.y;
-                        ph[r][q][1] += v.y >> 16;
-                        ex[r][q][0] += a * w0;
-                        ex[r][q][1] += a * w1;
-                        ex[r][q][2] += a * w2;
-                        ex[r][q][3] += a * w3;
+                    for (int q = 0; q < NQ; ++q) {
+                        const uint2 wv = *reinterpret_cast<const uint2*>(wb + (kk * NQ + q) * 8);   // broadcast
+                        const int w0 = (int)(int16_t)(wv.x & 0xffffu), w1 = (int)(int16_t)(wv.x >> 16);
+                        const int w2 = (int)(int16_t)(wv.y & 0xffffu), w3 = (int)(int16_t)(wv.y >> 16);
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const uint32_t cw = kc < 2 ? acode[r].x : kc < 4 ? acode[r].y : kc < 6 ? acode[r].z : acode[r].w;
+                            const int a = (int)(int16_t)((kc & 1) ? (cw >> 16) : (cw & 0xffffu));
+                            const uint32_t ua = (uint32_t)a & mask;
+                            const uint2 v = *reinterpret_cast<const uint2*>(tb + ((kk * NQ + q) * G::NCODES + ua) * 8);
+                            pa[r][q][0] += v.x;
+                            ph[r][q][0] += v.x >> 16;
+                            pa[r][q][1] += v.y;
+                            ph[r][q][1] += v.y >> 16;
+                            ex[r][q][0] += a * w0;
+                            ex[r][q][1] += a * w1;
+                            ex[r][q][2] += a * w2;
+                            ex[r][q][3] += a * w3;
+                        }
                     }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_empty + 8 * buf);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_empty + 8 * buf);
         }
         // ---- epilogue: E sums decoded, bias and padded lookups removed ----
         const int32_t corr = (int32_t)(32768 * P.Kp + (P.Kp - P.K) * (int64_t)P.t00);

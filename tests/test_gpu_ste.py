@@ -127,3 +127,96 @@ def test_ste_conv_backward(ax, shape, masked):
         assert np.isfinite(got).all()
         err = np.abs(got.astype(np.float64) - r.astype(np.float64))
         assert (err <= _bound(n, a_.astype(np.float64), r)).all(), float(err.max())
+
+
+@pytest.mark.parametrize("M,N,K", [(96, 40, 70), (300, 129, 257)])
+@pytest.mark.parametrize("masked", [False, True])
+def test_ste_backward_per_channel(ax, M, N, K, masked):
+    """Per-output-channel weight scales and clips (axq_ste_linear_backward_pc)."""
+    x = datagen.normal(65, M, (M, K))
+    W = datagen.normal(65, N, (N, K), 0.05) * np.linspace(0.3, 2.5, N, dtype=np.float32)[:, None]
+    qa, sa = oracle.quantize_tensor(x, 8)
+    amax_ch = np.abs(W).max(axis=1).astype(np.float32)
+    sw = (amax_ch / np.float32(127)).astype(np.float32)
+    qw = np.clip(np.rint(W / sw[:, None]), -127, 127).astype(np.int8)
+    gy = datagen.normal(65, 3, (M, N))
+    clip_a = np.float32(np.quantile(np.abs(x), 0.8))
+    clip_w = (amax_ch * np.float32(0.7)).astype(np.float32)
+    if masked:
+        ref = oracle.ste_linear_backward(gy, qa, sa, qw, sw, x, clip_a, W, clip_w)
+    else:
+        ref = oracle.ste_linear_backward(gy, qa, sa, qw, sw)
+    gx = torch.full((M, K), np.nan, device=DEV)
+    gw = torch.full((N, K), np.nan, device=DEV)
+    f = lambda v: _t(np.atleast_1d(np.asarray(v, dtype=np.float32)))
+    kw = dict(x=_t(x), d_clip_a=f(clip_a), w=_t(W), d_clip_w=f(clip_w)) if masked else {}
+    ax.axq_ste_linear_backward(_t(gy), _t(qa), f(sa), _t(qw), f(sw), gx=gx, gw=gw, **kw)
+    torch.cuda.synchronize()
+    wf = np.abs(oracle.fake_quant(qw, sw)).astype(np.float64)
+    xf = np.abs(oracle.fake_quant(qa, sa)).astype(np.float64)
+    ag = np.abs(gy).astype(np.float64)
+    for got, r, n, absprod in ((gx, ref[0], N, ag @ wf), (gw, ref[1], M, ag.T @ xf)):
+        got = got.cpu().numpy()
+        err = np.abs(got.astype(np.float64) - r.astype(np.float64))
+        assert (err <= _bound(n, absprod, r)).all(), float(err.max())
+        if masked:
+            assert ((got == 0) == (r == 0)).all()
+
+
+def test_ste_backward_large_m_workspace(ax):
+    """M >= 4096 with a workspace: the two-pass deterministic column sums and the split-K
+    products (the benchmarked paths)."""
+    _check(ax, 5000, 96, 80, 77, True, True)
+
+
+@pytest.mark.parametrize("masked", [False, True])
+def test_ste_conv_backward_workspace_large_m(ax, masked):
+    """A conv with N*Ho*Wo = 6272 positions and a workspace: gw split over up to 128 slices."""
+    N, C, H, W, K, R, S, st, pd = 8, 32, 28, 28, 32, 3, 3, 1, 1
+    x = datagen.normal(95, 1, (N, H, W, C))
+    wt = datagen.normal(95, 2, (K, R, S, C), 0.2)
+    qx, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(wt, 8)
+    gy = datagen.normal(95, 3, (N, H, W, K))
+    clip_a = np.float32(np.quantile(np.abs(x), 0.8)) if masked else None
+    clip_w = np.float32(np.quantile(np.abs(wt), 0.8)) if masked else None
+    mk = dict(x=x, clip_a=clip_a, w=wt, clip_w=clip_w) if masked else {}
+    ref = oracle.ste_conv2d_backward(gy, qx, sa, qw, sw, (st, st), (pd, pd), **mk)
+    absref = oracle.ste_conv2d_backward(np.abs(gy), np.abs(qx.astype(np.int64)).astype(np.int8), sa,
+                                        np.abs(qw.astype(np.int64)).astype(np.int8), sw, (st, st), (pd, pd))
+    f = lambda v: _t(np.array([v], dtype=np.float32))
+    d = ax.conv_desc(N, H, W, C, K, R, S, (st, st), (pd, pd))
+    gx = torch.full((N, H, W, C), np.nan, device=DEV)
+    gw = torch.full((K, R, S, C), np.nan, device=DEV)
+    gb = torch.full((K,), np.nan, device=DEV)
+    ws = torch.full((64 * 1024 * 1024 // 4,), np.nan, device=DEV)
+    kw = dict(x=_t(x), d_clip_a=f(clip_a), w=_t(wt), d_clip_w=f(clip_w)) if masked else {}
+    ax.axq_ste_conv2d_backward(d, _t(gy), _t(qx), f(sa), _t(qw), f(sw), gx=gx, gw=gw, gb=gb, workspace=ws, **kw)
+    torch.cuda.synchronize()
+    M = N * H * W
+    for got, r, a_, n in ((gx, ref[0], absref[0], K * R * S), (gw, ref[1], absref[1], M), (gb, ref[2], absref[2], M)):
+        got = got.cpu().numpy()
+        assert np.isfinite(got).all()
+        err = np.abs(got.astype(np.float64) - r.astype(np.float64))
+        assert (err <= _bound(n, a_.astype(np.float64), r)).all(), float(err.max())
+
+
+def test_ste_binding_checks_and_strided_grad(ax):
+    """The binding makes a strided / expanded gradient contiguous (autograd's stride-0 gy after
+    y.sum()) and rejects mismatched shapes instead of letting the kernel write out of bounds."""
+    M, N, K = 40, 24, 16
+    x = datagen.normal(66, 1, (M, K))
+    W = datagen.normal(66, 2, (N, K), 0.05)
+    qa, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(W, 8)
+    gy = torch.ones(1, 1, device=DEV).expand(M, N)              # stride 0
+    ref = oracle.ste_linear_backward(np.ones((M, N), np.float32), qa, sa, qw, sw)
+    gx = torch.empty(M, K, device=DEV)
+    f = lambda v: _t(np.array([v], dtype=np.float32))
+    ax.axq_ste_linear_backward(gy, _t(qa), f(sa), _t(qw), f(sw), gx=gx)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(gx.cpu().numpy(), ref[0], rtol=1e-5, atol=1e-6)
+    with pytest.raises(ValueError):
+        ax.axq_ste_linear_backward(gy, _t(qa), f(sa), _t(qw[:, :8]), f(sw), gx=gx)
+    with pytest.raises(ValueError):
+        ax.axq_ste_linear_backward(gy, _t(qa), f(sa), _t(qw), f(sw), gx=torch.empty(M, K + 1, device=DEV))

@@ -110,3 +110,32 @@ def test_ste_conv_1x1_equals_linear():
     np.testing.assert_allclose(gx.reshape(-1, C), lx, rtol=1e-6, atol=1e-9)
     np.testing.assert_allclose(gw.reshape(K, C), lw, rtol=1e-6, atol=1e-9)
     np.testing.assert_array_equal(gb, lb)
+
+
+@pytest.mark.parametrize("M,N,K", [(6, 5, 9), (17, 12, 33)])
+def test_ste_per_channel_weights_match_autograd(M, N, K):
+    """Per-output-channel weight scales and clips ("weight ranges are per channel"; the
+    layers of the paper's quantizer, NEXT-1): the gradients are those of y = fq(qa) fq_ch(qw)^T
+    with fq_ch(qw)[n] = fl32(s_w[n] * qw[n]) built here with torch, masked per row by
+    |w[n][k]| <= clip_w[n]."""
+    x = datagen.normal(80 + M, 1, (M, K))
+    W = datagen.normal(80 + M, 2, (N, K), 0.05) * np.linspace(0.2, 3.0, N, dtype=np.float32)[:, None]
+    qa, sa = oracle.quantize_tensor(x, 8)
+    amax_ch = np.abs(W).max(axis=1).astype(np.float32)
+    sw_ch = (amax_ch / np.float32(127)).astype(np.float32)
+    qw = np.clip(np.rint(W / sw_ch[:, None]), -127, 127).astype(np.int8)
+    gy = datagen.normal(80 + M, 3, (M, N))
+    clip_w = (amax_ch * np.float32(0.6)).astype(np.float32)
+    xf = torch.tensor(oracle.fake_quant(qa, sa), dtype=torch.float64, requires_grad=True)
+    wf32 = torch.from_numpy(qw).float() * torch.from_numpy(sw_ch)[:, None]        # fl32 per row
+    wf = wf32.double().requires_grad_(True)
+    torch.nn.functional.linear(xf, wf).backward(torch.tensor(gy, dtype=torch.float64))
+    gx, gw, gb = oracle.ste_linear_backward(gy, qa, sa, qw, sw_ch, w=W, clip_w=clip_w)
+    np.testing.assert_allclose(gx, xf.grad.numpy().astype(np.float32), rtol=2e-7, atol=1e-9)
+    keep = np.abs(W) <= clip_w[:, None]
+    assert keep.any() and (~keep).any()
+    ref_gw = np.where(keep, wf.grad.numpy(), 0.0).astype(np.float32)
+    np.testing.assert_allclose(gw, ref_gw, rtol=2e-7, atol=1e-9)
+    # a per-channel scale is not the per-tensor one: using s_w[0] for every row changes gx
+    gx1, _, _ = oracle.ste_linear_backward(gy, qa, sa, qw, sw_ch[0])
+    assert np.abs(gx1 - gx).max() > 1e-3 * np.abs(gx).max()
