@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(ste::NT) ste_gemm_kernel(int64_t M, int64_t N,
 // one TMEM lane (row i) in the epilogue.
 // ---------------------------------------------------------------------------------------
 namespace stetc {
-constexpr int BM = 128, BN = 128, BK = 32, NT = 128;
+constexpr int BM = 128, BN = 128, BK = 32, NT = 256;
 constexpr int A_TERM = BM * BK * 2;               // one bf16 term of the A tile: 8 KiB
 constexpr int A_STAGE = 3 * A_TERM;               // hi, mid, lo
 constexpr int B_STAGE = BN * BK * 2;              // 8 KiB
@@ -203,25 +203,36 @@ __global__ void __launch_bounds__(stetc::NT) ste_tc_kernel(int64_t M, int64_t N,
 
     // operand staging of the p-range [k0, k0 + 32) into stage buffer `buf`: thread t converts
     // row t of A (3 bf16 terms) and column t of B, 4 chunks of 8 p each
+    // two threads per row / column: thread (row, half) converts the K chunks 2 half, 2 half + 1
+    const int row = tid & (BM - 1), half = tid >> 7;
+    const bool avec = !TA && ((lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
     auto stage = [&](int buf, int64_t k0) {
         uint8_t* sa = st_smem + buf * STAGE;
         uint8_t* sbuf = sa + A_STAGE;
-        const int64_t i = m0 + tid, j = n0 + tid;
+        const int64_t i = m0 + row, j = n0 + row;
 #pragma unroll
-        for (int c = 0; c < BK / 8; ++c) {
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c = half * 2 + cc;
+            const int64_t p0 = k0 + c * 8;
             float a[8];
             int8_t q[8];
+            if (avec && i < M && p0 + 8 <= ke) {
+                const float4 f0 = __ldg(reinterpret_cast<const float4*>(A + i * lda + p0));
+                const float4 f1 = __ldg(reinterpret_cast<const float4*>(A + i * lda + p0) + 1);
+                a[0] = f0.x; a[1] = f0.y; a[2] = f0.z; a[3] = f0.w;
+                a[4] = f1.x; a[5] = f1.y; a[6] = f1.z; a[7] = f1.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int64_t p = p0 + e;
+                    a[e] = (p < ke && i < M) ? (TA ? __ldg(A + p * lda + i) : __ldg(A + i * lda + p)) : 0.f;
+                }
+            }
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const int64_t p = k0 + c * 8 + e;
-                const bool pin = p < ke;
-                float v = 0.f;
-                if (pin && i < M) {
-                    v = TA ? A[p * lda + i] : A[i * lda + p];
-                    if (PCS) v = __fmul_rn(v, s_b[p]);       // per-channel scale of the summed index
-                }
-                a[e] = v;
-                q[e] = (pin && j < N) ? B[p * ldb + j] : (int8_t)0;
+                const int64_t p = p0 + e;
+                if (PCS && p < ke) a[e] = __fmul_rn(a[e], __ldg(s_b + p));   // per-channel scale of the summed index
+                q[e] = (p < ke && j < N) ? B[p * ldb + j] : (int8_t)0;
             }
             uint32_t hw[4], mw[4], lw[4], bw[4];
 #pragma unroll
@@ -241,11 +252,11 @@ __global__ void __launch_bounds__(stetc::NT) ste_tc_kernel(int64_t M, int64_t N,
                 lw[e / 2] = (uint32_t)l[0] | ((uint32_t)l[1] << 16);
                 bw[e / 2] = (uint32_t)bf16_rn_bits((float)q[e]) | ((uint32_t)bf16_rn_bits((float)q[e + 1]) << 16);
             }
-            const int off = c * BM * 16 + tid * 16;
+            const int off = c * BM * 16 + row * 16;
             *reinterpret_cast<uint4*>(sa + 0 * A_TERM + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
             *reinterpret_cast<uint4*>(sa + 1 * A_TERM + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
             *reinterpret_cast<uint4*>(sa + 2 * A_TERM + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-            *reinterpret_cast<uint4*>(sbuf + c * BN * 16 + tid * 16) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+            *reinterpret_cast<uint4*>(sbuf + c * BN * 16 + row * 16) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
         }
     };
 
@@ -297,13 +308,14 @@ __global__ void __launch_bounds__(stetc::NT) ste_tc_kernel(int64_t M, int64_t N,
                      "@!p bra W_%=;\n}\n" ::"r"(bar + 8 * b1), "r"(mma_phase[b1]) : "memory");
     }
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    // ---- epilogue: thread tid owns row m0 + tid (TMEM lane tid) ----
-    const int64_t i = m0 + tid;
+    // ---- epilogue: warp w reads TMEM lane quarter w % 4 (rows), column half w / 4 ----
+    const int erow = (warp & 3) * 32 + (tid & 31);
+    const int64_t i = m0 + erow;
     const float cl = (R && !split) ? (clip_vec ? (i < M ? clip[i] : 0.f) : *clip) : 0.f;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = (warp >> 2) * (BN / 2); c0 < (warp >> 2) * (BN / 2) + BN / 2; c0 += 16) {
         uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),

@@ -13,6 +13,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2203_04071_b200 import _lib as ax  # noqa: E402
 
 PEAK = 148 * 128 * 2 * 1.965e9
+# bf16 dense tensor-core peak (MEASURED_PEAKS.json sustained cuBLAS bf16, when present)
+try:
+    BF16 = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] * 1e12
+except Exception:
+    BF16 = 2.25e15
+MMA_TERMS = 3     # the fp32 operand enters as three bf16 terms (hi + mid + lo): 3 MMAs per useful MAC
 
 
 def run(M, N, K):
@@ -41,7 +48,9 @@ def run(M, N, K):
     ms = float(np.median(ts))
     fl = 2 * 2 * M * N * K
     return {"M": M, "N": N, "K": K, "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
-            "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3)}
+            "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3),
+            "frac_bf16_peak_useful": round(fl / (ms * 1e-3) / BF16, 4),
+            "frac_bf16_peak_executed": round(MMA_TERMS * fl / (ms * 1e-3) / BF16, 4)}
 
 
 def run_conv(N, C, H, K, R, st):
@@ -72,7 +81,9 @@ def run_conv(N, C, H, K, R, st):
     ms = float(np.median(ts))
     fl = 2 * 2 * M * K * Kc
     return {"conv": [N, C, H, K, R, st], "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
-            "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3)}
+            "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3),
+            "frac_bf16_peak_useful": round(fl / (ms * 1e-3) / BF16, 4),
+            "frac_bf16_peak_executed": round(MMA_TERMS * fl / (ms * 1e-3) / BF16, 4)}
 
 
 if __name__ == "__main__":
