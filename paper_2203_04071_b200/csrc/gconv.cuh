@@ -196,4 +196,208 @@ __global__ void __launch_bounds__(256) lut_dwconv_kernel(const GConvArgs a) {
     }
 }
 
+// Depthwise 3x3, stride 1, pad 1, delta8 tables (the MobileNet layer): "DW3".  Input-stationary
+// with per-channel packed tables built in shared memory from the resident delta table:
+//   T[c][r][u] = (E[u][w(c,r,0)] + 128) | (E[u][w(c,r,1)] + 128) << 8 | (E[u][w(c,r,2)] + 128) << 16
+//                | u << 24
+// A CTA owns 16 channels (one per warp) and a strip of 32 input columns (30 outputs) of one
+// image.  Input rows are staged 8 at a time into shared memory (coalesced 16-byte pixel reads
+// of the channel block, 20-byte pixel stride: conflict-free byte reads).  Per input row each
+// lane reads its pixel's code u and fetches the 3 words T[c][r][u] (9 lookups in 3 LDS: the
+// three taps of a filter row serve three different outputs).  Output wo needs tap s = 0 / 1 / 2
+// from the lanes wo-1 / wo / wo+1, so each word is shuffled to its neighbours, the three bytes
+// are gathered with two PRMT and summed with one dp4a (byte 3 weighted 0); byte 3 carries the
+// neighbours' codes for the exact part a*w (one signed dp4a per filter row).  Output rows
+// complete one per input row (three rolling accumulators) and go through a shared int32 tile
+// to the fused epilogue with channel-fastest (coalesced) stores.  Padded taps read code 0 and
+// are looked up (A11).
+namespace dw3 {
+constexpr int CB = 16;                     // channels per CTA (one per warp)
+constexpr int NT = CB * 32;
+constexpr int RB = 8;                      // input rows staged per batch
+constexpr int PX = 34;                     // staged pixels per row (32 lanes + 2 spare)
+constexpr int PS = 20;                     // staged pixel stride (bytes): 5 words, conflict-free
+constexpr int QS = 20;                     // code tile pixel stride (bytes)
+constexpr int YS = 17;                     // fp32 tile pixel stride (words)
+constexpr int TAB = CB * 3 * 256 * 4;      // 48 KiB of packed tables
+constexpr int IN = RB * PX * PS;           // one staged batch of input rows
+constexpr int OUT = RB * 30 * CB * 4;      // int32 results (generic epilogue) / fp32 y tile
+constexpr int QT = RB * 30 * QS;           // int8 code tile
+constexpr int SMEM = TAB + IN + OUT + QT;
+}  // namespace dw3
+
+static __global__ void __launch_bounds__(dw3::NT) lut_dw3_kernel(const GConvArgs a) {
+    using namespace dw3;
+    extern __shared__ __align__(16) uint8_t dw3_smem[];
+    uint32_t* tabs = reinterpret_cast<uint32_t*>(dw3_smem);            // [CB][3][256]
+    uint8_t* tin = dw3_smem + TAB;                                      // [RB][PX][PS]
+    int32_t* tout = reinterpret_cast<int32_t*>(dw3_smem + TAB + IN);    // generic: [RB][CB][30]
+    float* ty = reinterpret_cast<float*>(dw3_smem + TAB + IN);          // fast: [RB][30][YS]
+    uint8_t* tq = dw3_smem + TAB + IN + OUT;                            // fast: [RB][30][QS]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int8_t* dtab = reinterpret_cast<const int8_t*>(a.table);      // delta8 [uw][ua]
+    const int c_blocks = (a.C + CB - 1) / CB;
+    const int strips = (a.Wo + 29) / 30;
+    const int64_t items = (int64_t)c_blocks * strips * a.N;
+    float sc = 0.f, s_out = 1.f, qm = 127.f, r_out = 1.f;
+    if (!a.C_out) {
+        sc = __fmul_rn(*a.ep.sa, *a.ep.sw);
+        if (a.ep.q) {
+            s_out = *a.ep.s_out;
+            qm = (float)((1 << (a.ep.bits_out - 1)) - 1);
+            r_out = __frcp_rn(s_out);
+        }
+    }
+    const bool vec16 = (a.C % CB) == 0 && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
+    // the fast epilogue: row-layout (NHWC) fp32 y and / or int8 codes, no residual, whole
+    // 16-channel blocks with 16-byte aligned rows -- computed by the lane that completes the
+    // output, transposed through shared memory, stored 16 bytes per pixel
+    const bool fast = !a.C_out && !a.ep.y_nchw && !a.ep.residual && (a.C % CB) == 0 &&
+                      (!a.ep.y || (((a.ep.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.ep.y) & 15) == 0))) &&
+                      (!a.ep.q || (((a.ep.ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(a.ep.q) & 15) == 0)));
+    // items ordered (channel block, strip) major, image minor: a CTA's consecutive items share
+    // the channel block, so its tables are rebuilt only when the block changes
+    const int64_t per = (items + gridDim.x - 1) / gridDim.x;
+    const int64_t i0 = blockIdx.x * per, i1 = min(items, i0 + per);
+    int built = -1;
+    for (int64_t it = i0; it < i1; ++it) {
+        const int cb = (int)(it / ((int64_t)strips * a.N));
+        const int64_t rem = it - (int64_t)cb * strips * a.N;
+        const int strip = (int)(rem / a.N), n = (int)(rem - (int64_t)strip * a.N);
+        const int c0 = cb * CB;
+        if (cb != built) {
+            __syncthreads();                        // previous item done with the tables
+            for (int e = tid; e < CB * 3 * 256; e += NT) {
+                const int c = c0 + e / 768, r = (e / 256) % 3, u = e & 255;
+                uint32_t v = (uint32_t)u << 24;
+                if (c < a.C) {
+#pragma unroll
+                    for (int s = 0; s < 3; ++s) {
+                        const int w = (int)__ldg(a.W + (int64_t)c * 9 + r * 3 + s);
+                        v |= (uint32_t)(uint8_t)(__ldg(dtab + (((w & 0xff) << 8) | u)) + 128) << (8 * s);
+                    }
+                } else {
+                    v |= 0x808080u;
+                }
+                tabs[e] = v;
+            }
+            built = cb;
+        }
+        const int c = c0 + warp;
+        const bool cvalid = c < a.C;
+        const uint32_t* tab = tabs + warp * 768;
+        uint32_t wr[3] = {0u, 0u, 0u};             // filter rows as signed bytes [w(r,0), w(r,1), w(r,2), 0]
+        if (cvalid) {
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                wr[r] = (uint32_t)(uint8_t)a.W[(int64_t)c * 9 + r * 3] |
+                        ((uint32_t)(uint8_t)a.W[(int64_t)c * 9 + r * 3 + 1] << 8) |
+                        ((uint32_t)(uint8_t)a.W[(int64_t)c * 9 + r * 3 + 2] << 16);
+        }
+        const float sc_c = (!a.C_out && cvalid) ? epi_sc(a.ep, sc, c) : 0.f;
+        const float b_c = (!a.C_out && a.ep.bias && cvalid) ? a.ep.bias[c] : 0.f;
+        const int w0 = strip * 30;                 // first output column of the strip
+        const int ncols = min(30, a.Wo - w0);
+        const int8_t* xb = a.X + (int64_t)n * a.H * a.Wd * a.C + c0;
+        // staging: thread e < RB * PX loads pixel (row e / PX, x = e % PX) of the channel block
+        const int srr = tid / PX, sx = tid - srr * PX;
+        const bool stager = tid < RB * PX;
+        auto fetch = [&](int hb, uint32_t (&v)[4]) {
+            v[0] = v[1] = v[2] = v[3] = 0u;
+            const int hi = hb + srr, wi = w0 - 1 + sx;
+            if (stager && (unsigned)hi < (unsigned)a.H && (unsigned)wi < (unsigned)a.Wd) {
+                const int8_t* src = xb + ((int64_t)hi * a.Wd + wi) * a.C;
+                if (vec16) {
+                    const uint4 q = __ldg(reinterpret_cast<const uint4*>(src));
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+                    for (int j = 0; j < CB; ++j)
+                        if (c0 + j < a.C) v[j >> 2] |= (uint32_t)(uint8_t)src[j] << (8 * (j & 3));
+                }
+            }
+        };
+        uint32_t pf[4];
+        fetch(-1, pf);
+        int acc_n = 0, acc_c = 0, acc_p = 0;       // output rows hi + 1, hi, hi - 1
+        for (int hb = -1; hb <= a.H; hb += RB) {   // batches of input rows hb .. hb + RB - 1
+            if (stager) {
+                uint32_t* dst = reinterpret_cast<uint32_t*>(tin + (srr * PX + sx) * PS);
+                dst[0] = pf[0]; dst[1] = pf[1]; dst[2] = pf[2]; dst[3] = pf[3];
+            }
+            __syncthreads();                        // staged rows visible; last batch's tiles consumed
+            if (hb + RB <= a.H) fetch(hb + RB, pf); // next batch in flight during this one
+#pragma unroll 1
+            for (int rr = 0; rr < RB; ++rr) {
+                const int hi = hb + rr;
+                if (hi > a.H) break;
+                const uint32_t u = tin[(rr * PX + lane) * PS + warp];
+                uint32_t W[3], L[3], Rt[3];
+#pragma unroll
+                for (int r = 0; r < 3; ++r) W[r] = tab[r * 256 + u];
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    L[r] = __shfl_up_sync(0xffffffffu, W[r], 1);
+                    Rt[r] = __shfl_down_sync(0xffffffffu, W[r], 1);
+                }
+                // neighbours' codes (byte 3): [a(wo-1), a(wo), a(wo+1), x]
+                const uint32_t codes = __byte_perm(__byte_perm(L[0], W[0], 0x7773u), Rt[0], 0x7710u);
+                // input row hi feeds output rows hi + 1 (tap r = 0), hi (r = 1), hi - 1 (r = 2):
+                // [L.b0, W.b1, Rt.b2, x] is tap s from lane wo - 1 + s (E + 3 * 128), plus a * w
+                const uint32_t g0 = __byte_perm(__byte_perm(L[0], W[0], 0x7650u), Rt[0], 0x7610u);
+                const uint32_t g1 = __byte_perm(__byte_perm(L[1], W[1], 0x7650u), Rt[1], 0x7610u);
+                const uint32_t g2 = __byte_perm(__byte_perm(L[2], W[2], 0x7650u), Rt[2], 0x7610u);
+                acc_n = __dp4a((int)codes, (int)wr[0], (int)__dp4a(g0, 0x00010101u, (unsigned)acc_n));
+                acc_c = __dp4a((int)codes, (int)wr[1], (int)__dp4a(g1, 0x00010101u, (unsigned)acc_c));
+                acc_p = __dp4a((int)codes, (int)wr[2], (int)__dp4a(g2, 0x00010101u, (unsigned)acc_p));
+                if (lane >= 1 && lane <= 30) {
+                    const int v = acc_p - 9 * 128;  // output row hi - 1 is complete
+                    if (fast) {
+                        float y = __fmul_rn(__int2float_rn(v), sc_c);
+                        if (a.ep.bias) y = __fadd_rn(y, b_c);
+                        if (a.ep.relu) y = y > 0.f ? y : 0.f;
+                        if (a.ep.y) ty[(rr * 30 + lane - 1) * YS + warp] = y;
+                        if (a.ep.q) tq[(rr * 30 + lane - 1) * QS + warp] = (uint8_t)epi_quant_r(y, s_out, r_out, qm);
+                    } else {
+                        tout[(rr * CB + warp) * 30 + (lane - 1)] = v;
+                    }
+                }
+                acc_p = acc_c;
+                acc_c = acc_n;
+                acc_n = 0;
+            }
+            __syncthreads();
+            // store the output rows completed in this batch (ho = hb - 1 .. hb + RB - 2)
+            if (fast) {
+                // one (row, pixel) per thread: 16 channels = 16 code bytes / 64 fp32 bytes
+                for (int e = tid; e < RB * 30; e += NT) {
+                    const int rr = e / 30, x = e - rr * 30, ho = hb - 1 + rr;
+                    if (ho < 0 || ho >= a.Ho || x >= ncols) continue;
+                    const int64_t m = ((int64_t)n * a.Ho + ho) * a.Wo + (w0 + x);
+                    if (a.ep.q) {
+                        const uint32_t* src = reinterpret_cast<const uint32_t*>(tq + (rr * 30 + x) * QS);
+                        *reinterpret_cast<uint4*>(a.ep.q + m * a.ep.ldq + c0) = make_uint4(src[0], src[1], src[2], src[3]);
+                    }
+                    if (a.ep.y) {
+                        const float* src = ty + (rr * 30 + x) * YS;
+                        float4* dst = reinterpret_cast<float4*>(a.ep.y + m * a.ep.ldy + c0);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            dst[j] = make_float4(src[4 * j], src[4 * j + 1], src[4 * j + 2], src[4 * j + 3]);
+                    }
+                }
+            } else {
+                for (int e = tid; e < RB * 30 * CB; e += NT) {
+                    const int cc = e % CB, x = (e / CB) % 30, rr = e / (30 * CB);
+                    const int ho = hb - 1 + rr, ch = c0 + cc;
+                    if (ho < 0 || ho >= a.Ho || x >= ncols || ch >= a.C) continue;
+                    const int v = tout[(rr * CB + cc) * 30 + x];
+                    const int64_t m = ((int64_t)n * a.Ho + ho) * a.Wo + (w0 + x);
+                    if (a.C_out) a.C_out[m * a.K + ch] = v;
+                    else epi_store(epi_value(v, m, ch, sc, a.ep), m, ch, a.K, a.ep, s_out, qm);
+                }
+            }
+        }
+    }
+}
+
 }  // namespace axq

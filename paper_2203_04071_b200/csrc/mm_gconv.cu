@@ -63,7 +63,30 @@ static int launch_dw_repr(const GConvArgs& a, cudaStream_t st) {
     return -1;
 }
 
+static int launch_dw3(const GConvArgs& a, cudaStream_t st) {
+    static bool configured[32] = {false};
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    dev &= 31;
+    if (!configured[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(lut_dw3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dw3::SMEM);
+        if (e != cudaSuccess) return (int)e;
+        configured[dev] = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lut_dw3_kernel, dw3::NT, dw3::SMEM);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = (int64_t)((a.C + dw3::CB - 1) / dw3::CB) * ((a.Wo + 29) / 30) * a.N;
+    const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    lut_dw3_kernel<<<(unsigned)(items < resident ? items : resident), dw3::NT, dw3::SMEM, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
 int launch_gconv(int repr, const GConvArgs& a, cudaStream_t st) {
+    // depthwise 3x3 / stride 1 / pad 1 with a delta8 table: the input-stationary packed kernel
+    if (repr == REPR_DELTA8 && a.C == a.G && a.K == a.C && a.R == 3 && a.S == 3 && a.sh == 1 && a.sw == 1 &&
+        a.ph == 1 && a.pw == 1 && a.dh == 1 && a.dw == 1 && a.Ho == a.H && a.Wo == a.Wd && a.N < (1 << 30))
+        return launch_dw3(a, st);
     const bool dw = a.C == a.G && a.K == a.C && (a.C % 4) == 0 &&
                     (reinterpret_cast<uintptr_t>(a.X) & 3) == 0 &&
                     (!a.C_out || (reinterpret_cast<uintptr_t>(a.C_out) & 15) == 0);

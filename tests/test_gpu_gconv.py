@@ -35,6 +35,8 @@ def _table(kind):
 
 # N, C, H, W, K, R, S, stride, pad, dil, groups
 CASES = [(2, 32, 10, 9, 32, 3, 3, 1, 1, 1, 32),     # depthwise 3x3
+         (3, 24, 7, 70, 24, 3, 3, 1, 1, 1, 24),     # depthwise 3x3 s1 p1 (DW3): 3 strips, partial channel block
+         (1, 40, 31, 61, 40, 3, 3, 1, 1, 1, 40),    # DW3: ragged last strip, 3 channel blocks
          (2, 64, 11, 37, 64, 3, 3, 2, 1, 1, 64),    # depthwise 3x3 stride 2, 2 channel blocks, ragged tiles
          (1, 96, 9, 70, 96, 3, 3, 1, 0, 1, 96),     # depthwise 3x3, no padding, 3 column tiles
          (1, 16, 12, 12, 32, 3, 3, 2, 1, 1, 16),    # depthwise, channel multiplier 2, stride 2
@@ -130,3 +132,40 @@ def test_im2col_nhwc_i8(ax, shape):
     ax.axq_im2col_nhwc_i8(_t(X), cv, R, R, (st, st), (pd, pd), A)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(A.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 13, 40), (1, 64, 9, 31), (3, 48, 7, 70)])
+@pytest.mark.parametrize("per_channel", [False, True])
+def test_depthwise_dw3_fused_nhwc(ax, shape, per_channel):
+    """The depthwise 3x3 / stride 1 / pad 1 kernel's fused NHWC epilogue (fp32 y and requantized
+    codes, bias, ReLU, per-channel weight scales), computed in-loop and stored through shared
+    memory, against the oracle."""
+    Nb, C, H, Wd = shape
+    T = datagen.lut_randerr(8, 0, 2)
+    qa = datagen.random_int8(700 + C, (Nb, C, H, Wd), full_range=False)
+    qw = datagen.random_int8(701 + C, (C, 1, 3, 3))
+    acc = oracle.lut_conv2d(qa, qw, T, 8, (1, 1), (1, 1), groups=C)          # NCHW int
+    rng = np.random.default_rng(C + H)
+    s_a = np.float32(0.011)
+    s_w = rng.uniform(0.002, 0.02, C).astype(np.float32) if per_channel else np.float32(0.009)
+    b = rng.standard_normal(C).astype(np.float32)
+    s_o = np.float32(0.37)
+    acc_nhwc = acc.transpose(0, 2, 3, 1).reshape(-1, C)
+    y_ref = (oracle.dequantize_pc(acc_nhwc, s_a, s_w, b) if per_channel
+             else oracle.dequantize(acc_nhwc, s_a, s_w, b))
+    y_ref = np.maximum(y_ref, 0).astype(np.float32)
+    q_ref = oracle.quantize(y_ref, s_o, 8)
+    lut = ax.Lut(8, T)
+    d = ax.conv_desc(Nb, H, Wd, C, C, 3, 3, (1, 1), (1, 1), groups=C)
+    M = Nb * H * Wd
+    y = torch.full((M, C), np.nan, device=DEV)
+    q = torch.zeros(M, C, dtype=torch.int8, device=DEV)
+    kw = dict(d_scale_w_ch=_t(s_w)) if per_channel else {}
+    ep = ax.make_epilogue(torch.tensor([s_a], device=DEV),
+                          torch.tensor([1.0 if per_channel else s_w], device=DEV), bias=_t(b), y=y,
+                          ldy=C, relu=True, y_nhwc=True, q_out=q, ldq=C,
+                          d_scale_out=torch.tensor([s_o], device=DEV), bits_out=8, **kw)
+    ax.axq_lut_conv2d_ep(d, _t(qa.transpose(0, 2, 3, 1)), _t(qw.transpose(0, 2, 3, 1)), lut, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+    np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
