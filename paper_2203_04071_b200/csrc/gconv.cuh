@@ -226,7 +226,21 @@ constexpr int QT = RB * 30 * QS;           // int8 code tile
 constexpr int SMEM = TAB + IN + OUT + QT;
 }  // namespace dw3
 
-static __global__ void __launch_bounds__(dw3::NT) lut_dw3_kernel(const GConvArgs a) {
+__device__ __forceinline__ uint32_t dw3_lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];\n" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t dw3_lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// QR: the MobileNet inner-layer epilogue specialised (ReLU + requantize to int8 NHWC, no fp32 y,
+// optional bias / per-channel scales); otherwise the runtime-selected paths
+template <bool QR>
+static __global__ void __launch_bounds__(dw3::NT, 2) lut_dw3_kernel(const GConvArgs a) {
     using namespace dw3;
     extern __shared__ __align__(16) uint8_t dw3_smem[];
     uint32_t* tabs = reinterpret_cast<uint32_t*>(dw3_smem);            // [CB][3][256]
@@ -252,7 +266,7 @@ static __global__ void __launch_bounds__(dw3::NT) lut_dw3_kernel(const GConvArgs
     // the fast epilogue: row-layout (NHWC) fp32 y and / or int8 codes, no residual, whole
     // 16-channel blocks with 16-byte aligned rows -- computed by the lane that completes the
     // output, transposed through shared memory, stored 16 bytes per pixel
-    const bool fast = !a.C_out && !a.ep.y_nchw && !a.ep.residual && (a.C % CB) == 0 &&
+    const bool fast = QR || !a.C_out && !a.ep.y_nchw && !a.ep.residual && (a.C % CB) == 0 &&
                       (!a.ep.y || (((a.ep.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.ep.y) & 15) == 0))) &&
                       (!a.ep.q || (((a.ep.ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(a.ep.q) & 15) == 0)));
     // items ordered (channel block, strip) major, image minor: a CTA's consecutive items share
@@ -285,7 +299,8 @@ static __global__ void __launch_bounds__(dw3::NT) lut_dw3_kernel(const GConvArgs
         }
         const int c = c0 + warp;
         const bool cvalid = c < a.C;
-        const uint32_t* tab = tabs + warp * 768;
+        const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tabs + warp * 768);
+        const uint32_t tin_s = (uint32_t)__cvta_generic_to_shared(tin);
         uint32_t wr[3] = {0u, 0u, 0u};             // filter rows as signed bytes [w(r,0), w(r,1), w(r,2), 0]
         if (cvalid) {
 #pragma unroll
@@ -330,10 +345,10 @@ static __global__ void __launch_bounds__(dw3::NT) lut_dw3_kernel(const GConvArgs
             for (int rr = 0; rr < RB; ++rr) {
                 const int hi = hb + rr;
                 if (hi > a.H) break;
-                const uint32_t u = tin[(rr * PX + lane) * PS + warp];
+                const uint32_t u = dw3_lds_u8(tin_s + (rr * PX + lane) * PS + warp);
                 uint32_t W[3], L[3], Rt[3];
 #pragma unroll
-                for (int r = 0; r < 3; ++r) W[r] = tab[r * 256 + u];
+                for (int r = 0; r < 3; ++r) W[r] = dw3_lds_u32(tab_s + (r * 256 + u) * 4);
 #pragma unroll
                 for (int r = 0; r < 3; ++r) {
                     L[r] = __shfl_up_sync(0xffffffffu, W[r], 1);
@@ -351,7 +366,12 @@ static __global__ void __launch_bounds__(dw3::NT) lut_dw3_kernel(const GConvArgs
                 acc_p = __dp4a((int)codes, (int)wr[2], (int)__dp4a(g2, 0x00010101u, (unsigned)acc_p));
                 if (lane >= 1 && lane <= 30) {
                     const int v = acc_p - 9 * 128;  // output row hi - 1 is complete
-                    if (fast) {
+                    if (QR) {
+                        float y = __fmul_rn(__int2float_rn(v), sc_c);
+                        if (a.ep.bias) y = __fadd_rn(y, b_c);
+                        y = y > 0.f ? y : 0.f;
+                        tq[(rr * 30 + lane - 1) * QS + warp] = (uint8_t)epi_quant_r(y, s_out, r_out, qm);
+                    } else if (fast) {
                         float y = __fmul_rn(__int2float_rn(v), sc_c);
                         if (a.ep.bias) y = __fadd_rn(y, b_c);
                         if (a.ep.relu) y = y > 0.f ? y : 0.f;
@@ -373,11 +393,11 @@ static __global__ void __launch_bounds__(dw3::NT) lut_dw3_kernel(const GConvArgs
                     const int rr = e / 30, x = e - rr * 30, ho = hb - 1 + rr;
                     if (ho < 0 || ho >= a.Ho || x >= ncols) continue;
                     const int64_t m = ((int64_t)n * a.Ho + ho) * a.Wo + (w0 + x);
-                    if (a.ep.q) {
+                    if (QR || a.ep.q) {
                         const uint32_t* src = reinterpret_cast<const uint32_t*>(tq + (rr * 30 + x) * QS);
                         *reinterpret_cast<uint4*>(a.ep.q + m * a.ep.ldq + c0) = make_uint4(src[0], src[1], src[2], src[3]);
                     }
-                    if (a.ep.y) {
+                    if (!QR && a.ep.y) {
                         const float* src = ty + (rr * 30 + x) * YS;
                         float4* dst = reinterpret_cast<float4*>(a.ep.y + m * a.ep.ldy + c0);
 #pragma unroll

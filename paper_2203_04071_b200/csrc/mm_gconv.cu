@@ -63,23 +63,31 @@ static int launch_dw_repr(const GConvArgs& a, cudaStream_t st) {
     return -1;
 }
 
-static int launch_dw3(const GConvArgs& a, cudaStream_t st) {
+template <bool QR>
+static int launch_dw3_t(const GConvArgs& a, cudaStream_t st) {
     static bool configured[32] = {false};
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     dev &= 31;
     if (!configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(lut_dw3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dw3::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(lut_dw3_kernel<QR>, cudaFuncAttributeMaxDynamicSharedMemorySize, dw3::SMEM);
         if (e != cudaSuccess) return (int)e;
         configured[dev] = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lut_dw3_kernel, dw3::NT, dw3::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lut_dw3_kernel<QR>, dw3::NT, dw3::SMEM);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t items = (int64_t)((a.C + dw3::CB - 1) / dw3::CB) * ((a.Wo + 29) / 30) * a.N;
     const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
-    lut_dw3_kernel<<<(unsigned)(items < resident ? items : resident), dw3::NT, dw3::SMEM, st>>>(a);
+    lut_dw3_kernel<QR><<<(unsigned)(items < resident ? items : resident), dw3::NT, dw3::SMEM, st>>>(a);
     return (int)cudaGetLastError();
+}
+
+static int launch_dw3(const GConvArgs& a, cudaStream_t st) {
+    const EpiArgs& e = a.ep;
+    const bool qr = !a.C_out && e.q && !e.y && e.relu && !e.residual && (a.C % dw3::CB) == 0 &&
+                    ((e.ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 15) == 0);
+    return qr ? launch_dw3_t<true>(a, st) : launch_dw3_t<false>(a, st);
 }
 
 int launch_gconv(int repr, const GConvArgs& a, cudaStream_t st) {

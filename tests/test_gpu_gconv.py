@@ -136,7 +136,8 @@ def test_im2col_nhwc_i8(ax, shape):
 
 @pytest.mark.parametrize("shape", [(2, 32, 13, 40), (1, 64, 9, 31), (3, 48, 7, 70)])
 @pytest.mark.parametrize("per_channel", [False, True])
-def test_depthwise_dw3_fused_nhwc(ax, shape, per_channel):
+@pytest.mark.parametrize("with_y", [True, False], ids=["y+q", "q-only"])
+def test_depthwise_dw3_fused_nhwc(ax, shape, per_channel, with_y):
     """The depthwise 3x3 / stride 1 / pad 1 kernel's fused NHWC epilogue (fp32 y and requantized
     codes, bias, ReLU, per-channel weight scales), computed in-loop and stored through shared
     memory, against the oracle."""
@@ -162,10 +163,11 @@ def test_depthwise_dw3_fused_nhwc(ax, shape, per_channel):
     q = torch.zeros(M, C, dtype=torch.int8, device=DEV)
     kw = dict(d_scale_w_ch=_t(s_w)) if per_channel else {}
     ep = ax.make_epilogue(torch.tensor([s_a], device=DEV),
-                          torch.tensor([1.0 if per_channel else s_w], device=DEV), bias=_t(b), y=y,
-                          ldy=C, relu=True, y_nhwc=True, q_out=q, ldq=C,
+                          torch.tensor([1.0 if per_channel else s_w], device=DEV), bias=_t(b),
+                          y=y if with_y else None, ldy=C, relu=True, y_nhwc=True, q_out=q, ldq=C,
                           d_scale_out=torch.tensor([s_o], device=DEV), bits_out=8, **kw)
     ax.axq_lut_conv2d_ep(d, _t(qa.transpose(0, 2, 3, 1)), _t(qw.transpose(0, 2, 3, 1)), lut, ep)
     torch.cuda.synchronize()
-    np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+    if with_y:
+        np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
     np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
