@@ -49,6 +49,9 @@ struct Shape {
 constexpr int CW = 28;
 constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots are sized for it)
 
+#ifndef P4W_ALU_QUADS     // quads whose adds run on the ALU pipe (the rest: multiply-adds by 1, FMA pipe)
+#define P4W_ALU_QUADS 2
+#endif
 #ifndef P4W_SMALL_FULL_STAGES
 #define P4W_SMALL_FULL_STAGES 3
 #endif
@@ -367,7 +370,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                     umma_commit(bar_mma + 8 * buf);
                     if (st + 1 == s_e) umma_commit(bar_tfull + 8 * tb);
                 }
-                const uint8_t* tbs = smem + G::SMEM_TBL + buf * TBL_STAGE;
+                // shared-window address of this stage's tables: one IMAD per code forms the row
+                // address, the (k, quad) offsets are immediates of the loads
+                const uint32_t tb_addr = s_base + G::SMEM_TBL + (uint32_t)(buf * TBL_STAGE);
                 const uint8_t* at = smem + G::SMEM_A + buf * A_STAGE;
                 if (wlive) {
 #pragma unroll
@@ -378,19 +383,21 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                         for (int kk = 0; kk < 16; kk += 2) {
                             const uint32_t ua0 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
                             const uint32_t ua1 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + ((kk + 1) & 3));
-                            const uint8_t* r0 = tbs + (pl * 16 + kk) * G::NQ * TQ + ua0 * 4u;
-                            const uint8_t* r1 = tbs + (pl * 16 + kk + 1) * G::NQ * TQ + ua1 * 4u;
+                            const uint32_t r0 = tb_addr + ua0 * 4u, r1 = tb_addr + ua1 * 4u;
 #pragma unroll
                             for (int q = 0; q < NACC; ++q) {
-                                const uint32_t v0 = *reinterpret_cast<const uint32_t*>(r0 + q * TQ);
-                                const uint32_t v1 = *reinterpret_cast<const uint32_t*>(r1 + q * TQ);
+                                uint32_t v0, v1;
+                                asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v0)
+                                             : "r"(r0 + (uint32_t)(((pl * 16 + kk) * G::NQ + q) * TQ)));
+                                asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v1)
+                                             : "r"(r1 + (uint32_t)(((pl * 16 + kk + 1) * G::NQ + q) * TQ)));
                                 if constexpr (E16) {
                                     pacc[q][0] += v0 + v1;
                                     pacc[q][1] += __byte_perm(v0, 0u, 0x4432u) + __byte_perm(v1, 0u, 0x4432u);
                                 } else {
                                     const uint32_t e0 = __byte_perm(v0, 0u, 0x4240u), e1 = __byte_perm(v1, 0u, 0x4240u);
                                     const uint32_t o0 = __byte_perm(v0, 0u, 0x4341u), o1 = __byte_perm(v1, 0u, 0x4341u);
-                                    if (q < 2) {     // ALU pipe: one 3-input add per accumulator
+                                    if (q < P4W_ALU_QUADS) {     // ALU pipe: one 3-input add per accumulator
                                         pacc[q][0] += e0 + e1;
                                         pacc[q][1] += o0 + o1;
                                     } else {         // FMA pipe: multiply-adds by an opaque 1
