@@ -9,17 +9,21 @@ rows = list(csv.reader(open(sys.argv[1])))
 h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
 hdr, units, vals = rows[h], rows[h + 1], rows[h + 2]
 d = {k: v for k, v in zip(hdr, vals)}
+u = {k: v for k, v in zip(hdr, units)}
+SCALE = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1.0, "ms": 1e3,
+         "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,                # -> bytes
+         "hz": 1e-6, "Khz": 1e-3, "Mhz": 1.0, "Ghz": 1e3}                      # -> MHz
 
 
 def f(k):
     try:
-        return float(d[k].replace(",", ""))
+        return float(d[k].replace(",", "")) * SCALE.get(u.get(k, ""), 1.0)
     except (KeyError, ValueError):
         return None
 
 
 out = {"kernel": d.get("Kernel Name", "")[:80],
-       "duration_us": f("gpu__time_duration.sum") / 1e3 if f("gpu__time_duration.sum") else None,
+       "duration_us": f("gpu__time_duration.sum"),
        "sm_mhz": f("sm__cycles_elapsed.avg.per_second"),
        "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
        "alu_pipe_pct": f("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
@@ -36,7 +40,7 @@ if out["shared_wavefronts"] and out["shared_wavefronts_ideal"]:
 if len(sys.argv) > 2 and out["duration_us"]:
     lk = float(sys.argv[2])
     out["lookups"] = lk
-    out["T_lookups_per_s"] = round(lk / out["duration_us"] / 1e6, 3)
+    out["T_lookups_per_s"] = round(lk / out["duration_us"] / 1e6, 3)   # lookups per us / 1e6 = T/s
     if out["shared_ld_wavefronts"]:
         out["lookups_per_shared_wavefront"] = round(lk / out["shared_ld_wavefronts"], 1)
 stalls = {k.split("smsp__average_warps_issue_stalled_")[1].split("_per_issue_active")[0]: f(k)
