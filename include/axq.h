@@ -339,12 +339,16 @@ axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw);
  * their device scales; x fp32 [M][K] / w fp32 [N][K]: the unquantized operands, with the
  * calibrated clip ranges (device scalars, e.g. amax; a value with |v| > clip gets no gradient);
  * x / w null: no mask.  All buffers contiguous, on the current device; gx / gw / gb nullable
- * (not computed).  workspace (nullable, workspace_elems floats, caller-owned, no contents
- * required): room for K-split partial products (up to 128 slices of one gradient; fewer when
- * the room is smaller, none without it); used to split the summed dimension when the output
- * alone cannot fill the SMs (the splits are added in a fixed order: deterministic).  fp32
- * accumulation on the tensor cores (not bit-exact against a different summation order: within
- * the fp32 dot-product bound).  Asynchronous on stream.  AXQ_ERR_INVALID for negative extents or a
+ * (not computed).  workspace (nullable, workspace_elems floats, 16-byte aligned, caller-owned,
+ * no contents required, one per concurrently running call): with at least
+ * axq_ste_linear_workspace_elems(M, N, K) elements each product first converts its operands
+ * once into the tensor cores' tiled bf16 layout there and streams them with bulk copies
+ * (several times faster); K-split slices are added inside a thread-block cluster through
+ * distributed shared memory, beyond 8 slices through partial slots in the workspace; with less
+ * room the operands are converted tile by tile inside the GEMM (fewer or no K slices).  The
+ * slices are always added in a fixed order: deterministic for a given (shape, workspace size).
+ * fp32 accumulation on the tensor cores (not bit-exact against a different summation order:
+ * within the fp32 dot-product bound).  Asynchronous on stream.  AXQ_ERR_INVALID for negative extents or a
  * missing operand of a requested gradient.
  * --------------------------------------------------------------------------------- */
 axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float* gy,
@@ -353,6 +357,13 @@ axq_status axq_ste_linear_backward(int64_t M, int64_t N, int64_t K, const float*
                                    const float* w, const float* d_clip_w, float* gx, float* gw,
                                    float* gb, float* workspace, int64_t workspace_elems,
                                    void* stream);
+
+/* axq_ste_linear_workspace_elems / axq_ste_conv2d_workspace_elems: the workspace (fp32
+ * elements) that enables the fastest decomposition of every product of the backward on the
+ * current device (pre-converted operands + partial slots + two-pass column sums).  -1 for
+ * negative extents or an invalid descriptor. */
+int64_t axq_ste_linear_workspace_elems(int64_t M, int64_t N, int64_t K);
+int64_t axq_ste_conv2d_workspace_elems(const axq_conv_desc* d);
 
 /* axq_ste_conv2d_backward: the same STE backward for a convolution (groups = 1, dilation 1,
  *   c_valid 0; the conv is the GEMM of its im2col matrix).  gy fp32 NHWC [N][Ho][Wo][K]

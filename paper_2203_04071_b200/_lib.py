@@ -34,7 +34,7 @@ EXPORTED = [
     "axq_im2col_nhwc_i8", "axq_wpack_repack", "axq_lut_gemm_xs",
     "axq_last_path", "axq_workspace_elems", "axq_lut_gemm_f32a", "axq_lut_conv2d_f32",
     "axq_wpack16_create", "axq_lut_gemm16_wp", "axq_ste_linear_backward_pc",
-    "axq_ste_conv2d_backward_pc",
+    "axq_ste_conv2d_backward_pc", "axq_ste_linear_workspace_elems", "axq_ste_conv2d_workspace_elems",
 ]
 
 # axq_last_path kernel families (include/axq.h AXQ_PATH_*)
@@ -84,6 +84,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "axq_version": ([], i32),
         "axq_last_path": ([ctypes.POINTER(i32)], i32),
         "axq_workspace_elems": ([i64, i64], i64),
+        "axq_ste_linear_workspace_elems": ([i64, i64, i64], i64),
+        "axq_ste_conv2d_workspace_elems": ([ctypes.POINTER(axq_conv_desc)], i64),
         "axq_wpack16_create": ([vp, vp, i64, i64, i64, ctypes.POINTER(vp)], i32),
         "axq_lut_gemm16_wp": ([i64, vp, i64, vp, ctypes.POINTER(axq_epilogue), vp, i64, vp], i32),
         "axq_lut_gemm_f32a": ([i64, i64, i64, vp, i64, vp, vp, i64, vp, ctypes.POINTER(axq_epilogue),
@@ -330,6 +332,16 @@ def axq_last_path() -> tuple[str, int]:
 def axq_workspace_elems(M: int, N: int) -> int:
     """Epilogue workspace size (int32 elements) enabling every decomposition for M x N outputs."""
     return int(load().axq_workspace_elems(int(M), int(N)))
+
+
+def axq_ste_linear_workspace_elems(M: int, N: int, K: int) -> int:
+    """STE backward workspace (fp32 elements) for the fastest decomposition (include/axq.h)."""
+    return int(load().axq_ste_linear_workspace_elems(int(M), int(N), int(K)))
+
+
+def axq_ste_conv2d_workspace_elems(d) -> int:
+    """STE conv backward workspace (fp32 elements) for the fastest decomposition."""
+    return int(load().axq_ste_conv2d_workspace_elems(ctypes.byref(d)))
 
 
 def axq_wpack_kernel(variant: int) -> int:

@@ -191,6 +191,26 @@ __global__ void im2col_nhwc_i8_kernel(const int8_t* __restrict__ X, int64_t M, i
     const int chunks = lda / 16;
     const int64_t total = M * chunks;
     const int64_t hw = (int64_t)Ho * Wo;
+    if (cv == C && (C & 15) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && total < ((int64_t)1 << 31) &&
+        (int64_t)H * W * C < ((int64_t)1 << 31)) {
+        // 16 consecutive k = 16 channels of one tap: one 16-byte load per chunk, 32-bit index math
+        const int hw32 = Ho * Wo, tot = (int)total;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+            const int m = i / chunks, j = i - m * chunks;
+            const int img = m / hw32, rem = m - img * hw32;
+            const int ho = rem / Wo, wo = rem - ho * Wo;
+            const uint32_t t = taps[16 * j];
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (t != ~0u) {
+                const int hi = ho * sh - ph + (int)(t & 0xffu), wi = wo * sw - pw + (int)((t >> 8) & 0xffu);
+                if ((unsigned)hi < (unsigned)H && (unsigned)wi < (unsigned)W)
+                    v = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)img * H * W * C + (hi * W + wi) * C +
+                                                             (int)(t >> 16)));
+            }
+            reinterpret_cast<uint4*>(A + (int64_t)m * lda)[j] = v;
+        }
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t m = i / chunks;
         const int j = (int)(i - m * chunks);

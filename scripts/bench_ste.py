@@ -32,7 +32,7 @@ def run(M, N, K):
     s = torch.tensor([0.01], device="cuda")
     clip = torch.tensor([3.0], device="cuda")
     gx, gw, gb = torch.empty(M, K, device="cuda"), torch.empty(N, K, device="cuda"), torch.empty(N, device="cuda")
-    ws = torch.empty(128 * min(M, N) * K, device="cuda")
+    ws = torch.empty(max(1, ax.axq_ste_linear_workspace_elems(M, N, K)), device="cuda")
     flush = torch.empty(64 << 20, device="cuda")
     ts = []
     for i in range(13):
@@ -47,7 +47,7 @@ def run(M, N, K):
             ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
     fl = 2 * 2 * M * N * K
-    return {"M": M, "N": N, "K": K, "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
+    return {"M": M, "N": N, "K": K, "ws_mib": round(ws.numel() * 4 / 2**20, 1), "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
             "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3),
             "frac_bf16_peak_useful": round(fl / (ms * 1e-3) / BF16, 4),
             "frac_bf16_peak_executed": round(MMA_TERMS * fl / (ms * 1e-3) / BF16, 4)}
@@ -65,8 +65,8 @@ def run_conv(N, C, H, K, R, st):
     M, Kc = N * Ho * Ho, R * R * C
     cols = torch.empty(M, (Kc + 15) // 16 * 16, dtype=torch.int8, device="cuda")
     gcols = torch.empty(M, Kc, device="cuda")
-    ws = torch.empty(128 * K * Kc, device="cuda")
     d = ax.conv_desc(N, H, H, C, K, R, R, (st, st), (pd, pd))
+    ws = torch.empty(max(1, ax.axq_ste_conv2d_workspace_elems(d)), device="cuda")
     flush = torch.empty(64 << 20, device="cuda")
     ts = []
     for i in range(8):
@@ -80,7 +80,7 @@ def run_conv(N, C, H, K, R, st):
             ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
     fl = 2 * 2 * M * K * Kc
-    return {"conv": [N, C, H, K, R, st], "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
+    return {"conv": [N, C, H, K, R, st], "ws_mib": round(ws.numel() * 4 / 2**20, 1), "ms": round(ms, 4), "gflops": round(fl / ms / 1e6, 1),
             "frac_fp32_fma_peak": round(fl / (ms * 1e-3) / PEAK, 3),
             "frac_bf16_peak_useful": round(fl / (ms * 1e-3) / BF16, 4),
             "frac_bf16_peak_executed": round(MMA_TERMS * fl / (ms * 1e-3) / BF16, 4)}

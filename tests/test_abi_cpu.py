@@ -73,6 +73,29 @@ def test_invalid_arguments_rejected_on_host(L):
     assert (ho.value, wo.value) == (112, 112)
 
 
+def test_ste_workspace_queries(L):
+    """axq_ste_*_workspace_elems: host-only sizing (no GPU needed).  The pre-converted operands
+    of a product are 3 bf16 terms of the fp32 operand (128 x 32 tiles) and the bf16 codes."""
+    from paper_2203_04071_b200._lib import axq_conv_desc
+    L.axq_ste_linear_workspace_elems.restype = ctypes.c_int64
+    L.axq_ste_linear_workspace_elems.argtypes = [ctypes.c_int64] * 3
+    L.axq_ste_conv2d_workspace_elems.restype = ctypes.c_int64
+    L.axq_ste_conv2d_workspace_elems.argtypes = [ctypes.c_void_p]
+    assert L.axq_ste_linear_workspace_elems(-1, 4, 4) == -1
+    assert L.axq_ste_conv2d_workspace_elems(None) == -1
+    assert L.axq_ste_linear_workspace_elems(0, 0, 0) == 0
+    M, N, K = 256, 1024, 1024
+    cdiv = lambda a, b: -(-a // b)
+    gx = cdiv(M, 128) * cdiv(N, 32) * 3 * 128 * 32 // 2 + cdiv(K, 128) * cdiv(N, 32) * 128 * 32 // 2
+    gw = cdiv(N, 128) * cdiv(M, 32) * 3 * 128 * 32 // 2 + cdiv(K, 128) * cdiv(M, 32) * 128 * 32 // 2
+    need = L.axq_ste_linear_workspace_elems(M, N, K)
+    assert need >= max(gx, gw)
+    assert L.axq_ste_linear_workspace_elems(2 * M, N, K) >= need
+    d = axq_conv_desc(32, 56, 56, 64, 64, 3, 3, 1, 1, 1, 1, 1, 1, 1)
+    Mc, Kc = 32 * 56 * 56, 9 * 64
+    assert L.axq_ste_conv2d_workspace_elems(ctypes.byref(d)) >= cdiv(Mc, 128) * cdiv(64, 32) * 3 * 128 * 32 // 2
+
+
 def test_product_package_does_not_import_oracle():
     """The product path must not route through the oracle (no CPU fallback)."""
     pkg = os.path.join(ROOT, "paper_2203_04071_b200")

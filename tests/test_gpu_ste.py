@@ -98,7 +98,10 @@ CONV_SHAPES = [(2, 8, 9, 9, 16, 3, 3, 1, 1), (1, 16, 11, 10, 24, 3, 3, 2, 1), (3
 
 @pytest.mark.parametrize("shape", CONV_SHAPES)
 @pytest.mark.parametrize("masked", [False, True])
-def test_ste_conv_backward(ax, shape, masked):
+@pytest.mark.parametrize("prep", [False, True], ids=["in-kernel", "prep"])
+def test_ste_conv_backward(ax, shape, masked, prep):
+    """prep: a workspace large enough for the pre-converted operands (ste_pp_kernel), else the
+    in-kernel conversion (ste_tc_kernel)."""
     N, C, H, W, K, R, S, st, pd = shape
     x = datagen.normal(90 + C, 1, (N, H, W, C))
     wt = datagen.normal(90 + C, 2, (K, R, S, C), 0.2)
@@ -119,7 +122,8 @@ def test_ste_conv_backward(ax, shape, masked):
     gw = torch.full((K, R, S, C), np.nan, device=DEV)
     gb = torch.full((K,), np.nan, device=DEV)
     kw = dict(x=_t(x), d_clip_a=f(clip_a), w=_t(wt), d_clip_w=f(clip_w)) if masked else {}
-    ax.axq_ste_conv2d_backward(d, _t(gy), _t(qx), f(sa), _t(qw), f(sw), gx=gx, gw=gw, gb=gb, **kw)
+    ws = torch.full((16 << 20,), np.nan, device=DEV) if prep else None
+    ax.axq_ste_conv2d_backward(d, _t(gy), _t(qx), f(sa), _t(qw), f(sw), gx=gx, gw=gw, gb=gb, workspace=ws, **kw)
     torch.cuda.synchronize()
     M = N * Ho * Wo
     for got, r, a_, n in ((gx, ref[0], absref[0], K * R * S), (gw, ref[1], absref[1], M), (gb, ref[2], absref[2], M)):
@@ -129,10 +133,12 @@ def test_ste_conv_backward(ax, shape, masked):
         assert (err <= _bound(n, a_.astype(np.float64), r)).all(), float(err.max())
 
 
-@pytest.mark.parametrize("M,N,K", [(96, 40, 70), (300, 129, 257)])
+@pytest.mark.parametrize("M,N,K", [(96, 40, 70), (300, 129, 257), (520, 1000, 1500)])
 @pytest.mark.parametrize("masked", [False, True])
-def test_ste_backward_per_channel(ax, M, N, K, masked):
-    """Per-output-channel weight scales and clips (axq_ste_linear_backward_pc)."""
+@pytest.mark.parametrize("prep", [False, True], ids=["in-kernel", "prep"])
+def test_ste_backward_per_channel(ax, M, N, K, masked, prep):
+    """Per-output-channel weight scales and clips (axq_ste_linear_backward_pc), with the
+    in-kernel conversion and with the pre-converted operands (workspace given)."""
     x = datagen.normal(65, M, (M, K))
     W = datagen.normal(65, N, (N, K), 0.05) * np.linspace(0.3, 2.5, N, dtype=np.float32)[:, None]
     qa, sa = oracle.quantize_tensor(x, 8)
@@ -150,7 +156,8 @@ def test_ste_backward_per_channel(ax, M, N, K, masked):
     gw = torch.full((N, K), np.nan, device=DEV)
     f = lambda v: _t(np.atleast_1d(np.asarray(v, dtype=np.float32)))
     kw = dict(x=_t(x), d_clip_a=f(clip_a), w=_t(W), d_clip_w=f(clip_w)) if masked else {}
-    ax.axq_ste_linear_backward(_t(gy), _t(qa), f(sa), _t(qw), f(sw), gx=gx, gw=gw, **kw)
+    ws = torch.full((16 << 20,), np.nan, device=DEV) if prep else None
+    ax.axq_ste_linear_backward(_t(gy), _t(qa), f(sa), _t(qw), f(sw), gx=gx, gw=gw, workspace=ws, **kw)
     torch.cuda.synchronize()
     wf = np.abs(oracle.fake_quant(qw, sw)).astype(np.float64)
     xf = np.abs(oracle.fake_quant(qa, sa)).astype(np.float64)
@@ -199,6 +206,32 @@ def test_ste_conv_backward_workspace_large_m(ax, masked):
         assert np.isfinite(got).all()
         err = np.abs(got.astype(np.float64) - r.astype(np.float64))
         assert (err <= _bound(n, a_.astype(np.float64), r)).all(), float(err.max())
+
+
+@pytest.mark.parametrize("elems", [1, 70000, 190000, 400000])
+def test_ste_backward_workspace_sizes(ax, elems):
+    """Workspaces too small for the pre-converted operands fall back to the in-kernel
+    conversion; in between, the pre-converted path runs with fewer (or no) split-K slices."""
+    M, N, K = 200, 300, 260
+    x = datagen.normal(67, 1, (M, K))
+    W = datagen.normal(67, 2, (N, K), 0.05)
+    qa, sa = oracle.quantize_tensor(x, 8)
+    qw, sw = oracle.quantize_tensor(W, 8)
+    gy = datagen.normal(67, 3, (M, N))
+    ref = oracle.ste_linear_backward(gy, qa, sa, qw, sw)
+    gx = torch.full((M, K), np.nan, device=DEV)
+    gw = torch.full((N, K), np.nan, device=DEV)
+    f = lambda v: _t(np.array([v], dtype=np.float32))
+    ws = torch.full((elems,), np.nan, device=DEV)
+    ax.axq_ste_linear_backward(_t(gy), _t(qa), f(sa), _t(qw), f(sw), gx=gx, gw=gw, workspace=ws)
+    torch.cuda.synchronize()
+    wf = np.abs(oracle.fake_quant(qw, sw)).astype(np.float64)
+    xf = np.abs(oracle.fake_quant(qa, sa)).astype(np.float64)
+    ag = np.abs(gy).astype(np.float64)
+    for got, r, n, absprod in ((gx, ref[0], N, ag @ wf), (gw, ref[1], M, ag.T @ xf)):
+        got = got.cpu().numpy()
+        err = np.abs(got.astype(np.float64) - r.astype(np.float64))
+        assert (err <= _bound(n, absprod, r)).all(), float(err.max())
 
 
 def test_ste_binding_checks_and_strided_grad(ax):
