@@ -345,299 +345,6 @@ __global__ void __launch_bounds__(stetc::NT) ste_tc_kernel(int64_t M, int64_t N,
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(BN) : "memory");
 }
 
-// ---------------------------------------------------------------------------------------
-// Pre-converted operands ("prep" path): each operand is converted ONCE per product into the
-// tiled canonical K-major layout the MMA reads, so a stage of the GEMM is a handful of bulk
-// copies and the tensor cores are not starved by the per-tile fp32 -> bf16 conversion.
-//   A' = [m tile][k tile][term hi / mid / lo][chunk 0..3][128 rows][8 bf16]   (3 x 8 KiB per tile pair)
-//   B' = [n tile][k tile][chunk 0..3][128 rows][8 bf16]                      (8 KiB)
-// (row = the GEMM's M resp. N index, chunk = 8 consecutive summed indices p.)
-// ---------------------------------------------------------------------------------------
-namespace stepp {
-constexpr int BM = 128, BN = 128, BK = 32;
-constexpr int TILE_A = 3 * BM * BK * 2;        // 24 KiB
-constexpr int TILE_B = BN * BK * 2;            // 8 KiB
-constexpr int STAGES = 3;
-constexpr int STAGE = TILE_A + TILE_B;         // 32 KiB
-constexpr int TS = BN + 4;                     // epilogue tile row stride (floats): conflict-free float4 rows
-constexpr int SMEM = STAGES * STAGE + 128;     // 2 CTAs per SM
-static_assert(BM * TS * 4 <= STAGES * STAGE, "epilogue tile must fit the stage buffers");
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
-}  // namespace stepp
-
-// thread -> (row, chunk) of one (m tile, k tile): 8 consecutive p of row i, split into 3 terms.
-// TA (A[p][i]): row fastest, a warp reads 32 consecutive i per p; else chunk fastest, 4 threads
-// read one row's 32 consecutive p (two float4 each when aligned).
-template <bool TA, bool PCS>
-__global__ void __launch_bounds__(256) ste_prep_a_kernel(int64_t M, int64_t K, const float* __restrict__ A,
-                                                         int64_t lda, const float* __restrict__ s_b,
-                                                         int64_t KT, int avec, uint4* __restrict__ out) {
-    const int64_t total = ((M + 127) / 128) * KT * 4 * 128;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-        const int row = TA ? (int)(g & 127) : (int)((g >> 2) & 127);
-        const int c = TA ? (int)((g >> 7) & 3) : (int)(g & 3);
-        const int64_t tk = g >> 9;                       // (m tile, k tile)
-        const int64_t kt = tk % KT, mt = tk / KT;
-        const int64_t i = mt * 128 + row, p0 = kt * 32 + c * 8;
-        float a[8];
-        if (!TA && avec && i < M && p0 + 8 <= K) {
-            const float4 f0 = __ldg(reinterpret_cast<const float4*>(A + i * lda + p0));
-            const float4 f1 = __ldg(reinterpret_cast<const float4*>(A + i * lda + p0) + 1);
-            a[0] = f0.x; a[1] = f0.y; a[2] = f0.z; a[3] = f0.w;
-            a[4] = f1.x; a[5] = f1.y; a[6] = f1.z; a[7] = f1.w;
-        } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int64_t p = p0 + e;
-                a[e] = (i < M && p < K) ? (TA ? __ldg(A + p * lda + i) : __ldg(A + i * lda + p)) : 0.f;
-            }
-        }
-        if (PCS) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (p0 + e < K) a[e] = __fmul_rn(a[e], __ldg(s_b + p0 + e));   // per-channel scale of p
-        }
-        uint32_t hw[4], mw[4], lw[4];
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-            uint16_t h[2], md[2], l[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const float x = a[e + u];
-                h[u] = bf16_rn_bits(x);
-                const float r1 = __fsub_rn(x, __bfloat162float(__ushort_as_bfloat16(h[u])));
-                md[u] = bf16_rn_bits(r1);
-                const float r2 = __fsub_rn(r1, __bfloat162float(__ushort_as_bfloat16(md[u])));
-                l[u] = bf16_rn_bits(r2);
-            }
-            hw[e / 2] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
-            mw[e / 2] = (uint32_t)md[0] | ((uint32_t)md[1] << 16);
-            lw[e / 2] = (uint32_t)l[0] | ((uint32_t)l[1] << 16);
-        }
-        uint4* base = out + tk * (3 * 4 * 128) + c * 128 + row;      // in 16-byte units
-        base[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        base[4 * 128] = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-        base[8 * 128] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-    }
-}
-
-// thread -> (4 columns j .. j + 3, chunk) of one (n tile, k tile): the int8 codes B[p][j] of 8
-// consecutive p, one 4-byte load per p when aligned, as bf16 (exact) into 4 rows of the tile
-__global__ void __launch_bounds__(256) ste_prep_b_kernel(int64_t N, int64_t K, const int8_t* __restrict__ B,
-                                                         int64_t ldb, int64_t KT, int bvec, uint4* __restrict__ out) {
-    const int64_t total = ((N + 127) / 128) * KT * 4 * 32;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-        const int rq = (int)(g & 31), c = (int)((g >> 5) & 3);
-        const int64_t tk = g >> 7;
-        const int64_t kt = tk % KT, nt = tk / KT;
-        const int64_t j0 = nt * 128 + rq * 4, p0 = kt * 32 + c * 8;
-        uint32_t q[8];     // q[e] = bytes of B[p0 + e][j0 .. j0 + 3]
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int64_t p = p0 + e;
-            uint32_t v = 0u;
-            if (p < K) {
-                if (bvec && j0 + 4 <= N) {
-                    v = __ldg(reinterpret_cast<const unsigned int*>(B + p * ldb + j0));
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (j0 + u < N) v |= (uint32_t)(uint8_t)B[p * ldb + j0 + u] << (8 * u);
-                }
-            }
-            q[e] = v;
-        }
-        uint4* base = out + tk * (4 * 128) + c * 128 + rq * 4;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-                const float f0 = (float)(int8_t)(q[e] >> (8 * u)), f1 = (float)(int8_t)(q[e + 1] >> (8 * u));
-                w[e / 2] = (uint32_t)bf16_rn_bits(f0) | ((uint32_t)bf16_rn_bits(f1) << 16);
-            }
-            base[u] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-    }
-}
-
-// C tile (128 x 128) of split z from the pre-converted operands: thread 0 streams the stages
-// (one bulk copy per operand), thread 32 issues the MMAs.  Epilogue: the 4 warps move the TMEM
-// accumulator into a padded shared-memory tile; the CZ CTAs of a cluster (the split-K slices
-// z = CZ * c .. CZ * c + CZ - 1 of one output tile) then reduce their tiles through distributed
-// shared memory, CTA rank q owning rows [q * 128 / CZ, (q + 1) * 128 / CZ), adding the slices
-// in rank order (deterministic), and write those rows with coalesced 512-byte row stores --
-// to C (scaled, masked) when the cluster covers every slice, else (scaled) to partial slot c of
-// the workspace for ste_reduce_kernel.
-template <bool PCS>
-__global__ void __launch_bounds__(128) ste_pp_kernel(int64_t M, int64_t N, int64_t KT, const uint4* __restrict__ Ap,
-                                                     const uint4* __restrict__ Bp, const float* __restrict__ s_b,
-                                                     float* __restrict__ C, int64_t ldc, const float* __restrict__ R,
-                                                     int64_t ldr, const float* __restrict__ clip, int clip_vec,
-                                                     int64_t kts_per_split, int CZ) {
-    using namespace stepp;
-    extern __shared__ __align__(1024) uint8_t pp_smem[];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t mt = blockIdx.x, nt = blockIdx.y;
-    const int64_t kt0 = (int64_t)blockIdx.z * kts_per_split, kt1 = min(KT, kt0 + kts_per_split);
-    const int nkt = (int)max((int64_t)0, kt1 - kt0);
-    const bool final_out = (int)gridDim.z == CZ;           // the cluster holds every K slice
-    if (!final_out) C += (int64_t)(blockIdx.z / CZ) * M * ldc;
-    const uint32_t s_base = smem_u32(pp_smem);
-    const uint32_t bar_full = s_base + STAGES * STAGE, bar_mma = bar_full + 8 * STAGES;
-    const uint32_t bar_done = bar_mma + 8 * STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pp_smem + STAGES * STAGE + 16 * STAGES + 8);
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_mma + 8 * s, 1);
-        }
-        mbar_init(bar_done, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                     "n"(BN) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-    if (tid == 0) {
-        // producer: stage s <- k tile kt0 + s (A' 24 KiB + B' 8 KiB, two bulk copies)
-        for (int s = 0; s < nkt; ++s) {
-            const int buf = s % STAGES;
-            if (s >= STAGES) mbar_wait(bar_mma + 8 * buf, ((s / STAGES) - 1) & 1u);
-            const uint32_t bar = bar_full + 8 * buf;
-            mbar_expect_tx(bar, STAGE);
-            const int64_t kt = kt0 + s;
-            bulk_g2s(s_base + buf * STAGE, Ap + (mt * KT + kt) * (3 * 4 * 128), TILE_A, bar);
-            bulk_g2s(s_base + buf * STAGE + TILE_A, Bp + (nt * KT + kt) * (4 * 128), TILE_B, bar);
-        }
-    } else if (tid == 32) {
-        // MMA issuer: 3 terms x 2 K steps of 16 per stage into one TMEM accumulator
-        for (int s = 0; s < nkt; ++s) {
-            const int buf = s % STAGES;
-            mbar_wait(bar_full + 8 * buf, (s / STAGES) & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t sa = s_base + buf * STAGE, sbb = sa + TILE_A;
-#pragma unroll
-            for (int t = 0; t < 3; ++t)
-#pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk) {
-                    const uint64_t ad = ste_desc(sa + t * (TILE_A / 3) + kk * 2 * BM * 16, BM * 16, 128);
-                    const uint64_t bd = ste_desc(sbb + kk * 2 * BN * 16, BN * 16, 128);
-                    const uint32_t acc = (s > 0 || t > 0 || kk > 0) ? 1u : 0u;
-                    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                                 "l"(ad), "l"(bd), "r"(IDESC), "r"(acc)
-                                 : "memory");
-                }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             bar_mma + 8 * buf) : "memory");
-        }
-        if (nkt > 0)
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             bar_done) : "memory");
-    }
-    // everyone waits for all MMAs: one more commit onto bar_done (single phase; a per-stage
-    // barrier's parity would alias with its phase STAGES stages earlier)
-    if (nkt > 0) mbar_wait(bar_done, 0u);
-    __syncwarp();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    // TMEM -> shared tile T[128][TS] (row = TMEM lane; the stage buffers are idle now)
-    float* T = reinterpret_cast<float*>(pp_smem);
-    {
-        const int r = warp * 32 + lane;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t v[16];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            if (nkt == 0) {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = 0u;
-            }
-            float4* dst = reinterpret_cast<float4*>(T + r * TS + c0);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                dst[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
-                                     __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    uint32_t q = 0;
-    if (CZ > 1) {
-        asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(q));
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    } else {
-        __syncthreads();
-    }
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(BN) : "memory");
-    // rows [r0, r1) of the tile: lane l owns columns 4l .. 4l + 3, a warp one row at a time
-    const int r0 = (int)(q * BM / CZ), r1 = (int)((q + 1) * BM / CZ);
-    const float sb = PCS ? 1.f : *s_b;
-    const bool apply_mask = R && final_out;
-    const int64_t j = nt * BN + 4 * lane;
-    const bool vec = j + 4 <= N && (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
-    const uint32_t t_base = smem_u32(T);
-    for (int r = r0 + warp; r < r1; r += 4) {
-        const int64_t i = mt * BM + r;
-        if (i >= M) break;
-        const uint32_t a = t_base + (uint32_t)(r * TS + 4 * lane) * 4u;
-        float4 x;
-        if (CZ == 1) {
-            x = *reinterpret_cast<const float4*>(T + r * TS + 4 * lane);
-        } else {
-            x = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int z = 0; z < CZ; ++z) {
-                uint32_t ra;
-                float4 y;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(a), "r"(z));
-                asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];\n"
-                             : "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w) : "r"(ra) : "memory");
-                if (z == 0) {
-                    x = y;
-                } else {
-                    x.x = __fadd_rn(x.x, y.x); x.y = __fadd_rn(x.y, y.y);
-                    x.z = __fadd_rn(x.z, y.z); x.w = __fadd_rn(x.w, y.w);
-                }
-            }
-        }
-        if (!PCS) {
-            x.x = __fmul_rn(x.x, sb); x.y = __fmul_rn(x.y, sb);
-            x.z = __fmul_rn(x.z, sb); x.w = __fmul_rn(x.w, sb);
-        }
-        if (apply_mask) {
-            const float cl = clip_vec ? clip[i] : *clip;
-            const float* rr = R + i * ldr + j;
-            if (j + 0 < N && !(fabsf(rr[0]) <= cl)) x.x = 0.f;
-            if (j + 1 < N && !(fabsf(rr[1]) <= cl)) x.y = 0.f;
-            if (j + 2 < N && !(fabsf(rr[2]) <= cl)) x.z = 0.f;
-            if (j + 3 < N && !(fabsf(rr[3]) <= cl)) x.w = 0.f;
-        }
-        float* crow = C + i * ldc + j;
-        if (vec) {
-            *reinterpret_cast<float4*>(crow) = x;
-        } else {
-            if (j + 0 < N) crow[0] = x.x;
-            if (j + 1 < N) crow[1] = x.y;
-            if (j + 2 < N) crow[2] = x.z;
-            if (j + 3 < N) crow[3] = x.w;
-        }
-    }
-    if (CZ > 1)   // keep this CTA's tile alive until every rank of the cluster has read it
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
 // C[i] = mask(i) * sum_{z < S} part[z][i], the splits added in order (deterministic); clip_vec:
 // the clip is per row (clip[i / N], a per-channel weight clip), else one scalar
 __global__ void ste_reduce_kernel(int S, int64_t MN, int64_t N, const float* __restrict__ part,
@@ -653,9 +360,8 @@ __global__ void ste_reduce_kernel(int S, int64_t MN, int64_t N, const float* __r
 }
 
 // Column sums over many rows, deterministic: block (column group of 32, row block rb) sums its
-// rows per warp (rows w, w + 8, ...), the 8 warps in order, into part[rb][n]; ste_colsum_kernel
-// then adds the row blocks in order.
-constexpr int COLSUM_RB = 128;
+// rows per warp (rows w, w + 8, ...), the 8 warps in order, into part[rb][n]; run again over
+// part with one row block it adds the row blocks in order.
 __global__ void __launch_bounds__(256) ste_colsum_part_kernel(int64_t M, int64_t N, const float* __restrict__ gy,
                                                               int64_t ldg, float* __restrict__ part) {
     __shared__ float red[8][33];
@@ -663,8 +369,10 @@ __global__ void __launch_bounds__(256) ste_colsum_part_kernel(int64_t M, int64_t
     const int64_t n = (int64_t)blockIdx.x * 32 + lane;
     const int64_t rows = (M + gridDim.y - 1) / gridDim.y, r0 = (int64_t)blockIdx.y * rows, r1 = min(M, r0 + rows);
     float s = 0.f;
-    if (n < N)
-        for (int64_t m = r0 + warp; m < r1; m += 8) s = __fadd_rn(s, gy[m * ldg + n]);
+    if (n < N) {
+#pragma unroll 8
+        for (int64_t m = r0 + warp; m < r1; m += 8) s = __fadd_rn(s, __ldg(gy + m * ldg + n));
+    }
     red[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && n < N) {
@@ -674,114 +382,39 @@ __global__ void __launch_bounds__(256) ste_colsum_part_kernel(int64_t M, int64_t
     }
 }
 
-// gb[n] = sum_m gy[m][n], sequential in m (one thread per column, coalesced rows)
-__global__ void ste_colsum_kernel(int64_t M, int64_t N, const float* __restrict__ gy, int64_t ldg,
-                                  float* __restrict__ gb) {
-    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= N) return;
-    float s = 0.f;
-    for (int64_t m = 0; m < M; ++m) s = __fadd_rn(s, gy[m * ldg + n]);
-    gb[n] = s;
-}
 
 }  // namespace axq
 
+#include "ste_pp.cuh"
 
 namespace axq {
-// Plan of the pre-converted path of one STE product (see stepp): the workspace holds, in order,
-// the split-K partial slots (slots x Mg x ldc fp32, slots > 1 only), A' and B'.  K slices: ~2
-// CTAs per SM, >= 4 k tiles each; up to 8 slices reduce inside a cluster (distributed shared
-// memory), beyond that clusters of 8 write partial slots that ste_reduce_kernel adds in order.
-struct PrepPlan {
-    int64_t Mt, Nt, KT, a_elems, b_elems, S, CZ, slots, kps, part, need;
-};
-static int64_t round32(int64_t e) { return (e + 31) / 32 * 32; }
-static bool ste_prep_plan(int64_t Mg, int64_t Ng, int64_t Kg, int64_t ldc, int sms, int64_t workspace_elems,
-                          PrepPlan& pl) {
-    using namespace stepp;
-    pl.Mt = (Mg + BM - 1) / BM;
-    pl.Nt = (Ng + BN - 1) / BN;
-    pl.KT = (Kg + BK - 1) / BK;
-    if (pl.Nt > 65535 || pl.Mt > 0x7fffffff || pl.KT == 0) return false;
-    pl.a_elems = pl.Mt * pl.KT * (TILE_A / 4);
-    pl.b_elems = pl.Nt * pl.KT * (TILE_B / 4);
-    const int64_t ab = round32(pl.a_elems) + round32(pl.b_elems);
-    if (workspace_elems < ab) return false;
-    const int64_t tiles = pl.Mt * pl.Nt;
-    int64_t S = std::min<int64_t>({(2 * (int64_t)sms + tiles - 1) / tiles, 128, std::max<int64_t>(1, pl.KT / 4)});
-    pl.CZ = std::min<int64_t>(S, 8);
-    if (S > 8) {
-        const int64_t room = (workspace_elems - ab) / std::max<int64_t>(1, round32(Mg * ldc));
-        const int64_t slots = std::min<int64_t>((S + 7) / 8, room);
-        S = slots >= 2 ? slots * 8 : 8;
-    }
-    pl.kps = (pl.KT + S - 1) / S;
-    if (S > 8) {   // drop whole clusters that would hold no k tile
-        S = (pl.KT + pl.kps - 1) / pl.kps;
-        S = std::max<int64_t>(8, (S + 7) / 8 * 8);
-    }
-    pl.S = S;
-    pl.slots = S / pl.CZ;
-    pl.part = pl.slots > 1 ? round32(pl.slots * Mg * ldc) : 0;
-    pl.need = pl.part + ab;
-    return pl.need <= workspace_elems;
-}
-
+// The pre-converted path of one product on its own (prep launch + GEMM launch [+ reduce]):
+// the workspace holds the partial slots (slots > 1 only), A' and B'.  Returns false (nothing
+// launched) when the workspace cannot hold A' and B' -- the caller then runs ste_tc_kernel.
 static bool ste_prep_product(bool ta, int64_t Mg, int64_t Ng, int64_t Kg, const float* A, int64_t lda,
                              const int8_t* B, int64_t ldb, const float* sB, bool sB_vec, float* C, int64_t ldc,
                              const float* R, const float* clip, bool clip_vec, float* workspace,
                              int64_t workspace_elems, int sms, cudaStream_t st) {
-    using namespace stepp;
     PrepPlan pl;
-    if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return false;
-    if (!ste_prep_plan(Mg, Ng, Kg, ldc, sms, workspace_elems, pl)) return false;
-    const int64_t Mt = pl.Mt, Nt = pl.Nt, KT = pl.KT, S = pl.S, slots = pl.slots, kps = pl.kps;
-    const int CZ = (int)pl.CZ;
+    if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return false;
+    if (!pp_plan(Mg, Ng, Kg, ldc, sms, 0, pl)) return false;
+    const int64_t ab = pp_ab_elems(pl);
+    if (workspace_elems < ab) return false;
+    if (!pp_plan(Mg, Ng, Kg, ldc, sms, workspace_elems - ab, pl)) return false;
     uint4* Ap = reinterpret_cast<uint4*>(workspace + pl.part);
     uint4* Bp = reinterpret_cast<uint4*>(workspace + pl.part + round32(pl.a_elems));
-    static unsigned configured = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(configured & (1u << (dev & 31)))) {
-        cudaFuncSetAttribute(ste_pp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaFuncSetAttribute(ste_pp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        configured |= 1u << (dev & 31);
-    }
-    const unsigned pg = (unsigned)std::min<int64_t>((Mt * KT * 512 + 255) / 256, 16 * (int64_t)sms);
-    const int avec = ((lda & 3) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0;
-    if (ta) {
-        if (sB_vec) ste_prep_a_kernel<true, true><<<pg, 256, 0, st>>>(Mg, Kg, A, lda, sB, KT, avec, Ap);
-        else ste_prep_a_kernel<true, false><<<pg, 256, 0, st>>>(Mg, Kg, A, lda, sB, KT, avec, Ap);
-    } else {
-        if (sB_vec) ste_prep_a_kernel<false, true><<<pg, 256, 0, st>>>(Mg, Kg, A, lda, sB, KT, avec, Ap);
-        else ste_prep_a_kernel<false, false><<<pg, 256, 0, st>>>(Mg, Kg, A, lda, sB, KT, avec, Ap);
-    }
-    const unsigned pb = (unsigned)std::min<int64_t>((Nt * KT * 128 + 255) / 256, 16 * (int64_t)sms);
-    const int bvec = ((ldb & 3) == 0 && (reinterpret_cast<uintptr_t>(B) & 3) == 0) ? 1 : 0;
-    ste_prep_b_kernel<<<pb, 256, 0, st>>>(Ng, Kg, B, ldb, KT, bvec, Bp);
-    float* out = slots > 1 ? workspace : C;
-    const int cv = clip_vec ? 1 : 0;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)Mt, (unsigned)Nt, (unsigned)S);
-    cfg.blockDim = dim3(128, 1, 1);
-    cfg.dynamicSmemBytes = SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = (unsigned)CZ;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (sB_vec)
-        cudaLaunchKernelEx(&cfg, ste_pp_kernel<true>, Mg, Ng, KT, (const uint4*)Ap, (const uint4*)Bp, sB, out, ldc, R, ldc,
-                           clip, cv, kps, CZ);
-    else
-        cudaLaunchKernelEx(&cfg, ste_pp_kernel<false>, Mg, Ng, KT, (const uint4*)Ap, (const uint4*)Bp, sB, out, ldc, R,
-                           ldc, clip, cv, kps, CZ);
-    if (slots > 1)
+    stepp::PrepArgs pa{};
+    pa.job[0] = pp_job_a(ta, Mg, Kg, A, lda, sB, sB_vec, pl.KT, Ap, sms);
+    pa.job[1] = pp_job_b(Ng, Kg, B, ldb, pl.KT, Bp, sms);
+    pa.njobs = 2;
+    pp_launch_prep(pa, st);
+    stepp::GemmArgs ga{};
+    ga.job[0] = pp_job_gemm(pl, Mg, Ng, ldc, Ap, Bp, sB, sB_vec, pl.slots > 1 ? workspace : C, R, clip, clip_vec, 0);
+    ga.njobs = 1;
+    pp_launch_gemm(ga, pl.CZ, pp_ctas(pl, pl.CZ), st);
+    if (pl.slots > 1)
         ste_reduce_kernel<<<(unsigned)std::min<int64_t>((Mg * ldc + 255) / 256, 8 * sms), 256, 0, st>>>(
-            (int)slots, Mg * ldc, Ng, workspace, C, R, clip, cv);
+            (int)pl.slots, Mg * ldc, Ng, workspace, C, R, clip, clip_vec ? 1 : 0);
     return true;
 }
 
@@ -847,17 +480,22 @@ static void ste_product(bool ta, int64_t Mg, int64_t Ng, int64_t Kg, const float
             (int)S, Mg * ldc, Ng, workspace, C, R, clip, cv);
 }
 
-// gb = column sums of gy [M][N], deterministic: RB row blocks (a function of M and N only, sized
-// for ~2 blocks per SM of a 148-SM part) summed by ste_colsum_part_kernel, then added in order;
-// RB = 1 (or no workspace for the RB x N partials): one pass straight into gb.
+// gb = column sums of gy [M][N], deterministic: RB = ceil(M / 128) row blocks (a function of M
+// only, <= 1024; ~16 rows per warp) summed by ste_colsum_part_kernel into RB x N partials, which
+// the same kernel then adds in order (one row block); RB < 4 (or no workspace for the
+// partials): one pass straight into gb.
+static int64_t ste_colsum_rb(int64_t M) {
+    const int64_t RB = std::min<int64_t>(1024, (M + 127) / 128);
+    return RB >= 4 ? RB : 1;
+}
 static void ste_colsum(int64_t M, int64_t N, const float* gy, float* gb, float* workspace, int64_t workspace_elems,
                        cudaStream_t st) {
     const int64_t cg = (N + 31) / 32;
-    int64_t RB = std::min<int64_t>({(296 + cg - 1) / cg, COLSUM_RB, (M + 255) / 256});
-    if (RB < 2 || !workspace || workspace_elems < RB * N) RB = 1;
+    int64_t RB = ste_colsum_rb(M);
+    if (!workspace || workspace_elems < RB * N) RB = 1;
     if (RB > 1) {
         ste_colsum_part_kernel<<<dim3((unsigned)cg, (unsigned)RB), 256, 0, st>>>(M, N, gy, N, workspace);
-        ste_colsum_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(RB, N, workspace, N, gb);
+        ste_colsum_part_kernel<<<dim3((unsigned)cg, 1), 256, 0, st>>>(RB, N, workspace, N, gb);
     } else {
         ste_colsum_part_kernel<<<dim3((unsigned)cg, 1), 256, 0, st>>>(M, N, gy, N, gb);
     }
@@ -950,15 +588,47 @@ static int ste_sms() {
 }
 static int64_t ste_colsum_need(int64_t M, int64_t N) {
     if (M <= 0 || N <= 0) return 0;
-    const int64_t cg = (N + 31) / 32;
-    const int64_t RB = std::min<int64_t>({(296 + cg - 1) / cg, COLSUM_RB, (M + 255) / 256});
-    return RB >= 2 ? RB * N : 0;
+    const int64_t RB = ste_colsum_rb(M);
+    return RB > 1 ? RB * N : 0;
 }
 static int64_t ste_product_need(int64_t Mg, int64_t Ng, int64_t Kg, int64_t ldc, int sms) {
     PrepPlan pl;
     if (Mg <= 0 || Ng <= 0 || Kg <= 0) return 0;
-    if (!ste_prep_plan(Mg, Ng, Kg, ldc, sms, INT64_MAX / 4, pl)) return 0;
-    return pl.need;
+    if (!pp_plan(Mg, Ng, Kg, ldc, sms, INT64_MAX / 4, pl)) return 0;
+    return pl.part + pp_ab_elems(pl);
+}
+
+// The fused linear backward (one prep launch, one GEMM launch for gx and gw): both products
+// with at most 8 K slices, sharing the larger cluster size.  Workspace: A'x B'x A'w B'w, then the
+// column-sum partials.
+struct FusedPlan {
+    bool ok;
+    PrepPlan px, pw;
+    int64_t cz, rb, need;
+};
+static FusedPlan ste_fused_plan(int64_t M, int64_t N, int64_t K, bool hx, bool hw, bool hb, int sms) {
+    FusedPlan f{};
+    if (K <= 0 || (!hx && !hw)) return f;
+    // room 0: a product wanting more than one cluster of slices gets exactly one (S = CZ); one
+    // wanting more than 8 (a long summed dimension) runs alone with partial slots instead
+    if (hx && (!pp_plan(M, K, N, K, sms, 0, f.px) || f.px.S0 > 8)) return f;
+    if (hw && (!pp_plan(N, K, M, K, sms, 0, f.pw) || f.pw.S0 > 8)) return f;
+    // slices for the launch as a whole: ~2 CTAs per SM over both products' tiles (a power of two
+    // <= the cluster cap), each product capped at >= 4 k tiles per slice
+    const int64_t tiles = (hx ? f.px.Mt * f.px.Nt : 0) + (hw ? f.pw.Mt * f.pw.Nt : 0);
+    int64_t S = 1;
+    while (S < pp_max_cz() && S * tiles < 2 * (int64_t)sms) S *= 2;
+    auto cap = [](const PrepPlan& p, int64_t s) {
+        while (s > 1 && s * 4 > p.KT) s /= 2;
+        return s;
+    };
+    if (hx) pp_set_s(f.px, cap(f.px, S));
+    if (hw) pp_set_s(f.pw, cap(f.pw, S));
+    f.cz = std::max<int64_t>(hx ? f.px.CZ : 1, hw ? f.pw.CZ : 1);   // each keeps its own S <= cz
+    f.rb = hb ? ste_colsum_rb(M) : 1;
+    f.need = (hx ? pp_ab_elems(f.px) : 0) + (hw ? pp_ab_elems(f.pw) : 0) + (f.rb > 1 ? round32(f.rb * N) : 0);
+    f.ok = true;
+    return f;
 }
 }  // namespace axq
 
@@ -967,7 +637,8 @@ extern "C" int64_t axq_ste_linear_workspace_elems(int64_t M, int64_t N, int64_t 
     if (M < 0 || N < 0 || K < 0 || M >= ((int64_t)1 << 40) || N >= ((int64_t)1 << 40) || K >= ((int64_t)1 << 40))
         return -1;
     const int sms = ste_sms();
-    return std::max<int64_t>({ste_product_need(M, K, N, K, sms), ste_product_need(N, K, M, K, sms),
+    const FusedPlan f = ste_fused_plan(M, N, K, true, true, true, sms);
+    return std::max<int64_t>({f.ok ? f.need : 0, ste_product_need(M, K, N, K, sms), ste_product_need(N, K, M, K, sms),
                               ste_colsum_need(M, N), 0});
 }
 
@@ -1009,6 +680,44 @@ extern "C" axq_status axq_ste_linear_backward_pc(int64_t M, int64_t N, int64_t K
     if (gw && (!qa || !d_scale_a || (w && !cw))) return AXQ_ERR_INVALID;
     if ((K + 127) / 128 > 65535 || (N + 127) / 128 > 65535) return AXQ_ERR_UNSUPPORTED;   // column tiles: grid.y
     cudaStream_t st = (cudaStream_t)stream;
+    static const bool noprep = std::getenv("AXQ_STE_NOPREP") != nullptr;   // A/B: the in-kernel conversion
+    const int sms = ste_sms();
+    const FusedPlan f = ste_fused_plan(M, N, K, gx != nullptr, gw != nullptr, gb != nullptr, sms);
+    if (!noprep && f.ok && workspace && (reinterpret_cast<uintptr_t>(workspace) & 15) == 0 &&
+        workspace_elems >= f.need) {
+        // one prep launch (A', B' of both products + the first column-sum pass), one GEMM launch
+        float* wp = workspace;
+        stepp::PrepArgs pa{};
+        stepp::GemmArgs ga{};
+        int64_t ctas = 0;
+        if (gx) {   // gx[m][k] = mask * sum_n gy[m][n] * fq(qw)[n][k]
+            uint4* Ap = reinterpret_cast<uint4*>(wp);
+            uint4* Bp = reinterpret_cast<uint4*>(wp + round32(f.px.a_elems));
+            wp += pp_ab_elems(f.px);
+            pa.job[pa.njobs++] = pp_job_a(false, M, N, gy, N, sw, d_scale_w_ch != nullptr, f.px.KT, Ap, sms);
+            pa.job[pa.njobs++] = pp_job_b(K, N, qw, K, f.px.KT, Bp, sms);
+            ga.job[ga.njobs++] = pp_job_gemm(f.px, M, K, K, Ap, Bp, sw, d_scale_w_ch != nullptr, gx, x, d_clip_a,
+                                             false, ctas);
+            ctas += pp_ctas(f.px, f.cz);
+        }
+        if (gw) {   // gw[n][k] = mask * sum_m gy[m][n] * fq(qa)[m][k]
+            uint4* Ap = reinterpret_cast<uint4*>(wp);
+            uint4* Bp = reinterpret_cast<uint4*>(wp + round32(f.pw.a_elems));
+            wp += pp_ab_elems(f.pw);
+            pa.job[pa.njobs++] = pp_job_a(true, N, M, gy, N, d_scale_a, false, f.pw.KT, Ap, sms);
+            pa.job[pa.njobs++] = pp_job_b(K, M, qa, K, f.pw.KT, Bp, sms);
+            ga.job[ga.njobs++] = pp_job_gemm(f.pw, N, K, K, Ap, Bp, d_scale_a, false, gw, w, cw,
+                                             d_clip_w_ch != nullptr, ctas);
+            ctas += pp_ctas(f.pw, f.cz);
+        }
+        if (gb) pa.job[pa.njobs++] = pp_job_colsum(M, N, gy, f.rb, f.rb > 1 ? wp : gb, sms);
+        pp_launch_prep(pa, st);
+        pp_launch_gemm(ga, f.cz, ctas, st);
+        if (gb && f.rb > 1)
+            ste_colsum_part_kernel<<<dim3((unsigned)((N + 31) / 32), 1), 256, 0, st>>>(f.rb, N, wp, N, gb);
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
+    }
     if (gx && K > 0)
         ste_product(false, M, K, N, gy, N, qw, K, sw, d_scale_w_ch != nullptr, gx, K, x, d_clip_a, false, workspace,
                     workspace_elems, st);
