@@ -127,21 +127,28 @@ __global__ void __launch_bounds__(wpk::NT, 1) lut_widepk_kernel(const __grid_con
 #pragma unroll
                 for (int j = 0; j < 4; ++j) ex[r][q][j] = 0;
             }
-        uint4 acode[R];
-        for (int k8 = 0; k8 < (int)P.Kp; k8 += 8) {
-            // 8 codes per row, zero beyond K (a padded k looks up a = 0)
+        // 8 codes per row, zero beyond K (a padded k looks up a = 0); loaded one k8 step ahead
+        auto load_codes = [&](int k8, uint4 (&dst)[R]) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int16_t* src = P.A + (valid[r] ? mrow[r] : 0) * P.lda + k8;
                 if (valid[r] && k8 + 8 <= P.K && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-                    acode[r] = __ldg(reinterpret_cast<const uint4*>(src));
+                    dst[r] = __ldg(reinterpret_cast<const uint4*>(src));
                 } else {
                     uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
                     for (int j = 0; j < 8; ++j)
                         if (valid[r] && k8 + j < P.K) w[j >> 1] |= (uint32_t)(uint16_t)src[j] << (16 * (j & 1));
-                    acode[r] = make_uint4(w[0], w[1], w[2], w[3]);
+                    dst[r] = make_uint4(w[0], w[1], w[2], w[3]);
                 }
             }
+        };
+        uint4 acode[R], anext[R];
+        load_codes(0, anext);
+        for (int k8 = 0; k8 < (int)P.Kp; k8 += 8) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) acode[r] = anext[r];
+            if (k8 + 8 < (int)P.Kp) load_codes(k8 + 8, anext);
 #pragma unroll
             for (int sub = 0; sub < 8 / KS; ++sub, ++item) {
                 const int buf = (int)(item % STAGES);
