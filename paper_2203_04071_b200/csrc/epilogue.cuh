@@ -72,6 +72,16 @@ __device__ __forceinline__ int8_t epi_quant_r(float v, float s, float r, float q
     return epi_quant(v, s, qm);
 }
 
+// epi_quant_r for v >= 0 (a ReLU output: +0 or positive, never NaN), bit-identical to
+// epi_quant: the same boundary test without the sign cases; returns the code as 0..qm
+__device__ __forceinline__ uint32_t epi_quant_r_nn(float v, float s, float r, float qm) {
+    const float t = __fmul_rn(v, r);
+    const float ti = rintf(t);
+    if (t >= qm + 0.75f || fabsf(t - ti) <= __fsub_rn(0.5f, __fmul_rn(t, 4.76837158e-7f)))
+        return (uint32_t)__float2int_rn(fminf(ti, qm));
+    return (uint32_t)(int)epi_quant(v, s, qm);
+}
+
 __device__ __forceinline__ void epi_store(float v, int64_t m, int64_t n, int64_t N,
                                           const EpiArgs& e, float s_out, float qm) {
     if (e.y) {

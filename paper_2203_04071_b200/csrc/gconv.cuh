@@ -214,16 +214,17 @@ __global__ void __launch_bounds__(256) lut_dwconv_kernel(const GConvArgs a) {
 namespace dw3 {
 constexpr int CB = 16;                     // channels per CTA (one per warp)
 constexpr int NT = CB * 32;
-constexpr int RB = 8;                      // input rows staged per batch
+constexpr int RB = 15;                     // input rows staged per batch (RB * PX <= NT stagers)
 constexpr int PX = 34;                     // staged pixels per row (32 lanes + 2 spare)
 constexpr int PS = 20;                     // staged pixel stride (bytes): 5 words, conflict-free
 constexpr int QS = 20;                     // code tile pixel stride (bytes)
 constexpr int YS = 17;                     // fp32 tile pixel stride (words)
 constexpr int TAB = CB * 3 * 256 * 4;      // 48 KiB of packed tables
 constexpr int IN = RB * PX * PS;           // one staged batch of input rows
-constexpr int OUT = RB * 30 * CB * 4;      // int32 results (generic epilogue) / fp32 y tile
+constexpr int OUT = RB * 30 * YS * 4;      // int32 results [RB][CB][30] (generic) / fp32 y tile [RB][30][YS] (fast)
 constexpr int QT = RB * 30 * QS;           // int8 code tile
 constexpr int SMEM = TAB + IN + OUT + QT;
+static_assert(RB * PX <= NT, "one staging thread per staged pixel");
 }  // namespace dw3
 
 __device__ __forceinline__ uint32_t dw3_lds_u8(uint32_t addr) {
@@ -311,6 +312,8 @@ static __global__ void __launch_bounds__(dw3::NT, 2) lut_dw3_kernel(const GConvA
         }
         const float sc_c = (!a.C_out && cvalid) ? epi_sc(a.ep, sc, c) : 0.f;
         const float b_c = (!a.C_out && a.ep.bias && cvalid) ? a.ep.bias[c] : 0.f;
+        // QR: this lane's code slot in the tile (output column lane - 1, channel warp)
+        const uint32_t tq_lane = (uint32_t)__cvta_generic_to_shared(tq) + (uint32_t)((lane - 1) * QS + warp);
         const int w0 = strip * 30;                 // first output column of the strip
         const int ncols = min(30, a.Wo - w0);
         const int8_t* xb = a.X + (int64_t)n * a.H * a.Wd * a.C + c0;
@@ -341,7 +344,7 @@ static __global__ void __launch_bounds__(dw3::NT, 2) lut_dw3_kernel(const GConvA
             }
             __syncthreads();                        // staged rows visible; last batch's tiles consumed
             if (hb + RB <= a.H) fetch(hb + RB, pf); // next batch in flight during this one
-#pragma unroll 1
+#pragma unroll 2
             for (int rr = 0; rr < RB; ++rr) {
                 const int hi = hb + rr;
                 if (hi > a.H) break;
@@ -364,14 +367,19 @@ static __global__ void __launch_bounds__(dw3::NT, 2) lut_dw3_kernel(const GConvA
                 acc_n = __dp4a((int)codes, (int)wr[0], (int)__dp4a(g0, 0x00010101u, (unsigned)acc_n));
                 acc_c = __dp4a((int)codes, (int)wr[1], (int)__dp4a(g1, 0x00010101u, (unsigned)acc_c));
                 acc_p = __dp4a((int)codes, (int)wr[2], (int)__dp4a(g2, 0x00010101u, (unsigned)acc_p));
-                if (lane >= 1 && lane <= 30) {
+                if (QR) {
+                    // output row hi - 1 is complete: every lane computes (no divergence), lanes
+                    // 1..30 store; + b_c (0 without a bias) only turns -0 into +0, as the ReLU does
+                    const int v = acc_p - 9 * 128;
+                    float y = __fadd_rn(__fmul_rn(__int2float_rn(v), sc_c), b_c);
+                    y = y > 0.f ? y : 0.f;
+                    const uint32_t qv = epi_quant_r_nn(y, s_out, r_out, qm);
+                    if (lane >= 1 && lane <= 30)
+                        asm volatile("st.shared.u8 [%0], %1;\n" ::"r"(tq_lane + (uint32_t)(rr * 30 * QS)), "r"(qv)
+                                     : "memory");
+                } else if (lane >= 1 && lane <= 30) {
                     const int v = acc_p - 9 * 128;  // output row hi - 1 is complete
-                    if (QR) {
-                        float y = __fmul_rn(__int2float_rn(v), sc_c);
-                        if (a.ep.bias) y = __fadd_rn(y, b_c);
-                        y = y > 0.f ? y : 0.f;
-                        tq[(rr * 30 + lane - 1) * QS + warp] = (uint8_t)epi_quant_r(y, s_out, r_out, qm);
-                    } else if (fast) {
+                    if (fast) {
                         float y = __fmul_rn(__int2float_rn(v), sc_c);
                         if (a.ep.bias) y = __fadd_rn(y, b_c);
                         if (a.ep.relu) y = y > 0.f ? y : 0.f;
