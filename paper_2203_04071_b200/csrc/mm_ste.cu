@@ -394,7 +394,8 @@ namespace axq {
 static bool ste_prep_product(bool ta, int64_t Mg, int64_t Ng, int64_t Kg, const float* A, int64_t lda,
                              const int8_t* B, int64_t ldb, const float* sB, bool sB_vec, float* C, int64_t ldc,
                              const float* R, const float* clip, bool clip_vec, float* workspace,
-                             int64_t workspace_elems, int sms, cudaStream_t st) {
+                             int64_t workspace_elems, int sms, cudaStream_t st,
+                             const stepp::ConvGeo* conv_b = nullptr) {
     PrepPlan pl;
     if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return false;
     if (!pp_plan(Mg, Ng, Kg, ldc, sms, 0, pl)) return false;
@@ -405,7 +406,7 @@ static bool ste_prep_product(bool ta, int64_t Mg, int64_t Ng, int64_t Kg, const 
     uint4* Bp = reinterpret_cast<uint4*>(workspace + pl.part + round32(pl.a_elems));
     stepp::PrepArgs pa{};
     pa.job[0] = pp_job_a(ta, Mg, Kg, A, lda, sB, sB_vec, pl.KT, Ap, sms);
-    pa.job[1] = pp_job_b(Ng, Kg, B, ldb, pl.KT, Bp, sms);
+    pa.job[1] = conv_b ? pp_job_b_conv(Ng, Kg, B, *conv_b, pl.KT, Bp, sms) : pp_job_b(Ng, Kg, B, ldb, pl.KT, Bp, sms);
     pa.njobs = 2;
     pp_launch_prep(pa, st);
     stepp::GemmArgs ga{};
@@ -772,12 +773,22 @@ extern "C" axq_status axq_ste_conv2d_backward_pc(const axq_conv_desc* d, const f
         if (e == cudaSuccess && gb) e = cudaMemsetAsync(gb, 0, No * sizeof(float), st);
         return e == cudaSuccess ? AXQ_OK : cuda_fail_ext((int)e);
     }
+    static const bool noprep = std::getenv("AXQ_STE_NOPREP") != nullptr;
     if (gw) {   // gw[k][(r, s, c)] = mask * sum_m gy[m][k] * fq(im2col(qx)[m][(r, s, c)])
-        const axq_status r = axq_im2col_nhwc_i8(qx, d->N, d->H, d->W, d->C, 0, d->R, d->S, d->stride_h, d->stride_w,
-                                                d->pad_h, d->pad_w, cols, ldcols, stream);
-        if (r != AXQ_OK) return r;
-        ste_product(true, No, Kc, M, gy, No, cols, ldcols, d_scale_a, false, gw, Kc, w, cw, d_clip_w_ch != nullptr,
-                    workspace, workspace_elems, st);
+        // pre-converted path: B' gathered straight from qx (implicit im2col, cols unused);
+        // otherwise the explicit im2col into cols
+        const stepp::ConvGeo cg{(int)d->H, (int)d->W, (int)d->C, (int)Ho, (int)Wo, (int)d->stride_h,
+                                (int)d->stride_w, (int)d->pad_h, (int)d->pad_w, (int)d->S};
+        const bool small = d->H * d->W * d->C < ((int64_t)1 << 31);
+        if (noprep || !small ||
+            !ste_prep_product(true, No, Kc, M, gy, No, qx, 0, d_scale_a, false, gw, Kc, w, cw, d_clip_w_ch != nullptr,
+                              workspace, workspace_elems, ste_sms(), st, &cg)) {
+            const axq_status r = axq_im2col_nhwc_i8(qx, d->N, d->H, d->W, d->C, 0, d->R, d->S, d->stride_h,
+                                                    d->stride_w, d->pad_h, d->pad_w, cols, ldcols, stream);
+            if (r != AXQ_OK) return r;
+            ste_product(true, No, Kc, M, gy, No, cols, ldcols, d_scale_a, false, gw, Kc, w, cw, d_clip_w_ch != nullptr,
+                        workspace, workspace_elems, st);
+        }
     }
     if (gx) {   // gcols = gy . fq(W) [M][(r, s, c)], then the adjoint of im2col, masked
         ste_product(false, M, Kc, No, gy, No, qw, Kc, sw, d_scale_w_ch != nullptr, gcols, Kc, nullptr, nullptr, false,

@@ -32,7 +32,13 @@ static_assert(BM * TS * 4 <= STAGES * STAGE, "epilogue tile must fit the stage b
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
 
-enum PrepKind { PREP_A = 0, PREP_B = 1, PREP_COLSUM = 2 };
+enum PrepKind { PREP_A = 0, PREP_B = 1, PREP_COLSUM = 2, PREP_B_CONV = 3 };
+// implicit im2col for PREP_B_CONV: B[p][j] = x[n][ho*sh - ph + r][wo*sw - pw + s][c] (0 outside)
+// with p = (n, ho, wo) an output pixel and j = (r, s, c) a tap (the conv is the GEMM of
+// its im2col matrix) -- the gw operand read straight from the NHWC codes
+struct ConvGeo {
+    int H, W, C, Ho, Wo, sh, sw, ph, pw, S;
+};
 // one job of the prep launch (blocks: its share of the grid)
 struct PrepJob {
     int kind;
@@ -43,6 +49,7 @@ struct PrepJob {
     const float* s_b;
     void* out;
     int64_t blocks;
+    ConvGeo cg;             // PREP_B_CONV only
 };
 struct PrepArgs {
     PrepJob job[5];
@@ -164,6 +171,80 @@ __device__ __forceinline__ void pp_prep_b(const stepp::PrepJob& J, int64_t g0, i
     }
 }
 
+// B' from the NHWC codes through the implicit im2col (PREP_B_CONV; rows = R*S*C taps, K = the
+// output pixels, < 2^31): thread -> (4 taps j .. j + 3, chunk of 8 pixels); with C % 4 == 0 the 4
+// taps are 4 channels of one (r, s): one 4-byte load per pixel
+__device__ __forceinline__ void pp_prep_b_conv(const stepp::PrepJob& J, int64_t g0, int64_t gs) {
+    const int64_t Nc = J.rows, K = J.K, KT = J.KT;
+    const stepp::ConvGeo& g = J.cg;
+    const int8_t* __restrict__ X = static_cast<const int8_t*>(J.src);
+    uint4* __restrict__ out = static_cast<uint4*>(J.out);
+    const int64_t total = ((Nc + 127) / 128) * KT * 4 * 32;
+    const int hw = g.Ho * g.Wo;
+    const bool c4 = (g.C & 3) == 0 && J.vec;
+    for (int64_t gi = g0; gi < total; gi += gs) {
+        const int rq = (int)(gi & 31), c = (int)((gi >> 5) & 3);
+        const int64_t tk = gi >> 7;
+        const int64_t kt = tk % KT, nt = tk / KT;
+        const int64_t j0 = nt * 128 + rq * 4;
+        const int p0 = (int)(kt * 32 + c * 8);
+        // taps of j0 .. j0 + 3
+        int tr[4], ts[4], tc[4];
+        bool tv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = (int)(j0 + u < Nc ? j0 + u : Nc - 1);
+            const int rs = j / g.C;
+            tc[u] = j - rs * g.C;
+            tr[u] = rs / g.S;
+            ts[u] = rs - tr[u] * g.S;
+            tv[u] = j0 + u < Nc;
+        }
+        int n = p0 / hw, rem = p0 - n * hw;
+        int ho = rem / g.Wo, wo = rem - ho * g.Wo;
+        uint32_t q[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            uint32_t v = 0u;
+            if (p0 + e < K) {
+                const int hb = ho * g.sh - g.ph, wb = wo * g.sw - g.pw;
+                const int8_t* xb = X + (int64_t)n * g.H * g.W * g.C;
+                if (c4 && tv[3]) {
+                    const int hi = hb + tr[0], wi = wb + ts[0];
+                    if ((unsigned)hi < (unsigned)g.H && (unsigned)wi < (unsigned)g.W)
+                        v = __ldg(reinterpret_cast<const unsigned int*>(xb + ((int64_t)hi * g.W + wi) * g.C + tc[0]));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int hi = hb + tr[u], wi = wb + ts[u];
+                        if (tv[u] && (unsigned)hi < (unsigned)g.H && (unsigned)wi < (unsigned)g.W)
+                            v |= (uint32_t)(uint8_t)xb[((int64_t)hi * g.W + wi) * g.C + tc[u]] << (8 * u);
+                    }
+                }
+            }
+            q[e] = v;
+            if (++wo == g.Wo) {
+                wo = 0;
+                if (++ho == g.Ho) {
+                    ho = 0;
+                    ++n;
+                }
+            }
+        }
+        uint4* base = out + tk * (4 * 128) + c * 128 + rq * 4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+                const float f0 = (float)(int8_t)(q[e] >> (8 * u)), f1 = (float)(int8_t)(q[e + 1] >> (8 * u));
+                w[e / 2] = (uint32_t)bf16_rn_bits(f0) | ((uint32_t)bf16_rn_bits(f1) << 16);
+            }
+            base[u] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
 // column sums, first pass (the ste_colsum_part_kernel order): block (column group x, row block
 // y) of RB row blocks -> out[y][n] (RB = 1: out = gb)
 __device__ __forceinline__ void pp_colsum(const stepp::PrepJob& J, int64_t bid, float (*red)[33]) {
@@ -201,6 +282,7 @@ __global__ void __launch_bounds__(256) ste_prep_kernel(const __grid_constant__ s
     const int64_t bid = (int64_t)blockIdx.x - b0;
     if (J.kind == stepp::PREP_A) pp_prep_a(J, bid * 256 + threadIdx.x, J.blocks * 256);
     else if (J.kind == stepp::PREP_B) pp_prep_b(J, bid * 256 + threadIdx.x, J.blocks * 256);
+    else if (J.kind == stepp::PREP_B_CONV) pp_prep_b_conv(J, bid * 256 + threadIdx.x, J.blocks * 256);
     else pp_colsum(J, bid, red);
     // the GEMM launch (programmatic dependent launch) may start its prologue now; its producer
     // waits (griddepcontrol.wait) for this grid's completion before the first bulk copy
@@ -497,6 +579,14 @@ static stepp::PrepJob pp_job_b(int64_t Ng, int64_t Kg, const int8_t* B, int64_t 
     j.src = B;
     j.out = out;
     j.blocks = std::max<int64_t>(1, std::min<int64_t>(((Ng + 127) / 128 * KT * 128 + 255) / 256, 8 * (int64_t)sms));
+    return j;
+}
+static stepp::PrepJob pp_job_b_conv(int64_t Nc, int64_t Mp, const int8_t* X, const stepp::ConvGeo& cg, int64_t KT,
+                                    uint4* out, int sms) {
+    stepp::PrepJob j = pp_job_b(Nc, Mp, X, 0, KT, out, sms);
+    j.kind = stepp::PREP_B_CONV;
+    j.vec = (reinterpret_cast<uintptr_t>(X) & 3) == 0 ? 1 : 0;
+    j.cg = cg;
     return j;
 }
 static stepp::PrepJob pp_job_colsum(int64_t M, int64_t N, const float* gy, int64_t RB, float* out, int sms) {
