@@ -49,7 +49,13 @@ struct Shape {
 constexpr int CW = 28;
 constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots are sized for it)
 
-#ifndef P4W_ALU_QUADS     // quads whose adds run on the ALU pipe (the rest: multiply-adds by 1, FMA pipe)
+#ifndef P4W_IDP_QUADS     // quads summed by dp4a over byte-interleaved k pairs (FMA pipe, 32-bit sums)
+#define P4W_IDP_QUADS 4
+#endif
+#ifndef P4W_K4            // with all quads on dp4a: transpose 4 k x 4 columns, one dp4a per column per 4 k
+#define P4W_K4 1
+#endif
+#ifndef P4W_ALU_QUADS     // of the rest, quads whose adds run on the ALU pipe (else multiply-adds by 1, FMA pipe)
 #define P4W_ALU_QUADS 2
 #endif
 #ifndef P4W_SMALL_FULL_STAGES
@@ -349,9 +355,13 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             // (mod 2^32) and pacc[p][1] = sum (v >> 16); the low column's sum is
             // pacc[p][0] - 2^16 pacc[p][1] (mod 2^32, exact: both sums < 2^32).
             constexpr int NACC = E16 ? 8 : 4;
+            constexpr int IDQ = E16 ? 0 : P4W_IDP_QUADS;   // quads 0 .. IDQ-1: per-column 32-bit sums
             uint32_t pacc[NACC][2];
+            uint32_t iacc[IDQ > 0 ? IDQ : 1][4];
 #pragma unroll
             for (int q = 0; q < NACC; ++q) pacc[q][0] = pacc[q][1] = 0u;
+#pragma unroll
+            for (int q = 0; q < (IDQ > 0 ? IDQ : 1); ++q) iacc[q][0] = iacc[q][1] = iacc[q][2] = iacc[q][3] = 0u;
             bool e_first = true;
             for (int st = s_b; st < s_e; ++st, ++item) {
                 const int buf = (int)(item % STAGES);
@@ -379,6 +389,34 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                     for (int pl = 0; pl < NPL; ++pl) {
                         const uint4 av = *reinterpret_cast<const uint4*>(at + pl * (BM * 16) + tid * 16);
                         const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+                        if constexpr (!E16 && IDQ == 4 && P4W_K4) {
+                            // 4 k at a time: per quad the 4 words (k .. k+3) are transposed into one
+                            // word per column (6 PRMT) and summed by one dp4a each
+#pragma unroll
+                            for (int kk = 0; kk < 16; kk += 4) {
+                                uint32_t ra[4];
+#pragma unroll
+                                for (int i = 0; i < 4; ++i)
+                                    ra[i] = tb_addr + __byte_perm(aw[kk >> 2], 0u, 0x4440u + i) * 4u;
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    uint32_t v[4];
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i)
+                                        asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v[i])
+                                                     : "r"(ra[i] + (uint32_t)(((pl * 16 + kk + i) * G::NQ + q) * TQ)));
+                                    const uint32_t t0 = __byte_perm(v[0], v[1], 0x5140u);   // c0 k0, c0 k1, c1 k0, c1 k1
+                                    const uint32_t t1 = __byte_perm(v[2], v[3], 0x5140u);   // c0 k2, c0 k3, c1 k2, c1 k3
+                                    const uint32_t t2 = __byte_perm(v[0], v[1], 0x7362u);   // c2 ..., c3 ...
+                                    const uint32_t t3 = __byte_perm(v[2], v[3], 0x7362u);
+                                    iacc[q][0] = __dp4a(__byte_perm(t0, t1, 0x5410u), 0x01010101u, iacc[q][0]);
+                                    iacc[q][1] = __dp4a(__byte_perm(t0, t1, 0x7632u), 0x01010101u, iacc[q][1]);
+                                    iacc[q][2] = __dp4a(__byte_perm(t2, t3, 0x5410u), 0x01010101u, iacc[q][2]);
+                                    iacc[q][3] = __dp4a(__byte_perm(t2, t3, 0x7632u), 0x01010101u, iacc[q][3]);
+                                }
+                            }
+                            continue;
+                        }
 #pragma unroll
                         for (int kk = 0; kk < 16; kk += 2) {
                             const uint32_t ua0 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
@@ -394,10 +432,19 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                                 if constexpr (E16) {
                                     pacc[q][0] += v0 + v1;
                                     pacc[q][1] += __byte_perm(v0, 0u, 0x4432u) + __byte_perm(v1, 0u, 0x4432u);
+                                } else if (q < IDQ) {
+                                    // interleave the two k's bytes per column pair, then one dp4a per
+                                    // column adds both k (biased bytes, unsigned)
+                                    const uint32_t x01 = __byte_perm(v0, v1, 0x5140u);   // c0 k, c0 k+1, c1 k, c1 k+1
+                                    const uint32_t x23 = __byte_perm(v0, v1, 0x7362u);   // c2 ..., c3 ...
+                                    iacc[q][0] = __dp4a(x01, 0x00000101u, iacc[q][0]);
+                                    iacc[q][1] = __dp4a(x01, 0x01010000u, iacc[q][1]);
+                                    iacc[q][2] = __dp4a(x23, 0x00000101u, iacc[q][2]);
+                                    iacc[q][3] = __dp4a(x23, 0x01010000u, iacc[q][3]);
                                 } else {
                                     const uint32_t e0 = __byte_perm(v0, 0u, 0x4240u), e1 = __byte_perm(v1, 0u, 0x4240u);
                                     const uint32_t o0 = __byte_perm(v0, 0u, 0x4341u), o1 = __byte_perm(v1, 0u, 0x4341u);
-                                    if (q < P4W_ALU_QUADS) {     // ALU pipe: one 3-input add per accumulator
+                                    if (q < IDQ + P4W_ALU_QUADS) {     // ALU pipe: one 3-input add per accumulator
                                         pacc[q][0] += e0 + e1;
                                         pacc[q][1] += o0 + o1;
                                     } else {         // FMA pipe: multiply-adds by an opaque 1
@@ -432,11 +479,19 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                     } else {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            ev[4 * q + 0] += pacc[q][0] & 0xffffu;
-                            ev[4 * q + 2] += pacc[q][0] >> 16;
-                            ev[4 * q + 1] += pacc[q][1] & 0xffffu;
-                            ev[4 * q + 3] += pacc[q][1] >> 16;
-                            pacc[q][0] = pacc[q][1] = 0u;
+                            if (q < IDQ) {
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    ev[4 * q + j] += iacc[q < IDQ ? q : 0][j];
+                                    iacc[q < IDQ ? q : 0][j] = 0u;
+                                }
+                            } else {
+                                ev[4 * q + 0] += pacc[q][0] & 0xffffu;
+                                ev[4 * q + 2] += pacc[q][0] >> 16;
+                                ev[4 * q + 1] += pacc[q][1] & 0xffffu;
+                                ev[4 * q + 3] += pacc[q][1] >> 16;
+                                pacc[q][0] = pacc[q][1] = 0u;
+                            }
                         }
                     }
                     tmem_st16(t_e, ev);
