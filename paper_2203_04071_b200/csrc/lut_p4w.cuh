@@ -89,8 +89,8 @@ struct Geo {
     // full[S], empty[S], mma[S], tile_full[2], tmem_free[2], then tmem address, flag
     static constexpr int NBAR = 3 * STAGES + 4;
     static constexpr int SMEM_MISC = SMEM_BAR + 8 * NBAR;
-    static constexpr int SMEM_KC = SMEM_MISC + 16;                 // EpiConst (16 B)
-    static constexpr int SMEM_TAP = SMEM_KC + 16;
+    static constexpr int SMEM_KC = SMEM_MISC + 16;                 // EpiConst (32 B)
+    static constexpr int SMEM_TAP = SMEM_KC + 32;
     static constexpr int SMEM_BYTES = SMEM_TAP + (HAS_TAP ? p4::TAP_BYTES : 0);
     static_assert(SMEM_BYTES <= 232448, "P4W shared memory exceeds 227 KiB");
 };
@@ -504,7 +504,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             // the row's residual groups: issued before the wait on the tile's MMAs, so their
             // latency overlaps it (the K loop's registers are free here)
             const int64_t m_row = m0 + tid;
-            const bool pre = RES && p.ep.residual != nullptr && m_row < p.M && p4t_vec_ok(P, n0);
+            const bool pre = RES && m_row < p.M &&
+                             (kconst.mode == EPI_RES_RELU_Y_Q ? n0 + TN <= p.N
+                                                               : p.ep.residual != nullptr && p4t_vec_ok(P, n0));
             float4 res[TN / 4];
             if (pre) {
                 const float4* rp = reinterpret_cast<const float4*>(p.ep.residual + m_row * p.ep.ldr + n0);

@@ -61,19 +61,77 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 // Output of one lane's row (16 columns, int32 totals in v): raw / atomic int32 or the fused
 // epilogue (P4's, one row per lane).
 // Per-launch epilogue constants (loaded once per CTA, not per tile).
+// Specialised epilogue modes (decided once per launch; the ResNet forward's three layer kinds),
+// all: row layout, per-tensor scale, no bias, 16-byte aligned rows and code rows.
+enum : int {
+    EPI_GENERIC = 0,
+    EPI_RELU_Q = 1,          // ReLU + requantize (bottleneck c1 / c2)
+    EPI_RES_RELU_Y_Q = 2,    // + fp32 residual, ReLU, fp32 y and requantize (block output c3)
+    EPI_Y = 3,               // fp32 y only (projection shortcut)
+};
 struct EpiConst {
     float sc, s_out, qm, r_out;   // r_out = RN(1 / s_out) for epi_quant_r
+    int mode, pad0, pad1, pad2;
 };
 __device__ __forceinline__ EpiConst p4t_epi_const(const P4Args& P) {
     const EpiArgs& e = P.mm.ep;
-    EpiConst k{0.f, 1.f, 127.f, 1.f};
+    EpiConst k{0.f, 1.f, 127.f, 1.f, EPI_GENERIC, 0, 0, 0};
     if (P.mm.C_out == nullptr) {
         k.sc = __fmul_rn(*e.sa, *e.sw);
         k.s_out = e.q ? *e.s_out : 1.f;
         k.qm = (float)((1 << ((e.q ? e.bits_out : 8) - 1)) - 1);
         k.r_out = __frcp_rn(k.s_out);
+        const auto a16 = [](const void* ptr, int64_t ld) {
+            return ((reinterpret_cast<uintptr_t>(ptr) & 15) == 0) && ((ld & 3) == 0);
+        };
+        const bool plain = !P.transposed && !e.bias && !e.sw_ch && !e.y_nchw;
+        const bool q16 = e.q && ((e.ldq & 15) == 0) && ((reinterpret_cast<uintptr_t>(e.q) & 15) == 0);
+        if (plain && e.relu && q16 && !e.residual && !e.y) k.mode = EPI_RELU_Q;
+        else if (plain && e.relu && q16 && e.residual && a16(e.residual, e.ldr) && e.y && a16(e.y, e.ldy))
+            k.mode = EPI_RES_RELU_Y_Q;
+        else if (plain && !e.relu && !e.q && !e.residual && e.y && a16(e.y, e.ldy)) k.mode = EPI_Y;
     }
     return k;
+}
+
+// the specialised row epilogue (kc.mode != EPI_GENERIC, whole 16-column tile, no split): the
+// generic path's arithmetic without its per-element flag tests; ReLU outputs requantize through
+// the sign-free reciprocal test (epi_quant_r_nn, bit-identical to epi_quant)
+__device__ __forceinline__ void p4t_store_row_fast(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
+                                                   const EpiConst& kc, const float4* res_pre) {
+    const EpiArgs& e = P.mm.ep;
+    const float sc = kc.sc;
+    if (kc.mode == EPI_Y) {
+        float4* yp = reinterpret_cast<float4*>(e.y + m * e.ldy + n0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            yp[j] = make_float4(__fmul_rn(__int2float_rn(eacc[4 * j]), sc), __fmul_rn(__int2float_rn(eacc[4 * j + 1]), sc),
+                                __fmul_rn(__int2float_rn(eacc[4 * j + 2]), sc), __fmul_rn(__int2float_rn(eacc[4 * j + 3]), sc));
+        return;
+    }
+    const bool res = kc.mode == EPI_RES_RELU_Y_Q;
+    const float4* rp = res ? reinterpret_cast<const float4*>(e.residual + m * e.ldr + n0) : nullptr;
+    float4* yp = res ? reinterpret_cast<float4*>(e.y + m * e.ldy + n0) : nullptr;
+    uint32_t qw[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __fmul_rn(__int2float_rn(eacc[4 * j + u]), sc);
+        if (res) {
+            const float4 r = res_pre ? res_pre[j] : __ldg(rp + j);
+            v[0] = __fadd_rn(v[0], r.x); v[1] = __fadd_rn(v[1], r.y);
+            v[2] = __fadd_rn(v[2], r.z); v[3] = __fadd_rn(v[3], r.w);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = v[u] > 0.f ? v[u] : 0.f;
+        if (res) yp[j] = make_float4(v[0], v[1], v[2], v[3]);
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w |= epi_quant_r_nn(v[u], kc.s_out, kc.r_out, kc.qm) << (8 * u);
+        qw[j] = w;
+    }
+    *reinterpret_cast<uint4*>(e.q + m * e.ldq + n0) = make_uint4(qw[0], qw[1], qw[2], qw[3]);
 }
 
 // the row-layout vector epilogue applies (16-byte aligned fp32 rows, 4-byte aligned codes)
@@ -105,6 +163,10 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
     using namespace p4;
     const MMArgs& p = P.mm;
     const EpiArgs& e = p.ep;
+    if (kc.mode != EPI_GENERIC && splits == 1 && n0 + TN <= p.N) {
+        p4t_store_row_fast(P, m, n0, eacc, kc, res_pre);
+        return;
+    }
     if (P.transposed) {
         // axq_lut_gemm_xs: rows are weight rows (bias / per-channel scale index), columns are
         // activation rows; lanes = consecutive weight rows -> coalesced along the output row
