@@ -905,7 +905,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
 // thread sees either value, both of which give bit-identical results.
 static std::atomic<int> g_p4w_main_cw{28};        // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
 static std::atomic<int64_t> g_p4w_main_cw_max_k{1 << 30};   // ... for layers with K up to this
-static std::atomic<int> g_p4w_res_cw{16};         // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape
+static std::atomic<int> g_p4w_res_cw{20};         // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape (r2: 20 after the specialised epilogue)
 static std::atomic<int> g_p4w_cw{0};              // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
 static std::atomic<int64_t> g_sk_full_waves{8};   // AXQ_SK_FULL_WAVES: P4W layers of fewer than this many waves of
                                                   // tiles cut every iteration (no whole-wave phase): measured
