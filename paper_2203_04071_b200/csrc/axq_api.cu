@@ -974,7 +974,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     a.tables = wp->tables;
     a.wpk = wp->wpk;
     a.Kp = wp->Kp;
-    a.is_conv = conv ? 1 : 0;
+    a.is_conv = (conv && !a.pointwise) ? 1 : 0;
     a.one = 1u;
     a.half = wp->half;
     a.mm.t00 = wp->t00;
@@ -1123,6 +1123,10 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
     const int64_t cv = d->c_valid ? d->c_valid : d->C;
     p.pad_lookups = (int32_t)(d->R * d->S * (d->C - cv));
     a.c4 = c4 ? 1 : 0;
+    // a 1x1 / stride-1 / unpadded conv is the GEMM of its NHWC rows (P:119 with a trivial im2col)
+    a.pointwise = (!c4 && d->R == 1 && d->S == 1 && d->stride_h == 1 && d->stride_w == 1 && d->pad_h == 0 &&
+                   d->pad_w == 0) ? 1 : 0;
+    if (a.pointwise) p.lda = d->C;
     return p4_run(a, wp, ep, true, Y, d->K, S(stream));
 }
 
