@@ -99,6 +99,14 @@ __device__ __forceinline__ RowInfo make_row(const MMArgs& p, int64_t m) {
     if constexpr (LOADER == LOAD_GEMM || LOADER == LOAD_GEMM_BYTES || LOADER == LOAD_GEMM_F32) {
         ri.base = m * p.lda;
         ri.hb = ri.wb = 0;
+    } else if (p.M <= 0x7fffffff) {   // 32-bit index arithmetic (uniform branch)
+        const uint32_t hw = (uint32_t)p.Ho * (uint32_t)p.Wo;
+        const uint32_t mm = ri.valid ? (uint32_t)m : 0u;
+        const uint32_t img = mm / hw, rem = mm - img * hw;
+        const int ho = (int)(rem / (uint32_t)p.Wo), wo = (int)(rem - (uint32_t)ho * (uint32_t)p.Wo);
+        ri.base = (int64_t)img * p.H * p.Wd * (p.cs ? p.cs : p.C);
+        ri.hb = ho * p.sh - p.ph;
+        ri.wb = wo * p.sw - p.pw;
     } else {
         int64_t hw = (int64_t)p.Ho * p.Wo;
         int64_t mm = ri.valid ? m : 0;
