@@ -293,3 +293,43 @@ def test_two_streams_concurrent(ax):
     for wp, ws, dA, ys, st, ref in run:
         for y in ys:
             np.testing.assert_array_equal(y.cpu().numpy(), ref.astype(np.float32))
+
+
+@pytest.mark.parametrize("mode", ["relu_q", "res_relu_y_q", "y"])
+@pytest.mark.parametrize("N", [64, 40])
+def test_specialised_epilogue_modes(ax, mode, N):
+    """The packed-table kernels' specialised epilogues (one per ResNet layer kind, decided once per
+    launch): ReLU + requantize, residual + ReLU + y + requantize, y only.  s_a*s_w = 1 and s_out = 2
+    put every odd integer sum on a half-even tie; N = 40 leaves a ragged last column block, which
+    takes the generic path in the same launch."""
+    M, K = 2048, 64
+    T = datagen.lut_randerr(8, 0, 2)
+    A = datagen.random_int8(811, (M, K), full_range=False)
+    W = datagen.random_int8(812, (N, K))
+    acc = oracle.lut_gemm(A, W, T, 8)
+    one_f = np.float32(1.0)
+    y_ref = oracle.dequantize(acc, one_f, one_f)
+    R = np.random.default_rng(813).integers(-300, 300, (M, N)).astype(np.float32)
+    if mode == "res_relu_y_q":
+        y_ref = (y_ref + R).astype(np.float32)
+    if mode != "y":
+        y_ref = np.where(y_ref > 0, y_ref, np.float32(0)).astype(np.float32)
+    q_ref = oracle.quantize(y_ref, np.float32(2.0), 8)
+    lut = ax.Lut(8, T)
+    wp = ax.WPack(lut, _t(W))
+    y = torch.full((M, N), np.nan, device=DEV)
+    q = torch.zeros(M, N, dtype=torch.int8, device=DEV)
+    ws = torch.zeros(ax.axq_workspace_elems(M, N), dtype=torch.int32, device=DEV)
+    one = torch.ones(1, device=DEV)
+    so = torch.tensor([2.0], device=DEV)
+    kw = {"relu_q": dict(relu=True, q_out=q, ldq=N, d_scale_out=so, bits_out=8),
+          "res_relu_y_q": dict(residual=_t(R), ldr=N, relu=True, y=y, ldy=N, q_out=q, ldq=N,
+                               d_scale_out=so, bits_out=8),
+          "y": dict(y=y, ldy=N)}[mode]
+    ep = ax.make_epilogue(one, one, workspace=ws, **kw)
+    ax.axq_lut_gemm_wp(_t(A), wp, ep)
+    torch.cuda.synchronize()
+    if mode != "relu_q":
+        np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+    if mode != "y":
+        np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
