@@ -38,10 +38,12 @@ SM_COUNT_NOMINAL = 148
 LANES = 32
 QUANTIZER = "max"
 LUT_KIND = "default"
-DESIGN_LOOKUPS_PER_CLK = 1024.0 / 11.0   # ALU-pipe bound of the P4W inner loop
-DESIGN_BASIS = ("packed-table inner loop: 22 ALU-pipe warp instructions (PRMT, IADD3) per 1024 "
-                "lookups; ALU pipe 2 warp instructions per SM clock (B300_MICROARCH rt_SMSP = 2) "
-                "-> 93.1 lookups per SM clock (DESIGN.md 5.4)")
+DESIGN_LOOKUPS_PER_CLK = 1024.0 / 8.0    # issue bound of the P4W inner loop
+DESIGN_BASIS = ("packed-table inner loop (r2, dp4a over 4-k byte transposes): per 1024 lookups "
+                "of a warp 32 issued warp instructions (8 LDS, 14 ALU-pipe: code extracts + "
+                "PRMT transposes, 10 FMA-pipe: row addresses + dp4a) at 4 issued per SM clock "
+                "-> 128 lookups per SM clock; the ALU pipe alone (2 per SM clock) would allow "
+                "146, shared memory at replay 1 (8 wavefronts) 128 (DESIGN.md 5.4)")
 
 
 def parse():
@@ -827,7 +829,7 @@ def run_ours(args, rank, world, local_rank):
                          "frac_at_measured_clock": round(achieved / (sm * 128 * f_meas / 1e9), 4)
                          if f_meas else None,
                          "design_roofline": {
-                             "bound": "alu", "peak": round(sm * f_max / 1e9 * DESIGN_LOOKUPS_PER_CLK, 2),
+                             "bound": "issue", "peak": round(sm * f_max / 1e9 * DESIGN_LOOKUPS_PER_CLK, 2),
                              "unit": "Glookup/s",
                              "frac": round(achieved / (sm * f_max / 1e9 * DESIGN_LOOKUPS_PER_CLK), 4),
                              "basis": DESIGN_BASIS},
