@@ -460,7 +460,10 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_empty + 8 * buf);
-                if ((st - s_b + 1) % G::FLUSH_STAGES == 0 || st + 1 == s_e) {
+                // E8 with every quad on dp4a: 32-bit per-column sums never overflow (< 2^32 / 255
+                // lookups), so they stay in registers for the whole tile -- no TMEM flush
+                constexpr bool REG_E = !E16 && IDQ == 4;
+                if (!REG_E && ((st - s_b + 1) % G::FLUSH_STAGES == 0 || st + 1 == s_e)) {
                     uint32_t ev[16];
                     if (!e_first) {
                         tmem_ld16(t_e, ev);
@@ -518,7 +521,14 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             tc_fence_after();
             uint32_t ex[16], es[16];
             tmem_ld16(tmem + t_lane + tb * 128u + slice_col, ex);
-            tmem_ld16(t_e, es);
+            if constexpr (!E16 && IDQ == 4) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) es[4 * q + j] = iacc[q < IDQ ? q : 0][j];
+            } else {
+                tmem_ld16(t_e, es);
+            }
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
