@@ -6,7 +6,7 @@ O=gpurun_out/final; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -q > $O/gputests.log 2>&1; tail -1 $O/gputests.log
 timeout 600 python bench.py > $O/bench_resnet_final.json 2> $O/bench_resnet.err
 timeout 600 python bench.py --quantizer paper --no-cpu-baseline > $O/bench_resnet_paper_final.json 2> $O/bench_resnet_paper.err
-for w in conv linear lstm; do timeout 600 python bench.py --workload $w > $O/bench_${w}_final.json 2> $O/bench_$w.err; done
+for w in conv linear lstm gemm; do timeout 600 python bench.py --workload $w > $O/bench_${w}_final.json 2> $O/bench_$w.err; done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/ref_resnet_final.json 2> $O/ref.err
 timeout 300 python scripts/scaling_probe.py > $O/scaling_probe_p4w.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --csv --log-file $O/launches_bench_resnet.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
