@@ -280,8 +280,12 @@ axq_status axq_lut_conv2d_f32(const axq_conv_desc* d, const float* X, const floa
  *   semantics; with ep->workspace the library may split K when the tiles alone cannot fill
  *   the GPU).  With ep == NULL the raw int32 result goes to C ([M][ldc]) / Y (NHWC), which is
  *   then also used as the split-K accumulator.  Requirements (else AXQ_ERR_UNSUPPORTED): A / X 16-byte
- *   aligned, lda % 16 == 0 (GEMM); conv: groups == 1, C % 4 == 0 and X 4-byte aligned (C % 16
- *   == 0 with a 16-byte aligned X takes 16-byte operand copies, otherwise 4-byte ones).
+ *   aligned, lda % 16 == 0 (GEMM); conv: C % 4 == 0 and X 4-byte aligned (C % 16 == 0 with a
+ *   16-byte aligned X takes 16-byte operand copies, otherwise 4-byte ones); grouped conv
+ *   (groups > 1, NEXT-3): wp packs the weights [K][R][S][C/groups] as an N = K,
+ *   K = R*S*C/groups GEMM operand; C/groups and K/groups multiples of 16, X 16-byte aligned,
+ *   c_valid 0, int8-E tables (each 16-column tile lies in one group and reads that group's
+ *   input channels).
  * ------------------------------------------------------------------------------- */
 typedef struct axq_wpack* axq_wpack_t;
 axq_status axq_wpack_create(axq_lut_t lut, const int8_t* W, int64_t N, int64_t K, int64_t ldw,

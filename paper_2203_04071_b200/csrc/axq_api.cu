@@ -1101,10 +1101,16 @@ axq_status axq_lut_gemm_wp(int64_t M, const int8_t* A, int64_t lda, axq_wpack_t 
 axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_t wp,
                              const axq_epilogue* ep, int32_t* Y, void* stream) {
     if (!wp || !d) return AXQ_ERR_INVALID;
-    if (d->groups != 1 || (d->C & 3) || (reinterpret_cast<uintptr_t>(X) & 3)) return AXQ_ERR_UNSUPPORTED;
+    if (d->groups < 1 || d->C % d->groups || d->K % d->groups) return AXQ_ERR_INVALID;
+    const int64_t cin_g = d->C / d->groups, cout_g = d->K / d->groups;
+    // grouped (NEXT-3): every 16-column tile inside one group, 16-byte channel runs per group
+    if (d->groups > 1 && ((cout_g & 15) || (cin_g & 15) || !aligned16(X) || d->c_valid || wp->e16 ||
+                          g_wpack_kernel.load() == 1))
+        return AXQ_ERR_UNSUPPORTED;
+    if ((d->C & 3) || (reinterpret_cast<uintptr_t>(X) & 3)) return AXQ_ERR_UNSUPPORTED;
     const bool c4 = (d->C & 15) || !aligned16(X);
     if (c4 && wp->Kp > axq::p4::TAP_BYTES) return AXQ_ERR_UNSUPPORTED;   // tap table capacity
-    if (d->K != wp->N || d->R * d->S * d->C != wp->K) return AXQ_ERR_INVALID;
+    if (d->K != wp->N || d->R * d->S * cin_g != wp->K) return AXQ_ERR_INVALID;
     axq::P4Args a{};
     int loader = 0;
     // reuse the generic conv validation (LUT-independent parts) through a shim LUT view
@@ -1117,7 +1123,12 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
     (void)loader;
     axq::MMArgs& p = a.mm;
     p.A = X; p.M = d->N * Ho * Wo; p.N = d->K; p.K = wp->K;
-    p.H = (int)d->H; p.Wd = (int)d->W; p.C = (int)d->C; p.Ho = (int)Ho; p.Wo = (int)Wo;
+    p.H = (int)d->H; p.Wd = (int)d->W; p.C = (int)cin_g; p.Ho = (int)Ho; p.Wo = (int)Wo;
+    if (d->groups > 1) {
+        p.cs = (int)d->C;
+        a.grp_cout = (int)cout_g;
+        a.grp_cin = (int)cin_g;
+    }
     p.S = (int)d->S; p.sh = (int)d->stride_h; p.sw = (int)d->stride_w;
     p.ph = (int)d->pad_h; p.pw = (int)d->pad_w; p.dh = (int)d->dil_h; p.dw = (int)d->dil_w;
     const int64_t cv = d->c_valid ? d->c_valid : d->C;
@@ -1126,7 +1137,7 @@ axq_status axq_lut_conv2d_wp(const axq_conv_desc* d, const int8_t* X, axq_wpack_
     // a 1x1 / stride-1 / unpadded conv is the GEMM of its NHWC rows (P:119 with a trivial im2col)
     a.pointwise = (!c4 && d->R == 1 && d->S == 1 && d->stride_h == 1 && d->stride_w == 1 && d->pad_h == 0 &&
                    d->pad_w == 0) ? 1 : 0;
-    if (a.pointwise) p.lda = d->C;
+    if (a.pointwise) p.lda = d->C;   // (grouped: the group's channel offset is added per tile)
     return p4_run(a, wp, ep, true, Y, d->K, S(stream));
 }
 

@@ -58,6 +58,9 @@ struct P4Args {
     int transposed;             // P4W: output element (row r, col c) goes to [c][r] (gemm_xs)
     int cw;                     // P4W consumer warps (tile rows / 32): 28 (default) or 16
     int e16;                    // P4W16: int16 E tables, 2 columns per packed word
+    int grp_cout, grp_cin;      // grouped conv (P4W): output / input channels per group (0: none);
+                                // a 16-column tile lies in group n0 / grp_cout, whose input
+                                // channels start at that group * grp_cin of the pixel (stride cs)
     int pointwise;              // conv that is a plain GEMM of its NHWC input (1x1, stride 1,
                                 // pad 0): rows loaded as GEMM rows (lda = C), no per-row division
     int nb_fast;                // tile order: column block fastest (the layer's tables stay in

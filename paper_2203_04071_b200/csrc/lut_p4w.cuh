@@ -236,14 +236,17 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
         int64_t t;
         int s_b, s_e;
         uint32_t item = 0;
+        const int64_t pix = p.cs ? p.cs : p.C;    // NHWC pixel stride (grouped conv: all channels)
         while (gen_next(g, t, s_b, s_e)) {
             int64_t nb, m0;
             tile_mn(t, nb, m0);
+            // grouped conv: this column tile's group selects its input channels
+            const int64_t goff = P.grp_cout ? (nb * TN / P.grp_cout) * P.grp_cin : 0;
 #pragma unroll 1
             for (int i = 0; i < RPT; ++i) {
                 const int r = pt + i * PT;
                 const RowInfo ri = P.is_conv ? make_row<LOAD_CONV>(p, m0 + r) : make_row<LOAD_GEMM>(p, m0 + r);
-                const int64_t ro = ri.base + (P.is_conv ? ((int64_t)ri.hb * p.Wd + ri.wb) * p.C : 0);
+                const int64_t ro = ri.base + goff + (P.is_conv ? ((int64_t)ri.hb * p.Wd + ri.wb) * pix : 0);
                 rowinfo[r] = make_int4((int)(ro & 0xffffffff), (int)(ro >> 32), ri.hb,
                                        ri.valid ? ri.wb : (int)0x80000000);
             }
@@ -280,13 +283,13 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                                 const bool ok = ri.w != (int)0x80000000 && tv[j] != ~0u &&
                                                 (unsigned)(ri.z + rdh) < (unsigned)p.H &&
                                                 (unsigned)(ri.w + sdw) < (unsigned)p.Wd;
-                                const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + (int)(tv[j] >> 16);
+                                const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * pix + (int)(tv[j] >> 16);
                                 cp_async4(dst0 + r * 16 + 4 * j, ok ? p.A + ro + toff : p.A, ok ? 4u : 0u);
                             }
                         }
                     } else if (P.is_conv) {
                         const int rdh = t_r * p.dh, sdw = t_s * p.dw;
-                        const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * p.C + t_c;
+                        const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * pix + t_c;
                         const bool kin = k0 < p.K;
 #pragma unroll 1
                         for (int i = 0; i < RPT; ++i) {

@@ -123,13 +123,16 @@ class ApproxConv2d:
     """Conv2d with every multiply a LUT lookup; NCHW fp32 in/out, implicit im2col."""
 
     def __init__(self, weight: torch.Tensor, bias: torch.Tensor | None, lut: ax.Lut,
-                 stride=(1, 1), padding=(0, 0), device="cuda", packed=True, a_nonneg=False):
+                 stride=(1, 1), padding=(0, 0), device="cuda", packed=True, a_nonneg=False, groups=1):
         """a_nonneg: the layer input is non-negative (e.g. a ReLU output), so its codes are >= 0
-        and the packed kernel may use half-range tables."""
+        and the packed kernel may use half-range tables.  groups (NEXT-3): weight [K][C/G][R][S];
+        packed tables when C/G and K/G are multiples of 16, else the grouped resident-table path."""
         self.lut = lut
         self.bits = lut.bits
-        w = weight.to(device=device, dtype=torch.float32).contiguous()   # [K][C][R][S]
-        self.Kout, self.C, self.R, self.S = w.shape
+        w = weight.to(device=device, dtype=torch.float32).contiguous()   # [K][C/G][R][S]
+        self.Kout, cg, self.R, self.S = w.shape
+        self.groups = int(groups)
+        self.C = cg * self.groups
         self.stride, self.padding = tuple(stride), tuple(padding)
         self.d_amax_w = torch.empty(1, device=device)
         self.d_scale_w = torch.empty(1, device=device)
@@ -141,7 +144,8 @@ class ApproxConv2d:
         self.qw = q.permute(0, 2, 3, 1).contiguous()                      # KRSC relayout
         self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
         self.wp = None
-        if packed and self.C % 16 == 0 and self.C * self.R * self.S >= 128:
+        grp_ok = self.groups == 1 or (cg % 16 == 0 and (self.Kout // self.groups) % 16 == 0 and lut.repr == "delta8")
+        if packed and grp_ok and self.C % 16 == 0 and cg * self.R * self.S >= 128:
             # delta8 tables: packed int8 E (P4W); other ACUs with |E| < 2^15 and non-negative
             # inputs: packed int16 E (P4W16); otherwise the resident-table kernel
             if lut.repr == "delta8":
@@ -158,7 +162,8 @@ class ApproxConv2d:
         self._bufs = {}
 
     def desc(self, N, H, W):
-        return ax.conv_desc(N, H, W, self.C, self.Kout, self.R, self.S, self.stride, self.padding)
+        return ax.conv_desc(N, H, W, self.C, self.Kout, self.R, self.S, self.stride, self.padding,
+                            groups=self.groups)
 
     def forward(self, x: torch.Tensor, y: torch.Tensor | None = None, d_scale_a=None):
         N, C, H, W = x.shape

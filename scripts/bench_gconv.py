@@ -43,3 +43,22 @@ for name, (N, C, H, K, R, G) in {"depthwise3x3": (128, 256, 56, 256, 3, 256),
     print(json.dumps({"layer": name, "ms": round(ms, 4), "G_lookups_s": round(lookups / ms / 1e6, 1),
                       "frac_smem_roofline": round(lookups / ms / 1e6 / 9306.24, 3),
                       "GBps": round(byts / ms / 1e6, 1), "frac_hbm": round(byts / ms / 1e6 / hbm, 3)}))
+    if G < C and (C // G) % 16 == 0 and (K // G) % 16 == 0:
+        # the same grouped layer on weight-specialised packed tables (axq_lut_conv2d_wp, P4W)
+        wp = ax.WPack(lut, w.reshape(K, -1), a_nonneg=True)
+        ws = torch.zeros(ax.axq_workspace_elems(M, K), dtype=torch.int32, device="cuda")
+        epw = ax.make_epilogue(sa, sw, relu=True, y_nhwc=True, q_out=q, ldq=K, d_scale_out=so, bits_out=8,
+                               workspace=ws)
+        for _ in range(3):
+            ax.axq_lut_conv2d_wp(d, x, wp, epw)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            ax.axq_lut_conv2d_wp(d, x, wp, epw)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        print(json.dumps({"layer": name + "_packed", "ms": round(ms, 4),
+                          "G_lookups_s": round(lookups / ms / 1e6, 1),
+                          "frac_smem_roofline": round(lookups / ms / 1e6 / 9306.24, 3),
+                          "path": ax.axq_last_path()[0]}))

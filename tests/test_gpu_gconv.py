@@ -171,3 +171,54 @@ def test_depthwise_dw3_fused_nhwc(ax, shape, per_channel, with_y):
     if with_y:
         np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
     np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
+
+
+# grouped convs on the packed-table P4W path (axq_lut_conv2d_wp; C/G and K/G multiples of 16)
+WP_CASES = [(2, 64, 10, 10, 64, 3, 3, 1, 1, 2),      # 3x3, G = 2
+            (2, 64, 12, 12, 64, 1, 1, 1, 0, 4),      # pointwise 1x1, G = 4 (GEMM-row loader)
+            (1, 96, 9, 11, 48, 1, 1, 2, 0, 3),       # 1x1 stride 2, G = 3
+            (3, 32, 7, 9, 64, 3, 3, 2, 1, 2),        # 3x3 stride 2, K/G = 32
+            (4, 64, 28, 28, 256, 1, 1, 1, 0, 4)]     # the bench's ShuffleNet-like shape, scaled down
+
+
+@pytest.mark.parametrize("case", WP_CASES)
+@pytest.mark.parametrize("half", [False, True])
+def test_grouped_conv_packed(ax, case, half):
+    """Grouped conv through weight-specialised packed tables: a 16-column tile's group selects its
+    input channels (bit-exact against the oracle's direct grouped conv)."""
+    Nb, C, H, Wd, K, R, S, st, pd, G = case
+    T, bits = _table("randerr")
+    X = datagen.random_int8(500 + C + G, (Nb, C, H, Wd), bits, full_range=not half)
+    if half:   # half-range tables: non-negative (ReLU'd) activation codes only
+        X = np.abs(X.astype(np.int16)).astype(np.int8)
+    Wt = datagen.random_int8(600 + K + G, (K, C // G, R, S), bits)
+    ref = oracle.lut_conv2d(X, Wt, T, bits, (st, st), (pd, pd), groups=G)
+    lut = ax.Lut(bits, T)
+    wp = ax.WPack(lut, _t(Wt.transpose(0, 2, 3, 1)).reshape(K, -1), a_nonneg=half)
+    d = ax.conv_desc(Nb, H, Wd, C, K, R, S, (st, st), (pd, pd), groups=G)
+    Ho, Wo = ax.axq_conv2d_out_hw(d)
+    Y = torch.empty(Nb, Ho, Wo, K, dtype=torch.int32, device=DEV)
+    ax.axq_lut_conv2d_wp(d, _t(X.transpose(0, 2, 3, 1)), wp, None, Y)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
+
+
+@pytest.mark.parametrize("G,C,K,R", [(4, 64, 64, 3), (3, 24, 36, 1), (2, 64, 64, 3), (4, 256, 128, 1)])
+def test_approx_conv2d_layer_groups(ax, G, C, K, R):
+    """layers.ApproxConv2d with groups: packed tables when C/G and K/G are multiples of 16 (and
+    the per-group K = R*S*C/G >= 128), else the grouped resident-table path; both equal the
+    oracle's quantize -> grouped LUT conv -> dequantize chain bit for bit."""
+    from paper_2203_04071_b200.layers import ApproxConv2d
+    Nb, H, Wd = 3, 12, 12
+    x = np.maximum(datagen.normal(70 + G, 1, (Nb, C, H, Wd)), 0).astype(np.float32)
+    w = datagen.normal(71 + G, 2, (K, C // G, R, R), 0.1)
+    T = datagen.lut_randerr(8, 0, 2)
+    s_a = oracle.scale(oracle.amax(x), 8)
+    qw, s_w = oracle.quantize_tensor(w, 8)
+    acc = oracle.lut_conv2d(oracle.quantize(x, s_a, 8), qw, T, 8, (1, 1), (R // 2, R // 2), groups=G)
+    y_ref = oracle.dequantize(acc, s_a, s_w, None, 1)
+    layer = ApproxConv2d(_t(w), None, ax.Lut(8, T), (1, 1), (R // 2, R // 2), a_nonneg=True, groups=G)
+    assert (layer.wp is not None) == ((C // G) % 16 == 0 and (K // G) % 16 == 0 and (C // G) * R * R >= 128)
+    y = layer(_t(x))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
