@@ -9,8 +9,9 @@
 //    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
 //    the consumer warps released it (empty barrier) and the MMA that read it completed.
 //  * 28 consumer warps (896 rows, one per lane) only wait for full buffers, do the lookups
-//    (4 per 32-bit LDS; the adds split between the ALU pipe -- two k per 3-input add -- and
-//    the FMA pipe -- multiply-add by an opaque 1) and release the buffer; consumer warp
+//    (4 per 32-bit LDS; per quad and 4 k the 4 words are byte-transposed and each column summed
+//    by one dp4a into a 32-bit register sum kept for the whole tile) and release the buffer;
+//    consumer warp
 //    0's lane 0 also issues the exact-part MMAs (7 slices of 128 rows, M = 128, N = 16, K = 32)
 //    into one of two TMEM accumulator sets, so the next tile's MMAs never wait for this
 //    tile's epilogue reads.  No CTA-wide barrier in the steady state.
@@ -31,7 +32,7 @@ namespace p4w {
 constexpr int PW = 4;                      // producer warps
 constexpr int TN = p4::TN;
 constexpr int W_STAGE = 512;
-constexpr int TMEM_COLS = 512;             // exact sets at 0 and 128, E sums at 256
+constexpr int TMEM_COLS = 512;             // exact sets at 0 and 128, E sums at 256 (P4W16 only)
 
 // CTA shape: CWX consumer warps (one tile row per lane).  28 (896-row tiles, 1024 threads) is
 // the default; 16 (512-row tiles, 640 threads) serves small row counts (M <= 1024), where 896-row
@@ -353,8 +354,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             const int64_t n0 = nb * TN;
             const uint32_t tb = tcount & 1u;
             const bool wlive = m0 + warp * 32 < p.M;
-            // E8: per quad q, pacc[q][0] / [1] = even / odd biased bytes in 16-bit lanes (exact
-            // for up to 256 words between flushes).  E16: per column pair p, pacc[p][0] = sum v
+            // E8 (default, IDQ = 4): iacc[q][j] = sum of column 4q + j's biased bytes, 32-bit, for the
+            // whole tile.  E8 with P4W_IDP_QUADS < 4 (A/B builds): the other quads keep even / odd
+            // bytes in 16-bit lanes, flushed every 256 k.  E16: per column pair p, pacc[p][0] = sum v
             // (mod 2^32) and pacc[p][1] = sum (v >> 16); the low column's sum is
             // pacc[p][0] - 2^16 pacc[p][1] (mod 2^32, exact: both sums < 2^32).
             constexpr int NACC = E16 ? 8 : 4;
