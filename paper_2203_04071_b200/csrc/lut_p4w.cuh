@@ -3,20 +3,23 @@
 // in int32, exact, as  sum_k a*w (tcgen05.mma kind::i8, TMEM)  +  sum_k E[a][w] (packed tables).
 //
 // Roles inside one persistent CTA (1024 threads, one CTA per SM):
-//  * 4 producer warps (warps 28..31) stream the operands of each (tile, stage) item into a
+//  * 3 producer warps (warps CW..CW+2) stream the operands of each (tile, stage) item into a
 //    ring of STAGES shared-memory buffers: the activation rows by cp.async (implicit im2col,
 //    zero-fill = padding taps), completion signalled with cp.async.mbarrier.arrive; the packed
 //    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
 //    the consumer warps released it (empty barrier) and the MMA that read it completed.
-//  * 28 consumer warps (896 rows, one per lane) only wait for full buffers, do the lookups
-//    (4 per 32-bit LDS; per quad and 4 k the 4 words are byte-transposed and each column summed
-//    by one dp4a into a 32-bit register sum kept for the whole tile) and release the buffer;
-//    consumer warp
-//    0's lane 0 also issues the exact-part MMAs (7 slices of 128 rows, M = 128, N = 16, K = 32)
-//    into one of two TMEM accumulator sets, so the next tile's MMAs never wait for this
-//    tile's epilogue reads.  No CTA-wide barrier in the steady state.
+//  * CW consumer warps (one tile row per lane) only wait for full buffers and do the lookups
+//    (4 per 32-bit LDS).  E8 tables (TCE): the gathered words of 4 k x 4 quads (16 words, 64
+//    biased E bytes of the row) go to a TMEM staging buffer with one tcgen05.st, and the
+//    tensor core sums them: D[m][n] += sum_j G[m][j] * SEL[j][n], SEL[j][n] = (j mod 16 == n),
+//    G read from TMEM (kind::i8, u8 x u8) -- no per-lookup ALU work in the consumer warps.
+//    E16 tables: 16-bit lane sums in registers, flushed to TMEM.
+//  * The MMA warp (warp CW+3, lane 0 issues) runs per stage the exact-part MMAs (slices of 128
+//    rows, M = 128, N = 16, K = 32) and per staged chunk the E MMAs, all into one of two TMEM
+//    accumulator sets (double-buffered across tiles, so the next tile's MMAs never wait for
+//    this tile's epilogue reads).  No CTA-wide barrier in the steady state.
 //  * Row 32*w + lane of a tile is TMEM lane 32*(w % 4) + lane of MMA slice w / 4, so every
-//    consumer warp reads exactly the TMEM lane quarter it may access.
+//    consumer warp reads and writes exactly the TMEM lane quarter it may access.
 //  * Tile order, stream-K tail (exact int32 pieces in the zero-filled workspace), split-K for
 //    raw output and the fused epilogue (tc_common.cuh).
 #pragma once
@@ -32,7 +35,12 @@ namespace p4w {
 constexpr int PW = 4;                      // producer warps
 constexpr int TN = p4::TN;
 constexpr int W_STAGE = 512;
-constexpr int TMEM_COLS = 512;             // exact sets at 0 and 128, E sums at 256 (P4W16 only)
+constexpr int TMEM_COLS = 512;
+// E8: one accumulator set at 0 (exact part + E sums), the E staging buffers from column 128;
+// E16: two exact sets at 0 and 128, the E sums at 256
+constexpr int STG_COLS = 16;               // one staged chunk: 4 k x 4 quads, 32-bit words
+constexpr int STG_BUFS = 3;                // staged chunks per slice
+constexpr int STG_BASE = 128;
 
 // CTA shape: CWX consumer warps (one tile row per lane).  28 (896-row tiles, 1024 threads) is
 // the default; 16 (512-row tiles, 640 threads) serves small row counts (M <= 1024), where 896-row
@@ -44,20 +52,14 @@ struct Shape {
     static constexpr int BM = CW * 32;             // rows per tile
     static constexpr int SLICES = BM / 128;        // MMA slices of 128 rows
     static constexpr int PT = PW * 32;             // 128 producer threads
-    static constexpr int RPT = BM / PT;            // rows per producer thread
     static_assert(BM % 128 == 0, "tile rows must be whole MMA slices");
+    static_assert(STG_BASE + SLICES * STG_BUFS * STG_COLS <= TMEM_COLS, "E staging exceeds TMEM");
 };
 constexpr int CW = 28;
 constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots are sized for it)
 
-#ifndef P4W_IDP_QUADS     // quads summed by dp4a over byte-interleaved k pairs (FMA pipe, 32-bit sums)
-#define P4W_IDP_QUADS 4
-#endif
-#ifndef P4W_K4            // with all quads on dp4a: transpose 4 k x 4 columns, one dp4a per column per 4 k
-#define P4W_K4 1
-#endif
-#ifndef P4W_ALU_QUADS     // of the rest, quads whose adds run on the ALU pipe (else multiply-adds by 1, FMA pipe)
-#define P4W_ALU_QUADS 2
+#ifndef P4W_TCE
+#define P4W_TCE 0
 #endif
 #ifndef P4W_SMALL_FULL_STAGES
 #define P4W_SMALL_FULL_STAGES 3
@@ -67,6 +69,7 @@ constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots 
 template <bool HALF, int KSX = (HALF ? 32 : 16), int CWX = 28, bool E16 = false>
 struct Geo {
     static constexpr int BM = Shape<CWX>::BM;
+    static constexpr int SLICES = Shape<CWX>::SLICES;
     static constexpr int KS = KSX;
     static constexpr int TROWS = HALF ? 128 : 256;
     static constexpr int TQ = TROWS * 4;
@@ -85,10 +88,12 @@ struct Geo {
     static constexpr int SMEM_TBL = 0;
     static constexpr int SMEM_A = SMEM_TBL + STAGES * TBL_STAGE;
     static constexpr int SMEM_W = SMEM_A + STAGES * A_STAGE;
-    static constexpr int SMEM_ROW = SMEM_W + STAGES * W_STAGE;     // producer row info [BM] x 16 B
+    static constexpr int SMEM_SEL = SMEM_W + STAGES * W_STAGE;    // E8: the selector SEL (512 B)
+    static constexpr int SMEM_ROW = SMEM_SEL + W_STAGE;           // producer row info [BM] x 16 B
     static constexpr int SMEM_BAR = SMEM_ROW + BM * 16;
-    // full[S], empty[S], mma[S], tile_full[2], tmem_free[2], then tmem address, flag
-    static constexpr int NBAR = 3 * STAGES + 4;
+    // full[S], empty[S], mma[S], tile_full[SLICES][2], tmem_free[SLICES][2],
+    // chunk_full[SLICES][STG_BUFS], chunk_free[SLICES][STG_BUFS], then tmem address, flag
+    static constexpr int NBAR = 3 * STAGES + 4 * SLICES + 2 * SLICES * STG_BUFS;
     static constexpr int SMEM_MISC = SMEM_BAR + 8 * NBAR;
     static constexpr int SMEM_KC = SMEM_MISC + 16;                 // EpiConst (32 B)
     static constexpr int SMEM_TAP = SMEM_KC + 32;
@@ -114,9 +119,13 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     using namespace p4w;
     using G = p4w::Geo<HALF, KSX, CWX, E16>;
     using S = p4w::Shape<CWX>;
-    constexpr int CW = S::CW, NT = S::NT, BM = S::BM, SLICES = S::SLICES, PT = S::PT, RPT = S::RPT;
+    constexpr int CW = S::CW, NT = S::NT, BM = S::BM, SLICES = S::SLICES, PT = S::PT;
     constexpr int KS = G::KS, STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ, A_STAGE = G::A_STAGE;
     constexpr int NPL = KS / 16;
+    // E8 sums: by dp4a in registers (default) or, with P4W_TCE, on the tensor core from
+    // TMEM-staged words (measured slower)
+    constexpr bool TCE = !E16 && P4W_TCE;
+    constexpr bool DP4 = !E16 && !P4W_TCE;
     extern __shared__ __align__(1024) uint8_t p4w_smem[];
     uint8_t* smem = p4w_smem;
     const MMArgs& p = P.mm;
@@ -125,8 +134,10 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     const uint32_t bar_full = s_base + G::SMEM_BAR;
     const uint32_t bar_empty = bar_full + 8 * STAGES;
     const uint32_t bar_mma = bar_empty + 8 * STAGES;
-    const uint32_t bar_tfull = bar_mma + 8 * STAGES;     // [2]
-    const uint32_t bar_tfree = bar_tfull + 16;           // [2]
+    const uint32_t bar_tfull = bar_mma + 8 * STAGES;     // [SLICES][2]
+    const uint32_t bar_tfree = bar_tfull + 16 * SLICES;  // [SLICES][2]
+    const uint32_t bar_cfull = bar_tfree + 16 * SLICES;  // [SLICES][STG_BUFS]
+    const uint32_t bar_cfree = bar_cfull + 8 * SLICES * STG_BUFS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + G::SMEM_MISC);
     int* fin_flag = reinterpret_cast<int*>(smem + G::SMEM_MISC + 4);
 
@@ -145,16 +156,30 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     if (KS == 16)   // K chunk 2 of the weight buffers is zero (the MMA's K is 32)
         for (int i = tid; i < STAGES * 64; i += NT)
             reinterpret_cast<uint32_t*>(smem + G::SMEM_W + (i >> 6) * W_STAGE + 256)[i & 63] = 0u;
+    if (TCE && tid < 128) {
+        // SEL in the K-major canonical layout of the weight stages ((j / 16) * 256 + (n / 8) * 128 +
+        // (n % 8) * 16 + j % 16): row n holds a 1 at byte n of both 16-byte K chunks
+        const int o = tid * 4, kc = o >> 8, n = ((o >> 7) & 1) * 8 + ((o >> 4) & 7), j0 = o & 15;
+        (void)kc;
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) v |= (j0 + b == n ? 1u : 0u) << (8 * b);
+        reinterpret_cast<uint32_t*>(smem + G::SMEM_SEL)[tid] = v;
+    }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(bar_full + 8 * s, PT + 1);     // 128 cp.async arrivals + expect_tx
+            mbar_init(bar_full + 8 * s, PT + 1);     // the producers' cp.async arrivals + expect_tx
             mbar_init(bar_empty + 8 * s, CW);
-            mbar_init(bar_mma + 8 * s, 1);
+            mbar_init(bar_mma + 8 * s, SLICES);      // every slice issuer's commit
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(bar_tfull + 8 * s, 1);
-            mbar_init(bar_tfree + 8 * s, CW);
+        for (int s = 0; s < 2 * SLICES; ++s) {
+            mbar_init(bar_tfull + 8 * s, 1);         // the slice issuer's commit
+            mbar_init(bar_tfree + 8 * s, 4);         // the slice's 4 consumer warps
+        }
+        for (int s = 0; s < SLICES * STG_BUFS; ++s) {
+            mbar_init(bar_cfull + 8 * s, 4);         // the slice's 4 consumer warps
+            mbar_init(bar_cfree + 8 * s, 1);         // the E MMAs' commit
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -173,7 +198,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
-    // ---- work decomposition (shared by both roles) ----
+    // ---- work decomposition (shared by all roles) ----
     const int64_t m_tiles = (p.M + BM - 1) / BM, n_blocks = (p.N + TN - 1) / TN;
     const int splits = P.splits > 0 ? P.splits : 1;
     const int64_t n_work = m_tiles * n_blocks * splits;
@@ -244,8 +269,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             // grouped conv: this column tile's group selects its input channels
             const int64_t goff = P.grp_cout ? (nb * TN / P.grp_cout) * P.grp_cin : 0;
 #pragma unroll 1
-            for (int i = 0; i < RPT; ++i) {
-                const int r = pt + i * PT;
+            for (int r = pt; r < BM; r += PT) {
                 const RowInfo ri = P.is_conv ? make_row<LOAD_CONV>(p, m0 + r) : make_row<LOAD_GEMM>(p, m0 + r);
                 const int64_t ro = ri.base + goff + (P.is_conv ? ((int64_t)ri.hb * p.Wd + ri.wb) * pix : 0);
                 rowinfo[r] = make_int4((int)(ro & 0xffffffff), (int)(ro >> 32), ri.hb,
@@ -274,8 +298,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
 #pragma unroll
                         for (int j = 0; j < 4; ++j) tv[j] = tap_s[(int)(k0 >> 2) + j];
 #pragma unroll 1
-                        for (int i = 0; i < RPT; ++i) {
-                            const int r = pt + i * PT;
+                        for (int r = pt; r < BM; r += PT) {
                             const int4 ri = rowinfo[r];
                             const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
 #pragma unroll
@@ -293,8 +316,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                         const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * pix + t_c;
                         const bool kin = k0 < p.K;
 #pragma unroll 1
-                        for (int i = 0; i < RPT; ++i) {
-                            const int r = pt + i * PT;
+                        for (int r = pt; r < BM; r += PT) {
                             const int4 ri = rowinfo[r];
                             const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
                             const bool ok = kin && ri.w != (int)0x80000000 && (unsigned)(ri.z + rdh) < (unsigned)p.H &&
@@ -310,8 +332,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                         const int64_t rem = p.K - k0;
                         const uint32_t nbytes = rem >= 16 ? 16u : (rem > 0 ? (uint32_t)rem : 0u);
 #pragma unroll 1
-                        for (int i = 0; i < RPT; ++i) {
-                            const int r = pt + i * PT;
+                        for (int r = pt; r < BM; r += PT) {
                             const int4 ri = rowinfo[r];
                             const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
                             const bool ok = ri.w != (int)0x80000000 && nbytes > 0;
@@ -333,142 +354,171 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     } else {
         // =============================== consumer warps ===============================
         const uint32_t t_lane = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t slice_col = (uint32_t)(warp >> 2) * TN;
-        const uint32_t t_e = tmem + t_lane + 256u + slice_col;
+        const int slice = warp >> 2;
+        const uint32_t slice_col = (uint32_t)slice * TN;
+        const uint32_t t_e = tmem + t_lane + 256u + slice_col;                                   // E16 sums
+        const uint32_t t_stg = tmem + t_lane + STG_BASE + (uint32_t)(slice * STG_BUFS) * STG_COLS;   // E8 staging
+        const uint32_t c_full = bar_cfull + 8 * slice * STG_BUFS, c_free = bar_cfree + 8 * slice * STG_BUFS;
+        const uint32_t t_full = bar_tfull + 16 * slice, t_free = bar_tfree + 16 * slice;
+        // the slice issuer (lane 0 of one of its 4 warps, spread over the 4 SM sub-partitions)
+        // issues every MMA into the slice's accumulators -- exact part and E sums -- so they
+        // execute in its issue order
+        const bool iss_warp = (warp & 3) == (slice & 3);
+        const bool issuer = iss_warp && lane == 0;
         constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) | ((128u >> 4) << 24);
-        const bool mma_thread = (tid == 0);
+        constexpr uint32_t IDESC_E = (2u << 4) | ((uint32_t)(TN >> 3) << 17) | ((128u >> 4) << 24);   // u8 x u8
         // per-launch epilogue scalars: loaded once into shared memory (not held in registers
         // across the lookup loop)
         EpiConst& kconst = *reinterpret_cast<EpiConst*>(smem + G::SMEM_KC);
         if (tid == 0) kconst = p4t_epi_const(P);
         consumer_sync<BM>();
-        const uint32_t one = P.one;   // = 1, opaque to the compiler (keeps those adds on the FMA pipe)
         Gen g;
         gen_init(g);
         int64_t tile;
         int s_b, s_e;
-        uint32_t item = 0, tcount = 0;
+        uint32_t item = 0, tcount = 0, chunk = 0;
+        bool pend = false;   // the issuer's staged chunk chunk - 1 is not summed yet
         while (gen_next(g, tile, s_b, s_e)) {
             int64_t nb, m0;
             tile_mn(tile, nb, m0);
             const int64_t n0 = nb * TN;
-            const uint32_t tb = tcount & 1u;
+            // accumulator sets: E8 one (the slice's warps meet at each tile boundary anyway: the
+            // next tile's E MMAs need all 4 warps' staged words), E16 two
+            constexpr uint32_t NSET = TCE ? 1u : 2u;
+            // DP4: iacc[q][j] = sum of column 4q + j's biased bytes, 32-bit, for the whole tile
+            uint32_t iacc[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) iacc[q][0] = iacc[q][1] = iacc[q][2] = iacc[q][3] = 0u;
+            const uint32_t tb = tcount % NSET, tph = (tcount / NSET) & 1u;
             const bool wlive = m0 + warp * 32 < p.M;
-            // E8 (default, IDQ = 4): iacc[q][j] = sum of column 4q + j's biased bytes, 32-bit, for the
-            // whole tile.  E8 with P4W_IDP_QUADS < 4 (A/B builds): the other quads keep even / odd
-            // bytes in 16-bit lanes, flushed every 256 k.  E16: per column pair p, pacc[p][0] = sum v
-            // (mod 2^32) and pacc[p][1] = sum (v >> 16); the low column's sum is
-            // pacc[p][0] - 2^16 pacc[p][1] (mod 2^32, exact: both sums < 2^32).
-            constexpr int NACC = E16 ? 8 : 4;
-            constexpr int IDQ = E16 ? 0 : P4W_IDP_QUADS;   // quads 0 .. IDQ-1: per-column 32-bit sums
-            uint32_t pacc[NACC][2];
-            uint32_t iacc[IDQ > 0 ? IDQ : 1][4];
+            // E16: per column pair q, pacc[q][0] = sum v (mod 2^32) and pacc[q][1] = sum (v >> 16);
+            // the low column's sum is pacc[q][0] - 2^16 pacc[q][1] (mod 2^32, exact: both sums < 2^32)
+            uint32_t pacc[8][2];
 #pragma unroll
-            for (int q = 0; q < NACC; ++q) pacc[q][0] = pacc[q][1] = 0u;
-#pragma unroll
-            for (int q = 0; q < (IDQ > 0 ? IDQ : 1); ++q) iacc[q][0] = iacc[q][1] = iacc[q][2] = iacc[q][3] = 0u;
+            for (int q = 0; q < 8; ++q) pacc[q][0] = pacc[q][1] = 0u;
             bool e_first = true;
+            const uint32_t d_acc = tmem + tb * 128u + slice_col;   // the slice's accumulator (set tb)
+            // E MMAs of staged chunk c: D += G * SEL, G = the slice's 128 rows x 64 staged bytes
+            auto issue_e = [&](uint32_t c) {
+                const uint32_t b = c % STG_BUFS;
+                mbar_wait(c_full + 8 * b, (c / STG_BUFS) & 1u);
+                tc_fence_after();
+                const uint32_t a_t = tmem + STG_BASE + (uint32_t)(slice * STG_BUFS + b) * STG_COLS;
+                const uint64_t sel = umma_desc_kmajor(s_base + G::SMEM_SEL, 256u, 128u);
+                umma_i8_ts(d_acc, a_t, sel, IDESC_E, 1u);
+                umma_i8_ts(d_acc, a_t + 8u, sel, IDESC_E, 1u);
+                umma_commit(c_free + 8 * b);
+            };
             for (int st = s_b; st < s_e; ++st, ++item) {
                 const int buf = (int)(item % STAGES);
                 mbar_wait(bar_full + 8 * buf, (item / STAGES) & 1u);
-                if (mma_thread) {
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> MMA
-                    if (st == s_b && tcount >= 2) mbar_wait(bar_tfree + 8 * tb, ((tcount >> 1) - 1) & 1u);
-                    tc_fence_after();
-                    const uint32_t a0 = s_base + G::SMEM_A + buf * A_STAGE;
-                    const uint64_t bdesc = umma_desc_kmajor(s_base + G::SMEM_W + buf * W_STAGE, 256u, 128u);
-#pragma unroll
-                    for (int j = 0; j < SLICES; ++j)
-                        umma_i8(tmem + tb * 128u + (uint32_t)j * TN,
-                                umma_desc_kmajor(a0 + j * 128 * 16, KS == 32 ? (uint32_t)(BM * 16) : 0u, 128u), bdesc,
-                                IDESC, st == s_b ? 0u : 1u);
-                    umma_commit(bar_mma + 8 * buf);
-                    if (st + 1 == s_e) umma_commit(bar_tfull + 8 * tb);
+                if (iss_warp) {
+                    if (issuer) {
+                        if (st == s_b && tcount >= NSET) mbar_wait(t_free + 8 * tb, tph ^ 1u);
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> MMA
+                        tc_fence_after();
+                        const uint32_t a0 = s_base + G::SMEM_A + buf * A_STAGE + slice * 128 * 16;
+                        umma_i8(d_acc, umma_desc_kmajor(a0, KS == 32 ? (uint32_t)(BM * 16) : 0u, 128u),
+                                umma_desc_kmajor(s_base + G::SMEM_W + buf * W_STAGE, 256u, 128u), IDESC,
+                                st == s_b ? 0u : 1u);
+                        umma_commit(bar_mma + 8 * buf);
+                    }
+                    __syncwarp();
                 }
                 // shared-window address of this stage's tables: one IMAD per code forms the row
                 // address, the (k, quad) offsets are immediates of the loads
                 const uint32_t tb_addr = s_base + G::SMEM_TBL + (uint32_t)(buf * TBL_STAGE);
                 const uint8_t* at = smem + G::SMEM_A + buf * A_STAGE;
-                if (wlive) {
 #pragma unroll
-                    for (int pl = 0; pl < NPL; ++pl) {
-                        const uint4 av = *reinterpret_cast<const uint4*>(at + pl * (BM * 16) + tid * 16);
-                        const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
-                        if constexpr (!E16 && IDQ == 4 && P4W_K4) {
-                            // 4 k at a time: per quad the 4 words (k .. k+3) are transposed into one
-                            // word per column (6 PRMT) and summed by one dp4a each
+                for (int pl = 0; pl < NPL; ++pl) {
+                    uint4 av = make_uint4(0u, 0u, 0u, 0u);
+                    if (wlive) av = *reinterpret_cast<const uint4*>(at + pl * (BM * 16) + tid * 16);
+                    const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+                    if constexpr (TCE) {
+                        // one chunk = 4 k: the 16 words (k, quad) of the row go to staging column
+                        // 4 k + quad; the slice's E MMA sums column bytes j with j mod 16 == n
 #pragma unroll
-                            for (int kk = 0; kk < 16; kk += 4) {
-                                uint32_t ra[4];
+                        for (int kk = 0; kk < 16; kk += 4) {
+                            const uint32_t b = chunk % STG_BUFS;
+                            if (chunk >= (uint32_t)STG_BUFS) {
+                                mbar_wait(c_free + 8 * b, ((chunk / STG_BUFS) - 1) & 1u);
+                                tc_fence_after();
+                            }
+                            if (wlive) {
+                                uint32_t ra[4], v[16];
 #pragma unroll
                                 for (int i = 0; i < 4; ++i)
                                     ra[i] = tb_addr + __byte_perm(aw[kk >> 2], 0u, 0x4440u + i) * 4u;
 #pragma unroll
-                                for (int q = 0; q < 4; ++q) {
-                                    uint32_t v[4];
+                                for (int i = 0; i < 4; ++i)
 #pragma unroll
-                                    for (int i = 0; i < 4; ++i)
-                                        asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v[i])
+                                    for (int q = 0; q < 4; ++q)
+                                        asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v[4 * i + q])
                                                      : "r"(ra[i] + (uint32_t)(((pl * 16 + kk + i) * G::NQ + q) * TQ)));
-                                    const uint32_t t0 = __byte_perm(v[0], v[1], 0x5140u);   // c0 k0, c0 k1, c1 k0, c1 k1
-                                    const uint32_t t1 = __byte_perm(v[2], v[3], 0x5140u);   // c0 k2, c0 k3, c1 k2, c1 k3
-                                    const uint32_t t2 = __byte_perm(v[0], v[1], 0x7362u);   // c2 ..., c3 ...
-                                    const uint32_t t3 = __byte_perm(v[2], v[3], 0x7362u);
-                                    iacc[q][0] = __dp4a(__byte_perm(t0, t1, 0x5410u), 0x01010101u, iacc[q][0]);
-                                    iacc[q][1] = __dp4a(__byte_perm(t0, t1, 0x7632u), 0x01010101u, iacc[q][1]);
-                                    iacc[q][2] = __dp4a(__byte_perm(t2, t3, 0x5410u), 0x01010101u, iacc[q][2]);
-                                    iacc[q][3] = __dp4a(__byte_perm(t2, t3, 0x7632u), 0x01010101u, iacc[q][3]);
-                                }
+                                tmem_st16(t_stg + b * STG_COLS, v);
+                                tmem_wait_st();
                             }
-                            continue;
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(c_full + 8 * b);
+                            // the issuer sums the PREVIOUS chunk (its 4 warps have most likely
+                            // staged it by now), so it rarely waits on its slice
+                            if (iss_warp) {
+                                if (issuer && pend) issue_e(chunk - 1u);
+                                __syncwarp();
+                            }
+                            pend = true;
+                            ++chunk;
                         }
+                    } else if (DP4 && wlive) {
+                        // 4 k at a time: per quad the 4 words (k .. k+3) are transposed into one
+                        // word per column (6 PRMT) and summed by one dp4a each
+#pragma unroll
+                        for (int kk = 0; kk < 16; kk += 4) {
+                            uint32_t ra[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                ra[i] = tb_addr + __byte_perm(aw[kk >> 2], 0u, 0x4440u + i) * 4u;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                uint32_t v[4];
+#pragma unroll
+                                for (int i = 0; i < 4; ++i)
+                                    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v[i])
+                                                 : "r"(ra[i] + (uint32_t)(((pl * 16 + kk + i) * G::NQ + q) * TQ)));
+                                const uint32_t t0 = __byte_perm(v[0], v[1], 0x5140u);   // c0 k0, c0 k1, c1 k0, c1 k1
+                                const uint32_t t1 = __byte_perm(v[2], v[3], 0x5140u);   // c0 k2, c0 k3, c1 k2, c1 k3
+                                const uint32_t t2 = __byte_perm(v[0], v[1], 0x7362u);   // c2 ..., c3 ...
+                                const uint32_t t3 = __byte_perm(v[2], v[3], 0x7362u);
+                                iacc[q][0] = __dp4a(__byte_perm(t0, t1, 0x5410u), 0x01010101u, iacc[q][0]);
+                                iacc[q][1] = __dp4a(__byte_perm(t0, t1, 0x7632u), 0x01010101u, iacc[q][1]);
+                                iacc[q][2] = __dp4a(__byte_perm(t2, t3, 0x5410u), 0x01010101u, iacc[q][2]);
+                                iacc[q][3] = __dp4a(__byte_perm(t2, t3, 0x7632u), 0x01010101u, iacc[q][3]);
+                            }
+                        }
+                    } else if (E16 && wlive) {
 #pragma unroll
                         for (int kk = 0; kk < 16; kk += 2) {
                             const uint32_t ua0 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + (kk & 3));
                             const uint32_t ua1 = __byte_perm(aw[kk >> 2], 0u, 0x4440u + ((kk + 1) & 3));
                             const uint32_t r0 = tb_addr + ua0 * 4u, r1 = tb_addr + ua1 * 4u;
 #pragma unroll
-                            for (int q = 0; q < NACC; ++q) {
+                            for (int q = 0; q < 8; ++q) {
                                 uint32_t v0, v1;
                                 asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v0)
                                              : "r"(r0 + (uint32_t)(((pl * 16 + kk) * G::NQ + q) * TQ)));
                                 asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v1)
                                              : "r"(r1 + (uint32_t)(((pl * 16 + kk + 1) * G::NQ + q) * TQ)));
-                                if constexpr (E16) {
-                                    pacc[q][0] += v0 + v1;
-                                    pacc[q][1] += __byte_perm(v0, 0u, 0x4432u) + __byte_perm(v1, 0u, 0x4432u);
-                                } else if (q < IDQ) {
-                                    // interleave the two k's bytes per column pair, then one dp4a per
-                                    // column adds both k (biased bytes, unsigned)
-                                    const uint32_t x01 = __byte_perm(v0, v1, 0x5140u);   // c0 k, c0 k+1, c1 k, c1 k+1
-                                    const uint32_t x23 = __byte_perm(v0, v1, 0x7362u);   // c2 ..., c3 ...
-                                    iacc[q][0] = __dp4a(x01, 0x00000101u, iacc[q][0]);
-                                    iacc[q][1] = __dp4a(x01, 0x01010000u, iacc[q][1]);
-                                    iacc[q][2] = __dp4a(x23, 0x00000101u, iacc[q][2]);
-                                    iacc[q][3] = __dp4a(x23, 0x01010000u, iacc[q][3]);
-                                } else {
-                                    const uint32_t e0 = __byte_perm(v0, 0u, 0x4240u), e1 = __byte_perm(v1, 0u, 0x4240u);
-                                    const uint32_t o0 = __byte_perm(v0, 0u, 0x4341u), o1 = __byte_perm(v1, 0u, 0x4341u);
-                                    if (q < IDQ + P4W_ALU_QUADS) {     // ALU pipe: one 3-input add per accumulator
-                                        pacc[q][0] += e0 + e1;
-                                        pacc[q][1] += o0 + o1;
-                                    } else {         // FMA pipe: multiply-adds by an opaque 1
-                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e0), "r"(one));
-                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][0]) : "r"(e1), "r"(one));
-                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o0), "r"(one));
-                                        asm("mad.lo.u32 %0, %1, %2, %0;\n" : "+r"(pacc[q][1]) : "r"(o1), "r"(one));
-                                    }
-                                }
+                                pacc[q][0] += v0 + v1;
+                                pacc[q][1] += __byte_perm(v0, 0u, 0x4432u) + __byte_perm(v1, 0u, 0x4432u);
                             }
                         }
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_empty + 8 * buf);
-                // E8 with every quad on dp4a: 32-bit per-column sums never overflow (< 2^32 / 255
-                // lookups), so they stay in registers for the whole tile -- no TMEM flush
-                constexpr bool REG_E = !E16 && IDQ == 4;
-                if (!REG_E && ((st - s_b + 1) % G::FLUSH_STAGES == 0 || st + 1 == s_e)) {
+                if (E16 && ((st - s_b + 1) % G::FLUSH_STAGES == 0 || st + 1 == s_e)) {
+                    // E16: the 16-bit lane sums, decoded, are added into TMEM every 256 k
                     uint32_t ev[16];
                     if (!e_first) {
                         tmem_ld16(t_e, ev);
@@ -477,36 +527,25 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
 #pragma unroll
                         for (int j = 0; j < 16; ++j) ev[j] = 0u;
                     }
-                    if constexpr (E16) {
 #pragma unroll
-                        for (int q = 0; q < NACC; ++q) {
-                            ev[2 * q + 0] += pacc[q][0] - (pacc[q][1] << 16);
-                            ev[2 * q + 1] += pacc[q][1];
-                            pacc[q][0] = pacc[q][1] = 0u;
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            if (q < IDQ) {
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    ev[4 * q + j] += iacc[q < IDQ ? q : 0][j];
-                                    iacc[q < IDQ ? q : 0][j] = 0u;
-                                }
-                            } else {
-                                ev[4 * q + 0] += pacc[q][0] & 0xffffu;
-                                ev[4 * q + 2] += pacc[q][0] >> 16;
-                                ev[4 * q + 1] += pacc[q][1] & 0xffffu;
-                                ev[4 * q + 3] += pacc[q][1] >> 16;
-                                pacc[q][0] = pacc[q][1] = 0u;
-                            }
-                        }
+                    for (int q = 0; q < 8; ++q) {
+                        ev[2 * q + 0] += pacc[q][0] - (pacc[q][1] << 16);
+                        ev[2 * q + 1] += pacc[q][1];
+                        pacc[q][0] = pacc[q][1] = 0u;
                     }
                     tmem_st16(t_e, ev);
                     tmem_wait_st();
                     e_first = false;
                 }
             }
+            if (iss_warp) {
+                if (issuer) {
+                    if (pend) issue_e(chunk - 1u);
+                    umma_commit(t_full + 8 * tb);
+                }
+                __syncwarp();
+            }
+            pend = false;
             int corr = (E16 ? 32768 : p4::E_BIAS) * KS * (s_e - s_b);
             if (s_e == nst_all) corr += (int)(((P.Kp - p.K) + p.pad_lookups) * (int64_t)p.t00);
             // the row's residual groups: issued before the wait on the tile's MMAs, so their
@@ -521,23 +560,26 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
 #pragma unroll
                 for (int j = 0; j < TN / 4; ++j) res[j] = __ldg(rp + j);
             }
-            // exact part of this tile: TMEM set tb, complete once tile_full[tb] flips
-            mbar_wait(bar_tfull + 8 * tb, (tcount >> 1) & 1u);
+            // this tile's sums: TMEM set tb (exact part + E sums for TCE), complete once tile_full[tb] flips
+            mbar_wait(t_full + 8 * tb, tph);
             tc_fence_after();
             uint32_t ex[16], es[16];
-            tmem_ld16(tmem + t_lane + tb * 128u + slice_col, ex);
-            if constexpr (!E16 && IDQ == 4) {
+            tmem_ld16(d_acc + t_lane, ex);
+            if constexpr (TCE) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) es[j] = 0u;
+            } else if constexpr (DP4) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) es[4 * q + j] = iacc[q < IDQ ? q : 0][j];
+                    for (int j = 0; j < 4; ++j) es[4 * q + j] = iacc[q][j];
             } else {
                 tmem_ld16(t_e, es);
             }
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tfree + 8 * tb);   // set tb may be overwritten
+            if (lane == 0) mbar_arrive(t_free + 8 * tb);   // set tb may be overwritten
             ++tcount;
             int eacc[16];
 #pragma unroll
