@@ -3,6 +3,7 @@
 #include "../../include/axq.h"
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -906,6 +907,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
 static std::atomic<int> g_p4w_main_cw{28};        // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
 static std::atomic<int64_t> g_p4w_main_cw_max_k{1 << 30};   // ... for layers with K up to this
 static std::atomic<int> g_p4w_res_cw{20};         // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape (r2: 20 after the specialised epilogue)
+static std::atomic<int> g_p4w_tma{1};             // AXQ_P4W_TMA: GEMM-row activation planes by TMA
 static std::atomic<int> g_p4w_cw{0};              // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
 static std::atomic<int64_t> g_sk_full_waves{8};   // AXQ_SK_FULL_WAVES: P4W layers of fewer than this many waves of
                                                   // tiles cut every iteration (no whole-wave phase): measured
@@ -927,7 +929,44 @@ static void p4w_read_env() {
         if (const char* v = std::getenv("AXQ_P4W_MAIN_CW")) g_p4w_main_cw = std::atoi(v);
         if (const char* v = std::getenv("AXQ_SK_FULL_WAVES")) g_sk_full_waves = std::atoll(v);
         if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
+        if (const char* v = std::getenv("AXQ_P4W_TMA")) g_p4w_tma = std::atoi(v);
     });
+}
+
+// cuTensorMapEncodeTiled from the driver (no link-time libcuda dependency)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+// P4W GEMM-row operand (plain GEMM, 1x1 / stride-1 / unpadded conv): a 2D u8 tensor map over
+// [M][K] with row stride lda, box 16 k x 128 rows (one MMA slice of one 16-k plane); rows >= M
+// and k >= K are zero-filled by the copy engine like the cp.async loader's zero-fill.  False
+// (cp.async loader kept) when the layout does not meet the copy engine's rules.
+static bool p4w_encode_tma(axq::P4Args& a) {
+    const axq::MMArgs& p = a.mm;
+    if (!g_p4w_tma.load() || a.is_conv || a.c4 || a.grp_cout || p.M <= 0 || p.M >= ((int64_t)1 << 31) ||
+        p.K <= 0 || p.K >= ((int64_t)1 << 31) || (p.lda & 15) != 0 || p.lda >= ((int64_t)1 << 40) ||
+        (reinterpret_cast<uintptr_t>(p.A) & 15) != 0)
+        return false;
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M};
+    cuuint64_t strides[1] = {(cuuint64_t)p.lda};
+    cuuint32_t box[2] = {16u, 128u};
+    cuuint32_t es[2] = {1u, 1u};
+    CUresult r = enc(&a.tmap_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(p.A), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 axq_status axq_wpack_shapes(int main_cw, int res_cw, int small_cw) {
@@ -1029,6 +1068,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
                       a.stages_per_split);
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
+    a.tma_a = (variant == 3 && p4w_encode_tma(a)) ? 1 : 0;
     auto launch = [&](const axq::P4Args& x) { return variant == 3 ? axq::launch_p4w(x, st) : axq::launch_p4(x, st); };
     int path = wp->e16 ? AXQ_PATH_P4W16 : variant == 3 ? AXQ_PATH_P4W : AXQ_PATH_P4;
     if (use_tc && ep && ep->workspace && ws_elems >= streamk_elems(bm) &&

@@ -1,6 +1,7 @@
 // lut_p4_args.h -- tile constants and launch arguments of the P4 kernel (lut_p4.cuh).
 #pragma once
 #include <cstdint>
+#include <cuda.h>   // CUtensorMap (the type only; the encoder is fetched from the driver at run time)
 
 #include "lut_mm.cuh"
 
@@ -66,6 +67,10 @@ struct P4Args {
     int nb_fast;                // tile order: column block fastest (the layer's tables stay in
                                 // L2 and each activation tile is read from HBM once) instead of
                                 // row tile fastest (concurrent CTAs share one table stream)
+    int tma_a;                  // P4W GEMM-row loader: activation planes by TMA (tmap_a) instead
+                                // of per-row cp.async (no LSU wavefronts for the operand stream)
+    alignas(64) CUtensorMap tmap_a;   // 2D u8 [M][K] (row stride lda), box 16 k x 128 rows,
+                                      // out-of-range rows and k >= K read as zeros
 };
 
 }  // namespace axq

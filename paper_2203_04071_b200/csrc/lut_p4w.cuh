@@ -3,21 +3,24 @@
 // in int32, exact, as  sum_k a*w (tcgen05.mma kind::i8, TMEM)  +  sum_k E[a][w] (packed tables).
 //
 // Roles inside one persistent CTA (1024 threads, one CTA per SM):
-//  * 3 producer warps (warps CW..CW+2) stream the operands of each (tile, stage) item into a
+//  * 4 producer warps (warps CW..CW+3) stream the operands of each (tile, stage) item into a
 //    ring of STAGES shared-memory buffers: the activation rows by cp.async (implicit im2col,
 //    zero-fill = padding taps), completion signalled with cp.async.mbarrier.arrive; the packed
 //    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
 //    the consumer warps released it (empty barrier) and the MMA that read it completed.
 //  * CW consumer warps (one tile row per lane) only wait for full buffers and do the lookups
-//    (4 per 32-bit LDS).  E8 tables (TCE): the gathered words of 4 k x 4 quads (16 words, 64
-//    biased E bytes of the row) go to a TMEM staging buffer with one tcgen05.st, and the
-//    tensor core sums them: D[m][n] += sum_j G[m][j] * SEL[j][n], SEL[j][n] = (j mod 16 == n),
-//    G read from TMEM (kind::i8, u8 x u8) -- no per-lookup ALU work in the consumer warps.
-//    E16 tables: 16-bit lane sums in registers, flushed to TMEM.
-//  * The MMA warp (warp CW+3, lane 0 issues) runs per stage the exact-part MMAs (slices of 128
-//    rows, M = 128, N = 16, K = 32) and per staged chunk the E MMAs, all into one of two TMEM
-//    accumulator sets (double-buffered across tiles, so the next tile's MMAs never wait for
-//    this tile's epilogue reads).  No CTA-wide barrier in the steady state.
+//    (4 per 32-bit LDS).  E8 tables: per quad and 4 k the 4 words are byte-transposed and each
+//    column summed by one dp4a into a 32-bit register sum kept for the whole tile.  E16
+//    tables: 16-bit lane sums in registers, flushed to TMEM.  (P4W_TCE = 1, measured slower:
+//    the gathered words of 4 k x 4 quads go to a TMEM staging buffer with one tcgen05.st and
+//    the tensor core sums them, D[m][n] += sum_j G[m][j] * SEL[j][n] with SEL[j][n] =
+//    (j mod 16 == n), G read from TMEM, kind::i8 u8 x u8.)
+//  * Each 128-row MMA slice has an issuer (lane 0 of one of its 4 warps, spread over the SM
+//    sub-partitions) that issues the slice's exact-part MMAs (M = 128, N = 16, K = 32) per
+//    stage -- and the TCE E MMAs -- into one of two TMEM accumulator sets (double-buffered
+//    across tiles, so the next tile's MMAs never wait for this tile's epilogue reads); one
+//    issuing thread per accumulator keeps them in issue order.  No CTA-wide barrier in the
+//    steady state.
 //  * Row 32*w + lane of a tile is TMEM lane 32*(w % 4) + lane of MMA slice w / 4, so every
 //    consumer warp reads and writes exactly the TMEM lane quarter it may access.
 //  * Tile order, stream-K tail (exact int32 pieces in the zero-filled workspace), split-K for
@@ -60,6 +63,9 @@ constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots 
 
 #ifndef P4W_TCE
 #define P4W_TCE 0
+#endif
+#ifndef P4W_TMA_ON
+#define P4W_TMA_ON 1
 #endif
 #ifndef P4W_SMALL_FULL_STAGES
 #define P4W_SMALL_FULL_STAGES 3
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             // grouped conv: this column tile's group selects its input channels
             const int64_t goff = P.grp_cout ? (nb * TN / P.grp_cout) * P.grp_cin : 0;
 #pragma unroll 1
-            for (int r = pt; r < BM; r += PT) {
+            for (int r = pt; r < ((P4W_TMA_ON && P.tma_a) ? 0 : BM); r += PT) {
                 const RowInfo ri = P.is_conv ? make_row<LOAD_CONV>(p, m0 + r) : make_row<LOAD_GEMM>(p, m0 + r);
                 const int64_t ro = ri.base + goff + (P.is_conv ? ((int64_t)ri.hb * p.Wd + ri.wb) * pix : 0);
                 rowinfo[r] = make_int4((int)(ro & 0xffffffff), (int)(ro >> 32), ri.hb,
@@ -293,7 +299,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                 for (int pl = 0; pl < NPL; ++pl) {
                     const int64_t k0 = (int64_t)st * KS + 16 * pl;
                     const uint32_t dst0 = s_base + G::SMEM_A + buf * A_STAGE + pl * (BM * 16);
-                    if (P.c4) {
+                    if (P4W_TMA_ON && P.tma_a) {
+                        // one 16 k x 128 row box per MMA slice, issued with the table copies
+                    } else if (P.c4) {
                         uint32_t tv[4];
 #pragma unroll
                         for (int j = 0; j < 4; ++j) tv[j] = tap_s[(int)(k0 >> 2) + j];
@@ -308,20 +316,24 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                                                 (unsigned)(ri.z + rdh) < (unsigned)p.H &&
                                                 (unsigned)(ri.w + sdw) < (unsigned)p.Wd;
                                 const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * pix + (int)(tv[j] >> 16);
-                                cp_async4(dst0 + r * 16 + 4 * j, ok ? p.A + ro + toff : p.A, ok ? 4u : 0u);
+                                cp_async4_p(dst0 + r * 16 + 4 * j, ok ? p.A + ro + toff : p.A, ok);
                             }
                         }
                     } else if (P.is_conv) {
                         const int rdh = t_r * p.dh, sdw = t_s * p.dw;
-                        const int64_t toff = ((int64_t)rdh * p.Wd + sdw) * pix + t_c;
+                        // the tap's source base, formed once per plane (pinned in a register: left
+                        // to itself the compiler re-derives it per row inside the row's branch)
+                        const int8_t* a_tap = p.A + (((int64_t)rdh * p.Wd + sdw) * pix + t_c);
+                        asm volatile("" : "+l"(a_tap));
                         const bool kin = k0 < p.K;
+                        const unsigned H = (unsigned)p.H, Wd = (unsigned)p.Wd;
 #pragma unroll 1
                         for (int r = pt; r < BM; r += PT) {
                             const int4 ri = rowinfo[r];
                             const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
-                            const bool ok = kin && ri.w != (int)0x80000000 && (unsigned)(ri.z + rdh) < (unsigned)p.H &&
-                                            (unsigned)(ri.w + sdw) < (unsigned)p.Wd;
-                            cp_async16(dst0 + r * 16, ok ? p.A + ro + toff : p.A, ok ? 16u : 0u);
+                            const bool ok = kin && ri.w != (int)0x80000000 && (unsigned)(ri.z + rdh) < H &&
+                                            (unsigned)(ri.w + sdw) < Wd;
+                            cp_async16_p(dst0 + r * 16, ok ? a_tap + ro : p.A, ok);
                         }
                         t_c += 16;
                         if (t_c >= p.C) {
@@ -336,7 +348,8 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                             const int4 ri = rowinfo[r];
                             const int64_t ro = (int64_t)(uint32_t)ri.x | ((int64_t)ri.y << 32);
                             const bool ok = ri.w != (int)0x80000000 && nbytes > 0;
-                            cp_async16(dst0 + r * 16, ok ? p.A + ro + k0 : p.A, ok ? nbytes : 0u);
+                            if (nbytes == 16u) cp_async16_p(dst0 + r * 16, ok ? p.A + ro + k0 : p.A, ok);
+                            else cp_async16(dst0 + r * 16, ok ? p.A + ro + k0 : p.A, ok ? nbytes : 0u);
                         }
                     }
                 }
@@ -345,7 +358,17 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                     const uint32_t bar = bar_full + 8 * buf;
                     const uint32_t* tbl_g = P.tables + ((size_t)nb * P.Kp + (size_t)st * KS) * G::NQ * G::TROWS;
                     const int8_t* w_g = P.wpk + ((size_t)nb * (P.Kp / 16) + (size_t)st * NPL) * p4::W_STAGE;
-                    mbar_expect_tx(bar, TBL_STAGE + NPL * p4::W_STAGE);
+                    mbar_expect_tx(bar, TBL_STAGE + NPL * p4::W_STAGE + ((P4W_TMA_ON && P.tma_a) ? NPL * BM * 16 : 0));
+#if P4W_TMA_ON
+                    if (P4W_TMA_ON && P.tma_a) {
+#pragma unroll
+                        for (int pl = 0; pl < NPL; ++pl)
+#pragma unroll 1
+                            for (int j = 0; j < SLICES; ++j)
+                                tma_load_2d(s_base + G::SMEM_A + buf * A_STAGE + pl * (BM * 16) + j * 128 * 16,
+                                            &P.tmap_a, st * KS + 16 * pl, (int)(m0 + j * 128), bar);
+                    }
+#endif
                     bulk_g2s(s_base + G::SMEM_TBL + buf * TBL_STAGE, tbl_g, TBL_STAGE, bar);
                     bulk_g2s(s_base + G::SMEM_W + buf * W_STAGE, w_g, NPL * p4::W_STAGE, bar);
                 }
