@@ -47,6 +47,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int 
         : "memory");
 }
 
+// 4D im2col-mode copy: pixelsPerColumn output pixels starting at the window corner (w, h, n),
+// channels c .. c + channelsPerPixel - 1 of the tap at offset (ow, oh) inside the window
+__device__ __forceinline__ void tma_load_im2col(uint32_t dst, const void* tmap, int c, int w, int h, int n,
+                                                uint16_t ow, uint16_t oh, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"(ow), "h"(oh)
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }

@@ -907,7 +907,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
 static std::atomic<int> g_p4w_main_cw{28};        // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
 static std::atomic<int64_t> g_p4w_main_cw_max_k{1 << 30};   // ... for layers with K up to this
 static std::atomic<int> g_p4w_res_cw{20};         // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape (r2: 20 after the specialised epilogue)
-static std::atomic<int> g_p4w_tma{1};             // AXQ_P4W_TMA: GEMM-row activation planes by TMA
+static std::atomic<int> g_p4w_tma{2};             // AXQ_P4W_TMA: activation planes by TMA (0 off, 1 GEMM rows, 2 + im2col)
 static std::atomic<int> g_p4w_cw{0};              // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
 static std::atomic<int64_t> g_sk_full_waves{8};   // AXQ_SK_FULL_WAVES: P4W layers of fewer than this many waves of
                                                   // tiles cut every iteration (no whole-wave phase): measured
@@ -934,6 +934,19 @@ static void p4w_read_env() {
 }
 
 // cuTensorMapEncodeTiled from the driver (no link-time libcuda dependency)
+static PFN_cuTensorMapEncodeIm2col_v12000 tmap_encoder_im2col() {
+    static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(ptr);
+    });
+    return fn;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -966,6 +979,41 @@ static bool p4w_encode_tma(axq::P4Args& a) {
     CUresult r = enc(&a.tmap_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(p.A), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// P4W implicit-im2col operand (a conv, any padding / stride, 16-channel planes): an im2col
+// tensor map over the NHWC input [N][H][W][pix] -- each copy loads 128 consecutive output
+// pixels' 16 channels of one tap (row, image boundaries and padding taps handled by the copy
+// engine's traversal of the window-corner box, padding zero-filled), i.e. one MMA slice of one
+// plane.  Square, symmetric windows only (the box corners are then order-free); the host checks
+// that the box's traversal yields exactly Ho x Wo positions.
+static bool p4w_encode_im2col(axq::P4Args& a) {
+    const axq::MMArgs& p = a.mm;
+    if (!g_p4w_tma.load() || !a.is_conv || a.c4 || a.grp_cout || p.M <= 0 || p.M >= ((int64_t)1 << 31) ||
+        (p.C & 15) != 0 || (reinterpret_cast<uintptr_t>(p.A) & 15) != 0 || p.ph != p.pw || p.sh != p.sw ||
+        p.dh != p.dw || p.sh < 1 || p.sh > 8)
+        return false;
+    const int64_t pix = p.cs ? p.cs : p.C;
+    const int64_t rs = p.K / p.C, R = rs / p.S;
+    if (R * p.S * p.C != p.K || R != p.S || (pix & 15) != 0) return false;
+    const int64_t hw = (int64_t)p.Ho * p.Wo, n_img = p.M / hw;
+    if (n_img * hw != p.M) return false;
+    const int lo = -p.pw, up = p.pw - (int)(R - 1) * p.dw;
+    if (lo < -128 || lo > 127 || up < -128 || up > 127) return false;
+    // positions the traversal visits per row / column must be the output extents
+    if ((p.Wd - 1 + up - lo) < 0 || (p.Wd - 1 + up - lo) / p.sw + 1 != p.Wo ||
+        (p.H - 1 + up - lo) / p.sh + 1 != p.Ho)
+        return false;
+    auto enc = tmap_encoder_im2col();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)pix, (cuuint64_t)p.Wd, (cuuint64_t)p.H, (cuuint64_t)n_img};
+    cuuint64_t strides[3] = {(cuuint64_t)pix, (cuuint64_t)(pix * p.Wd), (cuuint64_t)(pix * p.Wd * p.H)};
+    int lower[2] = {lo, lo}, upper[2] = {up, up};
+    cuuint32_t es[4] = {1u, (cuuint32_t)p.sw, (cuuint32_t)p.sh, 1u};
+    CUresult r = enc(&a.tmap_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(p.A), dims, strides, lower,
+                     upper, 16u, 128u, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -1068,7 +1116,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
                       a.stages_per_split);
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
-    a.tma_a = (variant == 3 && p4w_encode_tma(a)) ? 1 : 0;
+    a.tma_a = variant != 3 ? 0 : p4w_encode_tma(a) ? 1 : (g_p4w_tma.load() >= 2 && p4w_encode_im2col(a)) ? 2 : 0;
     auto launch = [&](const axq::P4Args& x) { return variant == 3 ? axq::launch_p4w(x, st) : axq::launch_p4(x, st); };
     int path = wp->e16 ? AXQ_PATH_P4W16 : variant == 3 ? AXQ_PATH_P4W : AXQ_PATH_P4;
     if (use_tc && ep && ep->workspace && ws_elems >= streamk_elems(bm) &&

@@ -281,6 +281,19 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                 rowinfo[r] = make_int4((int)(ro & 0xffffffff), (int)(ro >> 32), ri.hb,
                                        ri.valid ? ri.wb : (int)0x80000000);
             }
+            // im2col mode: each slice's first output pixel as its window corner (w, h, n)
+            int4 im_crd[SLICES];
+            if (P.tma_a == 2 && pt == 0) {
+                const uint32_t hw = (uint32_t)p.Ho * (uint32_t)p.Wo;
+#pragma unroll
+                for (int j = 0; j < SLICES; ++j) {
+                    const int64_t m = m0 + j * 128;
+                    const uint32_t mm = (uint32_t)(m < p.M ? m : p.M);   // rows past M: image N (zeros)
+                    const uint32_t img = mm / hw, rem = mm - img * hw, ho = rem / (uint32_t)p.Wo,
+                                   wo = rem - ho * (uint32_t)p.Wo;
+                    im_crd[j] = make_int4((int)wo * p.sw - p.pw, (int)ho * p.sh - p.ph, (int)img, 0);
+                }
+            }
             int t_r = 0, t_s = 0, t_c = 0;
             if (P.is_conv && !P.c4) {
                 const int k0 = s_b * KS, rs = k0 / p.C;
@@ -360,13 +373,29 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                     const int8_t* w_g = P.wpk + ((size_t)nb * (P.Kp / 16) + (size_t)st * NPL) * p4::W_STAGE;
                     mbar_expect_tx(bar, TBL_STAGE + NPL * p4::W_STAGE + ((P4W_TMA_ON && P.tma_a) ? NPL * BM * 16 : 0));
 #if P4W_TMA_ON
-                    if (P4W_TMA_ON && P.tma_a) {
+                    if (P.tma_a == 1) {
 #pragma unroll
                         for (int pl = 0; pl < NPL; ++pl)
 #pragma unroll 1
                             for (int j = 0; j < SLICES; ++j)
                                 tma_load_2d(s_base + G::SMEM_A + buf * A_STAGE + pl * (BM * 16) + j * 128 * 16,
                                             &P.tmap_a, st * KS + 16 * pl, (int)(m0 + j * 128), bar);
+                    } else if (P.tma_a == 2) {
+#pragma unroll
+                        for (int pl = 0; pl < NPL; ++pl) {
+                            // plane k0 = (r * S + s) * C + c: tap (r, s), channels c .. c + 15;
+                            // planes past K read channel C (out of range: zeros)
+                            const int k0 = st * KS + 16 * pl;
+                            const int rs = k0 / p.C, c = k0 < p.K ? k0 - rs * p.C : (p.cs ? p.cs : p.C);
+                            const int r = rs / p.S, s_ = rs - r * p.S;
+#pragma unroll 1
+                            for (int j = 0; j < SLICES; ++j) {
+                                const int4 cj = im_crd[j];
+                                tma_load_im2col(s_base + G::SMEM_A + buf * A_STAGE + pl * (BM * 16) + j * 128 * 16,
+                                                &P.tmap_a, c, cj.x, cj.y, cj.z, (uint16_t)(s_ * p.dw),
+                                                (uint16_t)(r * p.dh), bar);
+                            }
+                        }
                     }
 #endif
                     bulk_g2s(s_base + G::SMEM_TBL + buf * TBL_STAGE, tbl_g, TBL_STAGE, bar);
