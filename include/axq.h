@@ -69,6 +69,8 @@ typedef struct axq_lut* axq_lut_t;
 #define AXQ_PATH_WIDEPK 9     /* lut_widepk_kernel: packed wide (b = 9..12) tables (NEXT-2) */
 #define AXQ_PATH_SPLITK 0x100 /* K split across CTAs (int32 atomics + epilogue pass) */
 #define AXQ_PATH_STREAMK 0x200/* stream-K pieces in the caller's workspace */
+#define AXQ_PATH_TMA 0x400    /* P4W activation planes by TMA, 2D tiled (GEMM rows) */
+#define AXQ_PATH_TMA_IM2COL 0x800 /* P4W activation planes by TMA, im2col mode (convs) */
 axq_status axq_last_path(int* out);
 
 /* Returns the CUDA error code of the last AXQ_ERR_CUDA on this thread (0 if none). */

@@ -40,7 +40,7 @@ EXPORTED = [
 # axq_last_path kernel families (include/axq.h AXQ_PATH_*)
 PATH_NAMES = {1: "v1", 2: "p4", 3: "p4w", 4: "gconv", 5: "wide", 6: "lstm_rec", 7: "f32a",
               8: "p4w16", 9: "widepk"}
-PATH_SPLITK, PATH_STREAMK = 0x100, 0x200
+PATH_SPLITK, PATH_STREAMK, PATH_TMA, PATH_TMA_IM2COL = 0x100, 0x200, 0x400, 0x800
 
 
 class AxqError(RuntimeError):

@@ -1119,6 +1119,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     a.tma_a = variant != 3 ? 0 : p4w_encode_tma(a) ? 1 : (g_p4w_tma.load() >= 2 && p4w_encode_im2col(a)) ? 2 : 0;
     auto launch = [&](const axq::P4Args& x) { return variant == 3 ? axq::launch_p4w(x, st) : axq::launch_p4(x, st); };
     int path = wp->e16 ? AXQ_PATH_P4W16 : variant == 3 ? AXQ_PATH_P4W : AXQ_PATH_P4;
+    path |= a.tma_a == 1 ? AXQ_PATH_TMA : a.tma_a == 2 ? AXQ_PATH_TMA_IM2COL : 0;
     if (use_tc && ep && ep->workspace && ws_elems >= streamk_elems(bm) &&
         (reinterpret_cast<uintptr_t>(ep->workspace) & 15) == 0) {
         // stream-K whenever whole tiles would leave a partial wave (exact int32 pieces in the
