@@ -281,8 +281,9 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                 rowinfo[r] = make_int4((int)(ro & 0xffffffff), (int)(ro >> 32), ri.hb,
                                        ri.valid ? ri.wb : (int)0x80000000);
             }
-            // im2col mode: each slice's first output pixel as its window corner (w, h, n)
-            int4 im_crd[SLICES];
+            // im2col mode: each slice's first output pixel as its window corner (w, h, n), kept
+            // in the (otherwise unused) row-info slots, not in registers
+            int4* im_crd = rowinfo;
             if (P.tma_a == 2 && pt == 0) {
                 const uint32_t hw = (uint32_t)p.Ho * (uint32_t)p.Wo;
 #pragma unroll
