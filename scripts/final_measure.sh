@@ -15,6 +15,15 @@ timeout 600 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-contr
 python scripts/layer_table.py $O/launches_b256.csv 256 > $O/resnet_layers_b256_p4w.txt 2>&1
 python scripts/layer_table.py $O/launches_b32.csv 32 > $O/resnet_layers_b32_p4w.txt 2>&1
 rm -f $O/launches_b256.csv $O/launches_b32.csv
+# DRAM traffic of one 256-image forward (roofline.traffic) and full captures of three real-data
+# layers (3x3 s2b0.c2, residual K=64 s0b1.c3, residual K=256 s2b1.c3)
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --log-file $O/traffic.csv python scripts/profile_resnet.py 256 1 > /dev/null 2>&1
+python scripts/traffic_c3.py $O/traffic.csv > $O/traffic_c3_forward.json 2>&1; rm -f $O/traffic.csv
+for i in 26 7 30; do
+  timeout 900 ncu --set full --profile-from-start off -k regex:lut_p4w --launch-skip $i --launch-count 1 -o /tmp/fm_l$i python scripts/prof_net_layer.py > /dev/null 2>&1
+  ncu -i /tmp/fm_l$i.ncu-rep --page raw --csv > $O/ncu_net_l$i.csv 2>/dev/null
+  python scripts/ncu_summary.py $O/ncu_net_l$i.csv > $O/ncu_net_l${i}_summary.json 2>&1
+done
 for f in $O/bench_*_final.json $O/ref_resnet_final.json; do python -c "
 import json,sys; d=json.load(open('$f')); print('$f'.split('/')[-1], d.get('value'), d.get('ms_per_step'), (d.get('roofline') or {}).get('frac'), (d.get('e2e') or {}).get('value'), (d.get('clocks') or {}).get('sm_mhz'), (d.get('clocks') or {}).get('reasons'))" 2>&1 | tail -1; done
 grep predicted $O/scaling_probe_p4w.txt | tail -4
