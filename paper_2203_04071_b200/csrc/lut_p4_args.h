@@ -71,6 +71,8 @@ struct P4Args {
                                 // of per-row cp.async (no LSU wavefronts for the operand stream)
     alignas(64) CUtensorMap tmap_a;   // 2D u8 [M][K] (row stride lda), box 16 k x 128 rows,
                                       // out-of-range rows and k >= K read as zeros
+    int tma_res;                // P4W residual layers: the epilogue's fp32 residual rows by TMA
+    alignas(64) CUtensorMap tmap_res; // 2D fp32 [M][N] (row stride ldr), box 16 cols x 128 rows
 };
 
 }  // namespace axq

@@ -72,7 +72,7 @@ constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots 
 #endif
 // E16 (P4W16, tables whose E = LUT - a*w does not fit int8 but fits int16): a packed word holds
 // the biased E of 2 columns (a column pair) instead of 4 (a quad), so NQ = 8 words per k.
-template <bool HALF, int KSX = (HALF ? 32 : 16), int CWX = 28, bool E16 = false>
+template <bool HALF, int KSX = (HALF ? 32 : 16), int CWX = 28, bool E16 = false, bool RESX = false>
 struct Geo {
     static constexpr int BM = Shape<CWX>::BM;
     static constexpr int SLICES = Shape<CWX>::SLICES;
@@ -99,11 +99,19 @@ struct Geo {
     static constexpr int SMEM_BAR = SMEM_ROW + BM * 16;
     // full[S], empty[S], mma[S], tile_full[SLICES][2], tmem_free[SLICES][2],
     // chunk_full[SLICES][STG_BUFS], chunk_free[SLICES][STG_BUFS], then tmem address, flag
-    static constexpr int NBAR = 3 * STAGES + 4 * SLICES + 2 * SLICES * STG_BUFS;
+    // ... + res_full, res_free (residual-layer shapes with a residual buffer)
+    static constexpr int NBAR = 3 * STAGES + 4 * SLICES + 2 * SLICES * STG_BUFS + 2;
     static constexpr int SMEM_MISC = SMEM_BAR + 8 * NBAR;
     static constexpr int SMEM_KC = SMEM_MISC + 16;                 // EpiConst (32 B)
     static constexpr int SMEM_TAP = SMEM_KC + 32;
-    static constexpr int SMEM_BYTES = SMEM_TAP + (HAS_TAP ? p4::TAP_BYTES : 0);
+    static constexpr int SMEM_END = SMEM_TAP + (HAS_TAP ? p4::TAP_BYTES : 0);
+    // residual layers whose shape leaves room: the tile's fp32 residual rows [BM][16] staged by
+    // TMA (issued by consumer thread 0 as the tile's last stage starts), read from shared memory
+    // by the epilogue
+    static constexpr int SMEM_RES = (SMEM_END + 127) / 128 * 128;
+    static constexpr bool RESBUF = RESX && SMEM_RES + BM * 64 <= 232448;
+    static constexpr int SMEM_BYTES = RESBUF ? SMEM_RES + BM * 64 : SMEM_END;
+    static constexpr int NT_EXTRA = 0;
     static_assert(SMEM_BYTES <= 232448, "P4W shared memory exceeds 227 KiB");
 };
 }  // namespace p4w
@@ -121,9 +129,10 @@ __device__ __forceinline__ void consumer_sync() {   // named barrier 1: the BM_ 
 // residual rows before waiting on the tile's MMAs (their latency overlaps the wait).  Kept out
 // of the other layers' instantiation: its extra live registers would spill into their loop.
 template <bool HALF, int KSX, bool RES = false, int CWX = 28, bool E16 = false>
-__global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const __grid_constant__ P4Args P) {
+__global__ void __launch_bounds__(p4w::Shape<CWX>::NT + p4w::Geo<HALF, KSX, CWX, E16, RES>::NT_EXTRA, 1)
+    lut_p4w_kernel(const __grid_constant__ P4Args P) {
     using namespace p4w;
-    using G = p4w::Geo<HALF, KSX, CWX, E16>;
+    using G = p4w::Geo<HALF, KSX, CWX, E16, RES>;
     using S = p4w::Shape<CWX>;
     constexpr int CW = S::CW, NT = S::NT, BM = S::BM, SLICES = S::SLICES, PT = S::PT;
     constexpr int KS = G::KS, STAGES = G::STAGES, TBL_STAGE = G::TBL_STAGE, TQ = G::TQ, A_STAGE = G::A_STAGE;
@@ -144,6 +153,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
     const uint32_t bar_tfree = bar_tfull + 16 * SLICES;  // [SLICES][2]
     const uint32_t bar_cfull = bar_tfree + 16 * SLICES;  // [SLICES][STG_BUFS]
     const uint32_t bar_cfree = bar_cfull + 8 * SLICES * STG_BUFS;
+    const uint32_t bar_rfull = bar_cfree + 8 * SLICES * STG_BUFS, bar_rfree = bar_rfull + 8;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + G::SMEM_MISC);
     int* fin_flag = reinterpret_cast<int*>(smem + G::SMEM_MISC + 4);
 
@@ -187,6 +197,8 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
             mbar_init(bar_cfull + 8 * s, 4);         // the slice's 4 consumer warps
             mbar_init(bar_cfree + 8 * s, 1);         // the E MMAs' commit
         }
+        mbar_init(bar_rfull, 1);                     // the residual copies (expect_tx)
+        mbar_init(bar_rfree, CW);                    // every consumer warp read its rows
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 0) {
@@ -429,7 +441,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
         gen_init(g);
         int64_t tile;
         int s_b, s_e;
-        uint32_t item = 0, tcount = 0, chunk = 0;
+        uint32_t item = 0, tcount = 0, chunk = 0, rcount = 0;
         bool pend = false;   // the issuer's staged chunk chunk - 1 is not summed yet
         while (gen_next(g, tile, s_b, s_e)) {
             int64_t nb, m0;
@@ -477,6 +489,16 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                         umma_commit(bar_mma + 8 * buf);
                     }
                     __syncwarp();
+                }
+                if (G::RESBUF && P.tma_res && tid == 0 && st + 1 == s_e) {
+                    // the tile's residual rows: one 16-column x 128-row fp32 box per slice, once
+                    // every warp has read the previous piece's (res_free)
+                    if (rcount > 0) mbar_wait(bar_rfree, (rcount - 1) & 1u);
+                    mbar_expect_tx(bar_rfull, BM * 64);
+#pragma unroll 1
+                    for (int j = 0; j < SLICES; ++j)
+                        tma_load_2d(s_base + G::SMEM_RES + j * 128 * 64, &P.tmap_res, (int)n0, (int)(m0 + j * 128),
+                                    bar_rfull);
                 }
                 // shared-window address of this stage's tables: one IMAD per code forms the row
                 // address, the (k, quad) offsets are immediates of the loads
@@ -608,7 +630,18 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT, 1) lut_p4w_kernel(const _
                              (kconst.mode == EPI_RES_RELU_Y_Q ? n0 + TN <= p.N
                                                                : p.ep.residual != nullptr && p4t_vec_ok(P, n0));
             float4 res[TN / 4];
-            if (pre) {
+            if (G::RESBUF && P.tma_res) {
+                // the residual rows staged by the residual-copy warp
+                mbar_wait(bar_rfull, rcount & 1u);
+                if (pre) {
+                    const float4* rs = reinterpret_cast<const float4*>(smem + G::SMEM_RES + tid * 64);
+#pragma unroll
+                    for (int j = 0; j < TN / 4; ++j) res[j] = rs[j];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_rfree);
+                ++rcount;
+            } else if (pre) {
                 const float4* rp = reinterpret_cast<const float4*>(p.ep.residual + m_row * p.ep.ldr + n0);
 #pragma unroll
                 for (int j = 0; j < TN / 4; ++j) res[j] = __ldg(rp + j);

@@ -77,7 +77,7 @@ int g_p4w_pdl = 1;   // programmatic dependent launch of P4W (AXQ_P4W_PDL=0 disa
 
 template <bool HALF, int KSX, bool RES = false, int CWX = 28, bool E16 = false>
 static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
-    using G = p4w::Geo<HALF, KSX, CWX, E16>;
+    using G = p4w::Geo<HALF, KSX, CWX, E16, RES>;
     using S = p4w::Shape<CWX>;
     static unsigned configured = 0;
     int dev = 0;
@@ -98,7 +98,7 @@ static int launch_p4w_t(const P4Args& a, cudaStream_t st) {
     // its prologue) orders it after the previous kernel on the stream
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(g);
-    cfg.blockDim = dim3(S::NT);
+    cfg.blockDim = dim3(S::NT + G::NT_EXTRA);
     cfg.dynamicSmemBytes = G::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
