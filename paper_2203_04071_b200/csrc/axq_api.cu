@@ -907,7 +907,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
 static std::atomic<int> g_p4w_main_cw{28};        // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
 static std::atomic<int64_t> g_p4w_main_cw_max_k{1 << 30};   // ... for layers with K up to this
 static std::atomic<int> g_p4w_res_cw{20};         // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape (r2: 20 after the specialised epilogue)
-static std::atomic<int> g_p4w_tma_res{1};         // AXQ_P4W_TMA_RES: residual rows by TMA (RESBUF shapes)
+static std::atomic<int> g_p4w_tma_res{2};         // AXQ_P4W_TMA_RES: residual rows by TMA (RESBUF shapes), 2: + y stores
 static std::atomic<int> g_p4w_tma{2};             // AXQ_P4W_TMA: activation planes by TMA (0 off, 1 GEMM rows, 2 + im2col)
 static std::atomic<int> g_p4w_cw{0};              // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
 static std::atomic<int64_t> g_sk_full_waves{8};   // AXQ_SK_FULL_WAVES: P4W layers of fewer than this many waves of
@@ -987,21 +987,27 @@ static bool p4w_encode_tma(axq::P4Args& a) {
 // P4W residual layers: the epilogue's fp32 residual [M][N] (row stride ldr) as a 2D tensor map,
 // box 16 columns x 128 rows (one MMA slice of one column tile); used by the residual-layer
 // shapes that have room for the tile's rows in shared memory (lut_p4w.cuh Geo::RESBUF)
-static bool p4w_encode_res(axq::P4Args& a, const axq::EpiArgs& e) {
-    const axq::MMArgs& p = a.mm;
-    if (!g_p4w_tma_res.load() || a.transposed || !e.residual || p.M <= 0 || p.M >= ((int64_t)1 << 31) ||
-        p.N <= 0 || (e.ldr & 3) != 0 || e.ldr < p.N || (reinterpret_cast<uintptr_t>(e.residual) & 15) != 0)
+static bool p4w_encode_rows_f32(CUtensorMap* map, const float* base, int64_t M, int64_t N, int64_t ld) {
+    if (!base || M <= 0 || M >= ((int64_t)1 << 31) || N <= 0 || (ld & 3) != 0 || ld < N ||
+        (reinterpret_cast<uintptr_t>(base) & 15) != 0)
         return false;
     auto enc = tmap_encoder();
     if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.M};
-    cuuint64_t strides[1] = {(cuuint64_t)(e.ldr * 4)};
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
     cuuint32_t box[2] = {16u, 128u};
     cuuint32_t es[2] = {1u, 1u};
-    CUresult r = enc(&a.tmap_res, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(e.residual), dims, strides,
-                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool p4w_encode_res(axq::P4Args& a, const axq::EpiArgs& e) {
+    if (!g_p4w_tma_res.load() || a.transposed || !e.residual) return false;
+    if (!p4w_encode_rows_f32(&a.tmap_res, e.residual, a.mm.M, a.mm.N, e.ldr)) return false;
+    a.tma_y = (g_p4w_tma_res.load() >= 2 && e.y && !e.y_nchw &&
+               p4w_encode_rows_f32(&a.tmap_y, e.y, a.mm.M, a.mm.N, e.ldy)) ? 1 : 0;
+    return true;
 }
 
 // P4W implicit-im2col operand (a conv, any padding / stride, 16-channel planes): an im2col
@@ -1139,6 +1145,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
     else
         axq::p4_plan(a.mm.M, a.mm.N, wp->Kp, sm_count(), can_split, a.rpl, a.splits, a.stages_per_split);
     a.tma_a = variant != 3 ? 0 : p4w_encode_tma(a) ? 1 : (g_p4w_tma.load() >= 2 && p4w_encode_im2col(a)) ? 2 : 0;
+    a.tma_y = 0;
     a.tma_res = (variant == 3 && ep && ep->residual && p4w_encode_res(a, epi)) ? 1 : 0;
     auto launch = [&](const axq::P4Args& x) { return variant == 3 ? axq::launch_p4w(x, st) : axq::launch_p4(x, st); };
     int path = wp->e16 ? AXQ_PATH_P4W16 : variant == 3 ? AXQ_PATH_P4W : AXQ_PATH_P4;

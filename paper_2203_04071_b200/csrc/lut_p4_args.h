@@ -72,7 +72,10 @@ struct P4Args {
     alignas(64) CUtensorMap tmap_a;   // 2D u8 [M][K] (row stride lda), box 16 k x 128 rows,
                                       // out-of-range rows and k >= K read as zeros
     int tma_res;                // P4W residual layers: the epilogue's fp32 residual rows by TMA
-    alignas(64) CUtensorMap tmap_res; // 2D fp32 [M][N] (row stride ldr), box 16 cols x 128 rows
+    int tma_y;                  // ... and its fp32 y rows written back by TMA stores
+    alignas(64) CUtensorMap tmap_res; // 2D fp32 [M][N] (row stride ldr), box 16 cols x 128 rows,
+                                      // 64-byte swizzle (conflict-free row reads)
+    alignas(64) CUtensorMap tmap_y;   // 2D fp32 [M][N] (row stride ldy), same box and swizzle
 };
 
 }  // namespace axq

@@ -108,7 +108,7 @@ struct Geo {
     // residual layers whose shape leaves room: the tile's fp32 residual rows [BM][16] staged by
     // TMA (issued by consumer thread 0 as the tile's last stage starts), read from shared memory
     // by the epilogue
-    static constexpr int SMEM_RES = (SMEM_END + 127) / 128 * 128;
+    static constexpr int SMEM_RES = (SMEM_END + 1023) / 1024 * 1024;   // 64-byte swizzle atoms
     static constexpr bool RESBUF = RESX && SMEM_RES + BM * 64 <= 232448;
     static constexpr int SMEM_BYTES = RESBUF ? SMEM_RES + BM * 64 : SMEM_END;
     static constexpr int NT_EXTRA = 0;
@@ -630,16 +630,22 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT + p4w::Geo<HALF, KSX, CWX,
                              (kconst.mode == EPI_RES_RELU_Y_Q ? n0 + TN <= p.N
                                                                : p.ep.residual != nullptr && p4t_vec_ok(P, n0));
             float4 res[TN / 4];
-            if (G::RESBUF && P.tma_res) {
-                // the residual rows staged by the residual-copy warp
+            // residual rows staged by TMA: row tid, 16-byte chunk j at j ^ ((tid >> 1) & 3) (the
+            // tensor maps' 64-byte swizzle: conflict-free row reads); with P.tma_y the block's y
+            // goes back into the same rows and out through a TMA store per slice
+            const int swz = (tid >> 1) & 3;
+            float4* rrow = reinterpret_cast<float4*>(smem + G::SMEM_RES + tid * 64);
+            const bool tres = G::RESBUF && P.tma_res;
+            if (tres) {
                 mbar_wait(bar_rfull, rcount & 1u);
                 if (pre) {
-                    const float4* rs = reinterpret_cast<const float4*>(smem + G::SMEM_RES + tid * 64);
 #pragma unroll
-                    for (int j = 0; j < TN / 4; ++j) res[j] = rs[j];
+                    for (int j = 0; j < TN / 4; ++j) res[j] = rrow[j ^ swz];
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(bar_rfree);
+                if (!P.tma_y) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_rfree);
+                }
                 ++rcount;
             } else if (pre) {
                 const float4* rp = reinterpret_cast<const float4*>(p.ep.residual + m_row * p.ep.ldr + n0);
@@ -671,6 +677,29 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT + p4w::Geo<HALF, KSX, CWX,
 #pragma unroll
             for (int n = 0; n < 16; ++n) eacc[n] = (int)(ex[n] + es[n]) - corr;
             const int64_t m = m0 + tid;
+            // y by TMA store (residual-mode fast epilogue, whole column tile): each slice's 4 warps
+            // write their rows, then the slice issuer stores the 16 x 128 box; the residual
+            // buffer is released once every slice's store has read it
+            const bool ystore = tres && P.tma_y && kconst.mode == EPI_RES_RELU_Y_Q && n0 + TN <= p.N &&
+                                (splits == 1 || sk);
+            float4* ys = (ystore) ? rrow : nullptr;
+            auto ystore_done = [&](bool wrote) {
+                if (wrote) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    asm volatile("bar.sync %0, 128;\n" ::"r"(2 + slice) : "memory");
+                    if (issuer) {
+                        tma_store_2d(&P.tmap_y, (int)n0, (int)(m0 + slice * 128),
+                                     s_base + G::SMEM_RES + slice * 128 * 64);
+                        bulk_commit_wait_read();
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_rfree);
+            };
+            if (tres && P.tma_y && !ystore) {     // residual read, y not staged: release now
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_rfree);
+            }
             if (sk && !(s_b == 0 && s_e == nst_all)) {
                 // a stream-K piece: park it in this CTA's partial slot (0: the first piece of its
                 // range, 1: the last); the contributor completing the tile's stage count sums
@@ -709,13 +738,17 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT + p4w::Geo<HALF, KSX, CWX,
                             eacc[4 * j] += v.x; eacc[4 * j + 1] += v.y; eacc[4 * j + 2] += v.z; eacc[4 * j + 3] += v.w;
                         }
                     }
-                    if (m < p.M) p4t_store_row<RES>(P, m, n0, eacc, 1, kconst, pre ? res : nullptr);
+                    if (m < p.M) p4t_store_row<RES>(P, m, n0, eacc, 1, kconst, pre ? res : nullptr, ys, swz);
                 }
-            } else if (m < p.M) {
-                p4t_store_row<RES>(P, m, n0, eacc, splits, kconst, pre ? res : nullptr);
+                if (ystore && !fin) ystore_done(false);
+                else if (ystore) ystore_done(true);
+            } else {
+                if (m < p.M) p4t_store_row<RES>(P, m, n0, eacc, splits, kconst, pre ? res : nullptr, ys, swz);
+                if (ystore) ystore_done(true);
             }
         }
     }
+    if (G::RESBUF && P.tma_y) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // y stores done
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {

@@ -108,8 +108,11 @@ __device__ __forceinline__ EpiConst p4t_epi_const(const P4Args& P) {
 // the specialised row epilogue (kc.mode != EPI_GENERIC, whole 16-column tile, no split): the
 // generic path's arithmetic without its per-element flag tests; ReLU outputs requantize through
 // the sign-free reciprocal test (epi_quant_r_nn, bit-identical to epi_quant)
+// ys (residual mode only): the row's fp32 y goes to this shared-memory row instead (16-byte
+// chunk j at ys[j ^ swz], the 64-byte swizzle of the TMA store that writes it out)
 __device__ __forceinline__ void p4t_store_row_fast(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
-                                                   const EpiConst& kc, const float4* res_pre) {
+                                                   const EpiConst& kc, const float4* res_pre,
+                                                   float4* ys = nullptr, int swz = 0) {
     const EpiArgs& e = P.mm.ep;
     const float sc = kc.sc;
     if (kc.mode == EPI_Y) {
@@ -136,7 +139,10 @@ __device__ __forceinline__ void p4t_store_row_fast(const P4Args& P, int64_t m, i
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = v[u] > 0.f ? v[u] : 0.f;
-        if (res) yp[j] = make_float4(v[0], v[1], v[2], v[3]);
+        if (res) {
+            if (ys) ys[j ^ swz] = make_float4(v[0], v[1], v[2], v[3]);
+            else yp[j] = make_float4(v[0], v[1], v[2], v[3]);
+        }
         uint32_t w = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) w |= epi_quant_r_nn(v[u], kc.s_out, kc.r_out, kc.qm) << (8 * u);
@@ -158,7 +164,8 @@ __device__ __forceinline__ bool p4t_vec_ok(const P4Args& P, int64_t n0) {
 
 template <bool FASTQ = false>
 __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
-                                              int splits, const EpiConst& kc, const float4* res_pre);
+                                              int splits, const EpiConst& kc, const float4* res_pre,
+                                              float4* ys = nullptr, int swz = 0);
 
 __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
                                               int splits) {
@@ -170,12 +177,13 @@ __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_
 // instantiation only (elsewhere its registers cost more than the division it saves)
 template <bool FASTQ>
 __device__ __forceinline__ void p4t_store_row(const P4Args& P, int64_t m, int64_t n0, const int (&eacc)[16],
-                                              int splits, const EpiConst& kc, const float4* res_pre) {
+                                              int splits, const EpiConst& kc, const float4* res_pre,
+                                              float4* ys, int swz) {
     using namespace p4;
     const MMArgs& p = P.mm;
     const EpiArgs& e = p.ep;
     if (kc.mode != EPI_GENERIC && splits == 1 && n0 + TN <= p.N) {
-        p4t_store_row_fast(P, m, n0, eacc, kc, res_pre);
+        p4t_store_row_fast(P, m, n0, eacc, kc, res_pre, ys, swz);
         return;
     }
     if (P.transposed) {
