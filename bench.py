@@ -641,12 +641,18 @@ def count_launches(wl, stream, dist):
 def run_ours(args, rank, world, local_rank):
     import torch
 
-    dev = torch.device("cuda", local_rank)
+    # AXQ_BENCH_ONE_GPU=1 (path check only, not a measurement): every rank on cuda:0 over gloo,
+    # so the N > 1 code path can be exercised on a one-GPU box
+    one_gpu = os.environ.get("AXQ_BENCH_ONE_GPU") == "1"
+    dev = torch.device("cuda", 0 if one_gpu else local_rank)
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     timer = KernelTimer()
     global QUANTIZER, LUT_KIND
