@@ -46,7 +46,8 @@ def test_resnet_reduced_bit_exact(bits):
 
 def test_resnet50_config3_full_batch_sampled():
     """BJ configs[3] at full size: calibrate on images 0-7, forward all 256 images on one GPU
-    (the bench launch configuration); the oracle recomputes images 0 and 255."""
+    (the bench launch configuration); the oracle recomputes five images spread over the batch
+    (different row tiles, stream-K pieces and TMA boxes of every layer)."""
     lut = datagen.lut_randerr(8, 0, 2)                       # A15: c0's table
     net = _gpu_resnet(lut, 8, 3)
     orc = models.ResNetOracle(lut, 8, config=3)
@@ -57,7 +58,7 @@ def test_resnet50_config3_full_batch_sampled():
     for name, s in scales.items():
         assert net.s_act[net.slot[name]].item() == s, name
     y = net.forward(xd).cpu().numpy()
-    for i in (0, 255):
+    for i in (0, 37, 128, 201, 255):
         ref = orc.forward(x[i:i + 1], scales)
         assert _rel(y[i:i + 1], ref) <= 1e-6
         np.testing.assert_array_equal(y[i:i + 1], ref)
