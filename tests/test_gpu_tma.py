@@ -68,3 +68,31 @@ def test_tma_im2col_conv(ax, shape):
     want = ax.PATH_TMA if pointwise else ax.PATH_TMA_IM2COL
     assert fam == "p4w" and flags & want, (fam, hex(flags))
     np.testing.assert_array_equal(Y.cpu().numpy().transpose(0, 3, 1, 2), ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(3000, 64, 64), (20000, 48, 256), (641, 32, 128)])
+def test_tma_residual_rows_and_y_store(ax, M, N, K):
+    """The residual-layer shape's TMA residual staging and y stores (swizzled rows, one box per
+    128-row slice): ragged M (rows past M zero-filled on the way in, clipped on the way out),
+    a ragged column block when N % 16 != 0 is not used here (the generic path covers it), stream-K
+    tails at M = 20000.  Residual + ReLU + y + requantize against the oracle, bit-exact."""
+    T = datagen.lut_randerr(8, 0, 2)
+    A = np.random.default_rng(1100 + M).integers(0, 128, (M, K)).astype(np.int8)   # ReLU-input codes
+    W = datagen.random_int8(1200 + N, (N, K))
+    acc = oracle.lut_gemm(A, W, T, 8)
+    sa, sw = np.float32(0.0213), np.float32(0.0071)
+    R = datagen.normal(1300 + M, 3, (M, N), 1.0)
+    y_ref = (oracle.dequantize(acc, sa, sw) + R).astype(np.float32)
+    y_ref = np.where(y_ref > 0, y_ref, np.float32(0)).astype(np.float32)
+    so = np.float32(0.05)
+    q_ref = oracle.quantize(y_ref, so, 8)
+    wp = ax.WPack(ax.Lut(8, T), _t(W), a_nonneg=True)
+    y = torch.full((M, N), np.nan, device=DEV)
+    q = torch.zeros(M, N, dtype=torch.int8, device=DEV)
+    ws = torch.zeros(ax.axq_workspace_elems(M, N), dtype=torch.int32, device=DEV)
+    ep = ax.make_epilogue(_t(np.array([sa])), _t(np.array([sw])), workspace=ws, residual=_t(R), ldr=N,
+                          relu=True, y=y, ldy=N, q_out=q, ldq=N, d_scale_out=_t(np.array([so])), bits_out=8)
+    ax.axq_lut_gemm_wp(_t(A), wp, ep)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+    np.testing.assert_array_equal(q.cpu().numpy(), q_ref)
