@@ -64,7 +64,7 @@ constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots 
 #ifndef P4W_TCE
 #define P4W_TCE 0
 #endif
-#ifndef P4W_TMA_ON
+#ifndef P4W_TMA_ON        // A/B builds: 0 compiles the TMA activation loaders out (cp.async only)
 #define P4W_TMA_ON 1
 #endif
 #ifndef P4W_SMALL_FULL_STAGES
