@@ -907,6 +907,7 @@ axq_status axq_wpack_info(axq_wpack_t wp, int64_t* N, int64_t* K, int64_t* devic
 static std::atomic<int> g_p4w_main_cw{28};        // AXQ_P4W_MAIN_CW: consumer warps of the half-range 32-k shape
 static std::atomic<int64_t> g_p4w_main_cw_max_k{1 << 30};   // ... for layers with K up to this
 static std::atomic<int> g_p4w_res_cw{20};         // AXQ_P4W_RES_CW: consumer warps of the residual-layer shape (r2: 20 after the specialised epilogue)
+static std::atomic<int64_t> g_nbfast_mib{24};     // AXQ_NBFAST_MIB: column-block-fastest tile order up to this table size
 static std::atomic<int> g_p4w_tma_res{2};         // AXQ_P4W_TMA_RES: residual rows by TMA (RESBUF shapes), 2: + y stores
 static std::atomic<int> g_p4w_tma{2};             // AXQ_P4W_TMA: activation planes by TMA (0 off, 1 GEMM rows, 2 + im2col)
 static std::atomic<int> g_p4w_cw{0};              // AXQ_P4W_CW: 0 auto (16 for M <= 1024), 16 or 28 forced
@@ -932,6 +933,7 @@ static void p4w_read_env() {
         if (const char* v = std::getenv("AXQ_P4W_MAIN_CW_MAX_K")) g_p4w_main_cw_max_k = std::atoll(v);
         if (const char* v = std::getenv("AXQ_P4W_TMA")) g_p4w_tma = std::atoi(v);
         if (const char* v = std::getenv("AXQ_P4W_TMA_RES")) g_p4w_tma_res = std::atoi(v);
+        if (const char* v = std::getenv("AXQ_NBFAST_MIB")) g_nbfast_mib = std::atoll(v);
     });
 }
 
@@ -1170,7 +1172,7 @@ static axq_status p4_run(axq::P4Args& a, axq_wpack_t wp, const axq_epilogue* ep,
         }
     }
     // column-block-fastest order when all of the layer's tables fit comfortably in L2
-    a.nb_fast = (wp->bytes <= ((int64_t)24 << 20)) ? 1 : 0;
+    a.nb_fast = (wp->bytes <= (g_nbfast_mib.load() << 20)) ? 1 : 0;
     if (a.splits > 1) {
         int32_t* acc = ep ? ep->workspace : C;
         const int64_t ld = ep ? a.mm.N : ldc;
