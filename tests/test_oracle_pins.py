@@ -172,25 +172,28 @@ def test_conv_exact_lut_is_torch_conv(case):
     np.testing.assert_array_equal(Y, ref.astype(np.int64))
 
 
-@pytest.mark.parametrize("case", CONV_CASES[:4])
+@pytest.mark.parametrize("case", CONV_CASES)
 def test_conv_equals_explicit_im2col_gemm(case):
     """Random ACU: direct conv == materialised im2col (torch unfold, padding as a = 0)
     through the LUT-GEMM ("multiplying these 2 matrices would compute the same dot
-    product"; S:335)."""
+    product"); a grouped conv is that product per group (the group's input channels
+    against the group's filters), outputs concatenated in group order."""
     Nb, C, H, Wd, K, R, S, st, pd, g = case
-    if g != 1:
-        pytest.skip("im2col formulation here is groups=1")
     X = datagen.random_int8(300 + H, (Nb, C, H, Wd))
-    Wt = datagen.random_int8(400 + K, (K, C, R, S))
+    Wt = datagen.random_int8(400 + K, (K, C // g, R, S))
     T = datagen.random_lut(5, 8)
-    Y = oracle.lut_conv2d(X, Wt, T, 8, (st, st), (pd, pd))
-    cols = torch.nn.functional.unfold(torch.from_numpy(X.astype(np.float64)), (R, S),
-                                      padding=pd, stride=st)           # [N, C*R*S, L]
+    Y = oracle.lut_conv2d(X, Wt, T, 8, (st, st), (pd, pd), groups=g)
     Ho, Wo = Y.shape[2:]
-    Am = cols.permute(0, 2, 1).reshape(-1, C * R * S).numpy().astype(np.int8)
-    Wm = Wt.reshape(K, -1)
-    G = oracle.lut_gemm(Am, Wm, T, 8).reshape(Nb, Ho * Wo, K).transpose(0, 2, 1)
-    np.testing.assert_array_equal(Y.reshape(Nb, K, -1), G)
+    cg, kg = C // g, K // g
+    parts = []
+    for gi in range(g):
+        Xg = X[:, gi * cg:(gi + 1) * cg]
+        cols = torch.nn.functional.unfold(torch.from_numpy(Xg.astype(np.float64)), (R, S),
+                                          padding=pd, stride=st)           # [N, cg*R*S, L]
+        Am = cols.permute(0, 2, 1).reshape(-1, cg * R * S).numpy().astype(np.int8)
+        Wm = Wt[gi * kg:(gi + 1) * kg].reshape(kg, -1)
+        parts.append(oracle.lut_gemm(Am, Wm, T, 8).reshape(Nb, Ho * Wo, kg).transpose(0, 2, 1))
+    np.testing.assert_array_equal(Y.reshape(Nb, K, -1), np.concatenate(parts, axis=1))
 
 
 def test_conv_padding_probe():
