@@ -4,10 +4,15 @@
 //
 // Roles inside one persistent CTA (1024 threads, one CTA per SM):
 //  * 4 producer warps (warps CW..CW+3) stream the operands of each (tile, stage) item into a
-//    ring of STAGES shared-memory buffers: the activation rows by cp.async (implicit im2col,
-//    zero-fill = padding taps), completion signalled with cp.async.mbarrier.arrive; the packed
-//    E tables and weights by cp.async.bulk (mbarrier complete_tx).  A buffer is refilled once
-//    the consumer warps released it (empty barrier) and the MMA that read it completed.
+//    ring of STAGES shared-memory buffers: the activation planes (16 k x the tile's rows) by
+//    TMA -- a 2D tiled tensor map for GEMM rows, an im2col-mode map for convs (padding taps
+//    zero-filled by the copy engine) -- or, where neither applies, by cp.async (implicit
+//    im2col, ignore-src zero fill, signalled with cp.async.mbarrier.arrive); the packed E
+//    tables and weights by cp.async.bulk; all complete on the stage's full mbarrier.  A buffer
+//    is refilled once the consumer warps released it (empty barrier) and the MMA that read it
+//    completed.
+//  * Residual layers (640-row shape): the tile's fp32 residual rows are staged in shared memory
+//    by TMA (64-byte swizzle) and the block output y leaves through TMA stores per slice.
 //  * CW consumer warps (one tile row per lane) only wait for full buffers and do the lookups
 //    (4 per 32-bit LDS).  E8 tables: per quad and 4 k the 4 words are byte-transposed and each
 //    column summed by one dp4a into a 32-bit register sum kept for the whole tile.  E16
