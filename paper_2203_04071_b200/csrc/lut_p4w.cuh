@@ -72,6 +72,9 @@ constexpr int BM = CW * 32;                // 896 (host: stream-K partial slots 
 #ifndef P4W_TMA_ON        // A/B builds: 0 compiles the TMA activation loaders out (cp.async only)
 #define P4W_TMA_ON 1
 #endif
+#ifndef P4W_RES_LEAD      // residual rows requested this many stages before the tile's end
+#define P4W_RES_LEAD 2
+#endif
 #ifndef P4W_SMALL_FULL_STAGES
 #define P4W_SMALL_FULL_STAGES 3
 #endif
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(p4w::Shape<CWX>::NT + p4w::Geo<HALF, KSX, CWX,
                     }
                     __syncwarp();
                 }
-                if (G::RESBUF && P.tma_res && tid == 0 && st + 1 == s_e) {
+                if (G::RESBUF && P.tma_res && tid == 0 && st == (s_e - P4W_RES_LEAD > s_b ? s_e - P4W_RES_LEAD : s_b)) {
                     // the tile's residual rows: one 16-column x 128-row fp32 box per slice, once
                     // every warp has read the previous piece's (res_free)
                     if (rcount > 0) mbar_wait(bar_rfree, (rcount - 1) & 1u);
