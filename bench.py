@@ -56,9 +56,11 @@ def parse():
     ap.add_argument("--quantizer", default="max", choices=["max", "paper"],
                     help="resnet only: 'paper' = per-channel weights + 99.9%% histogram "
                          "activations (NEXT-1, P:93-95) instead of BASELINE's per-tensor max")
-    ap.add_argument("--lut", default="default", choices=["default", "err2000"],
+    ap.add_argument("--lut", default="default", choices=["default", "err2000", "err1e5"],
                     help="conv only: 'err2000' = an ACU with a +-2000 error (beyond int8 E: the "
-                         "packed int16-E kernel P4W16) instead of BJ configs[2]'s randerr table")
+                         "packed int16-E kernel P4W16) instead of BJ configs[2]'s randerr table; "
+                         "'err1e5' = a +-1e5-error ACU (beyond int16 E: the SM-resident int32 "
+                         "table in two halves, lut_mm_kernel<REPR_I32>)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
@@ -276,6 +278,8 @@ class ConvWL:
         c = datagen.config2()
         if LUT_KIND == "err2000":
             c.lut = datagen.lut_bigerr(8, 2000, 8, 1)
+        elif LUT_KIND == "err1e5":
+            c.lut = datagen.lut_bigerr(8, 100_000, 8, 1)
         self.c = c
         self.lut = Lut(8, c.lut)
         self.world, self.rank = world, rank
@@ -309,7 +313,9 @@ class ConvWL:
                                  "per-tensor max calibration (N > 1: all_reduce(MAX) of the shard "
                                  "amax, then the same scale as one GPU), randerr LUT, implicit "
                                  "im2col, fp32 NCHW output (N > 1: all-gathered)" +
-                                 (" -- with a +-2000-error ACU instead (--lut err2000)" if LUT_KIND == "err2000" else ""),
+                                 {"err2000": " -- with a +-2000-error ACU instead (--lut err2000)",
+                                  "err1e5": " -- with a +-1e5-error ACU instead (--lut err1e5, "
+                                            "int32 table)"}.get(LUT_KIND, ""),
                      "global_batch": total, "batch_per_gpu": Nb}
 
     def step(self, stream, dist):

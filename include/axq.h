@@ -48,7 +48,8 @@ typedef enum {
     AXQ_LUT_DELTA8 = 0, /* int8 E = LUT - a*w, shared-memory resident (64 KiB), exact part
                            added with dp4a */
     AXQ_LUT_I16 = 1,    /* int16 LUT values, shared-memory resident (128 KiB) */
-    AXQ_LUT_I32 = 2,    /* int32 values read through L1/L2 (correctness path) */
+    AXQ_LUT_I32 = 2,    /* int32 values, shared-memory resident in two 128 KiB halves split by
+                           the weight's high bit (each tile's K loop runs once per half) */
     AXQ_LUT_WIDE16 = 3, /* b = 9..12 (NEXT-2): int16 E = LUT - a*w, [uw][ua] in b-bit patterns,
                            read through L1/L2 (2^(2b+1) bytes: 32 MiB at b = 12) */
     AXQ_LUT_WIDE32 = 4  /* b = 9..12 with E beyond int16: int32 LUT values through L1/L2 */

@@ -12,7 +12,13 @@
 //    so a gather costs at most 2 wavefronts and 1 for the usual |a| < 64 codes.
 //  * Representation DELTA8 stores E = LUT - a*w as int8 (64 KiB); the exact part a*w is
 //    added with one dp4a per 4 lookups, so lookups stay 1 byte wide.  I16 stores LUT
-//    values directly (128 KiB); I32 reads a global int32 table (correctness path).
+//    values directly (128 KiB).  I32 (an ACU whose E = LUT - a*w does not fit int16 and
+//    whose values do not fit int16) keeps the 256 KiB int32 table SM-resident in two
+//    128 KiB halves split by the weight's high bit (rows uw < 128 | uw >= 128, P:147-149
+//    "populate the cache with the LUTs", north_star "int32 split across SM-resident
+//    halves"): each output tile runs its K loop once per half, a lookup contributing only
+//    in the pass whose half holds its row (idx >> 15), and consecutive tiles of a CTA start
+//    with the half already resident, so one tile costs one 128 KiB restage.
 //  * One lane owns R output rows (m) x TN output columns (n); the 32 lanes of a warp own
 //    32 consecutive rows.  The gather index (uw << 8) | ua is built by ONE byte-permute
 //    (PRMT) from a zero-padded activation word and the packed weight word.
@@ -68,6 +74,7 @@ struct MMArgs {
     EpiArgs ep;         // fused epilogue
 };
 
+// Grouped-conv kernels (gconv.cuh) keep the I32 table in global memory.
 template <int REPR>
 __device__ __forceinline__ int lut_fetch(const int8_t* lut_s, const int32_t* lut_g, uint32_t idx) {
     if constexpr (REPR == REPR_DELTA8) {
@@ -76,6 +83,22 @@ __device__ __forceinline__ int lut_fetch(const int8_t* lut_s, const int32_t* lut
         return (int)reinterpret_cast<const int16_t*>(lut_s)[idx];
     } else {
         return __ldg(lut_g + idx);
+    }
+}
+
+// I32: lut_s holds the resident half (rows uw in [128 half, 128 half + 127]); an index of
+// the other half reads an in-bounds word and contributes 0 (its own pass adds it).
+constexpr int I32_HALF_BYTES = 131072;
+
+template <int REPR>
+__device__ __forceinline__ int lut_fetch(const int8_t* lut_s, uint32_t idx, uint32_t half) {
+    if constexpr (REPR == REPR_DELTA8) {
+        return (int)lut_s[idx];
+    } else if constexpr (REPR == REPR_I16) {
+        return (int)reinterpret_cast<const int16_t*>(lut_s)[idx];
+    } else {
+        const int v = reinterpret_cast<const int32_t*>(lut_s)[idx & 0x7fffu];
+        return (idx >> 15) == half ? v : 0;
     }
 }
 
@@ -262,18 +285,17 @@ __device__ __forceinline__ uint4 load_w(const MMArgs& p, int64_t n, int64_t k0, 
 // only the columns (small M, e.g. the LSTM's
 // recurrent GEMM with M = 64): CTA tile = (32 R) rows x (WARPS TN) columns.
 template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, int WC = 1>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16 || WC > 1) ? 1 : (WARPS >= 8 ? 2 : 3))
+__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR != REPR_DELTA8 || WC > 1) ? 1 : (WARPS >= 8 ? 2 : 3))
 lut_mm_kernel(const MMArgs p) {
     constexpr int NT = WARPS * 32;
     constexpr int WR = WARPS / WC;                 // warps along the rows
     constexpr int BM = WR * 32 * R;
     constexpr int CTN = WC * TN;                   // columns per CTA tile
     extern __shared__ __align__(16) int8_t smem[];
-    // layout: [table (table_bytes, 0 for I32)] [W tiles: 2 x KC/4 x TN words]
+    // layout: [table (table_bytes; one 128 KiB half for I32)] [W tiles: 2 x KC/4 x TN words]
     int8_t* lut_s = smem;
-    const int tbytes = (REPR == REPR_I32) ? 0 : p.table_bytes;
+    const int tbytes = (REPR == REPR_I32) ? I32_HALF_BYTES : p.table_bytes;
     uint32_t* w_s = reinterpret_cast<uint32_t*>(smem + tbytes);
-    const int32_t* lut_g = reinterpret_cast<const int32_t*>(p.table);
 
     uint32_t* tap_s = w_s + 2 * (KC / 4) * CTN;  // LOAD_CONV_C4 tap table (K/4 entries)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -283,11 +305,13 @@ lut_mm_kernel(const MMArgs p) {
     // one bulk copy (TMA, mbarrier complete_tx): the whole 64 / 128 KiB in flight at once, so a
     // small problem (BJ configs[0]) pays one memory latency for it, not one per 16-byte round
     __shared__ __align__(8) uint64_t tbl_bar;
+    if (tid == 0) {
+        mbar_init(smem_u32(&tbl_bar), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     if constexpr (REPR != REPR_I32) {
         const uint32_t bar = smem_u32(&tbl_bar);
         if (tid == 0) {
-            mbar_init(bar, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             mbar_expect_tx(bar, (uint32_t)tbytes);
             bulk_g2s(smem_u32(lut_s), p.table, (uint32_t)tbytes, bar);
         }
@@ -314,6 +338,8 @@ lut_mm_kernel(const MMArgs p) {
         __syncthreads();                       // barrier initialised before anyone waits on it
         mbar_wait(smem_u32(&tbl_bar), 0u);
     }
+    int resident = -1;          // I32: the half in lut_s (-1: none yet)
+    uint32_t tbl_phase = 0;     // I32: parity of the next table-barrier completion
     const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + CTN - 1) / CTN;
     const int64_t n_split = (p.K + p.k_split - 1) / p.k_split;
     const int64_t n_work = m_tiles * n_tiles * (n_split > 0 ? n_split : 1);
@@ -339,6 +365,25 @@ lut_mm_kernel(const MMArgs p) {
 #pragma unroll
         for (int n = 0; n < TN; ++n) acc[r][n] = 0;
 
+    constexpr int NPASS = (REPR == REPR_I32) ? 2 : 1;
+    const int first_half = resident < 0 ? 0 : resident;
+    for (int pass = 0; pass < NPASS; ++pass) {
+    const uint32_t half = (uint32_t)(first_half ^ pass);
+    if constexpr (REPR == REPR_I32) {
+        if ((int)half != resident) {
+            __syncthreads();   // every warp is done reading the previous half
+            if (tid == 0) {
+                const uint32_t bar = smem_u32(&tbl_bar);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic reads -> async writes
+                mbar_expect_tx(bar, (uint32_t)I32_HALF_BYTES);
+                bulk_g2s(smem_u32(lut_s), static_cast<const int8_t*>(p.table) + (size_t)half * I32_HALF_BYTES,
+                         (uint32_t)I32_HALF_BYTES, bar);
+            }
+            mbar_wait(smem_u32(&tbl_bar), tbl_phase);
+            tbl_phase ^= 1u;
+            resident = (int)half;
+        }
+    }
     uint4 a_cur[R], a_nxt[R];
     uint4 w_nxt = make_uint4(0, 0, 0, 0);
     if (nchunks > 0) {
@@ -385,10 +430,10 @@ lut_mm_kernel(const MMArgs p) {
                         const uint32_t i1 = __byte_perm(alo[r], w4, 0x3352);
                         const uint32_t i2 = __byte_perm(ahi[r], w4, 0x1160);
                         const uint32_t i3 = __byte_perm(ahi[r], w4, 0x3372);
-                        const int e0 = lut_fetch<REPR>(lut_s, lut_g, i0);
-                        const int e1 = lut_fetch<REPR>(lut_s, lut_g, i1);
-                        const int e2 = lut_fetch<REPR>(lut_s, lut_g, i2);
-                        const int e3 = lut_fetch<REPR>(lut_s, lut_g, i3);
+                        const int e0 = lut_fetch<REPR>(lut_s, i0, half);
+                        const int e1 = lut_fetch<REPR>(lut_s, i1, half);
+                        const int e2 = lut_fetch<REPR>(lut_s, i2, half);
+                        const int e3 = lut_fetch<REPR>(lut_s, i3, half);
                         int s = acc[r][n4 * 4 + j];
                         if constexpr (REPR == REPR_DELTA8) s = __dp4a((int)a4[r], (int)w4, s);
                         acc[r][n4 * 4 + j] = s + e0 + e1 + e2 + e3;
@@ -409,6 +454,7 @@ lut_mm_kernel(const MMArgs p) {
         }
         __syncthreads();
     }
+    }   // pass
 
     // ---- remove storage-padding lookups (K tail of this split; padded channels) ----
     int64_t npad = (int64_t)nchunks * KC - (ke - kb);
