@@ -599,7 +599,10 @@ def qdq_split(wl, stream, flush):
             ax.axq_quantize_nchw_to_nhwc(wl.x, L.d_scale_a, 8, wl.qx, stream)
 
         def g():
-            ax.axq_lut_conv2d_wp(wl.d, wl.qx, L.wp, None, acc, stream)
+            if L.wp is not None:
+                ax.axq_lut_conv2d_wp(wl.d, wl.qx, L.wp, None, acc, stream)
+            else:        # int32 table (--lut err1e5): the resident-table kernel, raw int32 out
+                ax.axq_lut_conv2d(wl.d, wl.qx, L.qw, L.lut, acc, stream)
 
         def dq():
             ax.axq_dequantize_nhwc_to_nchw(acc, L.d_scale_a, L.d_scale_w, None, wl.y, stream)

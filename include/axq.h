@@ -48,8 +48,8 @@ typedef enum {
     AXQ_LUT_DELTA8 = 0, /* int8 E = LUT - a*w, shared-memory resident (64 KiB), exact part
                            added with dp4a */
     AXQ_LUT_I16 = 1,    /* int16 LUT values, shared-memory resident (128 KiB) */
-    AXQ_LUT_I32 = 2,    /* int32 values, shared-memory resident in two 128 KiB halves split by
-                           the weight's high bit (each tile's K loop runs once per half) */
+    AXQ_LUT_I32 = 2,    /* int32 values: gathered through L1 (default) or SM-resident as two
+                           128 KiB halves by the activation's high bit (axq_lut_set_i32_resident) */
     AXQ_LUT_WIDE16 = 3, /* b = 9..12 (NEXT-2): int16 E = LUT - a*w, [uw][ua] in b-bit patterns,
                            read through L1/L2 (2^(2b+1) bytes: 32 MiB at b = 12) */
     AXQ_LUT_WIDE32 = 4  /* b = 9..12 with E beyond int16: int32 LUT values through L1/L2 */
@@ -99,6 +99,17 @@ int axq_version(void);
 axq_status axq_lut_create(int bits, const int32_t* host_table, axq_lut_t* out);
 axq_status axq_lut_destroy(axq_lut_t lut);
 axq_status axq_lut_info(axq_lut_t lut, int* bits, int* repr, int32_t* tmin, int32_t* tmax);
+
+/*
+ * axq_lut_set_i32_resident: for an AXQ_LUT_I32 table, choose how the LUT kernel holds it
+ * (north_star "int32 split across SM-resident halves"):
+ * resident = 1 stages it in shared memory as two 128 KiB halves by the activation's high bit
+ * (a tile's second pass runs only when its codes need the other half); 0 (the default, or
+ * AXQ_I32_RESIDENT in the environment at the first table creation) gathers it through L1.
+ * Results are identical.  Not synchronised with launches in flight on the same table.
+ * Errors: AXQ_ERR_INVALID (null), AXQ_ERR_UNSUPPORTED (not an int32 table).
+ */
+axq_status axq_lut_set_i32_resident(axq_lut_t lut, int resident);
 
 /* ---------------------------------------------------------------------------------
  * Quantizer.  "real_value = A x quantized_value + B where A is the scale and B is the

@@ -20,7 +20,7 @@ REPR_NAMES = {0: "delta8", 1: "int16", 2: "int32", 3: "wide16", 4: "wide32"}
 
 EXPORTED = [
     "axq_last_cuda_error", "axq_status_string", "axq_version",
-    "axq_lut_create", "axq_lut_destroy", "axq_lut_info",
+    "axq_lut_create", "axq_lut_destroy", "axq_lut_info", "axq_lut_set_i32_resident",
     "axq_amax", "axq_scale", "axq_quantize", "axq_quantize_nchw_to_nhwc",
     "axq_lut_gemm", "axq_lut_gemm_dq",
     "axq_conv2d_out_hw", "axq_lut_conv2d", "axq_lut_conv2d_dq",
@@ -94,6 +94,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
                                 ctypes.POINTER(axq_epilogue), vp, vp], i32),
         "axq_lut_create": ([i32, vp, ctypes.POINTER(vp)], i32),
         "axq_lut_destroy": ([vp], i32),
+        "axq_lut_set_i32_resident": ([vp, i32], i32),
         "axq_lut_info": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32),
                           ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)], i32),
         "axq_amax": ([vp, i64, vp, vp], i32),
@@ -197,6 +198,10 @@ class Lut:
                                                    ctypes.byref(lo), ctypes.byref(hi)))
         self.repr = REPR_NAMES[r.value]
         self.tmin, self.tmax = lo.value, hi.value
+
+    def set_i32_resident(self, resident: bool) -> None:
+        """int32 tables: SM-resident halves (True) or the L1 gather (False); same results."""
+        _check("axq_lut_set_i32_resident", load().axq_lut_set_i32_resident(self.handle, int(resident)))
 
     def close(self):
         if self.handle is not None and self.handle.value:

@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaxq.so"
-SOURCES = [CSRC / "axq_api.cu", CSRC / "mm_delta8.cu", CSRC / "mm_i16.cu", CSRC / "mm_i32.cu", CSRC / "mm_p4.cu", CSRC / "mm_lstm.cu", CSRC / "mm_gconv.cu", CSRC / "mm_wide.cu", CSRC / "mm_ste.cu"]
+SOURCES = [CSRC / "axq_api.cu", CSRC / "mm_delta8.cu", CSRC / "mm_i16.cu", CSRC / "mm_i32.cu", CSRC / "mm_i32h.cu", CSRC / "mm_p4.cu", CSRC / "mm_lstm.cu", CSRC / "mm_gconv.cu", CSRC / "mm_wide.cu", CSRC / "mm_ste.cu"]
 DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "axq.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -48,6 +48,9 @@ struct axq_lut {
     int table_bytes;
     int16_t* d_e16;            // int16 E = LUT - a*w [uw8][ua8] when every E fits int16 and the
                                // table is not delta8 (feeds the P4W16 packer), else null
+    int32_t* d_i32h;           // AXQ_LUT_I32: the table as two 128 KiB halves by the activation's
+                               // high bit, [h][uw8][ua8 & 127] (lut_mm_kernel<REPR_I32H>), else null
+    int i32_resident;          // AXQ_LUT_I32: 1 -> the SM-resident halves kernel, 0 -> L1 gather
 };
 
 namespace {
@@ -99,12 +102,16 @@ using axq::Cfg;
 using axq::CFG_BIG;
 using axq::CFG_SMALL;
 
+// kernel representation beyond axq_lut_repr: the int32 table as SM-resident halves
+constexpr int KREPR_I32H = 16;
+
 axq_status launch_mm(int epi, int loader, int repr, const axq::MMArgs& p, const Cfg& c,
                      dim3 grid, cudaStream_t st) {
     int rc;
     switch (repr) {
         case AXQ_LUT_DELTA8: rc = axq::launch_mm_delta8(epi, loader, p, c, grid, st); break;
         case AXQ_LUT_I16: rc = axq::launch_mm_i16(epi, loader, p, c, grid, st); break;
+        case KREPR_I32H: rc = axq::launch_mm_i32h(epi, loader, p, c, grid, st); break;
         default: rc = axq::launch_mm_i32(epi, loader, p, c, grid, st); break;
     }
     if (rc != 0) return cuda_fail((cudaError_t)rc);
@@ -294,6 +301,8 @@ axq_status axq_lut_create(int bits, const int32_t* host_table, axq_lut_t* out) {
     L->bits = bits;
     L->repr = repr;
     L->d_e16 = nullptr;
+    L->d_i32h = nullptr;
+    L->i32_resident = 0;
     cudaGetDevice(&L->device);
     if (repr != AXQ_LUT_DELTA8) {
         // E16 copy for the packed int16-E kernel (P4W16): E = LUT - a*w within int16
@@ -331,8 +340,26 @@ axq_status axq_lut_create(int bits, const int32_t* host_table, axq_lut_t* out) {
         return cuda_fail(e);
     }
     e = cudaMemcpy(L->d_table, dev_tab.data(), L->table_bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && repr == AXQ_LUT_I32) {
+        // halves by the activation's high bit: entry [uw8][ua8] -> [ua8 >> 7][uw8][ua8 & 127]
+        std::vector<int32_t> h((size_t)65536);
+        const int32_t* t = reinterpret_cast<const int32_t*>(dev_tab.data());
+        for (int uw8 = 0; uw8 < 256; ++uw8)
+            for (int ua8 = 0; ua8 < 256; ++ua8)
+                h[((size_t)(ua8 >> 7) << 15) | ((size_t)uw8 << 7) | (size_t)(ua8 & 127)] =
+                    t[((size_t)uw8 << 8) | (size_t)ua8];
+        e = cudaMalloc(&L->d_i32h, 262144);
+        if (e == cudaSuccess) e = cudaMemcpy(L->d_i32h, h.data(), 262144, cudaMemcpyHostToDevice);
+        static const int resident_default = [] {
+            const char* v = std::getenv("AXQ_I32_RESIDENT");   // measurement switch
+            return v ? std::atoi(v) : 0;
+        }();
+        L->i32_resident = resident_default;
+    }
     if (e != cudaSuccess) {
         cudaFree(L->d_table);
+        if (L->d_i32h) cudaFree(L->d_i32h);
+        if (L->d_e16) cudaFree(L->d_e16);
         delete L;
         return cuda_fail(e);
     }
@@ -345,7 +372,15 @@ axq_status axq_lut_destroy(axq_lut_t lut) {
     cudaDeviceSynchronize();
     cudaFree(lut->d_table);
     if (lut->d_e16) cudaFree(lut->d_e16);
+    if (lut->d_i32h) cudaFree(lut->d_i32h);
     delete lut;
+    return AXQ_OK;
+}
+
+axq_status axq_lut_set_i32_resident(axq_lut_t lut, int resident) {
+    if (!lut) return AXQ_ERR_INVALID;
+    if (lut->repr != AXQ_LUT_I32) return AXQ_ERR_UNSUPPORTED;
+    lut->i32_resident = resident ? 1 : 0;
     return AXQ_OK;
 }
 
@@ -521,7 +556,12 @@ static axq_status launch_epilogue(int64_t M, int64_t N, const int32_t* acc, int6
 // Common driver: plan split-K, launch the fused or the split (atomic + epilogue) variant.
 static axq_status run_mm(axq::MMArgs& p, int loader, axq_lut_t lut, const axq::EpiArgs* epi,
                          int32_t* workspace, int32_t* C_raw, int64_t ldc, cudaStream_t st) {
-    Cfg c = pick_cfg(p.M, p.N, loader, lut->repr);
+    int krepr = lut->repr;
+    if (krepr == AXQ_LUT_I32 && lut->i32_resident && lut->d_i32h) {
+        krepr = KREPR_I32H;
+        p.table = lut->d_i32h;
+    }
+    Cfg c = pick_cfg(p.M, p.N, loader, krepr);
     const bool can_split = epi ? (workspace != nullptr) : true;
     p.k_split = pick_k_split(p.M, p.N, p.K, c, can_split);
     const int64_t splits = p.K > 0 ? (p.K + p.k_split - 1) / p.k_split : 1;
@@ -534,21 +574,21 @@ static axq_status run_mm(axq::MMArgs& p, int loader, axq_lut_t lut, const axq::E
         if (splits > 1) {
             cudaError_t e = cudaMemset2DAsync(C_raw, ldc * 4, 0, p.N * 4, p.M, st);
             if (e != cudaSuccess) return cuda_fail(e);
-            return launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, st);
+            return launch_mm(axq::EPI_RAW_ATOMIC, loader, krepr, p, c, grid, st);
         }
-        return launch_mm(axq::EPI_RAW, loader, lut->repr, p, c, grid, st);
+        return launch_mm(axq::EPI_RAW, loader, krepr, p, c, grid, st);
     }
     if (splits > 1) {
         p.C_out = workspace;
         p.ldc = p.N;
         cudaError_t e = cudaMemsetAsync(workspace, 0, (size_t)p.M * p.N * 4, st);
         if (e != cudaSuccess) return cuda_fail(e);
-        axq_status s = launch_mm(axq::EPI_RAW_ATOMIC, loader, lut->repr, p, c, grid, st);
+        axq_status s = launch_mm(axq::EPI_RAW_ATOMIC, loader, krepr, p, c, grid, st);
         if (s != AXQ_OK) return s;
         return launch_epilogue(p.M, p.N, workspace, p.N, *epi, st, workspace);
     }
     p.ep = *epi;
-    return launch_mm(axq::EPI_FUSED, loader, lut->repr, p, c, grid, st);
+    return launch_mm(axq::EPI_FUSED, loader, krepr, p, c, grid, st);
 }
 
 axq_status axq_lut_gemm(int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,

@@ -12,13 +12,14 @@
 //    so a gather costs at most 2 wavefronts and 1 for the usual |a| < 64 codes.
 //  * Representation DELTA8 stores E = LUT - a*w as int8 (64 KiB); the exact part a*w is
 //    added with one dp4a per 4 lookups, so lookups stay 1 byte wide.  I16 stores LUT
-//    values directly (128 KiB).  I32 (an ACU whose E = LUT - a*w does not fit int16 and
-//    whose values do not fit int16) keeps the 256 KiB int32 table SM-resident in two
-//    128 KiB halves split by the weight's high bit (rows uw < 128 | uw >= 128, P:147-149
-//    "populate the cache with the LUTs", north_star "int32 split across SM-resident
-//    halves"): each output tile runs its K loop once per half, a lookup contributing only
-//    in the pass whose half holds its row (idx >> 15), and consecutive tiles of a CTA start
-//    with the half already resident, so one tile costs one 128 KiB restage.
+//    values directly (128 KiB).  Tables whose values do not fit int16 (256 KiB of int32):
+//    I32 gathers through L1 (no shared-memory carve-out, 3 CTAs per SM: the L1 holds the
+//    touched rows); I32H keeps the table SM-resident in shared memory as two 128 KiB halves
+//    split by the activation's high bit ("populate the cache with the LUTs",
+//    north_star "int32 split across SM-resident halves" / "tiled by the a-operand's high
+//    bits"): a tile's K loop runs with the resident half, lookups of the other half adding
+//    0, and a second pass with the other half runs only if some code of the tile needs it
+//    (ReLU inputs: never, so the table is staged once per CTA).
 //  * One lane owns R output rows (m) x TN output columns (n); the 32 lanes of a warp own
 //    32 consecutive rows.  The gather index (uw << 8) | ua is built by ONE byte-permute
 //    (PRMT) from a zero-padded activation word and the packed weight word.
@@ -43,7 +44,7 @@ namespace axq {
 
 constexpr int KC = 16;
 
-enum { REPR_DELTA8 = 0, REPR_I16 = 1, REPR_I32 = 2 };
+enum { REPR_DELTA8 = 0, REPR_I16 = 1, REPR_I32 = 2, REPR_I32H = 3 };
 enum { EPI_RAW = 0, EPI_RAW_ATOMIC = 1, EPI_FUSED = 2 };
 enum { LOAD_GEMM = 0, LOAD_CONV = 1, LOAD_GEMM_BYTES = 2, LOAD_CONV_BYTES = 3, LOAD_CONV_C4 = 4,
        // quantize-on-load (SURVEY §8(b) axq_lut_gemm_f32a / axq_lut_conv2d_f32): the operand is
@@ -74,7 +75,7 @@ struct MMArgs {
     EpiArgs ep;         // fused epilogue
 };
 
-// Grouped-conv kernels (gconv.cuh) keep the I32 table in global memory.
+// Global-table form: I32 (through L1) and the grouped-conv kernels (gconv.cuh).
 template <int REPR>
 __device__ __forceinline__ int lut_fetch(const int8_t* lut_s, const int32_t* lut_g, uint32_t idx) {
     if constexpr (REPR == REPR_DELTA8) {
@@ -86,8 +87,9 @@ __device__ __forceinline__ int lut_fetch(const int8_t* lut_s, const int32_t* lut
     }
 }
 
-// I32: lut_s holds the resident half (rows uw in [128 half, 128 half + 127]); an index of
-// the other half reads an in-bounds word and contributes 0 (its own pass adds it).
+// I32H: lut_s holds half h = the entries with (ua >> 7) == h, laid out [uw][ua & 127]
+// (axq_lut_create's d_i32h); an index of the other half reads an in-bounds word and
+// contributes 0 (its own pass adds it).
 constexpr int I32_HALF_BYTES = 131072;
 
 template <int REPR>
@@ -97,8 +99,9 @@ __device__ __forceinline__ int lut_fetch(const int8_t* lut_s, uint32_t idx, uint
     } else if constexpr (REPR == REPR_I16) {
         return (int)reinterpret_cast<const int16_t*>(lut_s)[idx];
     } else {
-        const int v = reinterpret_cast<const int32_t*>(lut_s)[idx & 0x7fffu];
-        return (idx >> 15) == half ? v : 0;
+        const uint32_t j = ((idx >> 1) & 0x7f80u) | (idx & 0x7fu);
+        const int v = reinterpret_cast<const int32_t*>(lut_s)[j];
+        return ((idx >> 7) & 1u) == half ? v : 0;
     }
 }
 
@@ -285,17 +288,18 @@ __device__ __forceinline__ uint4 load_w(const MMArgs& p, int64_t n, int64_t k0, 
 // only the columns (small M, e.g. the LSTM's
 // recurrent GEMM with M = 64): CTA tile = (32 R) rows x (WARPS TN) columns.
 template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, int WC = 1>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR != REPR_DELTA8 || WC > 1) ? 1 : (WARPS >= 8 ? 2 : 3))
+__global__ void __launch_bounds__(WARPS * 32, (WARPS >= 16 || REPR == REPR_I16 || REPR == REPR_I32H || WC > 1) ? 1 : (WARPS >= 8 ? 2 : 3))
 lut_mm_kernel(const MMArgs p) {
     constexpr int NT = WARPS * 32;
     constexpr int WR = WARPS / WC;                 // warps along the rows
     constexpr int BM = WR * 32 * R;
     constexpr int CTN = WC * TN;                   // columns per CTA tile
     extern __shared__ __align__(16) int8_t smem[];
-    // layout: [table (table_bytes; one 128 KiB half for I32)] [W tiles: 2 x KC/4 x TN words]
+    // layout: [table (table_bytes; 0 for I32; one 128 KiB half for I32H)] [W tiles: 2 x KC/4 x TN words]
     int8_t* lut_s = smem;
-    const int tbytes = (REPR == REPR_I32) ? I32_HALF_BYTES : p.table_bytes;
+    const int tbytes = (REPR == REPR_I32) ? 0 : (REPR == REPR_I32H) ? I32_HALF_BYTES : p.table_bytes;
     uint32_t* w_s = reinterpret_cast<uint32_t*>(smem + tbytes);
+    const int32_t* lut_g = reinterpret_cast<const int32_t*>(p.table);
 
     uint32_t* tap_s = w_s + 2 * (KC / 4) * CTN;  // LOAD_CONV_C4 tap table (K/4 entries)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -309,7 +313,7 @@ lut_mm_kernel(const MMArgs p) {
         mbar_init(smem_u32(&tbl_bar), 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if constexpr (REPR != REPR_I32) {
+    if constexpr (REPR != REPR_I32 && REPR != REPR_I32H) {
         const uint32_t bar = smem_u32(&tbl_bar);
         if (tid == 0) {
             mbar_expect_tx(bar, (uint32_t)tbytes);
@@ -334,12 +338,12 @@ lut_mm_kernel(const MMArgs p) {
         qs = __ldg(p.qscale);
         qm = (float)((1 << (p.qbits - 1)) - 1);
     }
-    if constexpr (REPR != REPR_I32) {
+    if constexpr (REPR != REPR_I32 && REPR != REPR_I32H) {
         __syncthreads();                       // barrier initialised before anyone waits on it
         mbar_wait(smem_u32(&tbl_bar), 0u);
     }
-    int resident = -1;          // I32: the half in lut_s (-1: none yet)
-    uint32_t tbl_phase = 0;     // I32: parity of the next table-barrier completion
+    int resident = -1;          // I32H: the half in lut_s (-1: none yet)
+    uint32_t tbl_phase = 0;     // I32H: parity of the next table-barrier completion
     const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + CTN - 1) / CTN;
     const int64_t n_split = (p.K + p.k_split - 1) / p.k_split;
     const int64_t n_work = m_tiles * n_tiles * (n_split > 0 ? n_split : 1);
@@ -365,11 +369,17 @@ lut_mm_kernel(const MMArgs p) {
 #pragma unroll
         for (int n = 0; n < TN; ++n) acc[r][n] = 0;
 
-    constexpr int NPASS = (REPR == REPR_I32) ? 2 : 1;
+    constexpr int NPASS = (REPR == REPR_I32H) ? 2 : 1;
     const int first_half = resident < 0 ? 0 : resident;
+    uint32_t a_or = 0, a_nor = 0;   // I32H: OR of the tile's codes / of their complements
     for (int pass = 0; pass < NPASS; ++pass) {
     const uint32_t half = (uint32_t)(first_half ^ pass);
-    if constexpr (REPR == REPR_I32) {
+    if constexpr (REPR == REPR_I32H) {
+        if (pass == 1) {
+            // the other half is needed only if some code of the tile has its high bit
+            const uint32_t other = first_half == 0 ? a_or : a_nor;
+            if (!__syncthreads_or((other & 0x80808080u) != 0u)) break;
+        }
         if ((int)half != resident) {
             __syncthreads();   // every warp is done reading the previous half
             if (tid == 0) {
@@ -414,6 +424,9 @@ lut_mm_kernel(const MMArgs p) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 a4[r] = (kq == 0) ? a_cur[r].x : (kq == 1) ? a_cur[r].y : (kq == 2) ? a_cur[r].z : a_cur[r].w;
+                if constexpr (REPR == REPR_I32H) {
+                    if (pass == 0) { a_or |= a4[r]; a_nor |= ~a4[r]; }
+                }
                 alo[r] = __byte_perm(a4[r], 0u, 0x4140);  // [a0, 0, a1, 0]
                 ahi[r] = __byte_perm(a4[r], 0u, 0x4342);  // [a2, 0, a3, 0]
             }
@@ -430,10 +443,10 @@ lut_mm_kernel(const MMArgs p) {
                         const uint32_t i1 = __byte_perm(alo[r], w4, 0x3352);
                         const uint32_t i2 = __byte_perm(ahi[r], w4, 0x1160);
                         const uint32_t i3 = __byte_perm(ahi[r], w4, 0x3372);
-                        const int e0 = lut_fetch<REPR>(lut_s, i0, half);
-                        const int e1 = lut_fetch<REPR>(lut_s, i1, half);
-                        const int e2 = lut_fetch<REPR>(lut_s, i2, half);
-                        const int e3 = lut_fetch<REPR>(lut_s, i3, half);
+                        const int e0 = (REPR == REPR_I32 ? lut_fetch<REPR>(lut_s, lut_g, i0) : lut_fetch<REPR>(lut_s, i0, half));
+                        const int e1 = (REPR == REPR_I32 ? lut_fetch<REPR>(lut_s, lut_g, i1) : lut_fetch<REPR>(lut_s, i1, half));
+                        const int e2 = (REPR == REPR_I32 ? lut_fetch<REPR>(lut_s, lut_g, i2) : lut_fetch<REPR>(lut_s, i2, half));
+                        const int e3 = (REPR == REPR_I32 ? lut_fetch<REPR>(lut_s, lut_g, i3) : lut_fetch<REPR>(lut_s, i3, half));
                         int s = acc[r][n4 * 4 + j];
                         if constexpr (REPR == REPR_DELTA8) s = __dp4a((int)a4[r], (int)w4, s);
                         acc[r][n4 * 4 + j] = s + e0 + e1 + e2 + e3;

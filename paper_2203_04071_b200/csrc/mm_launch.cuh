@@ -8,7 +8,7 @@ namespace axq {
 template <int REPR, int TN, int R, int WARPS, int LOADER, int EPI, int WC = 1>
 int launch_one(const MMArgs& p, dim3 grid, cudaStream_t st) {
     auto kern = lut_mm_kernel<REPR, TN, R, WARPS, LOADER, EPI, WC>;
-    const int smem = (REPR == REPR_I32 ? I32_HALF_BYTES : p.table_bytes) + 2 * (KC / 4) * TN * WC * 4 +
+    const int smem = (REPR == REPR_I32 ? 0 : REPR == REPR_I32H ? I32_HALF_BYTES : p.table_bytes) + 2 * (KC / 4) * TN * WC * 4 +
                      (LOADER == LOAD_CONV_C4 ? 4 * (MAX_TAP_GROUPS + 4) : 0);
     static unsigned configured = 0;  // bit per device
     static int resident[32] = {0};   // CTAs per SM, per device

@@ -34,6 +34,7 @@ constexpr Cfg CFG_SQ{4, 1, 32, 2};
 int launch_mm_delta8(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
 int launch_mm_i16(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
 int launch_mm_i32(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
+int launch_mm_i32h(int epi, int loader, const MMArgs& p, const Cfg& c, dim3 grid, cudaStream_t st);
 
 // P4 kernel (lut_p4.cuh); declared here with an opaque argument struct.
 struct P4Args;

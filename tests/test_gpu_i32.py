@@ -1,12 +1,14 @@
-"""GPU parity of the SM-resident int32 table (lut_mm_kernel<REPR_I32>): an ACU whose error
-E = LUT - a*w does not fit int16, so neither the int8-E (P4W) nor the int16-E (P4W16) packed
-tables can hold it.  The 256 KiB int32 table is staged in shared memory as two 128 KiB halves
-split by the weight's high bit, each output tile runs its K loop once per half
-(north_star "int32 split across SM-resident halves").
+"""GPU parity of the int32 tables: an ACU whose error E = LUT - a*w does not fit int16, so
+neither the int8-E (P4W) nor the int16-E (P4W16) packed tables can hold it.  Both kernel forms
+run every case: the L1 gather (lut_mm_kernel<REPR_I32>) and the SM-resident halves
+(lut_mm_kernel<REPR_I32H>: the 256 KiB table as two 128 KiB shared-memory halves by the
+activation's high bit, a second pass only for tiles with codes of the other half; north_star
+"int32 split across SM-resident halves").
 
-Against the CPU oracle, bit-exact: ragged GEMM shapes (weights of both signs, so both halves
+Against the CPU oracle, bit-exact: ragged GEMM shapes (activations of both signs, so both halves
 contribute), tiles walked several per CTA (the resident half carries over between tiles),
-split-K, K-tail padding, low bitwidths, convolutions, and the fused dequant epilogue."""
+non-negative activations (one pass), split-K, K-tail padding, low bitwidths, convolutions, and
+the fused dequant epilogue."""
 import numpy as np
 import pytest
 import torch
@@ -18,6 +20,11 @@ pytestmark = pytest.mark.gpu
 
 DEV = "cuda"
 BIG = 100_000      # |E| up to 1e5: beyond int16
+
+
+@pytest.fixture(params=[False, True], ids=["l1", "resident"])
+def resident(request):
+    return request.param
 
 
 @pytest.fixture(scope="module")
@@ -35,9 +42,10 @@ def _table(bits, idx, err=BIG):
     return datagen.lut_bigerr(bits, err, 7, idx)
 
 
-def _gemm(ax, A, W, T, bits):
+def _gemm(ax, A, W, T, bits, resident):
     lut = ax.Lut(bits, T)
     assert lut.repr == "int32"
+    lut.set_i32_resident(resident)
     C = torch.empty(A.shape[0], W.shape[0], dtype=torch.int32, device=DEV)
     ax.axq_lut_gemm(_t(A), _t(W), lut, C)
     path = ax.axq_last_path()[0]
@@ -52,17 +60,17 @@ SHAPES = [(1, 1, 1), (7, 13, 5), (33, 5, 147), (129, 65, 300), (600, 40, 77),
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
-def test_i32_gemm_ragged(ax, M, N, K):
+def test_i32_gemm_ragged(ax, resident, M, N, K):
     A = datagen.random_int8(110 + M, (M, K))
     W = datagen.random_int8(120 + N, (N, K))
     T = _table(8, 1)
-    C, path = _gemm(ax, A, W, T, 8)
+    C, path = _gemm(ax, A, W, T, 8, resident)
     assert path.startswith("v1")
     np.testing.assert_array_equal(C, oracle.lut_gemm(A, W, T, 8))
 
 
-def test_i32_one_sign_of_weights(ax):
-    """All weights >= 0 (only half 0 holds their rows) and all < 0 (only half 1)."""
+def test_i32_one_sign_of_weights(ax, resident):
+    """All weights >= 0 and all < 0."""
     M, N, K = 300, 48, 96
     A = datagen.random_int8(131, (M, K))
     T = _table(8, 2)
@@ -70,29 +78,29 @@ def test_i32_one_sign_of_weights(ax):
         W = (np.abs(datagen.random_int8(132, (N, K)).astype(np.int64)) % 128).astype(np.int8)
         if sign < 0:
             W = (-W.astype(np.int64) - 1).astype(np.int8)
-        C, _ = _gemm(ax, A, W, T, 8)
+        C, _ = _gemm(ax, A, W, T, 8, resident)
         np.testing.assert_array_equal(C, oracle.lut_gemm(A, W, T, 8))
 
 
-def test_i32_extreme_corners(ax):
+def test_i32_extreme_corners(ax, resident):
     """Codes -128 / 127 and 0 only: the corner entries of both halves, K-tail padding."""
     M, N, K = 97, 17, 37
     vals = np.array([-128, 127, 0, -1], np.int8)
     A = vals[datagen.random_int8(141, (M, K)).astype(np.int64) & 3]
     W = vals[datagen.random_int8(142, (N, K)).astype(np.int64) & 3]
     T = _table(8, 3)
-    C, _ = _gemm(ax, A, W, T, 8)
+    C, _ = _gemm(ax, A, W, T, 8, resident)
     np.testing.assert_array_equal(C, oracle.lut_gemm(A, W, T, 8))
 
 
 @pytest.mark.parametrize("bits", [6, 7])
-def test_i32_low_bitwidths(ax, bits):
+def test_i32_low_bitwidths(ax, resident, bits):
     M, N, K = 200, 40, 129
     half = 1 << (bits - 1)
     A = (datagen.random_int8(150 + bits, (M, K)).astype(np.int64) % half).astype(np.int8)
     W = (datagen.random_int8(160 + bits, (N, K)).astype(np.int64) % half - half // 2).astype(np.int8)
     T = _table(bits, 4 + bits)
-    C, _ = _gemm(ax, A, W, T, bits)
+    C, _ = _gemm(ax, A, W, T, bits, resident)
     np.testing.assert_array_equal(C, oracle.lut_gemm(A, W, T, bits))
 
 
@@ -105,7 +113,7 @@ CONV_SHAPES = [
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES)
-def test_i32_conv(ax, shape):
+def test_i32_conv(ax, resident, shape):
     Nb, C, H, Wd, K, R, S, st, pd = shape
     X = datagen.random_int8(170 + C, (Nb, C, H, Wd))
     Wt = datagen.random_int8(180 + K, (K, C, R, S))
@@ -113,6 +121,7 @@ def test_i32_conv(ax, shape):
     ref = oracle.lut_conv2d(X, Wt, T, 8, (st, st), (pd, pd))
     lut = ax.Lut(8, T)
     assert lut.repr == "int32"
+    lut.set_i32_resident(resident)
     d = ax.conv_desc(Nb, H, Wd, C, K, R, S, (st, st), (pd, pd))
     Ho, Wo = ax.axq_conv2d_out_hw(d)
     Y = torch.empty(Nb, Ho, Wo, K, dtype=torch.int32, device=DEV)
@@ -122,7 +131,7 @@ def test_i32_conv(ax, shape):
     lut.close()
 
 
-def test_i32_fused_linear(ax):
+def test_i32_fused_linear(ax, resident):
     """quantize -> LUT-GEMM (int32 table) -> dequant + bias, against the oracle's layer."""
     from paper_2203_04071_b200.layers import ApproxLinear
     c1 = datagen.config1()
@@ -130,6 +139,31 @@ def test_i32_fused_linear(ax):
     T = _table(8, 30, err=40_000)
     lut = ax.Lut(8, T)
     assert lut.repr == "int32"
+    lut.set_i32_resident(resident)
     y = ApproxLinear(_t(W), _t(b), lut)(_t(x))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(y.cpu().numpy(), oracle.linear(x, W, b, T, 8)[0])
+
+
+@pytest.mark.parametrize("sign", ["nonneg", "neg", "mixed_rows"])
+def test_i32_activation_halves(ax, resident, sign):
+    """Activations all >= 0 (half 0 only: one pass), all < 0 (half 1 only), and only a few rows
+    with negative codes (the second pass runs for their tiles alone)."""
+    M, N, K = 3000, 40, 150
+    A = (np.abs(datagen.random_int8(191, (M, K)).astype(np.int64)) % 128).astype(np.int64)
+    if sign == "neg":
+        A = -A - 1
+    elif sign == "mixed_rows":
+        A[::997] = -A[::997] - 1
+    A = A.astype(np.int8)
+    W = datagen.random_int8(192, (N, K))
+    T = _table(8, 40)
+    C, _ = _gemm(ax, A, W, T, 8, resident)
+    np.testing.assert_array_equal(C, oracle.lut_gemm(A, W, T, 8))
+
+
+def test_i32_mode_switch_is_int32_only(ax):
+    lut = ax.Lut(8, datagen.lut_randerr(8, 0, 2))
+    with pytest.raises(ax.AxqError):
+        lut.set_i32_resident(True)
+    lut.close()
